@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""Bench: sparse-FFN decode tokens/s on a BASELINE.json shape (default configs[1]:
+ProSparse-Llama2-7B FFN stack, 32 layers d=4096 d_ff=11008, batch 1).
+
+One step = one decode token through all L sparse-FFN layers (sequential
+pipeline, ffn_exec.hpp:183-218), executed by ONE persistent cooperative launch
+of the sm_100a executor (sg_ffn_forward_layers). Inputs/weights are resident in
+HBM; the L layers touch ~2.3 GB per step (>> 126 MB L2), so every step streams
+its bytes from HBM (no L2 flush needed; stated in `config`).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 7b|mistral|13b|1layer]
+  python bench.py --impl reference ...   # the reference CPU path (oracle/_ref)
+
+N>1 (torchrun): the FFN intermediate dimension is sharded over ranks;
+each layer ends with an NCCL all-reduce of the d-sized output.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def touched_bytes(d, D, r, p, v):
+    """algorithmic bytes of one layer for one token."""
+    return 2 * r * d + 2 * D * r + 4 * D + 2 * d * p + 2 * d * v + 2 * d * v
+
+
+def dense_bytes(d, D):
+    return 3 * 2 * d * D
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device=0, period_ms=50):
+        self.rows = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", str(period_ms)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        self.t.join(1)
+        rows = [r for r in self.rows if len(r) >= 6]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's own executor headers (oracle/_ref) on host cores
+# ---------------------------------------------------------------------------
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    import oracle as O
+    from paper_2603_14110_b200 import bf16_to_f64
+    from paper_2603_14110_b200.model import CONFIGS, build_host_layer
+
+    cfg = CONFIGS[args.config]
+    d, D, L = cfg["d"], cfg["D"], cfg["L"]
+    kind = "reference" if O.ref_available() else "port"
+    h = build_host_layer(d, D, cfg["act"], seed=0, rank=args.rank, sparsity=args.sparsity)
+    gate = bf16_to_f64(h.gate)
+    up = bf16_to_f64(h.up)
+    down = np.ascontiguousarray(bf16_to_f64(h.down_t).T)  # reference layout d x D
+    A, B = bf16_to_f64(h.A), bf16_to_f64(h.B)
+    bias = h.bias.astype(np.float32).astype(np.float64)
+    if kind == "reference":
+        ref = O.RefLayer(gate, up, down, A, B, bias, activation=cfg["act"])
+        cores = int(O.ref().sgref_thread_budget())
+    else:
+        ref = None
+        cores = 1
+    ntok = max(1, min(cores, h.xs.shape[1]))
+    xs = np.ascontiguousarray(h.xs[:, :ntok].T)
+
+    def one_step():
+        if ref is not None:
+            _, st, el = ref.run(xs, pipeline=2)
+        else:
+            t0 = time.perf_counter()
+            for t in range(ntok):
+                O.sparse_ffn(gate, up, down, A, B, bias, xs[t])
+            el = time.perf_counter() - t0
+        return el
+
+    t_est = one_step()  # warm-up and cost estimate
+    budget = 120.0
+    k = max(1, min(args.steps, int(budget / max(t_est, 1e-6))))
+    for _ in range(max(0, min(args.warmup, 1) - 1)):
+        one_step()
+    tot = sum(one_step() for _ in range(k))
+    per_token_layer = tot / (k * ntok)        # seconds of one token through one layer (amortised)
+    tok_s = 1.0 / (per_token_layer * L)       # decode tokens/s through the L-layer stack
+    line = {
+        "impl": "reference", "metric": "sparse-FFN decode tokens/s", "value": tok_s,
+        "unit": "tokens/s", "n_gpus": 0, "steps": k, "warmup": min(args.warmup, 1),
+        "ms_per_step": 1000.0 / tok_s, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg['model']}: {L} layers d={d} d_ff={D} r={args.rank} "
+                               f"s={args.sparsity} batch 1", "layers": L, "hidden": d, "inter": D},
+        "per_layer_us": per_token_layer * 1e6,
+        "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": kind,
+                         "sample": f"{k} steps x {ntok} eval tokens through layer 0 of {L} "
+                                   f"(reference sparse_ffn_sequential, f64, per-call validation, "
+                                   f"parallel_for over tokens); tokens/s = 1/(t_token_layer*{L})"},
+        "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline_for(cfg, host_layer0, args):
+    """Rank-0 bounded sample of the reference CPU path on layer 0 (see run_reference)."""
+    import oracle as O
+    from paper_2603_14110_b200 import bf16_to_f64
+    d, D, L = cfg["d"], cfg["D"], cfg["L"]
+    if not O.ref_available():
+        kind, cores = "port", 1
+    else:
+        kind, cores = "reference", int(O.ref().sgref_thread_budget())
+    h = host_layer0
+    gate, up = bf16_to_f64(h.gate), bf16_to_f64(h.up)
+    down = np.ascontiguousarray(bf16_to_f64(h.down_t).T)
+    A, B = bf16_to_f64(h.A), bf16_to_f64(h.B)
+    bias = h.bias.astype(np.float32).astype(np.float64)
+    ntok = max(1, min(cores, h.xs.shape[1]))
+    xs = np.ascontiguousarray(h.xs[:, :ntok].T)
+    if kind == "reference":
+        ref = O.RefLayer(gate, up, down, A, B, bias, activation=cfg["act"])
+        ref.run(xs[:1], 2)
+        tot, reps = 0.0, 0
+        while tot < 10.0 and reps < 8:
+            _, _, el = ref.run(xs, 2)
+            tot += el
+            reps += 1
+    else:
+        t0 = time.perf_counter()
+        reps = 1
+        for t in range(ntok):
+            O.sparse_ffn(gate, up, down, A, B, bias, xs[t])
+        tot = time.perf_counter() - t0
+    per = tot / (reps * ntok)
+    return {"value": 1.0 / (per * L), "unit": "tokens/s", "cores": cores, "kind": kind,
+            "sample": f"{reps} x {ntok} eval tokens through layer 0 of {L} (reference "
+                      f"sparse_ffn_sequential, f64 incl. per-call validation, parallel_for over "
+                      f"tokens); tokens/s = 1/(t_token_layer*{L})",
+            "per_layer_us": per * 1e6}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="7b")
+    ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--rank", type=int, default=256)
+    ap.add_argument("--sparsity", type=float, default=0.5)
+    ap.add_argument("--mode", default="stack", choices=["stack", "per-layer"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import ctypes as C
+
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2603_14110_b200 import _capi as capi
+    from paper_2603_14110_b200.ffn_exec import Context, Pipeline, check
+    from paper_2603_14110_b200.model import CONFIGS, build_host_model, upload
+
+    t0 = time.time()
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(max(1, (os.cpu_count() or 8) // 8))
+    except Exception:
+        pass
+    cfg, host = build_host_model(args.config, args.layers, rank=args.rank,
+                                 sparsity=args.sparsity, workers=8)
+    d, D, L = cfg["d"], cfg["D"], len(host)
+    log(f"host model built in {time.time() - t0:.1f}s")
+    layers = [upload(h, d, D, cfg["act"], args.rank, device=local, shard_index=rank,
+                     shard_count=world) for h in host]
+    Dl = layers[0].local_inter
+    ctx = Context(local, d, Dl, args.rank)
+    lib = capi.lib()
+    arr = (C.c_void_p * L)(*[l.handle.value for l in layers])
+    xs = torch.tensor(np.stack([h.x for h in host]), dtype=torch.float32, device="cuda")
+    ys = torch.zeros_like(xs)
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    def step_stack(pipe=Pipeline.Sequential):
+        check(lib.sg_ffn_forward_layers(ctx.handle, arr, L, int(pipe), C.c_void_p(xs.data_ptr()),
+                                        C.c_void_p(ys.data_ptr()), 0, C.c_void_p(sh)))
+
+    def step_layers(pipe=Pipeline.Sequential):
+        for l in range(L):
+            check(lib.sg_ffn_forward_device(ctx.handle, layers[l].handle, int(pipe),
+                                            C.c_void_p(xs[l].data_ptr()),
+                                            C.c_void_p(ys[l].data_ptr()), C.c_void_p(sh)))
+            if world > 1:
+                torch.distributed.all_reduce(ys[l])
+
+    step = step_stack if (args.mode == "stack" and world == 1) else step_layers
+    launches_per_step = 1 if step is step_stack else L
+
+    def timed(fn, K, W, sample_clocks=False):
+        for _ in range(W):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        sampler = ClockSampler(local) if sample_clocks else None
+        if sampler:
+            time.sleep(0.15)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(K):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / K
+        clocks = sampler.stop() if sampler else None
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, clocks
+
+    ms, clocks = timed(step, args.steps, args.warmup, sample_clocks=True)
+
+    # per-layer stats (p, v) of the tokens just timed (deterministic per layer)
+    stats = (capi.sg_exec_stats * L)()
+    if step is step_stack:
+        check(lib.sg_ctx_read_stack_stats(ctx.handle, C.c_void_p(sh), L, stats))
+    else:
+        for l in range(L):
+            layers[l].forward_device(xs[l].data_ptr(), ys[l].data_ptr(), Pipeline.Sequential,
+                                     ctx, sh)
+            s1 = capi.sg_exec_stats()
+            check(lib.sg_ctx_read_stats(ctx.handle, C.c_void_p(sh), C.byref(s1)))
+            stats[l] = s1
+    ps = [int(s.predicted_active) for s in stats]
+    vs = [int(s.revalidated) for s in stats]
+    alg_bytes = sum(touched_bytes(d, Dl, args.rank, p, v) for p, v in zip(ps, vs))
+    hbm, hbm_kind = peaks()
+    per_launch_ms = ms / launches_per_step
+    achieved = alg_bytes / launches_per_step / (per_launch_ms * 1e-3) / 1e9
+
+    # e2e through the C ABI host entry: pinned x in, y out, synchronised per step
+    xh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
+    xh.copy_(xs.cpu())
+    yh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
+
+    def step_e2e():
+        check(lib.sg_ffn_forward_layers_host(ctx.handle, arr, L, int(Pipeline.Sequential),
+                                             C.c_void_p(xh.data_ptr()), C.c_void_p(yh.data_ptr()),
+                                             0, None, C.c_void_p(sh)))
+
+    e2e = None
+    if world == 1:
+        ke = max(10, min(args.steps, 500))
+        ms_e2e, _ = timed(step_e2e, ke, 3)
+        e2e = {"value": 1000.0 / ms_e2e, "unit": "tokens/s", "h2d_bytes_per_step": L * d * 4,
+               "d2h_bytes_per_step": L * d * 4, "ms_per_step": ms_e2e, "steps": ke}
+
+    dense = None
+    if not args.no_dense:
+        ms_dense, _ = timed(lambda: step(Pipeline.Dense) if step is step_stack else
+                            step_layers(Pipeline.Dense), max(10, args.steps // 4), 3)
+        dense = {"ms_per_step": ms_dense, "tokens_per_s": 1000.0 / ms_dense,
+                 "per_layer_us": ms_dense * 1000.0 / L,
+                 "achieved_gbs": dense_bytes(d, Dl) * L / (ms_dense * 1e-3) / 1e9,
+                 "sparse_speedup": ms_dense / ms}
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                tj = json.load(f)
+            traffic = tj.get(args.config)
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_for(cfg, host[0], args)
+        except Exception as e:  # report, never fake
+            cpu = {"value": None, "error": str(e)[:200]}
+
+    if rank == 0:
+        tok_s = 1000.0 / ms
+        line = {
+            "metric": "sparse-FFN decode tokens/s", "value": tok_s, "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{cfg['model']}: {L} layers d={d} d_ff={D} r={args.rank} "
+                                   f"s={args.sparsity} natural sparsity 0.9, batch 1, sequential "
+                                   f"pipeline", "layers": L, "hidden": d, "inter": D,
+                       "rank": args.rank, "predicted_sparsity_target": args.sparsity,
+                       "batch": 1, "parallelism": f"d_ff-shard{world}" if world > 1 else "none",
+                       "l2": "no flush: each step streams %.2f GB of distinct layers (> 126 MB L2)"
+                             % (alg_bytes / 1e9),
+                       "predictor": "naive-mode randomized rank-r SVD + greedy calibration (eta 8)",
+                       "mode": "stack (one persistent launch per step)" if step is step_stack
+                               else "per-layer launches"},
+            "per_layer_us": ms * 1000.0 / L,
+            "p_mean": float(np.mean(ps)), "v_mean": float(np.mean(vs)),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "peak_kind": hbm_kind,
+                         "frac_of_8000_nominal": achieved / 8000.0,
+                         "traffic": traffic,
+                         "bytes_per_launch": alg_bytes / launches_per_step,
+                         "kernel": "ffn_kernel<2> (sequential executor)"},
+            "dense": dense,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * launches_per_step,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

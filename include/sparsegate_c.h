@@ -1,0 +1,210 @@
+/*
+ * sparsegate-b200 — C ABI of the B200-native sparse gated-FFN decode executor.
+ *
+ * Drop-in boundary for the reference executor API
+ *   /root/reference/proj/include/sparsegate/ffn_exec.hpp (namespace sparsegate):
+ *     dense_ffn              ffn_exec.hpp:103-122   -> sg_ffn_forward(..., SG_PIPELINE_DENSE, ...)
+ *     predict_mask           ffn_exec.hpp:125-146   -> sg_predict_mask
+ *     sparse_ffn_parallel    ffn_exec.hpp:149-178   -> sg_ffn_forward(..., SG_PIPELINE_PARALLEL, ...)
+ *     sparse_ffn_sequential  ffn_exec.hpp:183-218   -> sg_ffn_forward(..., SG_PIPELINE_SEQUENTIAL, ...)
+ *     op_count_model         ffn_exec.hpp:229-244   -> sg_op_count_model (pure host)
+ *   with the data contract of types.hpp:21-105 (FfnWeights, Predictor, validate) and
+ *   the error taxonomy of common.hpp:20-37 (IoError / DataError / PropertyViolation)
+ *   mapped onto sg_status (CLI exit-code convention, tools/sparsegate_main.cpp:5).
+ *
+ * The reference functions are stateless and take f64 Eigen objects; a GPU
+ * executor needs resident weights, so the ABI splits each call into
+ *   sg_layer_create  (upload + validate ONCE; types.hpp:31-51 / :82-105 run here,
+ *                     not on every call as ffn_exec.hpp:57 / :126 do)
+ *   sg_ctx_create    (per-stream workspace; one per concurrently used stream/thread,
+ *                     which gives the reference's reentrancy)
+ *   sg_ffn_forward*  (the executor call).
+ * Plain pointers and sizes only; cudaStream_t is passed as void*.
+ * All functions are thread-safe for distinct sg_ctx objects.
+ */
+#ifndef SPARSEGATE_C_H_
+#define SPARSEGATE_C_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum sg_status {
+  SG_OK = 0,
+  SG_ERR_USAGE = 1,    /* bad arguments (CLI exit 1)                               */
+  SG_ERR_DATA = 2,     /* DataError: shapes, non-finite x / weights (common.hpp:30) */
+  SG_ERR_PROPERTY = 3, /* PropertyViolation (common.hpp:35)                        */
+  SG_ERR_IO = 4,       /* IoError (common.hpp:25)                                  */
+  SG_ERR_CUDA = 5,     /* CUDA runtime failure (no reference counterpart)          */
+  SG_ERR_NCCL = 6      /* NCCL failure (no reference counterpart)                  */
+} sg_status;
+
+typedef enum sg_activation { SG_REGLU = 0, SG_DRELU = 1 } sg_activation; /* types.hpp:12 */
+
+/* Same order as sparsegate::Pipeline (ffn_exec.hpp:32). */
+typedef enum sg_pipeline {
+  SG_PIPELINE_DENSE = 0,
+  SG_PIPELINE_PARALLEL = 1,
+  SG_PIPELINE_SEQUENTIAL = 2
+} sg_pipeline;
+
+typedef enum sg_dtype { SG_F64 = 0, SG_F32 = 1, SG_BF16 = 2 } sg_dtype;
+
+/* sparsegate::ExecStats (ffn_exec.hpp:35-40), computed exactly as ffn_exec.hpp:120,
+ * :173-180, :209-216 from the device-side counts; plus the counts themselves. */
+typedef struct sg_exec_stats {
+  double predicted_sparsity;
+  double realized_sparsity;
+  int64_t multiplies;
+  int32_t pipeline;
+  int32_t pad_;
+  int64_t predicted_active; /* |P| */
+  int64_t revalidated;      /* |V| (gate survivors) */
+} sg_exec_stats;
+
+/* One FFN layer (or one shard of it) plus its predictor, in the REFERENCE layouts:
+ *   gate, up : inter x hidden  row-major   (types.hpp:19-24)
+ *   down     : hidden x inter  row-major   (transposed to neuron-major on upload)
+ *   pred_A   : inter x rank    row-major   (types.hpp:72-76)
+ *   pred_B   : rank x hidden   row-major
+ *   bias     : inter, f64 or f32 (+inf allowed, types.hpp:99-101)
+ * Host arrays; dtype `weight_dtype` for gate/up/down/A/B (f64/f32 are rounded
+ * f64->f32->bf16 RNE; bf16 arrays are uint16 bit patterns), `bias_dtype` for bias.
+ * pred_A/pred_B/bias may all be NULL for a dense-only layer (rank ignored);
+ * gate/up/down may all be NULL for a predictor-only layer (sg_predict_mask only).
+ *
+ * Sharding: the layer keeps neurons {shard_index + k*shard_count}
+ * when shard_interleave != 0, else the contiguous block shard_index of
+ * shard_count near-equal blocks. The arrays always describe the FULL layer. */
+typedef struct sg_layer_desc {
+  int64_t hidden;
+  int64_t inter;
+  int64_t rank;
+  int32_t activation;   /* sg_activation */
+  int32_t weight_dtype; /* sg_dtype */
+  int32_t bias_dtype;   /* sg_dtype (SG_F64 or SG_F32) */
+  int32_t device;       /* CUDA device ordinal */
+  const void* gate;
+  const void* up;
+  const void* down;
+  const void* pred_A;
+  const void* pred_B;
+  const void* bias;
+  int32_t shard_index;
+  int32_t shard_count; /* 0 or 1 = unsharded */
+  int32_t shard_interleave;
+  int32_t down_neuron_major; /* 1: `down` is already inter x hidden (neuron-major) */
+} sg_layer_desc;
+
+typedef struct sg_layer sg_layer;
+typedef struct sg_ctx sg_ctx;
+
+/* Last error message of the calling thread ("" if none). */
+const char* sg_last_error(void);
+/* Library version string. */
+const char* sg_version(void);
+
+sg_status sg_layer_create(const sg_layer_desc* desc, sg_layer** out);
+sg_status sg_layer_destroy(sg_layer* layer);
+/* Local (shard) neuron count, and the global index of local neuron k. */
+int64_t sg_layer_local_inter(const sg_layer* layer);
+int64_t sg_layer_global_index(const sg_layer* layer, int64_t local);
+/* Device bytes held by the layer's resident weights. */
+int64_t sg_layer_device_bytes(const sg_layer* layer);
+
+/* Workspace for one stream. max_hidden/max_inter/max_rank bound the layers it
+ * will run; device = CUDA ordinal. */
+sg_status sg_ctx_create(int32_t device, int64_t max_hidden, int64_t max_inter, int64_t max_rank,
+                        sg_ctx** out);
+sg_status sg_ctx_destroy(sg_ctx* ctx);
+
+/* Executor, device buffers, asynchronous on `stream` (cudaStream_t; NULL = legacy
+ * default). x: fp32[hidden] (device). y: fp32[hidden] (device) receives this
+ * layer's (shard's) output. No host synchronisation; stats and index sets stay in
+ * the ctx until sg_ctx_read_* is called. A non-finite x is flagged on device and
+ * reported by sg_ctx_read_stats as SG_ERR_DATA (ffn_exec.hpp:61-63). */
+sg_status sg_ffn_forward_device(sg_ctx* ctx, const sg_layer* layer, sg_pipeline pipeline,
+                                const float* x, float* y, void* stream);
+
+/* Synchronises `stream`, then copies the last call's stats (computed with the
+ * reference formulas) to host. Returns SG_ERR_DATA if that call saw non-finite x. */
+sg_status sg_ctx_read_stats(sg_ctx* ctx, void* stream, sg_exec_stats* stats);
+
+/* Synchronises, then copies the last call's index sets (GLOBAL neuron indices,
+ * ascending): P (predicted active, capacity >= local inter), V (gate survivors),
+ * and optionally g (fp32 gate pre-activation per P entry) and z (fp32 gated value
+ * per V entry). Any pointer may be NULL. */
+sg_status sg_ctx_read_sets(sg_ctx* ctx, void* stream, int32_t* P, int64_t* p, int32_t* V,
+                           int64_t* v, float* g, float* z);
+
+/* Predictor only (stage 1): mask[local inter] bytes and count, host outputs.
+ * ffn_exec.hpp:125-146. x: host, dtype x_dtype (SG_F64 / SG_F32), length x_len. */
+sg_status sg_predict_mask(sg_ctx* ctx, const sg_layer* layer, const void* x, sg_dtype x_dtype,
+                          int64_t x_len, uint8_t* mask, int64_t* count, void* stream);
+
+/* Host-facing executor = the reference call shape: host x in, host y out
+ * (x_dtype/y_dtype SG_F64 or SG_F32), stats out (may be NULL). Validates x on
+ * host (length, finiteness -> SG_ERR_DATA), copies H2D through pinned staging,
+ * runs sg_ffn_forward_device, copies y D2H, synchronises. */
+sg_status sg_ffn_forward(sg_ctx* ctx, const sg_layer* layer, sg_pipeline pipeline, const void* x,
+                         sg_dtype x_dtype, int64_t x_len, void* y, sg_dtype y_dtype,
+                         sg_exec_stats* stats, void* stream);
+
+/* Multi-layer decode step on device: runs layers[0..n) in order on `stream`,
+ * layer l reading xs + l*hidden and writing ys + l*hidden (fp32, device). With
+ * chain != 0, layer l+1 reads layer l's output instead of xs (a real decode chain). */
+sg_status sg_ffn_forward_layers(sg_ctx* ctx, const sg_layer* const* layers, int32_t n,
+                                sg_pipeline pipeline, const float* xs, float* ys, int32_t chain,
+                                void* stream);
+
+/* Host-buffer variant of sg_ffn_forward_layers (the end-to-end call shape):
+ * copies xs_host (n*hidden fp32) H2D, runs the stack, copies ys_host back and
+ * synchronises. stats (n entries, may be NULL) gets each layer's ExecStats. */
+sg_status sg_ffn_forward_layers_host(sg_ctx* ctx, const sg_layer* const* layers, int32_t n,
+                                     sg_pipeline pipeline, const float* xs_host, float* ys_host,
+                                     int32_t chain, sg_exec_stats* stats, void* stream);
+
+/* Synchronises, then returns per-layer stats of the last sg_ffn_forward_layers* call. */
+sg_status sg_ctx_read_stack_stats(sg_ctx* ctx, void* stream, int32_t n, sg_exec_stats* stats);
+
+/* ffn_exec.hpp:229-244, pure host. */
+sg_status sg_op_count_model(int64_t d, int64_t D, int64_t r, double s, double s_prime,
+                            int64_t* dense, double* sparse, double* ratio);
+
+/* Host rounding used on upload: f64 -> f32 (RNE) -> bf16 (RNE), NaN-preserving. */
+void sg_round_bf16(const double* in, uint16_t* out, int64_t n);
+
+/* ---- host-side producers of the executor's inputs (not on the device path) ---- */
+
+/* synthetic.hpp:80-108 (make_synthetic_fixture), same mt19937_64 stream order.
+ * Outputs (any NULL to skip; the stream is still drawn): gate/up inter x hidden,
+ * down hidden x inter, calib hidden x calib_tokens, eval hidden x eval_tokens,
+ * all f64 row-major. */
+sg_status sg_synthetic_fixture(int64_t hidden, int64_t inter, int64_t calib_tokens,
+                               int64_t eval_tokens, double natural_sparsity, uint64_t seed,
+                               double* gate, double* up, double* down, double* calib,
+                               double* eval);
+
+/* Same stream, but weights are emitted directly as bf16 (f64->f32->bf16), down
+ * already transposed to neuron-major (inter x hidden), tokens as f64. Used to
+ * build multi-layer bench models without holding f64 weights. */
+sg_status sg_synthetic_fixture_bf16(int64_t hidden, int64_t inter, int64_t calib_tokens,
+                                    int64_t eval_tokens, double natural_sparsity, uint64_t seed,
+                                    uint16_t* gate, uint16_t* up, uint16_t* down_t,
+                                    double* calib, double* eval);
+
+/* calibration.hpp:61-96 + :128-205 (build_instance + greedy_calibrate): scores and
+ * weights are inter x T row-major f64; writes bias[inter] (+inf where the pointer
+ * stayed at 0), and the achieved sparsity. */
+sg_status sg_greedy_calibrate(const double* scores, const double* weights, int64_t inter,
+                              int64_t T, int32_t eta, double target_sparsity, double* bias,
+                              double* achieved_sparsity, double* total_damage);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif /* SPARSEGATE_C_H_ */

@@ -1,0 +1,835 @@
+// sparsegate-b200 host library: the C ABI (include/sparsegate_c.h).
+//
+// Host responsibilities, each mirroring a reference contract:
+//   * sg_layer_create: validate ONCE (types.hpp:31-51 FfnWeights, :82-105
+//     Predictor), round to bf16, pad rows to 128-B pitches, transpose `down`
+//     (reference d x D, types.hpp:19-24) to neuron-major and pack it behind the
+//     matching `up` row, upload.
+//   * sg_ffn_forward*: the executor entry points (ffn_exec.hpp:103-218); input
+//     checks of detail::check_input (ffn_exec.hpp:56-65); ExecStats formulas
+//     (ffn_exec.hpp:120, :173-180, :209-216).
+//   * sg_op_count_model: ffn_exec.hpp:229-244 verbatim semantics.
+//   * sg_synthetic_fixture*: synthetic.hpp:15-108 (same mt19937_64 stream).
+//   * sg_greedy_calibrate: calibration.hpp:61-96 and :128-205 (offline producer).
+#include "sparsegate_c.h"
+#include "sg_internal.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <numeric>
+#include <queue>
+#include <random>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+struct sg_layer {
+    int device = 0;
+    int64_t d = 0, D_full = 0, D_local = 0, r = 0;
+    int act = 0;
+    bool has_pred = false;
+    bool has_w = false;
+    int pitch_d = 0, pitch_r = 0;
+    int64_t gbase = 0, gstride = 1;
+    void* dmem = nullptr;
+    size_t bytes = 0;
+    sg::LayerView view{};
+};
+
+struct sg_ctx {
+    int device = 0;
+    int G = 0;
+    int64_t max_d = 0, max_D = 0, max_r = 0;
+    int pitch_dmax = 0, pitch_rmax = 0;
+    void* dmem = nullptr;
+    sg::WorkView W{};
+    float* xdev = nullptr;
+    float* ydev = nullptr;
+    uint8_t* maskdev = nullptr;
+    float* xpin = nullptr;
+    float* ypin = nullptr;
+    const sg_layer* last_layer = nullptr;
+    int last_pipeline = 0;
+    sg::LayerView* stackdev = nullptr;
+    int stack_cap = 0;
+    std::vector<const sg_layer*> last_stack;
+    float* xsdev = nullptr;  // host-entry staging for stacks
+    float* ysdev = nullptr;
+    size_t xs_cap = 0;
+};
+
+constexpr int kMaxStackLayers = 1024;
+
+namespace {
+
+thread_local std::string g_err;
+
+sg_status fail(sg_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+#define SG_CUDA(call)                                                                      \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(SG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+int round_up(int64_t v, int64_t a) { return static_cast<int>((v + a - 1) / a * a); }
+
+// f64 -> f32 (RNE, hardware cast) -> bf16 (RNE on the f32 bits), NaN kept quiet.
+inline uint16_t f32_to_bf16(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x007fffffu) != 0) {
+        return static_cast<uint16_t>((u >> 16) | 0x0040u);
+    }
+    const uint32_t lsb = (u >> 16) & 1u;
+    u += 0x7fffu + lsb;
+    return static_cast<uint16_t>(u >> 16);
+}
+inline uint16_t to_bf16(const void* base, int dtype, int64_t i) {
+    switch (dtype) {
+        case SG_F64: return f32_to_bf16(static_cast<float>(static_cast<const double*>(base)[i]));
+        case SG_F32: return f32_to_bf16(static_cast<const float*>(base)[i]);
+        default: return static_cast<const uint16_t*>(base)[i];
+    }
+}
+inline bool finite_at(const void* base, int dtype, int64_t i) {
+    switch (dtype) {
+        case SG_F64: return std::isfinite(static_cast<const double*>(base)[i]);
+        case SG_F32: return std::isfinite(static_cast<const float*>(base)[i]);
+        default: return (static_cast<const uint16_t*>(base)[i] & 0x7f80u) != 0x7f80u;
+    }
+}
+
+// Parallel for over [0, n) in contiguous blocks on hardware threads.
+void par_for(int64_t n, const std::function<void(int64_t, int64_t)>& fn) {
+    unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int64_t workers = std::min<int64_t>(hw, std::max<int64_t>(1, n / 64));
+    if (workers <= 1) {
+        fn(0, n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (int64_t w = 0; w < workers; ++w) {
+        pool.emplace_back([&, w] { fn(n * w / workers, n * (w + 1) / workers); });
+    }
+    for (auto& t : pool) t.join();
+}
+
+bool all_finite(const void* p, int dtype, int64_t n) {
+    std::atomic<bool> ok{true};
+    par_for(n, [&](int64_t a, int64_t b) {
+        for (int64_t i = a; i < b && ok.load(std::memory_order_relaxed); ++i) {
+            if (!finite_at(p, dtype, i)) ok = false;
+        }
+    });
+    return ok;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int64_t local_to_global(const sg_layer* L, int64_t k) { return L->gbase + k * L->gstride; }
+
+sg_exec_stats make_stats(const sg_layer* L, int pipeline, int64_t p, int64_t v) {
+    sg_exec_stats s{};
+    const int64_t d = L->d, D = L->D_local, r = L->r;
+    s.pipeline = pipeline;
+    s.predicted_active = p;
+    s.revalidated = v;
+    if (pipeline == SG_PIPELINE_DENSE) {  // ffn_exec.hpp:118-121
+        s.multiplies = int64_t{3} * d * D;
+        s.predicted_sparsity = 0.0;
+        s.realized_sparsity = 0.0;
+    } else if (pipeline == SG_PIPELINE_PARALLEL) {  // ffn_exec.hpp:173-180
+        s.multiplies = r * (d + D) + int64_t{3} * d * p;
+        s.predicted_sparsity = 1.0 - static_cast<double>(p) / static_cast<double>(D);
+        s.realized_sparsity = s.predicted_sparsity;
+    } else {  // ffn_exec.hpp:209-216
+        s.multiplies = r * (d + D) + d * p + int64_t{2} * d * v;
+        s.predicted_sparsity = 1.0 - static_cast<double>(p) / static_cast<double>(D);
+        s.realized_sparsity = 1.0 - static_cast<double>(v) / static_cast<double>(D);
+    }
+    return s;
+}
+
+sg::WorkView work_for(sg_ctx* ctx, const float* x, float* y) {
+    sg::WorkView W = ctx->W;
+    W.x = x;
+    W.y = y;
+    return W;
+}
+
+sg_status check_pair(sg_ctx* ctx, const sg_layer* L) {
+    if (ctx == nullptr || L == nullptr) return fail(SG_ERR_USAGE, "null ctx or layer");
+    if (ctx->device != L->device) return fail(SG_ERR_USAGE, "ctx and layer on different devices");
+    if (L->d > ctx->max_d || L->D_local > ctx->max_D || L->r > ctx->max_r)
+        return fail(SG_ERR_USAGE, "layer exceeds the ctx bounds (max_hidden/max_inter/max_rank)");
+    return SG_OK;
+}
+
+sg_status read_x(const void* x, sg_dtype dt, int64_t n, int64_t d, float* out, const char* what) {
+    if (x == nullptr) return fail(SG_ERR_USAGE, "null x");
+    if (n != d) {  // ffn_exec.hpp:58-60 / :127-129
+        return fail(SG_ERR_DATA, std::string(what) + " input length " + std::to_string(n) +
+                                     " does not match hidden size " + std::to_string(d));
+    }
+    for (int64_t i = 0; i < n; ++i) {
+        double v;
+        if (dt == SG_F64) v = static_cast<const double*>(x)[i];
+        else if (dt == SG_F32) v = static_cast<const float*>(x)[i];
+        else return fail(SG_ERR_USAGE, "x dtype must be SG_F64 or SG_F32");
+        if (!std::isfinite(v)) {  // ffn_exec.hpp:61-63
+            return fail(SG_ERR_DATA, std::string(what) + " input has non-finite entries");
+        }
+        out[i] = static_cast<float>(v);
+    }
+    return SG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sg_last_error(void) { return g_err.c_str(); }
+const char* sg_version(void) { return "sparsegate-b200 0.1 (sm_100a)"; }
+
+sg_status sg_op_count_model(int64_t d, int64_t D, int64_t r, double s, double sp, int64_t* dense,
+                            double* sparse, double* ratio) {
+    if (d < 1 || D < 1 || r < 0) {
+        return fail(SG_ERR_DATA, "op count model: dimensions must be positive and rank nonnegative");
+    }
+    if (!(0.0 <= s && s <= sp && sp <= 1.0)) {
+        return fail(SG_ERR_DATA, "op count model: need 0 <= s <= s' <= 1");
+    }
+    const int64_t dn = 3 * d * D;
+    const double sps = static_cast<double>(r) * static_cast<double>(d + D) +
+                       static_cast<double>(d) * (1.0 - s) * static_cast<double>(D) +
+                       2.0 * static_cast<double>(d) * (1.0 - sp) * static_cast<double>(D);
+    if (dense) *dense = dn;
+    if (sparse) *sparse = sps;
+    if (ratio) *ratio = static_cast<double>(dn) / sps;
+    return SG_OK;
+}
+
+void sg_round_bf16(const double* in, uint16_t* out, int64_t n) {
+    par_for(n, [&](int64_t a, int64_t b) {
+        for (int64_t i = a; i < b; ++i) out[i] = f32_to_bf16(static_cast<float>(in[i]));
+    });
+}
+
+sg_status sg_layer_create(const sg_layer_desc* desc, sg_layer** out) {
+    if (desc == nullptr || out == nullptr) return fail(SG_ERR_USAGE, "null argument");
+    *out = nullptr;
+    const int64_t d = desc->hidden, D = desc->inter;
+    if (d < 1 || D < 1) {  // types.hpp:34-37
+        return fail(SG_ERR_DATA, "ffn weights: gate must be at least 1x1, got " +
+                                     std::to_string(D) + "x" + std::to_string(d));
+    }
+    const bool has_w = desc->gate != nullptr || desc->up != nullptr || desc->down != nullptr;
+    if (has_w && (desc->gate == nullptr || desc->up == nullptr || desc->down == nullptr))
+        return fail(SG_ERR_USAGE, "gate/up/down must be given together");
+    const int wdt = desc->weight_dtype;
+    if (wdt != SG_F64 && wdt != SG_F32 && wdt != SG_BF16) return fail(SG_ERR_USAGE, "bad weight dtype");
+    const bool has_pred = desc->pred_A != nullptr || desc->pred_B != nullptr || desc->bias != nullptr;
+    int64_t r = 0;
+    if (has_pred) {
+        if (!desc->pred_A || !desc->pred_B || !desc->bias)
+            return fail(SG_ERR_USAGE, "pred_A, pred_B and bias must be given together");
+        r = desc->rank;
+        if (r < 1 || r > std::min(D, d)) {  // types.hpp:92-95
+            return fail(SG_ERR_DATA, "predictor: rank " + std::to_string(r) + " out of range [1, " +
+                                         std::to_string(std::min(D, d)) + "]");
+        }
+        if (desc->bias_dtype != SG_F64 && desc->bias_dtype != SG_F32)
+            return fail(SG_ERR_USAGE, "bias dtype must be SG_F64 or SG_F32");
+    }
+    if (!has_w && !has_pred) return fail(SG_ERR_USAGE, "layer needs weights and/or a predictor");
+    if (d > (1 << 20) || D > (1 << 30)) return fail(SG_ERR_USAGE, "layer too large");
+    // types.hpp:48-50 / :102-104 — once, here, instead of on every call.
+    if (has_w && (!all_finite(desc->gate, wdt, D * d) || !all_finite(desc->up, wdt, D * d) ||
+                  !all_finite(desc->down, wdt, D * d))) {
+        return fail(SG_ERR_DATA, "ffn weights: non-finite entries");
+    }
+    if (has_pred && (!all_finite(desc->pred_A, wdt, D * r) || !all_finite(desc->pred_B, wdt, r * d))) {
+        return fail(SG_ERR_DATA, "predictor: non-finite factor entries");
+    }
+
+    auto L = new sg_layer;
+    L->device = desc->device;
+    L->d = d;
+    L->D_full = D;
+    L->r = r;
+    L->act = desc->activation == SG_DRELU ? 1 : 0;
+    L->has_pred = has_pred;
+    L->has_w = has_w;
+    L->pitch_d = round_up(d, 64);
+    L->pitch_r = has_pred ? round_up(r, 64) : 64;
+    // shard -> local neuron list
+    const int S = desc->shard_count > 1 ? desc->shard_count : 1;
+    const int si = S > 1 ? desc->shard_index : 0;
+    if (si < 0 || si >= S) {
+        delete L;
+        return fail(SG_ERR_USAGE, "shard_index out of range");
+    }
+    if (S > 1 && desc->shard_interleave) {
+        L->gbase = si;
+        L->gstride = S;
+        L->D_local = (D - si + S - 1) / S;
+    } else {
+        const int64_t lo = D * si / S, hi = D * (si + 1) / S;
+        L->gbase = lo;
+        L->gstride = 1;
+        L->D_local = hi - lo;
+    }
+    if (L->D_local < 1) {
+        delete L;
+        return fail(SG_ERR_USAGE, "shard holds no neurons");
+    }
+    const int64_t Dl = L->D_local, pd = L->pitch_d, pr = L->pitch_r;
+    // device layout: [B r x pd][A Dl x pr][gate Dl x pd][ud Dl x 2pd][bias Dl f32]
+    const size_t nB = static_cast<size_t>(has_pred ? r : 0) * pd;
+    const size_t nA = static_cast<size_t>(has_pred ? Dl : 0) * pr;
+    const size_t nG = static_cast<size_t>(has_w ? Dl : 0) * pd;
+    const size_t nUD = static_cast<size_t>(has_w ? Dl : 0) * 2 * pd;
+    const size_t offB = 0, offA = offB + nB, offG = offA + nA, offUD = offG + nG;
+    const size_t n16 = offUD + nUD;
+    const size_t bias_off = (n16 * 2 + 255) / 256 * 256;
+    const size_t total = bias_off + static_cast<size_t>(Dl) * 4;
+    std::vector<uint16_t> host(n16, 0);
+    std::vector<float> hbias(static_cast<size_t>(Dl), 0.f);
+    const bool down_nm = desc->down_neuron_major != 0;
+    par_for(Dl, [&](int64_t a, int64_t b) {
+        for (int64_t k = a; k < b; ++k) {
+            const int64_t n = L->gbase + k * L->gstride;
+            uint16_t* g = host.data() + offG + k * pd;
+            uint16_t* u = host.data() + offUD + k * 2 * pd;
+            uint16_t* dn = u + pd;
+            for (int64_t j = 0; has_w && j < d; ++j) {
+                g[j] = to_bf16(desc->gate, wdt, n * d + j);
+                u[j] = to_bf16(desc->up, wdt, n * d + j);
+                dn[j] = down_nm ? to_bf16(desc->down, wdt, n * d + j)
+                                : to_bf16(desc->down, wdt, j * D + n);  // column n of d x D
+            }
+            if (has_pred) {
+                uint16_t* arow = host.data() + offA + k * pr;
+                for (int64_t j = 0; j < r; ++j) arow[j] = to_bf16(desc->pred_A, wdt, n * r + j);
+                hbias[k] = desc->bias_dtype == SG_F64
+                               ? static_cast<float>(static_cast<const double*>(desc->bias)[n])
+                               : static_cast<const float*>(desc->bias)[n];
+            }
+        }
+    });
+    if (has_pred) {
+        par_for(r, [&](int64_t a, int64_t b) {
+            for (int64_t j = a; j < b; ++j)
+                for (int64_t k = 0; k < d; ++k)
+                    host[offB + j * pd + k] = to_bf16(desc->pred_B, wdt, j * d + k);
+        });
+    }
+    DeviceGuard dg(desc->device);
+    cudaError_t e = cudaMalloc(&L->dmem, total);
+    if (e == cudaSuccess) e = cudaMemcpy(L->dmem, host.data(), n16 * 2, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(static_cast<char*>(L->dmem) + bias_off, hbias.data(), Dl * 4,
+                       cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        if (L->dmem) cudaFree(L->dmem);
+        delete L;
+        return fail(SG_ERR_CUDA, std::string("layer upload: ") + cudaGetErrorString(e));
+    }
+    L->bytes = total;
+    auto* base = static_cast<uint16_t*>(L->dmem);
+    sg::LayerView& V = L->view;
+    V.d = static_cast<int>(d);
+    V.D = static_cast<int>(Dl);
+    V.r = static_cast<int>(r);
+    V.pitch_d = L->pitch_d;
+    V.pitch_r = L->pitch_r;
+    V.act = L->act;
+    V.gbase = static_cast<int>(L->gbase);
+    V.gstride = static_cast<int>(L->gstride);
+    V.B = has_pred ? base + offB : nullptr;
+    V.A = has_pred ? base + offA : nullptr;
+    V.gate = has_w ? base + offG : nullptr;
+    V.ud = has_w ? base + offUD : nullptr;
+    V.bias = reinterpret_cast<const float*>(static_cast<char*>(L->dmem) + bias_off);
+    *out = L;
+    return SG_OK;
+}
+
+sg_status sg_layer_destroy(sg_layer* L) {
+    if (L == nullptr) return SG_OK;
+    DeviceGuard dg(L->device);
+    if (L->dmem) cudaFree(L->dmem);
+    delete L;
+    return SG_OK;
+}
+
+int64_t sg_layer_local_inter(const sg_layer* L) { return L ? L->D_local : 0; }
+int64_t sg_layer_global_index(const sg_layer* L, int64_t k) { return L ? local_to_global(L, k) : -1; }
+int64_t sg_layer_device_bytes(const sg_layer* L) { return L ? static_cast<int64_t>(L->bytes) : 0; }
+
+sg_status sg_ctx_create(int32_t device, int64_t max_hidden, int64_t max_inter, int64_t max_rank,
+                        sg_ctx** out) {
+    if (out == nullptr || max_hidden < 1 || max_inter < 1 || max_rank < 0)
+        return fail(SG_ERR_USAGE, "bad ctx bounds");
+    *out = nullptr;
+    DeviceGuard dg(device);
+    sg::LaunchInfo info{};
+    const int qe = sg::query_launch_info(device, &info);
+    if (qe != 0) return fail(SG_ERR_CUDA, std::string("device query: ") +
+                                             cudaGetErrorString(static_cast<cudaError_t>(qe)));
+    auto C = new sg_ctx;
+    C->device = device;
+    C->G = info.num_sms;
+    C->max_d = max_hidden;
+    C->max_D = max_inter;
+    C->max_r = std::max<int64_t>(max_rank, 1);
+    C->pitch_dmax = round_up(max_hidden, 64);
+    C->pitch_rmax = round_up(C->max_r, 64);
+    const int G = C->G;
+    const size_t Dm = static_cast<size_t>(max_inter) + 32;
+    const int nslices = C->pitch_dmax / 256 + 2;
+    // carve one allocation (256-B aligned pieces)
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off += (bytes + 255) / 256 * 256;
+        return o;
+    };
+    const size_t o_t = take(C->pitch_rmax * 4);
+    const size_t o_cnt = take(2 * G * 4);
+    const size_t o_plist = take(Dm * 4), o_P = take(Dm * 4), o_Pl = take(Dm * 4);
+    const size_t o_gP = take(Dm * 4), o_surv = take(Dm * 4), o_zP = take(Dm * 4);
+    const size_t o_vlist = take(Dm * 4), o_zlist = take(Dm * 4), o_V = take(Dm * 4);
+    const size_t o_zV = take(Dm * 4), o_zD = take(Dm * 4);
+    const size_t o_ypart = take(static_cast<size_t>(G) * C->pitch_dmax * 4);
+    const size_t o_slice = take(nslices * 4);
+    const size_t o_bar = take(32 * 4);
+    const size_t o_stats = take(4 * 4 * kMaxStackLayers);
+    const size_t o_x = take(C->pitch_dmax * 4), o_y = take(C->pitch_dmax * 4);
+    const size_t o_mask = take(Dm);
+    cudaError_t e = cudaMalloc(&C->dmem, off);
+    if (e == cudaSuccess) e = cudaMemset(C->dmem, 0, off);
+    if (e == cudaSuccess) e = cudaMallocHost(&C->xpin, C->pitch_dmax * 4);
+    if (e == cudaSuccess) e = cudaMallocHost(&C->ypin, C->pitch_dmax * 4);
+    if (e != cudaSuccess) {
+        if (C->dmem) cudaFree(C->dmem);
+        if (C->xpin) cudaFreeHost(C->xpin);
+        delete C;
+        return fail(SG_ERR_CUDA, std::string("ctx alloc: ") + cudaGetErrorString(e));
+    }
+    char* b = static_cast<char*>(C->dmem);
+    sg::WorkView& W = C->W;
+    W.t = reinterpret_cast<float*>(b + o_t);
+    W.cnt = reinterpret_cast<int*>(b + o_cnt);
+    W.plist = reinterpret_cast<int*>(b + o_plist);
+    W.P = reinterpret_cast<int*>(b + o_P);
+    W.Pl = reinterpret_cast<int*>(b + o_Pl);
+    W.gP = reinterpret_cast<float*>(b + o_gP);
+    W.surv = reinterpret_cast<int*>(b + o_surv);
+    W.zP = reinterpret_cast<float*>(b + o_zP);
+    W.vlist = reinterpret_cast<int*>(b + o_vlist);
+    W.zlist = reinterpret_cast<float*>(b + o_zlist);
+    W.V = reinterpret_cast<int*>(b + o_V);
+    W.zV = reinterpret_cast<float*>(b + o_zV);
+    W.zD = reinterpret_cast<float*>(b + o_zD);
+    W.ypart = reinterpret_cast<float*>(b + o_ypart);
+    W.slice_ctr = reinterpret_cast<unsigned*>(b + o_slice);
+    W.bar = reinterpret_cast<unsigned*>(b + o_bar);
+    W.stats = reinterpret_cast<int*>(b + o_stats);
+    C->xdev = reinterpret_cast<float*>(b + o_x);
+    C->ydev = reinterpret_cast<float*>(b + o_y);
+    C->maskdev = reinterpret_cast<uint8_t*>(b + o_mask);
+    *out = C;
+    return SG_OK;
+}
+
+sg_status sg_ctx_destroy(sg_ctx* C) {
+    if (C == nullptr) return SG_OK;
+    DeviceGuard dg(C->device);
+    if (C->dmem) cudaFree(C->dmem);
+    if (C->xpin) cudaFreeHost(C->xpin);
+    if (C->ypin) cudaFreeHost(C->ypin);
+    if (C->stackdev) cudaFree(C->stackdev);
+    if (C->xsdev) cudaFree(C->xsdev);
+    if (C->ysdev) cudaFree(C->ysdev);
+    delete C;
+    return SG_OK;
+}
+
+sg_status sg_ffn_forward_device(sg_ctx* C, const sg_layer* L, sg_pipeline pipeline,
+                                const float* x, float* y, void* stream) {
+    if (sg_status s = check_pair(C, L); s != SG_OK) return s;
+    if (pipeline != SG_PIPELINE_DENSE && !L->has_pred)
+        return fail(SG_ERR_USAGE, "sparse pipeline needs a layer with a predictor");
+    if (pipeline < 0 || pipeline > 2) return fail(SG_ERR_USAGE, "bad pipeline");
+    if (!L->has_w) return fail(SG_ERR_USAGE, "predictor-only layer cannot run the FFN");
+    if (x == nullptr || y == nullptr) return fail(SG_ERR_USAGE, "null x/y");
+    DeviceGuard dg(L->device);
+    const int e = sg::launch_layer(L->view, work_for(C, x, y), pipeline, C->G, stream);
+    if (e != 0) {
+        return fail(SG_ERR_CUDA, std::string("launch: ") +
+                                     cudaGetErrorString(static_cast<cudaError_t>(e)));
+    }
+    C->last_layer = L;
+    C->last_pipeline = pipeline;
+    return SG_OK;
+}
+
+sg_status sg_ctx_read_stats(sg_ctx* C, void* stream, sg_exec_stats* out) {
+    if (C == nullptr || out == nullptr) return fail(SG_ERR_USAGE, "null argument");
+    if (C->last_layer == nullptr) return fail(SG_ERR_USAGE, "no forward call on this ctx");
+    DeviceGuard dg(C->device);
+    SG_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    int st[4];
+    SG_CUDA(cudaMemcpy(st, C->W.stats, sizeof(st), cudaMemcpyDeviceToHost));
+    const int pipe = C->last_pipeline;
+    const int64_t p = pipe == SG_PIPELINE_DENSE ? C->last_layer->D_local : st[0];
+    const int64_t v = pipe == SG_PIPELINE_DENSE ? C->last_layer->D_local : st[1];
+    *out = make_stats(C->last_layer, pipe, p, v);
+    if (st[2] != 0) return fail(SG_ERR_DATA, "ffn input has non-finite entries");
+    return SG_OK;
+}
+
+sg_status sg_ctx_read_sets(sg_ctx* C, void* stream, int32_t* P, int64_t* p, int32_t* V, int64_t* v,
+                           float* g, float* z) {
+    if (C == nullptr) return fail(SG_ERR_USAGE, "null ctx");
+    if (C->last_layer == nullptr || C->last_pipeline == SG_PIPELINE_DENSE)
+        return fail(SG_ERR_USAGE, "no sparse forward call on this ctx");
+    DeviceGuard dg(C->device);
+    SG_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    int st[4];
+    SG_CUDA(cudaMemcpy(st, C->W.stats, sizeof(st), cudaMemcpyDeviceToHost));
+    if (p) *p = st[0];
+    if (v) *v = st[1];
+    if (P && st[0] > 0) SG_CUDA(cudaMemcpy(P, C->W.P, st[0] * 4, cudaMemcpyDeviceToHost));
+    if (g && st[0] > 0) SG_CUDA(cudaMemcpy(g, C->W.gP, st[0] * 4, cudaMemcpyDeviceToHost));
+    if (V && st[1] > 0) SG_CUDA(cudaMemcpy(V, C->W.V, st[1] * 4, cudaMemcpyDeviceToHost));
+    if (z && st[1] > 0) SG_CUDA(cudaMemcpy(z, C->W.zV, st[1] * 4, cudaMemcpyDeviceToHost));
+    return SG_OK;
+}
+
+sg_status sg_predict_mask(sg_ctx* C, const sg_layer* L, const void* x, sg_dtype x_dtype,
+                          int64_t x_len, uint8_t* mask, int64_t* count, void* stream) {
+    if (sg_status s = check_pair(C, L); s != SG_OK) return s;
+    if (!L->has_pred) return fail(SG_ERR_USAGE, "layer has no predictor");
+    if (sg_status s = read_x(x, x_dtype, x_len, L->d, C->xpin, "predictor"); s != SG_OK) return s;
+    DeviceGuard dg(L->device);
+    auto st = static_cast<cudaStream_t>(stream);
+    SG_CUDA(cudaMemcpyAsync(C->xdev, C->xpin, L->d * 4, cudaMemcpyHostToDevice, st));
+    const int e = sg::launch_predict(L->view, work_for(C, C->xdev, C->ydev), C->maskdev, C->G, st);
+    if (e != 0) return fail(SG_ERR_CUDA, std::string("launch: ") +
+                                             cudaGetErrorString(static_cast<cudaError_t>(e)));
+    int stv[4];
+    SG_CUDA(cudaMemcpyAsync(stv, C->W.stats, sizeof(stv), cudaMemcpyDeviceToHost, st));
+    if (mask) SG_CUDA(cudaMemcpyAsync(mask, C->maskdev, L->D_local, cudaMemcpyDeviceToHost, st));
+    SG_CUDA(cudaStreamSynchronize(st));
+    if (count) *count = stv[0];
+    return SG_OK;
+}
+
+sg_status sg_ffn_forward(sg_ctx* C, const sg_layer* L, sg_pipeline pipeline, const void* x,
+                         sg_dtype x_dtype, int64_t x_len, void* y, sg_dtype y_dtype,
+                         sg_exec_stats* stats, void* stream) {
+    if (sg_status s = check_pair(C, L); s != SG_OK) return s;
+    if (y == nullptr) return fail(SG_ERR_USAGE, "null y");
+    if (y_dtype != SG_F64 && y_dtype != SG_F32) return fail(SG_ERR_USAGE, "y dtype must be f64/f32");
+    if (sg_status s = read_x(x, x_dtype, x_len, L->d, C->xpin, "ffn"); s != SG_OK) return s;
+    DeviceGuard dg(L->device);
+    auto st = static_cast<cudaStream_t>(stream);
+    SG_CUDA(cudaMemcpyAsync(C->xdev, C->xpin, L->d * 4, cudaMemcpyHostToDevice, st));
+    if (sg_status s = sg_ffn_forward_device(C, L, pipeline, C->xdev, C->ydev, stream); s != SG_OK)
+        return s;
+    SG_CUDA(cudaMemcpyAsync(C->ypin, C->ydev, L->d * 4, cudaMemcpyDeviceToHost, st));
+    sg_exec_stats tmp{};
+    if (sg_status s = sg_ctx_read_stats(C, stream, &tmp); s != SG_OK) return s;
+    if (stats) *stats = tmp;
+    if (y_dtype == SG_F64) {
+        auto* yd = static_cast<double*>(y);
+        for (int64_t i = 0; i < L->d; ++i) yd[i] = static_cast<double>(C->ypin[i]);
+    } else {
+        std::memcpy(y, C->ypin, L->d * 4);
+    }
+    return SG_OK;
+}
+
+sg_status sg_ffn_forward_layers(sg_ctx* C, const sg_layer* const* layers, int32_t n,
+                                sg_pipeline pipeline, const float* xs, float* ys, int32_t chain,
+                                void* stream) {
+    if (C == nullptr || layers == nullptr || n < 1 || n > kMaxStackLayers)
+        return fail(SG_ERR_USAGE, "bad arguments");
+    if (xs == nullptr || ys == nullptr) return fail(SG_ERR_USAGE, "null xs/ys");
+    const sg_layer* L0 = layers[0];
+    for (int i = 0; i < n; ++i) {
+        const sg_layer* L = layers[i];
+        if (sg_status s = check_pair(C, L); s != SG_OK) return s;
+        if (L->d != L0->d || L->D_local != L0->D_local || L->r != L0->r)
+            return fail(SG_ERR_USAGE, "all layers of a stack must share hidden/inter/rank");
+        if (pipeline != SG_PIPELINE_DENSE && !L->has_pred)
+            return fail(SG_ERR_USAGE, "sparse pipeline needs layers with predictors");
+        if (!L->has_w) return fail(SG_ERR_USAGE, "predictor-only layer cannot run the FFN");
+    }
+    DeviceGuard dg(C->device);
+    auto st = static_cast<cudaStream_t>(stream);
+    if (C->stack_cap < n) {
+        C->last_stack.clear();
+        if (C->stackdev) cudaFree(C->stackdev);
+        C->stackdev = nullptr;
+        C->stack_cap = 0;
+        SG_CUDA(cudaMalloc(&C->stackdev, sizeof(sg::LayerView) * n));
+        C->stack_cap = n;
+    }
+    // The (tiny) descriptor table is uploaded only when the stack changes, so
+    // repeated calls — and CUDA-graph capture after a first warm call — issue
+    // nothing but the kernel launch.
+    const bool same = C->last_stack.size() == static_cast<size_t>(n) &&
+                      std::equal(C->last_stack.begin(), C->last_stack.end(), layers);
+    if (!same) {
+        std::vector<sg::LayerView> views(n);
+        for (int i = 0; i < n; ++i) views[i] = layers[i]->view;
+        SG_CUDA(cudaStreamSynchronize(st));
+        SG_CUDA(cudaMemcpy(C->stackdev, views.data(), sizeof(sg::LayerView) * n,
+                           cudaMemcpyHostToDevice));
+    }
+    const int e = sg::launch_layers(C->stackdev, n, L0->view, work_for(C, xs, ys), xs, ys, chain,
+                                    static_cast<int>(L0->d), pipeline, C->G, st);
+    if (e != 0) return fail(SG_ERR_CUDA, std::string("launch: ") +
+                                             cudaGetErrorString(static_cast<cudaError_t>(e)));
+    C->last_layer = layers[n - 1];
+    C->last_pipeline = pipeline;
+    C->last_stack.assign(layers, layers + n);
+    return SG_OK;
+}
+
+sg_status sg_ctx_read_stack_stats(sg_ctx* C, void* stream, int32_t n, sg_exec_stats* out) {
+    if (C == nullptr || out == nullptr) return fail(SG_ERR_USAGE, "null argument");
+    if (n < 1 || static_cast<size_t>(n) > C->last_stack.size())
+        return fail(SG_ERR_USAGE, "no stack call with that many layers on this ctx");
+    DeviceGuard dg(C->device);
+    SG_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    std::vector<int> st(4 * static_cast<size_t>(n));
+    SG_CUDA(cudaMemcpy(st.data(), C->W.stats, st.size() * 4, cudaMemcpyDeviceToHost));
+    bool bad = false;
+    for (int l = 0; l < n; ++l) {
+        const sg_layer* L = C->last_stack[l];
+        const int pipe = C->last_pipeline;
+        const int64_t p = pipe == SG_PIPELINE_DENSE ? L->D_local : st[4 * l];
+        const int64_t v = pipe == SG_PIPELINE_DENSE ? L->D_local : st[4 * l + 1];
+        out[l] = make_stats(L, pipe, p, v);
+        bad |= st[4 * l + 2] != 0;
+    }
+    if (bad) return fail(SG_ERR_DATA, "ffn input has non-finite entries");
+    return SG_OK;
+}
+
+sg_status sg_ffn_forward_layers_host(sg_ctx* C, const sg_layer* const* layers, int32_t n,
+                                     sg_pipeline pipeline, const float* xs_host, float* ys_host,
+                                     int32_t chain, sg_exec_stats* stats, void* stream) {
+    if (C == nullptr || layers == nullptr || n < 1 || xs_host == nullptr || ys_host == nullptr)
+        return fail(SG_ERR_USAGE, "bad arguments");
+    const size_t d = static_cast<size_t>(layers[0]->d);
+    const size_t need = d * static_cast<size_t>(n) * 4;
+    DeviceGuard dg(C->device);
+    if (C->xs_cap < need) {
+        if (C->xsdev) cudaFree(C->xsdev);
+        if (C->ysdev) cudaFree(C->ysdev);
+        C->xsdev = C->ysdev = nullptr;
+        C->xs_cap = 0;
+        SG_CUDA(cudaMalloc(&C->xsdev, need));
+        SG_CUDA(cudaMalloc(&C->ysdev, need));
+        C->xs_cap = need;
+    }
+    auto st = static_cast<cudaStream_t>(stream);
+    SG_CUDA(cudaMemcpyAsync(C->xsdev, xs_host, chain ? d * 4 : need, cudaMemcpyHostToDevice, st));
+    if (sg_status s = sg_ffn_forward_layers(C, layers, n, pipeline, C->xsdev, C->ysdev, chain, stream);
+        s != SG_OK)
+        return s;
+    SG_CUDA(cudaMemcpyAsync(ys_host, C->ysdev, need, cudaMemcpyDeviceToHost, st));
+    if (stats) return sg_ctx_read_stack_stats(C, stream, n, stats);
+    SG_CUDA(cudaStreamSynchronize(st));
+    return SG_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// synthetic.hpp:15-108
+// ---------------------------------------------------------------------------
+static double normal_quantile(double p) {
+    double z = 0.0;
+    for (int iter = 0; iter < 60; ++iter) {
+        const double cdf = 0.5 * std::erfc(-z / std::sqrt(2.0));
+        const double pdf = std::exp(-0.5 * z * z) / std::sqrt(2.0 * M_PI);
+        const double step = (cdf - p) / pdf;
+        z -= step;
+        if (std::abs(step) < 1e-14) break;
+    }
+    return z;
+}
+
+template <typename Sink>
+static sg_status synthetic_stream(int64_t hidden, int64_t inter, int64_t calib_tokens,
+                                  int64_t eval_tokens, double ns, uint64_t seed, Sink&& sink) {
+    if (hidden < 1 || inter < 1 || calib_tokens < 1 || eval_tokens < 0)
+        return fail(SG_ERR_DATA, "synthetic fixture: invalid sizes");
+    if (!(ns > 0.0 && ns < 1.0))
+        return fail(SG_ERR_DATA, "synthetic fixture: natural sparsity must lie in (0, 1)");
+    const auto d = static_cast<double>(hidden);
+    const double z = normal_quantile(ns);
+    double shift = z * std::sqrt(2.0);
+    shift = z * std::sqrt(2.0 + shift * shift / d);
+    std::mt19937_64 rng(seed);
+    const double means[5] = {-shift / d, 0.0, 0.0, 1.0, 1.0};
+    const double sds[5] = {1.0 / std::sqrt(d), 1.0 / std::sqrt(d),
+                           1.0 / std::sqrt(static_cast<double>(inter)), 1.0, 1.0};
+    const int64_t counts[5] = {inter * hidden, inter * hidden, hidden * inter,
+                               hidden * calib_tokens, hidden * eval_tokens};
+    for (int m = 0; m < 5; ++m) {
+        std::normal_distribution<double> dist(means[m], sds[m]);  // fresh per matrix
+        for (int64_t i = 0; i < counts[m]; ++i) sink(m, i, dist(rng));
+    }
+    return SG_OK;
+}
+
+extern "C" {
+
+sg_status sg_synthetic_fixture(int64_t hidden, int64_t inter, int64_t calib_tokens,
+                               int64_t eval_tokens, double ns, uint64_t seed, double* gate,
+                               double* up, double* down, double* calib, double* eval) {
+    double* outs[5] = {gate, up, down, calib, eval};
+    return synthetic_stream(hidden, inter, calib_tokens, eval_tokens, ns, seed,
+                            [&](int m, int64_t i, double v) {
+                                if (outs[m]) outs[m][i] = v;
+                            });
+}
+
+sg_status sg_synthetic_fixture_bf16(int64_t hidden, int64_t inter, int64_t calib_tokens,
+                                    int64_t eval_tokens, double ns, uint64_t seed, uint16_t* gate,
+                                    uint16_t* up, uint16_t* down_t, double* calib, double* eval) {
+    return synthetic_stream(hidden, inter, calib_tokens, eval_tokens, ns, seed,
+                            [&](int m, int64_t i, double v) {
+                                switch (m) {
+                                    case 0: if (gate) gate[i] = f32_to_bf16(static_cast<float>(v)); break;
+                                    case 1: if (up) up[i] = f32_to_bf16(static_cast<float>(v)); break;
+                                    case 2:
+                                        if (down_t) {  // down is hidden x inter: (j, n) -> down_t[n, j]
+                                            const int64_t j = i / inter, n = i % inter;
+                                            down_t[n * hidden + j] = f32_to_bf16(static_cast<float>(v));
+                                        }
+                                        break;
+                                    case 3: if (calib) calib[i] = v; break;
+                                    default: if (eval) eval[i] = v; break;
+                                }
+                            });
+}
+
+// ---------------------------------------------------------------------------
+// calibration.hpp:61-96 (build_instance) + :128-205 (greedy_calibrate)
+// ---------------------------------------------------------------------------
+sg_status sg_greedy_calibrate(const double* scores, const double* weights, int64_t D, int64_t T,
+                              int32_t eta, double target, double* bias, double* achieved,
+                              double* total_damage) {
+    if (scores == nullptr || weights == nullptr || bias == nullptr) return fail(SG_ERR_USAGE, "null argument");
+    if (D < 1 || T < 1) return fail(SG_ERR_DATA, "calibration instance: need at least one neuron and one sample");
+    if (eta < 1) return fail(SG_ERR_DATA, "calibration instance: eta must be >= 1");
+    for (int64_t i = 0; i < D * T; ++i)
+        if (weights[i] < 0.0) return fail(SG_ERR_DATA, "calibration instance: negative damage weight");
+    if (!(target > 0.0 && target <= 1.0)) return fail(SG_ERR_DATA, "target sparsity must lie in (0, 1]");
+    // build_instance: per-neuron stable co-sort by score; cumulative costs.
+    std::vector<double> ss(D * T), sw(D * T), cum(D * (T + 1));
+    par_for(D, [&](int64_t a, int64_t b) {
+        std::vector<int64_t> order(T);
+        for (int64_t i = a; i < b; ++i) {
+            std::iota(order.begin(), order.end(), int64_t{0});
+            const double* row = scores + i * T;
+            std::stable_sort(order.begin(), order.end(),
+                             [&](int64_t x, int64_t y) { return row[x] < row[y]; });
+            cum[i * (T + 1)] = 0.0;
+            for (int64_t k = 0; k < T; ++k) {
+                ss[i * T + k] = row[order[k]];
+                sw[i * T + k] = weights[i * T + order[k]];
+                cum[i * (T + 1) + k + 1] = cum[i * (T + 1) + k] + sw[i * T + k];
+            }
+        }
+    });
+    auto threshold_at = [&](int64_t i, int64_t k) {
+        return k == 0 ? -std::numeric_limits<double>::infinity() : ss[i * T + k - 1];
+    };
+    auto realized_drops = [&](int64_t i, double tau) {
+        const double* row = ss.data() + i * T;
+        return static_cast<int64_t>(std::upper_bound(row, row + T, tau) - row);
+    };
+    const double total = static_cast<double>(D) * static_cast<double>(T);
+    std::vector<int64_t> k(D, 0), realized(D, 0);
+    int64_t realized_total = 0;
+    for (int64_t i = 0; i < D; ++i) {
+        int64_t fr = 0;
+        while (fr < T && sw[i * T + fr] == 0.0) ++fr;
+        k[i] = fr;
+        realized[i] = realized_drops(i, threshold_at(i, fr));
+        realized_total += realized[i];
+    }
+    auto increment = [&](int64_t i) {
+        const int64_t cur = k[i];
+        const int64_t next = std::min<int64_t>(cur + eta, T);
+        return cum[i * (T + 1) + next] - cum[i * (T + 1) + cur];
+    };
+    using HeapEntry = std::tuple<double, int64_t, int64_t>;
+    std::priority_queue<HeapEntry, std::vector<HeapEntry>, std::greater<>> heap;
+    for (int64_t i = 0; i < D; ++i)
+        if (k[i] < T) heap.emplace(increment(i), i, k[i]);
+    while (static_cast<double>(realized_total) / total < target) {
+        int64_t chosen = -1;
+        while (!heap.empty()) {
+            const auto [inc, i, snap] = heap.top();
+            (void)inc;
+            heap.pop();
+            if (snap != k[i]) continue;
+            chosen = i;
+            break;
+        }
+        if (chosen < 0) {
+            return fail(SG_ERR_PROPERTY,
+                        "greedy calibration ran out of samples before the target; this state "
+                        "should be unreachable");
+        }
+        int64_t& ptr = k[chosen];
+        ptr = std::min<int64_t>(ptr + eta, T);
+        const int64_t nr = realized_drops(chosen, threshold_at(chosen, ptr));
+        realized_total += nr - realized[chosen];
+        realized[chosen] = nr;
+        if (ptr < T) heap.emplace(increment(chosen), chosen, ptr);
+    }
+    double dmg = 0.0;
+    for (int64_t i = 0; i < D; ++i) {
+        bias[i] = -threshold_at(i, k[i]);
+        dmg += cum[i * (T + 1) + k[i]];
+    }
+    if (achieved) *achieved = static_cast<double>(realized_total) / total;
+    if (total_damage) *total_damage = dmg;
+    return SG_OK;
+}
+
+}  // extern "C"

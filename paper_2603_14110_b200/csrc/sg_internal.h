@@ -1,0 +1,69 @@
+// Internal declarations shared by the host ABI (sg_host.cpp) and the device
+// code (sg_kernels.cu). Not part of the public ABI (include/sparsegate_c.h).
+#pragma once
+
+#include <cstdint>
+
+namespace sg {
+
+// Device-resident layer (one shard). All matrices bf16 (uint16 bit patterns),
+// rows padded with zeros to a pitch that is a multiple of 64 elements (128 B)
+// so every row start is 128-B aligned for cp.async.bulk and LDG.128.
+struct LayerView {
+    int d;        // hidden
+    int D;        // local (shard) inter
+    int r;        // predictor rank (0 = dense-only layer)
+    int pitch_d;  // round_up(d, 64)
+    int pitch_r;  // round_up(r, 64)
+    int act;      // 0 ReGLU, 1 dReLU
+    int gbase;    // global index of local neuron k = gbase + k * gstride
+    int gstride;
+    const uint16_t* B;     // r x pitch_d        (reference Predictor::B, types.hpp:75)
+    const uint16_t* A;     // D x pitch_r        (reference Predictor::A, types.hpp:74)
+    const float* bias;     // D                  (types.hpp:76, +inf kept)
+    const uint16_t* gate;  // D x pitch_d        (types.hpp:22)
+    const uint16_t* ud;    // D x 2*pitch_d : row k = [up_k | down_k] (down neuron-major)
+};
+
+// Per-context device workspace (one per stream). Sizes are bounded by the
+// ctx's max_inter (Dmax), max_hidden (pitch) and the SM count (G).
+struct WorkView {
+    const float* x;       // [d] input (caller's device buffer)
+    float* y;             // [d] output (caller's device buffer)
+    float* t;             // [pitch_r] predictor low-rank activations
+    int* cnt;             // [2*G] per-CTA counts: predicted, survivors
+    int* plist;           // [Dmax] per-CTA local predicted lists at neuron-range offsets
+    int* P;               // [Dmax] compacted GLOBAL predicted indices, by P position
+    int* Pl;              // [Dmax] compacted LOCAL predicted indices, by P position
+    float* gP;            // [Dmax] gate pre-activation, by P position
+    int* surv;            // [Dmax] survivor flag, by P position
+    float* zP;            // [Dmax] gated value, by P position
+    int* vlist;           // [Dmax] per-CTA local survivor lists at item-range offsets
+    float* zlist;         // [Dmax]
+    int* V;               // [Dmax] compacted GLOBAL survivor indices
+    float* zV;            // [Dmax] gated value per survivor
+    float* zD;            // [Dmax] dense pipeline: z per neuron
+    float* ypart;         // [G * pitch_dmax] phase-D partial column slices
+    unsigned* slice_ctr;  // [nslices_max] arrival counters (self-resetting)
+    unsigned* bar;        // [32] grid barrier {count, generation}
+    int* stats;           // [4] p, v, nonfinite(x), pipeline
+};
+
+struct LaunchInfo {
+    int num_sms;
+    int max_smem;  // opt-in dynamic shared memory per block
+};
+
+// Launch one layer of the given pipeline (0 dense, 1 parallel, 2 sequential)
+// on `stream`. Returns a cudaError_t value.
+int launch_layer(const LayerView& L, const WorkView& W, int pipeline, int num_ctas, void* stream);
+// Predictor only: t and per-neuron mask bytes into mask_out (device, D bytes).
+int launch_predict(const LayerView& L, const WorkView& W, uint8_t* mask_out, int num_ctas,
+                   void* stream);
+// Multi-layer: runs n layers (device array of LayerView) inside one persistent launch.
+int launch_layers(const LayerView* layers_dev, int n, const LayerView& first, const WorkView& W,
+                  const float* xs, float* ys, int chain, int pitch_stride, int pipeline,
+                  int num_ctas, void* stream);
+int query_launch_info(int device, LaunchInfo* info);
+
+}  // namespace sg

@@ -1,0 +1,102 @@
+"""Multi-layer synthetic decode models for the bench (host-side setup only).
+
+A "model" is a stack of L sparse-FFN layers of one BASELINE.json shape, each
+built exactly as SURVEY.md §8(d) prescribes:
+  * weights: make_synthetic_fixture{hidden=d, inter=D, natural_sparsity=0.9,
+    activation, seed=base+ℓ} (synthetic.hpp:80-108), emitted as bf16 with
+    `down` neuron-major;
+  * predictor: rank-r truncated SVD of W_gate (naive mode, factorization.hpp:93-144
+    with S = I) by a seeded randomized range finder, then greedy bias
+    calibration (calibration.hpp:61-205) on the fixture's calibration tokens to
+    predicted sparsity s, η = 8;
+  * input token of layer ℓ: eval token 0 of layer ℓ's fixture (N(1,1), bf16-exact).
+None of this is timed; it produces the resident inputs of the timed executor.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from .ffn_exec import Activation, DeviceLayer, bf16_to_f64, round_bf16
+from .offline import _randomized_svd, greedy_calibrate
+from .synthetic import SyntheticConfig, make_synthetic_bf16
+
+CONFIGS = {
+    # BASELINE.json configs[0]: one 7B-shape layer (the CPU-reference case)
+    "1layer": dict(d=4096, D=11008, L=1, act=0, model="single ReGLU FFN layer d=4096 d_ff=11008"),
+    # configs[1]: the headline
+    "7b": dict(d=4096, D=11008, L=32, act=0, model="ProSparse-Llama2-7B FFN stack"),
+    # configs[2]
+    "mistral": dict(d=4096, D=14336, L=32, act=1, model="TurboSparse-Mistral-7B FFN stack (dReLU)"),
+    # configs[3]
+    "13b": dict(d=5120, D=13824, L=40, act=0, model="ProSparse-Llama2-13B FFN stack"),
+    # small, for smoke tests
+    "tiny": dict(d=512, D=1408, L=4, act=0, model="tiny test stack"),
+}
+
+
+@dataclass
+class HostLayer:
+    gate: np.ndarray   # uint16 D x d
+    up: np.ndarray     # uint16 D x d
+    down_t: np.ndarray # uint16 D x d (neuron-major)
+    A: np.ndarray      # uint16 D x r
+    B: np.ndarray      # uint16 r x d
+    bias: np.ndarray   # f64 D (+inf allowed)
+    x: np.ndarray      # f64 d (eval token 0), bf16-exact
+    xs: np.ndarray     # f64 d x T eval tokens
+    calib_achieved: float = 0.0
+
+
+def build_host_layer(d, D, act, seed, rank=256, sparsity=0.5, calib_tokens=256, eval_tokens=16,
+                     eta=8, power_iters=1) -> HostLayer:
+    fx = make_synthetic_bf16(SyntheticConfig(hidden=d, inter=D, calib_tokens=calib_tokens,
+                                             eval_tokens=eval_tokens, activation=Activation(act),
+                                             seed=seed))
+    G = bf16_to_f64(fx["gate"]).astype(np.float32)
+    U, s, Vt = _randomized_svd(G, rank, oversample=8, power_iters=power_iters, seed=seed)
+    A = (U * s[None, :]).astype(np.float64)
+    B = Vt.astype(np.float64)
+    # the executor sees bf16 factors; calibrate the bias on exactly those
+    Aq = bf16_to_f64(round_bf16(A)).astype(np.float32)
+    Bq = bf16_to_f64(round_bf16(B)).astype(np.float32)
+    Xc = bf16_to_f64(round_bf16(fx["calib"])).astype(np.float32)
+    scores = (Aq @ (Bq @ Xc)).astype(np.float64)
+    gp = G @ Xc
+    up = bf16_to_f64(fx["up"]).astype(np.float32) @ Xc
+    if act == 1:
+        inner = np.maximum(gp, 0) * np.maximum(up, 0)
+    else:
+        inner = np.maximum(gp, 0) * up
+    dn = bf16_to_f64(fx["down_t"])
+    down_norm2 = np.sum(dn * dn, axis=1)
+    weights = (inner.astype(np.float64) ** 2) * down_norm2[:, None]
+    cal = greedy_calibrate(scores, weights, eta, sparsity)
+    ev = bf16_to_f64(round_bf16(fx["eval"]))
+    return HostLayer(fx["gate"], fx["up"], fx["down_t"], round_bf16(A), round_bf16(B), cal.bias,
+                     ev[:, 0].copy(), ev, cal.achieved_sparsity)
+
+
+def build_host_model(config: str, layers: int = None, seed_base: int = 0, rank: int = 256,
+                     sparsity: float = 0.5, workers: int = None, log=None):
+    cfg = CONFIGS[config]
+    L = layers or cfg["L"]
+    workers = workers or max(1, min(L, (os.cpu_count() or 4) // 2))
+    out = [None] * L
+    with cf.ThreadPoolExecutor(workers) as ex:
+        futs = {ex.submit(build_host_layer, cfg["d"], cfg["D"], cfg["act"], seed_base + l, rank,
+                          sparsity): l for l in range(L)}
+        for f in cf.as_completed(futs):
+            out[futs[f]] = f.result()
+            if log:
+                log(f"layer {futs[f]} ready")
+    return cfg, out
+
+
+def upload(host: HostLayer, d, D, act, rank=256, device=0, shard_index=0, shard_count=1):
+    raw = dict(hidden=d, inter=D, rank=rank, activation=act, gate=host.gate, up=host.up,
+               down_t=host.down_t, A=host.A, B=host.B, bias=host.bias)
+    return DeviceLayer(raw=raw, device=device, shard_index=shard_index, shard_count=shard_count)

@@ -1,0 +1,264 @@
+"""GPU parity: the CUDA executor (through the C ABI) vs the f64 oracle.
+
+Ports the executor tests of /root/reference/proj/tests/ffn_exec_tests.cpp to the
+GPU under the parity rules of tests/parity_util.py, plus GPU-only properties
+(run-to-run bit identity, sequential == parallel bitwise, edge shapes).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2603_14110_b200 import (Activation, DataError, DeviceLayer, FfnWeights, Pipeline,
+                                   Predictor, dense_ffn, predict_mask, read_sets,
+                                   sparse_ffn_parallel, sparse_ffn_sequential)
+from paper_2603_14110_b200.offline import (build_predictor, damage_weights, greedy_calibrate,
+                                           proxy_scores)
+from paper_2603_14110_b200.synthetic import SyntheticConfig, make_synthetic_fixture
+from parity_util import Y_RTOL, check_token, q_bf16, q_f32, quantize_layer
+
+pytestmark = pytest.mark.gpu
+
+
+def random_ffn(rng, d, D, act=Activation.ReGLU):
+    return FfnWeights(rng.standard_normal((D, d)), rng.standard_normal((D, d)),
+                      rng.standard_normal((d, D)), act)
+
+
+def exact_predictor(w):  # ffn_exec_tests.cpp:26-35
+    d = w.hidden_size()
+    return Predictor(w.gate.copy(), np.eye(d), np.zeros(w.inter_size()), d)
+
+
+def constant_bias_predictor(w, b):  # ffn_exec_tests.cpp:37-41
+    p = exact_predictor(w)
+    p.bias = np.full(w.inter_size(), b)
+    return p
+
+
+# ---- ffn_exec_tests.cpp:51-82 ------------------------------------------------
+def test_dense_2x2_known_answer():
+    w = FfnWeights(np.array([[1.0, 0.0], [-1.0, 0.0]]), np.eye(2), np.eye(2))
+    r = dense_ffn(w, [1.0, 1.0])
+    assert r.y[0] == 1.0 and r.y[1] == 0.0
+    assert r.stats.multiplies == 12 and r.stats.pipeline == Pipeline.Dense
+    assert np.all(dense_ffn(w, np.zeros(2)).y == 0.0)
+    with pytest.raises(DataError):
+        dense_ffn(w, [1.0, np.nan])
+    w2 = FfnWeights(w.gate, np.array([[-1.0, 0.0], [0.0, 1.0]]), np.eye(2))
+    assert dense_ffn(w2, [1.0, 1.0]).y[0] == -1.0
+    w3 = FfnWeights(w.gate, w2.up, np.eye(2), Activation.DReLU)
+    assert dense_ffn(w3, [1.0, 1.0]).y[0] == 0.0
+
+
+# ---- ffn_exec_tests.cpp:84-122 -----------------------------------------------
+def test_exact_predictor_mask_is_gate_support():
+    rng = np.random.default_rng(13)
+    w = random_ffn(rng, 8, 24)
+    pred = exact_predictor(w)
+    gq = q_bf16(w.gate)
+    for _ in range(10):
+        x = rng.standard_normal(8)
+        m = predict_mask(pred, x)
+        g = gq @ q_f32(x)
+        scale = np.abs(gq) @ np.abs(q_f32(x))
+        differ = np.nonzero(m.active.astype(bool) != (g > 0))[0]
+        assert all(abs(g[i]) <= 2.0 ** -14 * scale[i] for i in differ)
+        assert m.predicted_active_count == int(m.active.sum())
+        # on the GPU the mask and the revalidation use the same dot: V == mask
+        r = sparse_ffn_sequential(w, pred, x)
+        assert r.stats.revalidated == r.stats.predicted_active == m.predicted_active_count
+
+
+def test_zero_preactivation_is_inactive():
+    pred = Predictor(np.array([[1.0, -1.0], [1.0, 0.0]]), np.eye(2), np.zeros(2), 2)
+    m = predict_mask(pred, [1.0, 1.0])
+    assert list(m.active) == [0, 1] and m.predicted_active_count == 1
+
+
+def test_constant_bias_all_on_all_off():
+    rng = np.random.default_rng(14)
+    w = random_ffn(rng, 8, 24)
+    x = rng.standard_normal(8)
+    assert predict_mask(constant_bias_predictor(w, 1e12), x).predicted_active_count == 24
+    assert predict_mask(constant_bias_predictor(w, -1e12), x).predicted_active_count == 0
+
+
+def test_infinite_bias_activates():
+    rng = np.random.default_rng(15)
+    w = random_ffn(rng, 16, 40)
+    p = exact_predictor(w)
+    p.bias[::3] = np.inf
+    x = rng.standard_normal(16)
+    m = predict_mask(p, x)
+    assert np.all(m.active[::3] == 1)
+
+
+# ---- ffn_exec_tests.cpp:124-153 ----------------------------------------------
+@pytest.mark.parametrize("act", [Activation.ReGLU, Activation.DReLU])
+def test_all_active_sparse_matches_dense(act):
+    rng = np.random.default_rng(29)
+    w = random_ffn(rng, 16, 48, act)
+    on = constant_bias_predictor(w, 1e12)
+    for _ in range(5):
+        x = rng.standard_normal(16)
+        dn = dense_ffn(w, x)
+        par = sparse_ffn_parallel(w, on, x)
+        seq = sparse_ffn_sequential(w, on, x)
+        assert np.array_equal(par.y, seq.y)  # same mask -> bit-identical
+        nrm = max(np.linalg.norm(dn.y), 1e-30)
+        assert np.linalg.norm(seq.y - dn.y) <= 1e-5 * nrm
+
+
+def test_all_inactive_zero_output_and_predictor_cost():
+    rng = np.random.default_rng(31)
+    w = random_ffn(rng, 8, 24)
+    off = constant_bias_predictor(w, -1e12)
+    x = rng.standard_normal(8)
+    for run in (sparse_ffn_parallel, sparse_ffn_sequential):
+        r = run(w, off, x)
+        assert np.all(r.y == 0.0)
+        assert r.stats.multiplies == 8 * (8 + 24)
+        assert r.stats.predicted_sparsity == 1.0 and r.stats.realized_sparsity == 1.0
+
+
+# ---- ffn_exec_tests.cpp:155-204 ----------------------------------------------
+def test_perfect_recall_matches_dense():
+    rng = np.random.default_rng(37)
+    for trial in range(20):
+        act = Activation.ReGLU if trial % 2 == 0 else Activation.DReLU
+        w = random_ffn(rng, 12, 40, act)
+        pred = exact_predictor(w)
+        x = rng.standard_normal(12)
+        dn = dense_ffn(w, x)
+        for run in (sparse_ffn_parallel, sparse_ffn_sequential):
+            r = run(w, pred, x)
+            assert np.linalg.norm(r.y - dn.y) <= 1e-5 * max(np.linalg.norm(dn.y), 1e-30)
+
+
+def test_revalidation_filters_false_positives():
+    rng = np.random.default_rng(41)
+    w = random_ffn(rng, 8, 32)
+    on = constant_bias_predictor(w, 1e12)
+    x = rng.standard_normal(8)
+    par = sparse_ffn_parallel(w, on, x)
+    seq = sparse_ffn_sequential(w, on, x)
+    assert np.array_equal(seq.y, par.y)
+    support = int(((q_bf16(w.gate) @ q_f32(x)) > 0).sum())
+    assert support < 32
+    assert seq.stats.realized_sparsity > seq.stats.predicted_sparsity
+    assert seq.stats.multiplies < par.stats.multiplies
+    assert seq.stats.multiplies == 8 * (8 + 32) + 8 * 32 + 2 * 8 * support
+
+
+def test_realized_dominates_predicted():
+    rng = np.random.default_rng(43)
+    for _ in range(20):
+        w = random_ffn(rng, 8, 24)
+        p = exact_predictor(w)
+        p.bias = rng.standard_normal(24)
+        r = sparse_ffn_sequential(w, p, rng.standard_normal(8))
+        assert r.stats.realized_sparsity >= r.stats.predicted_sparsity
+
+
+# ---- ffn_exec_tests.cpp:232-254: determinism --------------------------------
+def test_repeated_calls_bit_identical():
+    rng = np.random.default_rng(53)
+    w = random_ffn(rng, 16, 64)
+    p = exact_predictor(w)
+    p.bias = rng.standard_normal(64)
+    x = rng.standard_normal(16)
+    for run in (dense_ffn, lambda w_, x_: sparse_ffn_parallel(w_, p, x_),
+                lambda w_, x_: sparse_ffn_sequential(w_, p, x_)):
+        a, b = run(w, x), run(w, x)
+        assert np.array_equal(a.y, b.y) and a.stats == b.stats
+    assert np.array_equal(sparse_ffn_parallel(w, p, x).y, sparse_ffn_sequential(w, p, x).y)
+
+
+# ---- oracle parity on calibrated synthetic layers ---------------------------
+def _calibrated_layer(d, D, r, seed, s=0.5, act=Activation.ReGLU, calib=512, mode="whitened"):
+    fx = make_synthetic_fixture(SyntheticConfig(hidden=d, inter=D, calib_tokens=calib,
+                                                eval_tokens=8, activation=act, seed=seed))
+    built = build_predictor(fx.weights.gate, fx.calib, r, mode=mode,
+                            svd="exact" if D * d <= 4_000_000 else "randomized")
+    pred = built.predictor
+    cal = greedy_calibrate(proxy_scores(pred, fx.calib), damage_weights(fx.weights, fx.calib),
+                           8, s)
+    pred.bias = cal.bias
+    return fx, pred
+
+
+@pytest.mark.parametrize("d,D,r,act", [
+    (64, 256, 16, Activation.ReGLU),
+    (64, 256, 16, Activation.DReLU),
+    (200, 700, 24, Activation.ReGLU),     # ragged: d, D not multiples of 8/64
+    (512, 2048, 64, Activation.ReGLU),
+    (1024, 2816, 128, Activation.DReLU),
+])
+def test_oracle_parity_calibrated(d, D, r, act):
+    fx, pred = _calibrated_layer(d, D, r, seed=d + D, act=act,
+                                 calib=max(512, 2 * d), mode="whitened")
+    layer = DeviceLayer(fx.weights, pred)
+    q = quantize_layer(fx.weights.gate, fx.weights.up, fx.weights.down, pred.A, pred.B, pred.bias)
+    ctx = layer.context()
+    worst = 0.0
+    for t in range(fx.eval.shape[1]):
+        x = fx.eval[:, t]
+        res = layer.forward(x, Pipeline.Sequential, ctx)
+        P, V, _, _ = read_sets(ctx, layer.local_inter)
+        diag = check_token(q, x, res.y, P, V, act=int(act))
+        worst = max(worst, diag["rel"])
+        st = res.stats
+        assert st.predicted_active == len(P) and st.revalidated == len(V)
+        assert st.multiplies == r * (d + D) + d * len(P) + 2 * d * len(V)
+        if diag["dP"] == 0 and diag["dV"] == 0:
+            o = diag["oracle"].stats
+            assert st.multiplies == o.multiplies
+            assert st.predicted_sparsity == o.predicted_sparsity
+            assert st.realized_sparsity == o.realized_sparsity
+    assert worst <= Y_RTOL
+
+
+def test_predict_mask_matches_oracle():
+    fx, pred = _calibrated_layer(256, 1024, 32, seed=7)
+    q = quantize_layer(fx.weights.gate, fx.weights.up, fx.weights.down, pred.A, pred.B, pred.bias)
+    layer = DeviceLayer(None, pred)
+    for t in range(fx.eval.shape[1]):
+        x = q_f32(fx.eval[:, t])
+        m = layer.predict_mask(x)
+        mo, co, pre = O.predict_mask(q["A"], q["B"], q["bias"], x)
+        ps, _ = O.threshold_scales(q["A"], q["B"], q["bias"], q["gate"], x)
+        diff = np.nonzero(m.active != mo)[0]
+        assert all(abs(pre[i]) <= 2.0 ** -14 * ps[i] for i in diff)
+        if len(diff) == 0:
+            assert m.predicted_active_count == co
+
+
+def test_x_length_and_nonfinite_rejected():
+    fx, pred = _calibrated_layer(64, 256, 8, seed=3)
+    with pytest.raises(DataError):
+        sparse_ffn_sequential(fx.weights, pred, np.ones(63))
+    bad = np.ones(64)
+    bad[5] = np.inf
+    with pytest.raises(DataError):
+        sparse_ffn_sequential(fx.weights, pred, bad)
+    with pytest.raises(DataError):
+        predict_mask(pred, np.ones(65))
+
+
+def test_nonfinite_weights_rejected_at_upload():
+    rng = np.random.default_rng(5)
+    w = random_ffn(rng, 8, 16)
+    w.up[3, 2] = np.nan
+    with pytest.raises(DataError):
+        DeviceLayer(w, None)
+
+
+def test_sequential_equals_parallel_bitwise_on_calibrated():
+    fx, pred = _calibrated_layer(512, 2048, 64, seed=11)
+    layer = DeviceLayer(fx.weights, pred)
+    for t in range(4):
+        x = fx.eval[:, t]
+        a = layer.forward(x, Pipeline.Sequential)
+        b = layer.forward(x, Pipeline.Parallel)
+        assert np.array_equal(a.y, b.y)
+        assert b.stats.multiplies == 64 * (512 + 2048) + 3 * 512 * a.stats.predicted_active
