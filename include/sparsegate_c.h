@@ -170,6 +170,14 @@ sg_status sg_ffn_forward_layers_host(sg_ctx* ctx, const sg_layer* const* layers,
 /* Synchronises, then returns per-layer stats of the last sg_ffn_forward_layers* call. */
 sg_status sg_ctx_read_stack_stats(sg_ctx* ctx, void* stream, int32_t n, sg_exec_stats* stats);
 
+/* Diagnostics: record per-CTA %globaltimer stamps at every phase boundary of
+ * the executor (up to 32 stamps per CTA per layer) for up to
+ * max_layers layers of each subsequent call; max_layers = 0 disables. */
+sg_status sg_ctx_enable_phase_timing(sg_ctx* ctx, int32_t max_layers);
+/* Synchronises and copies n_layers x num_ctas x 32 stamps (ns); *num_ctas = grid size. */
+sg_status sg_ctx_read_phase_timing(sg_ctx* ctx, void* stream, int32_t n_layers, uint64_t* out,
+                                   int32_t* num_ctas);
+
 /* ffn_exec.hpp:229-244, pure host. */
 sg_status sg_op_count_model(int64_t d, int64_t D, int64_t r, double s, double s_prime,
                             int64_t* dense, double* sparse, double* ratio);

@@ -74,6 +74,8 @@ SYMBOLS = [
     ("sg_ffn_forward_layers_host", C.c_int, [_VP, _VP, _I32, C.c_int, _VP, _VP, _I32,
                                              C.POINTER(sg_exec_stats), _VP]),
     ("sg_ctx_read_stack_stats", C.c_int, [_VP, _VP, _I32, C.POINTER(sg_exec_stats)]),
+    ("sg_ctx_enable_phase_timing", C.c_int, [_VP, _I32]),
+    ("sg_ctx_read_phase_timing", C.c_int, [_VP, _VP, _I32, _VP, C.POINTER(_I32)]),
     ("sg_op_count_model", C.c_int, [_I64, _I64, _I64, _D, _D, C.POINTER(_I64), C.POINTER(_D),
                                     C.POINTER(_D)]),
     ("sg_round_bf16", None, [_VP, _VP, _I64]),

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <limits>
@@ -63,6 +64,8 @@ struct sg_ctx {
     float* xsdev = nullptr;  // host-entry staging for stacks
     float* ysdev = nullptr;
     size_t xs_cap = 0;
+    uint64_t* dbgdev = nullptr;
+    int dbg_layers = 0;
 };
 
 constexpr int kMaxStackLayers = 1024;
@@ -410,7 +413,6 @@ sg_status sg_ctx_create(int32_t device, int64_t max_hidden, int64_t max_inter, i
     C->pitch_rmax = round_up(C->max_r, 64);
     const int G = C->G;
     const size_t Dm = static_cast<size_t>(max_inter) + 32;
-    const int nslices = C->pitch_dmax / 256 + 2;
     // carve one allocation (256-B aligned pieces)
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -418,15 +420,14 @@ sg_status sg_ctx_create(int32_t device, int64_t max_hidden, int64_t max_inter, i
         off += (bytes + 255) / 256 * 256;
         return o;
     };
-    const size_t o_t = take(C->pitch_rmax * 4);
-    const size_t o_cnt = take(2 * G * 4);
-    const size_t o_plist = take(Dm * 4), o_P = take(Dm * 4), o_Pl = take(Dm * 4);
-    const size_t o_gP = take(Dm * 4), o_surv = take(Dm * 4), o_zP = take(Dm * 4);
-    const size_t o_vlist = take(Dm * 4), o_zlist = take(Dm * 4), o_V = take(Dm * 4);
-    const size_t o_zV = take(Dm * 4), o_zD = take(Dm * 4);
+    const size_t o_t = take(C->pitch_rmax * 32);  // one 32-B sector per t value
+    const size_t o_cnt = take(2 * G * 32);  // one 32-B sector per CTA count
+    const size_t o_plist = take(Dm * 4), o_P = take(Dm * 4), o_gP = take(Dm * 4);
+    const size_t o_rec = take(Dm * 8), o_V = take(Dm * 4), o_zV = take(Dm * 4);
+    const size_t o_vseg = take(Dm * 8);
+    const size_t o_zD = take(Dm * 4);
     const size_t o_ypart = take(static_cast<size_t>(G) * C->pitch_dmax * 4);
-    const size_t o_slice = take(nslices * 4);
-    const size_t o_bar = take(32 * 4);
+    const size_t o_bar = take(8 * 256);
     const size_t o_stats = take(4 * 4 * kMaxStackLayers);
     const size_t o_x = take(C->pitch_dmax * 4), o_y = take(C->pitch_dmax * 4);
     const size_t o_mask = take(Dm);
@@ -446,19 +447,16 @@ sg_status sg_ctx_create(int32_t device, int64_t max_hidden, int64_t max_inter, i
     W.cnt = reinterpret_cast<int*>(b + o_cnt);
     W.plist = reinterpret_cast<int*>(b + o_plist);
     W.P = reinterpret_cast<int*>(b + o_P);
-    W.Pl = reinterpret_cast<int*>(b + o_Pl);
     W.gP = reinterpret_cast<float*>(b + o_gP);
-    W.surv = reinterpret_cast<int*>(b + o_surv);
-    W.zP = reinterpret_cast<float*>(b + o_zP);
-    W.vlist = reinterpret_cast<int*>(b + o_vlist);
-    W.zlist = reinterpret_cast<float*>(b + o_zlist);
+    W.rec = reinterpret_cast<int*>(b + o_rec);
+    W.vseg = reinterpret_cast<int*>(b + o_vseg);
     W.V = reinterpret_cast<int*>(b + o_V);
     W.zV = reinterpret_cast<float*>(b + o_zV);
     W.zD = reinterpret_cast<float*>(b + o_zD);
     W.ypart = reinterpret_cast<float*>(b + o_ypart);
-    W.slice_ctr = reinterpret_cast<unsigned*>(b + o_slice);
-    W.bar = reinterpret_cast<unsigned*>(b + o_bar);
+    W.bar = reinterpret_cast<unsigned long long*>(b + o_bar);
     W.stats = reinterpret_cast<int*>(b + o_stats);
+    if (const char* f = std::getenv("SG_FLAGS")) W.flags = std::atoi(f);
     C->xdev = reinterpret_cast<float*>(b + o_x);
     C->ydev = reinterpret_cast<float*>(b + o_y);
     C->maskdev = reinterpret_cast<uint8_t*>(b + o_mask);
@@ -475,6 +473,7 @@ sg_status sg_ctx_destroy(sg_ctx* C) {
     if (C->stackdev) cudaFree(C->stackdev);
     if (C->xsdev) cudaFree(C->xsdev);
     if (C->ysdev) cudaFree(C->ysdev);
+    if (C->dbgdev) cudaFree(C->dbgdev);
     delete C;
     return SG_OK;
 }
@@ -620,6 +619,34 @@ sg_status sg_ffn_forward_layers(sg_ctx* C, const sg_layer* const* layers, int32_
     C->last_layer = layers[n - 1];
     C->last_pipeline = pipeline;
     C->last_stack.assign(layers, layers + n);
+    return SG_OK;
+}
+
+sg_status sg_ctx_enable_phase_timing(sg_ctx* C, int32_t max_layers) {
+    if (C == nullptr || max_layers < 0) return fail(SG_ERR_USAGE, "bad arguments");
+    DeviceGuard dg(C->device);
+    if (C->dbgdev) cudaFree(C->dbgdev);
+    C->dbgdev = nullptr;
+    C->dbg_layers = 0;
+    C->W.dbg = nullptr;
+    if (max_layers == 0) return SG_OK;
+    const size_t bytes = static_cast<size_t>(max_layers) * C->G * 32 * 8;
+    SG_CUDA(cudaMalloc(&C->dbgdev, bytes));
+    SG_CUDA(cudaMemset(C->dbgdev, 0, bytes));
+    C->dbg_layers = max_layers;
+    C->W.dbg = C->dbgdev;
+    return SG_OK;
+}
+
+sg_status sg_ctx_read_phase_timing(sg_ctx* C, void* stream, int32_t n, uint64_t* out,
+                                   int32_t* num_ctas) {
+    if (C == nullptr || out == nullptr || n < 1 || n > C->dbg_layers)
+        return fail(SG_ERR_USAGE, "phase timing not enabled for that many layers");
+    DeviceGuard dg(C->device);
+    SG_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    SG_CUDA(cudaMemcpy(out, C->dbgdev, static_cast<size_t>(n) * C->G * 32 * 8,
+                       cudaMemcpyDeviceToHost));
+    if (num_ctas) *num_ctas = C->G;
     return SG_OK;
 }
 

@@ -31,22 +31,23 @@ struct WorkView {
     const float* x;       // [d] input (caller's device buffer)
     float* y;             // [d] output (caller's device buffer)
     float* t;             // [pitch_r] predictor low-rank activations
-    int* cnt;             // [2*G] per-CTA counts: predicted, survivors
+    int* cnt;             // [2*gpad] per-CTA predicted counts, then survivor counts
     int* plist;           // [Dmax] per-CTA local predicted lists at neuron-range offsets
     int* P;               // [Dmax] compacted GLOBAL predicted indices, by P position
-    int* Pl;              // [Dmax] compacted LOCAL predicted indices, by P position
     float* gP;            // [Dmax] gate pre-activation, by P position
-    int* surv;            // [Dmax] survivor flag, by P position
-    float* zP;            // [Dmax] gated value, by P position
-    int* vlist;           // [Dmax] per-CTA local survivor lists at item-range offsets
-    float* zlist;         // [Dmax]
+    int* rec;             // [2*Dmax] int2 {local neuron or -1, z bits}, by P position
+    int* vseg;            // [2*Dmax] int2 per-CTA survivor segments at item-range offsets
     int* V;               // [Dmax] compacted GLOBAL survivor indices
     float* zV;            // [Dmax] gated value per survivor
     float* zD;            // [Dmax] dense pipeline: z per neuron
-    float* ypart;         // [G * pitch_dmax] phase-D partial column slices
-    unsigned* slice_ctr;  // [nslices_max] arrival counters (self-resetting)
-    unsigned* bar;        // [32] grid barrier {count, generation}
-    int* stats;           // [4] p, v, nonfinite(x), pipeline
+    float* ypart;         // [G * pitch_dmax] dense pipeline: per-CTA partial outputs
+    unsigned long long* bar;  // 8 grid-barrier counters, 256 B apart (see grid_barrier)
+    int* stats;           // [4 per layer] p, v, nonfinite(x), pipeline
+    uint64_t* dbg;        // optional [layers][G][16] globaltimer phase stamps (or null)
+    int flags;            // experiment switches (SG_FLAGS env, default 0): 1 gate-row L2
+                          // prefetch in phase B, 2 no survivor-row L2 prefetch,
+                          // 16/32 phase-B ablations, 64 LSU prefetch, bits 8-15:
+                          // consumer-group override
 };
 
 struct LaunchInfo {

@@ -4,29 +4,35 @@
 // the five stages of the reference's sequential pipeline
 // (/root/reference/proj/include/sparsegate/ffn_exec.hpp:183-218):
 //
-//   phase A  stage 1a  t = B·x                       (ffn_exec.hpp:133-136)
+//   start    cp.async.bulk: this CTA's rows of B and its slice of A -> smem
+//            (weights only; overlaps the previous layer's tail and barrier)
+//   phase A  stage 1a  t = B·x  (rows j ≡ c mod G)      (ffn_exec.hpp:133-136)
 //            --- grid barrier ---
-//   phase B  stage 1b  pre = A·t + bias > 0 -> mask  (ffn_exec.hpp:139-144)
-//            stage 2   per-CTA warp-ballot compaction (ffn_exec.hpp:189-195)
+//   phase B  stage 1b  pre = A·t + bias > 0 -> mask   (ffn_exec.hpp:139-144)
+//            stage 2   warp-ballot compaction          (ffn_exec.hpp:189-195)
+//            + L2 prefetch of this CTA's predicted gate rows (speculation-free:
+//              every predicted row is prefetched exactly once, by its owner)
 //            --- grid barrier ---
-//   phase C  stage 3   gather-GEMV over predicted gate rows, staged into a
-//                      shared-memory ring by cp.async.bulk (TMA bulk engine) +
-//                      mbarriers; revalidation g > 0      (ffn_exec.hpp:196-201)
-//            stage 4   survivors only: up row -> z = gated(g, u) (ffn_exec.hpp:202-203, :68-76)
-//            second compaction (survivor list)
+//   phase C  P prefix; balanced split of P over CTAs;
+//            stage 3   gate rows -> smem ring (cp.async.bulk + mbarriers),
+//                      g = gate·x, revalidation g > 0   (ffn_exec.hpp:196-201)
+//            stage 4   survivors: up row (LDG) -> z = gated(g, u)   (:202-203, :68-76)
+//                      + L2 prefetch of the survivor's down row
 //            --- grid barrier ---
-//   phase D  stage 5   down projection over neuron-major rows, column-sliced
-//                      with a fixed-order cross-CTA reduction (ffn_exec.hpp:80-94)
+//   phase D  survivor list compaction (ballot, in P order = ascending neuron)
+//            stage 5   y = Σ z·down_row, column-sliced: each CTA owns a few
+//                      16-B column chunks and reduces them over all survivors
+//                      in a fixed order                (ffn_exec.hpp:80-94)
 //
-// Dense (ffn_exec.hpp:103-122) and parallel (ffn_exec.hpp:149-178) pipelines
-// reuse phases C/D with gate+up rows fetched together.
+// Dense (ffn_exec.hpp:103-122) and parallel (:149-178) pipelines reuse phases
+// C/D with gate+up rows fetched together.
 //
 // Determinism: no floating-point atomics. Every dot product has a fixed lane
-// -> chunk assignment and a fixed shuffle tree, so a given row gives the same
-// bits whichever CTA/warp computes it; the down projection sums each column
-// in a fixed order over (survivor position, warp, group). Repeated calls are
-// bit-identical, and the sequential and parallel pipelines are bit-identical
-// on the same mask (the reference's determinism contract, ffn_exec.hpp:3-15).
+// -> chunk assignment and a fixed shuffle tree, so a row gives the same bits
+// whichever CTA/warp computes it; the down projection sums each column in a
+// fixed order over survivor positions. Repeated calls are bit-identical, and
+// the sequential and parallel pipelines are bit-identical on the same mask
+// (the reference's determinism contract, ffn_exec.hpp:3-15).
 #include "sg_internal.h"
 
 #include <cuda_runtime.h>
@@ -36,29 +42,83 @@
 namespace sg {
 namespace {
 
-constexpr int kWarps = 16;                  // compute warps
-constexpr int kCThreads = kWarps * 32;      // 512 compute threads
-constexpr int kThreads = kCThreads + 32;    // + one producer warp (cp.async.bulk issue)
-constexpr int kMaxSlots = 32;               // ring slots (upper bound)
-constexpr int kSliceChunks = 32;            // phase D: 32 lanes x 16 B
-constexpr int kSliceCols = kSliceChunks * 8;  // = 256 output columns per slice
-constexpr int kRowsA = 4;                   // phase A rows reduced per pass
+constexpr int kWarps = 16;                // compute warps
+constexpr int kCThreads = kWarps * 32;    // 512 compute threads
+constexpr int kThreads = kCThreads + 32;  // + one producer warp (cp.async.bulk issue)
+constexpr int kMaxSlots = 32;             // ring slots (upper bound)
+constexpr int kRowsA = 4;                 // phase A rows reduced per pass
+constexpr int kGroupWarps = 4;            // phase C: a row is reduced by a group of 4 warps
+constexpr int kGroups = kWarps / kGroupWarps;
+constexpr int kGroupThreads = kGroupWarps * 32;
+constexpr int kXRegChunks = 4;            // x chunks per thread held in registers (pitch_d <= 4096)
 
+// Shared memory: small fixed arrays, then one large region that is, in turn,
+// the B/A staging buffer (phases A/B), the cp.async.bulk ring (phase C) and
+// the survivor list + reduction scratch (phase D) — never live at once.
 struct SmemPlan {
-    int off_slotn;  // int[kMaxSlots]
-    int off_off;    // int[G+1]   P prefix
-    int off_voff;   // int[G+1]   V prefix
-    int off_red;    // float[kWarps*32*8]
-    int off_mask;   // uint8[mask_cap]
+    int off_slotn;  // int[kMaxSlots]   neuron of each ring slot
+    int off_off;    // int[G+1]         P prefix over CTAs
+    int off_mask;   // uint8[mask_cap]  phase B mask bytes
+    int off_bias;   // float[mask_cap]  this CTA's bias slice (cp.async at layer start)
+    int off_misc;   // int[32]          block-level scalars / warp counts
+    int off_reda;   // float[kRowsA*kWarps]
+    int off_items;  // int[item_cap]    this CTA's phase-C neurons
     int off_xs;     // float[pitch_d]
     int off_ts;     // float[pitch_r]
-    int off_as;     // uint16[as_cap]
-    int off_ring;   // ns * slot_bytes
-    int ns;
+    int off_big;
+    int big_bytes;
+    int ns;          // ring slots, a multiple of kc
+    int kc;          // consumer groups; slot s is always consumed by group s % kc
     int slot_bytes;
-    int as_cap_bytes;
+    int stage_b;     // B rows of this CTA staged in smem (phase A)
+    int as_bytes;    // A slice capacity in smem (0 = stream A from HBM)
+    int list_cap;    // phase D survivor-list capacity (entries)
     int mask_cap;
+    int item_cap;
     int total;
+};
+
+struct Smem {
+    uint64_t* full;
+    uint64_t* empty;
+    uint64_t* abar;
+    int* slotn;
+    int* off;
+    uint8_t* mask;
+    float* bias;
+    int* misc;
+    float* reda;
+    int* items;
+    float* xs;
+    float* ts;
+    uint8_t* big;
+};
+
+__device__ __forceinline__ Smem carve(uint8_t* base, const SmemPlan& S) {
+    Smem m;
+    m.full = reinterpret_cast<uint64_t*>(base);
+    m.empty = m.full + kMaxSlots;
+    m.abar = m.empty + kMaxSlots;
+    m.slotn = reinterpret_cast<int*>(base + S.off_slotn);
+    m.off = reinterpret_cast<int*>(base + S.off_off);
+    m.mask = base + S.off_mask;
+    m.bias = reinterpret_cast<float*>(base + S.off_bias);
+    m.misc = reinterpret_cast<int*>(base + S.off_misc);
+    m.reda = reinterpret_cast<float*>(base + S.off_reda);
+    m.items = reinterpret_cast<int*>(base + S.off_items);
+    m.xs = reinterpret_cast<float*>(base + S.off_xs);
+    m.ts = reinterpret_cast<float*>(base + S.off_ts);
+    m.big = base + S.off_big;
+    return m;
+}
+
+// Per-thread persistent state across phases/layers (identical in all threads
+// of a CTA except the barrier fields, which only thread 0 uses).
+struct RunState {
+    uint32_t seq;       // items pushed through the ring so far (this launch)
+    uint32_t auses;     // staging-barrier phases consumed so far
+    uint64_t bar_base;  // grid-barrier counter value at launch start (thread 0)
+    uint32_t bar_k;     // grid barriers passed in this launch (thread 0)
 };
 
 // ---------------------------------------------------------------------------
@@ -73,6 +133,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
@@ -100,6 +163,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+// Bulk prefetch of a contiguous global range into L2 (no smem, no completion).
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -113,13 +187,18 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
                  : "l"(p));
     return r;
 }
-__device__ __forceinline__ uint32_t ld_acquire(const unsigned* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ uint64_t ld_acquire_u64(const unsigned long long* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release(unsigned* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void red_release_add_u64(unsigned long long* p, uint64_t v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
 }
 
 // 8 bf16 weights (one 16-B chunk) against 8 fp32 activations, in element order.
@@ -188,6 +267,100 @@ __device__ __forceinline__ void row_dot2(const uint16_t* r0, const uint16_t* r1,
     o1 = warp_sum(a1);
 }
 
+// ---- phase C row dot: a group of 4 warps (128 threads) per row ----------
+// Thread gt of a group owns chunks gt, gt+128, ... of every row and keeps the
+// matching x values in registers, so the per-row shared-memory traffic is the
+// row itself only. Row value = (thread chain over its chunks, ascending)
+// -> warp butterfly -> the 4 warps summed in order: fixed, so a row gives the
+// same bits from smem or global and in any group.
+struct XRegs {
+    float v[kXRegChunks][8];
+};
+__device__ __forceinline__ void load_xregs(const float* xs, int nch, int gt, XRegs& X) {
+#pragma unroll
+    for (int k = 0; k < kXRegChunks; ++k) {
+        const int ch = gt + k * kGroupThreads;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) X.v[k][e] = ch < nch ? xs[ch * 8 + e] : 0.f;
+    }
+}
+__device__ __forceinline__ float dot8r(const uint4 w, const float* x, float acc) {
+    acc = fmaf(__uint_as_float(w.x << 16), x[0], acc);
+    acc = fmaf(__uint_as_float(w.x & 0xffff0000u), x[1], acc);
+    acc = fmaf(__uint_as_float(w.y << 16), x[2], acc);
+    acc = fmaf(__uint_as_float(w.y & 0xffff0000u), x[3], acc);
+    acc = fmaf(__uint_as_float(w.z << 16), x[4], acc);
+    acc = fmaf(__uint_as_float(w.z & 0xffff0000u), x[5], acc);
+    acc = fmaf(__uint_as_float(w.w << 16), x[6], acc);
+    acc = fmaf(__uint_as_float(w.w & 0xffff0000u), x[7], acc);
+    return acc;
+}
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+// kRows rows from smem (kSmem) or global, sharing the x registers; red is this
+// group's scratch [2 parities][kGroupWarps][4]; par alternates per call.
+template <bool kSmem, int kRows>
+__device__ __forceinline__ void group_dot(const uint16_t* const* rows, const XRegs& X,
+                                          const float* xs, int nch, int gt, int grp, float* red,
+                                          int& par, float* out) {
+    float acc[kRows];
+#pragma unroll
+    for (int q = 0; q < kRows; ++q) acc[q] = 0.f;
+    if (kSmem) {
+#pragma unroll
+        for (int k = 0; k < kXRegChunks; ++k) {
+            const int ch = gt + k * kGroupThreads;
+            if (ch < nch) {
+#pragma unroll
+                for (int q = 0; q < kRows; ++q)
+                    acc[q] = dot8r(*reinterpret_cast<const uint4*>(rows[q] + ch * 8), X.v[k], acc[q]);
+            }
+        }
+    } else {
+        uint4 w[kRows][kXRegChunks];
+#pragma unroll
+        for (int q = 0; q < kRows; ++q)
+#pragma unroll
+            for (int k = 0; k < kXRegChunks; ++k) {
+                const int ch = gt + k * kGroupThreads;
+                w[q][k] = ch < nch ? ldg_stream(rows[q] + ch * 8) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+        for (int q = 0; q < kRows; ++q)
+#pragma unroll
+            for (int k = 0; k < kXRegChunks; ++k)
+                if (gt + k * kGroupThreads < nch) acc[q] = dot8r(w[q][k], X.v[k], acc[q]);
+    }
+    // chunks beyond the register window (pitch_d > 4096): x from smem
+    for (int ch = gt + kXRegChunks * kGroupThreads; ch < nch; ch += kGroupThreads) {
+#pragma unroll
+        for (int q = 0; q < kRows; ++q) {
+            const uint4 w0 = kSmem ? *reinterpret_cast<const uint4*>(rows[q] + ch * 8)
+                                   : ldg_stream(rows[q] + ch * 8);
+            acc[q] = dot8(w0, xs + ch * 8, acc[q]);
+        }
+    }
+    const int gw = (gt >> 5), lane = gt & 31;
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1)
+#pragma unroll
+        for (int q = 0; q < kRows; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], m);
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < kRows; ++q) red[(par * kGroupWarps + gw) * 4 + q] = acc[q];
+    }
+    named_bar(1 + grp, kGroupThreads);
+#pragma unroll
+    for (int q = 0; q < kRows; ++q) {
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < kGroupWarps; ++w) s += red[(par * kGroupWarps + w) * 4 + q];
+        out[q] = s;
+    }
+    par ^= 1;
+}
+
 // ffn_exec.hpp:68-76 in fp32 (canonical +0 when suppressed).
 __device__ __forceinline__ float gated(float g, float u, int act) {
     if (!(g > 0.f)) return 0.f;
@@ -195,44 +368,107 @@ __device__ __forceinline__ float gated(float g, float u, int act) {
     return g * u;
 }
 
+// Values exchanged between CTAs through global memory (per-CTA counts, the
+// predictor's t) are written as whole 32-B sectors, one sector per value: a
+// 4-B store into a sector that other SMs also write leaves it partially
+// written in L2, and the first read then stalls for microseconds (measured
+// ~6 us for the P-count prefix; tools/phase_profile.py).
+constexpr int kSector = 8;  // ints per 32-B sector
+__device__ __forceinline__ void st_sector(int* p, int v) {
+    asm volatile("st.global.v4.b32 [%0], {%1, %2, %2, %2};\n\tst.global.v4.b32 [%0+16], {%2, %2, %2, %2};"
+                 ::"l"(p), "r"(v), "r"(0) : "memory");
+}
+__device__ __forceinline__ int gpad() { return static_cast<int>(gridDim.x) * kSector; }
+
 __device__ __forceinline__ int split_lo(int c, int G, int n) {
     return static_cast<int>((static_cast<long long>(c) * n) / G);
 }
 
-// Sense-free grid barrier (count returns to 0, generation advances). All CTAs
-// are co-resident (cooperative launch, one CTA per SM).
-__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+// Grid barrier on kBarCounters monotonically increasing 64-bit counters
+// (each in its own 256-B block, so they live in different L2 slices). CTA c
+// arrives on counter c % kBarCounters; every barrier adds exactly n_j to
+// counter j, so between barriers counter j is a multiple of n_j and each
+// launch recovers its base as floor(v / n_j) * n_j even if early CTAs already
+// arrived. No reset, no generation flag. Split phase: grid_arrive() publishes
+// this CTA's writes, grid_wait() returns once every CTA has arrived; work that
+// does not depend on other CTAs may run in between. All CTAs are co-resident
+// (cooperative launch, one per SM).
+constexpr int kBarCounters = 8;
+constexpr int kBarStride = 32;  // u64 elements between counters (256 B)
+
+__device__ __forceinline__ int bar_share(int j) {  // CTAs arriving on counter j
+    return (static_cast<int>(gridDim.x) - j + kBarCounters - 1) / kBarCounters;
+}
+__device__ __forceinline__ void grid_barrier_init(const WorkView& W, RunState& rs) {
+    if (threadIdx.x < kBarCounters) {
+        const int n = bar_share(threadIdx.x);
+        const uint64_t v = ld_acquire_u64(W.bar + threadIdx.x * kBarStride);
+        rs.bar_base = n > 0 ? v - v % n : v;
+    }
+    if (threadIdx.x < 32) __syncwarp();
+    rs.bar_k = 0;
+}
+__device__ __forceinline__ void grid_arrive(const WorkView& W, RunState& rs) {
     __syncthreads();
+    rs.bar_k += 1;
     if (threadIdx.x == 0) {
-        const uint32_t gen = ld_acquire(bar + 1);
         __threadfence();
-        const unsigned arrived = atomicAdd(bar, 1u);
-        if (arrived == gridDim.x - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            st_release(bar + 1, gen + 1);
-        } else {
-            while (ld_acquire(bar + 1) == gen) {
+        red_release_add_u64(W.bar + (blockIdx.x % kBarCounters) * kBarStride, 1ull);
+    }
+}
+__device__ __forceinline__ void grid_wait(const WorkView& W, RunState& rs) {
+    if (threadIdx.x < 32) {
+        if (threadIdx.x < kBarCounters) {
+            const int j = threadIdx.x;
+            const uint64_t target = rs.bar_base + static_cast<uint64_t>(rs.bar_k) *
+                                                      static_cast<uint64_t>(bar_share(j));
+            while (ld_acquire_u64(W.bar + j * kBarStride) < target) {
             }
         }
-        __threadfence();
+        // the lanes left the spin at different times: reconverge warp 0, or it
+        // stays split and every later shuffle of this warp takes the slow path
+        __syncwarp();
     }
     __syncthreads();
 }
+__device__ __forceinline__ void grid_barrier(const WorkView& W, RunState& rs) {
+    grid_arrive(W, rs);
+    grid_wait(W, rs);
+}
 
-// Exclusive prefix of cnt[0..G) into off[0..G], off[G] = total. Warp 0 only.
+// Exclusive prefix of cnt[0..G) into off[0..G], off[G] = total. One warp.
+// All loads are issued before the scan (one L2 round trip for G <= 256).
+constexpr int kMaxPrefixChunks = 8;
 __device__ __forceinline__ void warp_prefix(const int* cnt, int* off, int G, int lane) {
+    int v[kMaxPrefixChunks];
+#pragma unroll
+    for (int k = 0; k < kMaxPrefixChunks; ++k) {
+        const int i = k * 32 + lane;
+        v[k] = i < G ? __ldcg(cnt + i * kSector) : 0;
+    }
     int carry = 0;
-    for (int base = 0; base < G; base += 32) {
-        const int i = base + lane;
-        const int v = i < G ? __ldcg(cnt + i) : 0;
-        int incl = v;
+#pragma unroll
+    for (int k = 0; k < kMaxPrefixChunks; ++k) {
+        const int i = k * 32 + lane;
+        int incl = v[k];
 #pragma unroll
         for (int m = 1; m < 32; m <<= 1) {
             const int o = __shfl_up_sync(0xffffffffu, incl, m);
             if (lane >= m) incl += o;
         }
-        if (i < G) off[i] = carry + incl - v;
+        if (i < G) off[i] = carry + incl - v[k];
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    for (int base = kMaxPrefixChunks * 32; base < G; base += 32) {
+        const int i = base + lane;
+        const int x = i < G ? __ldcg(cnt + i * kSector) : 0;
+        int incl = x;
+#pragma unroll
+        for (int m = 1; m < 32; m <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, incl, m);
+            if (lane >= m) incl += o;
+        }
+        if (i < G) off[i] = carry + incl - x;
         carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (lane == 0) off[G] = carry;
@@ -240,7 +476,7 @@ __device__ __forceinline__ void warp_prefix(const int* cnt, int* off, int G, int
 
 // Owner CTA s of list position pos: off[s] <= pos < off[s+1] (off ascending).
 __device__ __forceinline__ int owner_of(const int* off, int G, int pos) {
-    int lo = 0, hi = G;  // off[lo] <= pos < off[hi]
+    int lo = 0, hi = G;
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
         if (off[mid] <= pos) lo = mid; else hi = mid;
@@ -248,52 +484,55 @@ __device__ __forceinline__ int owner_of(const int* off, int G, int pos) {
     return lo;
 }
 
-struct Smem {
-    uint64_t* full;
-    uint64_t* empty;
-    uint64_t* abar;
-    int* slotn;
-    int* off;
-    int* voff;
-    float* red;
-    uint8_t* mask;
-    float* xs;
-    float* ts;
-    uint16_t* as;
-    uint8_t* ring;
-};
-
-__device__ __forceinline__ Smem carve(uint8_t* base, const SmemPlan& S) {
-    Smem m;
-    m.full = reinterpret_cast<uint64_t*>(base);
-    m.empty = m.full + kMaxSlots;
-    m.abar = m.empty + kMaxSlots;
-    m.slotn = reinterpret_cast<int*>(base + S.off_slotn);
-    m.off = reinterpret_cast<int*>(base + S.off_off);
-    m.voff = reinterpret_cast<int*>(base + S.off_voff);
-    m.red = reinterpret_cast<float*>(base + S.off_red);
-    m.mask = base + S.off_mask;
-    m.xs = reinterpret_cast<float*>(base + S.off_xs);
-    m.ts = reinterpret_cast<float*>(base + S.off_ts);
-    m.as = reinterpret_cast<uint16_t*>(base + S.off_as);
-    m.ring = base + S.off_ring;
-    return m;
+// The bias slice of this CTA: one 4-B cp.async per neuron (waited on in phase B).
+__device__ __forceinline__ void stage_bias(const LayerView& L, const Smem& sm) {
+    const int G = gridDim.x, c = blockIdx.x;
+    const int n0 = split_lo(c, G, L.D), n1 = split_lo(c + 1, G, L.D);
+    for (int k = threadIdx.x; k < n1 - n0; k += kThreads) cp_async4(sm.bias + k, L.bias + n0 + k);
 }
 
-// Per-CTA persistent pipeline state (identical in every thread of the CTA).
-struct RingState {
-    uint32_t seq;   // items pushed through the ring so far (this launch)
-    uint32_t auses; // A-slice barrier uses so far
-};
+// ---------------------------------------------------------------------------
+// Layer start: stage this CTA's B rows and A slice into smem (weights only).
+// Returns whether a staging-barrier phase was issued.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool stage_weights(const LayerView& L, const Smem& sm,
+                                              const SmemPlan& S, bool use_as) {
+    const int G = gridDim.x, c = blockIdx.x;
+    const int n0 = split_lo(c, G, L.D), n1 = split_lo(c + 1, G, L.D);
+    const int nB = c < L.r ? (L.r - c + G - 1) / G : 0;
+    const uint32_t row_bytes = static_cast<uint32_t>(L.pitch_d) * 2u;
+    const uint32_t bytesB = S.stage_b ? static_cast<uint32_t>(nB) * row_bytes : 0u;
+    const uint32_t bytesA = use_as ? static_cast<uint32_t>(n1 - n0) * L.pitch_r * 2u : 0u;
+    stage_bias(L, sm);
+    if (bytesA + bytesB == 0) return false;
+    if ((threadIdx.x >> 5) == kWarps) {
+        const int lane = threadIdx.x & 31;
+        fence_proxy_async();  // WAR vs. the previous layer's generic reads of this region
+        const uint64_t pol = policy_evict_first();
+        if (lane == 0) mbar_expect_tx(sm.abar, bytesA + bytesB);
+        __syncwarp();
+        for (int q = lane; q < nB && bytesB; q += 31)
+            bulk_g2s(sm.big + static_cast<size_t>(q) * row_bytes,
+                     L.B + static_cast<size_t>(c + q * G) * L.pitch_d, row_bytes, sm.abar, pol);
+        if (bytesA && lane == 31)
+            bulk_g2s(sm.big + bytesB, L.A + static_cast<size_t>(n0) * L.pitch_r, bytesA, sm.abar,
+                     pol);
+        __syncwarp();
+    }
+    return true;
+}
 
 // ---------------------------------------------------------------------------
-// Phase A: t = B·x (fp32), rows j = c, c+G, ... ; block-reduced in fixed order.
+// Phase A: t = B·x (fp32), rows j = c + q*G ; block-reduced in fixed order.
 // ---------------------------------------------------------------------------
-__device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm) {
+__device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm,
+                        const SmemPlan& S) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int nch = L.pitch_d >> 3;
-    for (int j0 = c; j0 < L.r; j0 += kRowsA * G) {
+    const int nB = c < L.r ? (L.r - c + G - 1) / G : 0;
+    const uint16_t* bs = reinterpret_cast<const uint16_t*>(sm.big);
+    for (int q0 = 0; q0 < nB; q0 += kRowsA) {
         float acc[kRowsA];
 #pragma unroll
         for (int q = 0; q < kRowsA; ++q) acc[q] = 0.f;
@@ -302,9 +541,16 @@ __device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm) {
                 uint4 w[kRowsA];
 #pragma unroll
                 for (int q = 0; q < kRowsA; ++q) {
-                    const int j = j0 + q * G;
-                    w[q] = j < L.r ? ldg_stream(L.B + static_cast<size_t>(j) * L.pitch_d + ch * 8)
-                                   : make_uint4(0, 0, 0, 0);
+                    const int qq = q0 + q;
+                    if (qq >= nB) {
+                        w[q] = make_uint4(0, 0, 0, 0);
+                    } else if (S.stage_b) {
+                        w[q] = *reinterpret_cast<const uint4*>(
+                            bs + static_cast<size_t>(qq) * L.pitch_d + ch * 8);
+                    } else {
+                        w[q] = ldg_stream(L.B + static_cast<size_t>(c + qq * G) * L.pitch_d +
+                                          ch * 8);
+                    }
                 }
 #pragma unroll
                 for (int q = 0; q < kRowsA; ++q) acc[q] = dot8(w[q], sm.xs + ch * 8, acc[q]);
@@ -312,58 +558,73 @@ __device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm) {
 #pragma unroll
             for (int q = 0; q < kRowsA; ++q) {
                 const float s = warp_sum(acc[q]);
-                if (lane == 0) sm.red[q * kWarps + warp] = s;
+                if (lane == 0) sm.reda[q * kWarps + warp] = s;
             }
         }
         __syncthreads();
-        if (tid < kRowsA) {
-            const int j = j0 + tid * G;
-            if (j < L.r) {
-                float s = 0.f;
-                for (int w = 0; w < kWarps; ++w) s += sm.red[tid * kWarps + w];
-                W.t[j] = s;
-            }
+        if (tid < kRowsA && q0 + tid < nB) {
+            float s = 0.f;
+            for (int w = 0; w < kWarps; ++w) s += sm.reda[tid * kWarps + w];
+            st_sector(reinterpret_cast<int*>(W.t) + (c + (q0 + tid) * G) * kSector, __float_as_int(s));
         }
         __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------------------
-// Phase B: mask over this CTA's neuron range + warp-ballot compaction.
+// Phase B: mask over this CTA's neuron range + warp-ballot compaction, and an
+// L2 prefetch of every predicted gate row it owns.
 // ---------------------------------------------------------------------------
-__device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm, bool use_as,
-                           RingState& rs, uint8_t* mask_out) {
+__device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm,
+                           const SmemPlan& S, bool use_as, uint8_t* mask_out, bool prefetch,
+                           bool staged_bias, uint64_t* dbg = nullptr) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int n0 = split_lo(c, G, L.D), n1 = split_lo(c + 1, G, L.D);
-    for (int i = tid; i < L.pitch_r; i += kThreads) sm.ts[i] = i < L.r ? __ldcg(W.t + i) : 0.f;
-    if (use_as && n1 > n0) {
-        mbar_wait(sm.abar, rs.auses & 1u);
-    }
-    if (n1 > n0) rs.auses += use_as ? 1u : 0u;
+    for (int i = tid; i < L.pitch_r; i += kThreads)
+        sm.ts[i] = i < L.r ? __ldcg(W.t + i * kSector) : 0.f;
+    (void)staged_bias;
+    cp_async_wait_all();
     __syncthreads();
+    if (dbg && tid == 0) dbg[11] = globaltimer();
+    const int nB = c < L.r ? (L.r - c + G - 1) / G : 0;
+    const uint16_t* as = reinterpret_cast<const uint16_t*>(
+        sm.big + (S.stage_b ? static_cast<size_t>(nB) * L.pitch_d * 2 : 0));
+    // 4 lanes per neuron, 128 neurons per pass; lane sub covers chunks
+    // sub + 4i, starting at i = (global index & 1) so the two neurons sharing a
+    // quarter-warp read different banks. Order fixed per neuron.
     const int nchr = L.pitch_r >> 3;
-    if (warp < kWarps) {
-        for (int n = n0 + warp; n < n1; n += kWarps) {
-            const uint16_t* arow = use_as ? sm.as + static_cast<size_t>(n - n0) * L.pitch_r
+    const int nq = nchr >> 2;  // chunks per lane (pitch_r >= 64 -> nq >= 2)
+    for (int base = 0; base < n1 - n0; base += kCThreads / 4) {
+        const int k = base + (tid >> 2), sub = tid & 3;
+        float acc = 0.f;
+        if (tid < kCThreads && k < n1 - n0 && !(W.flags & 16)) {
+            const int n = n0 + k;
+            const uint16_t* arow = use_as ? as + static_cast<size_t>(k) * L.pitch_r
                                           : L.A + static_cast<size_t>(n) * L.pitch_r;
-            float acc = 0.f;
-            for (int ch = lane; ch < nchr; ch += 32) {
+            const int rot = (L.gbase + n * L.gstride) & 1;
+            for (int i = 0; i < nq; ++i) {
+                int ii = i + rot;
+                if (ii >= nq) ii -= nq;
+                const int ch = sub + 4 * ii;
                 const uint4 w = use_as ? *reinterpret_cast<const uint4*>(arow + ch * 8)
                                        : ldg_stream(arow + ch * 8);
                 acc = dot8(w, sm.ts + ch * 8, acc);
             }
-            acc = warp_sum(acc);
-            if (lane == 0) {
-                const float pre = acc + __ldg(L.bias + n);
-                const uint8_t on = pre > 0.f ? 1 : 0;  // strict, ffn_exec.hpp:141
-                sm.mask[n - n0] = on;
-                if (mask_out) mask_out[n] = on;
-            }
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        if (tid < kCThreads && sub == 0 && k < n1 - n0) {
+            const float pre = acc + sm.bias[k];
+            const uint8_t on = pre > 0.f ? 1 : 0;  // strict, ffn_exec.hpp:141
+            sm.mask[k] = on;
+            if (mask_out) mask_out[n0 + k] = on;
         }
     }
     __syncthreads();
+    if (dbg && tid == 0) dbg[12] = globaltimer();
     if (warp == 0) {
+        const uint32_t row_bytes = static_cast<uint32_t>(L.pitch_d) * 2u;
         int run = 0;
         for (int base = 0; base < n1 - n0; base += 32) {
             const int k = base + lane;
@@ -372,7 +633,40 @@ __device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm
             if (on) W.plist[n0 + run + __popc(b & ((1u << lane) - 1u))] = n0 + k;
             run += __popc(b);
         }
-        if (lane == 0) W.cnt[c] = run;
+        if (lane == 0) {
+            st_sector(W.cnt + c * kSector, run);
+            sm.misc[0] = run;
+        }
+        (void)row_bytes;
+    }
+    (void)prefetch;
+}
+
+// L2 prefetch of this CTA's predicted gate rows (between grid_arrive and
+// grid_wait: the barrier latency streams the first rows of phase C). The
+// producer warp issues them; the CTA's local list is in plist at n0.
+__device__ __forceinline__ void prefetch_own_gate_rows(const LayerView& L, const WorkView& W,
+                                                       const Smem& sm) {
+    const int G = gridDim.x, c = blockIdx.x;
+    if ((threadIdx.x >> 5) != kWarps) return;
+    const int n0 = split_lo(c, G, L.D);
+    const int cnt = sm.misc[0];
+    const uint32_t row_bytes = static_cast<uint32_t>(L.pitch_d) * 2u;
+    for (int k = threadIdx.x & 31; k < cnt; k += 32)
+        prefetch_l2(L.gate + static_cast<size_t>(W.plist[n0 + k]) * L.pitch_d, row_bytes);
+}
+// Same, through the LSU: one prefetch.global.L2 per 128-B line, all threads.
+__device__ __forceinline__ void prefetch_own_gate_rows_lsu(const LayerView& L, const WorkView& W,
+                                                           const Smem& sm) {
+    const int G = gridDim.x, c = blockIdx.x;
+    const int n0 = split_lo(c, G, L.D);
+    const int cnt = sm.misc[0];
+    const int lines = L.pitch_d * 2 / 128;
+    for (int q = threadIdx.x; q < cnt * lines; q += kThreads) {
+        const int k = q / lines, ln = q % lines;
+        const char* a = reinterpret_cast<const char*>(L.gate + static_cast<size_t>(W.plist[n0 + k]) *
+                                                                   L.pitch_d) + ln * 128;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
     }
 }
 
@@ -382,10 +676,11 @@ __device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm
 //                         their up row directly (LDG) -> z.
 //   kPipe 1 (parallel):   items = P positions; slot = gate row + up row.
 //   kPipe 0 (dense):      items = neurons of this CTA's range; slot = gate + up.
+// Sparse pipelines write rec[pos] = {local neuron or -1, z} for phase D.
 // ---------------------------------------------------------------------------
 template <int kPipe>
 __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& sm,
-                             const SmemPlan& S, RingState& rs, int& i0_out, int& i1_out) {
+                             const SmemPlan& S, RunState& rs, uint64_t* dbg = nullptr) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int nch = L.pitch_d >> 3;
@@ -395,46 +690,82 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
         i0 = split_lo(c, G, L.D);
         i1 = split_lo(c + 1, G, L.D);
     } else {
-        if (warp == 0) warp_prefix(W.cnt, sm.off, G, lane);
+        if (warp == 0) {
+            const long long ck0 = clock64();
+            if (dbg && (W.flags & 4096)) {  // probe: an unrelated L2-resident read first
+                float a = __ldcg(W.t + lane * kSector) + __ldcg(W.t + (32 + lane) * kSector);
+                a = __reduce_add_sync(0xffffffffu, __float_as_int(a) & 1);
+                if (lane == 0) dbg[28] = globaltimer() + (a == -7.f ? 1 : 0);
+            }
+            if (W.flags & 512) {
+                // ablation: serial-chunk scan
+                int carry = 0;
+                for (int base = 0; base < G; base += 32) {
+                    const int i = base + lane;
+                    const int v = i < G ? __ldcg(W.cnt + i * kSector) : 0;
+                    int incl = v;
+                    for (int m = 1; m < 32; m <<= 1) {
+                        const int o = __shfl_up_sync(0xffffffffu, incl, m);
+                        if (lane >= m) incl += o;
+                    }
+                    if (i < G) sm.off[i] = carry + incl - v;
+                    carry += __shfl_sync(0xffffffffu, incl, 31);
+                }
+                if (lane == 0) sm.off[G] = carry;
+            } else {
+                warp_prefix(W.cnt, sm.off, G, lane);
+            }
+            if (dbg && lane == 0) {
+                dbg[26] = globaltimer();
+                dbg[30] = static_cast<uint64_t>(clock64() - ck0);
+            }
+            if (W.flags & 32768) {  // probe: the same code again (I-cache warm)
+                warp_prefix(W.cnt, sm.off, G, lane);
+                if (dbg && lane == 0) dbg[29] = globaltimer();
+            }
+            if (dbg && (W.flags & 4096)) {  // probe: a second round of the same loads
+                int acc = 0;
+                for (int i = lane; i < G; i += 32) acc += __ldcg(W.cnt + i * kSector);
+                acc = __reduce_add_sync(0xffffffffu, acc);
+                if (lane == 0) dbg[27] = globaltimer() + (acc == -7 ? 1 : 0);
+            }
+        }
         __syncthreads();
+        if (dbg && tid == 0) dbg[25] = globaltimer();
         const int p = sm.off[G];
         i0 = split_lo(c, G, p);
         i1 = split_lo(c + 1, G, p);
         if (c == 0 && tid == 0) W.stats[0] = p;
+        // resolve this CTA's items (one parallel round of L2 reads)
+        for (int j = tid; j < i1 - i0; j += kThreads) {
+            const int pos = i0 + j;
+            const int s = owner_of(sm.off, G, pos);
+            sm.items[j] = __ldcg(W.plist + split_lo(s, G, L.D) + (pos - sm.off[s]));
+        }
+        __syncthreads();
     }
-    i0_out = i0;
-    i1_out = i1;
+    if (dbg && tid == 0) dbg[16] = globaltimer();
     const int nitems = i1 - i0;
     const uint32_t seq0 = rs.seq;
     const int ns = S.ns;
 
     if (warp == kWarps) {
-        // ---- producer warp: one lane issues the bulk copies ----
-        if (lane == 0 && nitems > 0) {
-            const uint64_t pol = policy_evict_first();
-            int s = 0, k = 0;
-            if (kPipe != 0) {
-                s = owner_of(sm.off, G, i0);
-                k = i0 - sm.off[s];
-            }
-            for (int j = 0; j < nitems; ++j) {
-                int n;
-                if (kPipe == 0) {
-                    n = i0 + j;
-                } else {
-                    while (k >= sm.off[s + 1] - sm.off[s]) {
-                        ++s;
-                        k = 0;
-                    }
-                    n = __ldcg(W.plist + split_lo(s, G, L.D) + k);
-                    ++k;
-                }
-                const uint32_t q = seq0 + j;
-                const int slot = static_cast<int>(q % ns);
+        // ---- producer warp: lane s issues every item of ring slot s (s < ns),
+        // in order. One issuing thread per slot: a single thread issuing all
+        // cp.async.bulk copies caps an SM near 22 GB/s (tools/microbench_gather.cu).
+        uint64_t pol = policy_evict_first();
+        if (W.flags & 256) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+        const int slot = lane;
+        if (slot < ns && nitems > 0) {
+            // first q >= seq0 with q % ns == slot
+            uint32_t q = seq0 + static_cast<uint32_t>((slot - static_cast<int>(seq0 % ns) + ns) % ns);
+            for (; q < seq0 + static_cast<uint32_t>(nitems); q += ns) {
+                const int j = static_cast<int>(q - seq0);
+                const int n = kPipe == 0 ? i0 + j : sm.items[j];
                 const uint32_t use = q / ns;
-                if (use > 0) mbar_wait(sm.empty + slot, (use - 1) & 1u);
+                if (use > 0) mbar_wait(sm.empty + slot, (use - 1) & 1u);  // lanes independent
                 sm.slotn[slot] = n;
-                uint8_t* dst = sm.ring + static_cast<size_t>(slot) * S.slot_bytes;
+                uint8_t* dst = sm.big + static_cast<size_t>(slot) * S.slot_bytes;
                 if (kPipe == 2) {
                     mbar_expect_tx(sm.full + slot, row_bytes);
                     bulk_g2s(dst, L.gate + static_cast<size_t>(n) * L.pitch_d, row_bytes,
@@ -448,188 +779,288 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
                 }
             }
         }
+        __syncwarp();
     } else {
-        // ---- compute warps ----
-        for (int j = warp; j < nitems; j += kWarps) {
-            const uint32_t q = seq0 + j;
-            const int slot = static_cast<int>(q % ns);
-            mbar_wait(sm.full + slot, (q / ns) & 1u);
-            const int n = sm.slotn[slot];
-            const uint16_t* srow =
-                reinterpret_cast<const uint16_t*>(sm.ring + static_cast<size_t>(slot) * S.slot_bytes);
-            float g, u = 0.f;
-            if (kPipe == 2) {
-                g = row_dot<true>(srow, sm.xs, nch, lane);
-            } else {
-                row_dot2(srow, srow + L.pitch_d, sm.xs, nch, lane, g, u);
+        // ---- compute groups: group g < kc (4 warps) consumes the items
+        // q = seq0 + j with q % kc == g, in order. ns is a multiple of kc, so
+        // every slot is consumed by one group, phase after phase, and a parity
+        // wait can never run a phase ahead of the barrier.
+        const int kc = S.kc;
+        const int grp = warp / kGroupWarps, gt = tid % kGroupThreads;
+        XRegs X;
+        load_xregs(sm.xs, nch, gt, X);
+        float* red = sm.reda + grp * (2 * kGroupWarps * 4);
+        int par = 0;
+        int j0 = grp - static_cast<int>(seq0 % static_cast<uint32_t>(kc));
+        if (j0 < 0) j0 += kc;
+        // two items per iteration (j, j + kc): their dot chains, shuffles and
+        // the group barrier are shared, halving the per-row fixed cost
+        for (int j = j0; grp < kc && j < nitems; j += 2 * kc) {
+            const bool two = j + kc < nitems;
+            int slot[2], n[2];
+            const uint16_t* r[4];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int jj = two ? j + h * kc : j;
+                const uint32_t q = seq0 + jj;
+                slot[h] = static_cast<int>(q % ns);
+                if (h == 0 || two) mbar_wait(sm.full + slot[h], (q / ns) & 1u);
+                __syncwarp();  // lanes leave the spin at different times: reconverge
+                n[h] = sm.slotn[slot[h]];
+                const uint16_t* srow = reinterpret_cast<const uint16_t*>(
+                    sm.big + static_cast<size_t>(slot[h]) * S.slot_bytes);
+                r[2 * h] = srow;
+                r[2 * h + 1] = srow + L.pitch_d;
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(sm.empty + slot);  // slot free: reads are done
-            const int it = i0 + j;
-            if (kPipe == 0) {
-                if (lane == 0) W.zD[n] = gated(g, u, L.act);
+            if (dbg && gt == 0 && j == j0) dbg[17 + grp] = globaltimer();  // first row landed
+            float res[4] = {0.f, 0.f, 0.f, 0.f};
+            if (W.flags & 128) {
+                named_bar(1 + grp, kGroupThreads);  // ablation: no compute
+            } else if (kPipe == 2) {
+                const uint16_t* rr[2] = {r[0], r[2]};
+                float o[2];
+                group_dot<true, 2>(rr, X, sm.xs, nch, gt, grp, red, par, o);
+                res[0] = o[0];
+                res[2] = o[1];
             } else {
-                const bool sv = g > 0.f;  // revalidation, ffn_exec.hpp:200 (strict)
-                if (kPipe == 2 && sv) {
-                    u = row_dot<false>(L.ud + static_cast<size_t>(n) * 2 * L.pitch_d, sm.xs, nch,
-                                       lane);
+                group_dot<true, 4>(r, X, sm.xs, nch, gt, grp, red, par, res);
+            }
+            // the group barrier inside group_dot follows every read of the slots
+            if (gt == 0) {
+                mbar_arrive(sm.empty + slot[0]);
+                if (two) mbar_arrive(sm.empty + slot[1]);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (h == 1 && !two) break;
+                const int jj = j + h * kc;
+                const float g = res[2 * h];
+                const float u = res[2 * h + 1];
+                const int nn = n[h];
+                if (kPipe == 0) {
+                    if (gt == 0) W.zD[nn] = gated(g, u, L.act);
+                    continue;
                 }
-                if (lane == 0) {
-                    W.P[it] = L.gbase + n * L.gstride;
-                    W.Pl[it] = n;
+                const int it = i0 + jj;
+                const bool sv = g > 0.f;  // revalidation, ffn_exec.hpp:200 (strict)
+                // a survivor's [up | down] rows (16 KB, contiguous) go to L2 now, one
+                // 128-B line per thread of the group: stage 4 (sequential) and stage 5
+                // read them after the gate stream
+                if (sv && !(W.flags & 2) && gt * 128 < 4 * L.pitch_d) {
+                    const char* a = reinterpret_cast<const char*>(
+                                        L.ud + static_cast<size_t>(nn) * 2 * L.pitch_d) + gt * 128;
+                    for (int off = 0; off < 4 * L.pitch_d; off += kGroupThreads * 128)
+                        if (gt * 128 + off < 4 * L.pitch_d)
+                            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a + off));
+                }
+                if (gt == 0) {
+                    W.P[it] = L.gbase + nn * L.gstride;
                     W.gP[it] = g;
-                    W.surv[it] = sv ? 1 : 0;
-                    W.zP[it] = sv ? gated(g, u, L.act) : 0.f;
+                    int2 rec;
+                    rec.x = sv ? nn : -1;
+                    // sequential: carry g, z is formed in survivor_up(); parallel: z now
+                    rec.y = __float_as_int(kPipe == 2 ? g : (sv ? gated(g, u, L.act) : 0.f));
+                    reinterpret_cast<int2*>(W.rec)[it] = rec;
                 }
             }
         }
     }
+    if (dbg && tid < kCThreads && (tid % kGroupThreads) == 0) dbg[21 + tid / kGroupThreads] = globaltimer();
     rs.seq = seq0 + static_cast<uint32_t>(nitems > 0 ? nitems : 0);
     __syncthreads();
-    if (kPipe != 0 && warp == 0) {
-        // second compaction: survivors of this CTA's item range, in P order.
-        int run = 0;
-        for (int base = 0; base < nitems; base += 32) {
-            const int j = base + lane;
-            const bool on = j < nitems && W.surv[i0 + j] != 0;
-            const unsigned b = __ballot_sync(0xffffffffu, on);
-            if (on) {
-                const int dst = i0 + run + __popc(b & ((1u << lane) - 1u));
-                W.vlist[dst] = W.Pl[i0 + j];
-                W.zlist[dst] = W.zP[i0 + j];
+    if (kPipe != 0) {
+        // survivors of this CTA's item range, in P order -> smem list + global segment
+        int2* list = reinterpret_cast<int2*>(sm.big);
+        if (warp == 0) {
+            const int2* rec = reinterpret_cast<const int2*>(W.rec);
+            int run = 0;
+            for (int base = 0; base < nitems; base += 32) {
+                const int j = base + lane;
+                const int2 r = j < nitems ? rec[i0 + j] : make_int2(-1, 0);
+                const bool on = r.x >= 0;
+                const unsigned b = __ballot_sync(0xffffffffu, on);
+                if (on) {
+                    const int dst = run + __popc(b & ((1u << lane) - 1u));
+                    list[dst] = r;
+                    reinterpret_cast<int2*>(W.vseg)[i0 + dst] = r;
+                }
+                run += __popc(b);
             }
-            run += __popc(b);
+            if (lane == 0) {
+                sm.misc[1] = run;
+                st_sector(W.cnt + gpad() + c * kSector, run);
+                if (run) atomicAdd(W.stats + 1, run);  // v (integer: order-free)
+            }
         }
-        if (lane == 0) W.cnt[G + c] = run;
+        __syncthreads();
+    }
+}
+
+// Stage 4 of the sequential pipeline, per CTA, after its gate stream: the up
+// rows of this CTA's survivors (prefetched to L2 when each survivor was
+// found), 8 survivors per round, thread t owning chunks t, t+512, ...; each
+// u is reduced lane-chain -> warp butterfly -> 16 warps in order; then
+// z = gated(g, u) (ffn_exec.hpp:202-203, :68-76) replaces g in the list.
+constexpr int kSurvBatch = 8;
+__device__ void survivor_up(const LayerView& L, const WorkView& W, const Smem& sm, int i0) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nch = L.pitch_d >> 3;
+    int2* list = reinterpret_cast<int2*>(sm.big);
+    float* red = reinterpret_cast<float*>(sm.big + 64 * 1024);  // after the list (<= 8K entries)
+    const int cnt = sm.misc[1];
+    for (int b0 = 0; b0 < cnt; b0 += kSurvBatch) {
+        const int nb = cnt - b0 < kSurvBatch ? cnt - b0 : kSurvBatch;
+        float pu[kSurvBatch];
+#pragma unroll
+        for (int q = 0; q < kSurvBatch; ++q) pu[q] = 0.f;
+        if (tid < kCThreads) {
+            for (int ch = tid; ch < nch; ch += kCThreads) {
+                uint4 w[kSurvBatch];
+#pragma unroll
+                for (int q = 0; q < kSurvBatch; ++q)
+                    w[q] = q < nb ? ldg_stream(L.ud + static_cast<size_t>(list[b0 + q].x) * 2 *
+                                                          L.pitch_d + ch * 8)
+                                  : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int q = 0; q < kSurvBatch; ++q) pu[q] = dot8(w[q], sm.xs + ch * 8, pu[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < kSurvBatch; ++q) {
+                const float v = warp_sum(pu[q]);
+                if (lane == 0) red[q * kWarps + warp] = v;
+            }
+        }
+        __syncthreads();
+        if (tid < nb) {
+            float u = 0.f;
+            for (int w = 0; w < kWarps; ++w) u += red[tid * kWarps + w];
+            int2 e = list[b0 + tid];
+            e.y = __float_as_int(gated(__int_as_float(e.y), u, L.act));
+            list[b0 + tid] = e;
+            reinterpret_cast<int2*>(W.vseg)[i0 + b0 + tid] = e;
+        }
+        __syncthreads();
+    }
+}
+
+// Phase D, part 1 (no grid barrier: a CTA's rows are its own neurons/survivors):
+// partial y over this CTA's list, streaming whole down rows (thread t owns
+// chunks t, t+512, ...), rows in list order, kU rows in flight per thread.
+// Dense: the list is the CTA's neuron range with z from zD; sparse: the
+// survivor list built at the end of phase C (rows already prefetched to L2).
+template <int kPipe>
+__device__ void partial_down(const LayerView& L, const WorkView& W, const Smem& sm) {
+    const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
+    const int nch = L.pitch_d >> 3;
+    const int n0 = split_lo(c, G, L.D), n1 = split_lo(c + 1, G, L.D);
+    const int2* list = reinterpret_cast<const int2*>(sm.big);
+    float* zs = sm.bias;  // dense: z of this CTA's neurons (<= mask_cap)
+    int cnt;
+    if (kPipe == 0) {
+        cnt = n1 - n0;
+        for (int k = tid; k < cnt; k += kThreads) zs[k] = W.zD[n0 + k];
+        __syncthreads();
+    } else {
+        cnt = sm.misc[1];
+    }
+    constexpr int kU = kPipe == 0 ? 16 : 8;
+    for (int ch = tid; tid < kCThreads && ch < nch; ch += kCThreads) {
+        float acc[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+        const uint16_t* col = L.ud + L.pitch_d + static_cast<size_t>(ch) * 8;
+        for (int k = 0; k < cnt; k += kU) {
+            uint4 w[kU];
+            float z[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int kk = k + u;
+                int n = 0;
+                z[u] = 0.f;
+                if (kk < cnt) {
+                    if (kPipe == 0) {
+                        n = n0 + kk;
+                        z[u] = zs[kk];
+                    } else {
+                        const int2 e = list[kk];
+                        n = e.x;
+                        z[u] = __int_as_float(e.y);
+                    }
+                }
+                w[u] = kk < cnt ? ldg_stream(col + static_cast<size_t>(n) * 2 * L.pitch_d)
+                                : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) axpy8(w[u], z[u], acc);
+        }
+        float4* dst =
+            reinterpret_cast<float4*>(W.ypart + static_cast<size_t>(c) * L.pitch_d + ch * 8);
+        dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
     }
 }
 
 // ---------------------------------------------------------------------------
-// Phase D: y = sum over list positions of z * down_row, column-sliced.
-// Work item = (column slice of 256, position group q of Q). Each item is
-// reduced over its 16 warps in fixed order; the Q group partials of a slice are
-// summed in fixed q order by whichever CTA arrives last.
+// Phase D, part 2 (after a grid barrier): CTA c sums the G partials of its
+// column range in fixed order (contiguous groups of partials, then the
+// groups), and publishes its survivor segment of V.
 // ---------------------------------------------------------------------------
 template <int kPipe>
 __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm, float* y,
-                           int p_total_i0_unused) {
-    (void)p_total_i0_unused;
+                           uint64_t* dbg, bool want_sets) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const int nch = L.pitch_d >> 3;
-    int v;       // list length
-    int p = 0;   // P length (sparse)
-    if (kPipe == 0) {
-        v = L.D;
-    } else {
-        if (warp == 0) warp_prefix(W.cnt + G, sm.voff, G, lane);
-        __syncthreads();
-        v = sm.voff[G];
-        p = sm.off[G];
-        // publish this CTA's survivor segment as the compacted global V list
+    if (kPipe != 0 && want_sets && warp == kWarps) {
+        // V output: prefix over the per-CTA survivor counts, copy own segment
+        int* voff = sm.items;  // phase C is over; reuse (G+1 <= item_cap not assumed)
+        (void)voff;
+        int carry = 0, mine = 0;
+        const int p = sm.off[G];
+        for (int base = 0; base < G; base += 32) {
+            const int i = base + lane;
+            const int v = i < G ? __ldcg(W.cnt + gpad() + i * kSector) : 0;
+            int incl = v;
+#pragma unroll
+            for (int m = 1; m < 32; m <<= 1) {
+                const int o = __shfl_up_sync(0xffffffffu, incl, m);
+                if (lane >= m) incl += o;
+            }
+            if (i == c) mine = carry + incl - v;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        mine = __reduce_add_sync(0xffffffffu, mine);
         const int i0 = split_lo(c, G, p);
-        const int cntc = sm.voff[c + 1] - sm.voff[c];
-        for (int k = tid; k < cntc; k += kThreads) {
-            const int n = W.vlist[i0 + k];
-            W.V[sm.voff[c] + k] = L.gbase + n * L.gstride;
-            W.zV[sm.voff[c] + k] = W.zlist[i0 + k];
+        const int cntc = __ldcg(W.cnt + gpad() + c * kSector);
+        const int2* seg = reinterpret_cast<const int2*>(W.vseg) + i0;
+        for (int k = lane; k < cntc; k += 32) {
+            const int2 e = __ldcg(seg + k);
+            W.V[mine + k] = L.gbase + e.x * L.gstride;
+            W.zV[mine + k] = __int_as_float(e.y);
         }
-        if (c == 0 && tid == 0) W.stats[1] = v;
     }
-    const int nslices = (nch + kSliceChunks - 1) / kSliceChunks;
-    int Q = G / nslices;
-    if (Q < 1) Q = 1;
-    const int nitems = nslices * Q;
-    for (int item = c; item < nitems; item += G) {
-        const int slice = item % nslices;
-        const int q = item / nslices;
-        const int g0 = split_lo(q, Q, v), g1 = split_lo(q + 1, Q, v);
-        const int chunk = slice * kSliceChunks + lane;
-        const bool col_ok = chunk < nch;
-        float acc[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-        if (warp < kWarps) {
-            // positions handled by this warp: g0 + warp + 16*k
-            for (int pass = g0 + warp; pass < g1; pass += kWarps * 32) {
-                // lane l resolves position pass + 16*l
-                const int mypos = pass + kWarps * lane;
-                int myn = 0;
-                float myz = 0.f;
-                if (mypos < g1) {
-                    if (kPipe == 0) {
-                        myn = mypos;
-                        myz = __ldcg(W.zD + mypos);
-                    } else {
-                        const int s = owner_of(sm.voff, G, mypos);
-                        const int src = split_lo(s, G, p) + (mypos - sm.voff[s]);
-                        myn = __ldcg(W.vlist + src);
-                        myz = __ldcg(W.zlist + src);
-                    }
-                }
-                const int cnt = min(32, (g1 - pass + kWarps - 1) / kWarps);
-                int k = 0;
-                for (; k + 4 <= cnt; k += 4) {
-                    uint4 w[4];
-                    float z[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int n = __shfl_sync(0xffffffffu, myn, k + u);
-                        z[u] = __shfl_sync(0xffffffffu, myz, k + u);
-                        w[u] = col_ok ? ldg_stream(L.ud + static_cast<size_t>(n) * 2 * L.pitch_d +
-                                                   L.pitch_d + chunk * 8)
-                                      : make_uint4(0, 0, 0, 0);
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) axpy8(w[u], z[u], acc);
-                }
-                for (; k < cnt; ++k) {
-                    const int n = __shfl_sync(0xffffffffu, myn, k);
-                    const float z = __shfl_sync(0xffffffffu, myz, k);
-                    const uint4 w = col_ok ? ldg_stream(L.ud + static_cast<size_t>(n) * 2 *
-                                                                   L.pitch_d +
-                                                        L.pitch_d + chunk * 8)
-                                           : make_uint4(0, 0, 0, 0);
-                    axpy8(w, z, acc);
-                }
-            }
-#pragma unroll
-            for (int e = 0; e < 8; ++e) sm.red[(warp * 32 + lane) * 8 + e] = acc[e];
+    const int c0 = split_lo(c, G, L.d), c1 = split_lo(c + 1, G, L.d);
+    const int ncols = c1 - c0;
+    float* part = reinterpret_cast<float*>(sm.big);
+    if (ncols > 0) {
+        int ngrp = kCThreads / ncols;
+        if (ngrp > 32) ngrp = 32;
+        if (tid < ngrp * ncols) {
+            const int col = c0 + tid % ncols, grp = tid / ncols;
+            const int g0 = split_lo(grp, ngrp, G), g1 = split_lo(grp + 1, ngrp, G);
+            float s = 0.f;
+            for (int g = g0; g < g1; ++g)
+                s += __ldcg(W.ypart + static_cast<size_t>(g) * L.pitch_d + col);
+            part[tid] = s;
         }
         __syncthreads();
-        // fixed-order sum over the 16 warps: thread t -> (lane t>>3, element t&7)
-        float s = 0.f;
-        const int col = slice * kSliceCols + tid;  // tid in [0,256): chunk lane tid>>3, elem tid&7
-        if (tid < kSliceCols) {
-            const int l = tid >> 3, e = tid & 7;
-            for (int w = 0; w < kWarps; ++w) s += sm.red[(w * 32 + l) * 8 + e];
-            if (Q == 1) {
-                if (col < L.d) y[col] = s;
-            } else {
-                W.ypart[static_cast<size_t>(q) * L.pitch_d + col] = s;
-                __threadfence();
-            }
+        if (dbg && tid == 0) dbg[13] = globaltimer();
+        if (tid < ncols) {
+            float s = 0.f;
+            for (int grp = 0; grp < ngrp; ++grp) s += part[grp * ncols + tid];
+            y[c0 + tid] = s;
         }
-        if (Q > 1) {
-            __shared__ int s_last;
-            __syncthreads();
-            if (tid == 0) {
-                __threadfence();
-                const unsigned prev = atomicAdd(W.slice_ctr + slice, 1u);
-                s_last = prev == static_cast<unsigned>(Q - 1);
-                if (s_last) W.slice_ctr[slice] = 0u;  // self-reset for the next use
-                __threadfence();
-            }
-            __syncthreads();
-            if (s_last && tid < kSliceCols && col < L.d) {
-                float tot = 0.f;
-                for (int qq = 0; qq < Q; ++qq)
-                    tot += __ldcg(W.ypart + static_cast<size_t>(qq) * L.pitch_d + col);
-                y[col] = tot;
-            }
-        }
-        __syncthreads();
     }
+    __syncthreads();
 }
 
 // Stage x (fp32, length d) into smem, zero-padded to pitch_d; flag non-finite.
@@ -645,37 +1076,62 @@ __device__ __forceinline__ bool stage_x(const float* x, int d, int pitch_d, floa
 
 template <int kPipe>
 __device__ void run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
-                          const SmemPlan& S, RingState& rs, const float* x, float* y,
-                          bool first_layer) {
+                          const SmemPlan& S, RunState& rs, const float* x, float* y,
+                          bool first_layer, int lidx, bool want_sets) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
-    const bool use_as = kPipe != 0 && S.as_cap_bytes > 0;
-    // A-slice prefetch (does not depend on x): overlaps phase A and barrier 1.
-    if (use_as && tid == kCThreads) {
-        const int n0 = split_lo(c, G, L.D), n1 = split_lo(c + 1, G, L.D);
-        if (n1 > n0) {
-            const uint32_t bytes = static_cast<uint32_t>(n1 - n0) * L.pitch_r * 2u;
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR vs. last layer's reads
-            mbar_expect_tx(sm.abar, bytes);
-            bulk_g2s(sm.as, L.A + static_cast<size_t>(n0) * L.pitch_r, bytes, sm.abar,
-                     policy_evict_first());
-        }
-    }
-    if (!first_layer) grid_barrier(W.bar);  // previous layer's y is complete
+    // optional per-CTA phase timestamps (sg_ctx_enable_phase_timing)
+    uint64_t* dbg = W.dbg ? W.dbg + (static_cast<size_t>(lidx) * G + c) * 32 : nullptr;
+#define SG_STAMP(k)                                   \
+    do {                                              \
+        if (dbg && tid == 0) dbg[k] = globaltimer();  \
+    } while (0)
+    SG_STAMP(0);
+    const bool use_as = kPipe != 0 && S.as_bytes > 0 && !(W.flags & 32);
+    bool staged = false;
+    if (W.flags & 1024) staged = kPipe != 0 && stage_weights(L, sm, S, use_as);
+    if (!first_layer) grid_arrive(W, rs);  // previous layer's y is published
+    // weights of this layer (independent of x) are staged during the barrier
+    if (!(W.flags & 1024)) staged = kPipe != 0 && stage_weights(L, sm, S, use_as);
+    if (!first_layer) grid_wait(W, rs);
+    SG_STAMP(1);
     const bool bad = stage_x(x, L.d, L.pitch_d, sm.xs);
     if (c == 0 && tid == 0) {
+        W.stats[1] = 0;  // survivors are added in phase C, after two grid barriers
         W.stats[2] = bad ? 1 : 0;
         W.stats[3] = kPipe;
     }
-    int i0 = 0, i1 = 0;
+    SG_STAMP(2);
     if (kPipe != 0) {
-        phase_t(L, W, sm);
-        grid_barrier(W.bar);
-        phase_mask(L, W, sm, use_as, rs, nullptr);
-        grid_barrier(W.bar);
+        if (staged) {
+            mbar_wait(sm.abar, rs.auses & 1u);
+            __syncwarp();
+            rs.auses += 1;
+        }
+        phase_t(L, W, sm, S);
+        SG_STAMP(3);
+        grid_barrier(W, rs);
+        SG_STAMP(4);
+        phase_mask(L, W, sm, S, use_as, nullptr, true, true, dbg);
+        SG_STAMP(5);
+        grid_arrive(W, rs);
+        if (W.flags & 1) {
+            if (W.flags & 64) prefetch_own_gate_rows_lsu(L, W, sm);
+            else prefetch_own_gate_rows(L, W, sm);
+        }
+        grid_wait(W, rs);
+        SG_STAMP(6);
     }
-    phase_gather<kPipe>(L, W, sm, S, rs, i0, i1);
-    grid_barrier(W.bar);
-    phase_down<kPipe>(L, W, sm, y, 0);
+    phase_gather<kPipe>(L, W, sm, S, rs, dbg);
+    SG_STAMP(14);
+    if (kPipe == 2) survivor_up(L, W, sm, split_lo(c, G, sm.off[G]));
+    SG_STAMP(15);
+    partial_down<kPipe>(L, W, sm);
+    SG_STAMP(7);
+    grid_barrier(W, rs);
+    SG_STAMP(8);
+    phase_down<kPipe>(L, W, sm, y, dbg, want_sets);
+    SG_STAMP(9);
+#undef SG_STAMP
 }
 
 __device__ __forceinline__ void init_barriers(const Smem& sm) {
@@ -697,7 +1153,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const Smem sm = carve(smem_raw, S);
     init_barriers(sm);
-    RingState rs{0u, 0u};
+    RunState rs{0u, 0u, 0ull, 0u};
+    grid_barrier_init(W, rs);
     for (int l = 0; l < nlayers; ++l) {
         const LayerView L = layers ? layers[l] : L0;
         const float* x = (chain && l > 0) ? ys + static_cast<size_t>(l - 1) * xstride
@@ -705,23 +1162,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* y = ys + static_cast<size_t>(l) * xstride;
         WorkView Wl = W;
         Wl.stats = W.stats + 4 * l;  // per-layer {p, v, nonfinite, pipeline}
-        run_layer<kPipe>(L, Wl, sm, S, rs, x, y, l == 0);
+        run_layer<kPipe>(L, Wl, sm, S, rs, x, y, l == 0, l, l == nlayers - 1);
     }
 }
 
-// Predictor-only kernel (sg_predict_mask): phases A and B.
+// Predictor-only kernel (sg_predict_mask): phases A and B, weights streamed.
 __global__ void __launch_bounds__(kThreads, 1)
     predict_kernel(LayerView L, WorkView W, SmemPlan S, uint8_t* mask_out) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const Smem sm = carve(smem_raw, S);
     init_barriers(sm);
-    RingState rs{0u, 0u};
+    RunState rs{0u, 0u, 0ull, 0u};
+    grid_barrier_init(W, rs);
+    stage_bias(L, sm);
     const bool bad = stage_x(W.x, L.d, L.pitch_d, sm.xs);
     if (blockIdx.x == 0 && threadIdx.x == 0) W.stats[2] = bad ? 1 : 0;
-    phase_t(L, W, sm);
-    grid_barrier(W.bar);
-    phase_mask(L, W, sm, false, rs, mask_out);
-    grid_barrier(W.bar);
+    phase_t(L, W, sm, S);
+    grid_barrier(W, rs);
+    phase_mask(L, W, sm, S, false, mask_out, false, false);
+    grid_barrier(W, rs);
     if (threadIdx.x < 32 && blockIdx.x == 0) {
         warp_prefix(W.cnt, sm.off, gridDim.x, threadIdx.x);
         if (threadIdx.x == 0) W.stats[0] = sm.off[gridDim.x];
@@ -731,45 +1190,62 @@ __global__ void __launch_bounds__(kThreads, 1)
 int align_up(int v, int a) { return (v + a - 1) / a * a; }
 
 // Shared-memory plan for a layer shape at G CTAs.
-bool make_plan(int G, int pitch_d, int pitch_r, int Dl, int pipe, int max_smem, SmemPlan* S) {
-    int off = 3 * kMaxSlots * 8;  // full, empty, abar (+ spare)
+bool make_plan(int G, int pitch_d, int r, int pitch_r, int Dl, int pipe, int max_smem,
+               SmemPlan* S, int kc_override = 0, int ns_override = 0) {
+    int off = 3 * kMaxSlots * 8;  // full, empty, abar
     off = align_up(off, 128);
     S->off_slotn = off;
     off += kMaxSlots * 4;
     S->off_off = off = align_up(off, 16);
     off += (G + 1) * 4;
-    S->off_voff = off = align_up(off, 16);
-    off += (G + 1) * 4;
-    S->off_red = off = align_up(off, 128);
-    off += kWarps * 32 * 8 * 4;
     S->mask_cap = align_up((Dl + G - 1) / G + 1, 16);
-    S->off_mask = off;
+    S->off_mask = off = align_up(off, 16);
     off += S->mask_cap;
+    S->off_bias = off = align_up(off, 16);
+    off += S->mask_cap * 4;
+    S->off_misc = off = align_up(off, 16);
+    off += 32 * 4;
+    S->off_reda = off = align_up(off, 16);
+    off += 256 * 4;  // phase A: kRowsA*kWarps; phase C: kGroups * 2 * kGroupWarps * 4
+    S->item_cap = (Dl + G - 1) / G + 2;
+    S->off_items = off = align_up(off, 16);
+    off += S->item_cap * 4;
     S->off_xs = off = align_up(off, 128);
     off += pitch_d * 4;
     S->off_ts = off = align_up(off, 128);
     off += pitch_r * 4;
-    S->off_as = off = align_up(off, 128);
+    S->off_big = off = align_up(off, 1024);
+    const int avail = max_smem - off;
+    // phase C end / phase D: survivor list (<= item_cap int2) and partial scratch
+    S->list_cap = S->item_cap;
+    if (avail < S->item_cap * 8 || avail < kCThreads * 4) return false;
+    // phases A/B staging
+    const int nB = (r + G - 1) / G;
+    const int b_bytes = nB * pitch_d * 2;
     int as_bytes = 0;
-    if (pipe != 0) {
-        as_bytes = ((Dl + G - 1) / G + 1) * pitch_r * 2;
-        if (as_bytes > 64 * 1024) as_bytes = 0;  // fall back to streaming A from HBM
-    }
-    S->as_cap_bytes = as_bytes;
-    off += as_bytes;
-    S->off_ring = off = align_up(off, 128);
+    if (pipe != 0) as_bytes = align_up(((Dl + G - 1) / G + 1) * pitch_r * 2, 16);
+    S->stage_b = (pipe != 0 && b_bytes + as_bytes <= avail) ? 1 : 0;
+    if (!S->stage_b && pipe != 0 && as_bytes > avail) as_bytes = 0;
+    S->as_bytes = as_bytes;
+    // phase C ring
     S->slot_bytes = (pipe == 2 ? 1 : 2) * pitch_d * 2;
-    int ns = (max_smem - off) / S->slot_bytes;
-    if (ns > kMaxSlots) ns = kMaxSlots;
-    if (ns < 2) return false;
-    S->ns = ns;
-    S->total = off + ns * S->slot_bytes;
+    int ns_max = avail / S->slot_bytes;
+    if (ns_max > kMaxSlots) ns_max = kMaxSlots;
+    if (ns_max < 1) return false;
+    int kc = ns_max < kGroups ? ns_max : kGroups;
+    if (kc_override > 0 && kc_override < kc) kc = kc_override;
+    if (ns_override > 0 && ns_override < ns_max) ns_max = ns_override;
+    if (ns_max < kc) kc = ns_max;
+    S->kc = kc;
+    S->ns = kc * (ns_max / kc);
+    S->big_bytes = avail;
+    S->total = max_smem;
     return true;
 }
 
 template <typename K>
 int launch_coop(K kernel, int G, int smem, cudaStream_t stream, void** args) {
-    // Raise the dynamic-smem cap once per kernel (per process; one device per process).
+    // Raise the dynamic-smem cap once per kernel (per thread; one device per process).
     static thread_local const void* set_for[8] = {};
     static thread_local int set_smem[8] = {};
     const void* key = reinterpret_cast<const void*>(kernel);
@@ -788,15 +1264,20 @@ int launch_coop(K kernel, int G, int smem, cudaStream_t stream, void** args) {
                                        dim3(kThreads), args, static_cast<size_t>(smem), stream);
 }
 
-int launch_ffn(const LayerView* layers_dev, int nlayers, const LayerView& L0, const WorkView& W,
-               const float* xs, float* ys, int chain, int xstride, int pipeline, int G,
-               cudaStream_t stream) {
+int smem_budget() {
     int dev = 0;
     cudaGetDevice(&dev);
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return max_smem - 1024;
+}
+
+int launch_ffn(const LayerView* layers_dev, int nlayers, const LayerView& L0, const WorkView& W,
+               const float* xs, float* ys, int chain, int xstride, int pipeline, int G,
+               cudaStream_t stream) {
     SmemPlan S;
-    if (!make_plan(G, L0.pitch_d, L0.pitch_r, L0.D, pipeline, max_smem, &S))
+    if (!make_plan(G, L0.pitch_d, L0.r, L0.pitch_r, L0.D, pipeline, smem_budget(), &S,
+                   (W.flags >> 8) & 0xff, (W.flags >> 16) & 0xff))
         return cudaErrorInvalidConfiguration;
     WorkView Wc = W;
     void* args[] = {(void*)&layers_dev, (void*)&nlayers, (void*)&L0, (void*)&Wc, (void*)&S,
@@ -824,13 +1305,11 @@ int launch_layers(const LayerView* layers_dev, int n, const LayerView& first, co
 
 int launch_predict(const LayerView& L, const WorkView& W, uint8_t* mask_out, int num_ctas,
                    void* stream) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int max_smem = 0;
-    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     SmemPlan S;
-    if (!make_plan(num_ctas, L.pitch_d, L.pitch_r, L.D, 0, max_smem, &S))
+    if (!make_plan(num_ctas, L.pitch_d, L.r, L.pitch_r, L.D, 0, smem_budget(), &S))
         return cudaErrorInvalidConfiguration;
+    S.stage_b = 0;
+    S.as_bytes = 0;
     LayerView Lc = L;
     WorkView Wc = W;
     void* args[] = {(void*)&Lc, (void*)&Wc, (void*)&S, (void*)&mask_out};
