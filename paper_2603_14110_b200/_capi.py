@@ -11,7 +11,10 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsparsegate_b200.so")
+# SG_LIB=timing selects the instrumented build (per-phase %globaltimer stamps,
+# tools/phase_profile.py); the default is the production library.
+LIB_PATH = os.path.join(HERE, "libsparsegate_b200_timing.so" if os.environ.get("SG_LIB") == "timing"
+                        else "libsparsegate_b200.so")
 
 SG_OK, SG_ERR_USAGE, SG_ERR_DATA, SG_ERR_PROPERTY, SG_ERR_IO, SG_ERR_CUDA, SG_ERR_NCCL = range(7)
 SG_F64, SG_F32, SG_BF16 = 0, 1, 2

@@ -423,6 +423,7 @@ sg_status sg_ctx_create(int32_t device, int64_t max_hidden, int64_t max_inter, i
     const size_t o_t = take(C->pitch_rmax * 32);  // one 32-B sector per t value
     const size_t o_cnt = take(2 * G * 32);  // one 32-B sector per CTA count
     const size_t o_plist = take(Dm * 4), o_P = take(Dm * 4), o_gP = take(Dm * 4);
+    const size_t o_gN = take(Dm * 4);
     const size_t o_rec = take(Dm * 8), o_V = take(Dm * 4), o_zV = take(Dm * 4);
     const size_t o_vseg = take(Dm * 8);
     const size_t o_zD = take(Dm * 4);
@@ -448,6 +449,7 @@ sg_status sg_ctx_create(int32_t device, int64_t max_hidden, int64_t max_inter, i
     W.plist = reinterpret_cast<int*>(b + o_plist);
     W.P = reinterpret_cast<int*>(b + o_P);
     W.gP = reinterpret_cast<float*>(b + o_gP);
+    W.gN = reinterpret_cast<float*>(b + o_gN);
     W.rec = reinterpret_cast<int*>(b + o_rec);
     W.vseg = reinterpret_cast<int*>(b + o_vseg);
     W.V = reinterpret_cast<int*>(b + o_V);

@@ -34,7 +34,8 @@ struct WorkView {
     int* cnt;             // [2*gpad] per-CTA predicted counts, then survivor counts
     int* plist;           // [Dmax] per-CTA local predicted lists at neuron-range offsets
     int* P;               // [Dmax] compacted GLOBAL predicted indices, by P position
-    float* gP;            // [Dmax] gate pre-activation, by P position
+    float* gP;            // [Dmax] gate pre-activation, by P position (output)
+    float* gN;            // [Dmax] gate pre-activation per (local) neuron
     int* rec;             // [2*Dmax] int2 {local neuron or -1, z bits}, by P position
     int* vseg;            // [2*Dmax] int2 per-CTA survivor segments at item-range offsets
     int* V;               // [Dmax] compacted GLOBAL survivor indices

@@ -2,37 +2,43 @@
 //
 // One persistent, cooperative launch per layer (or per stack of layers) runs
 // the five stages of the reference's sequential pipeline
-// (/root/reference/proj/include/sparsegate/ffn_exec.hpp:183-218):
+// (/root/reference/proj/include/sparsegate/ffn_exec.hpp:183-218). CTA c owns a
+// contiguous range of neurons [n0, n1) and the predictor rows j = c + k*G.
 //
-//   start    cp.async.bulk: this CTA's rows of B and its slice of A -> smem
-//            (weights only; overlaps the previous layer's tail and barrier)
-//   phase A  stage 1a  t = B·x  (rows j ≡ c mod G)      (ffn_exec.hpp:133-136)
+//   start    cp.async.bulk: this CTA's rows of B and its slice of A -> smem;
+//            cp.async: its bias slice (weights only: staged during the
+//            previous layer's tail, overlapping its barrier)
+//   phase A  stage 1a  t = B·x  (rows j = c + k*G)    (ffn_exec.hpp:133-136)
 //            --- grid barrier ---
-//   phase B  stage 1b  pre = A·t + bias > 0 -> mask   (ffn_exec.hpp:139-144)
-//            stage 2   warp-ballot compaction          (ffn_exec.hpp:189-195)
-//            + L2 prefetch of this CTA's predicted gate rows (speculation-free:
-//              every predicted row is prefetched exactly once, by its owner)
+//   phase B  stage 1b  pre = A·t + bias > 0 -> mask  (ffn_exec.hpp:139-144)
+//            stage 2   warp-ballot compaction -> this CTA's predicted list
+//                                                     (ffn_exec.hpp:189-195)
+//   phase C  stage 3   its predicted gate rows -> smem ring (cp.async.bulk,
+//                      one issuing lane per slot, mbarriers); 4-warp groups
+//                      with x in registers compute g; revalidation g > 0
+//                                                     (ffn_exec.hpp:196-201)
+//                      survivors' [up | down] rows are prefetched to L2
+//            stage 4   survivors: u = up·x, z = gated(g, u)  (:202-203, :68-76)
+//            stage 5a  partial y = Σ z·down over its survivors (one pass with 4)
 //            --- grid barrier ---
-//   phase C  P prefix; balanced split of P over CTAs;
-//            stage 3   gate rows -> smem ring (cp.async.bulk + mbarriers),
-//                      g = gate·x, revalidation g > 0   (ffn_exec.hpp:196-201)
-//            stage 4   survivors: up row (LDG) -> z = gated(g, u)   (:202-203, :68-76)
-//                      + L2 prefetch of the survivor's down row
-//            --- grid barrier ---
-//   phase D  survivor list compaction (ballot, in P order = ascending neuron)
-//            stage 5   y = Σ z·down_row, column-sliced: each CTA owns a few
-//                      16-B column chunks and reduces them over all survivors
-//                      in a fixed order                (ffn_exec.hpp:80-94)
+//   phase D  stage 5b  y: CTA c sums the G partials of its column slice in a
+//                      fixed order                   (ffn_exec.hpp:80-94)
+//
+// No grid barrier between stages 2 and 3: a CTA streams its OWN predicted
+// rows, so the P prefix (needed only for the P/V outputs) is computed in
+// phase D, and only when the caller asks for the index sets.
 //
 // Dense (ffn_exec.hpp:103-122) and parallel (:149-178) pipelines reuse phases
 // C/D with gate+up rows fetched together.
 //
-// Determinism: no floating-point atomics. Every dot product has a fixed lane
-// -> chunk assignment and a fixed shuffle tree, so a row gives the same bits
-// whichever CTA/warp computes it; the down projection sums each column in a
-// fixed order over survivor positions. Repeated calls are bit-identical, and
-// the sequential and parallel pipelines are bit-identical on the same mask
-// (the reference's determinism contract, ffn_exec.hpp:3-15).
+// Determinism: no floating-point atomics. Every dot product has a fixed
+// thread -> chunk assignment and a fixed reduction tree; every partial sum is
+// over a fixed, ordered set (a CTA's own rows in ascending neuron order), and
+// the G partials are summed in CTA order. Repeated calls are bit-identical.
+//
+// Code size matters: the per-layer path must fit the SM instruction cache
+// (~32 KB), so cold paths (index-set outputs, barriers) are out of line and
+// the phase-timing instrumentation is compiled only with -DSG_PHASE_TIMING.
 #include "sg_internal.h"
 
 #include <cuda_runtime.h>
@@ -50,19 +56,23 @@ constexpr int kRowsA = 4;                 // phase A rows reduced per pass
 constexpr int kGroupWarps = 4;            // phase C: a row is reduced by a group of 4 warps
 constexpr int kGroups = kWarps / kGroupWarps;
 constexpr int kGroupThreads = kGroupWarps * 32;
+constexpr int kStageOff = 4096;           // staged B rows / A slice start here in the big region
 constexpr int kXRegChunks = 4;            // x chunks per thread held in registers (pitch_d <= 4096)
+constexpr int kSurvBatch = 4;             // survivors per round in stages 4+5a
+constexpr int kSector = 8;                // ints per 32-B sector
 
 // Shared memory: small fixed arrays, then one large region that is, in turn,
 // the B/A staging buffer (phases A/B), the cp.async.bulk ring (phase C) and
-// the survivor list + reduction scratch (phase D) — never live at once.
+// the survivor list + reduction scratch (stages 4/5) — never live at once.
 struct SmemPlan {
     int off_slotn;  // int[kMaxSlots]   neuron of each ring slot
-    int off_off;    // int[G+1]         P prefix over CTAs
+    int off_off;    // int[G+1]         predictor-kernel prefix scratch
     int off_mask;   // uint8[mask_cap]  phase B mask bytes
-    int off_bias;   // float[mask_cap]  this CTA's bias slice (cp.async at layer start)
-    int off_misc;   // int[32]          block-level scalars / warp counts
-    int off_reda;   // float[kRowsA*kWarps]
-    int off_items;  // int[item_cap]    this CTA's phase-C neurons
+    int off_bias;   // float[mask_cap]  this CTA's bias slice / dense z slice
+    int off_misc;   // int[32]          block-level scalars
+    int off_reda;   // float[256]       reduction scratch
+    int off_items;  // int[item_cap]    this CTA's predicted neurons
+    int off_recs;   // int2[item_cap]   per-item {neuron or -1, g or z}
     int off_xs;     // float[pitch_d]
     int off_ts;     // float[pitch_r]
     int off_big;
@@ -72,7 +82,6 @@ struct SmemPlan {
     int slot_bytes;
     int stage_b;     // B rows of this CTA staged in smem (phase A)
     int as_bytes;    // A slice capacity in smem (0 = stream A from HBM)
-    int list_cap;    // phase D survivor-list capacity (entries)
     int mask_cap;
     int item_cap;
     int total;
@@ -89,6 +98,7 @@ struct Smem {
     int* misc;
     float* reda;
     int* items;
+    int2* recs;
     float* xs;
     float* ts;
     uint8_t* big;
@@ -106,19 +116,19 @@ __device__ __forceinline__ Smem carve(uint8_t* base, const SmemPlan& S) {
     m.misc = reinterpret_cast<int*>(base + S.off_misc);
     m.reda = reinterpret_cast<float*>(base + S.off_reda);
     m.items = reinterpret_cast<int*>(base + S.off_items);
+    m.recs = reinterpret_cast<int2*>(base + S.off_recs);
     m.xs = reinterpret_cast<float*>(base + S.off_xs);
     m.ts = reinterpret_cast<float*>(base + S.off_ts);
     m.big = base + S.off_big;
     return m;
 }
 
-// Per-thread persistent state across phases/layers (identical in all threads
-// of a CTA except the barrier fields, which only thread 0 uses).
+// Per-thread persistent state across phases/layers.
 struct RunState {
-    uint32_t seq;       // items pushed through the ring so far (this launch)
+    uint32_t seq;       // ring items issued so far (this launch)
     uint32_t auses;     // staging-barrier phases consumed so far
-    uint64_t bar_base;  // grid-barrier counter value at launch start (thread 0)
-    uint32_t bar_k;     // grid barriers passed in this launch (thread 0)
+    uint64_t bar_base;  // grid-barrier counter base (lanes 0..7 of warp 0)
+    uint32_t bar_k;     // grid barriers passed in this launch
 };
 
 // ---------------------------------------------------------------------------
@@ -130,12 +140,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
                  : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
@@ -163,17 +167,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
-// Bulk prefetch of a contiguous global range into L2 (no smem, no completion).
-__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -192,14 +185,22 @@ __device__ __forceinline__ uint64_t ld_acquire_u64(const unsigned long long* p) 
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void red_release_add_u64(unsigned long long* p, uint64_t v) {
-    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
+
+#ifdef SG_PHASE_TIMING
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
+#define SG_STAMP(dbg, k)                                         \
+    do {                                                         \
+        if ((dbg) && threadIdx.x == 0) (dbg)[k] = globaltimer(); \
+    } while (0)
+#else
+#define SG_STAMP(dbg, k) \
+    do {                 \
+    } while (0)
+#endif
 
 // 8 bf16 weights (one 16-B chunk) against 8 fp32 activations, in element order.
 __device__ __forceinline__ float dot8(const uint4 w, const float* x, float acc) {
@@ -213,6 +214,17 @@ __device__ __forceinline__ float dot8(const uint4 w, const float* x, float acc) 
     acc = fmaf(__uint_as_float(w.z & 0xffff0000u), b.y, acc);
     acc = fmaf(__uint_as_float(w.w << 16), b.z, acc);
     acc = fmaf(__uint_as_float(w.w & 0xffff0000u), b.w, acc);
+    return acc;
+}
+__device__ __forceinline__ float dot8r(const uint4 w, const float* x, float acc) {
+    acc = fmaf(__uint_as_float(w.x << 16), x[0], acc);
+    acc = fmaf(__uint_as_float(w.x & 0xffff0000u), x[1], acc);
+    acc = fmaf(__uint_as_float(w.y << 16), x[2], acc);
+    acc = fmaf(__uint_as_float(w.y & 0xffff0000u), x[3], acc);
+    acc = fmaf(__uint_as_float(w.z << 16), x[4], acc);
+    acc = fmaf(__uint_as_float(w.z & 0xffff0000u), x[5], acc);
+    acc = fmaf(__uint_as_float(w.w << 16), x[6], acc);
+    acc = fmaf(__uint_as_float(w.w & 0xffff0000u), x[7], acc);
     return acc;
 }
 // acc[e] += z * w[e] for the 8 bf16 of one chunk.
@@ -232,158 +244,35 @@ __device__ __forceinline__ float warp_sum(float v) {
     for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
     return v;
 }
-
-// Canonical row dot: lane l owns chunks l, l+32, ... and accumulates them in
-// order; then the butterfly. Identical for rows read from smem or global.
-template <bool kSmem>
-__device__ __forceinline__ float row_dot(const uint16_t* row, const float* xs, int nch, int lane) {
-    float acc = 0.f;
-    if (kSmem) {
-        for (int c = lane; c < nch; c += 32)
-            acc = dot8(*reinterpret_cast<const uint4*>(row + c * 8), xs + c * 8, acc);
-    } else {
-        // Issue the whole row's loads first (up to 16 x 16 B per lane in flight).
-        int c = lane;
-        for (; c + 32 * 15 < nch; c += 32 * 16) {
-            uint4 w[16];
-#pragma unroll
-            for (int k = 0; k < 16; ++k) w[k] = ldg_stream(row + (c + 32 * k) * 8);
-#pragma unroll
-            for (int k = 0; k < 16; ++k) acc = dot8(w[k], xs + (c + 32 * k) * 8, acc);
-        }
-        for (; c < nch; c += 32) acc = dot8(ldg_stream(row + c * 8), xs + c * 8, acc);
-    }
-    return warp_sum(acc);
-}
-// Two rows (gate, up) sharing the x loads; per-row accumulation identical to row_dot.
-__device__ __forceinline__ void row_dot2(const uint16_t* r0, const uint16_t* r1, const float* xs,
-                                         int nch, int lane, float& o0, float& o1) {
-    float a0 = 0.f, a1 = 0.f;
-    for (int c = lane; c < nch; c += 32) {
-        a0 = dot8(*reinterpret_cast<const uint4*>(r0 + c * 8), xs + c * 8, a0);
-        a1 = dot8(*reinterpret_cast<const uint4*>(r1 + c * 8), xs + c * 8, a1);
-    }
-    o0 = warp_sum(a0);
-    o1 = warp_sum(a1);
-}
-
-// ---- phase C row dot: a group of 4 warps (128 threads) per row ----------
-// Thread gt of a group owns chunks gt, gt+128, ... of every row and keeps the
-// matching x values in registers, so the per-row shared-memory traffic is the
-// row itself only. Row value = (thread chain over its chunks, ascending)
-// -> warp butterfly -> the 4 warps summed in order: fixed, so a row gives the
-// same bits from smem or global and in any group.
-struct XRegs {
-    float v[kXRegChunks][8];
-};
-__device__ __forceinline__ void load_xregs(const float* xs, int nch, int gt, XRegs& X) {
-#pragma unroll
-    for (int k = 0; k < kXRegChunks; ++k) {
-        const int ch = gt + k * kGroupThreads;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) X.v[k][e] = ch < nch ? xs[ch * 8 + e] : 0.f;
-    }
-}
-__device__ __forceinline__ float dot8r(const uint4 w, const float* x, float acc) {
-    acc = fmaf(__uint_as_float(w.x << 16), x[0], acc);
-    acc = fmaf(__uint_as_float(w.x & 0xffff0000u), x[1], acc);
-    acc = fmaf(__uint_as_float(w.y << 16), x[2], acc);
-    acc = fmaf(__uint_as_float(w.y & 0xffff0000u), x[3], acc);
-    acc = fmaf(__uint_as_float(w.z << 16), x[4], acc);
-    acc = fmaf(__uint_as_float(w.z & 0xffff0000u), x[5], acc);
-    acc = fmaf(__uint_as_float(w.w << 16), x[6], acc);
-    acc = fmaf(__uint_as_float(w.w & 0xffff0000u), x[7], acc);
-    return acc;
-}
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-// kRows rows from smem (kSmem) or global, sharing the x registers; red is this
-// group's scratch [2 parities][kGroupWarps][4]; par alternates per call.
-template <bool kSmem, int kRows>
-__device__ __forceinline__ void group_dot(const uint16_t* const* rows, const XRegs& X,
-                                          const float* xs, int nch, int gt, int grp, float* red,
-                                          int& par, float* out) {
-    float acc[kRows];
-#pragma unroll
-    for (int q = 0; q < kRows; ++q) acc[q] = 0.f;
-    if (kSmem) {
-#pragma unroll
-        for (int k = 0; k < kXRegChunks; ++k) {
-            const int ch = gt + k * kGroupThreads;
-            if (ch < nch) {
-#pragma unroll
-                for (int q = 0; q < kRows; ++q)
-                    acc[q] = dot8r(*reinterpret_cast<const uint4*>(rows[q] + ch * 8), X.v[k], acc[q]);
-            }
-        }
-    } else {
-        uint4 w[kRows][kXRegChunks];
-#pragma unroll
-        for (int q = 0; q < kRows; ++q)
-#pragma unroll
-            for (int k = 0; k < kXRegChunks; ++k) {
-                const int ch = gt + k * kGroupThreads;
-                w[q][k] = ch < nch ? ldg_stream(rows[q] + ch * 8) : make_uint4(0, 0, 0, 0);
-            }
-#pragma unroll
-        for (int q = 0; q < kRows; ++q)
-#pragma unroll
-            for (int k = 0; k < kXRegChunks; ++k)
-                if (gt + k * kGroupThreads < nch) acc[q] = dot8r(w[q][k], X.v[k], acc[q]);
-    }
-    // chunks beyond the register window (pitch_d > 4096): x from smem
-    for (int ch = gt + kXRegChunks * kGroupThreads; ch < nch; ch += kGroupThreads) {
-#pragma unroll
-        for (int q = 0; q < kRows; ++q) {
-            const uint4 w0 = kSmem ? *reinterpret_cast<const uint4*>(rows[q] + ch * 8)
-                                   : ldg_stream(rows[q] + ch * 8);
-            acc[q] = dot8(w0, xs + ch * 8, acc[q]);
-        }
-    }
-    const int gw = (gt >> 5), lane = gt & 31;
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1)
-#pragma unroll
-        for (int q = 0; q < kRows; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], m);
-    if (lane == 0) {
-#pragma unroll
-        for (int q = 0; q < kRows; ++q) red[(par * kGroupWarps + gw) * 4 + q] = acc[q];
-    }
-    named_bar(1 + grp, kGroupThreads);
-#pragma unroll
-    for (int q = 0; q < kRows; ++q) {
-        float s = 0.f;
-#pragma unroll
-        for (int w = 0; w < kGroupWarps; ++w) s += red[(par * kGroupWarps + w) * 4 + q];
-        out[q] = s;
-    }
-    par ^= 1;
 }
 
 // ffn_exec.hpp:68-76 in fp32 (canonical +0 when suppressed).
 __device__ __forceinline__ float gated(float g, float u, int act) {
-    if (!(g > 0.f)) return 0.f;
-    if (act == 1 && !(u > 0.f)) return 0.f;
-    return g * u;
+    const bool on = g > 0.f && (act == 0 || u > 0.f);
+    return on ? g * u : 0.f;
+}
+
+// Balanced split of n items over G parts: part c starts at c*n/G (32-bit safe
+// for c <= 1024 and n < 2^21).
+__device__ __forceinline__ int split_lo(int c, int G, int n) {
+    return static_cast<int>(static_cast<unsigned>(c) * static_cast<unsigned>(n) /
+                            static_cast<unsigned>(G));
 }
 
 // Values exchanged between CTAs through global memory (per-CTA counts, the
-// predictor's t) are written as whole 32-B sectors, one sector per value: a
-// 4-B store into a sector that other SMs also write leaves it partially
-// written in L2, and the first read then stalls for microseconds (measured
-// ~6 us for the P-count prefix; tools/phase_profile.py).
-constexpr int kSector = 8;  // ints per 32-B sector
+// predictor's t) are written as whole 32-B sectors, one sector per value.
 __device__ __forceinline__ void st_sector(int* p, int v) {
-    asm volatile("st.global.v4.b32 [%0], {%1, %2, %2, %2};\n\tst.global.v4.b32 [%0+16], {%2, %2, %2, %2};"
-                 ::"l"(p), "r"(v), "r"(0) : "memory");
+    asm volatile(
+        "st.global.v4.b32 [%0], {%1, %2, %2, %2};\n\tst.global.v4.b32 [%0+16], {%2, %2, %2, %2};" ::"l"(
+            p),
+        "r"(v), "r"(0)
+        : "memory");
 }
 __device__ __forceinline__ int gpad() { return static_cast<int>(gridDim.x) * kSector; }
 
-__device__ __forceinline__ int split_lo(int c, int G, int n) {
-    return static_cast<int>((static_cast<long long>(c) * n) / G);
-}
-
+// ---------------------------------------------------------------------------
 // Grid barrier on kBarCounters monotonically increasing 64-bit counters
 // (each in its own 256-B block, so they live in different L2 slices). CTA c
 // arrives on counter c % kBarCounters; every barrier adds exactly n_j to
@@ -393,6 +282,7 @@ __device__ __forceinline__ int split_lo(int c, int G, int n) {
 // this CTA's writes, grid_wait() returns once every CTA has arrived; work that
 // does not depend on other CTAs may run in between. All CTAs are co-resident
 // (cooperative launch, one per SM).
+// ---------------------------------------------------------------------------
 constexpr int kBarCounters = 8;
 constexpr int kBarStride = 32;  // u64 elements between counters (256 B)
 
@@ -403,7 +293,7 @@ __device__ __forceinline__ void grid_barrier_init(const WorkView& W, RunState& r
     if (threadIdx.x < kBarCounters) {
         const int n = bar_share(threadIdx.x);
         const uint64_t v = ld_acquire_u64(W.bar + threadIdx.x * kBarStride);
-        rs.bar_base = n > 0 ? v - v % n : v;
+        rs.bar_base = n > 0 ? v - v % static_cast<uint64_t>(n) : v;
     }
     if (threadIdx.x < 32) __syncwarp();
     rs.bar_k = 0;
@@ -413,7 +303,9 @@ __device__ __forceinline__ void grid_arrive(const WorkView& W, RunState& rs) {
     rs.bar_k += 1;
     if (threadIdx.x == 0) {
         __threadfence();
-        red_release_add_u64(W.bar + (blockIdx.x % kBarCounters) * kBarStride, 1ull);
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(
+                         W.bar + (blockIdx.x % kBarCounters) * kBarStride)
+                     : "memory");
     }
 }
 __device__ __forceinline__ void grid_wait(const WorkView& W, RunState& rs) {
@@ -426,7 +318,7 @@ __device__ __forceinline__ void grid_wait(const WorkView& W, RunState& rs) {
             }
         }
         // the lanes left the spin at different times: reconverge warp 0, or it
-        // stays split and every later shuffle of this warp takes the slow path
+        // stays split and its later shuffles take the slow divergent path
         __syncwarp();
     }
     __syncthreads();
@@ -436,102 +328,101 @@ __device__ __forceinline__ void grid_barrier(const WorkView& W, RunState& rs) {
     grid_wait(W, rs);
 }
 
-// Exclusive prefix of cnt[0..G) into off[0..G], off[G] = total. One warp.
-// All loads are issued before the scan (one L2 round trip for G <= 256).
-constexpr int kMaxPrefixChunks = 8;
-__device__ __forceinline__ void warp_prefix(const int* cnt, int* off, int G, int lane) {
-    int v[kMaxPrefixChunks];
-#pragma unroll
-    for (int k = 0; k < kMaxPrefixChunks; ++k) {
-        const int i = k * 32 + lane;
-        v[k] = i < G ? __ldcg(cnt + i * kSector) : 0;
-    }
+// Exclusive prefix of the per-CTA sector counts cnt[i*kSector], i < G, into
+// off[0..G] (off[G] = total). One warp; loads first.
+__device__ __noinline__ void warp_prefix(const int* cnt, int* off, int G, int lane) {
     int carry = 0;
+    for (int base = 0; base < G; base += 128) {
+        int v[4];
 #pragma unroll
-    for (int k = 0; k < kMaxPrefixChunks; ++k) {
-        const int i = k * 32 + lane;
-        int incl = v[k];
-#pragma unroll
-        for (int m = 1; m < 32; m <<= 1) {
-            const int o = __shfl_up_sync(0xffffffffu, incl, m);
-            if (lane >= m) incl += o;
+        for (int k = 0; k < 4; ++k) {
+            const int i = base + k * 32 + lane;
+            v[k] = i < G ? __ldcg(cnt + i * kSector) : 0;
         }
-        if (i < G) off[i] = carry + incl - v[k];
-        carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    for (int base = kMaxPrefixChunks * 32; base < G; base += 32) {
-        const int i = base + lane;
-        const int x = i < G ? __ldcg(cnt + i * kSector) : 0;
-        int incl = x;
 #pragma unroll
-        for (int m = 1; m < 32; m <<= 1) {
-            const int o = __shfl_up_sync(0xffffffffu, incl, m);
-            if (lane >= m) incl += o;
+        for (int k = 0; k < 4; ++k) {
+            const int i = base + k * 32 + lane;
+            int incl = v[k];
+#pragma unroll
+            for (int m = 1; m < 32; m <<= 1) {
+                const int o = __shfl_up_sync(0xffffffffu, incl, m);
+                if (lane >= m) incl += o;
+            }
+            if (i < G) off[i] = carry + incl - v[k];
+            carry += __shfl_sync(0xffffffffu, incl, 31);
         }
-        if (i < G) off[i] = carry + incl - x;
-        carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (lane == 0) off[G] = carry;
-}
-
-// Owner CTA s of list position pos: off[s] <= pos < off[s+1] (off ascending).
-__device__ __forceinline__ int owner_of(const int* off, int G, int pos) {
-    int lo = 0, hi = G;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (off[mid] <= pos) lo = mid; else hi = mid;
-    }
-    return lo;
-}
-
-// The bias slice of this CTA: one 4-B cp.async per neuron (waited on in phase B).
-__device__ __forceinline__ void stage_bias(const LayerView& L, const Smem& sm) {
-    const int G = gridDim.x, c = blockIdx.x;
-    const int n0 = split_lo(c, G, L.D), n1 = split_lo(c + 1, G, L.D);
-    for (int k = threadIdx.x; k < n1 - n0; k += kThreads) cp_async4(sm.bias + k, L.bias + n0 + k);
+    __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
-// Layer start: stage this CTA's B rows and A slice into smem (weights only).
-// Returns whether a staging-barrier phase was issued.
+// Staging of one layer's predictor weights for this CTA (weights only, so it
+// may run during the previous layer's tail): B rows and the A slice by bulk
+// copy on `abar`, the bias slice by cp.async. Returns whether abar was armed.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ bool stage_weights(const LayerView& L, const Smem& sm,
-                                              const SmemPlan& S, bool use_as) {
+                                           const SmemPlan& S, bool use_as) {
     const int G = gridDim.x, c = blockIdx.x;
     const int n0 = split_lo(c, G, L.D), n1 = split_lo(c + 1, G, L.D);
+    for (int k = threadIdx.x; k < n1 - n0; k += kThreads) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sm.bias + k)),
+                     "l"(L.bias + n0 + k)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     const int nB = c < L.r ? (L.r - c + G - 1) / G : 0;
     const uint32_t row_bytes = static_cast<uint32_t>(L.pitch_d) * 2u;
     const uint32_t bytesB = S.stage_b ? static_cast<uint32_t>(nB) * row_bytes : 0u;
     const uint32_t bytesA = use_as ? static_cast<uint32_t>(n1 - n0) * L.pitch_r * 2u : 0u;
-    stage_bias(L, sm);
     if (bytesA + bytesB == 0) return false;
     if ((threadIdx.x >> 5) == kWarps) {
         const int lane = threadIdx.x & 31;
-        fence_proxy_async();  // WAR vs. the previous layer's generic reads of this region
+        // WAR vs. the generic-proxy reads of this region earlier in the layer
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         const uint64_t pol = policy_evict_first();
         if (lane == 0) mbar_expect_tx(sm.abar, bytesA + bytesB);
         __syncwarp();
         for (int q = lane; q < nB && bytesB; q += 31)
-            bulk_g2s(sm.big + static_cast<size_t>(q) * row_bytes,
+            bulk_g2s(sm.big + kStageOff + static_cast<size_t>(q) * row_bytes,
                      L.B + static_cast<size_t>(c + q * G) * L.pitch_d, row_bytes, sm.abar, pol);
         if (bytesA && lane == 31)
-            bulk_g2s(sm.big + bytesB, L.A + static_cast<size_t>(n0) * L.pitch_r, bytesA, sm.abar,
-                     pol);
+            bulk_g2s(sm.big + kStageOff + bytesB, L.A + static_cast<size_t>(n0) * L.pitch_r, bytesA,
+                     sm.abar, pol);
         __syncwarp();
     }
     return true;
 }
 
+// Stage x (fp32, length d) into smem, zero-padded to pitch_d; flag non-finite.
+__device__ __forceinline__ bool stage_x(const float* x, int d, int pitch_d, float* xs) {
+    bool bad = false;
+    if ((d & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+        for (int i = threadIdx.x * 4; i < pitch_d; i += kThreads * 4) {
+            const float4 w = i < d ? __ldcg(reinterpret_cast<const float4*>(x + i))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4*>(xs + i) = w;
+            bad |= !isfinite(w.x) || !isfinite(w.y) || !isfinite(w.z) || !isfinite(w.w);
+        }
+    } else {
+        for (int i = threadIdx.x; i < pitch_d; i += kThreads) {
+            const float v = i < d ? __ldcg(x + i) : 0.f;
+            xs[i] = v;
+            bad |= !isfinite(v);
+        }
+    }
+    return __syncthreads_or(bad) != 0;
+}
+
 // ---------------------------------------------------------------------------
 // Phase A: t = B·x (fp32), rows j = c + q*G ; block-reduced in fixed order.
 // ---------------------------------------------------------------------------
-__device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm,
-                        const SmemPlan& S) {
+__device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm, bool staged_b) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int nch = L.pitch_d >> 3;
     const int nB = c < L.r ? (L.r - c + G - 1) / G : 0;
-    const uint16_t* bs = reinterpret_cast<const uint16_t*>(sm.big);
+    const uint16_t* bs = reinterpret_cast<const uint16_t*>(sm.big + kStageOff);
     for (int q0 = 0; q0 < nB; q0 += kRowsA) {
         float acc[kRowsA];
 #pragma unroll
@@ -542,15 +433,14 @@ __device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm,
 #pragma unroll
                 for (int q = 0; q < kRowsA; ++q) {
                     const int qq = q0 + q;
-                    if (qq >= nB) {
+                    if (qq >= nB)
                         w[q] = make_uint4(0, 0, 0, 0);
-                    } else if (S.stage_b) {
+                    else if (staged_b)
                         w[q] = *reinterpret_cast<const uint4*>(
                             bs + static_cast<size_t>(qq) * L.pitch_d + ch * 8);
-                    } else {
+                    else
                         w[q] = ldg_stream(L.B + static_cast<size_t>(c + qq * G) * L.pitch_d +
                                           ch * 8);
-                    }
                 }
 #pragma unroll
                 for (int q = 0; q < kRowsA; ++q) acc[q] = dot8(w[q], sm.xs + ch * 8, acc[q]);
@@ -565,31 +455,29 @@ __device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm,
         if (tid < kRowsA && q0 + tid < nB) {
             float s = 0.f;
             for (int w = 0; w < kWarps; ++w) s += sm.reda[tid * kWarps + w];
-            st_sector(reinterpret_cast<int*>(W.t) + (c + (q0 + tid) * G) * kSector, __float_as_int(s));
+            st_sector(reinterpret_cast<int*>(W.t) + (c + (q0 + tid) * G) * kSector,
+                      __float_as_int(s));
         }
         __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------------------
-// Phase B: mask over this CTA's neuron range + warp-ballot compaction, and an
-// L2 prefetch of every predicted gate row it owns.
+// Phase B: mask over this CTA's neuron range + warp-ballot compaction into
+// its predicted list (smem items[], global plist at n0, count).
 // ---------------------------------------------------------------------------
-__device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm,
-                           const SmemPlan& S, bool use_as, uint8_t* mask_out, bool prefetch,
-                           bool staged_bias, uint64_t* dbg = nullptr) {
+__device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm, bool use_as,
+                           bool staged_b, uint8_t* mask_out) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int n0 = split_lo(c, G, L.D), n1 = split_lo(c + 1, G, L.D);
     for (int i = tid; i < L.pitch_r; i += kThreads)
         sm.ts[i] = i < L.r ? __ldcg(W.t + i * kSector) : 0.f;
-    (void)staged_bias;
-    cp_async_wait_all();
+    asm volatile("cp.async.wait_all;" ::: "memory");  // the bias slice
     __syncthreads();
-    if (dbg && tid == 0) dbg[11] = globaltimer();
     const int nB = c < L.r ? (L.r - c + G - 1) / G : 0;
     const uint16_t* as = reinterpret_cast<const uint16_t*>(
-        sm.big + (S.stage_b ? static_cast<size_t>(nB) * L.pitch_d * 2 : 0));
+        sm.big + kStageOff + (staged_b ? static_cast<size_t>(nB) * L.pitch_d * 2 : 0));
     // 4 lanes per neuron, 128 neurons per pass; lane sub covers chunks
     // sub + 4i, starting at i = (global index & 1) so the two neurons sharing a
     // quarter-warp read different banks. Order fixed per neuron.
@@ -598,7 +486,7 @@ __device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm
     for (int base = 0; base < n1 - n0; base += kCThreads / 4) {
         const int k = base + (tid >> 2), sub = tid & 3;
         float acc = 0.f;
-        if (tid < kCThreads && k < n1 - n0 && !(W.flags & 16)) {
+        if (tid < kCThreads && k < n1 - n0) {
             const int n = n0 + k;
             const uint16_t* arow = use_as ? as + static_cast<size_t>(k) * L.pitch_r
                                           : L.A + static_cast<size_t>(n) * L.pitch_r;
@@ -622,130 +510,105 @@ __device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm
         }
     }
     __syncthreads();
-    if (dbg && tid == 0) dbg[12] = globaltimer();
     if (warp == 0) {
-        const uint32_t row_bytes = static_cast<uint32_t>(L.pitch_d) * 2u;
         int run = 0;
         for (int base = 0; base < n1 - n0; base += 32) {
             const int k = base + lane;
             const bool on = k < n1 - n0 && sm.mask[k];
             const unsigned b = __ballot_sync(0xffffffffu, on);
-            if (on) W.plist[n0 + run + __popc(b & ((1u << lane) - 1u))] = n0 + k;
+            if (on) {
+                const int dst = run + __popc(b & ((1u << lane) - 1u));
+                W.plist[n0 + dst] = n0 + k;
+                sm.items[dst] = n0 + k;
+            }
             run += __popc(b);
         }
         if (lane == 0) {
             st_sector(W.cnt + c * kSector, run);
             sm.misc[0] = run;
+            if (run && !mask_out) atomicAdd(W.stats + 0, run);  // p (integer: order-free)
         }
-        (void)row_bytes;
     }
-    (void)prefetch;
+    __syncthreads();
 }
 
-// L2 prefetch of this CTA's predicted gate rows (between grid_arrive and
-// grid_wait: the barrier latency streams the first rows of phase C). The
-// producer warp issues them; the CTA's local list is in plist at n0.
-__device__ __forceinline__ void prefetch_own_gate_rows(const LayerView& L, const WorkView& W,
-                                                       const Smem& sm) {
-    const int G = gridDim.x, c = blockIdx.x;
-    if ((threadIdx.x >> 5) != kWarps) return;
-    const int n0 = split_lo(c, G, L.D);
-    const int cnt = sm.misc[0];
-    const uint32_t row_bytes = static_cast<uint32_t>(L.pitch_d) * 2u;
-    for (int k = threadIdx.x & 31; k < cnt; k += 32)
-        prefetch_l2(L.gate + static_cast<size_t>(W.plist[n0 + k]) * L.pitch_d, row_bytes);
-}
-// Same, through the LSU: one prefetch.global.L2 per 128-B line, all threads.
-__device__ __forceinline__ void prefetch_own_gate_rows_lsu(const LayerView& L, const WorkView& W,
-                                                           const Smem& sm) {
-    const int G = gridDim.x, c = blockIdx.x;
-    const int n0 = split_lo(c, G, L.D);
-    const int cnt = sm.misc[0];
-    const int lines = L.pitch_d * 2 / 128;
-    for (int q = threadIdx.x; q < cnt * lines; q += kThreads) {
-        const int k = q / lines, ln = q % lines;
-        const char* a = reinterpret_cast<const char*>(L.gate + static_cast<size_t>(W.plist[n0 + k]) *
-                                                                   L.pitch_d) + ln * 128;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+// ---- phase C row dot: a group of 4 warps (128 threads) per row ----------
+// Thread gt of a group owns chunks gt, gt+128, ... of every row and keeps the
+// matching x values in registers, so the per-row shared-memory traffic is the
+// row itself only. Row value = (thread chain over its chunks, ascending)
+// -> warp butterfly -> the 4 warps summed in order.
+struct XRegs {
+    float v[kXRegChunks][8];
+};
+__device__ __forceinline__ void load_xregs(const float* xs, int nch, int gt, XRegs& X) {
+#pragma unroll
+    for (int k = 0; k < kXRegChunks; ++k) {
+        const int ch = gt + k * kGroupThreads;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) X.v[k][e] = ch < nch ? xs[ch * 8 + e] : 0.f;
     }
+}
+// kRows smem rows sharing the x registers; red is this group's scratch
+// [2 parities][kGroupWarps][4]; par alternates per call.
+template <int kRows>
+__device__ __forceinline__ void group_dot(const uint16_t* const* rows, const XRegs& X,
+                                          const float* xs, int nch, int gt, int grp, float* red,
+                                          int& par, float* out) {
+    float acc[kRows];
+#pragma unroll
+    for (int q = 0; q < kRows; ++q) acc[q] = 0.f;
+#pragma unroll
+    for (int k = 0; k < kXRegChunks; ++k) {
+        const int ch = gt + k * kGroupThreads;
+        if (ch < nch) {
+#pragma unroll
+            for (int q = 0; q < kRows; ++q)
+                acc[q] = dot8r(*reinterpret_cast<const uint4*>(rows[q] + ch * 8), X.v[k], acc[q]);
+        }
+    }
+    // chunks beyond the register window (pitch_d > 4096): x from smem
+    for (int ch = gt + kXRegChunks * kGroupThreads; ch < nch; ch += kGroupThreads) {
+#pragma unroll
+        for (int q = 0; q < kRows; ++q)
+            acc[q] = dot8(*reinterpret_cast<const uint4*>(rows[q] + ch * 8), xs + ch * 8, acc[q]);
+    }
+    const int gw = gt >> 5, lane = gt & 31;
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1)
+#pragma unroll
+        for (int q = 0; q < kRows; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], m);
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < kRows; ++q) red[(par * kGroupWarps + gw) * 4 + q] = acc[q];
+    }
+    named_bar(1 + grp, kGroupThreads);
+#pragma unroll
+    for (int q = 0; q < kRows; ++q) {
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < kGroupWarps; ++w) s += red[(par * kGroupWarps + w) * 4 + q];
+        out[q] = s;
+    }
+    par ^= 1;
 }
 
 // ---------------------------------------------------------------------------
-// Phase C: gather-GEMV over list items through the cp.async.bulk ring.
-//   kPipe 2 (sequential): items = P positions; slot = gate row; survivors fetch
-//                         their up row directly (LDG) -> z.
-//   kPipe 1 (parallel):   items = P positions; slot = gate row + up row.
-//   kPipe 0 (dense):      items = neurons of this CTA's range; slot = gate + up.
-// Sparse pipelines write rec[pos] = {local neuron or -1, z} for phase D.
+// Phase C: gather-GEMV over this CTA's items through the cp.async.bulk ring.
+//   kPipe 2 (sequential): items = own predicted rows; slot = gate row.
+//   kPipe 1 (parallel):   items = own predicted rows; slot = gate row + up row.
+//   kPipe 0 (dense):      items = own neuron range;   slot = gate row + up row.
+// Sparse pipelines record {neuron or -1, g (seq) or z (par)} per item and end
+// with this CTA's survivor list (P order) in the big region.
 // ---------------------------------------------------------------------------
 template <int kPipe>
 __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& sm,
-                             const SmemPlan& S, RunState& rs, uint64_t* dbg = nullptr) {
+                             const SmemPlan& S, RunState& rs) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int nch = L.pitch_d >> 3;
     const uint32_t row_bytes = static_cast<uint32_t>(L.pitch_d) * 2u;
-    int i0, i1;
-    if (kPipe == 0) {
-        i0 = split_lo(c, G, L.D);
-        i1 = split_lo(c + 1, G, L.D);
-    } else {
-        if (warp == 0) {
-            const long long ck0 = clock64();
-            if (dbg && (W.flags & 4096)) {  // probe: an unrelated L2-resident read first
-                float a = __ldcg(W.t + lane * kSector) + __ldcg(W.t + (32 + lane) * kSector);
-                a = __reduce_add_sync(0xffffffffu, __float_as_int(a) & 1);
-                if (lane == 0) dbg[28] = globaltimer() + (a == -7.f ? 1 : 0);
-            }
-            if (W.flags & 512) {
-                // ablation: serial-chunk scan
-                int carry = 0;
-                for (int base = 0; base < G; base += 32) {
-                    const int i = base + lane;
-                    const int v = i < G ? __ldcg(W.cnt + i * kSector) : 0;
-                    int incl = v;
-                    for (int m = 1; m < 32; m <<= 1) {
-                        const int o = __shfl_up_sync(0xffffffffu, incl, m);
-                        if (lane >= m) incl += o;
-                    }
-                    if (i < G) sm.off[i] = carry + incl - v;
-                    carry += __shfl_sync(0xffffffffu, incl, 31);
-                }
-                if (lane == 0) sm.off[G] = carry;
-            } else {
-                warp_prefix(W.cnt, sm.off, G, lane);
-            }
-            if (dbg && lane == 0) {
-                dbg[26] = globaltimer();
-                dbg[30] = static_cast<uint64_t>(clock64() - ck0);
-            }
-            if (W.flags & 32768) {  // probe: the same code again (I-cache warm)
-                warp_prefix(W.cnt, sm.off, G, lane);
-                if (dbg && lane == 0) dbg[29] = globaltimer();
-            }
-            if (dbg && (W.flags & 4096)) {  // probe: a second round of the same loads
-                int acc = 0;
-                for (int i = lane; i < G; i += 32) acc += __ldcg(W.cnt + i * kSector);
-                acc = __reduce_add_sync(0xffffffffu, acc);
-                if (lane == 0) dbg[27] = globaltimer() + (acc == -7 ? 1 : 0);
-            }
-        }
-        __syncthreads();
-        if (dbg && tid == 0) dbg[25] = globaltimer();
-        const int p = sm.off[G];
-        i0 = split_lo(c, G, p);
-        i1 = split_lo(c + 1, G, p);
-        if (c == 0 && tid == 0) W.stats[0] = p;
-        // resolve this CTA's items (one parallel round of L2 reads)
-        for (int j = tid; j < i1 - i0; j += kThreads) {
-            const int pos = i0 + j;
-            const int s = owner_of(sm.off, G, pos);
-            sm.items[j] = __ldcg(W.plist + split_lo(s, G, L.D) + (pos - sm.off[s]));
-        }
-        __syncthreads();
-    }
-    if (dbg && tid == 0) dbg[16] = globaltimer();
-    const int nitems = i1 - i0;
+    const int n0 = split_lo(c, G, L.D);
+    const int nitems = kPipe == 0 ? split_lo(c + 1, G, L.D) - n0 : sm.misc[0];
     const uint32_t seq0 = rs.seq;
     const int ns = S.ns;
 
@@ -753,17 +616,15 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
         // ---- producer warp: lane s issues every item of ring slot s (s < ns),
         // in order. One issuing thread per slot: a single thread issuing all
         // cp.async.bulk copies caps an SM near 22 GB/s (tools/microbench_gather.cu).
-        uint64_t pol = policy_evict_first();
-        if (W.flags & 256) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+        const uint64_t pol = policy_evict_first();
         const int slot = lane;
         if (slot < ns && nitems > 0) {
-            // first q >= seq0 with q % ns == slot
-            uint32_t q = seq0 + static_cast<uint32_t>((slot - static_cast<int>(seq0 % ns) + ns) % ns);
+            uint32_t q = seq0 + static_cast<uint32_t>((slot + ns - static_cast<int>(seq0 % ns)) % ns);
             for (; q < seq0 + static_cast<uint32_t>(nitems); q += ns) {
                 const int j = static_cast<int>(q - seq0);
-                const int n = kPipe == 0 ? i0 + j : sm.items[j];
+                const int n = kPipe == 0 ? n0 + j : sm.items[j];
                 const uint32_t use = q / ns;
-                if (use > 0) mbar_wait(sm.empty + slot, (use - 1) & 1u);  // lanes independent
+                if (use > 0) mbar_wait(sm.empty + slot, (use - 1) & 1u);
                 sm.slotn[slot] = n;
                 uint8_t* dst = sm.big + static_cast<size_t>(slot) * S.slot_bytes;
                 if (kPipe == 2) {
@@ -782,9 +643,9 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
         __syncwarp();
     } else {
         // ---- compute groups: group g < kc (4 warps) consumes the items
-        // q = seq0 + j with q % kc == g, in order. ns is a multiple of kc, so
-        // every slot is consumed by one group, phase after phase, and a parity
-        // wait can never run a phase ahead of the barrier.
+        // q = seq0 + j with q % kc == g, in order, two per iteration. ns is a
+        // multiple of kc, so every slot is consumed by one group, phase after
+        // phase, and a parity wait can never run a phase ahead of the barrier.
         const int kc = S.kc;
         const int grp = warp / kGroupWarps, gt = tid % kGroupThreads;
         XRegs X;
@@ -793,8 +654,6 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
         int par = 0;
         int j0 = grp - static_cast<int>(seq0 % static_cast<uint32_t>(kc));
         if (j0 < 0) j0 += kc;
-        // two items per iteration (j, j + kc): their dot chains, shuffles and
-        // the group barrier are shared, halving the per-row fixed cost
         for (int j = j0; grp < kc && j < nitems; j += 2 * kc) {
             const bool two = j + kc < nitems;
             int slot[2], n[2];
@@ -805,25 +664,22 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
                 const uint32_t q = seq0 + jj;
                 slot[h] = static_cast<int>(q % ns);
                 if (h == 0 || two) mbar_wait(sm.full + slot[h], (q / ns) & 1u);
-                __syncwarp();  // lanes leave the spin at different times: reconverge
                 n[h] = sm.slotn[slot[h]];
                 const uint16_t* srow = reinterpret_cast<const uint16_t*>(
                     sm.big + static_cast<size_t>(slot[h]) * S.slot_bytes);
                 r[2 * h] = srow;
                 r[2 * h + 1] = srow + L.pitch_d;
             }
-            if (dbg && gt == 0 && j == j0) dbg[17 + grp] = globaltimer();  // first row landed
+            __syncwarp();  // lanes leave the spins at different times: reconverge
             float res[4] = {0.f, 0.f, 0.f, 0.f};
-            if (W.flags & 128) {
-                named_bar(1 + grp, kGroupThreads);  // ablation: no compute
-            } else if (kPipe == 2) {
+            if (kPipe == 2) {
                 const uint16_t* rr[2] = {r[0], r[2]};
                 float o[2];
-                group_dot<true, 2>(rr, X, sm.xs, nch, gt, grp, red, par, o);
+                group_dot<2>(rr, X, sm.xs, nch, gt, grp, red, par, o);
                 res[0] = o[0];
                 res[2] = o[1];
             } else {
-                group_dot<true, 4>(r, X, sm.xs, nch, gt, grp, red, par, res);
+                group_dot<4>(r, X, sm.xs, nch, gt, grp, red, par, res);
             }
             // the group barrier inside group_dot follows every read of the slots
             if (gt == 0) {
@@ -833,7 +689,6 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 if (h == 1 && !two) break;
-                const int jj = j + h * kc;
                 const float g = res[2 * h];
                 const float u = res[2 * h + 1];
                 const int nn = n[h];
@@ -841,48 +696,41 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
                     if (gt == 0) W.zD[nn] = gated(g, u, L.act);
                     continue;
                 }
-                const int it = i0 + jj;
                 const bool sv = g > 0.f;  // revalidation, ffn_exec.hpp:200 (strict)
-                // a survivor's [up | down] rows (16 KB, contiguous) go to L2 now, one
-                // 128-B line per thread of the group: stage 4 (sequential) and stage 5
-                // read them after the gate stream
-                if (sv && !(W.flags & 2) && gt * 128 < 4 * L.pitch_d) {
+                // a survivor's [up | down] rows (16 KB, contiguous) go to L2 now,
+                // one 128-B line per thread of the group, for stages 4 and 5a
+                if (sv && !(W.flags & 2)) {
                     const char* a = reinterpret_cast<const char*>(
-                                        L.ud + static_cast<size_t>(nn) * 2 * L.pitch_d) + gt * 128;
-                    for (int off = 0; off < 4 * L.pitch_d; off += kGroupThreads * 128)
-                        if (gt * 128 + off < 4 * L.pitch_d)
-                            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a + off));
+                        L.ud + static_cast<size_t>(nn) * 2 * L.pitch_d);
+                    for (int off = gt * 128; off < 4 * L.pitch_d; off += kGroupThreads * 128)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(a + off));
                 }
                 if (gt == 0) {
-                    W.P[it] = L.gbase + nn * L.gstride;
-                    W.gP[it] = g;
+                    W.gN[nn] = g;  // gate pre-activation per neuron (P output, phase D)
                     int2 rec;
                     rec.x = sv ? nn : -1;
-                    // sequential: carry g, z is formed in survivor_up(); parallel: z now
                     rec.y = __float_as_int(kPipe == 2 ? g : (sv ? gated(g, u, L.act) : 0.f));
-                    reinterpret_cast<int2*>(W.rec)[it] = rec;
+                    sm.recs[j + h * kc] = rec;
                 }
             }
         }
     }
-    if (dbg && tid < kCThreads && (tid % kGroupThreads) == 0) dbg[21 + tid / kGroupThreads] = globaltimer();
     rs.seq = seq0 + static_cast<uint32_t>(nitems > 0 ? nitems : 0);
     __syncthreads();
     if (kPipe != 0) {
-        // survivors of this CTA's item range, in P order -> smem list + global segment
+        // survivors of this CTA's items, in P order -> smem list + global segment
         int2* list = reinterpret_cast<int2*>(sm.big);
         if (warp == 0) {
-            const int2* rec = reinterpret_cast<const int2*>(W.rec);
             int run = 0;
             for (int base = 0; base < nitems; base += 32) {
                 const int j = base + lane;
-                const int2 r = j < nitems ? rec[i0 + j] : make_int2(-1, 0);
-                const bool on = r.x >= 0;
+                const int2 rr = j < nitems ? sm.recs[j] : make_int2(-1, 0);
+                const bool on = rr.x >= 0;
                 const unsigned b = __ballot_sync(0xffffffffu, on);
                 if (on) {
                     const int dst = run + __popc(b & ((1u << lane) - 1u));
-                    list[dst] = r;
-                    reinterpret_cast<int2*>(W.vseg)[i0 + dst] = r;
+                    list[dst] = rr;
+                    reinterpret_cast<int2*>(W.vseg)[n0 + dst] = rr;
                 }
                 run += __popc(b);
             }
@@ -896,33 +744,55 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
     }
 }
 
-// Stage 4 of the sequential pipeline, per CTA, after its gate stream: the up
-// rows of this CTA's survivors (prefetched to L2 when each survivor was
-// found), 8 survivors per round, thread t owning chunks t, t+512, ...; each
-// u is reduced lane-chain -> warp butterfly -> 16 warps in order; then
-// z = gated(g, u) (ffn_exec.hpp:202-203, :68-76) replaces g in the list.
-constexpr int kSurvBatch = 8;
-__device__ void survivor_up(const LayerView& L, const WorkView& W, const Smem& sm, int i0) {
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+// ---------------------------------------------------------------------------
+// Stages 4+5a of the sequential pipeline, per CTA, after its gate stream, in
+// one pass over its survivors (their [up | down] rows were prefetched to L2):
+// kSurvBatch survivors per round; thread t owns chunk t (and t+512, ...). Per
+// survivor: u = up·x reduced thread-chain -> warp butterfly -> 16 warps in
+// order; z = gated(g, u); then the thread's down chunk accumulates z·down
+// (survivors in P order) into this CTA's partial y.
+// ---------------------------------------------------------------------------
+__device__ void survivor_updown(const LayerView& L, const WorkView& W, const Smem& sm) {
+    const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nch = L.pitch_d >> 3;
+    const int n0 = split_lo(c, G, L.D);
     int2* list = reinterpret_cast<int2*>(sm.big);
-    float* red = reinterpret_cast<float*>(sm.big + 64 * 1024);  // after the list (<= 8K entries)
+    float* red = sm.reda;
+    float* zs = red + kSurvBatch * kWarps;
     const int cnt = sm.misc[1];
+    const int ch0 = tid;
+    const bool has0 = tid < kCThreads && ch0 < nch;
+    float acc0[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc0[e] = 0.f;
     for (int b0 = 0; b0 < cnt; b0 += kSurvBatch) {
         const int nb = cnt - b0 < kSurvBatch ? cnt - b0 : kSurvBatch;
         float pu[kSurvBatch];
+        uint4 dn[kSurvBatch];
 #pragma unroll
-        for (int q = 0; q < kSurvBatch; ++q) pu[q] = 0.f;
+        for (int q = 0; q < kSurvBatch; ++q) {
+            pu[q] = 0.f;
+            dn[q] = make_uint4(0, 0, 0, 0);
+        }
         if (tid < kCThreads) {
-            for (int ch = tid; ch < nch; ch += kCThreads) {
-                uint4 w[kSurvBatch];
+            uint4 w[kSurvBatch];
+#pragma unroll
+            for (int q = 0; q < kSurvBatch; ++q) {
+                const uint16_t* row =
+                    L.ud + static_cast<size_t>(q < nb ? list[b0 + q].x : 0) * 2 * L.pitch_d;
+                w[q] = (q < nb && has0) ? ldg_stream(row + ch0 * 8) : make_uint4(0, 0, 0, 0);
+                if (q < nb && has0) dn[q] = ldg_stream(row + L.pitch_d + ch0 * 8);
+            }
+#pragma unroll
+            for (int q = 0; q < kSurvBatch; ++q)
+                if (has0) pu[q] = dot8(w[q], sm.xs + ch0 * 8, pu[q]);
+            for (int ch = ch0 + kCThreads; ch < nch; ch += kCThreads) {
 #pragma unroll
                 for (int q = 0; q < kSurvBatch; ++q)
-                    w[q] = q < nb ? ldg_stream(L.ud + static_cast<size_t>(list[b0 + q].x) * 2 *
-                                                          L.pitch_d + ch * 8)
-                                  : make_uint4(0, 0, 0, 0);
-#pragma unroll
-                for (int q = 0; q < kSurvBatch; ++q) pu[q] = dot8(w[q], sm.xs + ch * 8, pu[q]);
+                    if (q < nb)
+                        pu[q] = dot8(ldg_stream(L.ud + static_cast<size_t>(list[b0 + q].x) * 2 *
+                                                           L.pitch_d + ch * 8),
+                                     sm.xs + ch * 8, pu[q]);
             }
 #pragma unroll
             for (int q = 0; q < kSurvBatch; ++q) {
@@ -935,19 +805,45 @@ __device__ void survivor_up(const LayerView& L, const WorkView& W, const Smem& s
             float u = 0.f;
             for (int w = 0; w < kWarps; ++w) u += red[tid * kWarps + w];
             int2 e = list[b0 + tid];
-            e.y = __float_as_int(gated(__int_as_float(e.y), u, L.act));
+            const float z = gated(__int_as_float(e.y), u, L.act);
+            e.y = __float_as_int(z);
             list[b0 + tid] = e;
-            reinterpret_cast<int2*>(W.vseg)[i0 + b0 + tid] = e;
+            zs[tid] = z;
+            reinterpret_cast<int2*>(W.vseg)[n0 + b0 + tid] = e;
+        }
+        __syncthreads();
+        if (has0) {
+#pragma unroll
+            for (int q = 0; q < kSurvBatch; ++q) axpy8(dn[q], q < nb ? zs[q] : 0.f, acc0);
         }
         __syncthreads();
     }
+    // this CTA's partial y (chunks beyond the first 512, for pitch_d > 4096,
+    // accumulated here from L2 in list order)
+    for (int ch = ch0; tid < kCThreads && ch < nch; ch += kCThreads) {
+        float acc[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = ch == ch0 ? acc0[e] : 0.f;
+        if (ch != ch0) {
+            for (int k = 0; k < cnt; ++k) {
+                const int2 en = list[k];
+                axpy8(ldg_stream(L.ud + static_cast<size_t>(en.x) * 2 * L.pitch_d + L.pitch_d +
+                                 ch * 8),
+                      __int_as_float(en.y), acc);
+            }
+        }
+        float4* dst = reinterpret_cast<float4*>(W.ypart + static_cast<size_t>(c) * L.pitch_d + ch * 8);
+        dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
 }
 
-// Phase D, part 1 (no grid barrier: a CTA's rows are its own neurons/survivors):
-// partial y over this CTA's list, streaming whole down rows (thread t owns
-// chunks t, t+512, ...), rows in list order, kU rows in flight per thread.
-// Dense: the list is the CTA's neuron range with z from zD; sparse: the
-// survivor list built at the end of phase C (rows already prefetched to L2).
+// ---------------------------------------------------------------------------
+// Stage 5a for the dense and parallel pipelines: partial y over this CTA's
+// list, streaming whole down rows (thread t owns chunks t, t+512, ...), rows
+// in list order, kU rows in flight per thread. Dense: the list is the CTA's
+// neuron range with z from zD; parallel: the survivor list of phase C.
+// ---------------------------------------------------------------------------
 template <int kPipe>
 __device__ void partial_down(const LayerView& L, const WorkView& W, const Smem& sm) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
@@ -993,51 +889,72 @@ __device__ void partial_down(const LayerView& L, const WorkView& W, const Smem& 
 #pragma unroll
             for (int u = 0; u < kU; ++u) axpy8(w[u], z[u], acc);
         }
-        float4* dst =
-            reinterpret_cast<float4*>(W.ypart + static_cast<size_t>(c) * L.pitch_d + ch * 8);
+        float4* dst = reinterpret_cast<float4*>(W.ypart + static_cast<size_t>(c) * L.pitch_d + ch * 8);
         dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
         dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
     }
 }
 
+// P and V index-set outputs (ascending global indices) for the caller: prefixes
+// over the per-CTA predicted / survivor counts; this CTA copies its own
+// segments. One warp; only for the last layer of a launch.
+__device__ __noinline__ void write_index_sets(int gbase, int gstride, int D, const int* cnt,
+                                              const int* plist, const float* gN,
+                                              const int* vseg_raw, int* P, float* gP, int* V,
+                                              float* zV) {
+    const int G = gridDim.x, c = blockIdx.x, lane = threadIdx.x & 31;
+    int carryP = 0, carryV = 0, mineP = 0, mineV = 0;
+    for (int base = 0; base < G; base += 32) {
+        const int i = base + lane;
+        const int vp = i < G ? __ldcg(cnt + i * kSector) : 0;
+        const int vv = i < G ? __ldcg(cnt + gpad() + i * kSector) : 0;
+        int ip = vp, iv = vv;
+#pragma unroll
+        for (int m = 1; m < 32; m <<= 1) {
+            const int op = __shfl_up_sync(0xffffffffu, ip, m);
+            const int ov = __shfl_up_sync(0xffffffffu, iv, m);
+            if (lane >= m) {
+                ip += op;
+                iv += ov;
+            }
+        }
+        if (i == c) {
+            mineP = carryP + ip - vp;
+            mineV = carryV + iv - vv;
+        }
+        carryP += __shfl_sync(0xffffffffu, ip, 31);
+        carryV += __shfl_sync(0xffffffffu, iv, 31);
+    }
+    mineP = __reduce_add_sync(0xffffffffu, mineP);
+    mineV = __reduce_add_sync(0xffffffffu, mineV);
+    const int n0 = split_lo(c, G, D);
+    const int cntP = __ldcg(cnt + c * kSector);
+    for (int k = lane; k < cntP; k += 32) {
+        const int n = __ldcg(plist + n0 + k);
+        P[mineP + k] = gbase + n * gstride;
+        gP[mineP + k] = __ldcg(gN + n);
+    }
+    const int cntV = __ldcg(cnt + gpad() + c * kSector);
+    const int2* seg = reinterpret_cast<const int2*>(vseg_raw) + n0;
+    for (int k = lane; k < cntV; k += 32) {
+        const int2 e = __ldcg(seg + k);
+        V[mineV + k] = gbase + e.x * gstride;
+        zV[mineV + k] = __int_as_float(e.y);
+    }
+    __syncwarp();
+}
+
 // ---------------------------------------------------------------------------
-// Phase D, part 2 (after a grid barrier): CTA c sums the G partials of its
-// column range in fixed order (contiguous groups of partials, then the
-// groups), and publishes its survivor segment of V.
+// Phase D (after a grid barrier): CTA c sums the G partials of its column
+// range in fixed order (contiguous groups of partials, then the groups).
 // ---------------------------------------------------------------------------
 template <int kPipe>
 __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm, float* y,
-                           uint64_t* dbg, bool want_sets) {
+                           bool want_sets) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
-    if (kPipe != 0 && want_sets && warp == kWarps) {
-        // V output: prefix over the per-CTA survivor counts, copy own segment
-        int* voff = sm.items;  // phase C is over; reuse (G+1 <= item_cap not assumed)
-        (void)voff;
-        int carry = 0, mine = 0;
-        const int p = sm.off[G];
-        for (int base = 0; base < G; base += 32) {
-            const int i = base + lane;
-            const int v = i < G ? __ldcg(W.cnt + gpad() + i * kSector) : 0;
-            int incl = v;
-#pragma unroll
-            for (int m = 1; m < 32; m <<= 1) {
-                const int o = __shfl_up_sync(0xffffffffu, incl, m);
-                if (lane >= m) incl += o;
-            }
-            if (i == c) mine = carry + incl - v;
-            carry += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        mine = __reduce_add_sync(0xffffffffu, mine);
-        const int i0 = split_lo(c, G, p);
-        const int cntc = __ldcg(W.cnt + gpad() + c * kSector);
-        const int2* seg = reinterpret_cast<const int2*>(W.vseg) + i0;
-        for (int k = lane; k < cntc; k += 32) {
-            const int2 e = __ldcg(seg + k);
-            W.V[mine + k] = L.gbase + e.x * L.gstride;
-            W.zV[mine + k] = __int_as_float(e.y);
-        }
-    }
+    if (kPipe != 0 && want_sets && (tid >> 5) == kWarps)
+        write_index_sets(L.gbase, L.gstride, L.D, W.cnt, W.plist, W.gN, W.vseg, W.P, W.gP, W.V,
+                         W.zV);
     const int c0 = split_lo(c, G, L.d), c1 = split_lo(c + 1, G, L.d);
     const int ncols = c1 - c0;
     float* part = reinterpret_cast<float*>(sm.big);
@@ -1053,7 +970,6 @@ __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm
             part[tid] = s;
         }
         __syncthreads();
-        if (dbg && tid == 0) dbg[13] = globaltimer();
         if (tid < ncols) {
             float s = 0.f;
             for (int grp = 0; grp < ngrp; ++grp) s += part[grp * ncols + tid];
@@ -1063,85 +979,73 @@ __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm
     __syncthreads();
 }
 
-// Stage x (fp32, length d) into smem, zero-padded to pitch_d; flag non-finite.
-__device__ __forceinline__ bool stage_x(const float* x, int d, int pitch_d, float* xs) {
-    bool bad = false;
-    for (int i = threadIdx.x; i < pitch_d; i += kThreads) {
-        const float v = i < d ? __ldcg(x + i) : 0.f;
-        xs[i] = v;
-        bad |= !isfinite(v);
-    }
-    return __syncthreads_or(bad) != 0;
-}
-
+// One layer. Returns whether it already staged the next layer's weights.
 template <int kPipe>
-__device__ void run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
+__device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
                           const SmemPlan& S, RunState& rs, const float* x, float* y,
-                          bool first_layer, int lidx, bool want_sets) {
-    const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
-    // optional per-CTA phase timestamps (sg_ctx_enable_phase_timing)
-    uint64_t* dbg = W.dbg ? W.dbg + (static_cast<size_t>(lidx) * G + c) * 32 : nullptr;
-#define SG_STAMP(k)                                   \
-    do {                                              \
-        if (dbg && tid == 0) dbg[k] = globaltimer();  \
-    } while (0)
-    SG_STAMP(0);
-    const bool use_as = kPipe != 0 && S.as_bytes > 0 && !(W.flags & 32);
-    bool staged = false;
-    if (W.flags & 1024) staged = kPipe != 0 && stage_weights(L, sm, S, use_as);
+                          bool first_layer, int lidx, bool want_sets, const LayerView* next,
+                          bool prestaged) {
+    const int c = blockIdx.x, tid = threadIdx.x;
+#ifdef SG_PHASE_TIMING
+    uint64_t* dbg =
+        W.dbg ? W.dbg + (static_cast<size_t>(lidx) * gridDim.x + c) * 32 : nullptr;
+#else
+    (void)lidx;
+#endif
+    SG_STAMP(dbg, 0);
+    const bool use_as = kPipe != 0 && S.as_bytes > 0;
+    bool staged = prestaged;
     if (!first_layer) grid_arrive(W, rs);  // previous layer's y is published
-    // weights of this layer (independent of x) are staged during the barrier
-    if (!(W.flags & 1024)) staged = kPipe != 0 && stage_weights(L, sm, S, use_as);
+    // weights of this layer (independent of x) are staged during the barrier,
+    // unless the previous layer already staged them during its tail
+    if (kPipe != 0 && !prestaged) staged = stage_weights(L, sm, S, use_as);
     if (!first_layer) grid_wait(W, rs);
-    SG_STAMP(1);
+    SG_STAMP(dbg, 1);
     const bool bad = stage_x(x, L.d, L.pitch_d, sm.xs);
     if (c == 0 && tid == 0) {
-        W.stats[1] = 0;  // survivors are added in phase C, after two grid barriers
+        W.stats[0] = 0;  // p and v are added (atomically) after the next grid barrier
+        W.stats[1] = 0;
         W.stats[2] = bad ? 1 : 0;
         W.stats[3] = kPipe;
     }
-    SG_STAMP(2);
+    SG_STAMP(dbg, 2);
     if (kPipe != 0) {
         if (staged) {
             mbar_wait(sm.abar, rs.auses & 1u);
             __syncwarp();
             rs.auses += 1;
         }
-        phase_t(L, W, sm, S);
-        SG_STAMP(3);
+        phase_t(L, W, sm, S.stage_b != 0);
+        SG_STAMP(dbg, 3);
         grid_barrier(W, rs);
-        SG_STAMP(4);
-        phase_mask(L, W, sm, S, use_as, nullptr, true, true, dbg);
-        SG_STAMP(5);
-        grid_arrive(W, rs);
-        if (W.flags & 1) {
-            if (W.flags & 64) prefetch_own_gate_rows_lsu(L, W, sm);
-            else prefetch_own_gate_rows(L, W, sm);
-        }
-        grid_wait(W, rs);
-        SG_STAMP(6);
+        SG_STAMP(dbg, 4);
+        phase_mask(L, W, sm, use_as, S.stage_b != 0, nullptr);
+        SG_STAMP(dbg, 6);
     }
-    phase_gather<kPipe>(L, W, sm, S, rs, dbg);
-    SG_STAMP(14);
-    if (kPipe == 2) survivor_up(L, W, sm, split_lo(c, G, sm.off[G]));
-    SG_STAMP(15);
-    partial_down<kPipe>(L, W, sm);
-    SG_STAMP(7);
-    grid_barrier(W, rs);
-    SG_STAMP(8);
-    phase_down<kPipe>(L, W, sm, y, dbg, want_sets);
-    SG_STAMP(9);
-#undef SG_STAMP
+    phase_gather<kPipe>(L, W, sm, S, rs);
+    SG_STAMP(dbg, 14);
+    if (kPipe == 2) {
+        survivor_updown(L, W, sm);
+    } else {
+        partial_down<kPipe>(L, W, sm);
+    }
+    SG_STAMP(dbg, 7);
+    // stage the next layer's predictor weights during the barrier: this CTA's
+    // ring and survivor list are done, and phase D only uses the first 2 KB
+    grid_arrive(W, rs);
+    bool next_staged = false;
+    if (kPipe != 0 && next != nullptr) next_staged = stage_weights(*next, sm, S, use_as);
+    grid_wait(W, rs);
+    SG_STAMP(dbg, 8);
+    phase_down<kPipe>(L, W, sm, y, want_sets);
+    SG_STAMP(dbg, 9);
+    return next_staged;
 }
 
-__device__ __forceinline__ void init_barriers(const Smem& sm) {
+__device__ __noinline__ void init_barriers(uint64_t* bars) {
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kMaxSlots; ++i) {
-            mbar_init(sm.full + i, 1);
-            mbar_init(sm.empty + i, 1);
-        }
-        mbar_init(sm.abar, 1);
-        fence_mbar_init();
+        for (int i = 0; i < 2 * kMaxSlots + 1; ++i) mbar_init(bars + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 }
@@ -1152,17 +1056,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                SmemPlan S, const float* xs, float* ys, int chain, int xstride) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const Smem sm = carve(smem_raw, S);
-    init_barriers(sm);
+    init_barriers(sm.full);
     RunState rs{0u, 0u, 0ull, 0u};
     grid_barrier_init(W, rs);
+    bool prestaged = false;
     for (int l = 0; l < nlayers; ++l) {
         const LayerView L = layers ? layers[l] : L0;
+        const LayerView* next = (layers && l + 1 < nlayers) ? layers + l + 1 : nullptr;
         const float* x = (chain && l > 0) ? ys + static_cast<size_t>(l - 1) * xstride
                                           : xs + static_cast<size_t>(l) * xstride;
         float* y = ys + static_cast<size_t>(l) * xstride;
         WorkView Wl = W;
         Wl.stats = W.stats + 4 * l;  // per-layer {p, v, nonfinite, pipeline}
-        run_layer<kPipe>(L, Wl, sm, S, rs, x, y, l == 0, l, l == nlayers - 1);
+        prestaged = run_layer<kPipe>(L, Wl, sm, S, rs, x, y, l == 0, l, l == nlayers - 1, next,
+                                     prestaged);
     }
 }
 
@@ -1171,15 +1078,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     predict_kernel(LayerView L, WorkView W, SmemPlan S, uint8_t* mask_out) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const Smem sm = carve(smem_raw, S);
-    init_barriers(sm);
+    init_barriers(sm.full);
     RunState rs{0u, 0u, 0ull, 0u};
     grid_barrier_init(W, rs);
-    stage_bias(L, sm);
+    stage_weights(L, sm, S, false);  // bias only (S.stage_b == 0)
     const bool bad = stage_x(W.x, L.d, L.pitch_d, sm.xs);
     if (blockIdx.x == 0 && threadIdx.x == 0) W.stats[2] = bad ? 1 : 0;
-    phase_t(L, W, sm, S);
+    phase_t(L, W, sm, false);
     grid_barrier(W, rs);
-    phase_mask(L, W, sm, S, false, mask_out, false, false);
+    phase_mask(L, W, sm, false, false, mask_out);
     grid_barrier(W, rs);
     if (threadIdx.x < 32 && blockIdx.x == 0) {
         warp_prefix(W.cnt, sm.off, gridDim.x, threadIdx.x);
@@ -1206,26 +1113,27 @@ bool make_plan(int G, int pitch_d, int r, int pitch_r, int Dl, int pipe, int max
     S->off_misc = off = align_up(off, 16);
     off += 32 * 4;
     S->off_reda = off = align_up(off, 16);
-    off += 256 * 4;  // phase A: kRowsA*kWarps; phase C: kGroups * 2 * kGroupWarps * 4
+    off += 256 * 4;  // phase A: kRowsA*kWarps; phase C: kGroups*2*kGroupWarps*4; stage 4
     S->item_cap = (Dl + G - 1) / G + 2;
     S->off_items = off = align_up(off, 16);
     off += S->item_cap * 4;
+    S->off_recs = off = align_up(off, 16);
+    off += S->item_cap * 8;
     S->off_xs = off = align_up(off, 128);
     off += pitch_d * 4;
     S->off_ts = off = align_up(off, 128);
     off += pitch_r * 4;
     S->off_big = off = align_up(off, 1024);
     const int avail = max_smem - off;
-    // phase C end / phase D: survivor list (<= item_cap int2) and partial scratch
-    S->list_cap = S->item_cap;
+    // stage 4/5a survivor list (<= item_cap int2) and phase D scratch
     if (avail < S->item_cap * 8 || avail < kCThreads * 4) return false;
     // phases A/B staging
     const int nB = (r + G - 1) / G;
     const int b_bytes = nB * pitch_d * 2;
     int as_bytes = 0;
     if (pipe != 0) as_bytes = align_up(((Dl + G - 1) / G + 1) * pitch_r * 2, 16);
-    S->stage_b = (pipe != 0 && b_bytes + as_bytes <= avail) ? 1 : 0;
-    if (!S->stage_b && pipe != 0 && as_bytes > avail) as_bytes = 0;
+    S->stage_b = (pipe != 0 && kStageOff + b_bytes + as_bytes <= avail) ? 1 : 0;
+    if (!S->stage_b && pipe != 0 && kStageOff + as_bytes > avail) as_bytes = 0;
     S->as_bytes = as_bytes;
     // phase C ring
     S->slot_bytes = (pipe == 2 ? 1 : 2) * pitch_d * 2;

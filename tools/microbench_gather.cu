@@ -63,9 +63,14 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
 }
 
 // ring: warp 16 lane 0 produces; warps 0..kc-1 consume slot s = q % ns (ns multiple of kc)
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 __global__ void ring_kernel(const uint8_t* __restrict__ mat, const int* __restrict__ rows,
                             int per_cta, int row_bytes, int ns, int kc, int split,
-                            float* out, int hint, int nprod = 1) {
+                            float* out, int hint, int nprod = 1, unsigned long long* tlog = nullptr) {
     extern __shared__ __align__(1024) uint8_t sm[];
     uint64_t* full = reinterpret_cast<uint64_t*>(sm);
     uint64_t* empty = full + 64;
@@ -84,6 +89,8 @@ __global__ void ring_kernel(const uint8_t* __restrict__ mat, const int* __restri
     __syncthreads();
     const int* myrows = srows;
     float acc = 0.f;
+    const unsigned long long t0 = gtime();
+    unsigned long long tfirst = 0;
     if (warp == 16) {
         if (lane < nprod) {
             for (int j = lane; j < per_cta; j += nprod) {
@@ -109,6 +116,7 @@ __global__ void ring_kernel(const uint8_t* __restrict__ mat, const int* __restri
         for (int j = warp; j < per_cta; j += kc) {
             const int slot = j % ns;
             mbar_wait(full + slot, (j / ns) & 1);
+            if (j == 0 && lane == 0) tfirst = gtime();
             const uint4* r = reinterpret_cast<const uint4*>(ring + static_cast<size_t>(slot) * row_bytes);
             for (int c = lane; c < row_bytes / 16; c += 32) {
                 const uint4 v = r[c];
@@ -119,6 +127,11 @@ __global__ void ring_kernel(const uint8_t* __restrict__ mat, const int* __restri
         }
     }
     if (acc == 12345.f) out[blockIdx.x] = acc;
+    __syncthreads();
+    if (tlog && tid == 0) {
+        tlog[blockIdx.x * 2] = tfirst - t0;
+        tlog[blockIdx.x * 2 + 1] = gtime() - t0;
+    }
 }
 
 // LDG: each warp takes rows j = warp, warp+16, ...; kU rows in flight per warp
@@ -238,6 +251,31 @@ int main(int argc, char** argv) {
         printf("%-44s %8.2f us/launch  %7.0f GB/s\n", name, us, bytes / (us * 1e-6) / 1e9);
     };
     CK(cudaFuncSetAttribute(ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    {
+        unsigned long long* tlog;
+        CK(cudaMalloc(&tlog, nsm * 16));
+        std::vector<unsigned long long> ht(nsm * 2);
+        for (int ns : {8, 16, 24}) {
+            for (int np : {1, 8, 24}) {
+                if (np > ns) continue;
+                double f = 0, l = 0, fm = 0, lm = 0;
+                for (int r = 0; r < 8; ++r) {
+                    ring_kernel<<<nsm, 544, 1024 + ns * row_bytes + per_cta * 4>>>(
+                        mat, rows + r * per_rep, per_cta, row_bytes, ns, 16 < ns ? 16 : (ns >= 16 ? 16 : ns), 1, out, 1, np, tlog);
+                    CK(cudaDeviceSynchronize());
+                    CK(cudaMemcpy(ht.data(), tlog, nsm * 16, cudaMemcpyDeviceToHost));
+                    for (int i = 0; i < nsm; ++i) {
+                        f += ht[2 * i];
+                        l += ht[2 * i + 1];
+                        fm = fm > ht[2 * i] ? fm : ht[2 * i];
+                        lm = lm > ht[2 * i + 1] ? lm : ht[2 * i + 1];
+                    }
+                }
+                printf("ring ns=%2d nprod=%2d: first row mean %.2f us (max %.2f), done mean %.2f us (max %.2f)\n",
+                       ns, np, f / (8 * nsm) / 1000, fm / 1000, l / (8 * nsm) / 1000, lm / 1000);
+            }
+        }
+    }
     const int maxslots = (220 * 1024 - per_cta * 4) / row_bytes;
     for (int hint : {0, 1}) {
         for (int ns : {4, 8, 16, 24}) {

@@ -25,11 +25,11 @@ for row in csv.reader(io.StringIO(out)):
         for i, h in enumerate(hdr):
             if h.startswith("stall_") and "Not Issued" not in h and i < len(row):
                 try:
-                    tot[h] += float(row[i] or 0)
+                    tot[h] += float(row[i]) if row[i].replace(".", "").isdigit() else 0.0
                 except ValueError:
                     pass
         for i, h in enumerate(hdr):
             if h == "Warp Stall Sampling (All Samples)":
-                tot["ALL"] += float(row[i] or 0)
+                tot["ALL"] += float(row[i]) if row[i].replace(".", "").isdigit() else 0.0
 for h, v in sorted(tot.items(), key=lambda t: -t[1])[:15]:
     print(f"{h:40s} {v:10.0f}")

@@ -17,6 +17,7 @@ import sys
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+os.environ.setdefault("SG_LIB", "timing")
 sys.path.insert(0, ROOT)
 
 NAMES = ["start", "bar_prev", "stage_x", "phase_A(t=Bx)", "bar1", "phase_B(mask)", "bar2",
@@ -85,7 +86,7 @@ def main():
         prev = k
     if True:
         for name, a, b in (("  B.ts+wait", 4, 11), ("  B.dots", 11, 12), ("  B.compact", 12, 5),
-                           ("  C.probe_t", 6, 28), ("  C.prefix_w0", 28, 26), ("  C.probe2", 26, 27), ("  C.prefix_again", 26, 29), ("  C.prefix_sync", 26, 25), ("  C.items", 25, 16), ("  C.first_row", 16, 17), ("  C.stream", 17, 21), ("  C.tail", 21, 14),
+                           ("  C.probe_t", 6, 28), ("  C.prefix_w0", 28, 26), ("  C.probe2", 26, 27), ("  C.prefix_again", 26, 29), ("  C.prefix_sync", 26, 25), ("  C.items", 25, 16), ("  C.prod_entry", 16, 28), ("  C.prod_waited", 16, 31), ("  C.issue_slot0", 16, 27), ("  C.first_row", 16, 17), ("  C.stream", 17, 21), ("  C.tail", 21, 14),
                            ("  C.gather", 6, 14), ("  C.up", 14, 15), ("  C.partial_down", 15, 7),
                            ("  D.partials", 8, 13), ("  D.final", 13, 9)):
             if pipe == 0 and name.startswith("  B."):
