@@ -185,6 +185,19 @@ sg_status sg_op_count_model(int64_t d, int64_t D, int64_t r, double s, double s_
 /* Host rounding used on upload: f64 -> f32 (RNE) -> bf16 (RNE), NaN-preserving. */
 void sg_round_bf16(const double* in, uint16_t* out, int64_t n);
 
+/* ---- multi-GPU sharding, pure host ----
+ * The neuron set a shard holds: global index of local k = base + k*stride,
+ * k in [0, count). Exactly the mapping sg_layer_create applies. */
+sg_status sg_shard_range(int64_t inter, int32_t shard_index, int32_t shard_count,
+                         int32_t shard_interleave, int64_t* base, int64_t* stride, int64_t* count);
+
+/* ExecStats of the WHOLE layer from counts summed over shards (|P|, |V|), with the
+ * reference formulas of ffn_exec.hpp:120, :173-180, :209-216 over the global
+ * inter. (A single shard's sg_ctx_read_stats reports its local inter.) */
+sg_status sg_exec_stats_from_counts(int64_t hidden, int64_t inter, int64_t rank,
+                                    sg_pipeline pipeline, int64_t predicted_active,
+                                    int64_t revalidated, sg_exec_stats* out);
+
 /* ---- host-side producers of the executor's inputs (not on the device path) ---- */
 
 /* synthetic.hpp:80-108 (make_synthetic_fixture), same mt19937_64 stream order.

@@ -82,6 +82,10 @@ SYMBOLS = [
     ("sg_op_count_model", C.c_int, [_I64, _I64, _I64, _D, _D, C.POINTER(_I64), C.POINTER(_D),
                                     C.POINTER(_D)]),
     ("sg_round_bf16", None, [_VP, _VP, _I64]),
+    ("sg_shard_range", C.c_int, [_I64, _I32, _I32, _I32, C.POINTER(_I64), C.POINTER(_I64),
+                                 C.POINTER(_I64)]),
+    ("sg_exec_stats_from_counts", C.c_int, [_I64, _I64, _I64, C.c_int, _I64, _I64,
+                                            C.POINTER(sg_exec_stats)]),
     ("sg_synthetic_fixture", C.c_int, [_I64, _I64, _I64, _I64, _D, C.c_uint64, _VP, _VP, _VP,
                                        _VP, _VP]),
     ("sg_synthetic_fixture_bf16", C.c_int, [_I64, _I64, _I64, _I64, _D, C.c_uint64, _VP, _VP,

@@ -154,9 +154,23 @@ struct DeviceGuard {
 
 int64_t local_to_global(const sg_layer* L, int64_t k) { return L->gbase + k * L->gstride; }
 
-sg_exec_stats make_stats(const sg_layer* L, int pipeline, int64_t p, int64_t v) {
+// interleaved (neuron base + k*S) or contiguous near-equal blocks.
+void shard_map(int64_t D, int64_t si, int64_t S, bool interleave, int64_t* base, int64_t* stride,
+               int64_t* count) {
+    if (S > 1 && interleave) {
+        *base = si;
+        *stride = S;
+        *count = si < D ? (D - si + S - 1) / S : 0;
+    } else {
+        const int64_t lo = D * si / S, hi = D * (si + 1) / S;
+        *base = lo;
+        *stride = 1;
+        *count = hi - lo;
+    }
+}
+
+sg_exec_stats stats_from_counts(int64_t d, int64_t D, int64_t r, int pipeline, int64_t p, int64_t v) {
     sg_exec_stats s{};
-    const int64_t d = L->d, D = L->D_local, r = L->r;
     s.pipeline = pipeline;
     s.predicted_active = p;
     s.revalidated = v;
@@ -174,6 +188,10 @@ sg_exec_stats make_stats(const sg_layer* L, int pipeline, int64_t p, int64_t v) 
         s.realized_sparsity = 1.0 - static_cast<double>(v) / static_cast<double>(D);
     }
     return s;
+}
+
+sg_exec_stats make_stats(const sg_layer* L, int pipeline, int64_t p, int64_t v) {
+    return stats_from_counts(L->d, L->D_local, L->r, pipeline, p, v);
 }
 
 sg::WorkView work_for(sg_ctx* ctx, const float* x, float* y) {
@@ -232,6 +250,30 @@ sg_status sg_op_count_model(int64_t d, int64_t D, int64_t r, double s, double sp
     if (dense) *dense = dn;
     if (sparse) *sparse = sps;
     if (ratio) *ratio = static_cast<double>(dn) / sps;
+    return SG_OK;
+}
+
+sg_status sg_shard_range(int64_t inter, int32_t shard_index, int32_t shard_count,
+                         int32_t shard_interleave, int64_t* base, int64_t* stride, int64_t* count) {
+    if (inter < 1) return fail(SG_ERR_DATA, "shard range: inter must be positive");
+    const int64_t S = shard_count > 1 ? shard_count : 1;
+    const int64_t si = S > 1 ? shard_index : 0;
+    if (si < 0 || si >= S) return fail(SG_ERR_USAGE, "shard_index out of range");
+    if (base == nullptr || stride == nullptr || count == nullptr) return fail(SG_ERR_USAGE, "null output");
+    shard_map(inter, si, S, shard_interleave != 0, base, stride, count);
+    return SG_OK;
+}
+
+sg_status sg_exec_stats_from_counts(int64_t hidden, int64_t inter, int64_t rank, sg_pipeline pipeline,
+                                    int64_t predicted_active, int64_t revalidated, sg_exec_stats* out) {
+    if (hidden < 1 || inter < 1 || rank < 0) return fail(SG_ERR_DATA, "stats: bad dimensions");
+    if (pipeline < SG_PIPELINE_DENSE || pipeline > SG_PIPELINE_SEQUENTIAL)
+        return fail(SG_ERR_USAGE, "stats: unknown pipeline");
+    if (predicted_active < 0 || predicted_active > inter || revalidated < 0 ||
+        revalidated > predicted_active)
+        return fail(SG_ERR_USAGE, "stats: counts out of range");
+    if (out == nullptr) return fail(SG_ERR_USAGE, "null output");
+    *out = stats_from_counts(hidden, inter, rank, pipeline, predicted_active, revalidated);
     return SG_OK;
 }
 
@@ -295,16 +337,7 @@ sg_status sg_layer_create(const sg_layer_desc* desc, sg_layer** out) {
         delete L;
         return fail(SG_ERR_USAGE, "shard_index out of range");
     }
-    if (S > 1 && desc->shard_interleave) {
-        L->gbase = si;
-        L->gstride = S;
-        L->D_local = (D - si + S - 1) / S;
-    } else {
-        const int64_t lo = D * si / S, hi = D * (si + 1) / S;
-        L->gbase = lo;
-        L->gstride = 1;
-        L->D_local = hi - lo;
-    }
+    shard_map(D, si, S, S > 1 && desc->shard_interleave, &L->gbase, &L->gstride, &L->D_local);
     if (L->D_local < 1) {
         delete L;
         return fail(SG_ERR_USAGE, "shard holds no neurons");

@@ -20,8 +20,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 os.environ.setdefault("SG_LIB", "timing")
 sys.path.insert(0, ROOT)
 
-NAMES = ["start", "bar_prev", "stage_x", "phase_A(t=Bx)", "bar1", "phase_B(mask)", "bar2",
-         "phase_C(gate/up+partial)", "bar3", "phase_D(reduce)"]
+NAMES = {0: "start", 1: "bar_prev", 2: "stage_x", 3: "phase_A(t=Bx)", 4: "bar1",
+         6: "phase_B(mask+compact)", 14: "phase_C(gate stream)", 7: "stage4+5a(up/down)",
+         8: "bar3", 9: "phase_D(reduce)"}
 
 
 def main():
@@ -72,7 +73,7 @@ def main():
     st = buf[: L * G * 32].reshape(L, G, 32).astype(np.int64)
     t0 = st[:, :, 0].min(axis=1, keepdims=True)
     rel = (st - t0[:, :, None]) / 1000.0  # us
-    used = [0, 1, 2, 3, 4, 5, 6, 7, 8, 9] if pipe != 0 else [0, 1, 2, 7, 8, 9]
+    used = [0, 1, 2, 3, 4, 6, 14, 7, 8, 9] if pipe != 0 else [0, 1, 2, 14, 7, 8, 9]
     rows = []
     prev = None
     for k in used:
@@ -84,20 +85,6 @@ def main():
         worst = np.median((rel[:, :, k] - rel[:, :, prev]).max(axis=1))
         rows.append((NAMES[k], crit, busy, worst))
         prev = k
-    if True:
-        for name, a, b in (("  B.ts+wait", 4, 11), ("  B.dots", 11, 12), ("  B.compact", 12, 5),
-                           ("  C.probe_t", 6, 28), ("  C.prefix_w0", 28, 26), ("  C.probe2", 26, 27), ("  C.prefix_again", 26, 29), ("  C.prefix_sync", 26, 25), ("  C.items", 25, 16), ("  C.prod_entry", 16, 28), ("  C.prod_waited", 16, 31), ("  C.issue_slot0", 16, 27), ("  C.first_row", 16, 17), ("  C.stream", 17, 21), ("  C.tail", 21, 14),
-                           ("  C.gather", 6, 14), ("  C.up", 14, 15), ("  C.partial_down", 15, 7),
-                           ("  D.partials", 8, 13), ("  D.final", 13, 9)):
-            if pipe == 0 and name.startswith("  B."):
-                continue
-            crit = np.median(rel[:, :, b].max(axis=1) - rel[:, :, a].max(axis=1))
-            rows.append((name, crit, np.median((rel[:, :, b] - rel[:, :, a]).mean(axis=1)),
-                         np.median((rel[:, :, b] - rel[:, :, a]).max(axis=1))))
-    if pipe != 0:
-        cyc = st[:, :, 30].astype(np.float64)
-        rows.append(("  C.prefix_w0 (clock64 us@1.965GHz)", np.median(cyc.max(axis=1)) / 1965.0,
-                     np.median(cyc.mean(axis=1)) / 1965.0, np.median(cyc.max(axis=1)) / 1965.0))
     layer_us = np.median(rel[:, :, used[-1]].max(axis=1) - rel[:, :, 0].min(axis=1))
     print(f"config={args.config} layers={L} pipeline={args.pipeline} G={G}")
     print(f"{'phase':20s} {'critical_us':>12s} {'mean_cta_us':>12s} {'max_cta_us':>12s}")
