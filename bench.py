@@ -330,12 +330,19 @@ def main():
                                              C.c_void_p(xh.data_ptr()), C.c_void_p(yh.data_ptr()),
                                              0, None, C.c_void_p(sh)))
 
-    e2e = None
-    if world == 1:
-        ke = max(10, min(args.steps, 500))
-        ms_e2e, _ = timed(step_e2e, ke, 3)
-        e2e = {"value": 1000.0 / ms_e2e, "unit": "tokens/s", "h2d_bytes_per_step": L * d * 4,
-               "d2h_bytes_per_step": L * d * 4, "ms_per_step": ms_e2e, "steps": ke}
+    def step_e2e_sharded():
+        # same call shape with the per-layer NCCL exchange: pinned x in, full y out
+        xs.copy_(xh, non_blocking=True)
+        step_layers()
+        yh.copy_(ys, non_blocking=True)
+        stream.synchronize()
+
+    ke = max(10, min(args.steps, 500))
+    ms_e2e, _ = timed(step_e2e if world == 1 else step_e2e_sharded, ke, 3)
+    e2e = {"value": 1000.0 / ms_e2e, "unit": "tokens/s", "h2d_bytes_per_step": L * d * 4,
+           "d2h_bytes_per_step": L * d * 4, "ms_per_step": ms_e2e, "steps": ke,
+           "call": "sg_ffn_forward_layers_host" if world == 1 else
+                   "H2D + per-layer sg_ffn_forward_device + NCCL all_reduce + D2H"}
 
     dense = None
     if not args.no_dense:
@@ -352,7 +359,9 @@ def main():
         try:
             with open(tp) as f:
                 tj = json.load(f)
-            traffic = tj.get(args.config)
+            meta = tj.get("_meta", {}).get(args.config)
+            if meta and Dl == D:  # ncu DRAM bytes per layer x layers per launch of this run
+                traffic = meta["per_layer"] * (L / launches_per_step)
         except Exception:
             traffic = None
 

@@ -58,7 +58,8 @@ constexpr int kGroups = kWarps / kGroupWarps;
 constexpr int kGroupThreads = kGroupWarps * 32;
 constexpr int kStageOff = 4096;           // staged B rows / A slice start here in the big region
 constexpr int kXRegChunks = 4;            // x chunks per thread held in registers (pitch_d <= 4096)
-constexpr int kSurvBatch = 4;             // survivors per round in stages 4+5a
+constexpr int kBatch = 8;                 // rows per transposed warp reduction (stage 4)
+constexpr int kSvChunk = 12;              // survivor [up | down] rows staged per round (stage 4/5a)
 constexpr int kSector = 8;                // ints per 32-B sector
 
 // Shared memory: small fixed arrays, then one large region that is, in turn,
@@ -84,6 +85,7 @@ struct SmemPlan {
     int as_bytes;    // A slice capacity in smem (0 = stream A from HBM)
     int mask_cap;
     int item_cap;
+    int off_sv;      // int2[item_cap] survivor list {n, g} (sequential pipeline), float[kSvChunk] z
     int total;
 };
 
@@ -99,6 +101,7 @@ struct Smem {
     float* reda;
     int* items;
     int2* recs;
+    int2* svl;
     float* xs;
     float* ts;
     uint8_t* big;
@@ -117,6 +120,7 @@ __device__ __forceinline__ Smem carve(uint8_t* base, const SmemPlan& S) {
     m.reda = reinterpret_cast<float*>(base + S.off_reda);
     m.items = reinterpret_cast<int*>(base + S.off_items);
     m.recs = reinterpret_cast<int2*>(base + S.off_recs);
+    m.svl = reinterpret_cast<int2*>(base + S.off_sv);
     m.xs = reinterpret_cast<float*>(base + S.off_xs);
     m.ts = reinterpret_cast<float*>(base + S.off_ts);
     m.big = base + S.off_big;
@@ -719,7 +723,7 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
     __syncthreads();
     if (kPipe != 0) {
         // survivors of this CTA's items, in P order -> smem list + global segment
-        int2* list = reinterpret_cast<int2*>(sm.big);
+        int2* list = kPipe == 2 ? sm.svl : reinterpret_cast<int2*>(sm.big);
         if (warp == 0) {
             int run = 0;
             for (int base = 0; base < nitems; base += 32) {
@@ -745,96 +749,134 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
 }
 
 // ---------------------------------------------------------------------------
-// Stages 4+5a of the sequential pipeline, per CTA, after its gate stream, in
-// one pass over its survivors (their [up | down] rows were prefetched to L2):
-// kSurvBatch survivors per round; thread t owns chunk t (and t+512, ...). Per
-// survivor: u = up·x reduced thread-chain -> warp butterfly -> 16 warps in
-// order; z = gated(g, u); then the thread's down chunk accumulates z·down
-// (survivors in P order) into this CTA's partial y.
+// Stages 4+5a of the sequential pipeline, per CTA, after its gate stream. The
+// survivors' [up | down] rows (16 KB each, contiguous, sent to L2 during the
+// gate stream) are bulk-copied into shared memory, up to kSvChunk at a time.
+// Thread t owns chunk t (and t + 512) of every row with x in registers: the
+// up rows of a chunk are dotted kBatch at a time (8 independent FMA chains,
+// one transposed warp butterfly, warps summed in order), warp 0 forms
+// z = gated(g, u) (ffn_exec.hpp:202-203, :68-76), and every thread adds z·down
+// for its chunk into its partial y, survivors in P order.
 // ---------------------------------------------------------------------------
-__device__ void survivor_updown(const LayerView& L, const WorkView& W, const Smem& sm) {
-    const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int nch = L.pitch_d >> 3;
-    const int n0 = split_lo(c, G, L.D);
-    int2* list = reinterpret_cast<int2*>(sm.big);
-    float* red = sm.reda;
-    float* zs = red + kSurvBatch * kWarps;
-    const int cnt = sm.misc[1];
-    const int ch0 = tid;
-    const bool has0 = tid < kCThreads && ch0 < nch;
-    float acc0[8];
+// Sum of v[0..7] over the 32 lanes, transposed: 9 shuffles instead of 40.
+// Afterwards lane l holds the total of item 4*(l>>4 & 1) + 2*(l>>3 & 1) + (l>>2 & 1).
+__device__ __forceinline__ float warp_sum8(float* v, int lane) {
+    const bool hi16 = lane & 16;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc0[e] = 0.f;
-    for (int b0 = 0; b0 < cnt; b0 += kSurvBatch) {
-        const int nb = cnt - b0 < kSurvBatch ? cnt - b0 : kSurvBatch;
-        float pu[kSurvBatch];
-        uint4 dn[kSurvBatch];
-#pragma unroll
-        for (int q = 0; q < kSurvBatch; ++q) {
-            pu[q] = 0.f;
-            dn[q] = make_uint4(0, 0, 0, 0);
-        }
-        if (tid < kCThreads) {
-            uint4 w[kSurvBatch];
-#pragma unroll
-            for (int q = 0; q < kSurvBatch; ++q) {
-                const uint16_t* row =
-                    L.ud + static_cast<size_t>(q < nb ? list[b0 + q].x : 0) * 2 * L.pitch_d;
-                w[q] = (q < nb && has0) ? ldg_stream(row + ch0 * 8) : make_uint4(0, 0, 0, 0);
-                if (q < nb && has0) dn[q] = ldg_stream(row + L.pitch_d + ch0 * 8);
-            }
-#pragma unroll
-            for (int q = 0; q < kSurvBatch; ++q)
-                if (has0) pu[q] = dot8(w[q], sm.xs + ch0 * 8, pu[q]);
-            for (int ch = ch0 + kCThreads; ch < nch; ch += kCThreads) {
-#pragma unroll
-                for (int q = 0; q < kSurvBatch; ++q)
-                    if (q < nb)
-                        pu[q] = dot8(ldg_stream(L.ud + static_cast<size_t>(list[b0 + q].x) * 2 *
-                                                           L.pitch_d + ch * 8),
-                                     sm.xs + ch * 8, pu[q]);
-            }
-#pragma unroll
-            for (int q = 0; q < kSurvBatch; ++q) {
-                const float v = warp_sum(pu[q]);
-                if (lane == 0) red[q * kWarps + warp] = v;
-            }
-        }
-        __syncthreads();
-        if (tid < nb) {
-            float u = 0.f;
-            for (int w = 0; w < kWarps; ++w) u += red[tid * kWarps + w];
-            int2 e = list[b0 + tid];
-            const float z = gated(__int_as_float(e.y), u, L.act);
-            e.y = __float_as_int(z);
-            list[b0 + tid] = e;
-            zs[tid] = z;
-            reinterpret_cast<int2*>(W.vseg)[n0 + b0 + tid] = e;
-        }
-        __syncthreads();
-        if (has0) {
-#pragma unroll
-            for (int q = 0; q < kSurvBatch; ++q) axpy8(dn[q], q < nb ? zs[q] : 0.f, acc0);
-        }
-        __syncthreads();
+    for (int i = 0; i < 4; ++i) {
+        const float send = hi16 ? v[i] : v[i + 4];
+        const float keep = hi16 ? v[i + 4] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
-    // this CTA's partial y (chunks beyond the first 512, for pitch_d > 4096,
-    // accumulated here from L2 in list order)
-    for (int ch = ch0; tid < kCThreads && ch < nch; ch += kCThreads) {
-        float acc[8];
+    const bool hi8 = lane & 8;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = ch == ch0 ? acc0[e] : 0.f;
-        if (ch != ch0) {
-            for (int k = 0; k < cnt; ++k) {
-                const int2 en = list[k];
-                axpy8(ldg_stream(L.ud + static_cast<size_t>(en.x) * 2 * L.pitch_d + L.pitch_d +
-                                 ch * 8),
-                      __int_as_float(en.y), acc);
+    for (int i = 0; i < 2; ++i) {
+        const float send = hi8 ? v[i] : v[i + 2];
+        const float keep = hi8 ? v[i + 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    const bool hi4 = lane & 4;
+    {
+        const float send = hi4 ? v[0] : v[1];
+        const float keep = hi4 ? v[1] : v[0];
+        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    float s = v[0];
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    return s;
+}
+
+__device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkView& W,
+                                                const Smem& sm, const SmemPlan& S, RunState& rs) {
+    const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nch = L.pitch_d >> 3;
+    const int n0 = split_lo(c, gridDim.x, L.D);
+    const int nsv = sm.misc[1];
+    const uint32_t ud_bytes = static_cast<uint32_t>(L.pitch_d) * 4u;
+    float* zs = reinterpret_cast<float*>(sm.svl + S.item_cap);  // after the list
+    const int ch0 = tid, ch1 = tid + kCThreads;
+    const bool comp = tid < kCThreads;
+    const bool h0 = comp && ch0 < nch, h1 = comp && ch1 < nch;
+    float x0[8], x1[8], a0[8], a1[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        x0[e] = h0 ? sm.xs[ch0 * 8 + e] : 0.f;
+        x1[e] = h1 ? sm.xs[ch1 * 8 + e] : 0.f;
+        a0[e] = 0.f;
+        a1[e] = 0.f;
+    }
+    for (int base = 0; base < nsv; base += kSvChunk) {
+        const int m = nsv - base < kSvChunk ? nsv - base : kSvChunk;
+        if (warp == kWarps) {
+            // the ring's last generic reads ended at a block barrier
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const uint64_t pol = policy_evict_first();
+            if (lane == 0) mbar_expect_tx(sm.abar, static_cast<uint32_t>(m) * ud_bytes);
+            __syncwarp();
+            if (lane < m)
+                bulk_g2s(sm.big + static_cast<size_t>(lane) * ud_bytes,
+                         L.ud + static_cast<size_t>(sm.svl[base + lane].x) * 2 * L.pitch_d, ud_bytes,
+                         sm.abar, pol);
+            __syncwarp();
+        }
+        mbar_wait(sm.abar, rs.auses & 1u);
+        rs.auses += 1;
+        __syncwarp();
+        for (int b = 0; b < m; b += kBatch) {
+            const int nb = m - b < kBatch ? m - b : kBatch;
+            float* red = sm.reda + ((b / kBatch) & 1) * (kWarps * kBatch);
+            if (comp) {
+                float part[kBatch];
+#pragma unroll
+                for (int j = 0; j < kBatch; ++j) {
+                    part[j] = 0.f;
+                    if (j < nb) {
+                        const uint16_t* up = reinterpret_cast<const uint16_t*>(
+                            sm.big + static_cast<size_t>(b + j) * ud_bytes);
+                        float acc = 0.f;
+                        if (h0) acc = dot8r(*reinterpret_cast<const uint4*>(up + ch0 * 8), x0, acc);
+                        if (h1) acc = dot8r(*reinterpret_cast<const uint4*>(up + ch1 * 8), x1, acc);
+                        part[j] = acc;
+                    }
+                }
+                const float s = warp_sum8(part, lane);
+                if ((lane & 3) == 0)
+                    red[warp * kBatch + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)] = s;
+            }
+            __syncthreads();
+            if (tid < nb) {
+                float u = 0.f;
+                for (int w = 0; w < kWarps; ++w) u += red[w * kBatch + tid];
+                int2 e = sm.svl[base + b + tid];
+                const float z = gated(__int_as_float(e.y), u, L.act);
+                zs[b + tid] = z;
+                e.y = __float_as_int(z);
+                reinterpret_cast<int2*>(W.vseg)[n0 + base + b + tid] = e;
             }
         }
-        float4* dst = reinterpret_cast<float4*>(W.ypart + static_cast<size_t>(c) * L.pitch_d + ch * 8);
-        dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-        dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        __syncthreads();  // zs complete
+        if (comp) {
+            for (int i = 0; i < m; ++i) {
+                const uint16_t* dn =
+                    reinterpret_cast<const uint16_t*>(sm.big + static_cast<size_t>(i) * ud_bytes) + L.pitch_d;
+                const float z = zs[i];
+                if (h0) axpy8(*reinterpret_cast<const uint4*>(dn + ch0 * 8), z, a0);
+                if (h1) axpy8(*reinterpret_cast<const uint4*>(dn + ch1 * 8), z, a1);
+            }
+        }
+        __syncthreads();  // the chunk's rows and zs are no longer read
+    }
+    // this CTA's partial y
+    if (h0) {
+        float4* dst = reinterpret_cast<float4*>(W.ypart + static_cast<size_t>(c) * L.pitch_d + ch0 * 8);
+        dst[0] = make_float4(a0[0], a0[1], a0[2], a0[3]);
+        dst[1] = make_float4(a0[4], a0[5], a0[6], a0[7]);
+    }
+    if (h1) {
+        float4* dst = reinterpret_cast<float4*>(W.ypart + static_cast<size_t>(c) * L.pitch_d + ch1 * 8);
+        dst[0] = make_float4(a1[0], a1[1], a1[2], a1[3]);
+        dst[1] = make_float4(a1[4], a1[5], a1[6], a1[7]);
     }
 }
 
@@ -1025,7 +1067,7 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
     phase_gather<kPipe>(L, W, sm, S, rs);
     SG_STAMP(dbg, 14);
     if (kPipe == 2) {
-        survivor_updown(L, W, sm);
+        survivor_updown(L, W, sm, S, rs);
     } else {
         partial_down<kPipe>(L, W, sm);
     }
@@ -1119,6 +1161,8 @@ bool make_plan(int G, int pitch_d, int r, int pitch_r, int Dl, int pipe, int max
     off += S->item_cap * 4;
     S->off_recs = off = align_up(off, 16);
     off += S->item_cap * 8;
+    S->off_sv = off = align_up(off, 16);
+    off += S->item_cap * 8 + kSvChunk * 4;
     S->off_xs = off = align_up(off, 128);
     off += pitch_d * 4;
     S->off_ts = off = align_up(off, 128);
