@@ -806,8 +806,10 @@ __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkVi
         a0[e] = 0.f;
         a1[e] = 0.f;
     }
-    for (int base = 0; base < nsv; base += kSvChunk) {
-        const int m = nsv - base < kSvChunk ? nsv - base : kSvChunk;
+    int chunk = S.big_bytes / static_cast<int>(ud_bytes);  // rows that fit in the big region
+    if (chunk > kSvChunk) chunk = kSvChunk;
+    for (int base = 0; base < nsv; base += chunk) {
+        const int m = nsv - base < chunk ? nsv - base : chunk;
         if (warp == kWarps) {
             // the ring's last generic reads ended at a block barrier
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

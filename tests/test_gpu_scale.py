@@ -1,0 +1,131 @@
+"""GPU parity at BASELINE.json sizes, for d_ff shards, and for multi-layer launches.
+
+* Full-size layers of configs[1..3] (7B ReGLU, Mistral-7B dReLU, 13B ReGLU),
+  built exactly as the bench builds them (paper_2603_14110_b200.model), checked
+  token by token against the f64 oracle under the rules of tests/parity_util.py.
+* d_ff sharding on one GPU: the shards of a layer, run one after
+  the other, must sum to the unsharded layer and their index sets must be the
+  global sets (the exchange itself is covered on CPU by tests/test_sharded_cpu.py).
+* The multi-layer persistent launch (sg_ffn_forward_layers) must equal layer-by-
+  layer launches bit for bit, with and without chaining.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2603_14110_b200 import (Activation, DeviceLayer, Pipeline, bf16_to_f64, read_sets,
+                                   read_stats)
+from paper_2603_14110_b200 import _capi as capi
+from paper_2603_14110_b200.ffn_exec import Context, check
+from paper_2603_14110_b200.model import CONFIGS, build_host_layer, upload
+from paper_2603_14110_b200.sharded import shard_indices, stats_from_counts
+from parity_util import Y_RTOL, check_token, q_f32, quantize_layer
+from test_gpu_parity import _calibrated_layer
+
+pytestmark = pytest.mark.gpu
+
+
+def _host_q(h):
+    return dict(gate=bf16_to_f64(h.gate), up=bf16_to_f64(h.up),
+                down=np.ascontiguousarray(bf16_to_f64(h.down_t).T), A=bf16_to_f64(h.A),
+                B=bf16_to_f64(h.B), bias=q_f32(h.bias))
+
+
+@pytest.mark.parametrize("config", ["7b", "mistral", "13b"])
+def test_full_size_layer_parity(config):
+    cfg = CONFIGS[config]
+    d, D, act = cfg["d"], cfg["D"], cfg["act"]
+    h = build_host_layer(d, D, act, seed=1, rank=256, sparsity=0.5, eval_tokens=3)
+    layer = upload(h, d, D, act, 256)
+    q = _host_q(h)
+    ctx = layer.context()
+    for t in range(h.xs.shape[1]):
+        x = h.xs[:, t]
+        res = layer.forward(x, Pipeline.Sequential, ctx)
+        P, V, _, _ = read_sets(ctx, D)
+        diag = check_token(q, x, res.y, P, V, act=act)
+        assert diag["rel"] <= Y_RTOL
+        # the calibrated operating point of the bench: p ~ D/2, v ~ 0.1 D
+        assert 0.3 * D < diag["p"] < 0.7 * D and 0.03 * D < diag["v"] < 0.2 * D
+        st = res.stats
+        assert st.multiplies == 256 * (d + D) + d * len(P) + 2 * d * len(V)
+
+
+@pytest.mark.parametrize("shards,interleave", [(2, False), (3, False), (2, True), (3, True)])
+def test_shards_sum_to_the_full_layer(shards, interleave):
+    d, D, r = 512, 1500, 64
+    fx, pred = _calibrated_layer(d, D, r, seed=77, calib=1024)
+    q = quantize_layer(fx.weights.gate, fx.weights.up, fx.weights.down, pred.A, pred.B, pred.bias)
+    parts = [DeviceLayer(fx.weights, pred, shard_index=k, shard_count=shards,
+                         shard_interleave=interleave) for k in range(shards)]
+    for k, lay in enumerate(parts):
+        idx = shard_indices(D, k, shards, interleave)
+        assert lay.local_inter == len(idx)
+        assert [lay.global_index(i) for i in (0, len(idx) - 1)] == [idx[0], idx[-1]]
+    for t in range(4):
+        x = fx.eval[:, t]
+        y = np.zeros(d)
+        P, V = [], []
+        p = v = 0
+        for lay in parts:
+            ctx = lay.context()
+            res = lay.forward(x, Pipeline.Sequential, ctx)
+            y += res.y
+            Pk, Vk, _, _ = read_sets(ctx, lay.local_inter)
+            P += Pk.tolist()
+            V += Vk.tolist()
+            p += res.stats.predicted_active
+            v += res.stats.revalidated
+        P, V = sorted(P), sorted(V)
+        diag = check_token(q, x, y, P, V)
+        assert diag["rel"] <= Y_RTOL
+        st = stats_from_counts(d, D, r, Pipeline.Sequential, p, v)
+        assert st.multiplies == r * (d + D) + d * len(P) + 2 * d * len(V)
+        if diag["dP"] == 0 and diag["dV"] == 0:
+            o = diag["oracle"].stats
+            assert (st.multiplies, st.predicted_sparsity, st.realized_sparsity) == \
+                (o.multiplies, o.predicted_sparsity, o.realized_sparsity)
+
+
+def _stack(layers, xs, chain, pipeline=Pipeline.Sequential):
+    import torch
+    d = layers[0].hidden
+    ctx = Context(0, d, max(l.local_inter for l in layers), max(l.rank for l in layers))
+    arr = (C.c_void_p * len(layers))(*[l.handle.value for l in layers])
+    xt = torch.tensor(np.asarray(xs, dtype=np.float32), device="cuda")
+    yt = torch.zeros_like(xt)
+    sh = torch.cuda.current_stream().cuda_stream
+    check(capi.lib().sg_ffn_forward_layers(ctx.handle, arr, len(layers), int(pipeline),
+                                           C.c_void_p(xt.data_ptr()), C.c_void_p(yt.data_ptr()),
+                                           int(chain), C.c_void_p(sh)))
+    st = (capi.sg_exec_stats * len(layers))()
+    check(capi.lib().sg_ctx_read_stack_stats(ctx.handle, C.c_void_p(sh), len(layers), st))
+    return yt.double().cpu().numpy(), [(s.predicted_active, s.revalidated) for s in st]
+
+
+@pytest.mark.parametrize("pipeline", [Pipeline.Sequential, Pipeline.Parallel, Pipeline.Dense])
+def test_stack_launch_equals_layer_launches(pipeline):
+    import torch
+    d, D, r = 512, 1408, 64
+    layers, xs = [], []
+    for s in range(3):
+        fx, pred = _calibrated_layer(d, D, r, seed=100 + s)
+        layers.append(DeviceLayer(fx.weights, pred))
+        xs.append(fx.eval[:, 0])
+    xs = np.stack(xs).astype(np.float32).astype(np.float64)
+    ys, stats = _stack(layers, xs, chain=0, pipeline=pipeline)
+    for l, lay in enumerate(layers):
+        ctx = lay.context()
+        res = lay.forward(xs[l], pipeline, ctx)
+        assert np.array_equal(ys[l], res.y), f"layer {l}"
+        if pipeline != Pipeline.Dense:
+            assert stats[l] == (res.stats.predicted_active, res.stats.revalidated)
+    # chained: layer l+1 reads layer l's output (fp32 on device)
+    yc, _ = _stack(layers, xs, chain=1, pipeline=pipeline)
+    x = xs[0]
+    for l, lay in enumerate(layers):
+        res = lay.forward(x, pipeline)
+        assert np.array_equal(yc[l], res.y), f"chained layer {l}"
+        x = res.y.astype(np.float32).astype(np.float64)
+    torch.cuda.synchronize()
