@@ -1,0 +1,462 @@
+// sparsegate-b200 — C++ drop-in for the reference executor API
+//   /root/reference/proj/include/sparsegate/ffn_exec.hpp (+ types.hpp, common.hpp)
+// implemented over the C ABI (include/sparsegate_c.h, libsparsegate_b200.so).
+//
+// Same names, argument meaning and error behaviour as the reference:
+//   dense_ffn              ffn_exec.hpp:103-122
+//   predict_mask           ffn_exec.hpp:125-146
+//   sparse_ffn_parallel    ffn_exec.hpp:149-178
+//   sparse_ffn_sequential  ffn_exec.hpp:183-218
+//   op_count_model         ffn_exec.hpp:229-244
+//   gating_error           ffn_exec.hpp:256-285
+//   FfnWeights / Predictor / validate   types.hpp:21-105
+//   Error / IoError / DataError / PropertyViolation   common.hpp:20-37
+// The reference's Mat / Vec are Eigen row-major double matrices / vectors;
+// Eigen is not part of this build, so minimal containers with the members the
+// reference code uses (rows, cols, size, data, operator(), Zero, Identity) stand
+// in. Values are f64 on the host; the device computes in bf16 weights / fp32
+// arithmetic.
+//
+// The reference functions are stateless. A GPU needs resident weights, so the
+// stateless calls here keep a per-thread cache of device layers keyed by the
+// weight / predictor buffers (address, shape and a strided content
+// fingerprint); call sparsegate::gpu::clear_cache() after mutating weights in
+// place, or use the explicit sparsegate::gpu::Layer / Context objects.
+#pragma once
+
+#include "sparsegate_c.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <initializer_list>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <utility>
+#include <vector>
+
+namespace sparsegate {
+
+using Index = std::int64_t;
+
+// ---- containers (row-major double, like the reference's Eigen types) ----
+class Mat {
+   public:
+    Mat() = default;
+    Mat(Index rows, Index cols) : r_(rows), c_(cols), v_(static_cast<size_t>(rows * cols), 0.0) {}
+    Mat(std::initializer_list<std::initializer_list<double>> rows) {
+        r_ = static_cast<Index>(rows.size());
+        c_ = r_ ? static_cast<Index>(rows.begin()->size()) : 0;
+        for (const auto& row : rows) {
+            if (static_cast<Index>(row.size()) != c_) throw std::invalid_argument("ragged Mat literal");
+            v_.insert(v_.end(), row.begin(), row.end());
+        }
+    }
+    static Mat Zero(Index rows, Index cols) { return Mat(rows, cols); }
+    static Mat Identity(Index n) {
+        Mat m(n, n);
+        for (Index i = 0; i < n; ++i) m(i, i) = 1.0;
+        return m;
+    }
+    Index rows() const { return r_; }
+    Index cols() const { return c_; }
+    Index size() const { return r_ * c_; }
+    double* data() { return v_.data(); }
+    const double* data() const { return v_.data(); }
+    double& operator()(Index i, Index j) { return v_[static_cast<size_t>(i * c_ + j)]; }
+    double operator()(Index i, Index j) const { return v_[static_cast<size_t>(i * c_ + j)]; }
+
+   private:
+    Index r_ = 0, c_ = 0;
+    std::vector<double> v_;
+};
+
+class Vec {
+   public:
+    Vec() = default;
+    explicit Vec(Index n) : v_(static_cast<size_t>(n), 0.0) {}
+    Vec(std::initializer_list<double> v) : v_(v) {}
+    static Vec Zero(Index n) { return Vec(n); }
+    Index size() const { return static_cast<Index>(v_.size()); }
+    double* data() { return v_.data(); }
+    const double* data() const { return v_.data(); }
+    double& operator()(Index i) { return v_[static_cast<size_t>(i)]; }
+    double operator()(Index i) const { return v_[static_cast<size_t>(i)]; }
+    double& operator[](Index i) { return v_[static_cast<size_t>(i)]; }
+    double operator[](Index i) const { return v_[static_cast<size_t>(i)]; }
+
+   private:
+    std::vector<double> v_;
+};
+
+// ---- errors (common.hpp:20-37) ----
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct IoError : Error {
+    using Error::Error;
+};
+struct DataError : Error {
+    using Error::Error;
+};
+struct PropertyViolation : Error {
+    using Error::Error;
+};
+// Failures with no reference counterpart (CUDA / NCCL, bad arguments).
+struct DeviceError : Error {
+    using Error::Error;
+};
+
+namespace detail {
+inline void check(sg_status s) {
+    if (s == SG_OK) return;
+    const std::string msg = sg_last_error();
+    switch (s) {
+        case SG_ERR_DATA: throw DataError(msg);
+        case SG_ERR_PROPERTY: throw PropertyViolation(msg);
+        case SG_ERR_IO: throw IoError(msg);
+        default: throw DeviceError(msg);
+    }
+}
+inline bool all_finite(const double* p, Index n) {
+    for (Index i = 0; i < n; ++i)
+        if (!std::isfinite(p[i])) return false;
+    return true;
+}
+}  // namespace detail
+
+// ---- domain types (types.hpp) ----
+enum class Activation { ReGLU, DReLU };
+inline std::string to_string(Activation a) { return a == Activation::ReGLU ? "reglu" : "drelu"; }
+
+struct FfnWeights {
+    Mat gate;  // D x d
+    Mat up;    // D x d
+    Mat down;  // d x D
+    Activation activation = Activation::ReGLU;
+    Index hidden_size() const { return gate.cols(); }
+    Index inter_size() const { return gate.rows(); }
+};
+
+struct Predictor {
+    Mat A;     // D x r
+    Mat B;     // r x d
+    Vec bias;  // D (+inf allowed)
+    Index rank = 0;
+    Index hidden_size() const { return B.cols(); }
+    Index inter_size() const { return A.rows(); }
+};
+
+// types.hpp:31-51: same checks and DataError messages.
+inline void validate(const FfnWeights& w) {
+    const Index d = w.gate.cols(), D = w.gate.rows();
+    if (d < 1 || D < 1)
+        throw DataError("ffn weights: gate must be at least 1x1, got " + std::to_string(D) + "x" +
+                        std::to_string(d));
+    if (w.up.rows() != D || w.up.cols() != d)
+        throw DataError("ffn weights: up is " + std::to_string(w.up.rows()) + "x" +
+                        std::to_string(w.up.cols()) + ", expected " + std::to_string(D) + "x" +
+                        std::to_string(d));
+    if (w.down.rows() != d || w.down.cols() != D)
+        throw DataError("ffn weights: down is " + std::to_string(w.down.rows()) + "x" +
+                        std::to_string(w.down.cols()) + ", expected " + std::to_string(d) + "x" +
+                        std::to_string(D));
+    if (!detail::all_finite(w.gate.data(), w.gate.size()) ||
+        !detail::all_finite(w.up.data(), w.up.size()) ||
+        !detail::all_finite(w.down.data(), w.down.size()))
+        throw DataError("ffn weights: non-finite entries");
+}
+
+// types.hpp:82-105.
+inline void validate(const Predictor& p) {
+    if (p.A.cols() != p.B.rows())
+        throw DataError("predictor: rank mismatch, A is " + std::to_string(p.A.rows()) + "x" +
+                        std::to_string(p.A.cols()) + " but B is " + std::to_string(p.B.rows()) +
+                        "x" + std::to_string(p.B.cols()));
+    if (p.rank != p.A.cols()) throw DataError("predictor: rank field disagrees with factor shapes");
+    if (p.bias.size() != p.A.rows())
+        throw DataError("predictor: bias length " + std::to_string(p.bias.size()) +
+                        " does not match intermediate size " + std::to_string(p.A.rows()));
+    const Index hi = std::min(p.A.rows(), p.B.cols());
+    if (p.rank < 1 || p.rank > hi)
+        throw DataError("predictor: rank " + std::to_string(p.rank) + " out of range [1, " +
+                        std::to_string(hi) + "]");
+    if (!detail::all_finite(p.A.data(), p.A.size()) || !detail::all_finite(p.B.data(), p.B.size()))
+        throw DataError("predictor: non-finite factor entries");
+}
+
+// ---- executor types (ffn_exec.hpp:27-52) ----
+struct Mask {
+    std::vector<std::uint8_t> active;
+    Index predicted_active_count = 0;
+};
+
+enum class Pipeline { Dense, Parallel, Sequential };
+inline std::string to_string(Pipeline p) {
+    switch (p) {
+        case Pipeline::Dense: return "dense";
+        case Pipeline::Parallel: return "parallel";
+        default: return "sequential";
+    }
+}
+
+struct ExecStats {
+    double predicted_sparsity = 0.0;
+    double realized_sparsity = 0.0;
+    std::int64_t multiplies = 0;
+    Pipeline pipeline = Pipeline::Dense;
+};
+
+struct FfnResult {
+    Vec y;
+    ExecStats stats;
+};
+
+struct OpCounts {
+    std::int64_t dense = 0;
+    double sparse = 0.0;
+    double ratio = 0.0;
+};
+
+struct GatingError {
+    double error_norm = 0.0;
+    double relative = 0.0;
+};
+
+// ---- explicit device objects ----
+namespace gpu {
+
+class Context {
+   public:
+    Context(int device, Index max_hidden, Index max_inter, Index max_rank) {
+        detail::check(sg_ctx_create(device, max_hidden, max_inter, max_rank, &ctx_));
+    }
+    ~Context() {
+        if (ctx_) sg_ctx_destroy(ctx_);
+    }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+    sg_ctx* get() const { return ctx_; }
+
+   private:
+    sg_ctx* ctx_ = nullptr;
+};
+
+// One layer (or d_ff shard) resident in HBM. w and/or pred may be null.
+class Layer {
+   public:
+    Layer(const FfnWeights* w, const Predictor* pred, int device = 0, int shard_index = 0,
+          int shard_count = 1, bool interleave = false) {
+        sg_layer_desc d{};
+        if (w) {
+            validate(*w);
+            d.hidden = w->hidden_size();
+            d.inter = w->inter_size();
+            d.activation = w->activation == Activation::DReLU ? SG_DRELU : SG_REGLU;
+            d.gate = w->gate.data();
+            d.up = w->up.data();
+            d.down = w->down.data();
+        }
+        if (pred) {
+            validate(*pred);
+            if (w && pred->hidden_size() != w->hidden_size())
+                throw DataError("predictor input length does not match hidden size");
+            if (w && pred->inter_size() != w->inter_size())
+                throw DataError("predictor intermediate size does not match weights");
+            d.hidden = pred->hidden_size();
+            d.inter = pred->inter_size();
+            d.rank = pred->rank;
+            d.pred_A = pred->A.data();
+            d.pred_B = pred->B.data();
+            d.bias = pred->bias.data();
+            d.bias_dtype = SG_F64;
+        }
+        if (!w && !pred) throw DataError("layer needs weights and/or a predictor");
+        d.weight_dtype = SG_F64;
+        d.device = device;
+        d.shard_index = shard_index;
+        d.shard_count = shard_count;
+        d.shard_interleave = interleave ? 1 : 0;
+        detail::check(sg_layer_create(&d, &layer_));
+        hidden_ = d.hidden;
+        inter_ = d.inter;
+        rank_ = d.rank;
+        device_ = device;
+    }
+    ~Layer() {
+        if (layer_) sg_layer_destroy(layer_);
+    }
+    Layer(const Layer&) = delete;
+    Layer& operator=(const Layer&) = delete;
+
+    sg_layer* get() const { return layer_; }
+    Index hidden() const { return hidden_; }
+    Index inter() const { return inter_; }
+    Index local_inter() const { return sg_layer_local_inter(layer_); }
+    Index rank() const { return rank_; }
+    int device() const { return device_; }
+
+    // Host x (f64) -> host y (f64) and the reference's ExecStats.
+    FfnResult forward(Context& ctx, Pipeline p, const Vec& x, void* stream = nullptr) const {
+        FfnResult r;
+        r.y = Vec(hidden_);
+        sg_exec_stats st{};
+        detail::check(sg_ffn_forward(ctx.get(), layer_, static_cast<sg_pipeline>(p), x.data(), SG_F64,
+                                     x.size(), r.y.data(), SG_F64, &st, stream));
+        r.stats.predicted_sparsity = st.predicted_sparsity;
+        r.stats.realized_sparsity = st.realized_sparsity;
+        r.stats.multiplies = st.multiplies;
+        r.stats.pipeline = static_cast<Pipeline>(st.pipeline);
+        return r;
+    }
+
+    Mask predict(Context& ctx, const Vec& x, void* stream = nullptr) const {
+        Mask m;
+        m.active.assign(static_cast<size_t>(local_inter()), 0);
+        int64_t cnt = 0;
+        detail::check(sg_predict_mask(ctx.get(), layer_, x.data(), SG_F64, x.size(), m.active.data(),
+                                      &cnt, stream));
+        m.predicted_active_count = cnt;
+        return m;
+    }
+
+   private:
+    sg_layer* layer_ = nullptr;
+    Index hidden_ = 0, inter_ = 0, rank_ = 0;
+    int device_ = 0;
+};
+
+namespace detail {
+// Strided fingerprint of a buffer (catches most in-place mutations cheaply).
+inline std::uint64_t fingerprint(const double* p, Index n) {
+    std::uint64_t h = 1469598103934665603ull ^ static_cast<std::uint64_t>(n);
+    const Index step = n > 4096 ? n / 4096 : 1;
+    for (Index i = 0; i < n; i += step) {
+        std::uint64_t b;
+        std::memcpy(&b, p + i, 8);
+        h = (h ^ b) * 1099511628211ull;
+    }
+    return h;
+}
+using Key = std::tuple<const void*, const void*, const void*, Index, Index, Index, int, std::uint64_t>;
+inline Key key_of(const FfnWeights* w, const Predictor* p) {
+    std::uint64_t f = 0;
+    const void *a = nullptr, *b = nullptr, *c = nullptr;
+    Index d = 0, D = 0, r = 0;
+    int act = 0;
+    if (w) {
+        a = w->gate.data();
+        b = w->down.data();
+        d = w->hidden_size();
+        D = w->inter_size();
+        act = static_cast<int>(w->activation);
+        f ^= fingerprint(w->gate.data(), w->gate.size()) ^ (fingerprint(w->up.data(), w->up.size()) << 1) ^
+             (fingerprint(w->down.data(), w->down.size()) << 2);
+    }
+    if (p) {
+        c = p->A.data();
+        r = p->rank;
+        f ^= (fingerprint(p->A.data(), p->A.size()) << 3) ^ (fingerprint(p->B.data(), p->B.size()) << 4) ^
+             (fingerprint(p->bias.data(), p->bias.size()) << 5);
+    }
+    return Key{a, b, c, d, D, r, act, f};
+}
+struct Cache {
+    std::map<Key, std::unique_ptr<Layer>> layers;
+    std::unique_ptr<Context> ctx;
+    Index cd = 0, cD = 0, cr = 0;
+};
+inline Cache& cache() {
+    thread_local Cache c;
+    return c;
+}
+}  // namespace detail
+
+inline void clear_cache() {
+    detail::cache().layers.clear();
+    detail::cache().ctx.reset();
+}
+
+inline const Layer& layer_for(const FfnWeights* w, const Predictor* p) {
+    auto& c = detail::cache();
+    const auto k = detail::key_of(w, p);
+    auto it = c.layers.find(k);
+    if (it == c.layers.end()) {
+        if (c.layers.size() >= 64) c.layers.clear();  // bounded
+        it = c.layers.emplace(k, std::make_unique<Layer>(w, p)).first;
+    }
+    return *it->second;
+}
+
+inline Context& context_for(const Layer& l) {
+    auto& c = detail::cache();
+    const Index r = l.rank() > 0 ? l.rank() : 1;
+    if (!c.ctx || l.hidden() > c.cd || l.inter() > c.cD || r > c.cr) {
+        c.cd = std::max(c.cd, l.hidden());
+        c.cD = std::max(c.cD, l.inter());
+        c.cr = std::max(c.cr, r);
+        c.ctx.reset();
+        c.ctx = std::make_unique<Context>(l.device(), c.cd, c.cD, c.cr);
+    }
+    return *c.ctx;
+}
+
+}  // namespace gpu
+
+// ---- the reference API ----
+inline FfnResult dense_ffn(const FfnWeights& w, const Vec& x) {
+    const auto& l = gpu::layer_for(&w, nullptr);
+    return l.forward(gpu::context_for(l), Pipeline::Dense, x);
+}
+
+inline Mask predict_mask(const Predictor& pred, const Vec& x) {
+    const auto& l = gpu::layer_for(nullptr, &pred);
+    return l.predict(gpu::context_for(l), x);
+}
+
+inline FfnResult sparse_ffn_parallel(const FfnWeights& w, const Predictor& pred, const Vec& x) {
+    const auto& l = gpu::layer_for(&w, &pred);
+    return l.forward(gpu::context_for(l), Pipeline::Parallel, x);
+}
+
+inline FfnResult sparse_ffn_sequential(const FfnWeights& w, const Predictor& pred, const Vec& x) {
+    const auto& l = gpu::layer_for(&w, &pred);
+    return l.forward(gpu::context_for(l), Pipeline::Sequential, x);
+}
+
+inline OpCounts op_count_model(std::int64_t d, std::int64_t D, std::int64_t r, double s,
+                               double s_prime) {
+    OpCounts c;
+    detail::check(sg_op_count_model(d, D, r, s, s_prime, &c.dense, &c.sparse, &c.ratio));
+    return c;
+}
+
+// ffn_exec.hpp:256-285: dropped gate mass under the (device) predictor mask;
+// the gate projection itself is evaluated on the host in f64.
+inline GatingError gating_error(const FfnWeights& w, const Predictor& pred, const Vec& x) {
+    validate(w);
+    if (x.size() != w.hidden_size())
+        throw DataError("input length " + std::to_string(x.size()) + " does not match hidden size " +
+                        std::to_string(w.hidden_size()));
+    if (!detail::all_finite(x.data(), x.size())) throw DataError("input: non-finite entries");
+    const Mask m = predict_mask(pred, x);
+    double e2 = 0.0, xx = 0.0;
+    for (Index i = 0; i < w.inter_size(); ++i) {
+        if (m.active[static_cast<size_t>(i)]) continue;
+        double g = 0.0;
+        for (Index j = 0; j < w.hidden_size(); ++j) g += w.gate(i, j) * x[j];
+        if (g > 0.0) e2 += g * g;
+    }
+    for (Index j = 0; j < x.size(); ++j) xx += x[j] * x[j];
+    if (xx == 0.0) throw DataError("gating error: zero input has no relative form");
+    GatingError err;
+    err.error_norm = std::sqrt(e2);
+    err.relative = err.error_norm / std::sqrt(xx);
+    return err;
+}
+
+}  // namespace sparsegate
