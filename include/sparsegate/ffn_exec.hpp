@@ -332,13 +332,18 @@ class Layer {
 
 namespace detail {
 // Strided fingerprint of a buffer (catches most in-place mutations cheaply).
-inline std::uint64_t fingerprint(const double* p, Index n) {
-    std::uint64_t h = 1469598103934665603ull ^ static_cast<std::uint64_t>(n);
+inline std::uint64_t mix64(std::uint64_t z) {  // splitmix64 finalizer: full avalanche
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+inline std::uint64_t fingerprint(const double* p, Index n, std::uint64_t salt) {
+    std::uint64_t h = mix64(salt ^ static_cast<std::uint64_t>(n));
     const Index step = n > 4096 ? n / 4096 : 1;
     for (Index i = 0; i < n; i += step) {
         std::uint64_t b;
         std::memcpy(&b, p + i, 8);
-        h = (h ^ b) * 1099511628211ull;
+        h = mix64(h ^ b);
     }
     return h;
 }
@@ -354,14 +359,16 @@ inline Key key_of(const FfnWeights* w, const Predictor* p) {
         d = w->hidden_size();
         D = w->inter_size();
         act = static_cast<int>(w->activation);
-        f ^= fingerprint(w->gate.data(), w->gate.size()) ^ (fingerprint(w->up.data(), w->up.size()) << 1) ^
-             (fingerprint(w->down.data(), w->down.size()) << 2);
+        f = mix64(f ^ fingerprint(w->gate.data(), w->gate.size(), 1));
+        f = mix64(f ^ fingerprint(w->up.data(), w->up.size(), 2));
+        f = mix64(f ^ fingerprint(w->down.data(), w->down.size(), 3));
     }
     if (p) {
         c = p->A.data();
         r = p->rank;
-        f ^= (fingerprint(p->A.data(), p->A.size()) << 3) ^ (fingerprint(p->B.data(), p->B.size()) << 4) ^
-             (fingerprint(p->bias.data(), p->bias.size()) << 5);
+        f = mix64(f ^ fingerprint(p->A.data(), p->A.size(), 4));
+        f = mix64(f ^ fingerprint(p->B.data(), p->B.size(), 5));
+        f = mix64(f ^ fingerprint(p->bias.data(), p->bias.size(), 6));
     }
     return Key{a, b, c, d, D, r, act, f};
 }

@@ -374,8 +374,23 @@ _cache: dict = {}
 _cache_lock = threading.Lock()
 
 
+def _fingerprint(*arrays) -> int:
+    """Strided content sample of the arrays: an in-place change of weights (or a
+    swapped array) gives a new device layer instead of a stale one."""
+    h = []
+    for a in arrays:
+        a = np.asarray(a)
+        flat = a.reshape(-1)
+        step = max(1, flat.size // 4096)
+        h.append((id(a), a.shape, hash(flat[::step].tobytes())))
+    return hash(tuple(h))
+
+
 def _layer_for(w: Optional[FfnWeights], pred: Optional[Predictor], device: int = 0) -> DeviceLayer:
-    key = (id(w), id(pred), device)
+    fp = _fingerprint(*(() if w is None else (w.gate, w.up, w.down)),
+                      *(() if pred is None else (pred.A, pred.B, pred.bias)))
+    key = (id(w), id(pred), device, fp, None if w is None else int(w.activation),
+           None if pred is None else int(pred.rank))
     with _cache_lock:
         hit = _cache.get(key)
         if hit is not None:
@@ -384,6 +399,8 @@ def _layer_for(w: Optional[FfnWeights], pred: Optional[Predictor], device: int =
                 return layer
     layer = DeviceLayer(w, pred, device)
     with _cache_lock:
+        for k in [k for k in _cache if k[:3] == key[:3]]:  # superseded contents of the same objects
+            _cache.pop(k, None)
         _cache[key] = (weakref.ref(w) if w is not None else (lambda: None),
                        weakref.ref(pred) if pred is not None else (lambda: None), layer)
         for obj in (w, pred):
