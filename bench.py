@@ -222,6 +222,8 @@ def main():
     ap.add_argument("--mode", default="stack", choices=["stack", "per-layer"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-balance", action="store_true",
+                    help="ascending neuron layout instead of the load-balanced order")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup()
@@ -251,7 +253,7 @@ def main():
     d, D, L = cfg["d"], cfg["D"], len(host)
     log(f"host model built in {time.time() - t0:.1f}s")
     layers = [upload(h, d, D, cfg["act"], args.rank, device=local, shard_index=rank,
-                     shard_count=world) for h in host]
+                     shard_count=world, balance=not args.no_balance) for h in host]
     Dl = layers[0].local_inter
     ctx = Context(local, d, Dl, args.rank)
     lib = capi.lib()
@@ -387,6 +389,8 @@ def main():
                        "l2": "no flush: each step streams %.2f GB of distinct layers (> 126 MB L2)"
                              % (alg_bytes / 1e9),
                        "predictor": "naive-mode randomized rank-r SVD + greedy calibration (eta 8)",
+                       "layout": "ascending" if args.no_balance else
+                                 "per-CTA load-balanced neuron order from calibration statistics",
                        "mode": "stack (one persistent launch per step)" if step is step_stack
                                else "per-layer launches"},
             "per_layer_us": ms * 1000.0 / L,

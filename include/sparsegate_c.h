@@ -97,6 +97,14 @@ typedef struct sg_layer_desc {
   int32_t shard_count; /* 0 or 1 = unsharded */
   int32_t shard_interleave;
   int32_t down_neuron_major; /* 1: `down` is already inter x hidden (neuron-major) */
+  /* Optional device layout order of the neurons (a permutation of 0..inter-1, or
+   * NULL = ascending). The executor gives CTA c the c-th contiguous block of the
+   * layout, so an order built from offline activity statistics (the calibrated
+   * predictor's hot / cold neurons) balances the per-CTA work. Results are the
+   * same function of the data; the summation order of y follows the layout.
+   * Index sets (sg_ctx_read_sets) are still reported ascending in GLOBAL indices;
+   * sg_predict_mask's mask and sg_layer_global_index use the local (layout) index. */
+  const int64_t* neuron_order;
 } sg_layer_desc;
 
 typedef struct sg_layer sg_layer;

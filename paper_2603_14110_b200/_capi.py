@@ -52,6 +52,7 @@ class sg_layer_desc(C.Structure):
         ("shard_count", C.c_int32),
         ("shard_interleave", C.c_int32),
         ("down_neuron_major", C.c_int32),
+        ("neuron_order", C.c_void_p),
     ]
 
 

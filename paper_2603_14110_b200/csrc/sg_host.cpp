@@ -41,6 +41,7 @@ struct sg_layer {
     int64_t gbase = 0, gstride = 1;
     void* dmem = nullptr;
     size_t bytes = 0;
+    std::vector<int> gidx;  // local -> global when a layout order was given (else empty)
     sg::LayerView view{};
 };
 
@@ -152,7 +153,9 @@ struct DeviceGuard {
     }
 };
 
-int64_t local_to_global(const sg_layer* L, int64_t k) { return L->gbase + k * L->gstride; }
+int64_t local_to_global(const sg_layer* L, int64_t k) {
+    return L->gidx.empty() ? L->gbase + k * L->gstride : L->gidx[static_cast<size_t>(k)];
+}
 
 // interleaved (neuron base + k*S) or contiguous near-equal blocks.
 void shard_map(int64_t D, int64_t si, int64_t S, bool interleave, int64_t* base, int64_t* stride,
@@ -343,6 +346,24 @@ sg_status sg_layer_create(const sg_layer_desc* desc, sg_layer** out) {
         return fail(SG_ERR_USAGE, "shard holds no neurons");
     }
     const int64_t Dl = L->D_local, pd = L->pitch_d, pr = L->pitch_r;
+    if (desc->neuron_order) {
+        // layout order of this shard's neurons: their order of appearance in neuron_order
+        std::vector<int64_t> pos(static_cast<size_t>(D), -1);
+        for (int64_t i = 0; i < D; ++i) {
+            const int64_t g = desc->neuron_order[i];
+            if (g < 0 || g >= D || pos[static_cast<size_t>(g)] >= 0) {
+                delete L;
+                return fail(SG_ERR_DATA, "neuron_order is not a permutation of 0..inter-1");
+            }
+            pos[static_cast<size_t>(g)] = i;
+        }
+        std::vector<int64_t> mine(static_cast<size_t>(Dl));
+        for (int64_t k = 0; k < Dl; ++k) mine[static_cast<size_t>(k)] = L->gbase + k * L->gstride;
+        std::sort(mine.begin(), mine.end(), [&](int64_t a, int64_t b) {
+            return pos[static_cast<size_t>(a)] < pos[static_cast<size_t>(b)];
+        });
+        L->gidx.assign(mine.begin(), mine.end());
+    }
     // device layout: [B r x pd][A Dl x pr][gate Dl x pd][ud Dl x 2pd][bias Dl f32]
     const size_t nB = static_cast<size_t>(has_pred ? r : 0) * pd;
     const size_t nA = static_cast<size_t>(has_pred ? Dl : 0) * pr;
@@ -351,13 +372,14 @@ sg_status sg_layer_create(const sg_layer_desc* desc, sg_layer** out) {
     const size_t offB = 0, offA = offB + nB, offG = offA + nA, offUD = offG + nG;
     const size_t n16 = offUD + nUD;
     const size_t bias_off = (n16 * 2 + 255) / 256 * 256;
-    const size_t total = bias_off + static_cast<size_t>(Dl) * 4;
+    const size_t gidx_off = bias_off + static_cast<size_t>(Dl) * 4;
+    const size_t total = gidx_off + (L->gidx.empty() ? 0 : static_cast<size_t>(Dl) * 4);
     std::vector<uint16_t> host(n16, 0);
     std::vector<float> hbias(static_cast<size_t>(Dl), 0.f);
     const bool down_nm = desc->down_neuron_major != 0;
     par_for(Dl, [&](int64_t a, int64_t b) {
         for (int64_t k = a; k < b; ++k) {
-            const int64_t n = L->gbase + k * L->gstride;
+            const int64_t n = local_to_global(L, k);
             uint16_t* g = host.data() + offG + k * pd;
             uint16_t* u = host.data() + offUD + k * 2 * pd;
             uint16_t* dn = u + pd;
@@ -389,6 +411,9 @@ sg_status sg_layer_create(const sg_layer_desc* desc, sg_layer** out) {
     if (e == cudaSuccess)
         e = cudaMemcpy(static_cast<char*>(L->dmem) + bias_off, hbias.data(), Dl * 4,
                        cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !L->gidx.empty())
+        e = cudaMemcpy(static_cast<char*>(L->dmem) + gidx_off, L->gidx.data(), Dl * 4,
+                       cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         if (L->dmem) cudaFree(L->dmem);
         delete L;
@@ -410,6 +435,8 @@ sg_status sg_layer_create(const sg_layer_desc* desc, sg_layer** out) {
     V.gate = has_w ? base + offG : nullptr;
     V.ud = has_w ? base + offUD : nullptr;
     V.bias = reinterpret_cast<const float*>(static_cast<char*>(L->dmem) + bias_off);
+    V.gidx = L->gidx.empty() ? nullptr
+                             : reinterpret_cast<const int*>(static_cast<char*>(L->dmem) + gidx_off);
     *out = L;
     return SG_OK;
 }
@@ -562,6 +589,21 @@ sg_status sg_ctx_read_sets(sg_ctx* C, void* stream, int32_t* P, int64_t* p, int3
     if (g && st[0] > 0) SG_CUDA(cudaMemcpy(g, C->W.gP, st[0] * 4, cudaMemcpyDeviceToHost));
     if (V && st[1] > 0) SG_CUDA(cudaMemcpy(V, C->W.V, st[1] * 4, cudaMemcpyDeviceToHost));
     if (z && st[1] > 0) SG_CUDA(cudaMemcpy(z, C->W.zV, st[1] * 4, cudaMemcpyDeviceToHost));
+    if (!C->last_layer->gidx.empty()) {
+        // segments follow the layout order: report ascending global indices
+        auto sort_pairs = [](int32_t* idx, float* val, int n) {
+            if (!idx || n <= 1) return;
+            std::vector<std::pair<int32_t, float>> t(static_cast<size_t>(n));
+            for (int i = 0; i < n; ++i) t[static_cast<size_t>(i)] = {idx[i], val ? val[i] : 0.f};
+            std::sort(t.begin(), t.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+            for (int i = 0; i < n; ++i) {
+                idx[i] = t[static_cast<size_t>(i)].first;
+                if (val) val[i] = t[static_cast<size_t>(i)].second;
+            }
+        };
+        sort_pairs(P, g, st[0]);
+        sort_pairs(V, z, st[1]);
+    }
     return SG_OK;
 }
 

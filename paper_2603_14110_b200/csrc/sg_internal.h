@@ -23,6 +23,7 @@ struct LayerView {
     const float* bias;     // D                  (types.hpp:76, +inf kept)
     const uint16_t* gate;  // D x pitch_d        (types.hpp:22)
     const uint16_t* ud;    // D x 2*pitch_d : row k = [up_k | down_k] (down neuron-major)
+    const int* gidx;       // global index of local neuron k (null: gbase + k * gstride)
 };
 
 // Per-context device workspace (one per stream). Sizes are bounded by the

@@ -942,8 +942,8 @@ __device__ void partial_down(const LayerView& L, const WorkView& W, const Smem& 
 // P and V index-set outputs (ascending global indices) for the caller: prefixes
 // over the per-CTA predicted / survivor counts; this CTA copies its own
 // segments. One warp; only for the last layer of a launch.
-__device__ __noinline__ void write_index_sets(int gbase, int gstride, int D, const int* cnt,
-                                              const int* plist, const float* gN,
+__device__ __noinline__ void write_index_sets(int gbase, int gstride, const int* gidx, int D,
+                                              const int* cnt, const int* plist, const float* gN,
                                               const int* vseg_raw, int* P, float* gP, int* V,
                                               float* zV) {
     const int G = gridDim.x, c = blockIdx.x, lane = threadIdx.x & 31;
@@ -975,14 +975,14 @@ __device__ __noinline__ void write_index_sets(int gbase, int gstride, int D, con
     const int cntP = __ldcg(cnt + c * kSector);
     for (int k = lane; k < cntP; k += 32) {
         const int n = __ldcg(plist + n0 + k);
-        P[mineP + k] = gbase + n * gstride;
+        P[mineP + k] = gidx ? __ldg(gidx + n) : gbase + n * gstride;
         gP[mineP + k] = __ldcg(gN + n);
     }
     const int cntV = __ldcg(cnt + gpad() + c * kSector);
     const int2* seg = reinterpret_cast<const int2*>(vseg_raw) + n0;
     for (int k = lane; k < cntV; k += 32) {
         const int2 e = __ldcg(seg + k);
-        V[mineV + k] = gbase + e.x * gstride;
+        V[mineV + k] = gidx ? __ldg(gidx + e.x) : gbase + e.x * gstride;
         zV[mineV + k] = __int_as_float(e.y);
     }
     __syncwarp();
@@ -997,8 +997,8 @@ __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm
                            bool want_sets) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     if (kPipe != 0 && want_sets && (tid >> 5) == kWarps)
-        write_index_sets(L.gbase, L.gstride, L.D, W.cnt, W.plist, W.gN, W.vseg, W.P, W.gP, W.V,
-                         W.zV);
+        write_index_sets(L.gbase, L.gstride, L.gidx, L.D, W.cnt, W.plist, W.gN, W.vseg, W.P, W.gP,
+                         W.V, W.zV);
     const int c0 = split_lo(c, G, L.d), c1 = split_lo(c + 1, G, L.d);
     const int ncols = c1 - c0;
     float* part = reinterpret_cast<float*>(sm.big);

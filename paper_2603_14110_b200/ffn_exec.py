@@ -286,6 +286,8 @@ class DeviceLayer:
                 desc.bias = ptr(_f64(pred.bias))
             desc.weight_dtype = capi.SG_F64
             self.hidden, self.inter, self.rank = desc.hidden, desc.inter, desc.rank
+        if raw is not None and raw.get("order") is not None:
+            desc.neuron_order = ptr(np.ascontiguousarray(raw["order"], dtype=np.int64))
         desc.device = device
         desc.shard_index, desc.shard_count = shard_index, shard_count
         desc.shard_interleave = int(shard_interleave)

@@ -49,6 +49,7 @@ class HostLayer:
     x: np.ndarray      # f64 d (eval token 0), bf16-exact
     xs: np.ndarray     # f64 d x T eval tokens
     calib_achieved: float = 0.0
+    load: np.ndarray = None  # expected rows streamed per token per neuron (calibration stats)
 
 
 def build_host_layer(d, D, act, seed, rank=256, sparsity=0.5, calib_tokens=256, eval_tokens=16,
@@ -76,8 +77,13 @@ def build_host_layer(d, D, act, seed, rank=256, sparsity=0.5, calib_tokens=256, 
     weights = (inner.astype(np.float64) ** 2) * down_norm2[:, None]
     cal = greedy_calibrate(scores, weights, eta, sparsity)
     ev = bf16_to_f64(round_bf16(fx["eval"]))
+    # offline activity statistics of the calibrated predictor on the calibration
+    # tokens: a neuron costs one gate row when predicted active and two more rows
+    # (up, down) when it also survives revalidation
+    on = (scores + cal.bias[:, None].astype(np.float32)) > 0
+    load = on.mean(axis=1) + 2.0 * (on & (gp > 0)).mean(axis=1)
     return HostLayer(fx["gate"], fx["up"], fx["down_t"], round_bf16(A), round_bf16(B), cal.bias,
-                     ev[:, 0].copy(), ev, cal.achieved_sparsity)
+                     ev[:, 0].copy(), ev, cal.achieved_sparsity, load)
 
 
 def build_host_model(config: str, layers: int = None, seed_base: int = 0, rank: int = 256,
@@ -96,7 +102,41 @@ def build_host_model(config: str, layers: int = None, seed_base: int = 0, rank: 
     return cfg, out
 
 
-def upload(host: HostLayer, d, D, act, rank=256, device=0, shard_index=0, shard_count=1):
+def balanced_order(load: np.ndarray, neurons: np.ndarray, G: int) -> np.ndarray:
+    """Layout order of `neurons` for G CTAs: CTA c gets the c-th contiguous block of
+    the layout (sizes c*n/G boundaries, as the kernel splits), and blocks get equal
+    expected load: neurons by decreasing load are dealt to the CTAs in serpentine
+    order (skipping full ones). Deterministic; within a block ascending index."""
+    n = len(neurons)
+    bounds = [c * n // G for c in range(G + 1)]
+    cap = np.diff(bounds)
+    bins = [[] for _ in range(G)]
+    order = neurons[np.argsort(-load[neurons], kind="stable")]
+    c, step = 0, 1
+    for nid in order:
+        while len(bins[c]) >= cap[c]:
+            c += step
+            if c == G or c < 0:
+                step = -step
+                c += step
+        bins[c].append(nid)
+        c += step
+        if c == G or c < 0:
+            step = -step
+            c += step
+    return np.concatenate([np.sort(np.asarray(b, dtype=np.int64)) for b in bins])
+
+
+def upload(host: HostLayer, d, D, act, rank=256, device=0, shard_index=0, shard_count=1,
+           balance=True):
     raw = dict(hidden=d, inter=D, rank=rank, activation=act, gate=host.gate, up=host.up,
                down_t=host.down_t, A=host.A, B=host.B, bias=host.bias)
+    if balance and host.load is not None:
+        import torch
+        from .sharded import shard_indices
+        G = torch.cuda.get_device_properties(device).multi_processor_count
+        mine = shard_indices(D, shard_index, shard_count)
+        first = balanced_order(host.load, mine, G)
+        rest = np.setdiff1d(np.arange(D, dtype=np.int64), mine)
+        raw["order"] = np.concatenate([first, rest])
     return DeviceLayer(raw=raw, device=device, shard_index=shard_index, shard_count=shard_count)

@@ -129,3 +129,41 @@ def test_stack_launch_equals_layer_launches(pipeline):
         assert np.array_equal(yc[l], res.y), f"chained layer {l}"
         x = res.y.astype(np.float32).astype(np.float64)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("shards", [1, 2])
+def test_layout_order_keeps_parity(shards):
+    """A neuron layout order (sg_layer_desc.neuron_order) moves work between CTAs
+    only: sets (reported in global indices, ascending) and y stay within parity."""
+    from paper_2603_14110_b200 import round_bf16
+    d, D, r = 512, 1500, 64
+    fx, pred = _calibrated_layer(d, D, r, seed=31, calib=1024)
+    q = quantize_layer(fx.weights.gate, fx.weights.up, fx.weights.down, pred.A, pred.B, pred.bias)
+    order = np.random.default_rng(3).permutation(D)
+    raw = dict(hidden=d, inter=D, rank=r, activation=0, gate=round_bf16(fx.weights.gate),
+               up=round_bf16(fx.weights.up), down_t=round_bf16(np.ascontiguousarray(fx.weights.down.T)),
+               A=round_bf16(pred.A), B=round_bf16(pred.B), bias=pred.bias.astype(np.float32),
+               order=order)
+    parts = [DeviceLayer(raw=raw, shard_index=k, shard_count=shards) for k in range(shards)]
+    for k, lay in enumerate(parts):
+        mine = set(shard_indices(D, k, shards).tolist())
+        gl = [lay.global_index(i) for i in range(lay.local_inter)]
+        assert set(gl) == mine
+        pos = {g: i for i, g in enumerate(order)}
+        assert [pos[g] for g in gl] == sorted(pos[g] for g in gl)  # layout follows the order
+    for t in range(4):
+        x = fx.eval[:, t]
+        y = np.zeros(d)
+        P, V = [], []
+        for lay in parts:
+            ctx = lay.context()
+            y += lay.forward(x, Pipeline.Sequential, ctx).y
+            Pk, Vk, _, _ = read_sets(ctx, lay.local_inter)
+            assert list(Pk) == sorted(Pk) and list(Vk) == sorted(Vk)
+            P += Pk.tolist()
+            V += Vk.tolist()
+        diag = check_token(q, x, y, sorted(P), sorted(V))
+        assert diag["rel"] <= Y_RTOL
+    with pytest.raises(Exception):
+        bad = dict(raw, order=np.zeros(D, dtype=np.int64))
+        DeviceLayer(raw=bad)
