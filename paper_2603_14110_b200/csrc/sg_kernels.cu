@@ -71,6 +71,7 @@ struct SmemPlan {
     int off_mask;   // uint8[mask_cap]  phase B mask bytes
     int off_bias;   // float[mask_cap]  this CTA's bias slice / dense z slice
     int off_misc;   // int[32]          block-level scalars
+    int off_lv;     // LayerView[2]     this and the next layer's view (stack launches)
     int off_reda;   // float[256]       reduction scratch
     int off_items;  // int[item_cap]    this CTA's predicted neurons
     int off_recs;   // int2[item_cap]   per-item {neuron or -1, g or z}
@@ -98,6 +99,7 @@ struct Smem {
     uint8_t* mask;
     float* bias;
     int* misc;
+    LayerView* lv;
     float* reda;
     int* items;
     int2* recs;
@@ -117,6 +119,7 @@ __device__ __forceinline__ Smem carve(uint8_t* base, const SmemPlan& S) {
     m.mask = base + S.off_mask;
     m.bias = reinterpret_cast<float*>(base + S.off_bias);
     m.misc = reinterpret_cast<int*>(base + S.off_misc);
+    m.lv = reinterpret_cast<LayerView*>(base + S.off_lv);
     m.reda = reinterpret_cast<float*>(base + S.off_reda);
     m.items = reinterpret_cast<int*>(base + S.off_items);
     m.recs = reinterpret_cast<int2*>(base + S.off_recs);
@@ -544,12 +547,28 @@ __device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm
 struct XRegs {
     float v[kXRegChunks][8];
 };
+// 32-B chunk of x as two LDS.128 (scalar loads at a 32-B thread stride would
+// be 8-way bank conflicts).
+__device__ __forceinline__ void load_x8(const float* xs, int ch, bool ok, float* v) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    if (ok) {
+        a = *reinterpret_cast<const float4*>(xs + ch * 8);
+        b = *reinterpret_cast<const float4*>(xs + ch * 8 + 4);
+    }
+    v[0] = a.x;
+    v[1] = a.y;
+    v[2] = a.z;
+    v[3] = a.w;
+    v[4] = b.x;
+    v[5] = b.y;
+    v[6] = b.z;
+    v[7] = b.w;
+}
 __device__ __forceinline__ void load_xregs(const float* xs, int nch, int gt, XRegs& X) {
 #pragma unroll
     for (int k = 0; k < kXRegChunks; ++k) {
         const int ch = gt + k * kGroupThreads;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) X.v[k][e] = ch < nch ? xs[ch * 8 + e] : 0.f;
+        load_x8(xs, ch, ch < nch, X.v[k]);
     }
 }
 // kRows smem rows sharing the x registers; red is this group's scratch
@@ -799,10 +818,10 @@ __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkVi
     const bool comp = tid < kCThreads;
     const bool h0 = comp && ch0 < nch, h1 = comp && ch1 < nch;
     float x0[8], x1[8], a0[8], a1[8];
+    load_x8(sm.xs, ch0, h0, x0);
+    load_x8(sm.xs, ch1, h1, x1);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-        x0[e] = h0 ? sm.xs[ch0 * 8 + e] : 0.f;
-        x1[e] = h1 ? sm.xs[ch1 * 8 + e] : 0.f;
         a0[e] = 0.f;
         a1[e] = 0.f;
     }
@@ -1104,8 +1123,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     RunState rs{0u, 0u, 0ull, 0u};
     grid_barrier_init(W, rs);
     bool prestaged = false;
+    // layer views live in shared memory: the next one is copied during the
+    // current layer, so a layer never starts with a global-memory round trip
+    constexpr int kLvWords = static_cast<int>(sizeof(LayerView) / 4);
+    static_assert(sizeof(LayerView) % 16 == 0, "LayerView is copied in 16-B pieces");
+    if (threadIdx.x == 0) {
+        if (layers) {
+            for (int k = 0; k < kLvWords; ++k)
+                reinterpret_cast<int*>(sm.lv)[k] = __ldg(reinterpret_cast<const int*>(layers) + k);
+        } else {
+            sm.lv[0] = L0;
+        }
+    }
+    __syncthreads();
     for (int l = 0; l < nlayers; ++l) {
-        const LayerView L = layers ? layers[l] : L0;
+        if (layers && l + 1 < nlayers && threadIdx.x < kLvWords / 4) {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                             smem_u32(reinterpret_cast<int4*>(sm.lv + ((l + 1) & 1)) + threadIdx.x)),
+                         "l"(reinterpret_cast<const int4*>(layers + l + 1) + threadIdx.x)
+                         : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        const LayerView L = sm.lv[l & 1];
         const LayerView* next = (layers && l + 1 < nlayers) ? layers + l + 1 : nullptr;
         const float* x = (chain && l > 0) ? ys + static_cast<size_t>(l - 1) * xstride
                                           : xs + static_cast<size_t>(l) * xstride;
@@ -1114,6 +1153,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         Wl.stats = W.stats + 4 * l;  // per-layer {p, v, nonfinite, pipeline}
         prestaged = run_layer<kPipe>(L, Wl, sm, S, rs, x, y, l == 0, l, l == nlayers - 1, next,
                                      prestaged);
+        if (layers && l + 1 < nlayers) {
+            if (threadIdx.x < kLvWords / 4) asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncthreads();
+        }
     }
 }
 
@@ -1156,6 +1199,8 @@ bool make_plan(int G, int pitch_d, int r, int pitch_r, int Dl, int pipe, int max
     off += S->mask_cap * 4;
     S->off_misc = off = align_up(off, 16);
     off += 32 * 4;
+    S->off_lv = off = align_up(off, 16);
+    off += 2 * static_cast<int>(sizeof(LayerView));
     S->off_reda = off = align_up(off, 16);
     off += 256 * 4;  // phase A: kRowsA*kWarps; phase C: kGroups*2*kGroupWarps*4; stage 4
     S->item_cap = (Dl + G - 1) / G + 2;
