@@ -549,6 +549,8 @@ sg_status sg_ffn_forward_device(sg_ctx* C, const sg_layer* L, sg_pipeline pipeli
     if (!L->has_w) return fail(SG_ERR_USAGE, "predictor-only layer cannot run the FFN");
     if (x == nullptr || y == nullptr) return fail(SG_ERR_USAGE, "null x/y");
     DeviceGuard dg(L->device);
+    // per-layer counts are accumulated with integer atomics by the kernel
+    SG_CUDA(cudaMemsetAsync(C->W.stats, 0, 4 * sizeof(int), static_cast<cudaStream_t>(stream)));
     const int e = sg::launch_layer(L->view, work_for(C, x, y), pipeline, C->G, stream);
     if (e != 0) {
         return fail(SG_ERR_CUDA, std::string("launch: ") +
@@ -615,6 +617,7 @@ sg_status sg_predict_mask(sg_ctx* C, const sg_layer* L, const void* x, sg_dtype 
     DeviceGuard dg(L->device);
     auto st = static_cast<cudaStream_t>(stream);
     SG_CUDA(cudaMemcpyAsync(C->xdev, C->xpin, L->d * 4, cudaMemcpyHostToDevice, st));
+    SG_CUDA(cudaMemsetAsync(C->W.stats, 0, 4 * sizeof(int), st));
     const int e = sg::launch_predict(L->view, work_for(C, C->xdev, C->ydev), C->maskdev, C->G, st);
     if (e != 0) return fail(SG_ERR_CUDA, std::string("launch: ") +
                                              cudaGetErrorString(static_cast<cudaError_t>(e)));
@@ -689,6 +692,7 @@ sg_status sg_ffn_forward_layers(sg_ctx* C, const sg_layer* const* layers, int32_
         SG_CUDA(cudaMemcpy(C->stackdev, views.data(), sizeof(sg::LayerView) * n,
                            cudaMemcpyHostToDevice));
     }
+    SG_CUDA(cudaMemsetAsync(C->W.stats, 0, static_cast<size_t>(n) * 4 * sizeof(int), st));
     const int e = sg::launch_layers(C->stackdev, n, L0->view, work_for(C, xs, ys), xs, ys, chain,
                                     static_cast<int>(L0->d), pipeline, C->G, st);
     if (e != 0) return fail(SG_ERR_CUDA, std::string("launch: ") +

@@ -136,6 +136,7 @@ struct RunState {
     uint32_t auses;     // staging-barrier phases consumed so far
     uint64_t bar_base;  // grid-barrier counter base (lanes 0..7 of warp 0)
     uint32_t bar_k;     // grid barriers passed in this launch
+    uint32_t tag0;      // grid barriers completed before this launch (exchange tags)
 };
 
 // ---------------------------------------------------------------------------
@@ -278,6 +279,21 @@ __device__ __forceinline__ void st_sector(int* p, int v) {
         : "memory");
 }
 __device__ __forceinline__ int gpad() { return static_cast<int>(gridDim.x) * kSector; }
+
+// Data-carrying exchange: a value and a launch-unique tag in ONE 64-bit store,
+// so a reader polls the value itself instead of a barrier and then the value.
+__device__ __forceinline__ void st_tagged(void* p, float v, uint32_t tag) {
+    asm volatile("st.relaxed.gpu.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(__float_as_uint(v)),
+                 "r"(tag)
+                 : "memory");
+}
+__device__ __forceinline__ float ld_tagged(const void* p, uint32_t tag) {
+    uint32_t v, t;
+    do {
+        asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(v), "=r"(t) : "l"(p) : "memory");
+    } while (t != tag);
+    return __uint_as_float(v);
+}
 
 // ---------------------------------------------------------------------------
 // Grid barrier on kBarCounters monotonically increasing 64-bit counters
@@ -424,7 +440,8 @@ __device__ __forceinline__ bool stage_x(const float* x, int d, int pitch_d, floa
 // ---------------------------------------------------------------------------
 // Phase A: t = B·x (fp32), rows j = c + q*G ; block-reduced in fixed order.
 // ---------------------------------------------------------------------------
-__device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm, bool staged_b) {
+__device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm, bool staged_b,
+                        uint32_t tag) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int nch = L.pitch_d >> 3;
@@ -462,8 +479,7 @@ __device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm, b
         if (tid < kRowsA && q0 + tid < nB) {
             float s = 0.f;
             for (int w = 0; w < kWarps; ++w) s += sm.reda[tid * kWarps + w];
-            st_sector(reinterpret_cast<int*>(W.t) + (c + (q0 + tid) * G) * kSector,
-                      __float_as_int(s));
+            st_tagged(reinterpret_cast<int*>(W.t) + (c + (q0 + tid) * G) * kSector, s, tag);
         }
         __syncthreads();
     }
@@ -474,12 +490,12 @@ __device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm, b
 // its predicted list (smem items[], global plist at n0, count).
 // ---------------------------------------------------------------------------
 __device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm, bool use_as,
-                           bool staged_b, uint8_t* mask_out) {
+                           bool staged_b, uint8_t* mask_out, uint32_t tag) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int n0 = split_lo(c, G, L.D), n1 = split_lo(c + 1, G, L.D);
     for (int i = tid; i < L.pitch_r; i += kThreads)
-        sm.ts[i] = i < L.r ? __ldcg(W.t + i * kSector) : 0.f;
+        sm.ts[i] = i < L.r ? ld_tagged(W.t + i * kSector, tag) : 0.f;
     asm volatile("cp.async.wait_all;" ::: "memory");  // the bias slice
     __syncthreads();
     const int nB = c < L.r ? (L.r - c + G - 1) / G : 0;
@@ -1066,8 +1082,7 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
     SG_STAMP(dbg, 1);
     const bool bad = stage_x(x, L.d, L.pitch_d, sm.xs);
     if (c == 0 && tid == 0) {
-        W.stats[0] = 0;  // p and v are added (atomically) after the next grid barrier
-        W.stats[1] = 0;
+        // p and v (stats[0], [1]) are zeroed by the host before the launch
         W.stats[2] = bad ? 1 : 0;
         W.stats[3] = kPipe;
     }
@@ -1078,11 +1093,12 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
             __syncwarp();
             rs.auses += 1;
         }
-        phase_t(L, W, sm, S.stage_b != 0);
+        // t travels with its tag: no grid barrier between stages 1a and 1b
+        const uint32_t tag = rs.tag0 + rs.bar_k + 1u;
+        phase_t(L, W, sm, S.stage_b != 0, tag);
         SG_STAMP(dbg, 3);
-        grid_barrier(W, rs);
         SG_STAMP(dbg, 4);
-        phase_mask(L, W, sm, use_as, S.stage_b != 0, nullptr);
+        phase_mask(L, W, sm, use_as, S.stage_b != 0, nullptr, tag);
         SG_STAMP(dbg, 6);
     }
     phase_gather<kPipe>(L, W, sm, S, rs);
@@ -1120,8 +1136,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const Smem sm = carve(smem_raw, S);
     init_barriers(sm.full);
-    RunState rs{0u, 0u, 0ull, 0u};
+    RunState rs{0u, 0u, 0ull, 0u, 0u};
     grid_barrier_init(W, rs);
+    // barriers completed by all earlier launches on this workspace: a tag base
+    // that no value left in the exchange buffers can carry yet
+    if (threadIdx.x == 0) sm.misc[9] = static_cast<int>(rs.bar_base / static_cast<uint64_t>(bar_share(0)));
     bool prestaged = false;
     // layer views live in shared memory: the next one is copied during the
     // current layer, so a layer never starts with a global-memory round trip
@@ -1136,6 +1155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     __syncthreads();
+    rs.tag0 = static_cast<uint32_t>(sm.misc[9]);
     for (int l = 0; l < nlayers; ++l) {
         if (layers && l + 1 < nlayers && threadIdx.x < kLvWords / 4) {
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
@@ -1166,14 +1186,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const Smem sm = carve(smem_raw, S);
     init_barriers(sm.full);
-    RunState rs{0u, 0u, 0ull, 0u};
+    RunState rs{0u, 0u, 0ull, 0u, 0u};
     grid_barrier_init(W, rs);
+    if (threadIdx.x == 0) sm.misc[9] = static_cast<int>(rs.bar_base / static_cast<uint64_t>(bar_share(0)));
     stage_weights(L, sm, S, false);  // bias only (S.stage_b == 0)
-    const bool bad = stage_x(W.x, L.d, L.pitch_d, sm.xs);
+    const bool bad = stage_x(W.x, L.d, L.pitch_d, sm.xs);  // (block barrier inside)
+    rs.tag0 = static_cast<uint32_t>(sm.misc[9]);
     if (blockIdx.x == 0 && threadIdx.x == 0) W.stats[2] = bad ? 1 : 0;
-    phase_t(L, W, sm, false);
-    grid_barrier(W, rs);
-    phase_mask(L, W, sm, false, false, mask_out);
+    const uint32_t tag = rs.tag0 + 1u;
+    phase_t(L, W, sm, false, tag);
+    phase_mask(L, W, sm, false, false, mask_out, tag);
     grid_barrier(W, rs);
     if (threadIdx.x < 32 && blockIdx.x == 0) {
         warp_prefix(W.cnt, sm.off, gridDim.x, threadIdx.x);
