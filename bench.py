@@ -209,6 +209,107 @@ def cpu_baseline_for(cfg, host_layer0, args):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def run_batch(args, cfg, host, layers, ctx, world, rank, local):
+    """Batched decode: B tokens per step through the L layers, one sg_ffn_forward_batch
+    per layer (≈10 kernels), the whole step captured in one CUDA graph."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2603_14110_b200 import _capi as capi
+    from paper_2603_14110_b200.ffn_exec import check
+    lib = capi.lib()
+    d, D, L, B = cfg["d"], cfg["D"], len(host), args.batch
+    X = torch.tensor(np.stack([h.xs[:, :B].T for h in host]), dtype=torch.float32, device="cuda")
+    Y = torch.zeros_like(X)
+    stream = torch.cuda.Stream()
+
+    def step(sh):
+        for l in range(L):
+            check(lib.sg_ffn_forward_batch(ctx.handle, layers[l].handle, C.c_void_p(X[l].data_ptr()),
+                                           B, C.c_void_p(Y[l].data_ptr()), C.c_void_p(sh)))
+
+    with torch.cuda.stream(stream):
+        step(stream.cuda_stream)  # allocations / attributes before capture
+    torch.cuda.synchronize()
+    # union sizes of the last layer (roofline bytes), per layer re-run un-captured
+    pb = np.zeros(layers[0].local_inter, dtype=np.uint64)
+    vb = np.zeros_like(pb)
+    up, uv = [], []
+    stats = (capi.sg_exec_stats * B)()
+    for l in range(L):
+        check(lib.sg_ffn_forward_batch(ctx.handle, layers[l].handle, C.c_void_p(X[l].data_ptr()), B,
+                                       C.c_void_p(Y[l].data_ptr()), C.c_void_p(stream.cuda_stream)))
+        check(lib.sg_ctx_read_batch(ctx.handle, C.c_void_p(stream.cuda_stream), B, stats,
+                                    pb.ctypes.data_as(C.c_void_p), vb.ctypes.data_as(C.c_void_p)))
+        up.append(int((pb != 0).sum()))
+        uv.append(int((vb != 0).sum()))
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        step(torch.cuda.current_stream().cuda_stream)
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    time.sleep(0.15)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        graph.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    clocks = sampler.stop()
+    r = args.rank
+    alg = sum(2 * r * d + 2 * D * r + 4 * D + 2 * d * p + 4 * d * v + 8 * d * B for p, v in zip(up, uv))
+    hbm, hbm_kind = peaks()
+    # e2e: pinned host tokens in, outputs back, through the same graph
+    xh = torch.empty_like(X, device="cpu").pin_memory()
+    xh.copy_(X)
+    yh = torch.empty_like(Y, device="cpu").pin_memory()
+
+    def e2e_step():
+        X.copy_(xh, non_blocking=True)
+        graph.replay()
+        yh.copy_(Y, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(3):
+        e2e_step()
+    ke = max(10, min(args.steps, 200))
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(ke):
+        e2e_step()
+    t1.record()
+    torch.cuda.synchronize()
+    ms_e2e = t0.elapsed_time(t1) / ke
+    line = {
+        "metric": "sparse-FFN decode tokens/s", "value": B * 1000.0 / ms, "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": f"{cfg['model']}: {L} layers d={d} d_ff={D} r={r} s={args.sparsity}, "
+                               f"batched decode B={B} (union mask, tensor-core gathered tiles)",
+                   "layers": L, "hidden": d, "inter": D, "rank": r, "batch": B,
+                   "l2": "no flush: each step streams the union rows of %d distinct layers" % L},
+        "per_layer_us": ms * 1000.0 / L,
+        "union_p_mean": float(np.mean(up)), "union_v_mean": float(np.mean(uv)),
+        "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                     "frac": alg / (ms * 1e-3) / 1e9 / hbm, "peak_kind": hbm_kind, "traffic": None,
+                     "bytes_per_step": alg, "kernel": "sg_batch.cu (mma.sync gathered GEMMs)"},
+        "e2e": {"value": B * 1000.0 / ms_e2e, "unit": "tokens/s", "h2d_bytes_per_step": L * B * d * 4,
+                "d2h_bytes_per_step": L * B * d * 4, "ms_per_step": ms_e2e},
+        "gpu_launches": args.steps * L * 11,
+        "clocks": clocks,
+        "cpu_baseline": None,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -224,6 +325,8 @@ def main():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-balance", action="store_true",
                     help="ascending neuron layout instead of the load-balanced order")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="batched decode (configs[4]): B tokens per step through all layers")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup()
@@ -249,7 +352,8 @@ def main():
     except Exception:
         pass
     cfg, host = build_host_model(args.config, args.layers, rank=args.rank,
-                                 sparsity=args.sparsity, workers=8)
+                                 sparsity=args.sparsity, workers=8,
+                                 eval_tokens=max(16, args.batch))
     d, D, L = cfg["d"], cfg["D"], len(host)
     log(f"host model built in {time.time() - t0:.1f}s")
     layers = [upload(h, d, D, cfg["act"], args.rank, device=local, shard_index=rank,
@@ -257,6 +361,8 @@ def main():
     Dl = layers[0].local_inter
     ctx = Context(local, d, Dl, args.rank)
     lib = capi.lib()
+    if args.batch > 0:
+        return run_batch(args, cfg, host, layers, ctx, world, rank, local)
     arr = (C.c_void_p * L)(*[l.handle.value for l in layers])
     xs = torch.tensor(np.stack([h.x for h in host]), dtype=torch.float32, device="cuda")
     ys = torch.zeros_like(xs)

@@ -178,6 +178,22 @@ sg_status sg_ffn_forward_layers_host(sg_ctx* ctx, const sg_layer* const* layers,
 /* Synchronises, then returns per-layer stats of the last sg_ffn_forward_layers* call. */
 sg_status sg_ctx_read_stack_stats(sg_ctx* ctx, void* stream, int32_t n, sg_exec_stats* stats);
 
+/* Batched decode (BASELINE.json configs[4]): `batch` (1..64) tokens through one
+ * layer, sequential pipeline. Each token gets exactly its own single-token
+ * result (its P_b, V_b, y_b, ExecStats); the batch reads each gate row of the
+ * union of the P_b and each [up | down] row of the union of the V_b once, on the
+ * tensor cores. xs, ys: device fp32 [batch][hidden]. Asynchronous on `stream`. */
+sg_status sg_ffn_forward_batch(sg_ctx* ctx, const sg_layer* layer, const float* xs, int32_t batch,
+                               float* ys, void* stream);
+/* Synchronises, then per-token stats (batch entries) and, optionally, per-neuron
+ * bit masks (local inter entries; bit b = token b): predicted active, survivor. */
+sg_status sg_ctx_read_batch(sg_ctx* ctx, void* stream, int32_t batch, sg_exec_stats* stats,
+                            uint64_t* pred_bits, uint64_t* surv_bits);
+/* Host-buffer variant: fp32 xs_host [batch][hidden] in, ys_host out, stats (may be NULL). */
+sg_status sg_ffn_forward_batch_host(sg_ctx* ctx, const sg_layer* layer, const float* xs_host,
+                                    int32_t batch, float* ys_host, sg_exec_stats* stats,
+                                    void* stream);
+
 /* Diagnostics: record per-CTA %globaltimer stamps at every phase boundary of
  * the executor (up to 32 stamps per CTA per layer) for up to
  * max_layers layers of each subsequent call; max_layers = 0 disables. */

@@ -1,0 +1,440 @@
+// sparsegate-b200: batched decode (BASELINE.json configs[4]) — B tokens, one layer.
+//
+// Per token the result means exactly what sparse_ffn_sequential
+// (/root/reference/proj/include/sparsegate/ffn_exec.hpp:183-218) returns for
+// that token alone: its own predicted set P_b (pre > 0, :141), survivors V_b
+// (g > 0, :200), gated values (:68-76) and y_b over V_b. The batch shares the
+// weight traffic: every gate row of the union of the P_b and every [up|down]
+// row of the union of the V_b is read ONCE and multiplied against all tokens
+// on the tensor cores (the gathered block is a real dense contraction).
+//
+// Stages (one launch each; all orders fixed, so results are deterministic):
+//   x -> bf16 hi/lo          x = hi + lo with both bf16 (relative error ~2^-16,
+//                            inside the 2^-14 parity band; tests/parity_util.py)
+//   T  = Bp x                gathered-row GEMM, split-K, fixed-order reduction
+//   pre = A T + bias         same GEMM over all D rows; epilogue: mask bits per
+//                            neuron (one bit per token), union flag, per-token |P|
+//   U_P                      ascending compaction of the union (one CTA scan)
+//   G = gate[U_P] x          epilogue: survivor bits = mask & (G > 0), union, |V|
+//   U_V                      ascending compaction
+//   U = up[U_V] x            epilogue: z = gated(G, U) on survivor bits, else +0
+//   Y = sum_{U_V} down z     split-K over U_V, fixed-order reduction
+//
+// GEMM tiles: 4 warps, 64 rows x Bp (<= 64) tokens, K chunks of 64 through a
+// 2-stage cp.async pipeline; fragments by ldmatrix; mma.sync.m16n8k16 bf16 with
+// fp32 accumulation (hi and lo parts are two MMAs into the same accumulator).
+#include "sg_internal.h"
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sg {
+namespace {
+
+constexpr int kBM = 64;                  // rows per CTA tile
+constexpr int kBK = 64;                  // K per pipeline stage
+constexpr int kBWarps = 4;               // one m16 slice per warp
+constexpr int kBThreads = kBWarps * 32;
+constexpr int kRowPad = kBK + 8;         // smem row stride (bf16): conflict-free ldmatrix
+constexpr int kMaxBatch = 64;
+
+__device__ __forceinline__ uint32_t smem_u32b(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32b(dst)), "l"(src),
+                 "r"(ok ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(const void* p, uint32_t& a, uint32_t& b, uint32_t& c,
+                                        uint32_t& d) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "r"(smem_u32b(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(const void* p, uint32_t& a, uint32_t& b, uint32_t& c,
+                                          uint32_t& d) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "r"(smem_u32b(p)));
+}
+__device__ __forceinline__ void ldsm_x2(const void* p, uint32_t& a, uint32_t& b) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];"
+                 : "=r"(a), "=r"(b)
+                 : "r"(smem_u32b(p)));
+}
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+        "{%8, %9}, {%0, %1, %2, %3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// ---------------------------------------------------------------------------
+// Gathered-row GEMM: acc[r][n] = sum_k W[row(r)][k] * (Xh[n][k] + Xl[n][k]),
+// r over this CTA's 64 rows, n < nb (a multiple of 8), k over [k0, k1).
+// W rows: row(r) = rows ? rows[r] : r, pitch wp elements; X: [nb][xp] bf16.
+// TRANS_A: W is stored [k][m] (m contiguous, pitch wp) — the down projection,
+// where "rows" index K (neurons) and the 64-wide tile runs over m.
+// ---------------------------------------------------------------------------
+template <bool TRANS_A>
+__device__ __forceinline__ void gemm_tile(const uint16_t* __restrict__ W, int wp,
+                                          const int* __restrict__ rows, int nrows, int m0,
+                                          const uint16_t* __restrict__ Xh,
+                                          const uint16_t* __restrict__ Xl, int xp, int nb, int k0,
+                                          int k1, uint16_t* sm, float (*acc)[4]) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ntile = nb >> 3;
+    // stage layout: A [64][kRowPad] (TRANS_A: [kBK][64 + 8]) then Xh, Xl [nb][kRowPad]
+    constexpr int kAElems = TRANS_A ? kBK * (kBM + 8) : kBM * kRowPad;
+    const int stage_elems = kAElems + 2 * kMaxBatch * kRowPad;
+    auto load = [&](int st, int kb) {
+        uint16_t* a = sm + st * stage_elems;
+        uint16_t* xh = a + kAElems;
+        uint16_t* xl = xh + kMaxBatch * kRowPad;
+        if (!TRANS_A) {
+            // 64 rows x 64 k: 8 pieces of 16 B per row
+            for (int i = tid; i < kBM * 8; i += kBThreads) {
+                const int r = i >> 3, p = i & 7;
+                const int gr = m0 + r;
+                const bool ok = gr < nrows;
+                const int row = ok ? (rows ? rows[gr] : gr) : 0;
+                cp16(a + r * kRowPad + p * 8, W + static_cast<size_t>(row) * wp + kb + p * 8, ok);
+            }
+        } else {
+            // 64 k (neurons) x 64 m: row k is the m-slice [m0, m0+64) of neuron rows[k]
+            for (int i = tid; i < kBK * 8; i += kBThreads) {
+                const int r = i >> 3, p = i & 7;
+                const int gk = kb + r;
+                const bool ok = gk < k1;
+                const int row = ok ? rows[gk] : 0;
+                cp16(a + r * (kBM + 8) + p * 8, W + static_cast<size_t>(row) * wp + m0 + p * 8, ok);
+            }
+        }
+        for (int i = tid; i < nb * 8; i += kBThreads) {
+            const int n = i >> 3, p = i & 7;
+            cp16(xh + n * kRowPad + p * 8, Xh + static_cast<size_t>(n) * xp + kb + p * 8, true);
+            cp16(xl + n * kRowPad + p * 8, Xl + static_cast<size_t>(n) * xp + kb + p * 8, true);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int t = 0; t < kMaxBatch / 8; ++t)
+        for (int e = 0; e < 4; ++e) acc[t][e] = 0.f;
+    const int nk = (k1 - k0 + kBK - 1) / kBK;
+    if (nk > 0) load(0, k0);
+    for (int it = 0; it < nk; ++it) {
+        if (it + 1 < nk) {
+            load((it + 1) & 1, k0 + (it + 1) * kBK);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const uint16_t* a = sm + (it & 1) * stage_elems;
+        const uint16_t* xh = a + kAElems;
+        const uint16_t* xl = xh + kMaxBatch * kRowPad;
+#pragma unroll
+        for (int ks = 0; ks < kBK; ks += 16) {
+            uint32_t af[4];
+            if (!TRANS_A) {
+                const int r = warp * 16 + (lane & 15);
+                const int kk = ks + (lane >> 4) * 8;
+                ldsm_x4(a + r * kRowPad + kk, af[0], af[1], af[2], af[3]);
+            } else {
+                // matrices: (m 0-7, k 0-7), (m 8-15, k 0-7), (m 0-7, k 8-15), (m 8-15, k 8-15)
+                const int q = lane >> 3, rr = lane & 7;
+                const int kk = ks + (q >> 1) * 8 + rr;
+                const int mm = warp * 16 + (q & 1) * 8;
+                ldsm_x4_t(a + kk * (kBM + 8) + mm, af[0], af[1], af[2], af[3]);
+            }
+#pragma unroll
+            for (int t = 0; t < kMaxBatch / 8; ++t) {
+                if (t < ntile) {
+                    const int n = t * 8 + (lane & 7);
+                    const int kk = ks + ((lane >> 3) & 1) * 8;
+                    uint32_t b0, b1;
+                    ldsm_x2(xh + n * kRowPad + kk, b0, b1);
+                    mma16816(acc[t], af, b0, b1);
+                    ldsm_x2(xl + n * kRowPad + kk, b0, b1);
+                    mma16816(acc[t], af, b0, b1);
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// x (fp32 [B][d]) -> bf16 hi/lo [nb][pitch] (zero padded rows and columns)
+__global__ void split_x_kernel(const float* __restrict__ x, int B, int d, int nb, int pitch,
+                               uint16_t* __restrict__ hi, uint16_t* __restrict__ lo) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nb * pitch) return;
+    const int n = i / pitch, k = i - n * pitch;
+    const float v = (n < B && k < d) ? x[static_cast<size_t>(n) * d + k] : 0.f;
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
+    hi[i] = __bfloat16_as_ushort(h);
+    lo[i] = __bfloat16_as_ushort(l);
+}
+
+// T partials: Tp[split][j][n] over K slice `split`
+__global__ void __launch_bounds__(kBThreads) t_kernel(BatchArgs a) {
+    extern __shared__ __align__(128) uint16_t smb[];
+    float acc[kMaxBatch / 8][4];
+    const int kslice = ((a.pitch_d + a.tsplit - 1) / a.tsplit + kBK - 1) / kBK * kBK;
+    const int k0 = min(a.pitch_d, blockIdx.y * kslice), k1 = min(a.pitch_d, k0 + kslice);
+    gemm_tile<false>(a.Bm, a.pitch_d, nullptr, a.r, blockIdx.x * kBM, a.xh, a.xl, a.pitch_d, a.nb, k0,
+                     k1, smb, acc);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int t = 0; t < kMaxBatch / 8; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (t >= a.nb / 8) continue;
+            const int j = blockIdx.x * kBM + warp * 16 + (lane >> 2) + (e >> 1) * 8;
+            const int n = t * 8 + (lane & 3) * 2 + (e & 1);
+            if (j < a.r) a.tp[(static_cast<size_t>(blockIdx.y) * a.pitch_r + j) * kMaxBatch + n] = acc[t][e];
+        }
+}
+
+// T = sum of the splits in order -> bf16 hi/lo [nb][pitch_r]
+__global__ void t_reduce_kernel(BatchArgs a) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.nb * a.pitch_r) return;
+    const int n = i / a.pitch_r, j = i - n * a.pitch_r;
+    float s = 0.f;
+    if (j < a.r)
+        for (int sp = 0; sp < a.tsplit; ++sp)
+            s += a.tp[(static_cast<size_t>(sp) * a.pitch_r + j) * kMaxBatch + n];
+    const __nv_bfloat16 h = __float2bfloat16_rn(s);
+    const __nv_bfloat16 l = __float2bfloat16_rn(s - __bfloat162float(h));
+    a.th[i] = __bfloat16_as_ushort(h);
+    a.tl[i] = __bfloat16_as_ushort(l);
+}
+
+// pre = A T + bias over all D rows: mask bits, union flags, per-token |P|
+__global__ void __launch_bounds__(kBThreads) mask_kernel(BatchArgs a) {
+    extern __shared__ __align__(128) uint16_t smb[];
+    float acc[kMaxBatch / 8][4];
+    gemm_tile<false>(a.A, a.pitch_r, nullptr, a.D, blockIdx.x * kBM, a.th, a.tl, a.pitch_r, a.nb, 0,
+                     a.pitch_r, smb, acc);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t bits[2] = {0ull, 0ull};
+    const int rb = blockIdx.x * kBM + warp * 16 + (lane >> 2);
+#pragma unroll
+    for (int t = 0; t < kMaxBatch / 8; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (t >= a.nb / 8) continue;
+            const int h = e >> 1, row = rb + h * 8;
+            const int n = t * 8 + (lane & 3) * 2 + (e & 1);
+            if (row < a.D && n < a.B && acc[t][e] + a.bias[row] > 0.f)  // strict, ffn_exec.hpp:141
+                bits[h] |= 1ull << n;
+        }
+    for (int h = 0; h < 2; ++h) {
+        bits[h] |= __shfl_xor_sync(0xffffffffu, bits[h], 1);
+        bits[h] |= __shfl_xor_sync(0xffffffffu, bits[h], 2);
+        const int row = rb + h * 8;
+        if ((lane & 3) == 0 && row < a.D) {
+            a.mbits[row] = bits[h];
+            a.uflag[row] = bits[h] != 0ull;
+            for (uint64_t b = bits[h]; b; b &= b - 1) atomicAdd(a.pcount + __ffsll(static_cast<long long>(b)) - 1, 1);
+        }
+    }
+}
+
+// ascending compaction of flags[0..D) into list, count into *count (one CTA)
+__global__ void __launch_bounds__(1024) compact_kernel(const int* __restrict__ flag, int D,
+                                                       int* __restrict__ list, int* __restrict__ count) {
+    __shared__ int wsum[32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int base = 0; base < D; base += 1024) {
+        const int i = base + threadIdx.x;
+        const int f = i < D ? flag[i] : 0;
+        const unsigned b = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) wsum[warp] = __popc(b);
+        __syncthreads();
+        int pre = 0;
+        for (int w = 0; w < warp; ++w) pre += wsum[w];
+        if (f) list[carry + pre + __popc(b & ((1u << lane) - 1u))] = i;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int w = 0; w < 32; ++w) t += wsum[w];
+            carry += t;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *count = carry;
+}
+
+// g = gate[U_P] x: survivor bits, union flags, per-token |V|; G stored per neuron
+__global__ void __launch_bounds__(kBThreads) gate_kernel(BatchArgs a) {
+    extern __shared__ __align__(128) uint16_t smb[];
+    const int np = *a.np;
+    if (blockIdx.x * kBM >= np) return;
+    float acc[kMaxBatch / 8][4];
+    gemm_tile<false>(a.gate, a.pitch_d, a.plist, np, blockIdx.x * kBM, a.xh, a.xl, a.pitch_d, a.nb, 0,
+                     a.pitch_d, smb, acc);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rb = blockIdx.x * kBM + warp * 16 + (lane >> 2);
+    uint64_t bits[2] = {0ull, 0ull};
+    int nid[2];
+    for (int h = 0; h < 2; ++h) nid[h] = rb + h * 8 < np ? a.plist[rb + h * 8] : -1;
+#pragma unroll
+    for (int t = 0; t < kMaxBatch / 8; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (t >= a.nb / 8) continue;
+            const int h = e >> 1;
+            const int n = t * 8 + (lane & 3) * 2 + (e & 1);
+            if (nid[h] < 0) continue;
+            a.G[static_cast<size_t>(nid[h]) * kMaxBatch + n] = acc[t][e];
+            if (n < a.B && ((a.mbits[nid[h]] >> n) & 1ull) && acc[t][e] > 0.f)  // ffn_exec.hpp:200
+                bits[h] |= 1ull << n;
+        }
+    for (int h = 0; h < 2; ++h) {
+        bits[h] |= __shfl_xor_sync(0xffffffffu, bits[h], 1);
+        bits[h] |= __shfl_xor_sync(0xffffffffu, bits[h], 2);
+        if ((lane & 3) == 0 && nid[h] >= 0) {
+            a.vbits[nid[h]] = bits[h];
+            a.vflag[nid[h]] = bits[h] != 0ull;
+            for (uint64_t b = bits[h]; b; b &= b - 1) atomicAdd(a.vcount + __ffsll(static_cast<long long>(b)) - 1, 1);
+        }
+    }
+}
+
+// u = up[U_V] x; z = gated(g, u) on survivor bits (ffn_exec.hpp:202-203, :68-76)
+// -> Z hi/lo [nb][pitch_v] (k = survivor position) and z per (neuron, token)
+__global__ void __launch_bounds__(kBThreads) up_kernel(BatchArgs a) {
+    extern __shared__ __align__(128) uint16_t smb[];
+    const int nv = *a.nv;
+    if (blockIdx.x * kBM >= nv) return;
+    float acc[kMaxBatch / 8][4];
+    gemm_tile<false>(a.ud, 2 * a.pitch_d, a.vlist, nv, blockIdx.x * kBM, a.xh, a.xl, a.pitch_d, a.nb, 0,
+                     a.pitch_d, smb, acc);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rb = blockIdx.x * kBM + warp * 16 + (lane >> 2);
+#pragma unroll
+    for (int t = 0; t < kMaxBatch / 8; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (t >= a.nb / 8) continue;
+            const int pos = rb + (e >> 1) * 8;
+            const int n = t * 8 + (lane & 3) * 2 + (e & 1);
+            if (pos >= nv) continue;
+            const int nid = a.vlist[pos];
+            float z = 0.f;
+            if (n < a.B && ((a.vbits[nid] >> n) & 1ull)) {
+                const float g = a.G[static_cast<size_t>(nid) * kMaxBatch + n], u = acc[t][e];
+                z = (g > 0.f && (a.act == 0 || u > 0.f)) ? g * u : 0.f;
+            }
+            a.Z[static_cast<size_t>(nid) * kMaxBatch + n] = z;
+            const __nv_bfloat16 h = __float2bfloat16_rn(z);
+            const __nv_bfloat16 l = __float2bfloat16_rn(z - __bfloat162float(h));
+            a.zh[static_cast<size_t>(n) * a.pitch_v + pos] = __bfloat16_as_ushort(h);
+            a.zl[static_cast<size_t>(n) * a.pitch_v + pos] = __bfloat16_as_ushort(l);
+        }
+}
+
+// zero the Z hi/lo columns [nv, round_up(nv, 64)) so the last K chunk adds +0
+__global__ void zpad_kernel(BatchArgs a) {
+    const int nv = *a.nv;
+    const int padto = (nv + kBK - 1) / kBK * kBK;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int w = padto - nv;
+    if (i >= w * a.nb) return;
+    const int n = i / w, pos = nv + (i - n * w);
+    a.zh[static_cast<size_t>(n) * a.pitch_v + pos] = 0;
+    a.zl[static_cast<size_t>(n) * a.pitch_v + pos] = 0;
+}
+
+// Y partials: Yp[split][n][m] = sum over survivor positions of split of down[.][m] z
+__global__ void __launch_bounds__(kBThreads) down_kernel(BatchArgs a) {
+    extern __shared__ __align__(128) uint16_t smb[];
+    const int nv = *a.nv;
+    const int chunks = (nv + kBK - 1) / kBK;
+    const int per = (chunks + a.dsplit - 1) / a.dsplit;
+    const int k0 = blockIdx.y * per * kBK, k1 = min(nv, k0 + per * kBK);
+    float acc[kMaxBatch / 8][4];
+    // down rows of neuron k live in ud at k * 2 pitch_d + pitch_d
+    gemm_tile<true>(a.ud + a.pitch_d, 2 * a.pitch_d, a.vlist, nv, blockIdx.x * kBM, a.zh, a.zl,
+                    a.pitch_v, a.nb, k0, k1 > k0 ? k1 : k0, smb, acc);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int t = 0; t < kMaxBatch / 8; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (t >= a.nb / 8) continue;
+            const int m = blockIdx.x * kBM + warp * 16 + (lane >> 2) + (e >> 1) * 8;
+            const int n = t * 8 + (lane & 3) * 2 + (e & 1);
+            if (m < a.pitch_d)
+                a.yp[(static_cast<size_t>(blockIdx.y) * kMaxBatch + n) * a.pitch_d + m] = acc[t][e];
+        }
+}
+
+__global__ void y_reduce_kernel(BatchArgs a, float* __restrict__ y) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.B * a.d) return;
+    const int n = i / a.d, m = i - n * a.d;
+    float s = 0.f;
+    for (int sp = 0; sp < a.dsplit; ++sp) s += a.yp[(static_cast<size_t>(sp) * kMaxBatch + n) * a.pitch_d + m];
+    y[i] = s;
+}
+
+int gemm_smem(bool trans) {
+    const int a = trans ? kBK * (kBM + 8) : kBM * kRowPad;
+    return 2 * (a + 2 * kMaxBatch * kRowPad) * 2;
+}
+
+}  // namespace
+
+int batch_max() { return kMaxBatch; }
+
+int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream_);
+    BatchArgs a = a0;
+    const int sm_rows = gemm_smem(false), sm_down = gemm_smem(true);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_rows);
+        cudaFuncSetAttribute(mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_rows);
+        cudaFuncSetAttribute(gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_rows);
+        cudaFuncSetAttribute(up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_rows);
+        cudaFuncSetAttribute(down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_down);
+        attr = true;
+    }
+    cudaMemsetAsync(a.pcount, 0, sizeof(int) * kMaxBatch, st);
+    cudaMemsetAsync(a.vcount, 0, sizeof(int) * kMaxBatch, st);
+    cudaMemsetAsync(a.vflag, 0, sizeof(int) * a.D, st);
+    cudaMemsetAsync(a.vbits, 0, sizeof(uint64_t) * a.D, st);
+    {
+        const int n = a.nb * a.pitch_d;
+        split_x_kernel<<<(n + 255) / 256, 256, 0, st>>>(xs, a.B, a.d, a.nb, a.pitch_d, a.xh, a.xl);
+    }
+    t_kernel<<<dim3((a.r + kBM - 1) / kBM, a.tsplit), kBThreads, sm_rows, st>>>(a);
+    {
+        const int n = a.nb * a.pitch_r;
+        t_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(a);
+    }
+    mask_kernel<<<(a.D + kBM - 1) / kBM, kBThreads, sm_rows, st>>>(a);
+    compact_kernel<<<1, 1024, 0, st>>>(a.uflag, a.D, a.plist, a.np);
+    gate_kernel<<<(a.D + kBM - 1) / kBM, kBThreads, sm_rows, st>>>(a);
+    compact_kernel<<<1, 1024, 0, st>>>(a.vflag, a.D, a.vlist, a.nv);
+    up_kernel<<<(a.D + kBM - 1) / kBM, kBThreads, sm_rows, st>>>(a);
+    zpad_kernel<<<(kBK * kMaxBatch + 255) / 256, 256, 0, st>>>(a);
+    down_kernel<<<dim3((a.pitch_d + kBM - 1) / kBM, a.dsplit), kBThreads, sm_down, st>>>(a);
+    {
+        const int n = a.B * a.d;
+        y_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(a, ys);
+    }
+    return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace sg

@@ -67,6 +67,13 @@ struct sg_ctx {
     size_t xs_cap = 0;
     uint64_t* dbgdev = nullptr;
     int dbg_layers = 0;
+    // batched decode workspace (allocated on first use)
+    void* bmem = nullptr;
+    sg::BatchArgs bw{};
+    float* bxdev = nullptr;  // host-entry staging [64][max_d]
+    float* bydev = nullptr;
+    const sg_layer* blast = nullptr;
+    int blast_B = 0;
 };
 
 constexpr int kMaxStackLayers = 1024;
@@ -536,8 +543,136 @@ sg_status sg_ctx_destroy(sg_ctx* C) {
     if (C->xsdev) cudaFree(C->xsdev);
     if (C->ysdev) cudaFree(C->ysdev);
     if (C->dbgdev) cudaFree(C->dbgdev);
+    if (C->bmem) cudaFree(C->bmem);
     delete C;
     return SG_OK;
+}
+
+// ---- batched decode ------------------------------------------------------------
+namespace {
+sg_status batch_workspace(sg_ctx* C) {
+    if (C->bmem) return SG_OK;
+    const int M = sg::batch_max();
+    const size_t Dm = static_cast<size_t>(C->max_D), pd = static_cast<size_t>(C->pitch_dmax),
+                 pr = static_cast<size_t>(C->pitch_rmax);
+    const size_t pv = (Dm + 63) / 64 * 64;
+    const int tsplit = 16, dsplit = 4;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off += (bytes + 255) / 256 * 256;
+        return o;
+    };
+    const size_t o_xh = take(M * pd * 2), o_xl = take(M * pd * 2), o_tp = take(tsplit * pr * M * 4),
+                 o_th = take(M * pr * 2), o_tl = take(M * pr * 2), o_mb = take(Dm * 8),
+                 o_uf = take(Dm * 4), o_pc = take(M * 4), o_pl = take(Dm * 4), o_np = take(4),
+                 o_G = take(Dm * M * 4), o_vb = take(Dm * 8), o_vf = take(Dm * 4), o_vc = take(M * 4),
+                 o_vl = take(Dm * 4), o_nv = take(4), o_Z = take(Dm * M * 4), o_zh = take(M * pv * 2),
+                 o_zl = take(M * pv * 2), o_yp = take(dsplit * M * pd * 4), o_bx = take(M * pd * 4),
+                 o_by = take(M * pd * 4);
+    DeviceGuard dg(C->device);
+    cudaError_t e = cudaMalloc(&C->bmem, off);
+    if (e == cudaSuccess) e = cudaMemset(C->bmem, 0, off);
+    if (e != cudaSuccess) {
+        C->bmem = nullptr;
+        return fail(SG_ERR_CUDA, std::string("batch workspace: ") + cudaGetErrorString(e));
+    }
+    char* b = static_cast<char*>(C->bmem);
+    sg::BatchArgs& a = C->bw;
+    a.pitch_v = static_cast<int>(pv);
+    a.tsplit = tsplit;
+    a.dsplit = dsplit;
+    a.xh = reinterpret_cast<uint16_t*>(b + o_xh);
+    a.xl = reinterpret_cast<uint16_t*>(b + o_xl);
+    a.tp = reinterpret_cast<float*>(b + o_tp);
+    a.th = reinterpret_cast<uint16_t*>(b + o_th);
+    a.tl = reinterpret_cast<uint16_t*>(b + o_tl);
+    a.mbits = reinterpret_cast<uint64_t*>(b + o_mb);
+    a.uflag = reinterpret_cast<int*>(b + o_uf);
+    a.pcount = reinterpret_cast<int*>(b + o_pc);
+    a.plist = reinterpret_cast<int*>(b + o_pl);
+    a.np = reinterpret_cast<int*>(b + o_np);
+    a.G = reinterpret_cast<float*>(b + o_G);
+    a.vbits = reinterpret_cast<uint64_t*>(b + o_vb);
+    a.vflag = reinterpret_cast<int*>(b + o_vf);
+    a.vcount = reinterpret_cast<int*>(b + o_vc);
+    a.vlist = reinterpret_cast<int*>(b + o_vl);
+    a.nv = reinterpret_cast<int*>(b + o_nv);
+    a.Z = reinterpret_cast<float*>(b + o_Z);
+    a.zh = reinterpret_cast<uint16_t*>(b + o_zh);
+    a.zl = reinterpret_cast<uint16_t*>(b + o_zl);
+    a.yp = reinterpret_cast<float*>(b + o_yp);
+    C->bxdev = reinterpret_cast<float*>(b + o_bx);
+    C->bydev = reinterpret_cast<float*>(b + o_by);
+    return SG_OK;
+}
+}  // namespace
+
+sg_status sg_ffn_forward_batch(sg_ctx* C, const sg_layer* L, const float* xs, int32_t batch,
+                               float* ys, void* stream) {
+    if (sg_status s = check_pair(C, L); s != SG_OK) return s;
+    if (!L->has_pred || !L->has_w) return fail(SG_ERR_USAGE, "batched decode needs weights and a predictor");
+    if (batch < 1 || batch > sg::batch_max())
+        return fail(SG_ERR_USAGE, "batch must be in [1, " + std::to_string(sg::batch_max()) + "]");
+    if (xs == nullptr || ys == nullptr) return fail(SG_ERR_USAGE, "null buffers");
+    if (sg_status s = batch_workspace(C); s != SG_OK) return s;
+    DeviceGuard dg(C->device);
+    sg::BatchArgs a = C->bw;
+    a.B = batch;
+    a.nb = (batch + 7) / 8 * 8;
+    a.d = static_cast<int>(L->d);
+    a.D = static_cast<int>(L->D_local);
+    a.r = static_cast<int>(L->r);
+    a.pitch_d = L->pitch_d;
+    a.pitch_r = L->pitch_r;
+    a.act = L->act;
+    a.Bm = L->view.B;
+    a.A = L->view.A;
+    a.bias = L->view.bias;
+    a.gate = L->view.gate;
+    a.ud = L->view.ud;
+    const int e = sg::launch_batch(a, xs, ys, stream);
+    if (e != 0) return fail(SG_ERR_CUDA, std::string("batch launch: ") +
+                                             cudaGetErrorString(static_cast<cudaError_t>(e)));
+    C->blast = L;
+    C->blast_B = batch;
+    return SG_OK;
+}
+
+sg_status sg_ctx_read_batch(sg_ctx* C, void* stream, int32_t batch, sg_exec_stats* stats,
+                            uint64_t* pred_bits, uint64_t* surv_bits) {
+    if (C == nullptr || C->blast == nullptr) return fail(SG_ERR_USAGE, "no batched call on this ctx");
+    if (batch != C->blast_B) return fail(SG_ERR_USAGE, "batch differs from the last batched call");
+    DeviceGuard dg(C->device);
+    SG_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    const sg_layer* L = C->blast;
+    int pc[64], vc[64];
+    SG_CUDA(cudaMemcpy(pc, C->bw.pcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
+    SG_CUDA(cudaMemcpy(vc, C->bw.vcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
+    for (int b = 0; stats && b < batch; ++b) stats[b] = make_stats(L, SG_PIPELINE_SEQUENTIAL, pc[b], vc[b]);
+    if (pred_bits)
+        SG_CUDA(cudaMemcpy(pred_bits, C->bw.mbits, sizeof(uint64_t) * L->D_local, cudaMemcpyDeviceToHost));
+    if (surv_bits)
+        SG_CUDA(cudaMemcpy(surv_bits, C->bw.vbits, sizeof(uint64_t) * L->D_local, cudaMemcpyDeviceToHost));
+    return SG_OK;
+}
+
+sg_status sg_ffn_forward_batch_host(sg_ctx* C, const sg_layer* L, const float* xs_host,
+                                    int32_t batch, float* ys_host, sg_exec_stats* stats,
+                                    void* stream) {
+    if (sg_status s = check_pair(C, L); s != SG_OK) return s;
+    if (xs_host == nullptr || ys_host == nullptr || batch < 1 || batch > sg::batch_max())
+        return fail(SG_ERR_USAGE, "bad batch buffers");
+    for (int64_t i = 0; i < static_cast<int64_t>(batch) * L->d; ++i)
+        if (!std::isfinite(xs_host[i])) return fail(SG_ERR_DATA, "input: non-finite entries");
+    if (sg_status s = batch_workspace(C); s != SG_OK) return s;
+    DeviceGuard dg(C->device);
+    auto st = static_cast<cudaStream_t>(stream);
+    const size_t bytes = static_cast<size_t>(batch) * L->d * 4;
+    SG_CUDA(cudaMemcpyAsync(C->bxdev, xs_host, bytes, cudaMemcpyHostToDevice, st));
+    if (sg_status s = sg_ffn_forward_batch(C, L, C->bxdev, batch, C->bydev, stream); s != SG_OK) return s;
+    SG_CUDA(cudaMemcpyAsync(ys_host, C->bydev, bytes, cudaMemcpyDeviceToHost, st));
+    return sg_ctx_read_batch(C, stream, batch, stats, nullptr, nullptr);
 }
 
 sg_status sg_ffn_forward_device(sg_ctx* C, const sg_layer* L, sg_pipeline pipeline,

@@ -69,4 +69,40 @@ int launch_layers(const LayerView* layers_dev, int n, const LayerView& first, co
                   int num_ctas, void* stream);
 int query_launch_info(int device, LaunchInfo* info);
 
+// Batched decode (sg_batch.cu): one layer, B <= batch_max() tokens.
+struct BatchArgs {
+    int B;        // tokens
+    int nb;       // B rounded up to a multiple of 8
+    int d, D, r;  // hidden, local inter, rank
+    int pitch_d, pitch_r, pitch_v;  // pitch_v: survivor-position pitch of Z (>= round_up(D, 64))
+    int act;
+    int tsplit, dsplit;             // split-K of the T and down GEMMs
+    // layer
+    const uint16_t* Bm;  // predictor B, r x pitch_d
+    const uint16_t* A;   // D x pitch_r
+    const float* bias;
+    const uint16_t* gate;
+    const uint16_t* ud;
+    // workspace
+    uint16_t *xh, *xl;       // [64][pitch_d]
+    float* tp;               // [tsplit][pitch_r][64]
+    uint16_t *th, *tl;       // [64][pitch_r]
+    uint64_t* mbits;         // [D] predicted-active bit per token
+    int* uflag;              // [D] union of the predicted sets
+    int* pcount;             // [64] |P_b|
+    int* plist;              // [D] union, ascending
+    int* np;
+    float* G;                // [D][64] gate pre-activations
+    uint64_t* vbits;         // [D] survivor bit per token
+    int* vflag;              // [D]
+    int* vcount;             // [64] |V_b|
+    int* vlist;              // [D]
+    int* nv;
+    float* Z;                // [D][64] gated values
+    uint16_t *zh, *zl;       // [64][pitch_v]
+    float* yp;               // [dsplit][64][pitch_d]
+};
+int batch_max();
+int launch_batch(const BatchArgs& a, const float* xs, float* ys, void* stream);
+
 }  // namespace sg

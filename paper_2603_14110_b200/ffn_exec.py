@@ -327,6 +327,30 @@ class DeviceLayer:
                                                C.c_void_p(x_ptr), C.c_void_p(y_ptr),
                                                C.c_void_p(stream)))
 
+    def forward_batch(self, X, ctx: Optional[Context] = None, stream: int = 0):
+        """Batched decode (sg_ffn_forward_batch_host): X (B, hidden) -> (Y (B, hidden) f64,
+        per-token ExecStats, per-token predicted and survivor index arrays (global))."""
+        ctx = ctx or self.context()
+        X = np.ascontiguousarray(np.asarray(X, dtype=np.float32))
+        if X.ndim != 2 or X.shape[1] != self.hidden:
+            raise DataError("batch input must be (B, hidden)")
+        B = X.shape[0]
+        Y = np.zeros_like(X)
+        st = (capi.sg_exec_stats * B)()
+        check(capi.lib().sg_ffn_forward_batch_host(ctx.handle, self.handle,
+                                                   X.ctypes.data_as(C.c_void_p), B,
+                                                   Y.ctypes.data_as(C.c_void_p), st,
+                                                   C.c_void_p(stream)))
+        pb = np.zeros(self.local_inter, dtype=np.uint64)
+        vb = np.zeros(self.local_inter, dtype=np.uint64)
+        check(capi.lib().sg_ctx_read_batch(ctx.handle, C.c_void_p(stream), B, None,
+                                           pb.ctypes.data_as(C.c_void_p),
+                                           vb.ctypes.data_as(C.c_void_p)))
+        gidx = np.array([self.global_index(k) for k in range(self.local_inter)], dtype=np.int64)
+        P = [np.sort(gidx[((pb >> np.uint64(b)) & np.uint64(1)).astype(bool)]) for b in range(B)]
+        V = [np.sort(gidx[((vb >> np.uint64(b)) & np.uint64(1)).astype(bool)]) for b in range(B)]
+        return Y.astype(np.float64), [ExecStats.from_c(s) for s in st], P, V
+
     def predict_mask(self, x, ctx: Optional[Context] = None, stream: int = 0) -> Mask:
         ctx = ctx or self.context()
         x = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1))

@@ -87,14 +87,14 @@ def build_host_layer(d, D, act, seed, rank=256, sparsity=0.5, calib_tokens=256, 
 
 
 def build_host_model(config: str, layers: int = None, seed_base: int = 0, rank: int = 256,
-                     sparsity: float = 0.5, workers: int = None, log=None):
+                     sparsity: float = 0.5, workers: int = None, log=None, eval_tokens: int = 16):
     cfg = CONFIGS[config]
     L = layers or cfg["L"]
     workers = workers or max(1, min(L, (os.cpu_count() or 4) // 2))
     out = [None] * L
     with cf.ThreadPoolExecutor(workers) as ex:
         futs = {ex.submit(build_host_layer, cfg["d"], cfg["D"], cfg["act"], seed_base + l, rank,
-                          sparsity): l for l in range(L)}
+                          sparsity, eval_tokens=eval_tokens): l for l in range(L)}
         for f in cf.as_completed(futs):
             out[futs[f]] = f.result()
             if log:
