@@ -80,6 +80,11 @@ __device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b
 // TRANS_A: W is stored [k][m] (m contiguous, pitch wp) — the down projection,
 // where "rows" index K (neurons) and the 64-wide tile runs over m.
 // ---------------------------------------------------------------------------
+constexpr int kStages = 6;  // cp.async pipeline depth (K chunks in flight)
+
+__host__ __device__ constexpr int a_elems(bool trans) { return trans ? kBK * (kBM + 8) : kBM * kRowPad; }
+__host__ __device__ inline int stage_elems(bool trans, int nb) { return a_elems(trans) + 2 * nb * kRowPad; }
+
 template <bool TRANS_A>
 __device__ __forceinline__ void gemm_tile(const uint16_t* __restrict__ W, int wp,
                                           const int* __restrict__ rows, int nrows, int m0,
@@ -88,15 +93,14 @@ __device__ __forceinline__ void gemm_tile(const uint16_t* __restrict__ W, int wp
                                           int k1, uint16_t* sm, float (*acc)[4]) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int ntile = nb >> 3;
-    // stage layout: A [64][kRowPad] (TRANS_A: [kBK][64 + 8]) then Xh, Xl [nb][kRowPad]
-    constexpr int kAElems = TRANS_A ? kBK * (kBM + 8) : kBM * kRowPad;
-    const int stage_elems = kAElems + 2 * kMaxBatch * kRowPad;
+    constexpr int kA = a_elems(TRANS_A);
+    const int se = stage_elems(TRANS_A, nb);
+    const int nk = k1 > k0 ? (k1 - k0 + kBK - 1) / kBK : 0;
     auto load = [&](int st, int kb) {
-        uint16_t* a = sm + st * stage_elems;
-        uint16_t* xh = a + kAElems;
-        uint16_t* xl = xh + kMaxBatch * kRowPad;
+        uint16_t* a = sm + st * se;
+        uint16_t* xh = a + kA;
+        uint16_t* xl = xh + nb * kRowPad;
         if (!TRANS_A) {
-            // 64 rows x 64 k: 8 pieces of 16 B per row
             for (int i = tid; i < kBM * 8; i += kBThreads) {
                 const int r = i >> 3, p = i & 7;
                 const int gr = m0 + r;
@@ -119,23 +123,27 @@ __device__ __forceinline__ void gemm_tile(const uint16_t* __restrict__ W, int wp
             cp16(xh + n * kRowPad + p * 8, Xh + static_cast<size_t>(n) * xp + kb + p * 8, true);
             cp16(xl + n * kRowPad + p * 8, Xl + static_cast<size_t>(n) * xp + kb + p * 8, true);
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
     };
+#pragma unroll
     for (int t = 0; t < kMaxBatch / 8; ++t)
+#pragma unroll
         for (int e = 0; e < 4; ++e) acc[t][e] = 0.f;
-    const int nk = (k1 - k0 + kBK - 1) / kBK;
-    if (nk > 0) load(0, k0);
+    // prologue: chunks 0 .. kStages-2 in flight (one commit group each, empty ones too)
+    for (int s = 0; s < kStages - 1; ++s) {
+        if (s < nk) load(s, k0 + s * kBK);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     for (int it = 0; it < nk; ++it) {
-        if (it + 1 < nk) {
-            load((it + 1) & 1, k0 + (it + 1) * kBK);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 2) : "memory");
+        __syncthreads();  // chunk `it` visible to all; stage (it-1) % S free to refill
+        {
+            const int nx = it + kStages - 1;
+            if (nx < nk) load(nx % kStages, k0 + nx * kBK);
+            asm volatile("cp.async.commit_group;" ::: "memory");
         }
-        __syncthreads();
-        const uint16_t* a = sm + (it & 1) * stage_elems;
-        const uint16_t* xh = a + kAElems;
-        const uint16_t* xl = xh + kMaxBatch * kRowPad;
+        const uint16_t* a = sm + (it % kStages) * se;
+        const uint16_t* xh = a + kA;
+        const uint16_t* xl = xh + nb * kRowPad;
 #pragma unroll
         for (int ks = 0; ks < kBK; ks += 16) {
             uint32_t af[4];
@@ -163,7 +171,35 @@ __device__ __forceinline__ void gemm_tile(const uint16_t* __restrict__ W, int wp
                 }
             }
         }
-        __syncthreads();
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+}
+
+// acc -> out[(split * cap + row) * 64 + n] for the CTA's rows (fp32 partial sums)
+__device__ __forceinline__ void store_partial(float (*acc)[4], float* out, int cap, int split, int m0,
+                                              int nrows, int nb) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int t = 0; t < kMaxBatch / 8; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (t >= nb / 8) continue;
+            const int row = m0 + warp * 16 + (lane >> 2) + (e >> 1) * 8;
+            const int n = t * 8 + (lane & 3) * 2 + (e & 1);
+            if (row < nrows) out[(static_cast<size_t>(split) * cap + row) * kMaxBatch + n] = acc[t][e];
+        }
+}
+
+// Per-token counts of the set bits of this warp's rows (each lane may carry up to
+// two rows' masks; duplicates across a lane group must be zero) -> one atomicAdd
+// per token per warp (integer: order-free).
+__device__ __forceinline__ void count_tokens(uint64_t m0, uint64_t m1, int B, int* counts) {
+    const int lane = threadIdx.x & 31;
+    for (int n = 0; n < B; ++n) {
+        const unsigned c = __popc(__ballot_sync(0xffffffffu, (m0 >> n) & 1ull)) +
+                           __popc(__ballot_sync(0xffffffffu, (m1 >> n) & 1ull));
+        if (lane == 0 && c) atomicAdd(counts + n, static_cast<int>(c));
     }
 }
 
@@ -180,7 +216,7 @@ __global__ void split_x_kernel(const float* __restrict__ x, int B, int d, int nb
     lo[i] = __bfloat16_as_ushort(l);
 }
 
-// T partials: Tp[split][j][n] over K slice `split`
+// T partials: tp[split][j][n] over K slice `split`
 __global__ void __launch_bounds__(kBThreads) t_kernel(BatchArgs a) {
     extern __shared__ __align__(128) uint16_t smb[];
     float acc[kMaxBatch / 8][4];
@@ -188,16 +224,7 @@ __global__ void __launch_bounds__(kBThreads) t_kernel(BatchArgs a) {
     const int k0 = min(a.pitch_d, blockIdx.y * kslice), k1 = min(a.pitch_d, k0 + kslice);
     gemm_tile<false>(a.Bm, a.pitch_d, nullptr, a.r, blockIdx.x * kBM, a.xh, a.xl, a.pitch_d, a.nb, k0,
                      k1, smb, acc);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-    for (int t = 0; t < kMaxBatch / 8; ++t)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            if (t >= a.nb / 8) continue;
-            const int j = blockIdx.x * kBM + warp * 16 + (lane >> 2) + (e >> 1) * 8;
-            const int n = t * 8 + (lane & 3) * 2 + (e & 1);
-            if (j < a.r) a.tp[(static_cast<size_t>(blockIdx.y) * a.pitch_r + j) * kMaxBatch + n] = acc[t][e];
-        }
+    store_partial(acc, a.tp, a.pitch_r, blockIdx.y, blockIdx.x * kBM, a.r, a.nb);
 }
 
 // T = sum of the splits in order -> bf16 hi/lo [nb][pitch_r]
@@ -241,106 +268,123 @@ __global__ void __launch_bounds__(kBThreads) mask_kernel(BatchArgs a) {
         if ((lane & 3) == 0 && row < a.D) {
             a.mbits[row] = bits[h];
             a.uflag[row] = bits[h] != 0ull;
-            for (uint64_t b = bits[h]; b; b &= b - 1) atomicAdd(a.pcount + __ffsll(static_cast<long long>(b)) - 1, 1);
         }
+        if ((lane & 3) != 0 || row >= a.D) bits[h] = 0ull;  // count each row once
     }
+    count_tokens(bits[0], bits[1], a.B, a.pcount);
 }
 
-// ascending compaction of flags[0..D) into list, count into *count (one CTA)
+// ascending compaction of flags[0..D) into list, count into *count (one CTA):
+// thread t scans a contiguous run, one block-wide exclusive scan, then writes.
 __global__ void __launch_bounds__(1024) compact_kernel(const int* __restrict__ flag, int D,
                                                        int* __restrict__ list, int* __restrict__ count) {
     __shared__ int wsum[32];
-    __shared__ int carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int base = 0; base < D; base += 1024) {
-        const int i = base + threadIdx.x;
-        const int f = i < D ? flag[i] : 0;
-        const unsigned b = __ballot_sync(0xffffffffu, f);
-        if (lane == 0) wsum[warp] = __popc(b);
-        __syncthreads();
-        int pre = 0;
-        for (int w = 0; w < warp; ++w) pre += wsum[w];
-        if (f) list[carry + pre + __popc(b & ((1u << lane) - 1u))] = i;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int t = 0;
-            for (int w = 0; w < 32; ++w) t += wsum[w];
-            carry += t;
-        }
-        __syncthreads();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (D + 1023) / 1024;
+    const int i0 = tid * per, i1 = min(D, i0 + per);
+    int c = 0;
+    for (int i = i0; i < i1; ++i) c += flag[i] != 0;
+    int incl = c;
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, m);
+        if (lane >= m) incl += o;
     }
-    if (threadIdx.x == 0) *count = carry;
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int w = wsum[lane], wi = w;
+#pragma unroll
+        for (int m = 1; m < 32; m <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, wi, m);
+            if (lane >= m) wi += o;
+        }
+        wsum[lane] = wi - w;  // exclusive
+        if (lane == 31) *count = wi;
+    }
+    __syncthreads();
+    int pos = wsum[warp] + incl - c;
+    for (int i = i0; i < i1; ++i)
+        if (flag[i]) list[pos++] = i;
 }
 
-// g = gate[U_P] x: survivor bits, union flags, per-token |V|; G stored per neuron
+// gate[U_P] x, split-K partials: gp[split][pos][n]
 __global__ void __launch_bounds__(kBThreads) gate_kernel(BatchArgs a) {
     extern __shared__ __align__(128) uint16_t smb[];
     const int np = *a.np;
     if (blockIdx.x * kBM >= np) return;
+    const int kslice = ((a.pitch_d + a.gsplit - 1) / a.gsplit + kBK - 1) / kBK * kBK;
+    const int k0 = min(a.pitch_d, blockIdx.y * kslice), k1 = min(a.pitch_d, k0 + kslice);
     float acc[kMaxBatch / 8][4];
-    gemm_tile<false>(a.gate, a.pitch_d, a.plist, np, blockIdx.x * kBM, a.xh, a.xl, a.pitch_d, a.nb, 0,
-                     a.pitch_d, smb, acc);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int rb = blockIdx.x * kBM + warp * 16 + (lane >> 2);
-    uint64_t bits[2] = {0ull, 0ull};
-    int nid[2];
-    for (int h = 0; h < 2; ++h) nid[h] = rb + h * 8 < np ? a.plist[rb + h * 8] : -1;
-#pragma unroll
-    for (int t = 0; t < kMaxBatch / 8; ++t)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            if (t >= a.nb / 8) continue;
-            const int h = e >> 1;
-            const int n = t * 8 + (lane & 3) * 2 + (e & 1);
-            if (nid[h] < 0) continue;
-            a.G[static_cast<size_t>(nid[h]) * kMaxBatch + n] = acc[t][e];
-            if (n < a.B && ((a.mbits[nid[h]] >> n) & 1ull) && acc[t][e] > 0.f)  // ffn_exec.hpp:200
-                bits[h] |= 1ull << n;
-        }
-    for (int h = 0; h < 2; ++h) {
-        bits[h] |= __shfl_xor_sync(0xffffffffu, bits[h], 1);
-        bits[h] |= __shfl_xor_sync(0xffffffffu, bits[h], 2);
-        if ((lane & 3) == 0 && nid[h] >= 0) {
-            a.vbits[nid[h]] = bits[h];
-            a.vflag[nid[h]] = bits[h] != 0ull;
-            for (uint64_t b = bits[h]; b; b &= b - 1) atomicAdd(a.vcount + __ffsll(static_cast<long long>(b)) - 1, 1);
-        }
-    }
+    gemm_tile<false>(a.gate, a.pitch_d, a.plist, np, blockIdx.x * kBM, a.xh, a.xl, a.pitch_d, a.nb, k0,
+                     k1, smb, acc);
+    store_partial(acc, a.gp, a.pitch_v, blockIdx.y, blockIdx.x * kBM, np, a.nb);
 }
 
-// u = up[U_V] x; z = gated(g, u) on survivor bits (ffn_exec.hpp:202-203, :68-76)
-// -> Z hi/lo [nb][pitch_v] (k = survivor position) and z per (neuron, token)
+// g = sum of the splits in order; survivor bits = mask & (g > 0) (ffn_exec.hpp:200),
+// union flags, per-token |V|; G stored per neuron. One warp per neuron: lane n, n+32.
+__global__ void gate_epi_kernel(BatchArgs a) {
+    const int np = *a.np;
+    const int pos = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (pos >= np) return;
+    const int nid = a.plist[pos];
+    const uint64_t mb = a.mbits[nid];
+    uint64_t bits = 0ull;
+    for (int h = 0; h < 2; ++h) {
+        const int n = lane + 32 * h;
+        if (n >= a.nb) continue;
+        float g = 0.f;
+        for (int sp = 0; sp < a.gsplit; ++sp)
+            g += a.gp[(static_cast<size_t>(sp) * a.pitch_v + pos) * kMaxBatch + n];
+        a.G[static_cast<size_t>(nid) * kMaxBatch + n] = g;
+        if (n < a.B && ((mb >> n) & 1ull) && g > 0.f) bits |= 1ull << n;
+    }
+    bits = static_cast<uint64_t>(__reduce_or_sync(0xffffffffu, static_cast<unsigned>(bits))) |
+           (static_cast<uint64_t>(__reduce_or_sync(0xffffffffu, static_cast<unsigned>(bits >> 32))) << 32);
+    if (lane == 0) {
+        a.vbits[nid] = bits;
+        a.vflag[nid] = bits != 0ull;
+    }
+    // per-token |V| (one neuron per warp: at most one atomic per token per neuron)
+    if (lane < a.B && ((bits >> lane) & 1ull)) atomicAdd(a.vcount + lane, 1);
+    if (lane + 32 < a.B && ((bits >> (lane + 32)) & 1ull)) atomicAdd(a.vcount + lane + 32, 1);
+}
+
+// up[U_V] x, split-K partials: gp[split][pos][n] (the gate partials are consumed)
 __global__ void __launch_bounds__(kBThreads) up_kernel(BatchArgs a) {
     extern __shared__ __align__(128) uint16_t smb[];
     const int nv = *a.nv;
     if (blockIdx.x * kBM >= nv) return;
+    const int kslice = ((a.pitch_d + a.gsplit - 1) / a.gsplit + kBK - 1) / kBK * kBK;
+    const int k0 = min(a.pitch_d, blockIdx.y * kslice), k1 = min(a.pitch_d, k0 + kslice);
     float acc[kMaxBatch / 8][4];
-    gemm_tile<false>(a.ud, 2 * a.pitch_d, a.vlist, nv, blockIdx.x * kBM, a.xh, a.xl, a.pitch_d, a.nb, 0,
-                     a.pitch_d, smb, acc);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int rb = blockIdx.x * kBM + warp * 16 + (lane >> 2);
-#pragma unroll
-    for (int t = 0; t < kMaxBatch / 8; ++t)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            if (t >= a.nb / 8) continue;
-            const int pos = rb + (e >> 1) * 8;
-            const int n = t * 8 + (lane & 3) * 2 + (e & 1);
-            if (pos >= nv) continue;
-            const int nid = a.vlist[pos];
-            float z = 0.f;
-            if (n < a.B && ((a.vbits[nid] >> n) & 1ull)) {
-                const float g = a.G[static_cast<size_t>(nid) * kMaxBatch + n], u = acc[t][e];
-                z = (g > 0.f && (a.act == 0 || u > 0.f)) ? g * u : 0.f;
-            }
-            a.Z[static_cast<size_t>(nid) * kMaxBatch + n] = z;
-            const __nv_bfloat16 h = __float2bfloat16_rn(z);
-            const __nv_bfloat16 l = __float2bfloat16_rn(z - __bfloat162float(h));
-            a.zh[static_cast<size_t>(n) * a.pitch_v + pos] = __bfloat16_as_ushort(h);
-            a.zl[static_cast<size_t>(n) * a.pitch_v + pos] = __bfloat16_as_ushort(l);
-        }
+    gemm_tile<false>(a.ud, 2 * a.pitch_d, a.vlist, nv, blockIdx.x * kBM, a.xh, a.xl, a.pitch_d, a.nb, k0,
+                     k1, smb, acc);
+    store_partial(acc, a.gp, a.pitch_v, blockIdx.y, blockIdx.x * kBM, nv, a.nb);
+}
+
+// u = sum of the splits; z = gated(g, u) on survivor bits (ffn_exec.hpp:202-203,
+// :68-76), else +0 -> Z per (neuron, token) and Z hi/lo [n][pos] for the down GEMM
+__global__ void up_epi_kernel(BatchArgs a) {
+    const int nv = *a.nv;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int pos = i / kMaxBatch, n = i - pos * kMaxBatch;
+    if (pos >= nv || n >= a.nb) return;
+    const int nid = a.vlist[pos];
+    float z = 0.f;
+    if (n < a.B && ((a.vbits[nid] >> n) & 1ull)) {
+        float u = 0.f;
+        for (int sp = 0; sp < a.gsplit; ++sp)
+            u += a.gp[(static_cast<size_t>(sp) * a.pitch_v + pos) * kMaxBatch + n];
+        const float g = a.G[static_cast<size_t>(nid) * kMaxBatch + n];
+        z = (g > 0.f && (a.act == 0 || u > 0.f)) ? g * u : 0.f;
+    }
+    a.Z[static_cast<size_t>(nid) * kMaxBatch + n] = z;
+    const __nv_bfloat16 h = __float2bfloat16_rn(z);
+    const __nv_bfloat16 l = __float2bfloat16_rn(z - __bfloat162float(h));
+    a.zh[static_cast<size_t>(n) * a.pitch_v + pos] = __bfloat16_as_ushort(h);
+    a.zl[static_cast<size_t>(n) * a.pitch_v + pos] = __bfloat16_as_ushort(l);
 }
 
 // zero the Z hi/lo columns [nv, round_up(nv, 64)) so the last K chunk adds +0
@@ -388,10 +432,7 @@ __global__ void y_reduce_kernel(BatchArgs a, float* __restrict__ y) {
     y[i] = s;
 }
 
-int gemm_smem(bool trans) {
-    const int a = trans ? kBK * (kBM + 8) : kBM * kRowPad;
-    return 2 * (a + 2 * kMaxBatch * kRowPad) * 2;
-}
+int gemm_smem(bool trans, int nb) { return kStages * stage_elems(trans, nb) * 2; }
 
 }  // namespace
 
@@ -400,14 +441,16 @@ int batch_max() { return kMaxBatch; }
 int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_) {
     cudaStream_t st = static_cast<cudaStream_t>(stream_);
     BatchArgs a = a0;
-    const int sm_rows = gemm_smem(false), sm_down = gemm_smem(true);
+    const int sm_rows = gemm_smem(false, a.nb), sm_down = gemm_smem(true, a.nb);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_rows);
-        cudaFuncSetAttribute(mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_rows);
-        cudaFuncSetAttribute(gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_rows);
-        cudaFuncSetAttribute(up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_rows);
-        cudaFuncSetAttribute(down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_down);
+        const int mx = gemm_smem(false, kMaxBatch);
+        cudaFuncSetAttribute(t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             gemm_smem(true, kMaxBatch));
         attr = true;
     }
     cudaMemsetAsync(a.pcount, 0, sizeof(int) * kMaxBatch, st);
@@ -425,9 +468,11 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
     }
     mask_kernel<<<(a.D + kBM - 1) / kBM, kBThreads, sm_rows, st>>>(a);
     compact_kernel<<<1, 1024, 0, st>>>(a.uflag, a.D, a.plist, a.np);
-    gate_kernel<<<(a.D + kBM - 1) / kBM, kBThreads, sm_rows, st>>>(a);
+    gate_kernel<<<dim3((a.D + kBM - 1) / kBM, a.gsplit), kBThreads, sm_rows, st>>>(a);
+    gate_epi_kernel<<<(a.D + 7) / 8, 256, 0, st>>>(a);
     compact_kernel<<<1, 1024, 0, st>>>(a.vflag, a.D, a.vlist, a.nv);
-    up_kernel<<<(a.D + kBM - 1) / kBM, kBThreads, sm_rows, st>>>(a);
+    up_kernel<<<dim3((a.D + kBM - 1) / kBM, a.gsplit), kBThreads, sm_rows, st>>>(a);
+    up_epi_kernel<<<(a.D * kMaxBatch + 255) / 256, 256, 0, st>>>(a);
     zpad_kernel<<<(kBK * kMaxBatch + 255) / 256, 256, 0, st>>>(a);
     down_kernel<<<dim3((a.pitch_d + kBM - 1) / kBM, a.dsplit), kBThreads, sm_down, st>>>(a);
     {

@@ -556,7 +556,7 @@ sg_status batch_workspace(sg_ctx* C) {
     const size_t Dm = static_cast<size_t>(C->max_D), pd = static_cast<size_t>(C->pitch_dmax),
                  pr = static_cast<size_t>(C->pitch_rmax);
     const size_t pv = (Dm + 63) / 64 * 64;
-    const int tsplit = 16, dsplit = 4;
+    const int tsplit = 16, dsplit = 4, gsplit = 4;
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const size_t o = off;
@@ -569,7 +569,7 @@ sg_status batch_workspace(sg_ctx* C) {
                  o_G = take(Dm * M * 4), o_vb = take(Dm * 8), o_vf = take(Dm * 4), o_vc = take(M * 4),
                  o_vl = take(Dm * 4), o_nv = take(4), o_Z = take(Dm * M * 4), o_zh = take(M * pv * 2),
                  o_zl = take(M * pv * 2), o_yp = take(dsplit * M * pd * 4), o_bx = take(M * pd * 4),
-                 o_by = take(M * pd * 4);
+                 o_by = take(M * pd * 4), o_gp = take(gsplit * pv * M * 4);
     DeviceGuard dg(C->device);
     cudaError_t e = cudaMalloc(&C->bmem, off);
     if (e == cudaSuccess) e = cudaMemset(C->bmem, 0, off);
@@ -582,6 +582,8 @@ sg_status batch_workspace(sg_ctx* C) {
     a.pitch_v = static_cast<int>(pv);
     a.tsplit = tsplit;
     a.dsplit = dsplit;
+    a.gsplit = gsplit;
+    a.gp = reinterpret_cast<float*>(b + o_gp);
     a.xh = reinterpret_cast<uint16_t*>(b + o_xh);
     a.xl = reinterpret_cast<uint16_t*>(b + o_xl);
     a.tp = reinterpret_cast<float*>(b + o_tp);

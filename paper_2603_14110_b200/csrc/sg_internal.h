@@ -76,7 +76,7 @@ struct BatchArgs {
     int d, D, r;  // hidden, local inter, rank
     int pitch_d, pitch_r, pitch_v;  // pitch_v: survivor-position pitch of Z (>= round_up(D, 64))
     int act;
-    int tsplit, dsplit;             // split-K of the T and down GEMMs
+    int tsplit, dsplit, gsplit;     // split-K of the T, down and gate/up GEMMs
     // layer
     const uint16_t* Bm;  // predictor B, r x pitch_d
     const uint16_t* A;   // D x pitch_r
@@ -101,6 +101,7 @@ struct BatchArgs {
     float* Z;                // [D][64] gated values
     uint16_t *zh, *zl;       // [64][pitch_v]
     float* yp;               // [dsplit][64][pitch_d]
+    float* gp;               // [gsplit][pitch_v][64] gate / up split-K partials
 };
 int batch_max();
 int launch_batch(const BatchArgs& a, const float* xs, float* ys, void* stream);
