@@ -167,3 +167,17 @@ def test_layout_order_keeps_parity(shards):
     with pytest.raises(Exception):
         bad = dict(raw, order=np.zeros(D, dtype=np.int64))
         DeviceLayer(raw=bad)
+
+
+def test_device_layer_container_round_trip(tmp_path):
+    """save_device_layer / load_device_layer (tensor_io extension) reproduce the layer."""
+    from paper_2603_14110_b200 import tensor_io as T
+    cfg = CONFIGS["tiny"]
+    d, D = cfg["d"], cfg["D"]
+    h = build_host_layer(d, D, 0, seed=4, rank=64, sparsity=0.5, eval_tokens=2)
+    a = upload(h, d, D, 0, 64, balance=False)
+    T.save_device_layer(str(tmp_path), d, D, 0, h.gate, h.up, h.down_t, h.A, h.B, h.bias.astype(np.float32))
+    b = T.load_device_layer(str(tmp_path))
+    for t in range(2):
+        ra, rb = a.forward(h.xs[:, t]), b.forward(h.xs[:, t])
+        assert np.array_equal(ra.y, rb.y) and ra.stats == rb.stats
