@@ -325,6 +325,8 @@ def main():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-balance", action="store_true",
                     help="ascending neuron layout instead of the load-balanced order")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="per-layer mode: eager launches instead of one CUDA graph per step")
     ap.add_argument("--batch", type=int, default=0,
                     help="batched decode (configs[4]): B tokens per step through all layers")
     args = ap.parse_args()
@@ -337,10 +339,17 @@ def main():
 
     import torch
 
+    # SG_BENCH_BACKEND / SG_BENCH_DEVICE: functional checks of the N>1 code path on a
+    # one-GPU box (gloo, every rank on device 0); never used for timing claims
+    local = int(os.environ.get("SG_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("SG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2603_14110_b200 import _capi as capi
     from paper_2603_14110_b200.ffn_exec import Context, Pipeline, check
     from paper_2603_14110_b200.model import CONFIGS, build_host_model, upload
@@ -383,6 +392,33 @@ def main():
 
     step = step_stack if (args.mode == "stack" and world == 1) else step_layers
     launches_per_step = 1 if step is step_stack else L
+    graph_mode = "none"
+    if step is step_layers and not args.no_graph and os.environ.get("SG_BENCH_BACKEND", "nccl") == "nccl":
+        # per-layer launches (+ one NCCL all-reduce each) replayed as one CUDA graph
+        try:
+            capture_stream = torch.cuda.Stream()
+            with torch.cuda.stream(capture_stream):
+                step_layers()  # warm: attributes / NCCL communicator before capture
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=capture_stream):
+                for l in range(L):
+                    check(lib.sg_ffn_forward_device(
+                        ctx.handle, layers[l].handle, int(Pipeline.Sequential),
+                        C.c_void_p(xs[l].data_ptr()), C.c_void_p(ys[l].data_ptr()),
+                        C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+                    if world > 1:
+                        torch.distributed.all_reduce(ys[l])
+            eager = step_layers
+
+            def step_graph(pipe=Pipeline.Sequential):
+                if pipe != Pipeline.Sequential:
+                    return eager(pipe)
+                g.replay()
+            step = step_graph
+            graph_mode = "per-layer launches captured in one CUDA graph"
+        except Exception as e:  # report, keep eager
+            log(f"graph capture failed, eager per-layer launches: {e}")
 
     def timed(fn, K, W, sample_clocks=False):
         for _ in range(W):
@@ -498,7 +534,7 @@ def main():
                        "layout": "ascending" if args.no_balance else
                                  "per-CTA load-balanced neuron order from calibration statistics",
                        "mode": "stack (one persistent launch per step)" if step is step_stack
-                               else "per-layer launches"},
+                               else "per-layer launches", "graph": graph_mode},
             "per_layer_us": ms * 1000.0 / L,
             "p_mean": float(np.mean(ps)), "v_mean": float(np.mean(vs)),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
