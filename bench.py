@@ -325,6 +325,8 @@ def main():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-balance", action="store_true",
                     help="ascending neuron layout instead of the load-balanced order")
+    ap.add_argument("--hot-rows", type=int, default=16,
+                    help="gate rows per CTA fetched before the mask (sg_layer_set_hot_rows; 0 = off)")
     ap.add_argument("--no-graph", action="store_true",
                     help="per-layer mode: eager launches instead of one CUDA graph per step")
     ap.add_argument("--batch", type=int, default=0,
@@ -366,7 +368,8 @@ def main():
     d, D, L = cfg["d"], cfg["D"], len(host)
     log(f"host model built in {time.time() - t0:.1f}s")
     layers = [upload(h, d, D, cfg["act"], args.rank, device=local, shard_index=rank,
-                     shard_count=world, balance=not args.no_balance) for h in host]
+                     shard_count=world, balance=not args.no_balance,
+                     hot_rows=args.hot_rows) for h in host]
     Dl = layers[0].local_inter
     ctx = Context(local, d, Dl, args.rank)
     lib = capi.lib()
@@ -533,6 +536,7 @@ def main():
                        "predictor": "naive-mode randomized rank-r SVD + greedy calibration (eta 8)",
                        "layout": "ascending" if args.no_balance else
                                  "per-CTA load-balanced neuron order from calibration statistics",
+                       "hot_rows": 0 if args.no_balance else args.hot_rows,
                        "mode": "stack (one persistent launch per step)" if step is step_stack
                                else "per-layer launches", "graph": graph_mode},
             "per_layer_us": ms * 1000.0 / L,

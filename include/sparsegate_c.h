@@ -122,6 +122,14 @@ int64_t sg_layer_local_inter(const sg_layer* layer);
 int64_t sg_layer_global_index(const sg_layer* layer, int64_t local);
 /* Device bytes held by the layer's resident weights. */
 int64_t sg_layer_device_bytes(const sg_layer* layer);
+/* Gate-row prefetch ahead of the predictor (sequential pipeline): the first `rows`
+ * neurons of every CTA block of the layout have their gate rows fetched as soon as
+ * the layer starts, overlapping stages 1a/1b; those that the mask then rejects are
+ * dropped unread. Meant for a neuron_order that puts each block's most frequently
+ * predicted neurons first. 0 (default) disables; capped by the free ring slots.
+ * Results do not depend on it (it changes only when rows arrive and the order in
+ * which a CTA's survivors are summed). */
+sg_status sg_layer_set_hot_rows(sg_layer* layer, int64_t rows);
 
 /* Workspace for one stream. max_hidden/max_inter/max_rank bound the layers it
  * will run; device = CUDA ordinal. */

@@ -66,6 +66,7 @@ SYMBOLS = [
     ("sg_layer_local_inter", _I64, [_VP]),
     ("sg_layer_global_index", _I64, [_VP, _I64]),
     ("sg_layer_device_bytes", _I64, [_VP]),
+    ("sg_layer_set_hot_rows", C.c_int, [_VP, _I64]),
     ("sg_ctx_create", C.c_int, [_I32, _I64, _I64, _I64, C.POINTER(_VP)]),
     ("sg_ctx_destroy", C.c_int, [_VP]),
     ("sg_ffn_forward_device", C.c_int, [_VP, _VP, C.c_int, _VP, _VP, _VP]),

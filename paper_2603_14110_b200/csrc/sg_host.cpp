@@ -460,6 +460,12 @@ int64_t sg_layer_local_inter(const sg_layer* L) { return L ? L->D_local : 0; }
 int64_t sg_layer_global_index(const sg_layer* L, int64_t k) { return L ? local_to_global(L, k) : -1; }
 int64_t sg_layer_device_bytes(const sg_layer* L) { return L ? static_cast<int64_t>(L->bytes) : 0; }
 
+sg_status sg_layer_set_hot_rows(sg_layer* L, int64_t rows) {
+    if (L == nullptr || rows < 0) return fail(SG_ERR_USAGE, "sg_layer_set_hot_rows: bad arguments");
+    L->view.hot = static_cast<int>(rows < L->D_local ? rows : L->D_local);
+    return SG_OK;
+}
+
 sg_status sg_ctx_create(int32_t device, int64_t max_hidden, int64_t max_inter, int64_t max_rank,
                         sg_ctx** out) {
     if (out == nullptr || max_hidden < 1 || max_inter < 1 || max_rank < 0)

@@ -24,6 +24,9 @@ struct LayerView {
     const uint16_t* gate;  // D x pitch_d        (types.hpp:22)
     const uint16_t* ud;    // D x 2*pitch_d : row k = [up_k | down_k] (down neuron-major)
     const int* gidx;       // global index of local neuron k (null: gbase + k * gstride)
+    int hot;               // leading neurons of each CTA block whose gate rows are fetched
+                           // before the mask is known (sg_layer_set_hot_rows; 0 = off)
+    int pad_[3];
 };
 
 // Per-context device workspace (one per stream). Sizes are bounded by the

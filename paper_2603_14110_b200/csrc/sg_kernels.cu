@@ -56,7 +56,6 @@ constexpr int kRowsA = 4;                 // phase A rows reduced per pass
 constexpr int kGroupWarps = 4;            // phase C: a row is reduced by a group of 4 warps
 constexpr int kGroups = kWarps / kGroupWarps;
 constexpr int kGroupThreads = kGroupWarps * 32;
-constexpr int kStageOff = 4096;           // staged B rows / A slice start here in the big region
 constexpr int kXRegChunks = 4;            // x chunks per thread held in registers (pitch_d <= 4096)
 constexpr int kBatch = 8;                 // rows per transposed warp reduction (stage 4)
 constexpr int kSvChunk = 12;              // survivor [up | down] rows staged per round (stage 4/5a)
@@ -67,12 +66,13 @@ constexpr int kSector = 8;                // ints per 32-B sector
 // the survivor list + reduction scratch (stages 4/5) — never live at once.
 struct SmemPlan {
     int off_slotn;  // int[kMaxSlots]   neuron of each ring slot
+    int off_uses;   // int[kMaxSlots]   fills of each ring slot before the current layer
     int off_off;    // int[G+1]         predictor-kernel prefix scratch
     int off_mask;   // uint8[mask_cap]  phase B mask bytes
     int off_bias;   // float[mask_cap]  this CTA's bias slice / dense z slice
     int off_misc;   // int[32]          block-level scalars
     int off_lv;     // LayerView[2]     this and the next layer's view (stack launches)
-    int off_reda;   // float[256]       reduction scratch
+    int off_reda;   // float[512]       reduction scratch (phases A, C, stage 4, phase D)
     int off_items;  // int[item_cap]    this CTA's predicted neurons
     int off_recs;   // int2[item_cap]   per-item {neuron or -1, g or z}
     int off_xs;     // float[pitch_d]
@@ -84,6 +84,8 @@ struct SmemPlan {
     int slot_bytes;
     int stage_b;     // B rows of this CTA staged in smem (phase A)
     int as_bytes;    // A slice capacity in smem (0 = stream A from HBM)
+    int stage_off;   // staged B rows / A slice: [stage_off, big_bytes) of the big region
+    int pre_slots;   // ring slots below stage_off (free while phases A/B run)
     int mask_cap;
     int item_cap;
     int off_sv;      // int2[item_cap] survivor list {n, g} (sequential pipeline), float[kSvChunk] z
@@ -95,6 +97,7 @@ struct Smem {
     uint64_t* empty;
     uint64_t* abar;
     int* slotn;
+    int* uses;
     int* off;
     uint8_t* mask;
     float* bias;
@@ -115,6 +118,7 @@ __device__ __forceinline__ Smem carve(uint8_t* base, const SmemPlan& S) {
     m.empty = m.full + kMaxSlots;
     m.abar = m.empty + kMaxSlots;
     m.slotn = reinterpret_cast<int*>(base + S.off_slotn);
+    m.uses = reinterpret_cast<int*>(base + S.off_uses);
     m.off = reinterpret_cast<int*>(base + S.off_off);
     m.mask = base + S.off_mask;
     m.bias = reinterpret_cast<float*>(base + S.off_bias);
@@ -132,7 +136,6 @@ __device__ __forceinline__ Smem carve(uint8_t* base, const SmemPlan& S) {
 
 // Per-thread persistent state across phases/layers.
 struct RunState {
-    uint32_t seq;       // ring items issued so far (this launch)
     uint32_t auses;     // staging-barrier phases consumed so far
     uint64_t bar_base;  // grid-barrier counter base (lanes 0..7 of warp 0)
     uint32_t bar_k;     // grid barriers passed in this launch
@@ -407,14 +410,45 @@ __device__ __forceinline__ bool stage_weights(const LayerView& L, const Smem& sm
         if (lane == 0) mbar_expect_tx(sm.abar, bytesA + bytesB);
         __syncwarp();
         for (int q = lane; q < nB && bytesB; q += 31)
-            bulk_g2s(sm.big + kStageOff + static_cast<size_t>(q) * row_bytes,
+            bulk_g2s(sm.big + S.stage_off + static_cast<size_t>(q) * row_bytes,
                      L.B + static_cast<size_t>(c + q * G) * L.pitch_d, row_bytes, sm.abar, pol);
         if (bytesA && lane == 31)
-            bulk_g2s(sm.big + kStageOff + bytesB, L.A + static_cast<size_t>(n0) * L.pitch_r, bytesA,
+            bulk_g2s(sm.big + S.stage_off + bytesB, L.A + static_cast<size_t>(n0) * L.pitch_r, bytesA,
                      sm.abar, pol);
         __syncwarp();
     }
     return true;
+}
+
+// Hot prefix of the sequential pipeline: the gate rows of the first h neurons
+// of this CTA's block go into ring slots 0..h-1 (free while phases A/B use the
+// staging area at the top of the big region) before x or the mask is known.
+// phase_mask keeps them as items 0..h-1; phase C drops the ones it rejected.
+// Called when the ring is idle (layer start, or the previous layer's tail).
+__device__ __forceinline__ void preissue_hot(const LayerView& L, const Smem& sm,
+                                             const SmemPlan& S) {
+    const int G = gridDim.x, c = blockIdx.x;
+    const int n0 = split_lo(c, G, L.D), n1 = split_lo(c + 1, G, L.D);
+    int h = L.hot < S.pre_slots ? L.hot : S.pre_slots;
+    if (h > S.ns) h = S.ns;
+    if (h > n1 - n0) h = n1 - n0;
+    if (h < 0) h = 0;
+    if ((threadIdx.x >> 5) == kWarps) {
+        const int lane = threadIdx.x & 31;
+        if (lane == 0) sm.misc[4] = h;
+        if (lane < h) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const uint32_t row_bytes = static_cast<uint32_t>(L.pitch_d) * 2u;
+            const uint32_t use = static_cast<uint32_t>(sm.uses[lane]);
+            if (use > 0) mbar_wait(sm.empty + lane, (use - 1) & 1u);
+            sm.slotn[lane] = n0 + lane;
+            mbar_expect_tx(sm.full + lane, row_bytes);
+            bulk_g2s(sm.big + static_cast<size_t>(lane) * S.slot_bytes,
+                     L.gate + static_cast<size_t>(n0 + lane) * L.pitch_d, row_bytes, sm.full + lane,
+                     policy_evict_first());
+        }
+        __syncwarp();
+    }
 }
 
 // Stage x (fp32, length d) into smem, zero-padded to pitch_d; flag non-finite.
@@ -440,13 +474,13 @@ __device__ __forceinline__ bool stage_x(const float* x, int d, int pitch_d, floa
 // ---------------------------------------------------------------------------
 // Phase A: t = B·x (fp32), rows j = c + q*G ; block-reduced in fixed order.
 // ---------------------------------------------------------------------------
-__device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm, bool staged_b,
-                        uint32_t tag) {
+__device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm, const SmemPlan& S,
+                        bool staged_b, uint32_t tag) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int nch = L.pitch_d >> 3;
     const int nB = c < L.r ? (L.r - c + G - 1) / G : 0;
-    const uint16_t* bs = reinterpret_cast<const uint16_t*>(sm.big + kStageOff);
+    const uint16_t* bs = reinterpret_cast<const uint16_t*>(sm.big + S.stage_off);
     for (int q0 = 0; q0 < nB; q0 += kRowsA) {
         float acc[kRowsA];
 #pragma unroll
@@ -489,8 +523,8 @@ __device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm, b
 // Phase B: mask over this CTA's neuron range + warp-ballot compaction into
 // its predicted list (smem items[], global plist at n0, count).
 // ---------------------------------------------------------------------------
-__device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm, bool use_as,
-                           bool staged_b, uint8_t* mask_out, uint32_t tag) {
+__device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm, const SmemPlan& S,
+                           bool use_as, bool staged_b, uint8_t* mask_out, uint32_t tag) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int n0 = split_lo(c, G, L.D), n1 = split_lo(c + 1, G, L.D);
@@ -500,7 +534,7 @@ __device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm
     __syncthreads();
     const int nB = c < L.r ? (L.r - c + G - 1) / G : 0;
     const uint16_t* as = reinterpret_cast<const uint16_t*>(
-        sm.big + kStageOff + (staged_b ? static_cast<size_t>(nB) * L.pitch_d * 2 : 0));
+        sm.big + S.stage_off + (staged_b ? static_cast<size_t>(nB) * L.pitch_d * 2 : 0));
     // 4 lanes per neuron, 128 neurons per pass; lane sub covers chunks
     // sub + 4i, starting at i = (global index & 1) so the two neurons sharing a
     // quarter-warp read different banks. Order fixed per neuron.
@@ -534,21 +568,27 @@ __device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm
     }
     __syncthreads();
     if (warp == 0) {
-        int run = 0;
+        // P list (ascending) and the phase C item list: the hot prefix fetched
+        // ahead of the mask (items 0..hpre-1 = the block's first neurons, kept
+        // whether predicted or not), then the other predicted neurons
+        const int hpre = sm.misc[4];
+        int run = 0, irun = hpre;
         for (int base = 0; base < n1 - n0; base += 32) {
             const int k = base + lane;
             const bool on = k < n1 - n0 && sm.mask[k];
             const unsigned b = __ballot_sync(0xffffffffu, on);
-            if (on) {
-                const int dst = run + __popc(b & ((1u << lane) - 1u));
-                W.plist[n0 + dst] = n0 + k;
-                sm.items[dst] = n0 + k;
-            }
+            const unsigned bi = __ballot_sync(0xffffffffu, on && k >= hpre);
+            const unsigned below = (1u << lane) - 1u;
+            if (on) W.plist[n0 + run + __popc(b & below)] = n0 + k;
+            if (k < hpre) sm.items[k] = n0 + k;
+            if (on && k >= hpre) sm.items[irun + __popc(bi & below)] = n0 + k;
             run += __popc(b);
+            irun += __popc(bi);
         }
         if (lane == 0) {
             st_sector(W.cnt + c * kSector, run);
             sm.misc[0] = run;
+            sm.misc[3] = irun;
             if (run && !mask_out) atomicAdd(W.stats + 0, run);  // p (integer: order-free)
         }
     }
@@ -647,9 +687,9 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
     const int nch = L.pitch_d >> 3;
     const uint32_t row_bytes = static_cast<uint32_t>(L.pitch_d) * 2u;
     const int n0 = split_lo(c, G, L.D);
-    const int nitems = kPipe == 0 ? split_lo(c + 1, G, L.D) - n0 : sm.misc[0];
-    const uint32_t seq0 = rs.seq;
+    const int nitems = kPipe == 0 ? split_lo(c + 1, G, L.D) - n0 : sm.misc[3];
     const int ns = S.ns;
+    // item j lives in slot j % ns as that slot's fill uses[slot] + j / ns
 
     if (warp == kWarps) {
         // ---- producer warp: lane s issues every item of ring slot s (s < ns),
@@ -657,12 +697,15 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
         // cp.async.bulk copies caps an SM near 22 GB/s (tools/microbench_gather.cu).
         const uint64_t pol = policy_evict_first();
         const int slot = lane;
-        if (slot < ns && nitems > 0) {
-            uint32_t q = seq0 + static_cast<uint32_t>((slot + ns - static_cast<int>(seq0 % ns)) % ns);
-            for (; q < seq0 + static_cast<uint32_t>(nitems); q += ns) {
-                const int j = static_cast<int>(q - seq0);
+        // WAR vs. the generic reads of the staging area under the last slots
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (slot < ns) {
+            const uint32_t u0 = static_cast<uint32_t>(sm.uses[slot]);
+            const int hpre = kPipe == 2 ? sm.misc[4] : 0;  // items already issued (hot prefix)
+            for (int j = slot; j < nitems; j += ns) {
+                if (j < hpre) continue;
                 const int n = kPipe == 0 ? n0 + j : sm.items[j];
-                const uint32_t use = q / ns;
+                const uint32_t use = u0 + static_cast<uint32_t>(j / ns);
                 if (use > 0) mbar_wait(sm.empty + slot, (use - 1) & 1u);
                 sm.slotn[slot] = n;
                 uint8_t* dst = sm.big + static_cast<size_t>(slot) * S.slot_bytes;
@@ -682,27 +725,26 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
         __syncwarp();
     } else {
         // ---- compute groups: group g < kc (4 warps) consumes the items
-        // q = seq0 + j with q % kc == g, in order, two per iteration. ns is a
-        // multiple of kc, so every slot is consumed by one group, phase after
-        // phase, and a parity wait can never run a phase ahead of the barrier.
+        // j with j % kc == g, in order, two per iteration. ns is a multiple of
+        // kc, so every slot is consumed by one group, phase after phase, and a
+        // parity wait can never run a phase ahead of the barrier.
         const int kc = S.kc;
         const int grp = warp / kGroupWarps, gt = tid % kGroupThreads;
         XRegs X;
         load_xregs(sm.xs, nch, gt, X);
         float* red = sm.reda + grp * (2 * kGroupWarps * 4);
         int par = 0;
-        int j0 = grp - static_cast<int>(seq0 % static_cast<uint32_t>(kc));
-        if (j0 < 0) j0 += kc;
-        for (int j = j0; grp < kc && j < nitems; j += 2 * kc) {
+        for (int j = grp; grp < kc && j < nitems; j += 2 * kc) {
             const bool two = j + kc < nitems;
             int slot[2], n[2];
             const uint16_t* r[4];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int jj = two ? j + h * kc : j;
-                const uint32_t q = seq0 + jj;
-                slot[h] = static_cast<int>(q % ns);
-                if (h == 0 || two) mbar_wait(sm.full + slot[h], (q / ns) & 1u);
+                slot[h] = jj % ns;
+                if (h == 0 || two)
+                    mbar_wait(sm.full + slot[h],
+                              (static_cast<uint32_t>(sm.uses[slot[h]]) + jj / ns) & 1u);
                 n[h] = sm.slotn[slot[h]];
                 const uint16_t* srow = reinterpret_cast<const uint16_t*>(
                     sm.big + static_cast<size_t>(slot[h]) * S.slot_bytes);
@@ -735,7 +777,10 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
                     if (gt == 0) W.zD[nn] = gated(g, u, L.act);
                     continue;
                 }
-                const bool sv = g > 0.f;  // revalidation, ffn_exec.hpp:200 (strict)
+                // a hot-prefix item the mask rejected is dropped (never in P)
+                const int jj = j + h * kc;
+                const bool inP = kPipe != 2 || jj >= sm.misc[4] || sm.mask[jj];
+                const bool sv = inP && g > 0.f;  // revalidation, ffn_exec.hpp:200 (strict)
                 // a survivor's [up | down] rows (16 KB, contiguous) go to L2 now,
                 // one 128-B line per thread of the group, for stages 4 and 5a
                 if (sv && !(W.flags & 2)) {
@@ -745,17 +790,19 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(a + off));
                 }
                 if (gt == 0) {
-                    W.gN[nn] = g;  // gate pre-activation per neuron (P output, phase D)
+                    if (inP) W.gN[nn] = g;  // gate pre-activation per neuron (P output)
                     int2 rec;
                     rec.x = sv ? nn : -1;
                     rec.y = __float_as_int(kPipe == 2 ? g : (sv ? gated(g, u, L.act) : 0.f));
-                    sm.recs[j + h * kc] = rec;
+                    sm.recs[jj] = rec;
                 }
             }
         }
     }
-    rs.seq = seq0 + static_cast<uint32_t>(nitems > 0 ? nitems : 0);
     __syncthreads();
+    if (tid < ns && nitems > tid) sm.uses[tid] += (nitems - tid + ns - 1) / ns;
+    if (tid == 0) sm.misc[4] = 0;
+    if (kPipe == 0) __syncthreads();
     if (kPipe != 0) {
         // survivors of this CTA's items, in P order -> smem list + global segment
         int2* list = kPipe == 2 ? sm.svl : reinterpret_cast<int2*>(sm.big);
@@ -1036,7 +1083,7 @@ __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm
                          W.V, W.zV);
     const int c0 = split_lo(c, G, L.d), c1 = split_lo(c + 1, G, L.d);
     const int ncols = c1 - c0;
-    float* part = reinterpret_cast<float*>(sm.big);
+    float* part = sm.reda;  // the big region may hold the next layer's hot prefix
     if (ncols > 0) {
         int ngrp = kCThreads / ncols;
         if (ngrp > 32) ngrp = 32;
@@ -1077,7 +1124,10 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
     if (!first_layer) grid_arrive(W, rs);  // previous layer's y is published
     // weights of this layer (independent of x) are staged during the barrier,
     // unless the previous layer already staged them during its tail
-    if (kPipe != 0 && !prestaged) staged = stage_weights(L, sm, S, use_as);
+    if (kPipe != 0 && !prestaged) {
+        staged = stage_weights(L, sm, S, use_as);
+        if (kPipe == 2) preissue_hot(L, sm, S);
+    }
     if (!first_layer) grid_wait(W, rs);
     SG_STAMP(dbg, 1);
     const bool bad = stage_x(x, L.d, L.pitch_d, sm.xs);
@@ -1095,10 +1145,10 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
         }
         // t travels with its tag: no grid barrier between stages 1a and 1b
         const uint32_t tag = rs.tag0 + rs.bar_k + 1u;
-        phase_t(L, W, sm, S.stage_b != 0, tag);
+        phase_t(L, W, sm, S, S.stage_b != 0, tag);
         SG_STAMP(dbg, 3);
         SG_STAMP(dbg, 4);
-        phase_mask(L, W, sm, use_as, S.stage_b != 0, nullptr, tag);
+        phase_mask(L, W, sm, S, use_as, S.stage_b != 0, nullptr, tag);
         SG_STAMP(dbg, 6);
     }
     phase_gather<kPipe>(L, W, sm, S, rs);
@@ -1109,11 +1159,14 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
         partial_down<kPipe>(L, W, sm);
     }
     SG_STAMP(dbg, 7);
-    // stage the next layer's predictor weights during the barrier: this CTA's
-    // ring and survivor list are done, and phase D only uses the first 2 KB
+    // stage the next layer's predictor weights and hot prefix during the
+    // barrier: this CTA's ring and survivor rows are done, phase D uses reda
     grid_arrive(W, rs);
     bool next_staged = false;
-    if (kPipe != 0 && next != nullptr) next_staged = stage_weights(*next, sm, S, use_as);
+    if (kPipe != 0 && next != nullptr) {
+        next_staged = stage_weights(*next, sm, S, use_as);
+        if (kPipe == 2) preissue_hot(*next, sm, S);
+    }
     grid_wait(W, rs);
     SG_STAMP(dbg, 8);
     phase_down<kPipe>(L, W, sm, y, want_sets);
@@ -1136,8 +1189,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const Smem sm = carve(smem_raw, S);
     init_barriers(sm.full);
-    RunState rs{0u, 0u, 0ull, 0u, 0u};
+    RunState rs{0u, 0ull, 0u, 0u};
     grid_barrier_init(W, rs);
+    if (threadIdx.x < kMaxSlots) sm.uses[threadIdx.x] = 0;
+    if (threadIdx.x == 0) sm.misc[4] = 0;
     // barriers completed by all earlier launches on this workspace: a tag base
     // that no value left in the exchange buffers can carry yet
     if (threadIdx.x == 0) sm.misc[9] = static_cast<int>(rs.bar_base / static_cast<uint64_t>(bar_share(0)));
@@ -1186,16 +1241,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const Smem sm = carve(smem_raw, S);
     init_barriers(sm.full);
-    RunState rs{0u, 0u, 0ull, 0u, 0u};
+    RunState rs{0u, 0ull, 0u, 0u};
     grid_barrier_init(W, rs);
+    if (threadIdx.x == 0) sm.misc[4] = 0;
     if (threadIdx.x == 0) sm.misc[9] = static_cast<int>(rs.bar_base / static_cast<uint64_t>(bar_share(0)));
     stage_weights(L, sm, S, false);  // bias only (S.stage_b == 0)
     const bool bad = stage_x(W.x, L.d, L.pitch_d, sm.xs);  // (block barrier inside)
     rs.tag0 = static_cast<uint32_t>(sm.misc[9]);
     if (blockIdx.x == 0 && threadIdx.x == 0) W.stats[2] = bad ? 1 : 0;
     const uint32_t tag = rs.tag0 + 1u;
-    phase_t(L, W, sm, false, tag);
-    phase_mask(L, W, sm, false, false, mask_out, tag);
+    phase_t(L, W, sm, S, false, tag);
+    phase_mask(L, W, sm, S, false, false, mask_out, tag);
     grid_barrier(W, rs);
     if (threadIdx.x < 32 && blockIdx.x == 0) {
         warp_prefix(W.cnt, sm.off, gridDim.x, threadIdx.x);
@@ -1212,6 +1268,8 @@ bool make_plan(int G, int pitch_d, int r, int pitch_r, int Dl, int pipe, int max
     off = align_up(off, 128);
     S->off_slotn = off;
     off += kMaxSlots * 4;
+    S->off_uses = off;
+    off += kMaxSlots * 4;
     S->off_off = off = align_up(off, 16);
     off += (G + 1) * 4;
     S->mask_cap = align_up((Dl + G - 1) / G + 1, 16);
@@ -1224,7 +1282,7 @@ bool make_plan(int G, int pitch_d, int r, int pitch_r, int Dl, int pipe, int max
     S->off_lv = off = align_up(off, 16);
     off += 2 * static_cast<int>(sizeof(LayerView));
     S->off_reda = off = align_up(off, 16);
-    off += 256 * 4;  // phase A: kRowsA*kWarps; phase C: kGroups*2*kGroupWarps*4; stage 4
+    off += 512 * 4;  // phase A: kRowsA*kWarps; C: kGroups*2*kGroupWarps*4; 4: 2*kWarps*kBatch; D: kCThreads
     S->item_cap = (Dl + G - 1) / G + 2;
     S->off_items = off = align_up(off, 16);
     off += S->item_cap * 4;
@@ -1238,18 +1296,20 @@ bool make_plan(int G, int pitch_d, int r, int pitch_r, int Dl, int pipe, int max
     off += pitch_r * 4;
     S->off_big = off = align_up(off, 1024);
     const int avail = max_smem - off;
-    // stage 4/5a survivor list (<= item_cap int2) and phase D scratch
-    if (avail < S->item_cap * 8 || avail < kCThreads * 4) return false;
+    if (avail < S->item_cap * 8) return false;
     // phases A/B staging
     const int nB = (r + G - 1) / G;
     const int b_bytes = nB * pitch_d * 2;
     int as_bytes = 0;
     if (pipe != 0) as_bytes = align_up(((Dl + G - 1) / G + 1) * pitch_r * 2, 16);
-    S->stage_b = (pipe != 0 && kStageOff + b_bytes + as_bytes <= avail) ? 1 : 0;
-    if (!S->stage_b && pipe != 0 && kStageOff + as_bytes > avail) as_bytes = 0;
+    S->stage_b = (pipe != 0 && b_bytes + as_bytes <= avail) ? 1 : 0;
+    if (!S->stage_b && pipe != 0 && as_bytes > avail) as_bytes = 0;
     S->as_bytes = as_bytes;
+    // the staging area sits at the top of the big region, under the ring's last slots
+    S->stage_off = (avail - (S->stage_b ? b_bytes : 0) - as_bytes) / 128 * 128;
     // phase C ring
     S->slot_bytes = (pipe == 2 ? 1 : 2) * pitch_d * 2;
+    S->pre_slots = S->stage_off / S->slot_bytes;
     int ns_max = avail / S->slot_bytes;
     if (ns_max > kMaxSlots) ns_max = kMaxSlots;
     if (ns_max < 1) return false;

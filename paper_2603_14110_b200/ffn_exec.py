@@ -305,6 +305,11 @@ class DeviceLayer:
     def device_bytes(self) -> int:
         return int(capi.lib().sg_layer_device_bytes(self.handle))
 
+    def set_hot_rows(self, rows: int) -> None:
+        """sg_layer_set_hot_rows: gate rows of the first `rows` neurons of every CTA block
+        are fetched before the mask is known (0 = off). Timing only."""
+        check(capi.lib().sg_layer_set_hot_rows(self.handle, int(rows)))
+
     def context(self) -> Context:
         return default_context(self.device, self.hidden, self.local_inter, max(self.rank, 1))
 

@@ -106,7 +106,9 @@ def balanced_order(load: np.ndarray, neurons: np.ndarray, G: int) -> np.ndarray:
     """Layout order of `neurons` for G CTAs: CTA c gets the c-th contiguous block of
     the layout (sizes c*n/G boundaries, as the kernel splits), and blocks get equal
     expected load: neurons by decreasing load are dealt to the CTAs in serpentine
-    order (skipping full ones). Deterministic; within a block ascending index."""
+    order (skipping full ones). Deterministic; within a block by decreasing load
+    (ties ascending), so each block's most frequently predicted neurons lead it
+    (the hot prefix of sg_layer_set_hot_rows)."""
     n = len(neurons)
     bounds = [c * n // G for c in range(G + 1)]
     cap = np.diff(bounds)
@@ -124,11 +126,15 @@ def balanced_order(load: np.ndarray, neurons: np.ndarray, G: int) -> np.ndarray:
         if c == G or c < 0:
             step = -step
             c += step
-    return np.concatenate([np.sort(np.asarray(b, dtype=np.int64)) for b in bins])
+    out = []
+    for b in bins:
+        b = np.sort(np.asarray(b, dtype=np.int64))
+        out.append(b[np.argsort(-load[b], kind="stable")])
+    return np.concatenate(out)
 
 
 def upload(host: HostLayer, d, D, act, rank=256, device=0, shard_index=0, shard_count=1,
-           balance=True):
+           balance=True, hot_rows=16):
     raw = dict(hidden=d, inter=D, rank=rank, activation=act, gate=host.gate, up=host.up,
                down_t=host.down_t, A=host.A, B=host.B, bias=host.bias)
     if balance and host.load is not None:
@@ -139,4 +145,7 @@ def upload(host: HostLayer, d, D, act, rank=256, device=0, shard_index=0, shard_
         first = balanced_order(host.load, mine, G)
         rest = np.setdiff1d(np.arange(D, dtype=np.int64), mine)
         raw["order"] = np.concatenate([first, rest])
-    return DeviceLayer(raw=raw, device=device, shard_index=shard_index, shard_count=shard_count)
+    layer = DeviceLayer(raw=raw, device=device, shard_index=shard_index, shard_count=shard_count)
+    if balance and host.load is not None and hot_rows:
+        layer.set_hot_rows(hot_rows)
+    return layer

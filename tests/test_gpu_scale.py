@@ -104,14 +104,18 @@ def _stack(layers, xs, chain, pipeline=Pipeline.Sequential):
     return yt.double().cpu().numpy(), [(s.predicted_active, s.revalidated) for s in st]
 
 
-@pytest.mark.parametrize("pipeline", [Pipeline.Sequential, Pipeline.Parallel, Pipeline.Dense])
-def test_stack_launch_equals_layer_launches(pipeline):
+@pytest.mark.parametrize("pipeline,hot", [(Pipeline.Sequential, 0), (Pipeline.Sequential, 5),
+                                          (Pipeline.Parallel, 0), (Pipeline.Dense, 0)])
+def test_stack_launch_equals_layer_launches(pipeline, hot):
+    """hot > 0: the next layer's hot prefix is fetched during the previous layer's
+    tail in a stack, at layer start otherwise; the results must not differ."""
     import torch
     d, D, r = 512, 1408, 64
     layers, xs = [], []
     for s in range(3):
         fx, pred = _calibrated_layer(d, D, r, seed=100 + s)
         layers.append(DeviceLayer(fx.weights, pred))
+        layers[-1].set_hot_rows(hot)
         xs.append(fx.eval[:, 0])
     xs = np.stack(xs).astype(np.float32).astype(np.float64)
     ys, stats = _stack(layers, xs, chain=0, pipeline=pipeline)
@@ -167,6 +171,33 @@ def test_layout_order_keeps_parity(shards):
     with pytest.raises(Exception):
         bad = dict(raw, order=np.zeros(D, dtype=np.int64))
         DeviceLayer(raw=bad)
+
+
+@pytest.mark.parametrize("hot", [1, 7, 64])
+def test_hot_prefix_keeps_parity(hot):
+    """sg_layer_set_hot_rows on a layout whose block prefixes are NOT the hot
+    neurons (ascending order): many prefetched rows are rejected by the mask and
+    must be dropped. The item order stays ascending (the prefix is the block's
+    first neurons), so the result is bit-identical to the hot-off run."""
+    d, D, r = 512, 1500, 64
+    fx, pred = _calibrated_layer(d, D, r, seed=41, calib=1024)
+    q = quantize_layer(fx.weights.gate, fx.weights.up, fx.weights.down, pred.A, pred.B, pred.bias)
+    base = DeviceLayer(fx.weights, pred)
+    hl = DeviceLayer(fx.weights, pred)
+    hl.set_hot_rows(hot)
+    for t in range(6):
+        x = fx.eval[:, t]
+        ctx = base.context()
+        r0 = base.forward(x, Pipeline.Sequential, ctx)
+        P0, V0, g0, z0 = read_sets(ctx, D)
+        r1 = hl.forward(x, Pipeline.Sequential, ctx)
+        P1, V1, g1, z1 = read_sets(ctx, D)
+        assert np.array_equal(P0, P1) and np.array_equal(V0, V1)
+        assert np.array_equal(g0, g1) and np.array_equal(z0, z1)
+        assert r0.stats == r1.stats
+        diag = check_token(q, x, r1.y, P1, V1)
+        assert diag["rel"] <= Y_RTOL
+        assert np.array_equal(r0.y, r1.y)
 
 
 def test_device_layer_container_round_trip(tmp_path):
