@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--pipeline", default="seq")
     ap.add_argument("--steps", type=int, default=0, help="plain repeated stack calls (ncu target)")
     ap.add_argument("--json", default=None)
+    ap.add_argument("--hot-rows", type=int, default=16)
     args = ap.parse_args()
     import torch
     from paper_2603_14110_b200 import _capi as capi
@@ -40,7 +41,7 @@ def main():
 
     cfg, host = build_host_model(args.config, args.layers, workers=8)
     d, D, L = cfg["d"], cfg["D"], len(host)
-    layers = [upload(h, d, D, cfg["act"]) for h in host]
+    layers = [upload(h, d, D, cfg["act"], hot_rows=args.hot_rows) for h in host]
     ctx = Context(0, d, D, 256)
     lib = capi.lib()
     arr = (C.c_void_p * L)(*[l.handle.value for l in layers])
