@@ -299,6 +299,9 @@ class Layer {
     Index local_inter() const { return sg_layer_local_inter(layer_); }
     Index rank() const { return rank_; }
     int device() const { return device_; }
+    // Gate rows of the first `rows` neurons of every CTA block fetched before the
+    // mask (sg_layer_set_hot_rows): timing only, results unchanged.
+    void set_hot_rows(Index rows) { detail::check(sg_layer_set_hot_rows(layer_, rows)); }
 
     // Host x (f64) -> host y (f64) and the reference's ExecStats.
     FfnResult forward(Context& ctx, Pipeline p, const Vec& x, void* stream = nullptr) const {
