@@ -502,6 +502,7 @@ sg_status sg_ctx_create(int32_t device, int64_t max_hidden, int64_t max_inter, i
     const size_t o_zD = take(Dm * 4);
     const size_t o_ypart = take(static_cast<size_t>(G) * C->pitch_dmax * 4);
     const size_t o_bar = take(8 * 256);
+    const size_t o_ytag = take(static_cast<size_t>(C->pitch_dmax) * 8);
     const size_t o_stats = take(4 * 4 * kMaxStackLayers);
     const size_t o_x = take(C->pitch_dmax * 4), o_y = take(C->pitch_dmax * 4);
     const size_t o_mask = take(Dm);
@@ -530,6 +531,7 @@ sg_status sg_ctx_create(int32_t device, int64_t max_hidden, int64_t max_inter, i
     W.zD = reinterpret_cast<float*>(b + o_zD);
     W.ypart = reinterpret_cast<float*>(b + o_ypart);
     W.bar = reinterpret_cast<unsigned long long*>(b + o_bar);
+    W.ytag = reinterpret_cast<uint32_t*>(b + o_ytag);
     W.stats = reinterpret_cast<int*>(b + o_stats);
     if (const char* f = std::getenv("SG_FLAGS")) W.flags = std::atoi(f);
     C->xdev = reinterpret_cast<float*>(b + o_x);

@@ -46,6 +46,7 @@ struct WorkView {
     float* zV;            // [Dmax] gated value per survivor
     float* zD;            // [Dmax] dense pipeline: z per neuron
     float* ypart;         // [G * pitch_dmax] dense pipeline: per-CTA partial outputs
+    uint32_t* ytag;       // [2 * pitch_dmax] {y bits, tag} published by phase D inside a stack
     unsigned long long* bar;  // 8 grid-barrier counters, 256 B apart (see grid_barrier)
     int* stats;           // [4 per layer] p, v, nonfinite(x), pipeline
     uint64_t* dbg;        // optional [layers][G][16] globaltimer phase stamps (or null)

@@ -471,6 +471,49 @@ __device__ __forceinline__ bool stage_x(const float* x, int d, int pitch_d, floa
     return __syncthreads_or(bad) != 0;
 }
 
+// Inside a stack, layer l+1 starts without a grid barrier: phase D of layer l
+// publishes y as tagged values and the next stage x polls them (chained: all
+// of y is the next x; unchained: one value per CTA slice, which orders the
+// layers — a CTA only reuses ypart once every CTA has finished reading it).
+__device__ __forceinline__ bool stage_x_poll(const float* x, const WorkView& W, int d, int pitch_d,
+                                             float* xs, uint32_t tag) {
+    bool bad = false;
+    const int tid = threadIdx.x;
+    if (x == nullptr) {
+        constexpr int kIn = 8;
+        for (int i0 = tid; i0 < pitch_d; i0 += kIn * kThreads) {
+            uint32_t v[kIn], t[kIn];
+#pragma unroll
+            for (int k = 0; k < kIn; ++k) {
+                const int i = i0 + k * kThreads;
+                v[k] = 0u;
+                t[k] = tag;
+                if (i < d)
+                    asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];"
+                                 : "=r"(v[k]), "=r"(t[k])
+                                 : "l"(W.ytag + 2 * i)
+                                 : "memory");
+            }
+#pragma unroll
+            for (int k = 0; k < kIn; ++k) {
+                const int i = i0 + k * kThreads;
+                if (i >= pitch_d) continue;
+                float f = __uint_as_float(v[k]);
+                if (t[k] != tag) f = ld_tagged(W.ytag + 2 * i, tag);
+                xs[i] = f;
+                bad |= !isfinite(f);
+            }
+        }
+        return __syncthreads_or(bad) != 0;
+    }
+    const int G = gridDim.x;
+    if (tid < G) {
+        const int col = split_lo(tid, G, d);
+        if (col < split_lo(tid + 1, G, d)) (void)ld_tagged(W.ytag + 2 * col, tag);
+    }
+    return stage_x(x, d, pitch_d, xs);
+}
+
 // ---------------------------------------------------------------------------
 // Phase A: t = B·x (fp32), rows j = c + q*G ; block-reduced in fixed order.
 // ---------------------------------------------------------------------------
@@ -1076,7 +1119,7 @@ __device__ __noinline__ void write_index_sets(int gbase, int gstride, const int*
 // ---------------------------------------------------------------------------
 template <int kPipe>
 __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm, float* y,
-                           bool want_sets) {
+                           bool want_sets, bool publish, uint32_t ytag) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     if (kPipe != 0 && want_sets && (tid >> 5) == kWarps)
         write_index_sets(L.gbase, L.gstride, L.gidx, L.D, W.cnt, W.plist, W.gN, W.vseg, W.P, W.gP,
@@ -1100,6 +1143,7 @@ __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm
             float s = 0.f;
             for (int grp = 0; grp < ngrp; ++grp) s += part[grp * ncols + tid];
             y[c0 + tid] = s;
+            if (publish) st_tagged(W.ytag + 2 * (c0 + tid), s, ytag);
         }
     }
     __syncthreads();
@@ -1109,8 +1153,8 @@ __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm
 template <int kPipe>
 __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
                           const SmemPlan& S, RunState& rs, const float* x, float* y,
-                          bool first_layer, int lidx, bool want_sets, const LayerView* next,
-                          bool prestaged) {
+                          bool first_layer, bool chained, int lidx, bool want_sets,
+                          const LayerView* next, bool prestaged) {
     const int c = blockIdx.x, tid = threadIdx.x;
 #ifdef SG_PHASE_TIMING
     uint64_t* dbg =
@@ -1121,16 +1165,18 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
     SG_STAMP(dbg, 0);
     const bool use_as = kPipe != 0 && S.as_bytes > 0;
     bool staged = prestaged;
-    if (!first_layer) grid_arrive(W, rs);  // previous layer's y is published
-    // weights of this layer (independent of x) are staged during the barrier,
-    // unless the previous layer already staged them during its tail
+    // weights of this layer (independent of x), unless the previous layer
+    // already staged them during its tail
     if (kPipe != 0 && !prestaged) {
         staged = stage_weights(L, sm, S, use_as);
         if (kPipe == 2) preissue_hot(L, sm, S);
     }
-    if (!first_layer) grid_wait(W, rs);
     SG_STAMP(dbg, 1);
-    const bool bad = stage_x(x, L.d, L.pitch_d, sm.xs);
+    // no grid barrier between the layers of a stack: the previous layer's y
+    // arrives tagged (its tag: the partial barrier it followed)
+    const bool bad = first_layer ? stage_x(x, L.d, L.pitch_d, sm.xs)
+                                 : stage_x_poll(chained ? nullptr : x, W, L.d, L.pitch_d, sm.xs,
+                                                rs.tag0 + rs.bar_k);
     if (c == 0 && tid == 0) {
         // p and v (stats[0], [1]) are zeroed by the host before the launch
         W.stats[2] = bad ? 1 : 0;
@@ -1169,7 +1215,7 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
     }
     grid_wait(W, rs);
     SG_STAMP(dbg, 8);
-    phase_down<kPipe>(L, W, sm, y, want_sets);
+    phase_down<kPipe>(L, W, sm, y, want_sets, next != nullptr, rs.tag0 + rs.bar_k);
     SG_STAMP(dbg, 9);
     return next_staged;
 }
@@ -1226,8 +1272,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* y = ys + static_cast<size_t>(l) * xstride;
         WorkView Wl = W;
         Wl.stats = W.stats + 4 * l;  // per-layer {p, v, nonfinite, pipeline}
-        prestaged = run_layer<kPipe>(L, Wl, sm, S, rs, x, y, l == 0, l, l == nlayers - 1, next,
-                                     prestaged);
+        prestaged = run_layer<kPipe>(L, Wl, sm, S, rs, x, y, l == 0, chain != 0, l, l == nlayers - 1,
+                                     next, prestaged);
         if (layers && l + 1 < nlayers) {
             if (threadIdx.x < kLvWords / 4) asm volatile("cp.async.wait_all;" ::: "memory");
             __syncthreads();

@@ -135,6 +135,40 @@ def test_stack_launch_equals_layer_launches(pipeline, hot):
     torch.cuda.synchronize()
 
 
+def test_repeated_stacks_on_one_context():
+    """Layers inside a stack exchange t and y as tagged values instead of grid
+    barriers; the tags derive from the context's barrier counters. Stacks of
+    different depths, single-layer calls and predictor-only calls interleaved on
+    ONE context must keep giving the same bits (a stale tag would let a reader
+    take a previous launch's value)."""
+    import torch
+    d, D, r = 512, 1408, 64
+    layers, xs = [], []
+    for s in range(4):
+        fx, pred = _calibrated_layer(d, D, r, seed=200 + s)
+        layers.append(DeviceLayer(fx.weights, pred))
+        xs.append(fx.eval[:, 0])
+    xt = torch.tensor(np.asarray(xs, dtype=np.float32), device="cuda")
+    ctx = Context(0, d, D, r)
+    sh = torch.cuda.current_stream().cuda_stream
+
+    def stack(n, chain):
+        arr = (C.c_void_p * n)(*[l.handle.value for l in layers[:n]])
+        yt = torch.zeros_like(xt)
+        check(capi.lib().sg_ffn_forward_layers(ctx.handle, arr, n, int(Pipeline.Sequential),
+                                               C.c_void_p(xt.data_ptr()), C.c_void_p(yt.data_ptr()),
+                                               int(chain), C.c_void_p(sh)))
+        return yt[:n].double().cpu().numpy()
+
+    ref = {(n, c): stack(n, c) for n in (2, 4) for c in (0, 1)}
+    for it in range(6):
+        for n, c in ((4, 1), (2, 0), (4, 0), (2, 1)):
+            assert np.array_equal(stack(n, c), ref[(n, c)]), (it, n, c)
+        layers[it % 4].forward(xs[it % 4], Pipeline.Sequential, ctx)
+        layers[it % 4].predict_mask(xs[it % 4], ctx)
+    torch.cuda.synchronize()
+
+
 @pytest.mark.parametrize("shards", [1, 2])
 def test_layout_order_keeps_parity(shards):
     """A neuron layout order (sg_layer_desc.neuron_order) moves work between CTAs
