@@ -562,6 +562,15 @@ __device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm, c
     }
 }
 
+// All of t (tagged: no grid barrier between stages 1a and 1b) and the bias slice.
+__device__ __forceinline__ void poll_t(const LayerView& L, const WorkView& W, const Smem& sm,
+                                       uint32_t tag) {
+    for (int i = threadIdx.x; i < L.pitch_r; i += kThreads)
+        sm.ts[i] = i < L.r ? ld_tagged(W.t + i * kSector, tag) : 0.f;
+    asm volatile("cp.async.wait_all;" ::: "memory");  // the bias slice
+    __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 // Phase B: mask over this CTA's neuron range + warp-ballot compaction into
 // its predicted list (smem items[], global plist at n0, count).
@@ -571,10 +580,6 @@ __device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int n0 = split_lo(c, G, L.D), n1 = split_lo(c + 1, G, L.D);
-    for (int i = tid; i < L.pitch_r; i += kThreads)
-        sm.ts[i] = i < L.r ? ld_tagged(W.t + i * kSector, tag) : 0.f;
-    asm volatile("cp.async.wait_all;" ::: "memory");  // the bias slice
-    __syncthreads();
     const int nB = c < L.r ? (L.r - c + G - 1) / G : 0;
     const uint16_t* as = reinterpret_cast<const uint16_t*>(
         sm.big + S.stage_off + (staged_b ? static_cast<size_t>(nB) * L.pitch_d * 2 : 0));
@@ -1193,6 +1198,7 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
         const uint32_t tag = rs.tag0 + rs.bar_k + 1u;
         phase_t(L, W, sm, S, S.stage_b != 0, tag);
         SG_STAMP(dbg, 3);
+        poll_t(L, W, sm, tag);
         SG_STAMP(dbg, 4);
         phase_mask(L, W, sm, S, use_as, S.stage_b != 0, nullptr, tag);
         SG_STAMP(dbg, 6);
@@ -1297,6 +1303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (blockIdx.x == 0 && threadIdx.x == 0) W.stats[2] = bad ? 1 : 0;
     const uint32_t tag = rs.tag0 + 1u;
     phase_t(L, W, sm, S, false, tag);
+    poll_t(L, W, sm, tag);
     phase_mask(L, W, sm, S, false, false, mask_out, tag);
     grid_barrier(W, rs);
     if (threadIdx.x < 32 && blockIdx.x == 0) {
