@@ -50,10 +50,9 @@ struct WorkView {
     unsigned long long* bar;  // 8 grid-barrier counters, 256 B apart (see grid_barrier)
     int* stats;           // [4 per layer] p, v, nonfinite(x), pipeline
     uint64_t* dbg;        // optional [layers][G][16] globaltimer phase stamps (or null)
-    int flags;            // experiment switches (SG_FLAGS env, default 0): 1 gate-row L2
-                          // prefetch in phase B, 2 no survivor-row L2 prefetch,
-                          // 16/32 phase-B ablations, 64 LSU prefetch, bits 8-15:
-                          // consumer-group override
+    int flags;            // experiment switches (SG_FLAGS env, default 0): 2 no survivor-row
+                          // L2 prefetch; bits 8-15 consumer-group override, bits 16-23
+                          // ring-slot override (timing studies only; results unchanged)
 };
 
 struct LaunchInfo {

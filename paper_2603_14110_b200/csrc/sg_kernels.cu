@@ -6,10 +6,12 @@
 // contiguous range of neurons [n0, n1) and the predictor rows j = c + k*G.
 //
 //   start    cp.async.bulk: this CTA's rows of B and its slice of A -> smem;
-//            cp.async: its bias slice (weights only: staged during the
-//            previous layer's tail, overlapping its barrier)
+//            cp.async: its bias slice; the gate rows of its block's hot prefix
+//            (the first sg_layer_set_hot_rows neurons of the layout) -> ring
+//            slots (all x-independent: issued during the previous layer's tail)
+//            x: inside a stack, the previous layer's y is polled as tagged values
 //   phase A  stage 1a  t = B·x  (rows j = c + k*G)    (ffn_exec.hpp:133-136)
-//            --- grid barrier ---
+//            --- t exchanged as tagged values (no grid barrier) ---
 //   phase B  stage 1b  pre = A·t + bias > 0 -> mask  (ffn_exec.hpp:139-144)
 //            stage 2   warp-ballot compaction -> this CTA's predicted list
 //                                                     (ffn_exec.hpp:189-195)
@@ -23,6 +25,7 @@
 //            --- grid barrier ---
 //   phase D  stage 5b  y: CTA c sums the G partials of its column slice in a
 //                      fixed order                   (ffn_exec.hpp:80-94)
+//                      and, inside a stack, publishes it tagged for the next layer
 //
 // No grid barrier between stages 2 and 3: a CTA streams its OWN predicted
 // rows, so the P prefix (needed only for the P/V outputs) is computed in
@@ -729,7 +732,7 @@ __device__ __forceinline__ void group_dot(const uint16_t* const* rows, const XRe
 // ---------------------------------------------------------------------------
 template <int kPipe>
 __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& sm,
-                             const SmemPlan& S, RunState& rs) {
+                             const SmemPlan& S) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int nch = L.pitch_d >> 3;
@@ -1203,7 +1206,7 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
         phase_mask(L, W, sm, S, use_as, S.stage_b != 0, nullptr, tag);
         SG_STAMP(dbg, 6);
     }
-    phase_gather<kPipe>(L, W, sm, S, rs);
+    phase_gather<kPipe>(L, W, sm, S);
     SG_STAMP(dbg, 14);
     if (kPipe == 2) {
         survivor_updown(L, W, sm, S, rs);
