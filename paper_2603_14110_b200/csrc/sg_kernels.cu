@@ -331,7 +331,8 @@ __device__ __forceinline__ void grid_arrive(const WorkView& W, RunState& rs) {
     __syncthreads();
     rs.bar_k += 1;
     if (threadIdx.x == 0) {
-        __threadfence();
+        // release is cumulative: the block's writes, ordered before this
+        // thread by the barrier above, are published with it
         asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(
                          W.bar + (blockIdx.x % kBarCounters) * kBarStride)
                      : "memory");
