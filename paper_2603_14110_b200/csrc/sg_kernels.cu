@@ -1142,8 +1142,18 @@ __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm
         if (tid < ngrp * ncols) {
             const int col = c0 + tid % ncols, grp = tid / ncols;
             const int g0 = split_lo(grp, ngrp, G), g1 = split_lo(grp + 1, ngrp, G);
+            // all loads in flight before the (ordered) sum: one L2 round trip
+            constexpr int kPer = 12;
+            const float* src = W.ypart + static_cast<size_t>(g0) * L.pitch_d + col;
+            float v[kPer];
+#pragma unroll
+            for (int i = 0; i < kPer; ++i)
+                v[i] = g0 + i < g1 ? __ldcg(src + static_cast<size_t>(i) * L.pitch_d) : 0.f;
             float s = 0.f;
-            for (int g = g0; g < g1; ++g)
+#pragma unroll
+            for (int i = 0; i < kPer; ++i)
+                if (g0 + i < g1) s += v[i];
+            for (int g = g0 + kPer; g < g1; ++g)
                 s += __ldcg(W.ypart + static_cast<size_t>(g) * L.pitch_d + col);
             part[tid] = s;
         }
