@@ -141,17 +141,19 @@ def run_reference(args, world, rank):
             el = time.perf_counter() - t0
         return el
 
-    t_est = one_step()  # warm-up and cost estimate
-    budget = 120.0
+    t_est = one_step()  # first warm-up step doubles as the cost estimate
+    budget = 120.0      # timed CPU work per run (each step is a bounded sample)
     k = max(1, min(args.steps, int(budget / max(t_est, 1e-6))))
-    for _ in range(max(0, min(args.warmup, 1) - 1)):
+    w = max(1, min(args.warmup, 1 + int(20.0 / max(t_est, 1e-6))))
+    for _ in range(w - 1):
         one_step()
     tot = sum(one_step() for _ in range(k))
     per_token_layer = tot / (k * ntok)        # seconds of one token through one layer (amortised)
     tok_s = 1.0 / (per_token_layer * L)       # decode tokens/s through the L-layer stack
     line = {
         "impl": "reference", "metric": "sparse-FFN decode tokens/s", "value": tok_s,
-        "unit": "tokens/s", "n_gpus": 0, "steps": k, "warmup": min(args.warmup, 1),
+        "unit": "tokens/s", "n_gpus": 0, "steps": k, "warmup": w,
+        "steps_requested": args.steps, "warmup_requested": args.warmup,
         "ms_per_step": 1000.0 / tok_s, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg['model']}: {L} layers d={d} d_ff={D} r={args.rank} "
