@@ -210,10 +210,14 @@ __device__ __forceinline__ uint64_t globaltimer() {
     do {                                                         \
         if ((dbg) && threadIdx.x == 0) (dbg)[k] = globaltimer(); \
     } while (0)
+#define SG_DBG_PARAM , uint64_t* dbg
+#define SG_DBG_ARG , dbg
 #else
 #define SG_STAMP(dbg, k) \
     do {                 \
     } while (0)
+#define SG_DBG_PARAM
+#define SG_DBG_ARG
 #endif
 
 // 8 bf16 weights (one 16-B chunk) against 8 fp32 activations, in element order.
@@ -566,6 +570,52 @@ __device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm, c
     }
 }
 
+// 32-B chunk of x as two LDS.128 (scalar loads at a 32-B thread stride would
+// be 8-way bank conflicts).
+__device__ __forceinline__ void load_x8(const float* xs, int ch, bool ok, float* v) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    if (ok) {
+        a = *reinterpret_cast<const float4*>(xs + ch * 8);
+        b = *reinterpret_cast<const float4*>(xs + ch * 8 + 4);
+    }
+    v[0] = a.x;
+    v[1] = a.y;
+    v[2] = a.z;
+    v[3] = a.w;
+    v[4] = b.x;
+    v[5] = b.y;
+    v[6] = b.z;
+    v[7] = b.w;
+}
+// Sum of v[0..7] over the 32 lanes, transposed: 9 shuffles instead of 40.
+// Afterwards lane l holds the total of item 4*(l>>4 & 1) + 2*(l>>3 & 1) + (l>>2 & 1).
+__device__ __forceinline__ float warp_sum8(float* v, int lane) {
+    const bool hi16 = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float send = hi16 ? v[i] : v[i + 4];
+        const float keep = hi16 ? v[i + 4] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    const bool hi8 = lane & 8;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const float send = hi8 ? v[i] : v[i + 2];
+        const float keep = hi8 ? v[i + 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    const bool hi4 = lane & 4;
+    {
+        const float send = hi4 ? v[0] : v[1];
+        const float keep = hi4 ? v[1] : v[0];
+        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    float s = v[0];
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    return s;
+}
+
 // All of t (tagged: no grid barrier between stages 1a and 1b) and the bias slice.
 __device__ __forceinline__ void poll_t(const LayerView& L, const WorkView& W, const Smem& sm,
                                        uint32_t tag) {
@@ -580,42 +630,73 @@ __device__ __forceinline__ void poll_t(const LayerView& L, const WorkView& W, co
 // its predicted list (smem items[], global plist at n0, count).
 // ---------------------------------------------------------------------------
 __device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm, const SmemPlan& S,
-                           bool use_as, bool staged_b, uint8_t* mask_out, uint32_t tag) {
+                           bool use_as, bool staged_b, uint8_t* mask_out, uint32_t tag SG_DBG_PARAM) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int n0 = split_lo(c, G, L.D), n1 = split_lo(c + 1, G, L.D);
     const int nB = c < L.r ? (L.r - c + G - 1) / G : 0;
     const uint16_t* as = reinterpret_cast<const uint16_t*>(
         sm.big + S.stage_off + (staged_b ? static_cast<size_t>(nB) * L.pitch_d * 2 : 0));
-    // 4 lanes per neuron, 128 neurons per pass; lane sub covers chunks
-    // sub + 4i, starting at i = (global index & 1) so the two neurons sharing a
-    // quarter-warp read different banks. Order fixed per neuron.
     const int nchr = L.pitch_r >> 3;
-    const int nq = nchr >> 2;  // chunks per lane (pitch_r >= 64 -> nq >= 2)
-    for (int base = 0; base < n1 - n0; base += kCThreads / 4) {
-        const int k = base + (tid >> 2), sub = tid & 3;
-        float acc = 0.f;
-        if (tid < kCThreads && k < n1 - n0) {
-            const int n = n0 + k;
-            const uint16_t* arow = use_as ? as + static_cast<size_t>(k) * L.pitch_r
-                                          : L.A + static_cast<size_t>(n) * L.pitch_r;
-            const int rot = (L.gbase + n * L.gstride) & 1;
-            for (int i = 0; i < nq; ++i) {
-                int ii = i + rot;
-                if (ii >= nq) ii -= nq;
-                const int ch = sub + 4 * ii;
-                const uint4 w = use_as ? *reinterpret_cast<const uint4*>(arow + ch * 8)
-                                       : ldg_stream(arow + ch * 8);
-                acc = dot8(w, sm.ts + ch * 8, acc);
+    if (use_as && nchr <= 32) {
+        // A slice in smem, r <= 256: warp w takes 8 neurons per pass; lane l
+        // holds t chunk l in registers and dots chunk l of the 8 rows (each row
+        // read contiguously), then one transposed warp reduction. Order fixed
+        // per neuron: the 8 products of chunk l, then the butterfly.
+        float tr[8];
+        load_x8(sm.ts, lane, lane < nchr, tr);
+        const uint32_t abase = smem_u32(as) + static_cast<uint32_t>(lane * 16);
+        for (int base = warp * 8; warp < kWarps && base < n1 - n0; base += kWarps * 8) {
+            float part[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                uint4 w = make_uint4(0u, 0u, 0u, 0u);
+                if (base + j < n1 - n0 && lane < nchr)
+                    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                                 : "r"(abase + static_cast<uint32_t>((base + j) * L.pitch_r * 2)));
+                part[j] = dot8r(w, tr, 0.f);
             }
-        }
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        if (tid < kCThreads && sub == 0 && k < n1 - n0) {
-            const float pre = acc + sm.bias[k];
-            const uint8_t on = pre > 0.f ? 1 : 0;  // strict, ffn_exec.hpp:141
-            sm.mask[k] = on;
-            if (mask_out) mask_out[n0 + k] = on;
+                const float sum = warp_sum8(part, lane);
+                const int k = base + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+            if ((lane & 3) == 0 && k < n1 - n0) {
+                const float pre = sum + sm.bias[k];
+                const uint8_t on = pre > 0.f ? 1 : 0;  // strict, ffn_exec.hpp:141
+                sm.mask[k] = on;
+                if (mask_out) mask_out[n0 + k] = on;
+            }
+            }
+    } else {
+        // 4 lanes per neuron, 128 neurons per pass; lane sub covers chunks
+        // sub + 4i, starting at i = (global index & 1) so the two neurons sharing a
+        // quarter-warp read different banks. Order fixed per neuron.
+        const int nchr = L.pitch_r >> 3;
+        const int nq = nchr >> 2;  // chunks per lane (pitch_r >= 64 -> nq >= 2)
+        for (int base = 0; base < n1 - n0; base += kCThreads / 4) {
+            const int k = base + (tid >> 2), sub = tid & 3;
+            float acc = 0.f;
+            if (tid < kCThreads && k < n1 - n0) {
+                const int n = n0 + k;
+                const uint16_t* arow = use_as ? as + static_cast<size_t>(k) * L.pitch_r
+                                              : L.A + static_cast<size_t>(n) * L.pitch_r;
+                const int rot = (L.gbase + n * L.gstride) & 1;
+                for (int i = 0; i < nq; ++i) {
+                    int ii = i + rot;
+                    if (ii >= nq) ii -= nq;
+                    const int ch = sub + 4 * ii;
+                    const uint4 w = use_as ? *reinterpret_cast<const uint4*>(arow + ch * 8)
+                                           : ldg_stream(arow + ch * 8);
+                    acc = dot8(w, sm.ts + ch * 8, acc);
+                }
+            }
+            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+            if (tid < kCThreads && sub == 0 && k < n1 - n0) {
+                const float pre = acc + sm.bias[k];
+                const uint8_t on = pre > 0.f ? 1 : 0;  // strict, ffn_exec.hpp:141
+                sm.mask[k] = on;
+                if (mask_out) mask_out[n0 + k] = on;
+            }
         }
     }
     __syncthreads();
@@ -655,23 +736,6 @@ __device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm
 struct XRegs {
     float v[kXRegChunks][8];
 };
-// 32-B chunk of x as two LDS.128 (scalar loads at a 32-B thread stride would
-// be 8-way bank conflicts).
-__device__ __forceinline__ void load_x8(const float* xs, int ch, bool ok, float* v) {
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-    if (ok) {
-        a = *reinterpret_cast<const float4*>(xs + ch * 8);
-        b = *reinterpret_cast<const float4*>(xs + ch * 8 + 4);
-    }
-    v[0] = a.x;
-    v[1] = a.y;
-    v[2] = a.z;
-    v[3] = a.w;
-    v[4] = b.x;
-    v[5] = b.y;
-    v[6] = b.z;
-    v[7] = b.w;
-}
 __device__ __forceinline__ void load_xregs(const float* xs, int nch, int gt, XRegs& X) {
 #pragma unroll
     for (int k = 0; k < kXRegChunks; ++k) {
@@ -892,35 +956,6 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
 // z = gated(g, u) (ffn_exec.hpp:202-203, :68-76), and every thread adds z·down
 // for its chunk into its partial y, survivors in P order.
 // ---------------------------------------------------------------------------
-// Sum of v[0..7] over the 32 lanes, transposed: 9 shuffles instead of 40.
-// Afterwards lane l holds the total of item 4*(l>>4 & 1) + 2*(l>>3 & 1) + (l>>2 & 1).
-__device__ __forceinline__ float warp_sum8(float* v, int lane) {
-    const bool hi16 = lane & 16;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float send = hi16 ? v[i] : v[i + 4];
-        const float keep = hi16 ? v[i + 4] : v[i];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-    const bool hi8 = lane & 8;
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const float send = hi8 ? v[i] : v[i + 2];
-        const float keep = hi8 ? v[i + 2] : v[i];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    const bool hi4 = lane & 4;
-    {
-        const float send = hi4 ? v[0] : v[1];
-        const float keep = hi4 ? v[1] : v[0];
-        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    float s = v[0];
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    return s;
-}
-
 __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkView& W,
                                                 const Smem& sm, const SmemPlan& S, RunState& rs) {
     const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1214,7 +1249,7 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
         SG_STAMP(dbg, 3);
         poll_t(L, W, sm, tag);
         SG_STAMP(dbg, 4);
-        phase_mask(L, W, sm, S, use_as, S.stage_b != 0, nullptr, tag);
+        phase_mask(L, W, sm, S, use_as, S.stage_b != 0, nullptr, tag SG_DBG_ARG);
         SG_STAMP(dbg, 6);
     }
     phase_gather<kPipe>(L, W, sm, S);
@@ -1318,7 +1353,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tag = rs.tag0 + 1u;
     phase_t(L, W, sm, S, false, tag);
     poll_t(L, W, sm, tag);
-    phase_mask(L, W, sm, S, false, false, mask_out, tag);
+#ifdef SG_PHASE_TIMING
+    uint64_t* dbg = nullptr;
+#endif
+    phase_mask(L, W, sm, S, false, false, mask_out, tag SG_DBG_ARG);
     grid_barrier(W, rs);
     if (threadIdx.x < 32 && blockIdx.x == 0) {
         warp_prefix(W.cnt, sm.off, gridDim.x, threadIdx.x);
