@@ -638,6 +638,10 @@ __device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm
     const uint16_t* as = reinterpret_cast<const uint16_t*>(
         sm.big + S.stage_off + (staged_b ? static_cast<size_t>(nB) * L.pitch_d * 2 : 0));
     const int nchr = L.pitch_r >> 3;
+    // the setup above (divisions, parameter-bank reads) is pinned here, before
+    // the wait for t, so its latency hides under the exchange
+    asm volatile("" ::"r"(n0), "r"(n1), "l"(as), "r"(nchr));
+    poll_t(L, W, sm, tag);
     if (use_as && nchr <= 32) {
         // A slice in smem, r <= 256: warp w takes 8 neurons per pass; lane l
         // holds t chunk l in registers and dots chunk l of the 8 rows (each row
@@ -1161,25 +1165,46 @@ __device__ __noinline__ void write_index_sets(int gbase, int gstride, const int*
 // Phase D (after a grid barrier): CTA c sums the G partials of its column
 // range in fixed order (contiguous groups of partials, then the groups).
 // ---------------------------------------------------------------------------
+// Phase D's index arithmetic, computed before the partial barrier's wait so
+// its latency (divisions, parameter reads) hides under the barrier.
+struct DownPlan {
+    int c0, ncols, ngrp, g0, g1;
+    const float* src;  // this thread's first partial (column c0 + tid % ncols)
+};
+__device__ __forceinline__ DownPlan down_plan(const LayerView& L, const WorkView& W) {
+    const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
+    DownPlan p;
+    p.c0 = split_lo(c, G, L.d);
+    p.ncols = split_lo(c + 1, G, L.d) - p.c0;
+    p.ngrp = p.ncols > 0 ? kCThreads / p.ncols : 0;
+    if (p.ngrp > 32) p.ngrp = 32;
+    p.g0 = p.g1 = 0;
+    p.src = W.ypart;
+    if (p.ncols > 0 && tid < p.ngrp * p.ncols) {
+        const int grp = tid / p.ncols;
+        p.g0 = split_lo(grp, p.ngrp, G);
+        p.g1 = split_lo(grp + 1, p.ngrp, G);
+        p.src = W.ypart + static_cast<size_t>(p.g0) * L.pitch_d + p.c0 + tid % p.ncols;
+    }
+    asm volatile("" ::"r"(p.c0), "r"(p.ncols), "r"(p.ngrp), "r"(p.g0), "r"(p.g1), "l"(p.src));
+    return p;
+}
+
 template <int kPipe>
 __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm, float* y,
-                           bool want_sets, bool publish, uint32_t ytag) {
-    const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
+                           bool want_sets, bool publish, uint32_t ytag, const DownPlan& dp) {
+    const int tid = threadIdx.x;
     if (kPipe != 0 && want_sets && (tid >> 5) == kWarps)
         write_index_sets(L.gbase, L.gstride, L.gidx, L.D, W.cnt, W.plist, W.gN, W.vseg, W.P, W.gP,
                          W.V, W.zV);
-    const int c0 = split_lo(c, G, L.d), c1 = split_lo(c + 1, G, L.d);
-    const int ncols = c1 - c0;
+    const int c0 = dp.c0, ncols = dp.ncols, ngrp = dp.ngrp;
     float* part = sm.reda;  // the big region may hold the next layer's hot prefix
     if (ncols > 0) {
-        int ngrp = kCThreads / ncols;
-        if (ngrp > 32) ngrp = 32;
         if (tid < ngrp * ncols) {
-            const int col = c0 + tid % ncols, grp = tid / ncols;
-            const int g0 = split_lo(grp, ngrp, G), g1 = split_lo(grp + 1, ngrp, G);
+            const int g0 = dp.g0, g1 = dp.g1;
             // all loads in flight before the (ordered) sum: one L2 round trip
             constexpr int kPer = 12;
-            const float* src = W.ypart + static_cast<size_t>(g0) * L.pitch_d + col;
+            const float* src = dp.src;
             float v[kPer];
 #pragma unroll
             for (int i = 0; i < kPer; ++i)
@@ -1189,7 +1214,7 @@ __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm
             for (int i = 0; i < kPer; ++i)
                 if (g0 + i < g1) s += v[i];
             for (int g = g0 + kPer; g < g1; ++g)
-                s += __ldcg(W.ypart + static_cast<size_t>(g) * L.pitch_d + col);
+                s += __ldcg(src + static_cast<size_t>(g - g0) * L.pitch_d);
             part[tid] = s;
         }
         __syncthreads();
@@ -1247,7 +1272,6 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
         const uint32_t tag = rs.tag0 + rs.bar_k + 1u;
         phase_t(L, W, sm, S, S.stage_b != 0, tag);
         SG_STAMP(dbg, 3);
-        poll_t(L, W, sm, tag);
         SG_STAMP(dbg, 4);
         phase_mask(L, W, sm, S, use_as, S.stage_b != 0, nullptr, tag SG_DBG_ARG);
         SG_STAMP(dbg, 6);
@@ -1268,9 +1292,10 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
         next_staged = stage_weights(*next, sm, S, use_as);
         if (kPipe == 2) preissue_hot(*next, sm, S);
     }
+    const DownPlan dp = down_plan(L, W);
     grid_wait(W, rs);
     SG_STAMP(dbg, 8);
-    phase_down<kPipe>(L, W, sm, y, want_sets, next != nullptr, rs.tag0 + rs.bar_k);
+    phase_down<kPipe>(L, W, sm, y, want_sets, next != nullptr, rs.tag0 + rs.bar_k, dp);
     SG_STAMP(dbg, 9);
     return next_staged;
 }
@@ -1352,7 +1377,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (blockIdx.x == 0 && threadIdx.x == 0) W.stats[2] = bad ? 1 : 0;
     const uint32_t tag = rs.tag0 + 1u;
     phase_t(L, W, sm, S, false, tag);
-    poll_t(L, W, sm, tag);
 #ifdef SG_PHASE_TIMING
     uint64_t* dbg = nullptr;
 #endif

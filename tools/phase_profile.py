@@ -20,7 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 os.environ.setdefault("SG_LIB", "timing")
 sys.path.insert(0, ROOT)
 
-NAMES = {0: "start", 1: "bar_prev", 2: "stage_x", 3: "phase_A(t=Bx)", 4: "t_poll",
+NAMES = {0: "start", 1: "bar_prev", 2: "stage_x", 3: "phase_A(t=Bx)", 4: "-",
          6: "phase_B(mask+compact)", 14: "phase_C(gate stream)", 7: "stage4+5a(up/down)",
          8: "bar3", 9: "phase_D(reduce)"}
 
