@@ -92,6 +92,7 @@ struct SmemPlan {
     int mask_cap;
     int item_cap;
     int off_sv;      // int2[item_cap] survivor list {n, g} (sequential pipeline), float[kSvChunk] z
+    int sv_chunk;    // survivor [up | down] rows staged per round: min(kSvChunk, big / row)
     int total;
 };
 
@@ -525,12 +526,15 @@ __device__ __forceinline__ bool stage_x_poll(const float* x, const WorkView& W, 
 // ---------------------------------------------------------------------------
 // Phase A: t = B·x (fp32), rows j = c + q*G ; block-reduced in fixed order.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ int rows_b(const LayerView& L) {  // predictor rows c + k*G
+    const int G = gridDim.x, c = blockIdx.x;
+    return c < L.r ? (L.r - c + G - 1) / G : 0;
+}
 __device__ void phase_t(const LayerView& L, const WorkView& W, const Smem& sm, const SmemPlan& S,
-                        bool staged_b, uint32_t tag) {
+                        bool staged_b, uint32_t tag, int nB) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int nch = L.pitch_d >> 3;
-    const int nB = c < L.r ? (L.r - c + G - 1) / G : 0;
     const uint16_t* bs = reinterpret_cast<const uint16_t*>(sm.big + S.stage_off);
     for (int q0 = 0; q0 < nB; q0 += kRowsA) {
         float acc[kRowsA];
@@ -979,8 +983,7 @@ __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkVi
         a0[e] = 0.f;
         a1[e] = 0.f;
     }
-    int chunk = S.big_bytes / static_cast<int>(ud_bytes);  // rows that fit in the big region
-    if (chunk > kSvChunk) chunk = kSvChunk;
+    const int chunk = S.sv_chunk;  // rows that fit in the big region, <= kSvChunk
     for (int base = 0; base < nsv; base += chunk) {
         const int m = nsv - base < chunk ? nsv - base : chunk;
         if (warp == kWarps) {
@@ -1251,6 +1254,11 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
         if (kPipe == 2) preissue_hot(L, sm, S);
     }
     SG_STAMP(dbg, 1);
+    // phase A's row count and the ring / survivor parameters, read before the
+    // x wait so their latency hides under it
+    const int nB = rows_b(L);
+    asm volatile("" ::"r"(nB), "r"(S.stage_off), "r"(S.ns), "r"(S.kc), "r"(S.slot_bytes),
+                 "r"(S.sv_chunk), "r"(S.item_cap));
     // no grid barrier between the layers of a stack: the previous layer's y
     // arrives tagged (its tag: the partial barrier it followed)
     const bool bad = first_layer ? stage_x(x, L.d, L.pitch_d, sm.xs)
@@ -1270,7 +1278,7 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
         }
         // t travels with its tag: no grid barrier between stages 1a and 1b
         const uint32_t tag = rs.tag0 + rs.bar_k + 1u;
-        phase_t(L, W, sm, S, S.stage_b != 0, tag);
+        phase_t(L, W, sm, S, S.stage_b != 0, tag, nB);
         SG_STAMP(dbg, 3);
         SG_STAMP(dbg, 4);
         phase_mask(L, W, sm, S, use_as, S.stage_b != 0, nullptr, tag SG_DBG_ARG);
@@ -1376,7 +1384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     rs.tag0 = static_cast<uint32_t>(sm.misc[9]);
     if (blockIdx.x == 0 && threadIdx.x == 0) W.stats[2] = bad ? 1 : 0;
     const uint32_t tag = rs.tag0 + 1u;
-    phase_t(L, W, sm, S, false, tag);
+    phase_t(L, W, sm, S, false, tag, rows_b(L));
 #ifdef SG_PHASE_TIMING
     uint64_t* dbg = nullptr;
 #endif
@@ -1449,6 +1457,8 @@ bool make_plan(int G, int pitch_d, int r, int pitch_r, int Dl, int pipe, int max
     S->kc = kc;
     S->ns = kc * (ns_max / kc);
     S->big_bytes = avail;
+    S->sv_chunk = avail / (pitch_d * 4) < kSvChunk ? avail / (pitch_d * 4) : kSvChunk;
+    if (pipe == 2 && S->sv_chunk < 1) return false;
     S->total = max_smem;
     return true;
 }
