@@ -516,6 +516,30 @@ __device__ __forceinline__ bool stage_x_poll(const float* x, const WorkView& W, 
         return __syncthreads_or(bad) != 0;
     }
     const int G = gridDim.x;
+    constexpr int kXV = 4;  // float4 per thread held across the poll
+    if ((d & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && pitch_d <= kXV * 4 * kThreads) {
+        // this layer's x does not depend on the previous layer: its loads are
+        // in flight while the previous layer's completion is polled
+        float4 v[kXV];
+#pragma unroll
+        for (int k = 0; k < kXV; ++k) {
+            const int i = (tid + k * kThreads) * 4;
+            v[k] = i < d ? __ldcg(reinterpret_cast<const float4*>(x + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (tid < G) {
+            const int col = split_lo(tid, G, d);
+            if (col < split_lo(tid + 1, G, d)) (void)ld_tagged(W.ytag + 2 * col, tag);
+        }
+#pragma unroll
+        for (int k = 0; k < kXV; ++k) {
+            const int i = (tid + k * kThreads) * 4;
+            if (i < pitch_d) {
+                *reinterpret_cast<float4*>(xs + i) = v[k];
+                bad |= !isfinite(v[k].x) || !isfinite(v[k].y) || !isfinite(v[k].z) || !isfinite(v[k].w);
+            }
+        }
+        return __syncthreads_or(bad) != 0;
+    }
     if (tid < G) {
         const int col = split_lo(tid, G, d);
         if (col < split_lo(tid + 1, G, d)) (void)ld_tagged(W.ytag + 2 * col, tag);
