@@ -91,3 +91,61 @@ def layer_metrics(w: FfnWeights, pred: Predictor, x_cols, layer: int = 0) -> Met
     labels = gate_pre > 0.0
     row.roc_auc = roc_auc(pred_pre, labels) if labels.any() and not labels.all() else 1.0
     return row
+
+
+# ---- the cmd_run JSONL parity stream ----
+def fnv1a64(data: bytes) -> int:
+    """sparsegate_main.cpp:73-81: FNV-1a 64 over raw bytes, with the reference's offset
+    basis literal 1469598103934665603 (not the published 14695981039346656037) so that
+    hashes match the reference's streams."""
+    h = 1469598103934665603
+    for b in bytes(data):
+        h ^= b
+        h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def hex64(v: int) -> str:  # sparsegate_main.cpp:83-87 ("%016" PRIx64)
+    return f"{v & 0xFFFFFFFFFFFFFFFF:016x}"
+
+
+def run_record(t: int, result) -> dict:
+    """One cmd_run record (sparsegate_main.cpp:251-258) for token t: the executor's stats
+    and the FNV-1a hash of y as f64 bytes."""
+    y = np.ascontiguousarray(np.asarray(result.y, dtype="<f8"))
+    return {"token_index": int(t),
+            "predicted_sparsity": float(result.stats.predicted_sparsity),
+            "realized_sparsity": float(result.stats.realized_sparsity),
+            "multiplies": int(result.stats.multiplies),
+            "output_hash": hex64(fnv1a64(y.tobytes()))}
+
+
+def format_stream(records) -> str:
+    """JSONL as cmd_run writes it: one compact object per line, keys in nlohmann's
+    (std::map) order, shortest round-trip doubles."""
+    import json
+    return "".join(json.dumps(r, sort_keys=True, separators=(",", ":")) + "\n" for r in records)
+
+
+def run_stream(w: FfnWeights, pred, x_cols, mode: str = "sequential") -> str:
+    """cmd_run (sparsegate_main.cpp:224-267) with the executor on the GPU: mode dense,
+    parallel or sequential over the tokens (columns) of x_cols. The stats fields equal
+    the reference's whenever the index sets do; output_hash hashes the GPU's y (fp32
+    widened to f64), so it is stable run to run but not equal to the f64 CPU hash."""
+    from .ffn_exec import sparse_ffn_parallel
+    X = np.asarray(x_cols, dtype=np.float64)
+    if X.ndim != 2:
+        raise DataError("activation batch: expected d x tokens")
+    recs = []
+    for t in range(X.shape[1]):
+        x = X[:, t]
+        if mode == "dense":
+            r = dense_ffn(w, x)
+        elif mode == "parallel":
+            r = sparse_ffn_parallel(w, pred, x)
+        elif mode == "sequential":
+            r = sparse_ffn_sequential(w, pred, x)
+        else:
+            raise DataError(f"unknown mode {mode}")
+        recs.append(run_record(t, r))
+    return format_stream(recs)

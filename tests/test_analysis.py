@@ -5,7 +5,8 @@ import numpy as np
 import pytest
 
 from paper_2603_14110_b200 import DataError, FfnWeights, Predictor
-from paper_2603_14110_b200.analysis import layer_metrics, roc_auc
+from paper_2603_14110_b200.analysis import (fnv1a64, format_stream, hex64, layer_metrics,
+                                            roc_auc, run_record, run_stream)
 
 
 def brute_force_auc(scores, labels):
@@ -64,3 +65,56 @@ def test_layer_metrics_controlled_predictors():  # :270-322
            for t in range(16) if (g[:, t] > 0).any()]
     assert abs(row.recall - np.mean(rec)) <= 1e-12
     assert abs(row.roc_auc - brute_force_auc(pre.T.reshape(-1), (g > 0).T.reshape(-1))) <= 1e-12
+
+
+def test_fnv1a64_and_hex64():
+    """sparsegate_main.cpp:73-87. The reference's offset basis literal is
+    1469598103934665603 (the published FNV-1a basis is 14695981039346656037): the
+    stream must hash like the reference, so the restatement keeps its constant."""
+    basis, prime = 1469598103934665603, 1099511628211
+    assert fnv1a64(b"") == basis
+    assert fnv1a64(b"a") == ((basis ^ 0x61) * prime) % 2 ** 64 == 0x44BD8AD473CD9906
+    h = basis
+    for b in b"foobar":
+        h = ((h ^ b) * prime) % 2 ** 64
+    assert fnv1a64(b"foobar") == h
+    assert hex64(1) == "0000000000000001" and hex64(fnv1a64(b"a")) == "44bd8ad473cd9906"
+
+
+def test_run_stream_format():
+    """cmd_run records (sparsegate_main.cpp:251-258): compact, keys in std::map order."""
+    class St:
+        predicted_sparsity, realized_sparsity, multiplies = 0.5, 0.75, 12
+
+    class R:
+        y, stats = np.array([1.0, 0.0]), St()
+
+    rec = run_record(3, R())
+    h = hex64(fnv1a64(np.array([1.0, 0.0], dtype="<f8").tobytes()))
+    assert format_stream([rec]) == ('{"multiplies":12,"output_hash":"%s","predicted_sparsity":0.5,'
+                                    '"realized_sparsity":0.75,"token_index":3}\n' % h)
+
+
+@pytest.mark.gpu
+def test_run_stream_gpu():
+    """The stream from GPU runs: byte-identical reruns, the reference's stats fields
+    (multiplies exact unless a near-threshold neuron flips), dense multiplies 3dD."""
+    import json
+    import oracle as O
+    from parity_util import q_f32, quantize_layer
+    from test_gpu_parity import _calibrated_layer
+    d, D, r = 256, 1024, 32
+    fx, pred = _calibrated_layer(d, D, r, seed=5)
+    X = fx.eval[:, :6]
+    s1 = run_stream(fx.weights, pred, X)
+    assert s1 == run_stream(fx.weights, pred, X)
+    q = quantize_layer(fx.weights.gate, fx.weights.up, fx.weights.down, pred.A, pred.B, pred.bias)
+    for t, line in enumerate(s1.splitlines()):
+        rec = json.loads(line)
+        assert rec["token_index"] == t and list(rec) == sorted(rec)
+        o = O.sparse_ffn(q["gate"], q["up"], q["down"], q["A"], q["B"], q["bias"], q_f32(X[:, t]))
+        assert abs(rec["multiplies"] - o.stats.multiplies) <= 4 * d
+    for line in run_stream(fx.weights, pred, X, mode="dense").splitlines():
+        assert json.loads(line)["multiplies"] == 3 * d * D
+    with pytest.raises(DataError):
+        run_stream(fx.weights, pred, X, mode="bogus")
