@@ -103,6 +103,21 @@ def dist_setup():
     return world, rank, local
 
 
+def cpu_model() -> str:
+    """Host CPU model and logical CPU count (SURVEY.md §8d asks for both)."""
+    name = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    name = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return f"{name} ({os.cpu_count()} logical CPUs, SPARSEGATE_THREADS="
+    f"{os.environ.get('SPARSEGATE_THREADS', 'unset')})"
+
+
 # ---------------------------------------------------------------------------
 # reference arm: the reference's own executor headers (oracle/_ref) on host cores
 # ---------------------------------------------------------------------------
@@ -160,6 +175,7 @@ def run_reference(args, world, rank):
                                f"s={args.sparsity} batch 1", "layers": L, "hidden": d, "inter": D},
         "per_layer_us": per_token_layer * 1e6,
         "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": kind,
+                         "cpu_model": cpu_model(),
                          "sample": f"{k} steps x {ntok} eval tokens through layer 0 of {L} "
                                    f"(reference sparse_ffn_sequential, f64, per-call validation, "
                                    f"parallel_for over tokens); tokens/s = 1/(t_token_layer*{L})"},
@@ -202,6 +218,7 @@ def cpu_baseline_for(cfg, host_layer0, args):
         tot = time.perf_counter() - t0
     per = tot / (reps * ntok)
     return {"value": 1.0 / (per * L), "unit": "tokens/s", "cores": cores, "kind": kind,
+            "cpu_model": cpu_model(),
             "sample": f"{reps} x {ntok} eval tokens through layer 0 of {L} (reference "
                       f"sparse_ffn_sequential, f64 incl. per-call validation, parallel_for over "
                       f"tokens); tokens/s = 1/(t_token_layer*{L})",
@@ -395,8 +412,9 @@ def main():
             if world > 1:
                 torch.distributed.all_reduce(ys[l])
 
-    step = step_stack if (args.mode == "stack" and world == 1) else step_layers
-    launches_per_step = 1 if step is step_stack else L
+    is_stack = args.mode == "stack" and world == 1
+    step = step_stack if is_stack else step_layers
+    launches_per_step = 1 if is_stack else L
     graph_mode = "none"
     if step is step_layers and not args.no_graph and os.environ.get("SG_BENCH_BACKEND", "nccl") == "nccl":
         # per-layer launches (+ one NCCL all-reduce each) replayed as one CUDA graph
@@ -424,6 +442,30 @@ def main():
             graph_mode = "per-layer launches captured in one CUDA graph"
         except Exception as e:  # report, keep eager
             log(f"graph capture failed, eager per-layer launches: {e}")
+
+    if step is step_stack and not args.no_graph:
+        # the per-step stack launch (+ its stats memset) replayed as a CUDA graph
+        try:
+            capture_stream = torch.cuda.Stream()
+            with torch.cuda.stream(capture_stream):
+                step_stack()
+            torch.cuda.synchronize()
+            gs = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gs, stream=capture_stream):
+                check(lib.sg_ffn_forward_layers(
+                    ctx.handle, arr, L, int(Pipeline.Sequential), C.c_void_p(xs.data_ptr()),
+                    C.c_void_p(ys.data_ptr()), 0,
+                    C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+            eager_stack = step_stack
+
+            def step_stack_graph(pipe=Pipeline.Sequential):
+                if pipe != Pipeline.Sequential:
+                    return eager_stack(pipe)
+                gs.replay()
+            step = step_stack_graph
+            graph_mode = "stack launch captured in a CUDA graph"
+        except Exception as e:  # report, keep eager
+            log(f"graph capture failed, eager stack launches: {e}")
 
     def timed(fn, K, W, sample_clocks=False):
         for _ in range(W):
@@ -453,7 +495,7 @@ def main():
 
     # per-layer stats (p, v) of the tokens just timed (deterministic per layer)
     stats = (capi.sg_exec_stats * L)()
-    if step is step_stack:
+    if is_stack:
         check(lib.sg_ctx_read_stack_stats(ctx.handle, C.c_void_p(sh), L, stats))
     else:
         for l in range(L):
@@ -495,7 +537,7 @@ def main():
 
     dense = None
     if not args.no_dense:
-        ms_dense, _ = timed(lambda: step(Pipeline.Dense) if step is step_stack else
+        ms_dense, _ = timed(lambda: step_stack(Pipeline.Dense) if is_stack else
                             step_layers(Pipeline.Dense), max(10, args.steps // 4), 3)
         dense = {"ms_per_step": ms_dense, "tokens_per_s": 1000.0 / ms_dense,
                  "per_layer_us": ms_dense * 1000.0 / L,
@@ -539,7 +581,7 @@ def main():
                        "layout": "ascending" if args.no_balance else
                                  "per-CTA load-balanced neuron order from calibration statistics",
                        "hot_rows": 0 if args.no_balance else args.hot_rows,
-                       "mode": "stack (one persistent launch per step)" if step is step_stack
+                       "mode": "stack (one persistent launch per step)" if is_stack
                                else "per-layer launches", "graph": graph_mode},
             "per_layer_us": ms * 1000.0 / L,
             "p_mean": float(np.mean(ps)), "v_mean": float(np.mean(vs)),
