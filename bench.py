@@ -114,8 +114,8 @@ def cpu_model() -> str:
                     break
     except OSError:
         pass
-    return f"{name} ({os.cpu_count()} logical CPUs, SPARSEGATE_THREADS="
-    f"{os.environ.get('SPARSEGATE_THREADS', 'unset')})"
+    threads = os.environ.get("SPARSEGATE_THREADS", "unset")
+    return f"{name} ({os.cpu_count()} logical CPUs, SPARSEGATE_THREADS={threads})"
 
 
 # ---------------------------------------------------------------------------
