@@ -43,6 +43,7 @@ struct sg_layer {
     size_t bytes = 0;
     std::vector<int> gidx;  // local -> global when a layout order was given (else empty)
     sg::LayerView view{};
+    sg::LayerView* repdev = nullptr;  // [64] copies of view: small batches as one stack launch
 };
 
 struct sg_ctx {
@@ -74,6 +75,7 @@ struct sg_ctx {
     float* bydev = nullptr;
     const sg_layer* blast = nullptr;
     int blast_B = 0;
+    bool blast_stack = false;  // the last batch ran as a stack launch (small B)
 };
 
 constexpr int kMaxStackLayers = 1024;
@@ -204,6 +206,17 @@ sg_exec_stats make_stats(const sg_layer* L, int pipeline, int64_t p, int64_t v) 
     return stats_from_counts(L->d, L->D_local, L->r, pipeline, p, v);
 }
 
+// Batches up to this size run through the persistent single-token executor (one
+// stack launch, token b as layer b): below ~6 tokens it beats the batched GEMM
+// path. SG_BATCH_STACK_MAX overrides (0 = always the GEMM path).
+int small_batch_limit() {
+    static const int v = [] {
+        const char* e = std::getenv("SG_BATCH_STACK_MAX");
+        return e ? std::atoi(e) : 6;
+    }();
+    return v;
+}
+
 sg::WorkView work_for(sg_ctx* ctx, const float* x, float* y) {
     sg::WorkView W = ctx->W;
     W.x = x;
@@ -235,6 +248,74 @@ sg_status read_x(const void* x, sg_dtype dt, int64_t n, int64_t d, float* out, c
         }
         out[i] = static_cast<float>(v);
     }
+    return SG_OK;
+}
+
+sg_status stack_launch(sg_ctx* C, const sg_layer* const* layers, int32_t n,
+                              sg_pipeline pipeline, const float* xs, float* ys, int32_t chain,
+                              void* stream, unsigned long long* mbits, unsigned long long* vbits,
+                              const sg::LayerView* views_dev = nullptr) {
+    if (C == nullptr || layers == nullptr || n < 1 || n > kMaxStackLayers)
+        return fail(SG_ERR_USAGE, "bad arguments");
+    if (xs == nullptr || ys == nullptr) return fail(SG_ERR_USAGE, "null xs/ys");
+    const sg_layer* L0 = layers[0];
+    for (int i = 0; i < n; ++i) {
+        const sg_layer* L = layers[i];
+        if (sg_status s = check_pair(C, L); s != SG_OK) return s;
+        if (L->d != L0->d || L->D_local != L0->D_local || L->r != L0->r)
+            return fail(SG_ERR_USAGE, "all layers of a stack must share hidden/inter/rank");
+        if (pipeline != SG_PIPELINE_DENSE && !L->has_pred)
+            return fail(SG_ERR_USAGE, "sparse pipeline needs layers with predictors");
+        if (!L->has_w) return fail(SG_ERR_USAGE, "predictor-only layer cannot run the FFN");
+    }
+    DeviceGuard dg(C->device);
+    auto st = static_cast<cudaStream_t>(stream);
+    if (views_dev != nullptr) {
+        // caller-provided descriptor table (no upload: graph-capture safe)
+        SG_CUDA(cudaMemsetAsync(C->W.stats, 0, static_cast<size_t>(n) * 4 * sizeof(int), st));
+        sg::WorkView W = work_for(C, xs, ys);
+        W.mbits = mbits;
+        W.vbits = vbits;
+        const int e = sg::launch_layers(views_dev, n, L0->view, W, xs, ys, chain,
+                                        static_cast<int>(L0->d), pipeline, C->G, st);
+        if (e != 0) return fail(SG_ERR_CUDA, std::string("launch: ") +
+                                                 cudaGetErrorString(static_cast<cudaError_t>(e)));
+        C->last_layer = layers[n - 1];
+        C->last_pipeline = pipeline;
+        C->last_stack.clear();
+        return SG_OK;
+    }
+    if (C->stack_cap < n) {
+        C->last_stack.clear();
+        if (C->stackdev) cudaFree(C->stackdev);
+        C->stackdev = nullptr;
+        C->stack_cap = 0;
+        SG_CUDA(cudaMalloc(&C->stackdev, sizeof(sg::LayerView) * n));
+        C->stack_cap = n;
+    }
+    // The (tiny) descriptor table is uploaded only when the stack changes, so
+    // repeated calls — and CUDA-graph capture after a first warm call — issue
+    // nothing but the kernel launch.
+    const bool same = C->last_stack.size() == static_cast<size_t>(n) &&
+                      std::equal(C->last_stack.begin(), C->last_stack.end(), layers);
+    if (!same) {
+        std::vector<sg::LayerView> views(n);
+        for (int i = 0; i < n; ++i) views[i] = layers[i]->view;
+        SG_CUDA(cudaStreamSynchronize(st));
+        SG_CUDA(cudaMemcpy(C->stackdev, views.data(), sizeof(sg::LayerView) * n,
+                           cudaMemcpyHostToDevice));
+    }
+    SG_CUDA(cudaMemsetAsync(C->W.stats, 0, static_cast<size_t>(n) * 4 * sizeof(int), st));
+    sg::WorkView W = work_for(C, xs, ys);
+    W.mbits = mbits;
+    W.vbits = vbits;
+    const int e = sg::launch_layers(C->stackdev, n, L0->view, W, xs, ys, chain,
+                                    static_cast<int>(L0->d), pipeline, C->G, st);
+    if (e != 0) return fail(SG_ERR_CUDA, std::string("launch: ") +
+                                             cudaGetErrorString(static_cast<cudaError_t>(e)));
+    C->last_layer = layers[n - 1];
+    C->last_pipeline = pipeline;
+    C->last_stack.assign(layers, layers + n);
     return SG_OK;
 }
 
@@ -452,6 +533,7 @@ sg_status sg_layer_destroy(sg_layer* L) {
     if (L == nullptr) return SG_OK;
     DeviceGuard dg(L->device);
     if (L->dmem) cudaFree(L->dmem);
+    if (L->repdev) cudaFree(L->repdev);
     delete L;
     return SG_OK;
 }
@@ -463,6 +545,11 @@ int64_t sg_layer_device_bytes(const sg_layer* L) { return L ? static_cast<int64_
 sg_status sg_layer_set_hot_rows(sg_layer* L, int64_t rows) {
     if (L == nullptr || rows < 0) return fail(SG_ERR_USAGE, "sg_layer_set_hot_rows: bad arguments");
     L->view.hot = static_cast<int>(rows < L->D_local ? rows : L->D_local);
+    if (L->repdev) {  // stale copies of the view: rebuilt by the next small batch
+        DeviceGuard dg(L->device);
+        cudaFree(L->repdev);
+        L->repdev = nullptr;
+    }
     return SG_OK;
 }
 
@@ -627,6 +714,32 @@ sg_status sg_ffn_forward_batch(sg_ctx* C, const sg_layer* L, const float* xs, in
     if (xs == nullptr || ys == nullptr) return fail(SG_ERR_USAGE, "null buffers");
     if (sg_status s = batch_workspace(C); s != SG_OK) return s;
     DeviceGuard dg(C->device);
+    if (batch <= small_batch_limit() && batch <= kMaxStackLayers) {
+        // few tokens: one persistent launch with token b as "layer" b of a stack
+        // (unchained; same per-token results), predicted / survivor bits per token
+        auto st = static_cast<cudaStream_t>(stream);
+        const size_t bits = static_cast<size_t>(L->D_local) * sizeof(uint64_t);
+        SG_CUDA(cudaMemsetAsync(C->bw.mbits, 0, bits, st));
+        SG_CUDA(cudaMemsetAsync(C->bw.vbits, 0, bits, st));
+        if (L->repdev == nullptr) {  // first small batch on this layer (not under capture)
+            sg::LayerView* dev = nullptr;
+            std::vector<sg::LayerView> views(64, L->view);
+            SG_CUDA(cudaMalloc(&dev, sizeof(sg::LayerView) * views.size()));
+            SG_CUDA(cudaMemcpy(dev, views.data(), sizeof(sg::LayerView) * views.size(),
+                               cudaMemcpyHostToDevice));
+            const_cast<sg_layer*>(L)->repdev = dev;
+        }
+        std::vector<const sg_layer*> rep(static_cast<size_t>(batch), L);
+        if (sg_status s = stack_launch(C, rep.data(), batch, SG_PIPELINE_SEQUENTIAL, xs, ys, 0, stream,
+                                       reinterpret_cast<unsigned long long*>(C->bw.mbits),
+                                       reinterpret_cast<unsigned long long*>(C->bw.vbits), L->repdev);
+            s != SG_OK)
+            return s;
+        C->blast = L;
+        C->blast_B = batch;
+        C->blast_stack = true;
+        return SG_OK;
+    }
     sg::BatchArgs a = C->bw;
     a.B = batch;
     a.nb = (batch + 7) / 8 * 8;
@@ -646,6 +759,7 @@ sg_status sg_ffn_forward_batch(sg_ctx* C, const sg_layer* L, const float* xs, in
                                              cudaGetErrorString(static_cast<cudaError_t>(e)));
     C->blast = L;
     C->blast_B = batch;
+    C->blast_stack = false;
     return SG_OK;
 }
 
@@ -657,8 +771,17 @@ sg_status sg_ctx_read_batch(sg_ctx* C, void* stream, int32_t batch, sg_exec_stat
     SG_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
     const sg_layer* L = C->blast;
     int pc[64], vc[64];
-    SG_CUDA(cudaMemcpy(pc, C->bw.pcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
-    SG_CUDA(cudaMemcpy(vc, C->bw.vcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
+    if (C->blast_stack) {
+        std::vector<int> st4(static_cast<size_t>(batch) * 4);
+        SG_CUDA(cudaMemcpy(st4.data(), C->W.stats, st4.size() * sizeof(int), cudaMemcpyDeviceToHost));
+        for (int b = 0; b < batch; ++b) {
+            pc[b] = st4[4 * b];
+            vc[b] = st4[4 * b + 1];
+        }
+    } else {
+        SG_CUDA(cudaMemcpy(pc, C->bw.pcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
+        SG_CUDA(cudaMemcpy(vc, C->bw.vcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
+    }
     for (int b = 0; stats && b < batch; ++b) stats[b] = make_stats(L, SG_PIPELINE_SEQUENTIAL, pc[b], vc[b]);
     if (pred_bits)
         SG_CUDA(cudaMemcpy(pred_bits, C->bw.mbits, sizeof(uint64_t) * L->D_local, cudaMemcpyDeviceToHost));
@@ -802,51 +925,9 @@ sg_status sg_ffn_forward(sg_ctx* C, const sg_layer* L, sg_pipeline pipeline, con
 sg_status sg_ffn_forward_layers(sg_ctx* C, const sg_layer* const* layers, int32_t n,
                                 sg_pipeline pipeline, const float* xs, float* ys, int32_t chain,
                                 void* stream) {
-    if (C == nullptr || layers == nullptr || n < 1 || n > kMaxStackLayers)
-        return fail(SG_ERR_USAGE, "bad arguments");
-    if (xs == nullptr || ys == nullptr) return fail(SG_ERR_USAGE, "null xs/ys");
-    const sg_layer* L0 = layers[0];
-    for (int i = 0; i < n; ++i) {
-        const sg_layer* L = layers[i];
-        if (sg_status s = check_pair(C, L); s != SG_OK) return s;
-        if (L->d != L0->d || L->D_local != L0->D_local || L->r != L0->r)
-            return fail(SG_ERR_USAGE, "all layers of a stack must share hidden/inter/rank");
-        if (pipeline != SG_PIPELINE_DENSE && !L->has_pred)
-            return fail(SG_ERR_USAGE, "sparse pipeline needs layers with predictors");
-        if (!L->has_w) return fail(SG_ERR_USAGE, "predictor-only layer cannot run the FFN");
-    }
-    DeviceGuard dg(C->device);
-    auto st = static_cast<cudaStream_t>(stream);
-    if (C->stack_cap < n) {
-        C->last_stack.clear();
-        if (C->stackdev) cudaFree(C->stackdev);
-        C->stackdev = nullptr;
-        C->stack_cap = 0;
-        SG_CUDA(cudaMalloc(&C->stackdev, sizeof(sg::LayerView) * n));
-        C->stack_cap = n;
-    }
-    // The (tiny) descriptor table is uploaded only when the stack changes, so
-    // repeated calls — and CUDA-graph capture after a first warm call — issue
-    // nothing but the kernel launch.
-    const bool same = C->last_stack.size() == static_cast<size_t>(n) &&
-                      std::equal(C->last_stack.begin(), C->last_stack.end(), layers);
-    if (!same) {
-        std::vector<sg::LayerView> views(n);
-        for (int i = 0; i < n; ++i) views[i] = layers[i]->view;
-        SG_CUDA(cudaStreamSynchronize(st));
-        SG_CUDA(cudaMemcpy(C->stackdev, views.data(), sizeof(sg::LayerView) * n,
-                           cudaMemcpyHostToDevice));
-    }
-    SG_CUDA(cudaMemsetAsync(C->W.stats, 0, static_cast<size_t>(n) * 4 * sizeof(int), st));
-    const int e = sg::launch_layers(C->stackdev, n, L0->view, work_for(C, xs, ys), xs, ys, chain,
-                                    static_cast<int>(L0->d), pipeline, C->G, st);
-    if (e != 0) return fail(SG_ERR_CUDA, std::string("launch: ") +
-                                             cudaGetErrorString(static_cast<cudaError_t>(e)));
-    C->last_layer = layers[n - 1];
-    C->last_pipeline = pipeline;
-    C->last_stack.assign(layers, layers + n);
-    return SG_OK;
+    return stack_launch(C, layers, n, pipeline, xs, ys, chain, stream, nullptr, nullptr);
 }
+
 
 sg_status sg_ctx_enable_phase_timing(sg_ctx* C, int32_t max_layers) {
     if (C == nullptr || max_layers < 0) return fail(SG_ERR_USAGE, "bad arguments");

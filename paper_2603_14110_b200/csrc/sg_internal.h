@@ -50,6 +50,9 @@ struct WorkView {
     unsigned long long* bar;  // 8 grid-barrier counters, 256 B apart (see grid_barrier)
     int* stats;           // [4 per layer] p, v, nonfinite(x), pipeline
     uint64_t* dbg;        // optional [layers][G][16] globaltimer phase stamps (or null)
+    unsigned long long* mbits;  // optional [D]: bit `bitpos` set for predicted neurons
+    unsigned long long* vbits;  // optional [D]: bit `bitpos` set for survivors
+    int bitpos;                 //   (small batches run as a stack, token b = layer b)
     int flags;            // experiment switches (SG_FLAGS env, default 0): 2 no survivor-row
                           // L2 prefetch; bits 8-15 consumer-group override, bits 16-23
                           // ring-slot override (timing studies only; results unchanged)

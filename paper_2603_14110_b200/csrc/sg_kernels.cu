@@ -696,6 +696,7 @@ __device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm
                 const uint8_t on = pre > 0.f ? 1 : 0;  // strict, ffn_exec.hpp:141
                 sm.mask[k] = on;
                 if (mask_out) mask_out[n0 + k] = on;
+                if (on && W.mbits) atomicOr(W.mbits + n0 + k, 1ull << W.bitpos);
             }
             }
     } else {
@@ -728,6 +729,7 @@ __device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm
                 const uint8_t on = pre > 0.f ? 1 : 0;  // strict, ffn_exec.hpp:141
                 sm.mask[k] = on;
                 if (mask_out) mask_out[n0 + k] = on;
+                if (on && W.mbits) atomicOr(W.mbits + n0 + k, 1ull << W.bitpos);
             }
         }
     }
@@ -938,6 +940,7 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(a + off));
                 }
                 if (gt == 0) {
+                    if (kPipe == 2 && sv && W.vbits) atomicOr(W.vbits + nn, 1ull << W.bitpos);
                     if (inP) W.gN[nn] = g;  // gate pre-activation per neuron (P output)
                     int2 rec;
                     rec.x = sv ? nn : -1;
@@ -1384,6 +1387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* y = ys + static_cast<size_t>(l) * xstride;
         WorkView Wl = W;
         Wl.stats = W.stats + 4 * l;  // per-layer {p, v, nonfinite, pipeline}
+        Wl.bitpos = l;
         prestaged = run_layer<kPipe>(L, Wl, sm, S, rs, x, y, l == 0, chain != 0, l, l == nlayers - 1,
                                      next, prestaged);
         if (layers && l + 1 < nlayers) {
