@@ -432,6 +432,109 @@ __global__ void y_reduce_kernel(BatchArgs a, float* __restrict__ y) {
     y[i] = s;
 }
 
+// Down projection for small batches (nb <= 16) on the CUDA cores, streaming
+// whole row pieces: CTA (rg, cg) takes the survivor-union positions of row
+// group rg and the 1024 columns of column group cg (2 KB contiguous per row;
+// the GEMM tile reads 128 B per row at a 16 KB stride). Thread = (row lane rl,
+// column thread ct): CP columns x TB tokens of fp32 accumulators over the rows
+// rl, rl + RL, ... of its group in order; the RL lanes are summed in order
+// through shared memory, then the row groups in order by y_rows_reduce.
+// Deterministic; bits differ from the tensor-core path (tolerance-checked).
+constexpr int kDrCols = 1024;  // columns per column group
+template <int TB>
+__global__ void __launch_bounds__(512) down_rows_kernel(BatchArgs a, int ncg, int nrg) {
+    constexpr int CP = 64 / TB;            // columns per thread
+    constexpr int T = kDrCols / CP;        // threads per row piece
+    constexpr int RL = 512 / T;            // row lanes
+    extern __shared__ __align__(16) float red[];  // [RL][T][TB*CP]
+    const int nv = *a.nv;
+    const int cg = blockIdx.x % ncg, rg = blockIdx.x / ncg;
+    const int tid = threadIdx.x, rl = tid / T, ct = tid % T;
+    const int col = cg * kDrCols + ct * CP;
+    const int p0 = static_cast<int>(static_cast<long long>(rg) * nv / nrg);
+    const int p1 = static_cast<int>(static_cast<long long>(rg + 1) * nv / nrg);
+    float acc[TB][CP];
+#pragma unroll
+    for (int b = 0; b < TB; ++b)
+#pragma unroll
+        for (int e = 0; e < CP; ++e) acc[b][e] = 0.f;
+    const bool okc = col < a.pitch_d;
+    const uint16_t* base = a.ud + a.pitch_d + col;
+    // U rows per step: their index, weight and z loads all in flight together
+    constexpr int U = TB == 8 ? 4 : 2;
+    for (int pos0 = p0 + rl; pos0 < p1; pos0 += U * RL) {
+        int nid[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int pos = pos0 + u * RL;
+            nid[u] = pos < p1 ? __ldg(a.vlist + pos) : -1;
+        }
+        uint32_t w[U][CP / 2];
+        float4 z[U][TB / 4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const bool ok = nid[u] >= 0;
+            const uint16_t* src = base + static_cast<size_t>(ok ? nid[u] : 0) * 2 * a.pitch_d;
+            if (CP == 8) {
+                const uint4 v = ok && okc ? __ldg(reinterpret_cast<const uint4*>(src)) : make_uint4(0u, 0u, 0u, 0u);
+                w[u][0] = v.x;
+                w[u][1 % (CP / 2)] = v.y;
+                w[u][2 % (CP / 2)] = v.z;
+                w[u][3 % (CP / 2)] = v.w;
+            } else {
+                const uint2 v = ok && okc ? __ldg(reinterpret_cast<const uint2*>(src)) : make_uint2(0u, 0u);
+                w[u][0] = v.x;
+                w[u][1 % (CP / 2)] = v.y;
+            }
+            const float4* zr = reinterpret_cast<const float4*>(
+                a.Z + static_cast<size_t>(ok ? nid[u] : 0) * kMaxBatch);
+#pragma unroll
+            for (int b4 = 0; b4 < TB / 4; ++b4)
+                z[u][b4] = ok ? __ldg(zr + b4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        // rows in position order (u ascending): the accumulation order per thread
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int b4 = 0; b4 < TB / 4; ++b4) {
+                const float zz[4] = {z[u][b4].x, z[u][b4].y, z[u][b4].z, z[u][b4].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int i = 0; i < CP / 2; ++i) {
+                        acc[b4 * 4 + q][2 * i] =
+                            fmaf(zz[q], __uint_as_float(w[u][i] << 16), acc[b4 * 4 + q][2 * i]);
+                        acc[b4 * 4 + q][2 * i + 1] =
+                            fmaf(zz[q], __uint_as_float(w[u][i] & 0xffff0000u), acc[b4 * 4 + q][2 * i + 1]);
+                    }
+            }
+    }
+    float* mine = red + (static_cast<size_t>(rl) * T + ct) * (TB * CP);
+#pragma unroll
+    for (int b = 0; b < TB; ++b)
+#pragma unroll
+        for (int e = 0; e < CP; ++e) mine[b * CP + e] = acc[b][e];
+    __syncthreads();
+    if (rl == 0 && okc) {
+        for (int b = 0; b < a.B; ++b)
+            for (int e = 0; e < CP; ++e) {
+                float s = 0.f;
+                for (int l = 0; l < RL; ++l) s += red[(static_cast<size_t>(l) * T + ct) * (TB * CP) + b * CP + e];
+                a.gp[(static_cast<size_t>(rg) * TB + b) * a.pitch_d + col + e] = s;
+            }
+    }
+}
+
+template <int TB>
+__global__ void y_rows_reduce_kernel(BatchArgs a, int nrg, float* __restrict__ y) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.B * a.d) return;
+    const int n = i / a.d, m = i - n * a.d;
+    float s = 0.f;
+    for (int rg = 0; rg < nrg; ++rg) s += a.gp[(static_cast<size_t>(rg) * TB + n) * a.pitch_d + m];
+    y[i] = s;
+}
+
 int gemm_smem(bool trans, int nb) { return kStages * stage_elems(trans, nb) * 2; }
 
 }  // namespace
@@ -473,6 +576,33 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
     compact_kernel<<<1, 1024, 0, st>>>(a.vflag, a.D, a.vlist, a.nv);
     up_kernel<<<dim3((a.D + kBM - 1) / kBM, a.gsplit), kBThreads, sm_rows, st>>>(a);
     up_epi_kernel<<<(a.D * kMaxBatch + 255) / 256, 256, 0, st>>>(a);
+    // small batches: whole-row-piece streaming on the CUDA cores (partials reuse gp,
+    // free after up_epi); larger: the tensor-core GEMM over Z hi/lo
+    const int ncg = (a.pitch_d + kDrCols - 1) / kDrCols;
+    const int tb = a.nb <= 8 ? 8 : 16;
+    const size_t cap = static_cast<size_t>(a.gsplit) * a.pitch_v * kMaxBatch;  // floats in gp
+    int nrg = a.sms / ncg;
+    if (static_cast<size_t>(nrg) * tb * a.pitch_d > cap)
+        nrg = static_cast<int>(cap / (static_cast<size_t>(tb) * a.pitch_d));
+    const bool rows_path = a.nb <= 16 && nrg >= 8;
+    if (rows_path) {
+        const int smem = 512 * 64 * 4;
+        static bool rattr = false;
+        if (!rattr) {
+            cudaFuncSetAttribute(down_rows_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaFuncSetAttribute(down_rows_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            rattr = true;
+        }
+        const int n = a.B * a.d;
+        if (tb == 8) {
+            down_rows_kernel<8><<<ncg * nrg, 512, smem, st>>>(a, ncg, nrg);
+            y_rows_reduce_kernel<8><<<(n + 255) / 256, 256, 0, st>>>(a, nrg, ys);
+        } else {
+            down_rows_kernel<16><<<ncg * nrg, 512, smem, st>>>(a, ncg, nrg);
+            y_rows_reduce_kernel<16><<<(n + 255) / 256, 256, 0, st>>>(a, nrg, ys);
+        }
+        return static_cast<int>(cudaGetLastError());
+    }
     zpad_kernel<<<(kBK * kMaxBatch + 255) / 256, 256, 0, st>>>(a);
     down_kernel<<<dim3((a.pitch_d + kBM - 1) / kBM, a.dsplit), kBThreads, sm_down, st>>>(a);
     {

@@ -678,6 +678,7 @@ sg_status batch_workspace(sg_ctx* C) {
     a.tsplit = tsplit;
     a.dsplit = dsplit;
     a.gsplit = gsplit;
+    a.sms = C->G;
     a.gp = reinterpret_cast<float*>(b + o_gp);
     a.xh = reinterpret_cast<uint16_t*>(b + o_xh);
     a.xl = reinterpret_cast<uint16_t*>(b + o_xl);

@@ -83,6 +83,7 @@ struct BatchArgs {
     int pitch_d, pitch_r, pitch_v;  // pitch_v: survivor-position pitch of Z (>= round_up(D, 64))
     int act;
     int tsplit, dsplit, gsplit;     // split-K of the T, down and gate/up GEMMs
+    int sms;                        // SM count (grid of the row-streaming down kernel)
     // layer
     const uint16_t* Bm;  // predictor B, r x pitch_d
     const uint16_t* A;   // D x pitch_r
