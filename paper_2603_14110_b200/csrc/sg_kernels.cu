@@ -1010,68 +1010,84 @@ __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkVi
         a0[e] = 0.f;
         a1[e] = 0.f;
     }
-    const int chunk = S.sv_chunk;  // rows that fit in the big region, <= kSvChunk
-    for (int base = 0; base < nsv; base += chunk) {
-        const int m = nsv - base < chunk ? nsv - base : chunk;
-        if (warp == kWarps) {
-            // the ring's last generic reads ended at a block barrier
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            const uint64_t pol = policy_evict_first();
-            if (lane == 0) mbar_expect_tx(sm.abar, static_cast<uint32_t>(m) * ud_bytes);
-            __syncwarp();
-            if (lane < m)
-                bulk_g2s(sm.big + static_cast<size_t>(lane) * ud_bytes,
-                         L.ud + static_cast<size_t>(sm.svl[base + lane].x) * 2 * L.pitch_d, ud_bytes,
-                         sm.abar, pol);
-            __syncwarp();
-        }
-        mbar_wait(sm.abar, rs.auses & 1u);
-        rs.auses += 1;
+    // groups of `half` survivors alternate between two row buffers (barriers
+    // full[kMaxSlots-2+b], never used by the ring): group g + 2 is fetched while
+    // group g + 1 is computed, so a CTA with more survivors than fit at once does
+    // not pay a second exposed L2 round trip
+    const int half = S.sv_chunk / 2;
+    int* bu = sm.uses + kMaxSlots - 2;  // fills of the two buffer barriers so far
+    const uint64_t pol = policy_evict_first();
+    auto issue = [&](int g) {  // producer warp
+        const int r0 = g * half;
+        const int m = nsv - r0 < half ? nsv - r0 : half;
+        if (m <= 0) return;
+        uint64_t* bar = sm.full + kMaxSlots - 2 + (g & 1);
+        if (lane == 0) mbar_expect_tx(bar, static_cast<uint32_t>(m) * ud_bytes);
         __syncwarp();
-        for (int b = 0; b < m; b += kBatch) {
-            const int nb = m - b < kBatch ? m - b : kBatch;
-            float* red = sm.reda + ((b / kBatch) & 1) * (kWarps * kBatch);
-            if (comp) {
-                float part[kBatch];
+        if (lane < m)
+            bulk_g2s(sm.big + static_cast<size_t>((g & 1) * half + lane) * ud_bytes,
+                     L.ud + static_cast<size_t>(sm.svl[r0 + lane].x) * 2 * L.pitch_d, ud_bytes, bar,
+                     pol);
+        __syncwarp();
+    };
+    if (warp == kWarps) {
+        // the ring's last generic reads ended at a block barrier
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(0);
+        issue(1);
+    }
+    const int ngroups = nsv > 0 ? (nsv + half - 1) / half : 0;
+    for (int g = 0; g < ngroups; ++g) {
+        const int r0 = g * half;
+        const int m = nsv - r0 < half ? nsv - r0 : half;  // <= kBatch
+        const uint8_t* rows = sm.big + static_cast<size_t>((g & 1) * half) * ud_bytes;
+        mbar_wait(sm.full + kMaxSlots - 2 + (g & 1), static_cast<uint32_t>(bu[g & 1] + (g >> 1)) & 1u);
+        __syncwarp();
+        float* red = sm.reda + (g & 1) * (kWarps * kBatch);
+        if (comp) {
+            float part[kBatch];
 #pragma unroll
-                for (int j = 0; j < kBatch; ++j) {
-                    part[j] = 0.f;
-                    if (j < nb) {
-                        const uint16_t* up = reinterpret_cast<const uint16_t*>(
-                            sm.big + static_cast<size_t>(b + j) * ud_bytes);
-                        float acc = 0.f;
-                        if (h0) acc = dot8r(*reinterpret_cast<const uint4*>(up + ch0 * 8), x0, acc);
-                        if (h1) acc = dot8r(*reinterpret_cast<const uint4*>(up + ch1 * 8), x1, acc);
-                        part[j] = acc;
-                    }
+            for (int j = 0; j < kBatch; ++j) {
+                part[j] = 0.f;
+                if (j < m) {
+                    const uint16_t* up = reinterpret_cast<const uint16_t*>(rows + static_cast<size_t>(j) * ud_bytes);
+                    float acc = 0.f;
+                    if (h0) acc = dot8r(*reinterpret_cast<const uint4*>(up + ch0 * 8), x0, acc);
+                    if (h1) acc = dot8r(*reinterpret_cast<const uint4*>(up + ch1 * 8), x1, acc);
+                    part[j] = acc;
                 }
-                const float s = warp_sum8(part, lane);
-                if ((lane & 3) == 0)
-                    red[warp * kBatch + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)] = s;
             }
-            __syncthreads();
-            if (tid < nb) {
-                float u = 0.f;
-                for (int w = 0; w < kWarps; ++w) u += red[w * kBatch + tid];
-                int2 e = sm.svl[base + b + tid];
-                const float z = gated(__int_as_float(e.y), u, L.act);
-                zs[b + tid] = z;
-                e.y = __float_as_int(z);
-                reinterpret_cast<int2*>(W.vseg)[n0 + base + b + tid] = e;
-            }
+            const float s = warp_sum8(part, lane);
+            if ((lane & 3) == 0)
+                red[warp * kBatch + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)] = s;
+        }
+        __syncthreads();
+        if (tid < m) {
+            float u = 0.f;
+            for (int w = 0; w < kWarps; ++w) u += red[w * kBatch + tid];
+            int2 e = sm.svl[r0 + tid];
+            const float z = gated(__int_as_float(e.y), u, L.act);
+            zs[tid] = z;
+            e.y = __float_as_int(z);
+            reinterpret_cast<int2*>(W.vseg)[n0 + r0 + tid] = e;
         }
         __syncthreads();  // zs complete
         if (comp) {
             for (int i = 0; i < m; ++i) {
                 const uint16_t* dn =
-                    reinterpret_cast<const uint16_t*>(sm.big + static_cast<size_t>(i) * ud_bytes) + L.pitch_d;
+                    reinterpret_cast<const uint16_t*>(rows + static_cast<size_t>(i) * ud_bytes) + L.pitch_d;
                 const float z = zs[i];
                 if (h0) axpy8(*reinterpret_cast<const uint4*>(dn + ch0 * 8), z, a0);
                 if (h1) axpy8(*reinterpret_cast<const uint4*>(dn + ch1 * 8), z, a1);
             }
         }
-        __syncthreads();  // the chunk's rows and zs are no longer read
+        __syncthreads();  // the group's rows and zs are no longer read
+        if (warp == kWarps) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(g + 2);
+        }
     }
+    if (tid < 2) bu[tid] += (ngroups + 1 - tid) / 2;  // buffer 0: ceil(n/2), buffer 1: floor(n/2)
     // this CTA's partial y
     if (h0) {
         float4* dst = reinterpret_cast<float4*>(W.ypart + static_cast<size_t>(c) * L.pitch_d + ch0 * 8);
@@ -1476,7 +1492,7 @@ bool make_plan(int G, int pitch_d, int r, int pitch_r, int Dl, int pipe, int max
     S->slot_bytes = (pipe == 2 ? 1 : 2) * pitch_d * 2;
     S->pre_slots = S->stage_off / S->slot_bytes;
     int ns_max = avail / S->slot_bytes;
-    if (ns_max > kMaxSlots) ns_max = kMaxSlots;
+    if (ns_max > kMaxSlots - 2) ns_max = kMaxSlots - 2;  // full[kMaxSlots-2..]: survivor buffers
     if (ns_max < 1) return false;
     int kc = ns_max < kGroups ? ns_max : kGroups;
     if (kc_override > 0 && kc_override < kc) kc = kc_override;
@@ -1486,7 +1502,7 @@ bool make_plan(int G, int pitch_d, int r, int pitch_r, int Dl, int pipe, int max
     S->ns = kc * (ns_max / kc);
     S->big_bytes = avail;
     S->sv_chunk = avail / (pitch_d * 4) < kSvChunk ? avail / (pitch_d * 4) : kSvChunk;
-    if (pipe == 2 && S->sv_chunk < 1) return false;
+    if (pipe == 2 && S->sv_chunk < 2) return false;  // two survivor row buffers
     S->total = max_smem;
     return true;
 }
