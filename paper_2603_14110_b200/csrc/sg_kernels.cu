@@ -984,7 +984,8 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
 // ---------------------------------------------------------------------------
 // Stages 4+5a of the sequential pipeline, per CTA, after its gate stream. The
 // survivors' [up | down] rows (16 KB each, contiguous, sent to L2 during the
-// gate stream) are bulk-copied into shared memory, up to kSvChunk at a time.
+// gate stream) are bulk-copied into shared memory in groups of sv_chunk / 2,
+// alternating between two row buffers so one group lands while another is computed.
 // Thread t owns chunk t (and t + 512) of every row with x in registers: the
 // up rows of a chunk are dotted kBatch at a time (8 independent FMA chains,
 // one transposed warp butterfly, warps summed in order), warp 0 forms
