@@ -55,7 +55,7 @@ constexpr int kWarps = 16;                // compute warps
 constexpr int kCThreads = kWarps * 32;    // 512 compute threads
 constexpr int kThreads = kCThreads + 32;  // + one producer warp (cp.async.bulk issue)
 constexpr int kMaxSlots = 32;             // ring slots (upper bound)
-constexpr int kRowsA = 4;                 // phase A rows reduced per pass
+constexpr int kRowsA = 2;                 // phase A rows reduced per pass (r = 256 over 148 CTAs: <= 2)
 constexpr int kGroupWarps = 4;            // phase C: a row is reduced by a group of 4 warps
 constexpr int kGroups = kWarps / kGroupWarps;
 constexpr int kGroupThreads = kGroupWarps * 32;
