@@ -234,6 +234,31 @@ def test_hot_prefix_keeps_parity(hot):
         assert np.array_equal(r0.y, r1.y)
 
 
+@pytest.mark.parametrize("shards", [2, 3])
+def test_bench_shards_with_layout_and_hot_prefix(shards):
+    """Shards uploaded as the N > 1 bench does (model.upload: balanced hot-first layout
+    per shard + 16-row hot prefix): their outputs sum to the oracle's y, their sets
+    (global indices) partition the oracle's sets."""
+    cfg = CONFIGS["tiny"]
+    d, D = cfg["d"], cfg["D"]
+    h = build_host_layer(d, D, 0, seed=6, rank=64, sparsity=0.5, eval_tokens=3)
+    q = _host_q(h)
+    parts = [upload(h, d, D, 0, 64, shard_index=k, shard_count=shards) for k in range(shards)]
+    for t in range(h.xs.shape[1]):
+        x = h.xs[:, t]
+        y = np.zeros(d)
+        P, V = [], []
+        for lay in parts:
+            ctx = lay.context()
+            y += lay.forward(x, Pipeline.Sequential, ctx).y
+            Pk, Vk, _, _ = read_sets(ctx, lay.local_inter)
+            P += Pk.tolist()
+            V += Vk.tolist()
+        assert len(set(P)) == len(P) and len(set(V)) == len(V)
+        diag = check_token(q, x, y, sorted(P), sorted(V))
+        assert diag["rel"] <= Y_RTOL
+
+
 def test_device_layer_container_round_trip(tmp_path):
     """save_device_layer / load_device_layer (tensor_io extension) reproduce the layer."""
     from paper_2603_14110_b200 import tensor_io as T
