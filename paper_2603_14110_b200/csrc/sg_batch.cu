@@ -580,7 +580,7 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
     // free after up_epi); larger: the tensor-core GEMM over Z hi/lo
     const int ncg = (a.pitch_d + kDrCols - 1) / kDrCols;
     const int tb = a.nb <= 8 ? 8 : 16;
-    const size_t cap = static_cast<size_t>(a.gsplit) * a.pitch_v * kMaxBatch;  // floats in gp
+    const size_t cap = static_cast<size_t>(kGpSplits) * a.pitch_v * kMaxBatch;  // floats in gp
     int nrg = a.sms / ncg;
     if (static_cast<size_t>(nrg) * tb * a.pitch_d > cap)
         nrg = static_cast<int>(cap / (static_cast<size_t>(tb) * a.pitch_d));

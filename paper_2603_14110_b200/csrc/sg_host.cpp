@@ -651,7 +651,14 @@ sg_status batch_workspace(sg_ctx* C) {
     const size_t Dm = static_cast<size_t>(C->max_D), pd = static_cast<size_t>(C->pitch_dmax),
                  pr = static_cast<size_t>(C->pitch_rmax);
     const size_t pv = (Dm + 63) / 64 * 64;
-    const int tsplit = 16, dsplit = 4, gsplit = 4;
+    const int tsplit = 16, dsplit = 4;
+    // split-K of the gate / up GEMMs (SG_BATCH_GSPLIT overrides; the partial buffer
+    // is sized for sg::kGpSplits)
+    const int gsplit = [] {
+        const char* e = std::getenv("SG_BATCH_GSPLIT");
+        const int v = e ? std::atoi(e) : 0;  // 0: per call (see sg_ffn_forward_batch)
+        return v < 0 ? 0 : (v > sg::kGpSplits ? sg::kGpSplits : v);
+    }();
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const size_t o = off;
@@ -664,7 +671,7 @@ sg_status batch_workspace(sg_ctx* C) {
                  o_G = take(Dm * M * 4), o_vb = take(Dm * 8), o_vf = take(Dm * 4), o_vc = take(M * 4),
                  o_vl = take(Dm * 4), o_nv = take(4), o_Z = take(Dm * M * 4), o_zh = take(M * pv * 2),
                  o_zl = take(M * pv * 2), o_yp = take(dsplit * M * pd * 4), o_bx = take(M * pd * 4),
-                 o_by = take(M * pd * 4), o_gp = take(gsplit * pv * M * 4);
+                 o_by = take(M * pd * 4), o_gp = take(sg::kGpSplits * pv * M * 4);
     DeviceGuard dg(C->device);
     cudaError_t e = cudaMalloc(&C->bmem, off);
     if (e == cudaSuccess) e = cudaMemset(C->bmem, 0, off);
@@ -743,6 +750,9 @@ sg_status sg_ffn_forward_batch(sg_ctx* C, const sg_layer* L, const float* xs, in
     }
     sg::BatchArgs a = C->bw;
     a.B = batch;
+    // split-K of the gate / up GEMMs: enough CTAs for ~2 full waves of the union
+    // tiles (measured at the 7B shape: 7 best up to B = 32, 4 at B = 64)
+    if (a.gsplit == 0) a.gsplit = batch <= 32 ? 7 : 4;
     a.nb = (batch + 7) / 8 * 8;
     a.d = static_cast<int>(L->d);
     a.D = static_cast<int>(L->D_local);

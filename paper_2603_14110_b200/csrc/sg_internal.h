@@ -76,6 +76,7 @@ int launch_layers(const LayerView* layers_dev, int n, const LayerView& first, co
 int query_launch_info(int device, LaunchInfo* info);
 
 // Batched decode (sg_batch.cu): one layer, B <= batch_max() tokens.
+constexpr int kGpSplits = 8;  // capacity of BatchArgs::gp in split-K partials
 struct BatchArgs {
     int B;        // tokens
     int nb;       // B rounded up to a multiple of 8
