@@ -525,6 +525,95 @@ __global__ void __launch_bounds__(512) down_rows_kernel(BatchArgs a, int ncg, in
     }
 }
 
+// Gate / up projections for small batches (nb <= 16) on the CUDA cores:
+// gp[cg][pos][n] = sum over the 1024 columns of column group cg of
+// W[rows[pos]][c] * x[n][c], x exact fp32 (no hi/lo split). CTA (cg, rg) stages
+// its column group of x in smem and its 16 warps stream whole 2-KB row pieces:
+// warp step s covers positions p0 + s*R .. +R of row group rg (steps dealt to the
+// warps round-robin), lane l takes the 16-B chunks l + 32 i (i < 4) of every row,
+// so a warp has 4R 16-B loads per lane in flight. The R x TB lane partials are
+// summed by a fixed transposed butterfly (lane j ends with output j); the column
+// groups are summed in order by gate_epi / up_epi. Deterministic.
+template <int TB>
+__global__ void __launch_bounds__(512) rows_dot_kernel(BatchArgs a, const float* __restrict__ xs,
+                                                       const uint16_t* __restrict__ W, int wp,
+                                                       const int* __restrict__ rows,
+                                                       const int* __restrict__ count, int ncg,
+                                                       int nrg) {
+    constexpr int R = 32 / TB;  // rows per warp step: R x TB = 32 outputs
+    extern __shared__ __align__(16) float4 xsm[];  // [TB][2][128]: chunk ch, half h
+    const int cg = blockIdx.x % ncg, rg = blockIdx.x / ncg;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int c0 = cg * kDrCols;
+    for (int i = tid; i < TB * 256; i += 512) {
+        const int b = i >> 8, q = i & 255, ch = q >> 1, h = q & 1;
+        const int c = c0 + ch * 8 + h * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (b < a.B) {
+            const float* src = xs + static_cast<size_t>(b) * a.d;
+            if (c + 0 < a.d) v.x = src[c + 0];
+            if (c + 1 < a.d) v.y = src[c + 1];
+            if (c + 2 < a.d) v.z = src[c + 2];
+            if (c + 3 < a.d) v.w = src[c + 3];
+        }
+        xsm[(b * 2 + h) * 128 + ch] = v;
+    }
+    __syncthreads();
+    const int n = *count;
+    const int p0 = static_cast<int>(static_cast<long long>(rg) * n / nrg);
+    const int p1 = static_cast<int>(static_cast<long long>(rg + 1) * n / nrg);
+    for (int pos0 = p0 + warp * R; pos0 < p1; pos0 += 16 * R) {
+        uint4 w[R][4];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const bool ok = pos0 + r < p1;
+            const uint16_t* src = W + static_cast<size_t>(ok ? __ldg(rows + pos0 + r) : 0) * wp + c0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int c = (lane + 32 * i) * 8;
+                w[r][i] = ok && c0 + c < a.pitch_d ? __ldg(reinterpret_cast<const uint4*>(src + c))
+                                                   : make_uint4(0u, 0u, 0u, 0u);
+            }
+        }
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int b = 0; b < TB; ++b) {
+                const float4 xa = xsm[(b * 2) * 128 + lane + 32 * i];
+                const float4 xb = xsm[(b * 2 + 1) * 128 + lane + 32 * i];
+                const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const uint32_t wv[4] = {w[r][i].x, w[r][i].y, w[r][i].z, w[r][i].w};
+                    float s = v[r * TB + b];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        s = fmaf(__uint_as_float(wv[e] << 16), xv[2 * e], s);
+                        s = fmaf(__uint_as_float(wv[e] & 0xffff0000u), xv[2 * e + 1], s);
+                    }
+                    v[r * TB + b] = s;
+                }
+            }
+        // transposed butterfly: after the level with offset o, v[j] (j < o) holds
+        // index j + (lane & o ? o : 0) summed over the lanes that differ in bit o
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int j = 0; j < o; ++j) {
+                const float send = up ? v[j] : v[j + o];
+                const float keep = up ? v[j + o] : v[j];
+                v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        const int r = lane / TB, b = lane % TB, pos = pos0 + r;
+        if (pos < p1) a.gp[(static_cast<size_t>(cg) * a.pitch_v + pos) * kMaxBatch + b] = v[0];
+    }
+}
+
 template <int TB>
 __global__ void y_rows_reduce_kernel(BatchArgs a, int nrg, float* __restrict__ y) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -571,14 +660,37 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
     }
     mask_kernel<<<(a.D + kBM - 1) / kBM, kBThreads, sm_rows, st>>>(a);
     compact_kernel<<<1, 1024, 0, st>>>(a.uflag, a.D, a.plist, a.np);
-    gate_kernel<<<dim3((a.D + kBM - 1) / kBM, a.gsplit), kBThreads, sm_rows, st>>>(a);
+    // small batches: gate / up row pieces streamed on the CUDA cores (x exact fp32,
+    // one partial per column group); larger: the tensor-core GEMM tiles, split-K
+    const int ncg = (a.pitch_d + kDrCols - 1) / kDrCols;
+    const bool dot_rows = a.nb <= 16 && ncg <= kGpSplits && a.gdot;
+    const int dtb = a.nb <= 8 ? 8 : 16;
+    const int dgrid = ncg * (a.sms / ncg < 1 ? 1 : a.sms / ncg);
+    const int dsm = dtb * 256 * 16;
+    if (dot_rows) {
+        static bool dattr = false;
+        if (!dattr) {
+            cudaFuncSetAttribute(rows_dot_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 256 * 16);
+            cudaFuncSetAttribute(rows_dot_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 256 * 16);
+            dattr = true;
+        }
+        a.gsplit = ncg;
+        auto k = dtb == 8 ? rows_dot_kernel<8> : rows_dot_kernel<16>;
+        k<<<dgrid, 512, dsm, st>>>(a, xs, a.gate, a.pitch_d, a.plist, a.np, ncg, dgrid / ncg);
+    } else {
+        gate_kernel<<<dim3((a.D + kBM - 1) / kBM, a.gsplit), kBThreads, sm_rows, st>>>(a);
+    }
     gate_epi_kernel<<<(a.D + 7) / 8, 256, 0, st>>>(a);
     compact_kernel<<<1, 1024, 0, st>>>(a.vflag, a.D, a.vlist, a.nv);
-    up_kernel<<<dim3((a.D + kBM - 1) / kBM, a.gsplit), kBThreads, sm_rows, st>>>(a);
+    if (dot_rows) {
+        auto k = dtb == 8 ? rows_dot_kernel<8> : rows_dot_kernel<16>;
+        k<<<dgrid, 512, dsm, st>>>(a, xs, a.ud, 2 * a.pitch_d, a.vlist, a.nv, ncg, dgrid / ncg);
+    } else {
+        up_kernel<<<dim3((a.D + kBM - 1) / kBM, a.gsplit), kBThreads, sm_rows, st>>>(a);
+    }
     up_epi_kernel<<<(a.D * kMaxBatch + 255) / 256, 256, 0, st>>>(a);
     // small batches: whole-row-piece streaming on the CUDA cores (partials reuse gp,
     // free after up_epi); larger: the tensor-core GEMM over Z hi/lo
-    const int ncg = (a.pitch_d + kDrCols - 1) / kDrCols;
     const int tb = a.nb <= 8 ? 8 : 16;
     const size_t cap = static_cast<size_t>(kGpSplits) * a.pitch_v * kMaxBatch;  // floats in gp
     int nrg = a.sms / ncg;

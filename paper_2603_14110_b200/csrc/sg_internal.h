@@ -77,6 +77,7 @@ int query_launch_info(int device, LaunchInfo* info);
 
 // Batched decode (sg_batch.cu): one layer, B <= batch_max() tokens.
 constexpr int kGpSplits = 8;  // capacity of BatchArgs::gp in split-K partials
+constexpr int kDpSplits = 12; // capacity of BatchArgs::yp in split-K partials
 struct BatchArgs {
     int B;        // tokens
     int nb;       // B rounded up to a multiple of 8
@@ -84,6 +85,7 @@ struct BatchArgs {
     int pitch_d, pitch_r, pitch_v;  // pitch_v: survivor-position pitch of Z (>= round_up(D, 64))
     int act;
     int tsplit, dsplit, gsplit;     // split-K of the T, down and gate/up GEMMs
+    int gdot;                       // B <= 16: gate / up on the CUDA cores (rows_dot_kernel)
     int sms;                        // SM count (grid of the row-streaming down kernel)
     // layer
     const uint16_t* Bm;  // predictor B, r x pitch_d
