@@ -274,6 +274,58 @@ __global__ void __launch_bounds__(kBThreads) mask_kernel(BatchArgs a) {
     count_tokens(bits[0], bits[1], a.B, a.pcount);
 }
 
+// ascending compaction of flags[0..D), D <= 16384, into list, count into *count
+// (one CTA): element j*1024 + t is read by thread t (coalesced), each warp
+// ballots it, one block-wide scan over the (j, warp) counts gives every warp's
+// output offset for every j, the flags stay in the ballot masks.
+constexpr int kCompactPer = 16;
+__global__ void __launch_bounds__(1024) compact_ballot_kernel(const int* __restrict__ flag, int D,
+                                                              int* __restrict__ list,
+                                                              int* __restrict__ count) {
+    __shared__ int woff[kCompactPer * 32];
+    __shared__ int wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (D + 1023) / 1024;
+    uint32_t m[kCompactPer];
+#pragma unroll
+    for (int j = 0; j < kCompactPer; ++j) {
+        m[j] = 0u;
+        if (j < per) {
+            const int i = j * 1024 + tid;
+            m[j] = __ballot_sync(0xffffffffu, i < D && flag[i] != 0);
+            if (lane == 0) woff[j * 32 + warp] = __popc(m[j]);
+        }
+    }
+    __syncthreads();
+    const int v = tid < per * 32 ? woff[tid & (kCompactPer * 32 - 1)] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int w = wsum[lane];
+        int wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += u;
+        }
+        wsum[lane] = wi - w;  // exclusive
+        if (lane == 31) *count = wi;
+    }
+    __syncthreads();
+    if (tid < per * 32) woff[tid] = wsum[warp] + incl - v;
+    __syncthreads();
+    const uint32_t below = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < kCompactPer; ++j)
+        if (j < per && ((m[j] >> lane) & 1u)) list[woff[j * 32 + warp] + __popc(m[j] & below)] = j * 1024 + tid;
+}
+
 // ascending compaction of flags[0..D) into list, count into *count (one CTA):
 // thread t scans a contiguous run, one block-wide exclusive scan, then writes.
 __global__ void __launch_bounds__(1024) compact_kernel(const int* __restrict__ flag, int D,
@@ -659,7 +711,10 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
         t_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(a);
     }
     mask_kernel<<<(a.D + kBM - 1) / kBM, kBThreads, sm_rows, st>>>(a);
-    compact_kernel<<<1, 1024, 0, st>>>(a.uflag, a.D, a.plist, a.np);
+    if (a.D <= kCompactPer * 1024)
+        compact_ballot_kernel<<<1, 1024, 0, st>>>(a.uflag, a.D, a.plist, a.np);
+    else
+        compact_kernel<<<1, 1024, 0, st>>>(a.uflag, a.D, a.plist, a.np);
     // small batches: gate / up row pieces streamed on the CUDA cores (x exact fp32,
     // one partial per column group); larger: the tensor-core GEMM tiles, split-K
     const int ncg = (a.pitch_d + kDrCols - 1) / kDrCols;
@@ -681,7 +736,10 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
         gate_kernel<<<dim3((a.D + kBM - 1) / kBM, a.gsplit), kBThreads, sm_rows, st>>>(a);
     }
     gate_epi_kernel<<<(a.D + 7) / 8, 256, 0, st>>>(a);
-    compact_kernel<<<1, 1024, 0, st>>>(a.vflag, a.D, a.vlist, a.nv);
+    if (a.D <= kCompactPer * 1024)
+        compact_ballot_kernel<<<1, 1024, 0, st>>>(a.vflag, a.D, a.vlist, a.nv);
+    else
+        compact_kernel<<<1, 1024, 0, st>>>(a.vflag, a.D, a.vlist, a.nv);
     if (dot_rows) {
         auto k = dtb == 8 ? rows_dot_kernel<8> : rows_dot_kernel<16>;
         k<<<dgrid, 512, dsm, st>>>(a, xs, a.ud, 2 * a.pitch_d, a.vlist, a.nv, ncg, dgrid / ncg);
