@@ -80,13 +80,13 @@ __device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b
 // TRANS_A: W is stored [k][m] (m contiguous, pitch wp) — the down projection,
 // where "rows" index K (neurons) and the 64-wide tile runs over m.
 // ---------------------------------------------------------------------------
-constexpr int kStages = 6;  // cp.async pipeline depth (K chunks in flight)
+constexpr int kStages = 6;  // cp.async pipeline depth (K chunks in flight), default
 
 __host__ __device__ constexpr int a_elems(bool trans) { return trans ? kBK * (kBM + 8) : kBM * kRowPad; }
 __host__ __device__ inline int stage_elems(bool trans, int nb) { return a_elems(trans) + 2 * nb * kRowPad; }
 
-template <bool TRANS_A>
-__device__ __forceinline__ void gemm_tile(const uint16_t* __restrict__ W, int wp,
+template <bool TRANS_A, int kStages>
+__device__ __forceinline__ void gemm_tile_s(const uint16_t* __restrict__ W, int wp,
                                           const int* __restrict__ rows, int nrows, int m0,
                                           const uint16_t* __restrict__ Xh,
                                           const uint16_t* __restrict__ Xl, int xp, int nb, int k0,
@@ -176,6 +176,24 @@ __device__ __forceinline__ void gemm_tile(const uint16_t* __restrict__ W, int wp
     __syncthreads();
 }
 
+// pipeline depth chosen per call (BatchArgs::stages): fewer stages at large B
+// so more CTAs fit per SM
+template <bool TRANS_A>
+__device__ __forceinline__ void gemm_tile(int stages, const uint16_t* __restrict__ W, int wp,
+                                          const int* __restrict__ rows, int nrows, int m0,
+                                          const uint16_t* __restrict__ Xh,
+                                          const uint16_t* __restrict__ Xl, int xp, int nb, int k0,
+                                          int k1, uint16_t* sm, float (*acc)[4]) {
+    if (stages == 2)
+        gemm_tile_s<TRANS_A, 2>(W, wp, rows, nrows, m0, Xh, Xl, xp, nb, k0, k1, sm, acc);
+    else if (stages == 3)
+        gemm_tile_s<TRANS_A, 3>(W, wp, rows, nrows, m0, Xh, Xl, xp, nb, k0, k1, sm, acc);
+    else if (stages == 4)
+        gemm_tile_s<TRANS_A, 4>(W, wp, rows, nrows, m0, Xh, Xl, xp, nb, k0, k1, sm, acc);
+    else
+        gemm_tile_s<TRANS_A, kStages>(W, wp, rows, nrows, m0, Xh, Xl, xp, nb, k0, k1, sm, acc);
+}
+
 // acc -> out[(split * cap + row) * 64 + n] for the CTA's rows (fp32 partial sums)
 __device__ __forceinline__ void store_partial(float (*acc)[4], float* out, int cap, int split, int m0,
                                               int nrows, int nb) {
@@ -222,7 +240,7 @@ __global__ void __launch_bounds__(kBThreads) t_kernel(BatchArgs a) {
     float acc[kMaxBatch / 8][4];
     const int kslice = ((a.pitch_d + a.tsplit - 1) / a.tsplit + kBK - 1) / kBK * kBK;
     const int k0 = min(a.pitch_d, blockIdx.y * kslice), k1 = min(a.pitch_d, k0 + kslice);
-    gemm_tile<false>(a.Bm, a.pitch_d, nullptr, a.r, blockIdx.x * kBM, a.xh, a.xl, a.pitch_d, a.nb, k0,
+    gemm_tile<false>(a.stages, a.Bm, a.pitch_d, nullptr, a.r, blockIdx.x * kBM, a.xh, a.xl, a.pitch_d, a.nb, k0,
                      k1, smb, acc);
     store_partial(acc, a.tp, a.pitch_r, blockIdx.y, blockIdx.x * kBM, a.r, a.nb);
 }
@@ -246,7 +264,7 @@ __global__ void t_reduce_kernel(BatchArgs a) {
 __global__ void __launch_bounds__(kBThreads) mask_kernel(BatchArgs a) {
     extern __shared__ __align__(128) uint16_t smb[];
     float acc[kMaxBatch / 8][4];
-    gemm_tile<false>(a.A, a.pitch_r, nullptr, a.D, blockIdx.x * kBM, a.th, a.tl, a.pitch_r, a.nb, 0,
+    gemm_tile<false>(a.stages, a.A, a.pitch_r, nullptr, a.D, blockIdx.x * kBM, a.th, a.tl, a.pitch_r, a.nb, 0,
                      a.pitch_r, smb, acc);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint64_t bits[2] = {0ull, 0ull};
@@ -368,7 +386,7 @@ __global__ void __launch_bounds__(kBThreads) gate_kernel(BatchArgs a) {
     const int kslice = ((a.pitch_d + a.gsplit - 1) / a.gsplit + kBK - 1) / kBK * kBK;
     const int k0 = min(a.pitch_d, blockIdx.y * kslice), k1 = min(a.pitch_d, k0 + kslice);
     float acc[kMaxBatch / 8][4];
-    gemm_tile<false>(a.gate, a.pitch_d, a.plist, np, blockIdx.x * kBM, a.xh, a.xl, a.pitch_d, a.nb, k0,
+    gemm_tile<false>(a.stages, a.gate, a.pitch_d, a.plist, np, blockIdx.x * kBM, a.xh, a.xl, a.pitch_d, a.nb, k0,
                      k1, smb, acc);
     store_partial(acc, a.gp, a.pitch_v, blockIdx.y, blockIdx.x * kBM, np, a.nb);
 }
@@ -411,7 +429,7 @@ __global__ void __launch_bounds__(kBThreads) up_kernel(BatchArgs a) {
     const int kslice = ((a.pitch_d + a.gsplit - 1) / a.gsplit + kBK - 1) / kBK * kBK;
     const int k0 = min(a.pitch_d, blockIdx.y * kslice), k1 = min(a.pitch_d, k0 + kslice);
     float acc[kMaxBatch / 8][4];
-    gemm_tile<false>(a.ud, 2 * a.pitch_d, a.vlist, nv, blockIdx.x * kBM, a.xh, a.xl, a.pitch_d, a.nb, k0,
+    gemm_tile<false>(a.stages, a.ud, 2 * a.pitch_d, a.vlist, nv, blockIdx.x * kBM, a.xh, a.xl, a.pitch_d, a.nb, k0,
                      k1, smb, acc);
     store_partial(acc, a.gp, a.pitch_v, blockIdx.y, blockIdx.x * kBM, nv, a.nb);
 }
@@ -460,7 +478,7 @@ __global__ void __launch_bounds__(kBThreads) down_kernel(BatchArgs a) {
     const int k0 = blockIdx.y * per * kBK, k1 = min(nv, k0 + per * kBK);
     float acc[kMaxBatch / 8][4];
     // down rows of neuron k live in ud at k * 2 pitch_d + pitch_d
-    gemm_tile<true>(a.ud + a.pitch_d, 2 * a.pitch_d, a.vlist, nv, blockIdx.x * kBM, a.zh, a.zl,
+    gemm_tile<true>(a.stages, a.ud + a.pitch_d, 2 * a.pitch_d, a.vlist, nv, blockIdx.x * kBM, a.zh, a.zl,
                     a.pitch_v, a.nb, k0, k1 > k0 ? k1 : k0, smb, acc);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
@@ -676,7 +694,7 @@ __global__ void y_rows_reduce_kernel(BatchArgs a, int nrg, float* __restrict__ y
     y[i] = s;
 }
 
-int gemm_smem(bool trans, int nb) { return kStages * stage_elems(trans, nb) * 2; }
+int gemm_smem(bool trans, int nb, int stages) { return stages * stage_elems(trans, nb) * 2; }
 
 }  // namespace
 
@@ -685,16 +703,16 @@ int batch_max() { return kMaxBatch; }
 int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_) {
     cudaStream_t st = static_cast<cudaStream_t>(stream_);
     BatchArgs a = a0;
-    const int sm_rows = gemm_smem(false, a.nb), sm_down = gemm_smem(true, a.nb);
+    const int sm_rows = gemm_smem(false, a.nb, a.stages), sm_down = gemm_smem(true, a.nb, a.stages);
     static bool attr = false;
     if (!attr) {
-        const int mx = gemm_smem(false, kMaxBatch);
+        const int mx = gemm_smem(false, kMaxBatch, kStages);
         cudaFuncSetAttribute(t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             gemm_smem(true, kMaxBatch));
+                             gemm_smem(true, kMaxBatch, kStages));
         attr = true;
     }
     cudaMemsetAsync(a.pcount, 0, sizeof(int) * kMaxBatch, st);

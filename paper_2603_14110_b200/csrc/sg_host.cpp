@@ -764,9 +764,21 @@ sg_status sg_ffn_forward_batch(sg_ctx* C, const sg_layer* L, const float* xs, in
     // split-K of the gate / up GEMMs: enough CTAs for ~2 full waves of the union
     // tiles (measured at the 7B shape: 7 best up to B = 32, 4 at B = 64)
     if (a.gsplit == 0) a.gsplit = batch <= 32 ? 7 : 4;
-    // split-K of the down GEMM (B > 16; measured at the 7B shape, B = 32: 4 best,
-    // B = 64: split 4 / 9 / 12 = 18.7k / 19.1k / 19.4k tokens/s)
-    if (a.dsplit == 0) a.dsplit = batch <= 32 ? 4 : 12;
+    // split-K of the down GEMM (B > 16; measured at the 7B shape with the stage
+    // depths below, B = 32: 4 best; B = 64: split 4 / 8 / 12 = 29.6k / 33.5k / 31.5k
+    // tokens/s)
+    if (a.dsplit == 0) a.dsplit = batch <= 32 ? 4 : 8;
+    {  // cp.async depth of the GEMM tiles (SG_BATCH_STAGES overrides: 2, 3, 4 or 6)
+        static const int st = [] {
+            const char* e = std::getenv("SG_BATCH_STAGES");
+            return e ? std::atoi(e) : 0;
+        }();
+        // measured at the 7B shape (8-layer stack): B = 64: 6 / 4 / 3 / 2 stages =
+        // 19.3k / 26.0k / 26.0k / 31.5k tokens/s (smem per CTA bounds the CTAs per
+        // SM, and the tiles are latency-bound per warp); B = 32: 17.1k / 17.6k /
+        // 18.6k / 18.5k; B <= 16 (T / mask tiles only): no difference
+        a.stages = st >= 2 && st <= 4 ? st : st == 6 ? 6 : (batch > 32 ? 2 : 3);
+    }
     a.nb = (batch + 7) / 8 * 8;
     a.d = static_cast<int>(L->d);
     a.D = static_cast<int>(L->D_local);

@@ -86,6 +86,7 @@ struct BatchArgs {
     int act;
     int tsplit, dsplit, gsplit;     // split-K of the T, down and gate/up GEMMs
     int gdot;                       // B <= 16: gate / up on the CUDA cores (rows_dot_kernel)
+    int stages;                     // cp.async depth of the GEMM tiles (3, 4 or 6)
     int sms;                        // SM count (grid of the row-streaming down kernel)
     // layer
     const uint16_t* Bm;  // predictor B, r x pitch_d
