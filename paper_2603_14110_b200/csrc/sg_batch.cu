@@ -29,12 +29,14 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 namespace sg {
 namespace {
 
 constexpr int kBM = 64;                  // rows per CTA tile
-constexpr int kBK = 64;                  // K per pipeline stage
+constexpr int kBK = 32;                  // K per pipeline stage
+constexpr int kCh = kBK / 8;             // 16-B chunks per row per stage
 constexpr int kBWarps = 4;               // one m16 slice per warp
 constexpr int kBThreads = kBWarps * 32;
 constexpr int kRowPad = kBK + 8;         // smem row stride (bf16): conflict-free ldmatrix
@@ -101,8 +103,8 @@ __device__ __forceinline__ void gemm_tile_s(const uint16_t* __restrict__ W, int 
         uint16_t* xh = a + kA;
         uint16_t* xl = xh + nb * kRowPad;
         if (!TRANS_A) {
-            for (int i = tid; i < kBM * 8; i += kBThreads) {
-                const int r = i >> 3, p = i & 7;
+            for (int i = tid; i < kBM * kCh; i += kBThreads) {
+                const int r = i / kCh, p = i % kCh;
                 const int gr = m0 + r;
                 const bool ok = gr < nrows;
                 const int row = ok ? (rows ? rows[gr] : gr) : 0;
@@ -118,8 +120,8 @@ __device__ __forceinline__ void gemm_tile_s(const uint16_t* __restrict__ W, int 
                 cp16(a + r * (kBM + 8) + p * 8, W + static_cast<size_t>(row) * wp + m0 + p * 8, ok);
             }
         }
-        for (int i = tid; i < nb * 8; i += kBThreads) {
-            const int n = i >> 3, p = i & 7;
+        for (int i = tid; i < nb * kCh; i += kBThreads) {
+            const int n = i / kCh, p = i % kCh;
             cp16(xh + n * kRowPad + p * 8, Xh + static_cast<size_t>(n) * xp + kb + p * 8, true);
             cp16(xl + n * kRowPad + p * 8, Xl + static_cast<size_t>(n) * xp + kb + p * 8, true);
         }
@@ -509,20 +511,44 @@ __global__ void y_reduce_kernel(BatchArgs a, float* __restrict__ y) {
 // column thread ct): CP columns x TB tokens of fp32 accumulators over the rows
 // rl, rl + RL, ... of its group in order; the RL lanes are summed in order
 // through shared memory, then the row groups in order by y_rows_reduce.
+// Rows arrive through a kDrStages-deep cp.async ring: each thread copies (and
+// later reads) its own CP columns of each row; the rows' z values are copied by
+// the first TB / 4 threads of each row lane (one __syncthreads per step).
 // Deterministic; bits differ from the tensor-core path (tolerance-checked).
 constexpr int kDrCols = 1024;  // columns per column group
+constexpr int kDrStages = 4;   // ring depth (steps of U rows per row lane)
+constexpr int kDrU = 4;        // rows per row lane per step
+constexpr int kDrIdx = 1024;   // row ids staged in smem per CTA
+template <int TB>
+constexpr int down_rows_smem() {
+    constexpr int CP = 64 / TB, RL = 512 / (kDrCols / CP);
+    constexpr int ring = kDrStages * kDrU * 512 * CP * 2 + kDrStages * kDrU * RL * TB * 4;
+    constexpr int red = 512 * TB * CP * 4;
+    return ring > red ? ring : red;
+}
 template <int TB>
 __global__ void __launch_bounds__(512) down_rows_kernel(BatchArgs a, int ncg, int nrg) {
     constexpr int CP = 64 / TB;            // columns per thread
     constexpr int T = kDrCols / CP;        // threads per row piece
     constexpr int RL = 512 / T;            // row lanes
-    extern __shared__ __align__(16) float red[];  // [RL][T][TB*CP]
+    constexpr int U = kDrU;
+    constexpr int NS = kDrStages;
+    using WV = typename std::conditional<CP == 8, uint4, uint2>::type;
+    extern __shared__ __align__(16) float red[];  // [RL][T][TB*CP] after the loop
+    WV* wring = reinterpret_cast<WV*>(red);                              // [NS][U][512]
+    float* zring = reinterpret_cast<float*>(wring + NS * U * 512);       // [NS][U][RL][TB]
     const int nv = *a.nv;
     const int cg = blockIdx.x % ncg, rg = blockIdx.x / ncg;
     const int tid = threadIdx.x, rl = tid / T, ct = tid % T;
     const int col = cg * kDrCols + ct * CP;
     const int p0 = static_cast<int>(static_cast<long long>(rg) * nv / nrg);
     const int p1 = static_cast<int>(static_cast<long long>(rg + 1) * nv / nrg);
+    const int nsteps = (p1 - p0 + U * RL - 1) / (U * RL);
+    // the group's neuron ids, staged once (the copies then issue without a
+    // dependent global load each)
+    __shared__ int sidx[kDrIdx];
+    for (int i = tid; i < p1 - p0 && i < kDrIdx; i += 512) sidx[i] = __ldg(a.vlist + p0 + i);
+    __syncthreads();
     float acc[TB][CP];
 #pragma unroll
     for (int b = 0; b < TB; ++b)
@@ -530,55 +556,70 @@ __global__ void __launch_bounds__(512) down_rows_kernel(BatchArgs a, int ncg, in
         for (int e = 0; e < CP; ++e) acc[b][e] = 0.f;
     const bool okc = col < a.pitch_d;
     const uint16_t* base = a.ud + a.pitch_d + col;
-    // U rows per step: their index, weight and z loads all in flight together
-    constexpr int U = TB == 8 ? 4 : 2;
-    for (int pos0 = p0 + rl; pos0 < p1; pos0 += U * RL) {
-        int nid[U];
+    auto issue = [&](int k, int stg) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int pos = pos0 + u * RL;
-            nid[u] = pos < p1 ? __ldg(a.vlist + pos) : -1;
+            const int pos = p0 + rl + (k * U + u) * RL;
+            const bool ok = pos < p1;
+            const int nid = !ok ? 0 : pos - p0 < kDrIdx ? sidx[pos - p0] : __ldg(a.vlist + pos);
+            const uint16_t* src = base + static_cast<size_t>(nid) * 2 * a.pitch_d;
+            const uint32_t dst = smem_u32b(wring + (stg * U + u) * 512 + tid);
+            if (CP == 8)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                             "r"(ok && okc ? 16 : 0)
+                             : "memory");
+            else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
+                             "r"(ok && okc ? 8 : 0)
+                             : "memory");
+            if (ct < TB / 4)
+                cp16(zring + ((stg * U + u) * RL + rl) * TB + ct * 4,
+                     a.Z + static_cast<size_t>(nid) * kMaxBatch + ct * 4, ok);
         }
-        uint32_t w[U][CP / 2];
-        float4 z[U][TB / 4];
+    };
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const bool ok = nid[u] >= 0;
-            const uint16_t* src = base + static_cast<size_t>(ok ? nid[u] : 0) * 2 * a.pitch_d;
-            if (CP == 8) {
-                const uint4 v = ok && okc ? __ldg(reinterpret_cast<const uint4*>(src)) : make_uint4(0u, 0u, 0u, 0u);
-                w[u][0] = v.x;
-                w[u][1 % (CP / 2)] = v.y;
-                w[u][2 % (CP / 2)] = v.z;
-                w[u][3 % (CP / 2)] = v.w;
-            } else {
-                const uint2 v = ok && okc ? __ldg(reinterpret_cast<const uint2*>(src)) : make_uint2(0u, 0u);
-                w[u][0] = v.x;
-                w[u][1 % (CP / 2)] = v.y;
-            }
-            const float4* zr = reinterpret_cast<const float4*>(
-                a.Z + static_cast<size_t>(ok ? nid[u] : 0) * kMaxBatch);
-#pragma unroll
-            for (int b4 = 0; b4 < TB / 4; ++b4)
-                z[u][b4] = ok ? __ldg(zr + b4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < NS - 1; ++k) {
+        if (k < nsteps) issue(k, k);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int k = 0; k < nsteps; ++k) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
+        __syncthreads();  // step k's z visible; the stage read at step k - 1 is free
+        {
+            const int kn = k + NS - 1;
+            if (kn < nsteps) issue(kn, kn % NS);
+            asm volatile("cp.async.commit_group;" ::: "memory");
         }
+        const int stg = k % NS;
         // rows in position order (u ascending): the accumulation order per thread
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+        for (int u = 0; u < U; ++u) {
+            const WV wv = wring[(stg * U + u) * 512 + tid];
+            uint32_t w[CP / 2];
+            if constexpr (CP == 8) {
+                w[0] = wv.x; w[1] = wv.y; w[2] = wv.z; w[3] = wv.w;
+            } else {
+                w[0] = wv.x; w[1] = wv.y;
+            }
+            const float4* zr = reinterpret_cast<const float4*>(zring + ((stg * U + u) * RL + rl) * TB);
 #pragma unroll
             for (int b4 = 0; b4 < TB / 4; ++b4) {
-                const float zz[4] = {z[u][b4].x, z[u][b4].y, z[u][b4].z, z[u][b4].w};
+                const float4 zq = zr[b4];
+                const float zz[4] = {zq.x, zq.y, zq.z, zq.w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
 #pragma unroll
                     for (int i = 0; i < CP / 2; ++i) {
                         acc[b4 * 4 + q][2 * i] =
-                            fmaf(zz[q], __uint_as_float(w[u][i] << 16), acc[b4 * 4 + q][2 * i]);
+                            fmaf(zz[q], __uint_as_float(w[i] << 16), acc[b4 * 4 + q][2 * i]);
                         acc[b4 * 4 + q][2 * i + 1] =
-                            fmaf(zz[q], __uint_as_float(w[u][i] & 0xffff0000u), acc[b4 * 4 + q][2 * i + 1]);
+                            fmaf(zz[q], __uint_as_float(w[i] & 0xffff0000u), acc[b4 * 4 + q][2 * i + 1]);
                     }
             }
+        }
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // the ring is reused as the reduction area
     float* mine = red + (static_cast<size_t>(rl) * T + ct) * (TB * CP);
 #pragma unroll
     for (int b = 0; b < TB; ++b)
@@ -615,6 +656,12 @@ __global__ void __launch_bounds__(512) rows_dot_kernel(BatchArgs a, const float*
     const int cg = blockIdx.x % ncg, rg = blockIdx.x / ncg;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int c0 = cg * kDrCols;
+    const int n = *count;
+    const int p0 = static_cast<int>(static_cast<long long>(rg) * n / nrg);
+    const int p1 = static_cast<int>(static_cast<long long>(rg + 1) * n / nrg);
+    // the group's row ids, staged once with x (no dependent global load per step)
+    __shared__ int sidx[kDrIdx];
+    for (int i = tid; i < p1 - p0 && i < kDrIdx; i += 512) sidx[i] = __ldg(rows + p0 + i);
     for (int i = tid; i < TB * 256; i += 512) {
         const int b = i >> 8, q = i & 255, ch = q >> 1, h = q & 1;
         const int c = c0 + ch * 8 + h * 4;
@@ -629,15 +676,13 @@ __global__ void __launch_bounds__(512) rows_dot_kernel(BatchArgs a, const float*
         xsm[(b * 2 + h) * 128 + ch] = v;
     }
     __syncthreads();
-    const int n = *count;
-    const int p0 = static_cast<int>(static_cast<long long>(rg) * n / nrg);
-    const int p1 = static_cast<int>(static_cast<long long>(rg + 1) * n / nrg);
     for (int pos0 = p0 + warp * R; pos0 < p1; pos0 += 16 * R) {
         uint4 w[R][4];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const bool ok = pos0 + r < p1;
-            const uint16_t* src = W + static_cast<size_t>(ok ? __ldg(rows + pos0 + r) : 0) * wp + c0;
+            const int rid = !ok ? 0 : pos0 + r - p0 < kDrIdx ? sidx[pos0 + r - p0] : __ldg(rows + pos0 + r);
+            const uint16_t* src = W + static_cast<size_t>(rid) * wp + c0;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int c = (lane + 32 * i) * 8;
@@ -774,11 +819,13 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
         nrg = static_cast<int>(cap / (static_cast<size_t>(tb) * a.pitch_d));
     const bool rows_path = a.nb <= 16 && nrg >= 8;
     if (rows_path) {
-        const int smem = 512 * 64 * 4;
+        const int smem = tb == 8 ? down_rows_smem<8>() : down_rows_smem<16>();
         static bool rattr = false;
         if (!rattr) {
-            cudaFuncSetAttribute(down_rows_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            cudaFuncSetAttribute(down_rows_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaFuncSetAttribute(down_rows_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 down_rows_smem<8>());
+            cudaFuncSetAttribute(down_rows_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 down_rows_smem<16>());
             rattr = true;
         }
         const int n = a.B * a.d;

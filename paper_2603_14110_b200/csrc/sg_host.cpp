@@ -773,11 +773,12 @@ sg_status sg_ffn_forward_batch(sg_ctx* C, const sg_layer* L, const float* xs, in
             const char* e = std::getenv("SG_BATCH_STAGES");
             return e ? std::atoi(e) : 0;
         }();
-        // measured at the 7B shape (8-layer stack): B = 64: 6 / 4 / 3 / 2 stages =
-        // 19.3k / 26.0k / 26.0k / 31.5k tokens/s (smem per CTA bounds the CTAs per
-        // SM, and the tiles are latency-bound per warp); B = 32: 17.1k / 17.6k /
-        // 18.6k / 18.5k; B <= 16 (T / mask tiles only): no difference
-        a.stages = st >= 2 && st <= 4 ? st : st == 6 ? 6 : (batch > 32 ? 2 : 3);
+        // measured at the 7B shape (8-layer stack), 64-wide K chunks: B = 64: 6 / 4 /
+        // 3 / 2 stages = 19.3k / 26.0k / 26.0k / 31.5k tokens/s (smem per CTA bounds
+        // the CTAs per SM, and the tiles are latency-bound per warp); 32-wide K
+        // chunks (shipped): B = 64: 4 / 3 / 2 = 28.7k / 33.5k / 31.6k, B = 32:
+        // 19.4k / 19.1k / 18.0k; B <= 16 (T / mask tiles only): no difference
+        a.stages = st >= 2 && st <= 4 ? st : st == 6 ? 6 : (batch > 32 ? 3 : 4);
     }
     a.nb = (batch + 7) / 8 * 8;
     a.d = static_cast<int>(L->d);
