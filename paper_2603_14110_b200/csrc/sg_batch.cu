@@ -626,13 +626,15 @@ __global__ void __launch_bounds__(512) down_rows_kernel(BatchArgs a, int ncg, in
 #pragma unroll
         for (int e = 0; e < CP; ++e) mine[b * CP + e] = acc[b][e];
     __syncthreads();
-    if (rl == 0 && okc) {
-        for (int b = 0; b < a.B; ++b)
-            for (int e = 0; e < CP; ++e) {
-                float s = 0.f;
-                for (int l = 0; l < RL; ++l) s += red[(static_cast<size_t>(l) * T + ct) * (TB * CP) + b * CP + e];
-                a.gp[(static_cast<size_t>(rg) * TB + b) * a.pitch_d + col + e] = s;
-            }
+    // row lanes summed in order; all threads, one (token, column) output each per pass
+    for (int o = tid; o < a.B * kDrCols; o += 512) {
+        const int b = o / kDrCols, cc = o - b * kDrCols, c = cg * kDrCols + cc;
+        if (c >= a.pitch_d) continue;
+        const float* q = red + static_cast<size_t>(cc / CP) * (TB * CP) + b * CP + cc % CP;
+        float s = 0.f;
+#pragma unroll
+        for (int l = 0; l < RL; ++l) s += q[static_cast<size_t>(l) * T * (TB * CP)];
+        a.gp[(static_cast<size_t>(rg) * TB + b) * a.pitch_d + c] = s;
     }
 }
 
