@@ -317,13 +317,13 @@ def run_batch(args, cfg, host, layers, ctx, world, rank, local):
         "union_p_mean": float(np.mean(up)), "union_v_mean": float(np.mean(uv)),
         "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                      "frac": alg / (ms * 1e-3) / 1e9 / hbm, "peak_kind": hbm_kind, "traffic": None,
-                     "bytes_per_step": alg, "kernel": "sg_batch.cu (B <= 6: persistent stack executor; "
+                     "bytes_per_step": alg, "kernel": "sg_batch.cu (B <= 4: persistent stack executor; "
                                                "B <= 16: CUDA-core row streaming; above: mma.sync gathered GEMMs)"},
         "e2e": {"value": B * 1000.0 / ms_e2e, "unit": "tokens/s", "h2d_bytes_per_step": L * B * d * 4,
                 "d2h_bytes_per_step": L * B * d * 4, "ms_per_step": ms_e2e},
-        # per layer: B <= SG_BATCH_STACK_MAX (6): one persistent stack launch; nb <= 16:
+        # per layer: B <= SG_BATCH_STACK_MAX (4): one persistent stack launch; nb <= 16:
         # 12 kernels (CUDA-core gate / up / down row streaming); above: 13 (GEMM tiles)
-        "gpu_launches": args.steps * L * (1 if B <= int(os.environ.get("SG_BATCH_STACK_MAX", "6"))
+        "gpu_launches": args.steps * L * (1 if B <= int(os.environ.get("SG_BATCH_STACK_MAX", "4"))
                                           else 12 if B <= 16 else 13),
         "clocks": clocks,
         "cpu_baseline": None,

@@ -29,10 +29,24 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 namespace sg {
 namespace {
+
+// Programmatic dependent launch (opt-in, see pdl_enabled): every kernel of the
+// batched path can be launched with programmatic stream serialization, so the
+// next kernel's CTAs are set up while this one drains. Each kernel first waits for its predecessor grid to
+// complete (griddepcontrol.wait, unconditionally and before any memory access:
+// the ordering is exactly that of plain stream order, transitively), then
+// allows its own dependents to launch.
+#define SG_PDL_ENTRY()                                          \
+    do {                                                        \
+        asm volatile("griddepcontrol.wait;" ::: "memory");      \
+        asm volatile("griddepcontrol.launch_dependents;" :::);  \
+    } while (0)
+
 
 constexpr int kBM = 64;                  // rows per CTA tile
 constexpr int kBK = 32;                  // K per pipeline stage
@@ -224,9 +238,20 @@ __device__ __forceinline__ void count_tokens(uint64_t m0, uint64_t m1, int B, in
 }
 
 // x (fp32 [B][d]) -> bf16 hi/lo [nb][pitch] (zero padded rows and columns)
+// Also clears the call's counters and survivor flags / bits (in place of
+// memsets, which would break the programmatic-launch chain).
 __global__ void split_x_kernel(const float* __restrict__ x, int B, int d, int nb, int pitch,
-                               uint16_t* __restrict__ hi, uint16_t* __restrict__ lo) {
+                               uint16_t* __restrict__ hi, uint16_t* __restrict__ lo, BatchArgs a) {
+    SG_PDL_ENTRY();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < kMaxBatch) {
+        a.pcount[i] = 0;
+        a.vcount[i] = 0;
+    }
+    if (i < a.D) {
+        a.vflag[i] = 0;
+        a.vbits[i] = 0ull;
+    }
     if (i >= nb * pitch) return;
     const int n = i / pitch, k = i - n * pitch;
     const float v = (n < B && k < d) ? x[static_cast<size_t>(n) * d + k] : 0.f;
@@ -238,6 +263,7 @@ __global__ void split_x_kernel(const float* __restrict__ x, int B, int d, int nb
 
 // T partials: tp[split][j][n] over K slice `split`
 __global__ void __launch_bounds__(kBThreads) t_kernel(BatchArgs a) {
+    SG_PDL_ENTRY();
     extern __shared__ __align__(128) uint16_t smb[];
     float acc[kMaxBatch / 8][4];
     const int kslice = ((a.pitch_d + a.tsplit - 1) / a.tsplit + kBK - 1) / kBK * kBK;
@@ -249,6 +275,7 @@ __global__ void __launch_bounds__(kBThreads) t_kernel(BatchArgs a) {
 
 // T = sum of the splits in order -> bf16 hi/lo [nb][pitch_r]
 __global__ void t_reduce_kernel(BatchArgs a) {
+    SG_PDL_ENTRY();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.nb * a.pitch_r) return;
     const int n = i / a.pitch_r, j = i - n * a.pitch_r;
@@ -264,6 +291,7 @@ __global__ void t_reduce_kernel(BatchArgs a) {
 
 // pre = A T + bias over all D rows: mask bits, union flags, per-token |P|
 __global__ void __launch_bounds__(kBThreads) mask_kernel(BatchArgs a) {
+    SG_PDL_ENTRY();
     extern __shared__ __align__(128) uint16_t smb[];
     float acc[kMaxBatch / 8][4];
     gemm_tile<false>(a.stages, a.A, a.pitch_r, nullptr, a.D, blockIdx.x * kBM, a.th, a.tl, a.pitch_r, a.nb, 0,
@@ -302,17 +330,23 @@ constexpr int kCompactPer = 16;
 __global__ void __launch_bounds__(1024) compact_ballot_kernel(const int* __restrict__ flag, int D,
                                                               int* __restrict__ list,
                                                               int* __restrict__ count) {
+    SG_PDL_ENTRY();
     __shared__ int woff[kCompactPer * 32];
     __shared__ int wsum[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int per = (D + 1023) / 1024;
     uint32_t m[kCompactPer];
+    int f[kCompactPer];  // all flag loads in flight before the first ballot
+#pragma unroll
+    for (int j = 0; j < kCompactPer; ++j) {
+        const int i = j * 1024 + tid;
+        f[j] = j < per && i < D ? __ldcg(flag + i) : 0;
+    }
 #pragma unroll
     for (int j = 0; j < kCompactPer; ++j) {
         m[j] = 0u;
         if (j < per) {
-            const int i = j * 1024 + tid;
-            m[j] = __ballot_sync(0xffffffffu, i < D && flag[i] != 0);
+            m[j] = __ballot_sync(0xffffffffu, f[j] != 0);
             if (lane == 0) woff[j * 32 + warp] = __popc(m[j]);
         }
     }
@@ -350,6 +384,7 @@ __global__ void __launch_bounds__(1024) compact_ballot_kernel(const int* __restr
 // thread t scans a contiguous run, one block-wide exclusive scan, then writes.
 __global__ void __launch_bounds__(1024) compact_kernel(const int* __restrict__ flag, int D,
                                                        int* __restrict__ list, int* __restrict__ count) {
+    SG_PDL_ENTRY();
     __shared__ int wsum[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int per = (D + 1023) / 1024;
@@ -382,6 +417,7 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int* __restrict__ f
 
 // gate[U_P] x, split-K partials: gp[split][pos][n]
 __global__ void __launch_bounds__(kBThreads) gate_kernel(BatchArgs a) {
+    SG_PDL_ENTRY();
     extern __shared__ __align__(128) uint16_t smb[];
     const int np = *a.np;
     if (blockIdx.x * kBM >= np) return;
@@ -396,6 +432,7 @@ __global__ void __launch_bounds__(kBThreads) gate_kernel(BatchArgs a) {
 // g = sum of the splits in order; survivor bits = mask & (g > 0) (ffn_exec.hpp:200),
 // union flags, per-token |V|; G stored per neuron. One warp per neuron: lane n, n+32.
 __global__ void gate_epi_kernel(BatchArgs a) {
+    SG_PDL_ENTRY();
     const int np = *a.np;
     const int pos = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -425,6 +462,7 @@ __global__ void gate_epi_kernel(BatchArgs a) {
 
 // up[U_V] x, split-K partials: gp[split][pos][n] (the gate partials are consumed)
 __global__ void __launch_bounds__(kBThreads) up_kernel(BatchArgs a) {
+    SG_PDL_ENTRY();
     extern __shared__ __align__(128) uint16_t smb[];
     const int nv = *a.nv;
     if (blockIdx.x * kBM >= nv) return;
@@ -439,6 +477,7 @@ __global__ void __launch_bounds__(kBThreads) up_kernel(BatchArgs a) {
 // u = sum of the splits; z = gated(g, u) on survivor bits (ffn_exec.hpp:202-203,
 // :68-76), else +0 -> Z per (neuron, token) and Z hi/lo [n][pos] for the down GEMM
 __global__ void up_epi_kernel(BatchArgs a) {
+    SG_PDL_ENTRY();
     const int nv = *a.nv;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int pos = i / kMaxBatch, n = i - pos * kMaxBatch;
@@ -461,6 +500,7 @@ __global__ void up_epi_kernel(BatchArgs a) {
 
 // zero the Z hi/lo columns [nv, round_up(nv, 64)) so the last K chunk adds +0
 __global__ void zpad_kernel(BatchArgs a) {
+    SG_PDL_ENTRY();
     const int nv = *a.nv;
     const int padto = (nv + kBK - 1) / kBK * kBK;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -473,6 +513,7 @@ __global__ void zpad_kernel(BatchArgs a) {
 
 // Y partials: Yp[split][n][m] = sum over survivor positions of split of down[.][m] z
 __global__ void __launch_bounds__(kBThreads) down_kernel(BatchArgs a) {
+    SG_PDL_ENTRY();
     extern __shared__ __align__(128) uint16_t smb[];
     const int nv = *a.nv;
     const int chunks = (nv + kBK - 1) / kBK;
@@ -496,6 +537,7 @@ __global__ void __launch_bounds__(kBThreads) down_kernel(BatchArgs a) {
 }
 
 __global__ void y_reduce_kernel(BatchArgs a, float* __restrict__ y) {
+    SG_PDL_ENTRY();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.B * a.d) return;
     const int n = i / a.d, m = i - n * a.d;
@@ -528,6 +570,7 @@ constexpr int down_rows_smem() {
 }
 template <int TB>
 __global__ void __launch_bounds__(512) down_rows_kernel(BatchArgs a, int ncg, int nrg) {
+    SG_PDL_ENTRY();
     constexpr int CP = 64 / TB;            // columns per thread
     constexpr int T = kDrCols / CP;        // threads per row piece
     constexpr int RL = 512 / T;            // row lanes
@@ -653,6 +696,7 @@ __global__ void __launch_bounds__(512) rows_dot_kernel(BatchArgs a, const float*
                                                        const int* __restrict__ rows,
                                                        const int* __restrict__ count, int ncg,
                                                        int nrg) {
+    SG_PDL_ENTRY();
     constexpr int R = 32 / TB;  // rows per warp step: R x TB = 32 outputs
     extern __shared__ __align__(16) float4 xsm[];  // [TB][2][128]: chunk ch, half h
     const int cg = blockIdx.x % ncg, rg = blockIdx.x / ncg;
@@ -733,6 +777,7 @@ __global__ void __launch_bounds__(512) rows_dot_kernel(BatchArgs a, const float*
 
 template <int TB>
 __global__ void y_rows_reduce_kernel(BatchArgs a, int nrg, float* __restrict__ y) {
+    SG_PDL_ENTRY();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.B * a.d) return;
     const int n = i / a.d, m = i - n * a.d;
@@ -742,6 +787,33 @@ __global__ void y_rows_reduce_kernel(BatchArgs a, int nrg, float* __restrict__ y
 }
 
 int gemm_smem(bool trans, int nb, int stages) { return stages * stage_elems(trans, nb) * 2; }
+
+// Launch with programmatic stream serialization when SG_PDL=1. Off by default:
+// measured on B200 (8-layer 7B stack in a CUDA graph, tokens/s, PDL vs plain):
+// B = 5 6587 / 6514, 8 9714 / 9799, 16 12218 / 12318, 32 19942 / 20547,
+// 64 35072 / 35131 (tools/pdl_ab.sh). griddepcontrol.wait is a no-op in a
+// kernel launched without the attribute.
+bool pdl_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("SG_PDL");
+        return e && std::atoi(e) != 0;
+    }();
+    return v;
+}
+template <typename... KArgs, typename... Args>
+void launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
 
 }  // namespace
 
@@ -762,24 +834,22 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
                              gemm_smem(true, kMaxBatch, kStages));
         attr = true;
     }
-    cudaMemsetAsync(a.pcount, 0, sizeof(int) * kMaxBatch, st);
-    cudaMemsetAsync(a.vcount, 0, sizeof(int) * kMaxBatch, st);
-    cudaMemsetAsync(a.vflag, 0, sizeof(int) * a.D, st);
-    cudaMemsetAsync(a.vbits, 0, sizeof(uint64_t) * a.D, st);
     {
-        const int n = a.nb * a.pitch_d;
-        split_x_kernel<<<(n + 255) / 256, 256, 0, st>>>(xs, a.B, a.d, a.nb, a.pitch_d, a.xh, a.xl);
+        int n = a.nb * a.pitch_d;
+        if (n < a.D) n = a.D;
+        if (n < kMaxBatch) n = kMaxBatch;
+        launch(split_x_kernel, (n + 255) / 256, 256, 0, st, xs, a.B, a.d, a.nb, a.pitch_d, a.xh, a.xl, a);
     }
-    t_kernel<<<dim3((a.r + kBM - 1) / kBM, a.tsplit), kBThreads, sm_rows, st>>>(a);
+    launch(t_kernel, dim3((a.r + kBM - 1) / kBM, a.tsplit), kBThreads, sm_rows, st, a);
     {
         const int n = a.nb * a.pitch_r;
-        t_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(a);
+        launch(t_reduce_kernel, (n + 255) / 256, 256, 0, st, a);
     }
-    mask_kernel<<<(a.D + kBM - 1) / kBM, kBThreads, sm_rows, st>>>(a);
+    launch(mask_kernel, (a.D + kBM - 1) / kBM, kBThreads, sm_rows, st, a);
     if (a.D <= kCompactPer * 1024)
-        compact_ballot_kernel<<<1, 1024, 0, st>>>(a.uflag, a.D, a.plist, a.np);
+        launch(compact_ballot_kernel, 1, 1024, 0, st, a.uflag, a.D, a.plist, a.np);
     else
-        compact_kernel<<<1, 1024, 0, st>>>(a.uflag, a.D, a.plist, a.np);
+        launch(compact_kernel, 1, 1024, 0, st, a.uflag, a.D, a.plist, a.np);
     // small batches: gate / up row pieces streamed on the CUDA cores (x exact fp32,
     // one partial per column group); larger: the tensor-core GEMM tiles, split-K
     const int ncg = (a.pitch_d + kDrCols - 1) / kDrCols;
@@ -796,22 +866,22 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
         }
         a.gsplit = ncg;
         auto k = dtb == 8 ? rows_dot_kernel<8> : rows_dot_kernel<16>;
-        k<<<dgrid, 512, dsm, st>>>(a, xs, a.gate, a.pitch_d, a.plist, a.np, ncg, dgrid / ncg);
+        launch(k, dgrid, 512, dsm, st, a, xs, a.gate, a.pitch_d, a.plist, a.np, ncg, dgrid / ncg);
     } else {
-        gate_kernel<<<dim3((a.D + kBM - 1) / kBM, a.gsplit), kBThreads, sm_rows, st>>>(a);
+        launch(gate_kernel, dim3((a.D + kBM - 1) / kBM, a.gsplit), kBThreads, sm_rows, st, a);
     }
-    gate_epi_kernel<<<(a.D + 7) / 8, 256, 0, st>>>(a);
+    launch(gate_epi_kernel, (a.D + 7) / 8, 256, 0, st, a);
     if (a.D <= kCompactPer * 1024)
-        compact_ballot_kernel<<<1, 1024, 0, st>>>(a.vflag, a.D, a.vlist, a.nv);
+        launch(compact_ballot_kernel, 1, 1024, 0, st, a.vflag, a.D, a.vlist, a.nv);
     else
-        compact_kernel<<<1, 1024, 0, st>>>(a.vflag, a.D, a.vlist, a.nv);
+        launch(compact_kernel, 1, 1024, 0, st, a.vflag, a.D, a.vlist, a.nv);
     if (dot_rows) {
         auto k = dtb == 8 ? rows_dot_kernel<8> : rows_dot_kernel<16>;
-        k<<<dgrid, 512, dsm, st>>>(a, xs, a.ud, 2 * a.pitch_d, a.vlist, a.nv, ncg, dgrid / ncg);
+        launch(k, dgrid, 512, dsm, st, a, xs, a.ud, 2 * a.pitch_d, a.vlist, a.nv, ncg, dgrid / ncg);
     } else {
-        up_kernel<<<dim3((a.D + kBM - 1) / kBM, a.gsplit), kBThreads, sm_rows, st>>>(a);
+        launch(up_kernel, dim3((a.D + kBM - 1) / kBM, a.gsplit), kBThreads, sm_rows, st, a);
     }
-    up_epi_kernel<<<(a.D * kMaxBatch + 255) / 256, 256, 0, st>>>(a);
+    launch(up_epi_kernel, (a.D * kMaxBatch + 255) / 256, 256, 0, st, a);
     // small batches: whole-row-piece streaming on the CUDA cores (partials reuse gp,
     // free after up_epi); larger: the tensor-core GEMM over Z hi/lo
     const int tb = a.nb <= 8 ? 8 : 16;
@@ -832,19 +902,19 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
         }
         const int n = a.B * a.d;
         if (tb == 8) {
-            down_rows_kernel<8><<<ncg * nrg, 512, smem, st>>>(a, ncg, nrg);
-            y_rows_reduce_kernel<8><<<(n + 255) / 256, 256, 0, st>>>(a, nrg, ys);
+            launch(down_rows_kernel<8>, ncg * nrg, 512, smem, st, a, ncg, nrg);
+            launch(y_rows_reduce_kernel<8>, (n + 255) / 256, 256, 0, st, a, nrg, ys);
         } else {
-            down_rows_kernel<16><<<ncg * nrg, 512, smem, st>>>(a, ncg, nrg);
-            y_rows_reduce_kernel<16><<<(n + 255) / 256, 256, 0, st>>>(a, nrg, ys);
+            launch(down_rows_kernel<16>, ncg * nrg, 512, smem, st, a, ncg, nrg);
+            launch(y_rows_reduce_kernel<16>, (n + 255) / 256, 256, 0, st, a, nrg, ys);
         }
         return static_cast<int>(cudaGetLastError());
     }
-    zpad_kernel<<<(kBK * kMaxBatch + 255) / 256, 256, 0, st>>>(a);
-    down_kernel<<<dim3((a.pitch_d + kBM - 1) / kBM, a.dsplit), kBThreads, sm_down, st>>>(a);
+    launch(zpad_kernel, (kBK * kMaxBatch + 255) / 256, 256, 0, st, a);
+    launch(down_kernel, dim3((a.pitch_d + kBM - 1) / kBM, a.dsplit), kBThreads, sm_down, st, a);
     {
         const int n = a.B * a.d;
-        y_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(a, ys);
+        launch(y_reduce_kernel, (n + 255) / 256, 256, 0, st, a, ys);
     }
     return static_cast<int>(cudaGetLastError());
 }

@@ -17,7 +17,7 @@ from test_gpu_scale import _host_q
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("B", [1, 3, 7, 8, 12, 16, 17, 64])
+@pytest.mark.parametrize("B", [1, 3, 4, 5, 7, 8, 12, 16, 17, 64])
 def test_batch_tokens_match_single_token_oracle(B):
     d, D, r = 512, 2048, 64
     fx, pred = _calibrated_layer(d, D, r, seed=9, calib=1024)
