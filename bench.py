@@ -30,6 +30,17 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 
+
+def batch_launches_per_layer(B):
+    """Kernels one sg_ffn_forward_batch call launches (sg_batch.cu launch_batch)."""
+    if B <= int(os.environ.get("SG_BATCH_STACK_MAX", "4")):
+        return 1
+    fuse = int(os.environ.get("SG_BATCH_FUSE", "0"))
+    n = 12 if B <= 16 else 13
+    n -= 1 if fuse & 1 else 0
+    n -= 1 if (fuse & 2) and B <= 16 else 0
+    return n
+
 def log(*a):
     print("[bench]", *a, file=sys.stderr, flush=True)
 
@@ -322,9 +333,10 @@ def run_batch(args, cfg, host, layers, ctx, world, rank, local):
         "e2e": {"value": B * 1000.0 / ms_e2e, "unit": "tokens/s", "h2d_bytes_per_step": L * B * d * 4,
                 "d2h_bytes_per_step": L * B * d * 4, "ms_per_step": ms_e2e},
         # per layer: B <= SG_BATCH_STACK_MAX (4): one persistent stack launch; nb <= 16:
-        # 12 kernels (CUDA-core gate / up / down row streaming); above: 13 (GEMM tiles)
-        "gpu_launches": args.steps * L * (1 if B <= int(os.environ.get("SG_BATCH_STACK_MAX", "4"))
-                                          else 12 if B <= 16 else 13),
+        # 12 kernels (CUDA-core gate / up / down row streaming) minus the fused ones
+        # (SG_BATCH_FUSE bit 0: survivor compaction in gate_epi's last block; bit 1,
+        # nb <= 16 only: T reduced in t_kernel's last split block); above: 13 (GEMM tiles)
+        "gpu_launches": args.steps * L * batch_launches_per_layer(B),
         "clocks": clocks,
         "cpu_baseline": None,
     }

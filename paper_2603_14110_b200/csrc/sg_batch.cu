@@ -51,6 +51,7 @@ namespace {
 constexpr int kBM = 64;                  // rows per CTA tile
 constexpr int kBK = 32;                  // K per pipeline stage
 constexpr int kCh = kBK / 8;             // 16-B chunks per row per stage
+constexpr int kTickets = 16;  // ints at BatchArgs::ticket: [0] gate_epi, [1 + tile] t_kernel
 constexpr int kBWarps = 4;               // one m16 slice per warp
 constexpr int kBThreads = kBWarps * 32;
 constexpr int kRowPad = kBK + 8;         // smem row stride (bf16): conflict-free ldmatrix
@@ -262,7 +263,9 @@ __global__ void split_x_kernel(const float* __restrict__ x, int B, int d, int nb
 }
 
 // T partials: tp[split][j][n] over K slice `split`
-__global__ void __launch_bounds__(kBThreads) t_kernel(BatchArgs a) {
+// fuse != 0: the last of the tsplit blocks of a row tile sums its splits in
+// order into T hi/lo (what t_reduce_kernel does, one kernel boundary less)
+__global__ void __launch_bounds__(kBThreads) t_kernel(BatchArgs a, int fuse) {
     SG_PDL_ENTRY();
     extern __shared__ __align__(128) uint16_t smb[];
     float acc[kMaxBatch / 8][4];
@@ -271,6 +274,27 @@ __global__ void __launch_bounds__(kBThreads) t_kernel(BatchArgs a) {
     gemm_tile<false>(a.stages, a.Bm, a.pitch_d, nullptr, a.r, blockIdx.x * kBM, a.xh, a.xl, a.pitch_d, a.nb, k0,
                      k1, smb, acc);
     store_partial(acc, a.tp, a.pitch_r, blockIdx.y, blockIdx.x * kBM, a.r, a.nb);
+    if (!fuse) return;
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(a.ticket + 1 + blockIdx.x, 1) == static_cast<int>(gridDim.y) - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int m0 = blockIdx.x * kBM;
+    for (int o = threadIdx.x; o < kBM * a.nb; o += blockDim.x) {
+        const int n = o / kBM, j = m0 + o % kBM;
+        float s = 0.f;  // padding columns (r <= j < pitch_r = tiles * kBM) get +0
+        if (j < a.r)
+            for (int sp = 0; sp < a.tsplit; ++sp)
+            s += __ldcg(a.tp + (static_cast<size_t>(sp) * a.pitch_r + j) * kMaxBatch + n);
+        const __nv_bfloat16 h = __float2bfloat16_rn(s);
+        const __nv_bfloat16 l = __float2bfloat16_rn(s - __bfloat162float(h));
+        a.th[static_cast<size_t>(n) * a.pitch_r + j] = __bfloat16_as_ushort(h);
+        a.tl[static_cast<size_t>(n) * a.pitch_r + j] = __bfloat16_as_ushort(l);
+    }
+    if (threadIdx.x == 0) a.ticket[1 + blockIdx.x] = 0;
 }
 
 // T = sum of the splits in order -> bf16 hi/lo [nb][pitch_r]
@@ -327,10 +351,10 @@ __global__ void __launch_bounds__(kBThreads) mask_kernel(BatchArgs a) {
 // ballots it, one block-wide scan over the (j, warp) counts gives every warp's
 // output offset for every j, the flags stay in the ballot masks.
 constexpr int kCompactPer = 16;
-__global__ void __launch_bounds__(1024) compact_ballot_kernel(const int* __restrict__ flag, int D,
-                                                              int* __restrict__ list,
-                                                              int* __restrict__ count) {
-    SG_PDL_ENTRY();
+// one 1024-thread block; flags read through L2 (written by other blocks of the
+// calling kernel when fused into gate_epi)
+__device__ __forceinline__ void compact_ballot_block(const int* __restrict__ flag, int D,
+                                                     int* __restrict__ list, int* __restrict__ count) {
     __shared__ int woff[kCompactPer * 32];
     __shared__ int wsum[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -378,6 +402,12 @@ __global__ void __launch_bounds__(1024) compact_ballot_kernel(const int* __restr
 #pragma unroll
     for (int j = 0; j < kCompactPer; ++j)
         if (j < per && ((m[j] >> lane) & 1u)) list[woff[j * 32 + warp] + __popc(m[j] & below)] = j * 1024 + tid;
+}
+__global__ void __launch_bounds__(1024) compact_ballot_kernel(const int* __restrict__ flag, int D,
+                                                              int* __restrict__ list,
+                                                              int* __restrict__ count) {
+    SG_PDL_ENTRY();
+    compact_ballot_block(flag, D, list, count);
 }
 
 // ascending compaction of flags[0..D) into list, count into *count (one CTA):
@@ -431,12 +461,7 @@ __global__ void __launch_bounds__(kBThreads) gate_kernel(BatchArgs a) {
 
 // g = sum of the splits in order; survivor bits = mask & (g > 0) (ffn_exec.hpp:200),
 // union flags, per-token |V|; G stored per neuron. One warp per neuron: lane n, n+32.
-__global__ void gate_epi_kernel(BatchArgs a) {
-    SG_PDL_ENTRY();
-    const int np = *a.np;
-    const int pos = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (pos >= np) return;
+__device__ __forceinline__ void gate_epi_neuron(const BatchArgs& a, int pos, int lane) {
     const int nid = a.plist[pos];
     const uint64_t mb = a.mbits[nid];
     uint64_t bits = 0ull;
@@ -458,6 +483,26 @@ __global__ void gate_epi_kernel(BatchArgs a) {
     // per-token |V| (one neuron per warp: at most one atomic per token per neuron)
     if (lane < a.B && ((bits >> lane) & 1ull)) atomicAdd(a.vcount + lane, 1);
     if (lane + 32 < a.B && ((bits >> (lane + 32)) & 1ull)) atomicAdd(a.vcount + lane + 32, 1);
+}
+
+// fuse != 0 (1024-thread blocks): the last block to finish compacts the
+// survivor union (one kernel boundary less than a separate compaction launch)
+__global__ void __launch_bounds__(1024) gate_epi_kernel(BatchArgs a, int fuse) {
+    SG_PDL_ENTRY();
+    const int np = *a.np;
+    const int pos = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (pos < np) gate_epi_neuron(a, pos, lane);
+    if (!fuse) return;
+    __shared__ int last;
+    __threadfence();  // this block's vflag writes before its ticket
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(a.ticket, 1) == static_cast<int>(gridDim.x) - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    compact_ballot_block(a.vflag, a.D, a.vlist, a.nv);
+    if (threadIdx.x == 0) *a.ticket = 0;
 }
 
 // up[U_V] x, split-K partials: gp[split][pos][n] (the gate partials are consumed)
@@ -793,6 +838,19 @@ int gemm_smem(bool trans, int nb, int stages) { return stages * stage_elems(tran
 // B = 5 6587 / 6514, 8 9714 / 9799, 16 12218 / 12318, 32 19942 / 20547,
 // 64 35072 / 35131 (tools/pdl_ab.sh). griddepcontrol.wait is a no-op in a
 // kernel launched without the attribute.
+// SG_BATCH_FUSE bit 0: survivor compaction in gate_epi's last block; bit 1: T
+// reduced by t_kernel's last split block. Off by default: the serial last-block
+// work costs more than the kernel boundary it saves in a CUDA graph (B200, 7B
+// 8-layer stack, tokens/s for fuse 0 / 1 / 2 / 3: B = 5 6532 / 6340 / 6269 / 6100,
+// B = 8 9837 / 9564 / 9463 / 9220, B = 16 12300 / 12086 / 11313 / 11137;
+// tools/fuse_ab.sh).
+int fuse_mask() {
+    static const int v = [] {
+        const char* e = std::getenv("SG_BATCH_FUSE");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
 bool pdl_enabled() {
     static const bool v = [] {
         const char* e = std::getenv("SG_PDL");
@@ -840,10 +898,15 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
         if (n < kMaxBatch) n = kMaxBatch;
         launch(split_x_kernel, (n + 255) / 256, 256, 0, st, xs, a.B, a.d, a.nb, a.pitch_d, a.xh, a.xl, a);
     }
-    launch(t_kernel, dim3((a.r + kBM - 1) / kBM, a.tsplit), kBThreads, sm_rows, st, a);
     {
-        const int n = a.nb * a.pitch_r;
-        launch(t_reduce_kernel, (n + 255) / 256, 256, 0, st, a);
+        // small batches: T reduced by the last split block of each row tile
+        const int tiles = (a.r + kBM - 1) / kBM;
+        const int fuse = (fuse_mask() & 2) && a.nb <= 16 && tiles <= kTickets - 1;
+        launch(t_kernel, dim3(tiles, a.tsplit), kBThreads, sm_rows, st, a, fuse);
+        if (!fuse) {
+            const int n = a.nb * a.pitch_r;
+            launch(t_reduce_kernel, (n + 255) / 256, 256, 0, st, a);
+        }
     }
     launch(mask_kernel, (a.D + kBM - 1) / kBM, kBThreads, sm_rows, st, a);
     if (a.D <= kCompactPer * 1024)
@@ -870,11 +933,15 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
     } else {
         launch(gate_kernel, dim3((a.D + kBM - 1) / kBM, a.gsplit), kBThreads, sm_rows, st, a);
     }
-    launch(gate_epi_kernel, (a.D + 7) / 8, 256, 0, st, a);
-    if (a.D <= kCompactPer * 1024)
-        launch(compact_ballot_kernel, 1, 1024, 0, st, a.vflag, a.D, a.vlist, a.nv);
-    else
-        launch(compact_kernel, 1, 1024, 0, st, a.vflag, a.D, a.vlist, a.nv);
+    if (a.D <= kCompactPer * 1024 && (fuse_mask() & 1)) {
+        launch(gate_epi_kernel, (a.D + 31) / 32, 1024, 0, st, a, 1);
+    } else {
+        launch(gate_epi_kernel, (a.D + 7) / 8, 256, 0, st, a, 0);
+        if (a.D <= kCompactPer * 1024)
+            launch(compact_ballot_kernel, 1, 1024, 0, st, a.vflag, a.D, a.vlist, a.nv);
+        else
+            launch(compact_kernel, 1, 1024, 0, st, a.vflag, a.D, a.vlist, a.nv);
+    }
     if (dot_rows) {
         auto k = dtb == 8 ? rows_dot_kernel<8> : rows_dot_kernel<16>;
         launch(k, dgrid, 512, dsm, st, a, xs, a.ud, 2 * a.pitch_d, a.vlist, a.nv, ncg, dgrid / ncg);

@@ -679,7 +679,7 @@ sg_status batch_workspace(sg_ctx* C) {
                  o_G = take(Dm * M * 4), o_vb = take(Dm * 8), o_vf = take(Dm * 4), o_vc = take(M * 4),
                  o_vl = take(Dm * 4), o_nv = take(4), o_Z = take(Dm * M * 4), o_zh = take(M * pv * 2),
                  o_zl = take(M * pv * 2), o_yp = take(sg::kDpSplits * M * pd * 4), o_bx = take(M * pd * 4),
-                 o_by = take(M * pd * 4), o_gp = take(sg::kGpSplits * pv * M * 4);
+                 o_by = take(M * pd * 4), o_gp = take(sg::kGpSplits * pv * M * 4), o_tk = take(16 * 4);
     DeviceGuard dg(C->device);
     cudaError_t e = cudaMalloc(&C->bmem, off);
     if (e == cudaSuccess) e = cudaMemset(C->bmem, 0, off);
@@ -715,6 +715,7 @@ sg_status batch_workspace(sg_ctx* C) {
     a.vcount = reinterpret_cast<int*>(b + o_vc);
     a.vlist = reinterpret_cast<int*>(b + o_vl);
     a.nv = reinterpret_cast<int*>(b + o_nv);
+    a.ticket = reinterpret_cast<int*>(b + o_tk);
     a.Z = reinterpret_cast<float*>(b + o_Z);
     a.zh = reinterpret_cast<uint16_t*>(b + o_zh);
     a.zl = reinterpret_cast<uint16_t*>(b + o_zl);

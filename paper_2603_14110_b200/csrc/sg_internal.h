@@ -109,6 +109,8 @@ struct BatchArgs {
     int* vcount;             // [64] |V_b|
     int* vlist;              // [D]
     int* nv;
+    int* ticket;             // [16] blocks-done tickets: [0] gate_epi (its last block compacts V),
+                             // [1 + tile] t_kernel row tiles (the last split reduces T); reset to 0
     float* Z;                // [D][64] gated values
     uint16_t *zh, *zl;       // [64][pitch_v]
     float* yp;               // [dsplit][64][pitch_d]
