@@ -465,12 +465,25 @@ __device__ __forceinline__ void gate_epi_neuron(const BatchArgs& a, int pos, int
     const int nid = a.plist[pos];
     const uint64_t mb = a.mbits[nid];
     uint64_t bits = 0ull;
+    // all split partials in flight first, then summed in split order
+    float pg[2][kGpSplits];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int sp = 0; sp < kGpSplits; ++sp) {
+            const int n = lane + 32 * h;
+            pg[h][sp] = n < a.nb && sp < a.gsplit
+                            ? a.gp[(static_cast<size_t>(sp) * a.pitch_v + pos) * kMaxBatch + n]
+                            : 0.f;
+        }
+#pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int n = lane + 32 * h;
         if (n >= a.nb) continue;
         float g = 0.f;
-        for (int sp = 0; sp < a.gsplit; ++sp)
-            g += a.gp[(static_cast<size_t>(sp) * a.pitch_v + pos) * kMaxBatch + n];
+#pragma unroll
+        for (int sp = 0; sp < kGpSplits; ++sp)
+            if (sp < a.gsplit) g += pg[h][sp];
         a.G[static_cast<size_t>(nid) * kMaxBatch + n] = g;
         if (n < a.B && ((mb >> n) & 1ull) && g > 0.f) bits |= 1ull << n;
     }
@@ -530,10 +543,15 @@ __global__ void up_epi_kernel(BatchArgs a) {
     const int nid = a.vlist[pos];
     float z = 0.f;
     if (n < a.B && ((a.vbits[nid] >> n) & 1ull)) {
-        float u = 0.f;
-        for (int sp = 0; sp < a.gsplit; ++sp)
-            u += a.gp[(static_cast<size_t>(sp) * a.pitch_v + pos) * kMaxBatch + n];
+        float pu[kGpSplits];  // all split partials in flight first, summed in split order
+#pragma unroll
+        for (int sp = 0; sp < kGpSplits; ++sp)
+            pu[sp] = sp < a.gsplit ? a.gp[(static_cast<size_t>(sp) * a.pitch_v + pos) * kMaxBatch + n] : 0.f;
         const float g = a.G[static_cast<size_t>(nid) * kMaxBatch + n];
+        float u = 0.f;
+#pragma unroll
+        for (int sp = 0; sp < kGpSplits; ++sp)
+            if (sp < a.gsplit) u += pu[sp];
         z = (g > 0.f && (a.act == 0 || u > 0.f)) ? g * u : 0.f;
     }
     a.Z[static_cast<size_t>(nid) * kMaxBatch + n] = z;
