@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kBThreads) gate_kernel(BatchArgs a) {
 
 // g = sum of the splits in order; survivor bits = mask & (g > 0) (ffn_exec.hpp:200),
 // union flags, per-token |V|; G stored per neuron. One warp per neuron: lane n, n+32.
-__device__ __forceinline__ void gate_epi_neuron(const BatchArgs& a, int pos, int lane) {
+__device__ __forceinline__ void gate_epi_neuron(const BatchArgs& a, int pos, int lane, int* scnt) {
     const int nid = a.plist[pos];
     const uint64_t mb = a.mbits[nid];
     uint64_t bits = 0ull;
@@ -493,19 +493,26 @@ __device__ __forceinline__ void gate_epi_neuron(const BatchArgs& a, int pos, int
         a.vbits[nid] = bits;
         a.vflag[nid] = bits != 0ull;
     }
-    // per-token |V| (one neuron per warp: at most one atomic per token per neuron)
-    if (lane < a.B && ((bits >> lane) & 1ull)) atomicAdd(a.vcount + lane, 1);
-    if (lane + 32 < a.B && ((bits >> (lane + 32)) & 1ull)) atomicAdd(a.vcount + lane + 32, 1);
+    // per-token |V|: counted in the block's shared counters (integer, order-free);
+    // one global atomic per token per block (same-address global atomics from
+    // every warp left the kernel drain-stalled: 24 us at B = 64)
+    if (lane < a.B && ((bits >> lane) & 1ull)) atomicAdd(scnt + lane, 1);
+    if (lane + 32 < a.B && ((bits >> (lane + 32)) & 1ull)) atomicAdd(scnt + lane + 32, 1);
 }
 
-// fuse != 0 (1024-thread blocks): the last block to finish compacts the
+// 1024-thread blocks, one predicted neuron per warp. fuse != 0: the last block to finish compacts the
 // survivor union (one kernel boundary less than a separate compaction launch)
 __global__ void __launch_bounds__(1024) gate_epi_kernel(BatchArgs a, int fuse) {
     SG_PDL_ENTRY();
     const int np = *a.np;
     const int pos = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (pos < np) gate_epi_neuron(a, pos, lane);
+    __shared__ int scnt[kMaxBatch];
+    if (threadIdx.x < kMaxBatch) scnt[threadIdx.x] = 0;
+    __syncthreads();
+    if (pos < np) gate_epi_neuron(a, pos, lane, scnt);
+    __syncthreads();
+    if (threadIdx.x < a.B && scnt[threadIdx.x] != 0) atomicAdd(a.vcount + threadIdx.x, scnt[threadIdx.x]);
     if (!fuse) return;
     __shared__ int last;
     __threadfence();  // this block's vflag writes before its ticket
@@ -954,7 +961,7 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
     if (a.D <= kCompactPer * 1024 && (fuse_mask() & 1)) {
         launch(gate_epi_kernel, (a.D + 31) / 32, 1024, 0, st, a, 1);
     } else {
-        launch(gate_epi_kernel, (a.D + 7) / 8, 256, 0, st, a, 0);
+        launch(gate_epi_kernel, (a.D + 31) / 32, 1024, 0, st, a, 0);
         if (a.D <= kCompactPer * 1024)
             launch(compact_ballot_kernel, 1, 1024, 0, st, a.vflag, a.D, a.vlist, a.nv);
         else
