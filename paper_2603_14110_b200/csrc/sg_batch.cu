@@ -317,6 +317,9 @@ __global__ void t_reduce_kernel(BatchArgs a) {
 __global__ void __launch_bounds__(kBThreads) mask_kernel(BatchArgs a) {
     SG_PDL_ENTRY();
     extern __shared__ __align__(128) uint16_t smb[];
+    __shared__ int scnt[kMaxBatch];  // per-token |P| of this block's rows
+    for (int i = threadIdx.x; i < kMaxBatch; i += blockDim.x) scnt[i] = 0;
+    __syncthreads();
     float acc[kMaxBatch / 8][4];
     gemm_tile<false>(a.stages, a.A, a.pitch_r, nullptr, a.D, blockIdx.x * kBM, a.th, a.tl, a.pitch_r, a.nb, 0,
                      a.pitch_r, smb, acc);
@@ -343,7 +346,10 @@ __global__ void __launch_bounds__(kBThreads) mask_kernel(BatchArgs a) {
         }
         if ((lane & 3) != 0 || row >= a.D) bits[h] = 0ull;  // count each row once
     }
-    count_tokens(bits[0], bits[1], a.B, a.pcount);
+    count_tokens(bits[0], bits[1], a.B, scnt);
+    __syncthreads();
+    for (int n = threadIdx.x; n < a.B; n += blockDim.x)
+        if (scnt[n] != 0) atomicAdd(a.pcount + n, scnt[n]);
 }
 
 // ascending compaction of flags[0..D), D <= 16384, into list, count into *count
