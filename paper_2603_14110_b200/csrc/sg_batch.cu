@@ -547,12 +547,13 @@ __global__ void __launch_bounds__(kBThreads) up_kernel(BatchArgs a) {
 
 // u = sum of the splits; z = gated(g, u) on survivor bits (ffn_exec.hpp:202-203,
 // :68-76), else +0 -> Z per (neuron, token) and Z hi/lo [n][pos] for the down GEMM
-__global__ void up_epi_kernel(BatchArgs a) {
+// (split_z = 0: the row-streamed down projection reads Z only; no hi/lo copy)
+__global__ void up_epi_kernel(BatchArgs a, int split_z) {
     SG_PDL_ENTRY();
     const int nv = *a.nv;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int pos = i / kMaxBatch, n = i - pos * kMaxBatch;
-    if (pos >= nv || n >= a.nb) return;
+    const int pos = i / a.nb, n = i - pos * a.nb;
+    if (pos >= nv) return;
     const int nid = a.vlist[pos];
     float z = 0.f;
     if (n < a.B && ((a.vbits[nid] >> n) & 1ull)) {
@@ -568,6 +569,7 @@ __global__ void up_epi_kernel(BatchArgs a) {
         z = (g > 0.f && (a.act == 0 || u > 0.f)) ? g * u : 0.f;
     }
     a.Z[static_cast<size_t>(nid) * kMaxBatch + n] = z;
+    if (!split_z) return;
     const __nv_bfloat16 h = __float2bfloat16_rn(z);
     const __nv_bfloat16 l = __float2bfloat16_rn(z - __bfloat162float(h));
     a.zh[static_cast<size_t>(n) * a.pitch_v + pos] = __bfloat16_as_ushort(h);
@@ -979,7 +981,6 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
     } else {
         launch(up_kernel, dim3((a.D + kBM - 1) / kBM, a.gsplit), kBThreads, sm_rows, st, a);
     }
-    launch(up_epi_kernel, (a.D * kMaxBatch + 255) / 256, 256, 0, st, a);
     // small batches: whole-row-piece streaming on the CUDA cores (partials reuse gp,
     // free after up_epi); larger: the tensor-core GEMM over Z hi/lo
     const int tb = a.nb <= 8 ? 8 : 16;
@@ -988,6 +989,7 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
     if (static_cast<size_t>(nrg) * tb * a.pitch_d > cap)
         nrg = static_cast<int>(cap / (static_cast<size_t>(tb) * a.pitch_d));
     const bool rows_path = a.nb <= 16 && nrg >= 8;
+    launch(up_epi_kernel, (a.D * a.nb + 255) / 256, 256, 0, st, a, rows_path ? 0 : 1);
     if (rows_path) {
         const int smem = tb == 8 ? down_rows_smem<8>() : down_rows_smem<16>();
         static bool rattr = false;
