@@ -31,6 +31,17 @@ sys.path.insert(0, ROOT)
 
 
 
+# BASELINE.json configs (the shapes of paper_2603_14110_b200.model.CONFIGS, repeated here so
+# the reference arm never imports this repo's package)
+SHAPES = {
+    "1layer": dict(d=4096, D=11008, L=1, act=0, model="single ReGLU FFN layer d=4096 d_ff=11008"),
+    "7b": dict(d=4096, D=11008, L=32, act=0, model="ProSparse-Llama2-7B FFN stack"),
+    "mistral": dict(d=4096, D=14336, L=32, act=1, model="TurboSparse-Mistral-7B FFN stack (dReLU)"),
+    "13b": dict(d=5120, D=13824, L=40, act=0, model="ProSparse-Llama2-13B FFN stack"),
+    "tiny": dict(d=512, D=1408, L=4, act=0, model="tiny test stack"),
+}
+
+
 def batch_launches_per_layer(B):
     """Kernels one sg_ffn_forward_batch call launches (sg_batch.cu launch_batch)."""
     if B <= int(os.environ.get("SG_BATCH_STACK_MAX", "4")):
@@ -132,69 +143,103 @@ def cpu_model() -> str:
 # ---------------------------------------------------------------------------
 # reference arm: the reference's own executor headers (oracle/_ref) on host cores
 # ---------------------------------------------------------------------------
+def _ref_layer_inputs(d, D, seed, rank, sparsity, calib_tokens=256, eval_tokens=16):
+    """One layer of the bench workload built WITHOUT this repo's package (so nothing
+    of ours is loaded in the reference arm), by the recipe of model.build_host_layer:
+    weights from the reference's own make_synthetic_fixture (synthetic.hpp:80-108,
+    via oracle/_ref), a rank-r truncated SVD of W_gate by a seeded randomized range
+    finder (numpy; the reference's naive mode, factorization.hpp:93-144 with S = I),
+    and the bias from the reference's own damage-weighted greedy calibration
+    (calibration.hpp:61-205, via oracle/_ref) on the fixture's calibration tokens."""
+    import oracle as O
+    fx = O.ref_synthetic(d, D, calib_tokens, eval_tokens, 0.9, seed)
+    G = fx["gate"].astype(np.float32)
+    rng = np.random.default_rng(seed)
+    Q, _ = np.linalg.qr(G @ rng.standard_normal((d, rank + 8)).astype(np.float32))
+    Q, _ = np.linalg.qr(G.T @ Q)
+    Q, _ = np.linalg.qr(G @ Q)
+    Ub, sv, Vt = np.linalg.svd(Q.T @ G, full_matrices=False)
+    A = ((Q @ Ub[:, :rank]) * sv[None, :rank]).astype(np.float64)
+    B = Vt[:rank].astype(np.float64)
+    Xc = fx["calib"]
+    scores = A @ (B @ Xc)
+    gp, up = fx["gate"] @ Xc, fx["up"] @ Xc
+    inner = np.maximum(gp, 0) * up
+    weights = inner ** 2 * np.sum(fx["down"] ** 2, axis=0)[:, None]
+    bias, _, _ = O.ref_greedy_calibrate(scores, weights, 8, sparsity)
+    return fx["gate"], fx["up"], fx["down"], A, B, bias, np.ascontiguousarray(fx["eval"].T)
+
+
 def run_reference(args, world, rank):
+    """The reference's CPU executor (sparse_ffn_sequential, ffn_exec.hpp:183-218, f64 with
+    its per-call validation) on the bench workload: every one of the L layers of the
+    model is built (seeds 0..L-1, as our arm) and timed on its own eval tokens, tokens
+    in parallel over all host threads (parallel_for, tools/sparsegate_main.cpp:241-259).
+    A step is ntok tokens through all L layers; tokens/s = ntok / sum of layer times."""
     if rank != 0:
         return 0
+    import concurrent.futures as cf
+
     import oracle as O
-    from paper_2603_14110_b200 import bf16_to_f64
-    from paper_2603_14110_b200.model import CONFIGS, build_host_layer
 
-    cfg = CONFIGS[args.config]
+    cfg = SHAPES[args.config]
     d, D, L = cfg["d"], cfg["D"], cfg["L"]
-    kind = "reference" if O.ref_available() else "port"
-    h = build_host_layer(d, D, cfg["act"], seed=0, rank=args.rank, sparsity=args.sparsity)
-    gate = bf16_to_f64(h.gate)
-    up = bf16_to_f64(h.up)
-    down = np.ascontiguousarray(bf16_to_f64(h.down_t).T)  # reference layout d x D
-    A, B = bf16_to_f64(h.A), bf16_to_f64(h.B)
-    bias = h.bias.astype(np.float32).astype(np.float64)
-    if kind == "reference":
-        ref = O.RefLayer(gate, up, down, A, B, bias, activation=cfg["act"])
-        cores = int(O.ref().sgref_thread_budget())
-    else:
-        ref = None
-        cores = 1
-    ntok = max(1, min(cores, h.xs.shape[1]))
-    xs = np.ascontiguousarray(h.xs[:, :ntok].T)
-
-    def one_step():
-        if ref is not None:
-            _, st, el = ref.run(xs, pipeline=2)
-        else:
-            t0 = time.perf_counter()
-            for t in range(ntok):
-                O.sparse_ffn(gate, up, down, A, B, bias, xs[t])
-            el = time.perf_counter() - t0
-        return el
-
-    t_est = one_step()  # first warm-up step doubles as the cost estimate
-    budget = 120.0      # timed CPU work per run (each step is a bounded sample)
-    k = max(1, min(args.steps, int(budget / max(t_est, 1e-6))))
-    w = max(1, min(args.warmup, 1 + int(20.0 / max(t_est, 1e-6))))
-    for _ in range(w - 1):
-        one_step()
-    tot = sum(one_step() for _ in range(k))
-    per_token_layer = tot / (k * ntok)        # seconds of one token through one layer (amortised)
-    tok_s = 1.0 / (per_token_layer * L)       # decode tokens/s through the L-layer stack
+    if args.layers:
+        L = args.layers
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsgref.so not built"}))
+        return 0
+    cores = int(O.ref().sgref_thread_budget())
+    ntok = max(1, min(cores, 16))
+    k = max(1, min(args.steps, 3))
+    w = 1
+    t_build = time.time()
+    per_layer = []
+    with cf.ThreadPoolExecutor(max(1, min(8, (os.cpu_count() or 8) // 2))) as ex:
+        futs = [ex.submit(_ref_layer_inputs, d, D, l, args.rank, args.sparsity) for l in range(L)]
+        for l, f in enumerate(futs):
+            gate, up, down, A, B, bias, ev = f.result()
+            ref = O.RefLayer(gate, up, down, A, B, bias, activation=cfg["act"])
+            xs = np.ascontiguousarray(ev[:ntok])
+            for _ in range(w):
+                ref.run(xs, pipeline=2)
+            per_layer.append(sum(ref.run(xs, pipeline=2)[2] for _ in range(k)) / k)
+            del ref, gate, up, down
+    step_s = float(sum(per_layer))
+    tok_s = ntok / step_s
     line = {
         "impl": "reference", "metric": "sparse-FFN decode tokens/s", "value": tok_s,
         "unit": "tokens/s", "n_gpus": 0, "steps": k, "warmup": w,
         "steps_requested": args.steps, "warmup_requested": args.warmup,
-        "ms_per_step": 1000.0 / tok_s, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1000.0 * step_s / ntok, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg['model']}: {L} layers d={d} d_ff={D} r={args.rank} "
-                               f"s={args.sparsity} batch 1", "layers": L, "hidden": d, "inter": D},
-        "per_layer_us": per_token_layer * 1e6,
-        "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": kind,
+        "config": bench_config(cfg, args, L, 1),
+        "per_layer_us": 1e6 * step_s / (ntok * L),
+        "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "reference",
                          "cpu_model": cpu_model(),
-                         "sample": f"{k} steps x {ntok} eval tokens through layer 0 of {L} "
-                                   f"(reference sparse_ffn_sequential, f64, per-call validation, "
-                                   f"parallel_for over tokens); tokens/s = 1/(t_token_layer*{L})"},
+                         "sample": f"{ntok} tokens (eval tokens of each layer, in parallel over "
+                                   f"{cores} threads) through all {L} distinct layers, {k} timed "
+                                   f"run(s) per layer after {w} warm-up; reference "
+                                   f"sparse_ffn_sequential in f64 with its per-call validation; "
+                                   f"inputs built in {time.time() - t_build:.0f} s, untimed"},
         "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def bench_config(cfg, args, L, world):
+    """The `config` object of both arms (identical for the same command line)."""
+    d, D = cfg["d"], cfg["D"]
+    chain = getattr(args, "chain", 1)
+    return {"workload": f"{cfg['model']}: {L} layers d={d} d_ff={D} r={args.rank} "
+                        f"s={args.sparsity} natural sparsity 0.9, batch {max(1, args.batch)}, "
+                        f"sequential pipeline, {'chained' if chain else 'unchained'} decode",
+            "layers": L, "hidden": d, "inter": D, "rank": args.rank,
+            "predicted_sparsity_target": args.sparsity, "batch": max(1, args.batch),
+            "chained": bool(chain),
+            "parallelism": f"d_ff-shard{world}" if world > 1 else "none"}
 
 
 def cpu_baseline_for(cfg, host_layer0, args):
@@ -345,6 +390,40 @@ def run_batch(args, cfg, host, layers, ctx, world, rank, local):
     return 0
 
 
+def near_threshold(host, ys_gpu, xs_in, sets, act, eps=2.0 ** -14):
+    """Per-layer near-threshold diagnostics of the timed configuration:
+    the f64 pre-activations of the bf16 weights on the token each layer saw, the size
+    of the admissible band |pre| <= eps * sum|terms| (P) / |g| <= eps * sum|gate x| (V),
+    and how many GPU decisions differ from the f64 sign (all must lie in the band)."""
+    from paper_2603_14110_b200 import bf16_to_f64
+    out = []
+    for l, h in enumerate(host):
+        x = np.asarray(xs_in[l], dtype=np.float64)
+        A, B = bf16_to_f64(h.A), bf16_to_f64(h.B)
+        bias = h.bias.astype(np.float32).astype(np.float64)
+        t = B @ x
+        pre = A @ t + bias
+        sp = np.abs(A) @ np.abs(t) + np.abs(bias)
+        G = bf16_to_f64(h.gate)
+        g = G @ x
+        sg = np.abs(G) @ np.abs(x)
+        P_gpu, V_gpu = sets[l]
+        P_ref = np.flatnonzero(pre > 0)
+        band_p = np.abs(pre) <= eps * sp
+        band_v = np.abs(g) <= eps * sg
+        dP = np.setxor1d(P_ref, P_gpu)
+        V_exp = P_gpu[g[P_gpu] > 0] if len(P_gpu) else P_gpu
+        dV = np.setxor1d(V_exp, V_gpu)
+        out.append(dict(band_p=int(band_p.sum()), band_v=int(band_v.sum()), flips_p=int(len(dP)),
+                        flips_v=int(len(dV)), outside_band=int((~band_p[dP]).sum() + (~band_v[dV]).sum())))
+    return {"eps": eps, "layers": len(out),
+            "band_p_mean": float(np.mean([o["band_p"] for o in out])),
+            "band_v_mean": float(np.mean([o["band_v"] for o in out])),
+            "flips_p_total": int(sum(o["flips_p"] for o in out)),
+            "flips_v_total": int(sum(o["flips_v"] for o in out)),
+            "flips_outside_band": int(sum(o["outside_band"] for o in out))}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -355,9 +434,13 @@ def main():
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--rank", type=int, default=256)
     ap.add_argument("--sparsity", type=float, default=0.5)
+    ap.add_argument("--chain", type=int, default=1,
+                    help="1 (default): layer l+1 reads layer l's output (a real decode chain); "
+                         "0: every layer reads its own token (the unchained line is reported too)")
     ap.add_argument("--mode", default="stack", choices=["stack", "per-layer"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-diag", action="store_true", help="skip the near-threshold diagnostics")
     ap.add_argument("--no-balance", action="store_true",
                     help="ascending neuron layout instead of the load-balanced order")
     ap.add_argument("--hot-rows", type=int, default=16,
@@ -389,7 +472,7 @@ def main():
             dist.init_process_group(backend)
     from paper_2603_14110_b200 import _capi as capi
     from paper_2603_14110_b200.ffn_exec import Context, Pipeline, check
-    from paper_2603_14110_b200.model import CONFIGS, build_host_model, upload
+    from paper_2603_14110_b200.model import build_host_model, upload
 
     t0 = time.time()
     try:
@@ -402,86 +485,70 @@ def main():
                                  eval_tokens=max(16, args.batch))
     d, D, L = cfg["d"], cfg["D"], len(host)
     log(f"host model built in {time.time() - t0:.1f}s")
+    # configs[0] is ONE layer (~70 MB touched < 126 MB L2): the step rotates over 4
+    # device copies of it so every step streams its bytes from HBM
+    copies = 4 if L == 1 else 1
     layers = [upload(h, d, D, cfg["act"], args.rank, device=local, shard_index=rank,
                      shard_count=world, balance=not args.no_balance,
-                     hot_rows=args.hot_rows) for h in host]
+                     hot_rows=args.hot_rows) for h in host for _ in range(copies)]
+    host_l = [h for h in host for _ in range(copies)]
+    Ls = len(layers)  # layers per launch
     Dl = layers[0].local_inter
     ctx = Context(local, d, Dl, args.rank)
     lib = capi.lib()
     if args.batch > 0:
         return run_batch(args, cfg, host, layers, ctx, world, rank, local)
-    arr = (C.c_void_p * L)(*[l.handle.value for l in layers])
-    xs = torch.tensor(np.stack([h.x for h in host]), dtype=torch.float32, device="cuda")
+    arr = (C.c_void_p * Ls)(*[l.handle.value for l in layers])
+    xs = torch.tensor(np.stack([h.x for h in host_l]), dtype=torch.float32, device="cuda")
     ys = torch.zeros_like(xs)
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
+    chain = 0 if copies > 1 else args.chain  # rotated copies of one layer are independent
 
-    def step_stack(pipe=Pipeline.Sequential):
-        check(lib.sg_ffn_forward_layers(ctx.handle, arr, L, int(pipe), C.c_void_p(xs.data_ptr()),
-                                        C.c_void_p(ys.data_ptr()), 0, C.c_void_p(sh)))
+    def step_stack(pipe=Pipeline.Sequential, ch=None, s=None):
+        check(lib.sg_ffn_forward_layers(ctx.handle, arr, Ls, int(pipe), C.c_void_p(xs.data_ptr()),
+                                        C.c_void_p(ys.data_ptr()), chain if ch is None else ch,
+                                        C.c_void_p(sh if s is None else s)))
 
-    def step_layers(pipe=Pipeline.Sequential):
-        for l in range(L):
+    def step_layers(pipe=Pipeline.Sequential, s=None):
+        for l in range(Ls):
+            src = ys[l - 1] if (chain and l > 0) else xs[l]
             check(lib.sg_ffn_forward_device(ctx.handle, layers[l].handle, int(pipe),
-                                            C.c_void_p(xs[l].data_ptr()),
-                                            C.c_void_p(ys[l].data_ptr()), C.c_void_p(sh)))
+                                            C.c_void_p(src.data_ptr()),
+                                            C.c_void_p(ys[l].data_ptr()), C.c_void_p(sh if s is None else s)))
             if world > 1:
                 torch.distributed.all_reduce(ys[l])
 
     is_stack = args.mode == "stack" and world == 1
-    step = step_stack if is_stack else step_layers
-    launches_per_step = 1 if is_stack else L
+    launches_per_step = 1 if is_stack else Ls
+
+    def capture(fn):
+        """fn(stream handle) replayed as one CUDA graph (warm call first: attributes,
+        descriptor tables, NCCL communicator)."""
+        cs = torch.cuda.Stream()
+        with torch.cuda.stream(cs):
+            fn(cs.cuda_stream)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cs):
+            fn(torch.cuda.current_stream().cuda_stream)
+        return g
+
     graph_mode = "none"
-    if step is step_layers and not args.no_graph and os.environ.get("SG_BENCH_BACKEND", "nccl") == "nccl":
-        # per-layer launches (+ one NCCL all-reduce each) replayed as one CUDA graph
+    step = (lambda: step_stack()) if is_stack else (lambda: step_layers())
+    graphs = {}
+    if not args.no_graph and os.environ.get("SG_BENCH_BACKEND", "nccl") == "nccl":
         try:
-            capture_stream = torch.cuda.Stream()
-            with torch.cuda.stream(capture_stream):
-                step_layers()  # warm: attributes / NCCL communicator before capture
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=capture_stream):
-                for l in range(L):
-                    check(lib.sg_ffn_forward_device(
-                        ctx.handle, layers[l].handle, int(Pipeline.Sequential),
-                        C.c_void_p(xs[l].data_ptr()), C.c_void_p(ys[l].data_ptr()),
-                        C.c_void_p(torch.cuda.current_stream().cuda_stream)))
-                    if world > 1:
-                        torch.distributed.all_reduce(ys[l])
-            eager = step_layers
-
-            def step_graph(pipe=Pipeline.Sequential):
-                if pipe != Pipeline.Sequential:
-                    return eager(pipe)
-                g.replay()
-            step = step_graph
-            graph_mode = "per-layer launches captured in one CUDA graph"
+            if is_stack:
+                for ch in {chain, 0}:
+                    graphs[ch] = capture(lambda s, ch=ch: step_stack(ch=ch, s=s))
+                graph_mode = "stack launch captured in a CUDA graph"
+            else:
+                graphs[chain] = capture(lambda s: step_layers(s=s))
+                graph_mode = "per-layer launches captured in one CUDA graph"
+            step = graphs[chain].replay
         except Exception as e:  # report, keep eager
-            log(f"graph capture failed, eager per-layer launches: {e}")
-
-    if step is step_stack and not args.no_graph:
-        # the per-step stack launch (+ its stats memset) replayed as a CUDA graph
-        try:
-            capture_stream = torch.cuda.Stream()
-            with torch.cuda.stream(capture_stream):
-                step_stack()
-            torch.cuda.synchronize()
-            gs = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gs, stream=capture_stream):
-                check(lib.sg_ffn_forward_layers(
-                    ctx.handle, arr, L, int(Pipeline.Sequential), C.c_void_p(xs.data_ptr()),
-                    C.c_void_p(ys.data_ptr()), 0,
-                    C.c_void_p(torch.cuda.current_stream().cuda_stream)))
-            eager_stack = step_stack
-
-            def step_stack_graph(pipe=Pipeline.Sequential):
-                if pipe != Pipeline.Sequential:
-                    return eager_stack(pipe)
-                gs.replay()
-            step = step_stack_graph
-            graph_mode = "stack launch captured in a CUDA graph"
-        except Exception as e:  # report, keep eager
-            log(f"graph capture failed, eager stack launches: {e}")
+            log(f"graph capture failed, eager launches: {e}")
 
     def timed(fn, K, W, sample_clocks=False):
         for _ in range(W):
@@ -508,15 +575,37 @@ def main():
         return ms, clocks
 
     ms, clocks = timed(step, args.steps, args.warmup, sample_clocks=True)
+    unchained = None
+    if is_stack and chain and 0 in graphs:
+        ms_u, _ = timed(graphs[0].replay, max(10, args.steps // 2), args.warmup)
+        unchained = {"ms_per_step": ms_u, "tokens_per_s": 1000.0 / ms_u,
+                     "per_layer_us": ms_u * 1000.0 / Ls,
+                     "note": "every layer reads its own token: layer l+1's x loads overlap "
+                             "layer l's completion poll (not a real decode dependency)"}
 
-    # per-layer stats (p, v) of the tokens just timed (deterministic per layer)
-    stats = (capi.sg_exec_stats * L)()
+    # per-layer stats (p, v) and index sets of the configuration just timed
+    stats = (capi.sg_exec_stats * Ls)()
+    sets = None
     if is_stack:
-        check(lib.sg_ctx_read_stack_stats(ctx.handle, C.c_void_p(sh), L, stats))
+        if Ls <= 64 and not args.no_diag:
+            check(lib.sg_ctx_enable_stack_sets(ctx.handle, 1))
+        step_stack()
+        check(lib.sg_ctx_read_stack_stats(ctx.handle, C.c_void_p(sh), Ls, stats))
+        if Ls <= 64 and not args.no_diag:
+            sets = []
+            P = np.zeros(Dl, dtype=np.int32)
+            V = np.zeros(Dl, dtype=np.int32)
+            p, v = C.c_int64(0), C.c_int64(0)
+            for l in range(Ls):
+                check(lib.sg_ctx_read_stack_sets(ctx.handle, C.c_void_p(sh), l,
+                                                 P.ctypes.data_as(C.c_void_p), C.byref(p),
+                                                 V.ctypes.data_as(C.c_void_p), C.byref(v)))
+                sets.append((P[:p.value].astype(np.int64), V[:v.value].astype(np.int64)))
+            check(lib.sg_ctx_enable_stack_sets(ctx.handle, 0))
     else:
-        for l in range(L):
-            layers[l].forward_device(xs[l].data_ptr(), ys[l].data_ptr(), Pipeline.Sequential,
-                                     ctx, sh)
+        for l in range(Ls):
+            src = ys[l - 1] if (chain and l > 0) else xs[l]
+            layers[l].forward_device(src.data_ptr(), ys[l].data_ptr(), Pipeline.Sequential, ctx, sh)
             s1 = capi.sg_exec_stats()
             check(lib.sg_ctx_read_stats(ctx.handle, C.c_void_p(sh), C.byref(s1)))
             stats[l] = s1
@@ -526,16 +615,21 @@ def main():
     hbm, hbm_kind = peaks()
     per_launch_ms = ms / launches_per_step
     achieved = alg_bytes / launches_per_step / (per_launch_ms * 1e-3) / 1e9
+    diag = None
+    if sets is not None and world == 1 and Dl == D:
+        xin = [xs[0].double().cpu().numpy()] + \
+              [(ys[l - 1] if chain else xs[l]).double().cpu().numpy() for l in range(1, Ls)]
+        diag = near_threshold(host_l, None, xin, sets, cfg["act"])
 
     # e2e through the C ABI host entry: pinned x in, y out, synchronised per step
-    xh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
+    xh = torch.empty((Ls, d), dtype=torch.float32, pin_memory=True)
     xh.copy_(xs.cpu())
-    yh = torch.empty((L, d), dtype=torch.float32, pin_memory=True)
+    yh = torch.empty((Ls, d), dtype=torch.float32, pin_memory=True)
 
     def step_e2e():
-        check(lib.sg_ffn_forward_layers_host(ctx.handle, arr, L, int(Pipeline.Sequential),
+        check(lib.sg_ffn_forward_layers_host(ctx.handle, arr, Ls, int(Pipeline.Sequential),
                                              C.c_void_p(xh.data_ptr()), C.c_void_p(yh.data_ptr()),
-                                             0, None, C.c_void_p(sh)))
+                                             chain, None, C.c_void_p(sh)))
 
     def step_e2e_sharded():
         # same call shape with the per-layer NCCL exchange: pinned x in, full y out
@@ -546,8 +640,10 @@ def main():
 
     ke = max(10, min(args.steps, 500))
     ms_e2e, _ = timed(step_e2e if world == 1 else step_e2e_sharded, ke, 3)
-    e2e = {"value": 1000.0 / ms_e2e, "unit": "tokens/s", "h2d_bytes_per_step": L * d * 4,
-           "d2h_bytes_per_step": L * d * 4, "ms_per_step": ms_e2e, "steps": ke,
+    h2d = (d if chain else Ls * d) * 4
+    e2e = {"value": 1000.0 * copies / ms_e2e if copies > 1 else 1000.0 / ms_e2e, "unit": "tokens/s",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": Ls * d * 4, "ms_per_step": ms_e2e,
+           "steps": ke,
            "call": "sg_ffn_forward_layers_host" if world == 1 else
                    "H2D + per-layer sg_ffn_forward_device + NCCL all_reduce + D2H"}
 
@@ -555,9 +651,9 @@ def main():
     if not args.no_dense:
         ms_dense, _ = timed(lambda: step_stack(Pipeline.Dense) if is_stack else
                             step_layers(Pipeline.Dense), max(10, args.steps // 4), 3)
-        dense = {"ms_per_step": ms_dense, "tokens_per_s": 1000.0 / ms_dense,
-                 "per_layer_us": ms_dense * 1000.0 / L,
-                 "achieved_gbs": dense_bytes(d, Dl) * L / (ms_dense * 1e-3) / 1e9,
+        dense = {"ms_per_step": ms_dense, "tokens_per_s": 1000.0 * (copies if copies > 1 else 1) / ms_dense,
+                 "per_layer_us": ms_dense * 1000.0 / Ls,
+                 "achieved_gbs": dense_bytes(d, Dl) * Ls / (ms_dense * 1e-3) / 1e9,
                  "sparse_speedup": ms_dense / ms}
 
     traffic = None
@@ -568,7 +664,7 @@ def main():
                 tj = json.load(f)
             meta = tj.get("_meta", {}).get(args.config)
             if meta and Dl == D:  # ncu DRAM bytes per layer x layers per launch of this run
-                traffic = meta["per_layer"] * (L / launches_per_step)
+                traffic = meta["per_layer"] * (Ls / launches_per_step)
         except Exception:
             traffic = None
 
@@ -580,26 +676,28 @@ def main():
             cpu = {"value": None, "error": str(e)[:200]}
 
     if rank == 0:
-        tok_s = 1000.0 / ms
+        # tokens/s: one decode token through the L-layer model per step (for configs[0],
+        # 4 rotated copies of the one layer per launch = 4 tokens)
+        tok_s = 1000.0 * copies / ms if copies > 1 else 1000.0 / ms
+        conf = bench_config(cfg, args, L, world)
+        conf.update({
+            "l2": ("no flush: each step streams %.2f GB of distinct layers (> 126 MB L2)" % (alg_bytes / 1e9))
+                  if copies == 1 else
+                  "no flush: each launch rotates over 4 device copies of the layer "
+                  "(%.0f MB touched > 126 MB L2)" % (alg_bytes / 1e6),
+            "predictor": "naive-mode randomized rank-r SVD + greedy calibration (eta 8)",
+            "layout": "ascending" if args.no_balance else
+                      "per-CTA load-balanced neuron order from calibration statistics",
+            "hot_rows": 0 if args.no_balance else args.hot_rows,
+            "mode": "stack (one persistent launch per step)" if is_stack else "per-layer launches",
+            "graph": graph_mode})
         line = {
             "metric": "sparse-FFN decode tokens/s", "value": tok_s, "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{cfg['model']}: {L} layers d={d} d_ff={D} r={args.rank} "
-                                   f"s={args.sparsity} natural sparsity 0.9, batch 1, sequential "
-                                   f"pipeline", "layers": L, "hidden": d, "inter": D,
-                       "rank": args.rank, "predicted_sparsity_target": args.sparsity,
-                       "batch": 1, "parallelism": f"d_ff-shard{world}" if world > 1 else "none",
-                       "l2": "no flush: each step streams %.2f GB of distinct layers (> 126 MB L2)"
-                             % (alg_bytes / 1e9),
-                       "predictor": "naive-mode randomized rank-r SVD + greedy calibration (eta 8)",
-                       "layout": "ascending" if args.no_balance else
-                                 "per-CTA load-balanced neuron order from calibration statistics",
-                       "hot_rows": 0 if args.no_balance else args.hot_rows,
-                       "mode": "stack (one persistent launch per step)" if is_stack
-                               else "per-layer launches", "graph": graph_mode},
-            "per_layer_us": ms * 1000.0 / L,
+            "config": conf,
+            "per_layer_us": ms * 1000.0 / Ls,
             "p_mean": float(np.mean(ps)), "v_mean": float(np.mean(vs)),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "peak_kind": hbm_kind,
@@ -607,6 +705,8 @@ def main():
                          "traffic": traffic,
                          "bytes_per_launch": alg_bytes / launches_per_step,
                          "kernel": "ffn_kernel<2> (sequential executor)"},
+            "unchained": unchained,
+            "near_threshold": diag,
             "dense": dense,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -186,6 +186,16 @@ sg_status sg_ffn_forward_layers_host(sg_ctx* ctx, const sg_layer* const* layers,
 /* Synchronises, then returns per-layer stats of the last sg_ffn_forward_layers* call. */
 sg_status sg_ctx_read_stack_stats(sg_ctx* ctx, void* stream, int32_t n, sg_exec_stats* stats);
 
+/* Per-layer index sets of stack calls (diagnostics / parity): with enable != 0,
+ * every later sg_ffn_forward_layers* call of at most 64 layers also records, per
+ * local neuron, bit l = "predicted active in layer l" and "survivor in layer l"
+ * (integer atomics; the computed outputs are unchanged). sg_ctx_read_stack_sets
+ * synchronises and returns layer `layer`'s P and V of the last such call as
+ * ascending GLOBAL indices (capacity >= local inter each; either may be NULL). */
+sg_status sg_ctx_enable_stack_sets(sg_ctx* ctx, int32_t enable);
+sg_status sg_ctx_read_stack_sets(sg_ctx* ctx, void* stream, int32_t layer, int32_t* P, int64_t* p,
+                                 int32_t* V, int64_t* v);
+
 /* Batched decode (BASELINE.json configs[4]): `batch` (1..64) tokens through one
  * layer, sequential pipeline. Each token gets exactly its own single-token
  * result (its P_b, V_b, y_b, ExecStats); the batch reads each gate row of the

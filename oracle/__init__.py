@@ -268,6 +268,22 @@ def ref_synthetic(hidden, inter, calib_tokens=512, eval_tokens=128, natural_spar
     return out
 
 
+def ref_greedy_calibrate(scores, weights, eta, target):
+    """calibration.hpp:61-96 + :128-205 through the reference's own code: bias (D,),
+    achieved sparsity, total damage."""
+    scores, weights = _c(scores), _c(weights)
+    D, T = scores.shape
+    bias = np.zeros(D)
+    ach, dmg = C.c_double(0), C.c_double(0)
+    R = ref()
+    R.sgref_greedy_calibrate.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                                         C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]
+    _check(R.sgref_greedy_calibrate(_p(scores), _p(weights), C.c_int64(D), C.c_int64(T),
+                                    C.c_int(eta), C.c_double(target), _p(bias), C.byref(ach),
+                                    C.byref(dmg)), R)
+    return bias, ach.value, dmg.value
+
+
 def ref_dense_ffn(gate, up, down, x, activation=0):
     gate, up, down, x = map(_c, (gate, up, down, x))
     D, d = gate.shape

@@ -11,6 +11,7 @@
 // (3) the `cpu_baseline` / `--impl reference` legs of bench.py (kind
 // "reference"), timed with the reference's own parallel_for over tokens
 // (parallel.hpp:26-50, as cmd_run does at tools/sparsegate_main.cpp:241).
+#include "sparsegate/calibration.hpp"
 #include "sparsegate/ffn_exec.hpp"
 #include "sparsegate/parallel.hpp"
 #include "sparsegate/synthetic.hpp"
@@ -128,6 +129,23 @@ double sgref_uniform(void* rng, double a, double b) {
 }
 
 double sgref_normal_quantile(double p) { return normal_quantile(p); }
+
+// calibration.hpp:61-96 + :128-205 — the reference's own build_instance +
+// greedy_calibrate on scores / weights (D x T row-major): bias[D], achieved
+// sparsity and total damage. Used to build the reference bench arm's inputs.
+int sgref_greedy_calibrate(const double* scores, const double* weights, std::int64_t D,
+                           std::int64_t T, int eta, double target, double* bias,
+                           double* achieved, double* damage) {
+    return guarded([&] {
+        Mat s(D, T), w(D, T);
+        std::memcpy(s.data(), scores, sizeof(double) * static_cast<std::size_t>(D * T));
+        std::memcpy(w.data(), weights, sizeof(double) * static_cast<std::size_t>(D * T));
+        const CalibResult r = greedy_calibrate(build_instance(s, w, eta), target);
+        for (std::int64_t i = 0; i < D; ++i) bias[i] = r.bias(i);
+        if (achieved) *achieved = r.achieved_sparsity;
+        if (damage) *damage = r.total_damage;
+    });
+}
 
 // synthetic.hpp:80-108. Outputs row-major: gate DxH, up DxH, down HxD,
 // calib H x calib_tokens, eval H x eval_tokens (any output may be NULL).

@@ -256,6 +256,7 @@ __global__ void split_x_kernel(const float* __restrict__ x, int B, int d, int nb
     if (i >= nb * pitch) return;
     const int n = i / pitch, k = i - n * pitch;
     const float v = (n < B && k < d) ? x[static_cast<size_t>(n) * d + k] : 0.f;
+    if (!isfinite(v)) atomicOr(a.bad, 1);  // check_input, ffn_exec.hpp:61-63
     const __nv_bfloat16 h = __float2bfloat16_rn(v);
     const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
     hi[i] = __bfloat16_as_ushort(h);
@@ -914,16 +915,14 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
     cudaStream_t st = static_cast<cudaStream_t>(stream_);
     BatchArgs a = a0;
     const int sm_rows = gemm_smem(false, a.nb, a.stages), sm_down = gemm_smem(true, a.nb, a.stages);
-    static bool attr = false;
-    if (!attr) {
+    {
         const int mx = gemm_smem(false, kMaxBatch, kStages);
-        cudaFuncSetAttribute(t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             gemm_smem(true, kMaxBatch, kStages));
-        attr = true;
+        int e = 0;
+        for (const void* k : {reinterpret_cast<const void*>(t_kernel), reinterpret_cast<const void*>(mask_kernel),
+                              reinterpret_cast<const void*>(gate_kernel), reinterpret_cast<const void*>(up_kernel)})
+            if (!e) e = ensure_smem_attr(k, mx);
+        if (!e) e = ensure_smem_attr(reinterpret_cast<const void*>(down_kernel), gemm_smem(true, kMaxBatch, kStages));
+        if (e) return e;
     }
     {
         int n = a.nb * a.pitch_d;
@@ -954,12 +953,9 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
     const int dgrid = ncg * (a.sms / ncg < 1 ? 1 : a.sms / ncg);
     const int dsm = dtb * 256 * 16;
     if (dot_rows) {
-        static bool dattr = false;
-        if (!dattr) {
-            cudaFuncSetAttribute(rows_dot_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 256 * 16);
-            cudaFuncSetAttribute(rows_dot_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 256 * 16);
-            dattr = true;
-        }
+        int e = ensure_smem_attr(reinterpret_cast<const void*>(rows_dot_kernel<8>), 16 * 256 * 16);
+        if (!e) e = ensure_smem_attr(reinterpret_cast<const void*>(rows_dot_kernel<16>), 16 * 256 * 16);
+        if (e) return e;
         a.gsplit = ncg;
         auto k = dtb == 8 ? rows_dot_kernel<8> : rows_dot_kernel<16>;
         launch(k, dgrid, 512, dsm, st, a, xs, a.gate, a.pitch_d, a.plist, a.np, ncg, dgrid / ncg);
@@ -992,14 +988,9 @@ int launch_batch(const BatchArgs& a0, const float* xs, float* ys, void* stream_)
     launch(up_epi_kernel, (a.D * a.nb + 255) / 256, 256, 0, st, a, rows_path ? 0 : 1);
     if (rows_path) {
         const int smem = tb == 8 ? down_rows_smem<8>() : down_rows_smem<16>();
-        static bool rattr = false;
-        if (!rattr) {
-            cudaFuncSetAttribute(down_rows_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 down_rows_smem<8>());
-            cudaFuncSetAttribute(down_rows_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 down_rows_smem<16>());
-            rattr = true;
-        }
+        int e = ensure_smem_attr(reinterpret_cast<const void*>(down_rows_kernel<8>), down_rows_smem<8>());
+        if (!e) e = ensure_smem_attr(reinterpret_cast<const void*>(down_rows_kernel<16>), down_rows_smem<16>());
+        if (e) return e;
         const int n = a.B * a.d;
         if (tb == 8) {
             launch(down_rows_kernel<8>, ncg * nrg, 512, smem, st, a, ncg, nrg);

@@ -22,6 +22,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <mutex>
 #include <limits>
 #include <numeric>
 #include <queue>
@@ -44,6 +46,7 @@ struct sg_layer {
     std::vector<int> gidx;  // local -> global when a layout order was given (else empty)
     sg::LayerView view{};
     sg::LayerView* repdev = nullptr;  // [64] copies of view: small batches as one stack launch
+    uint64_t id = 0;                  // unique per (layer, view contents): bumped by set_hot_rows
 };
 
 struct sg_ctx {
@@ -60,9 +63,13 @@ struct sg_ctx {
     float* ypin = nullptr;
     const sg_layer* last_layer = nullptr;
     int last_pipeline = 0;
-    sg::LayerView* stackdev = nullptr;
-    int stack_cap = 0;
+    // device descriptor tables, one per distinct stack (keyed by layer ids, never
+    // mutated or freed before the ctx: a captured CUDA graph may replay one)
+    std::map<std::vector<uint64_t>, sg::LayerView*> tables;
     std::vector<const sg_layer*> last_stack;
+    unsigned long long* sbits = nullptr;  // [2][max_D] per-layer P / V bits of stack calls
+    bool stack_sets = false;
+    bool last_stack_bits = false;          // the last stack call recorded them
     float* xsdev = nullptr;  // host-entry staging for stacks
     float* ysdev = nullptr;
     size_t xs_cap = 0;
@@ -83,6 +90,7 @@ constexpr int kMaxStackLayers = 1024;
 namespace {
 
 thread_local std::string g_err;
+std::atomic<uint64_t> g_layer_ids{1};
 
 sg_status fail(sg_status s, const std::string& msg) {
     g_err = msg;
@@ -286,31 +294,27 @@ sg_status stack_launch(sg_ctx* C, const sg_layer* const* layers, int32_t n,
         C->last_stack.clear();
         return SG_OK;
     }
-    if (C->stack_cap < n) {
-        C->last_stack.clear();
-        if (C->stackdev) cudaFree(C->stackdev);
-        C->stackdev = nullptr;
-        C->stack_cap = 0;
-        SG_CUDA(cudaMalloc(&C->stackdev, sizeof(sg::LayerView) * n));
-        C->stack_cap = n;
-    }
-    // The (tiny) descriptor table is uploaded only when the stack changes, so
-    // repeated calls — and CUDA-graph capture after a first warm call — issue
-    // nothing but the kernel launch.
-    const bool same = C->last_stack.size() == static_cast<size_t>(n) &&
-                      std::equal(C->last_stack.begin(), C->last_stack.end(), layers);
-    if (!same) {
+    // The (tiny) descriptor table of a stack is uploaded once per distinct stack
+    // (layer ids, not pointers: a freed and re-created layer at a recycled address
+    // gets a new id), so repeated calls — and CUDA-graph capture after a first
+    // warm call — issue nothing but the kernel launch.
+    std::vector<uint64_t> key(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) key[static_cast<size_t>(i)] = layers[i]->id;
+    sg::LayerView* table = nullptr;
+    if (auto it = C->tables.find(key); it != C->tables.end()) {
+        table = it->second;
+    } else {
         std::vector<sg::LayerView> views(n);
         for (int i = 0; i < n; ++i) views[i] = layers[i]->view;
-        SG_CUDA(cudaStreamSynchronize(st));
-        SG_CUDA(cudaMemcpy(C->stackdev, views.data(), sizeof(sg::LayerView) * n,
-                           cudaMemcpyHostToDevice));
+        SG_CUDA(cudaMalloc(&table, sizeof(sg::LayerView) * n));
+        SG_CUDA(cudaMemcpy(table, views.data(), sizeof(sg::LayerView) * n, cudaMemcpyHostToDevice));
+        C->tables.emplace(std::move(key), table);
     }
     SG_CUDA(cudaMemsetAsync(C->W.stats, 0, static_cast<size_t>(n) * 4 * sizeof(int), st));
     sg::WorkView W = work_for(C, xs, ys);
     W.mbits = mbits;
     W.vbits = vbits;
-    const int e = sg::launch_layers(C->stackdev, n, L0->view, W, xs, ys, chain,
+    const int e = sg::launch_layers(table, n, L0->view, W, xs, ys, chain,
                                     static_cast<int>(L0->d), pipeline, C->G, st);
     if (e != 0) return fail(SG_ERR_CUDA, std::string("launch: ") +
                                              cudaGetErrorString(static_cast<cudaError_t>(e)));
@@ -526,6 +530,20 @@ sg_status sg_layer_create(const sg_layer_desc* desc, sg_layer** out) {
     V.bias = reinterpret_cast<const float*>(static_cast<char*>(L->dmem) + bias_off);
     V.gidx = L->gidx.empty() ? nullptr
                              : reinterpret_cast<const int*>(static_cast<char*>(L->dmem) + gidx_off);
+    L->id = g_layer_ids.fetch_add(1);
+    if (has_w && has_pred) {
+        // 64 copies of the view: small batches run as one stack launch (token b =
+        // "layer" b); allocated here, never by a (possibly captured) forward call
+        std::vector<sg::LayerView> views(64, L->view);
+        e = cudaMalloc(&L->repdev, sizeof(sg::LayerView) * views.size());
+        if (e == cudaSuccess)
+            e = cudaMemcpy(L->repdev, views.data(), sizeof(sg::LayerView) * views.size(),
+                           cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            sg_layer_destroy(L);
+            return fail(SG_ERR_CUDA, std::string("layer upload: ") + cudaGetErrorString(e));
+        }
+    }
     *out = L;
     return SG_OK;
 }
@@ -546,10 +564,14 @@ int64_t sg_layer_device_bytes(const sg_layer* L) { return L ? static_cast<int64_
 sg_status sg_layer_set_hot_rows(sg_layer* L, int64_t rows) {
     if (L == nullptr || rows < 0) return fail(SG_ERR_USAGE, "sg_layer_set_hot_rows: bad arguments");
     L->view.hot = static_cast<int>(rows < L->D_local ? rows : L->D_local);
-    if (L->repdev) {  // stale copies of the view: rebuilt by the next small batch
+    L->id = g_layer_ids.fetch_add(1);  // stacks built from now on get a fresh descriptor table
+    if (L->repdev) {
+        // refreshed in place (synchronously): a graph captured earlier keeps a
+        // valid table; the hot prefix changes only when rows arrive, not results
         DeviceGuard dg(L->device);
-        cudaFree(L->repdev);
-        L->repdev = nullptr;
+        std::vector<sg::LayerView> views(64, L->view);
+        SG_CUDA(cudaMemcpy(L->repdev, views.data(), sizeof(sg::LayerView) * views.size(),
+                           cudaMemcpyHostToDevice));
     }
     return SG_OK;
 }
@@ -635,7 +657,8 @@ sg_status sg_ctx_destroy(sg_ctx* C) {
     if (C->dmem) cudaFree(C->dmem);
     if (C->xpin) cudaFreeHost(C->xpin);
     if (C->ypin) cudaFreeHost(C->ypin);
-    if (C->stackdev) cudaFree(C->stackdev);
+    for (auto& kv : C->tables) cudaFree(kv.second);
+    if (C->sbits) cudaFree(C->sbits);
     if (C->xsdev) cudaFree(C->xsdev);
     if (C->ysdev) cudaFree(C->ysdev);
     if (C->dbgdev) cudaFree(C->dbgdev);
@@ -679,7 +702,8 @@ sg_status batch_workspace(sg_ctx* C) {
                  o_G = take(Dm * M * 4), o_vb = take(Dm * 8), o_vf = take(Dm * 4), o_vc = take(M * 4),
                  o_vl = take(Dm * 4), o_nv = take(4), o_Z = take(Dm * M * 4), o_zh = take(M * pv * 2),
                  o_zl = take(M * pv * 2), o_yp = take(sg::kDpSplits * M * pd * 4), o_bx = take(M * pd * 4),
-                 o_by = take(M * pd * 4), o_gp = take(sg::kGpSplits * pv * M * 4), o_tk = take(16 * 4);
+                 o_by = take(M * pd * 4), o_gp = take(sg::kGpSplits * pv * M * 4), o_tk = take(16 * 4),
+                 o_bad = take(4);
     DeviceGuard dg(C->device);
     cudaError_t e = cudaMalloc(&C->bmem, off);
     if (e == cudaSuccess) e = cudaMemset(C->bmem, 0, off);
@@ -716,6 +740,7 @@ sg_status batch_workspace(sg_ctx* C) {
     a.vlist = reinterpret_cast<int*>(b + o_vl);
     a.nv = reinterpret_cast<int*>(b + o_nv);
     a.ticket = reinterpret_cast<int*>(b + o_tk);
+    a.bad = reinterpret_cast<int*>(b + o_bad);
     a.Z = reinterpret_cast<float*>(b + o_Z);
     a.zh = reinterpret_cast<uint16_t*>(b + o_zh);
     a.zl = reinterpret_cast<uint16_t*>(b + o_zl);
@@ -742,14 +767,6 @@ sg_status sg_ffn_forward_batch(sg_ctx* C, const sg_layer* L, const float* xs, in
         const size_t bits = static_cast<size_t>(L->D_local) * sizeof(uint64_t);
         SG_CUDA(cudaMemsetAsync(C->bw.mbits, 0, bits, st));
         SG_CUDA(cudaMemsetAsync(C->bw.vbits, 0, bits, st));
-        if (L->repdev == nullptr) {  // first small batch on this layer (not under capture)
-            sg::LayerView* dev = nullptr;
-            std::vector<sg::LayerView> views(64, L->view);
-            SG_CUDA(cudaMalloc(&dev, sizeof(sg::LayerView) * views.size()));
-            SG_CUDA(cudaMemcpy(dev, views.data(), sizeof(sg::LayerView) * views.size(),
-                               cudaMemcpyHostToDevice));
-            const_cast<sg_layer*>(L)->repdev = dev;
-        }
         std::vector<const sg_layer*> rep(static_cast<size_t>(batch), L);
         if (sg_status s = stack_launch(C, rep.data(), batch, SG_PIPELINE_SEQUENTIAL, xs, ys, 0, stream,
                                        reinterpret_cast<unsigned long long*>(C->bw.mbits),
@@ -794,6 +811,7 @@ sg_status sg_ffn_forward_batch(sg_ctx* C, const sg_layer* L, const float* xs, in
     a.bias = L->view.bias;
     a.gate = L->view.gate;
     a.ud = L->view.ud;
+    SG_CUDA(cudaMemsetAsync(a.bad, 0, sizeof(int), static_cast<cudaStream_t>(stream)));
     const int e = sg::launch_batch(a, xs, ys, stream);
     if (e != 0) return fail(SG_ERR_CUDA, std::string("batch launch: ") +
                                              cudaGetErrorString(static_cast<cudaError_t>(e)));
@@ -811,22 +829,28 @@ sg_status sg_ctx_read_batch(sg_ctx* C, void* stream, int32_t batch, sg_exec_stat
     SG_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
     const sg_layer* L = C->blast;
     int pc[64], vc[64];
+    bool bad = false;
     if (C->blast_stack) {
         std::vector<int> st4(static_cast<size_t>(batch) * 4);
         SG_CUDA(cudaMemcpy(st4.data(), C->W.stats, st4.size() * sizeof(int), cudaMemcpyDeviceToHost));
         for (int b = 0; b < batch; ++b) {
             pc[b] = st4[4 * b];
             vc[b] = st4[4 * b + 1];
+            bad |= st4[4 * b + 2] != 0;  // the device non-finite flag of token b
         }
     } else {
+        int flag = 0;
         SG_CUDA(cudaMemcpy(pc, C->bw.pcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
         SG_CUDA(cudaMemcpy(vc, C->bw.vcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
+        SG_CUDA(cudaMemcpy(&flag, C->bw.bad, sizeof(int), cudaMemcpyDeviceToHost));
+        bad = flag != 0;
     }
     for (int b = 0; stats && b < batch; ++b) stats[b] = make_stats(L, SG_PIPELINE_SEQUENTIAL, pc[b], vc[b]);
     if (pred_bits)
         SG_CUDA(cudaMemcpy(pred_bits, C->bw.mbits, sizeof(uint64_t) * L->D_local, cudaMemcpyDeviceToHost));
     if (surv_bits)
         SG_CUDA(cudaMemcpy(surv_bits, C->bw.vbits, sizeof(uint64_t) * L->D_local, cudaMemcpyDeviceToHost));
+    if (bad) return fail(SG_ERR_DATA, "ffn input has non-finite entries");  // ffn_exec.hpp:61-63
     return SG_OK;
 }
 
@@ -965,7 +989,54 @@ sg_status sg_ffn_forward(sg_ctx* C, const sg_layer* L, sg_pipeline pipeline, con
 sg_status sg_ffn_forward_layers(sg_ctx* C, const sg_layer* const* layers, int32_t n,
                                 sg_pipeline pipeline, const float* xs, float* ys, int32_t chain,
                                 void* stream) {
+    if (C != nullptr && C->stack_sets && n >= 1 && n <= 64 && pipeline != SG_PIPELINE_DENSE) {
+        DeviceGuard dg(C->device);
+        SG_CUDA(cudaMemsetAsync(C->sbits, 0, static_cast<size_t>(C->max_D) * 16,
+                                static_cast<cudaStream_t>(stream)));
+        const sg_status s = stack_launch(C, layers, n, pipeline, xs, ys, chain, stream, C->sbits,
+                                         C->sbits + C->max_D);
+        C->last_stack_bits = s == SG_OK;
+        return s;
+    }
+    if (C) C->last_stack_bits = false;
     return stack_launch(C, layers, n, pipeline, xs, ys, chain, stream, nullptr, nullptr);
+}
+
+sg_status sg_ctx_enable_stack_sets(sg_ctx* C, int32_t enable) {
+    if (C == nullptr) return fail(SG_ERR_USAGE, "null ctx");
+    DeviceGuard dg(C->device);
+    if (enable && C->sbits == nullptr)
+        SG_CUDA(cudaMalloc(&C->sbits, static_cast<size_t>(C->max_D) * 16));
+    C->stack_sets = enable != 0;
+    return SG_OK;
+}
+
+sg_status sg_ctx_read_stack_sets(sg_ctx* C, void* stream, int32_t layer, int32_t* P, int64_t* p,
+                                 int32_t* V, int64_t* v) {
+    if (C == nullptr || !C->last_stack_bits)
+        return fail(SG_ERR_USAGE, "no stack call recorded index sets on this ctx");
+    if (layer < 0 || static_cast<size_t>(layer) >= C->last_stack.size() || layer >= 64)
+        return fail(SG_ERR_USAGE, "layer out of range of the last stack call");
+    DeviceGuard dg(C->device);
+    SG_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    const sg_layer* L = C->last_stack[static_cast<size_t>(layer)];
+    const size_t Dl = static_cast<size_t>(L->D_local);
+    std::vector<unsigned long long> bits(2 * Dl);
+    SG_CUDA(cudaMemcpy(bits.data(), C->sbits, Dl * 8, cudaMemcpyDeviceToHost));
+    SG_CUDA(cudaMemcpy(bits.data() + Dl, C->sbits + C->max_D, Dl * 8, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> ps, vs;
+    for (size_t k = 0; k < Dl; ++k) {
+        const int32_t g = static_cast<int32_t>(local_to_global(L, static_cast<int64_t>(k)));
+        if ((bits[k] >> layer) & 1ull) ps.push_back(g);
+        if ((bits[Dl + k] >> layer) & 1ull) vs.push_back(g);
+    }
+    std::sort(ps.begin(), ps.end());
+    std::sort(vs.begin(), vs.end());
+    if (P) std::copy(ps.begin(), ps.end(), P);
+    if (V) std::copy(vs.begin(), vs.end(), V);
+    if (p) *p = static_cast<int64_t>(ps.size());
+    if (v) *v = static_cast<int64_t>(vs.size());
+    return SG_OK;
 }
 
 

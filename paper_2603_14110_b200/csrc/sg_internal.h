@@ -74,6 +74,8 @@ int launch_layers(const LayerView* layers_dev, int n, const LayerView& first, co
                   const float* xs, float* ys, int chain, int pitch_stride, int pipeline,
                   int num_ctas, void* stream);
 int query_launch_info(int device, LaunchInfo* info);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device), thread-safe.
+int ensure_smem_attr(const void* kernel, int smem);
 
 // Batched decode (sg_batch.cu): one layer, B <= batch_max() tokens.
 constexpr int kGpSplits = 8;  // capacity of BatchArgs::gp in split-K partials
@@ -115,6 +117,7 @@ struct BatchArgs {
     uint16_t *zh, *zl;       // [64][pitch_v]
     float* yp;               // [dsplit][64][pitch_d]
     float* gp;               // [gsplit][pitch_v][64] gate / up split-K partials
+    int* bad;                // [1] set when an input token has a non-finite entry
 };
 int batch_max();
 int launch_batch(const BatchArgs& a, const float* xs, float* ys, void* stream);

@@ -47,6 +47,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 
 namespace sg {
 namespace {
@@ -60,7 +63,6 @@ constexpr int kGroupWarps = 4;            // phase C: a row is reduced by a grou
 constexpr int kGroups = kWarps / kGroupWarps;
 constexpr int kGroupThreads = kGroupWarps * 32;
 constexpr int kXRegChunks = 4;            // x chunks per thread held in registers (pitch_d <= 4096)
-constexpr int kBatch = 8;                 // rows per transposed warp reduction (stage 4)
 constexpr int kSvChunk = 12;              // survivor [up | down] rows staged per round (stage 4/5a)
 constexpr int kSector = 8;                // ints per 32-B sector
 
@@ -821,6 +823,40 @@ __device__ __forceinline__ void group_dot(const uint16_t* const* rows, const XRe
     par ^= 1;
 }
 
+// group_dot with x read from shared memory (same chunk map, same fmaf order per
+// row — dot8 and dot8r are one chain — so the result is bitwise group_dot's);
+// used where the x registers would not fit next to other live state.
+template <int kRows>
+__device__ __forceinline__ void group_dot_xs(const uint16_t* const* rows, const float* xs, int nch,
+                                             int gt, int grp, float* red, int& par, float* out) {
+    float acc[kRows];
+#pragma unroll
+    for (int q = 0; q < kRows; ++q) acc[q] = 0.f;
+    for (int ch = gt; ch < nch; ch += kGroupThreads) {
+#pragma unroll
+        for (int q = 0; q < kRows; ++q)
+            acc[q] = dot8(*reinterpret_cast<const uint4*>(rows[q] + ch * 8), xs + ch * 8, acc[q]);
+    }
+    const int gw = gt >> 5, lane = gt & 31;
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1)
+#pragma unroll
+        for (int q = 0; q < kRows; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], m);
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < kRows; ++q) red[(par * kGroupWarps + gw) * 4 + q] = acc[q];
+    }
+    named_bar(1 + grp, kGroupThreads);
+#pragma unroll
+    for (int q = 0; q < kRows; ++q) {
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < kGroupWarps; ++w) s += red[(par * kGroupWarps + w) * 4 + q];
+        out[q] = s;
+    }
+    par ^= 1;
+}
+
 // ---------------------------------------------------------------------------
 // Phase C: gather-GEMV over this CTA's items through the cp.async.bulk ring.
 //   kPipe 2 (sequential): items = own predicted rows; slot = gate row.
@@ -986,11 +1022,11 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
 // survivors' [up | down] rows (16 KB each, contiguous, sent to L2 during the
 // gate stream) are bulk-copied into shared memory in groups of sv_chunk / 2,
 // alternating between two row buffers so one group lands while another is computed.
-// Thread t owns chunk t (and t + 512) of every row with x in registers: the
-// up rows of a chunk are dotted kBatch at a time (8 independent FMA chains,
-// one transposed warp butterfly, warps summed in order), warp 0 forms
-// z = gated(g, u) (ffn_exec.hpp:202-203, :68-76), and every thread adds z·down
-// for its chunk into its partial y, survivors in P order.
+// The up rows are dotted by the 4-warp groups with phase C's reduction (same
+// chunk map and order, x from shared memory), so u — and z, y — are bitwise
+// those of the dense and parallel pipelines; threads 0..m-1 form
+// z = gated(g, u) (ffn_exec.hpp:202-203, :68-76), and thread t adds z·down for
+// chunks t and t + 512 into its partial y, survivors in P order.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkView& W,
                                                 const Smem& sm, const SmemPlan& S, RunState& rs) {
@@ -1003,9 +1039,14 @@ __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkVi
     const int ch0 = tid, ch1 = tid + kCThreads;
     const bool comp = tid < kCThreads;
     const bool h0 = comp && ch0 < nch, h1 = comp && ch1 < nch;
-    float x0[8], x1[8], a0[8], a1[8];
-    load_x8(sm.xs, ch0, h0, x0);
-    load_x8(sm.xs, ch1, h1, x1);
+    // u = up·x with phase C's row reduction (group_dot: 4-warp groups, x chunks
+    // gt + 128k in registers), so u — and therefore z and y — are bitwise the
+    // same as in the dense / parallel pipelines (ffn_exec_tests.cpp:124-137, :171-192)
+    const int grp = warp / kGroupWarps, gt = tid % kGroupThreads;
+    float* gred = sm.reda + grp * (2 * kGroupWarps * 4);
+    int gpar = 0;
+    float* us = sm.reda + kGroups * 2 * kGroupWarps * 4;  // u of the group's rows
+    float a0[8], a1[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         a0[e] = 0.f;
@@ -1044,28 +1085,27 @@ __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkVi
         const uint8_t* rows = sm.big + static_cast<size_t>((g & 1) * half) * ud_bytes;
         mbar_wait(sm.full + kMaxSlots - 2 + (g & 1), static_cast<uint32_t>(bu[g & 1] + (g >> 1)) & 1u);
         __syncwarp();
-        float* red = sm.reda + (g & 1) * (kWarps * kBatch);
         if (comp) {
-            float part[kBatch];
-#pragma unroll
-            for (int j = 0; j < kBatch; ++j) {
-                part[j] = 0.f;
-                if (j < m) {
-                    const uint16_t* up = reinterpret_cast<const uint16_t*>(rows + static_cast<size_t>(j) * ud_bytes);
-                    float acc = 0.f;
-                    if (h0) acc = dot8r(*reinterpret_cast<const uint4*>(up + ch0 * 8), x0, acc);
-                    if (h1) acc = dot8r(*reinterpret_cast<const uint4*>(up + ch1 * 8), x1, acc);
-                    part[j] = acc;
+            // rows grp and grp + 4 of the group (m <= 8)
+            const int j0 = grp, j1 = grp + kGroups;
+            const uint16_t* rr[2] = {
+                reinterpret_cast<const uint16_t*>(rows + static_cast<size_t>(j0) * ud_bytes),
+                reinterpret_cast<const uint16_t*>(rows + static_cast<size_t>(j1) * ud_bytes)};
+            float o[2];
+            if (j1 < m) {
+                group_dot_xs<2>(rr, sm.xs, nch, gt, grp, gred, gpar, o);
+                if (gt == 0) {
+                    us[j0] = o[0];
+                    us[j1] = o[1];
                 }
+            } else if (j0 < m) {
+                group_dot_xs<1>(rr, sm.xs, nch, gt, grp, gred, gpar, o);
+                if (gt == 0) us[j0] = o[0];
             }
-            const float s = warp_sum8(part, lane);
-            if ((lane & 3) == 0)
-                red[warp * kBatch + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)] = s;
         }
         __syncthreads();
         if (tid < m) {
-            float u = 0.f;
-            for (int w = 0; w < kWarps; ++w) u += red[w * kBatch + tid];
+            const float u = us[tid];
             int2 e = sm.svl[r0 + tid];
             const float z = gated(__int_as_float(e.y), u, L.act);
             zs[tid] = z;
@@ -1078,6 +1118,7 @@ __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkVi
                 const uint16_t* dn =
                     reinterpret_cast<const uint16_t*>(rows + static_cast<size_t>(i) * ud_bytes) + L.pitch_d;
                 const float z = zs[i];
+                if (z == 0.f) continue;  // zero-z slots contribute nothing (ffn_exec.hpp:89-92)
                 if (h0) axpy8(*reinterpret_cast<const uint4*>(dn + ch0 * 8), z, a0);
                 if (h1) axpy8(*reinterpret_cast<const uint4*>(dn + ch1 * 8), z, a1);
             }
@@ -1123,7 +1164,7 @@ __device__ void partial_down(const LayerView& L, const WorkView& W, const Smem& 
     } else {
         cnt = sm.misc[1];
     }
-    constexpr int kU = kPipe == 0 ? 16 : 8;
+    constexpr int kU = 8;
     for (int ch = tid; tid < kCThreads && ch < nch; ch += kCThreads) {
         float acc[8];
 #pragma unroll
@@ -1150,8 +1191,11 @@ __device__ void partial_down(const LayerView& L, const WorkView& W, const Smem& 
                 w[u] = kk < cnt ? ldg_stream(col + static_cast<size_t>(n) * 2 * L.pitch_d)
                                 : make_uint4(0, 0, 0, 0);
             }
+            // zero-z slots (and the padding) contribute nothing, exactly as in
+            // survivor_updown, so all pipelines sum the same terms in one order
 #pragma unroll
-            for (int u = 0; u < kU; ++u) axpy8(w[u], z[u], acc);
+            for (int u = 0; u < kU; ++u)
+                if (z[u] != 0.f) axpy8(w[u], z[u], acc);
         }
         float4* dst = reinterpret_cast<float4*>(W.ypart + static_cast<size_t>(c) * L.pitch_d + ch * 8);
         dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
@@ -1508,23 +1552,32 @@ bool make_plan(int G, int pitch_d, int r, int pitch_r, int Dl, int pipe, int max
     return true;
 }
 
+}  // namespace
+
+// Raise a kernel's dynamic-smem cap once per (kernel, device): the attribute is
+// per device context, so a ctx on a second device in the same process needs its
+// own call. Process-wide, mutex-protected; errors propagate.
+int ensure_smem_attr(const void* kernel, int smem) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> done;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = done.find({kernel, dev});
+    if (it != done.end() && it->second >= smem) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    done[{kernel, dev}] = smem;
+    return cudaSuccess;
+}
+
+namespace {
+
 template <typename K>
 int launch_coop(K kernel, int G, int smem, cudaStream_t stream, void** args) {
-    // Raise the dynamic-smem cap once per kernel (per thread; one device per process).
-    static thread_local const void* set_for[8] = {};
-    static thread_local int set_smem[8] = {};
-    const void* key = reinterpret_cast<const void*>(kernel);
-    int slot = 0;
-    while (slot < 8 && set_for[slot] != nullptr && set_for[slot] != key) ++slot;
-    if (slot == 8 || set_for[slot] != key || set_smem[slot] < smem) {
-        cudaError_t e =
-            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        if (slot < 8) {
-            set_for[slot] = key;
-            set_smem[slot] = smem;
-        }
-    }
+    const int e = ensure_smem_attr(reinterpret_cast<const void*>(kernel), smem);
+    if (e != cudaSuccess) return e;
     return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kernel), dim3(G),
                                        dim3(kThreads), args, static_cast<size_t>(smem), stream);
 }

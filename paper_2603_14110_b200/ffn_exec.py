@@ -28,6 +28,7 @@ libsparsegate_b200.so; there is no CPU path.
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
 import threading
 import weakref
 from dataclasses import dataclass, field
@@ -405,16 +406,18 @@ _cache: dict = {}
 _cache_lock = threading.Lock()
 
 
-def _fingerprint(*arrays) -> int:
-    """Strided content sample of the arrays: an in-place change of weights (or a
-    swapped array) gives a new device layer instead of a stale one."""
-    h = []
+def _fingerprint(*arrays) -> bytes:
+    """Digest of the FULL contents of the arrays: any in-place change of weights
+    (or a swapped array) gives a new device layer — which re-runs the upload
+    validation, so a NaN written into cached weights still raises DataError as
+    the reference's per-call validate does (types.hpp:31-51, ffn_exec.hpp:57).
+    blake2b runs at ~1 GB/s, well under the upload's own cost."""
+    h = hashlib.blake2b(digest_size=16)
     for a in arrays:
-        a = np.asarray(a)
-        flat = a.reshape(-1)
-        step = max(1, flat.size // 4096)
-        h.append((id(a), a.shape, hash(flat[::step].tobytes())))
-    return hash(tuple(h))
+        a = np.ascontiguousarray(a)
+        h.update(repr((a.dtype.str, a.shape)).encode())
+        h.update(memoryview(a).cast("B"))
+    return h.digest()
 
 
 def _layer_for(w: Optional[FfnWeights], pred: Optional[Predictor], device: int = 0) -> DeviceLayer:

@@ -13,6 +13,9 @@
   ||y_gpu - y_ref||_2 <= Y_RTOL * ||y_ref||_2 with Y_RTOL = 1e-3, where y_ref is
   the oracle output; when a token's sets differ (only at admissible neurons)
   y_ref is recomputed in f64 on the GPU's own sets.
+* The number of such admissible flips is bounded: at most MAX_FLIPS neurons
+  per token may differ in P, and as many in V (observed: 0 on almost every
+  token; tests record the counts and the band sizes).
 """
 from __future__ import annotations
 
@@ -23,6 +26,7 @@ from paper_2603_14110_b200 import bf16_to_f64, round_bf16
 
 EPS = 2.0 ** -14
 Y_RTOL = 1e-3
+MAX_FLIPS = 4
 
 
 def q_bf16(a) -> np.ndarray:
@@ -48,7 +52,7 @@ def gated(g, u, act):
     return z
 
 
-def check_token(q, x, gpu_y, gpu_P, gpu_V, act=0, eps=EPS, y_rtol=Y_RTOL):
+def check_token(q, x, gpu_y, gpu_P, gpu_V, act=0, eps=EPS, y_rtol=Y_RTOL, max_flips=MAX_FLIPS):
     """Compare one GPU token with the oracle. q: quantized layer dict (f64).
 
     Returns a dict of diagnostics; raises AssertionError on a parity failure.
@@ -70,6 +74,8 @@ def check_token(q, x, gpu_y, gpu_P, gpu_V, act=0, eps=EPS, y_rtol=Y_RTOL):
     dV = V_gpu ^ {i for i in P_gpu if gfull[i] > 0}
     bad_V = [i for i in dV if not near_v[i]]
     assert not bad_V, f"V differs outside the near-threshold band at {bad_V[:10]}"
+    assert len(dP) <= max_flips and len(dV) <= max_flips, \
+        f"{len(dP)} P / {len(dV)} V near-threshold flips exceed the bound {max_flips}"
     assert len(gpu_P) == len(P_gpu) and list(gpu_P) == sorted(gpu_P), "P not ascending/unique"
     assert len(gpu_V) == len(V_gpu) and list(gpu_V) == sorted(gpu_V), "V not ascending/unique"
     if not dP and not dV:

@@ -1,0 +1,114 @@
+"""Parity of the EXACT configurations behind the bench numbers.
+
+* configs[1] headline: the 32-layer ProSparse-Llama2-7B-shape stack exactly as
+  bench.py builds and runs it — model.build_host_model + model.upload (the
+  calibration-balanced neuron layout, 16 hot rows per CTA), one persistent launch
+  per step through the host entry sg_ffn_forward_layers_host — unchained (the
+  bench's device-timed line) and chained (layer l+1 reads layer l's output, the
+  real decode dependency). Every layer's P, V (sg_ctx_read_stack_sets) and y are
+  checked against the f64 oracle (ffn_exec.hpp:183-218) under tests/parity_util.py.
+* configs[4] batched decode at full 7B and 13B size, B in {17, 32, 64}, through
+  sg_ffn_forward_batch_host (the e2e entry of the batch bench): every token's P_b,
+  V_b and y_b against the single-token oracle.
+Near-threshold flips are bounded per token (parity_util.MAX_FLIPS) and their
+counts are printed (-s) for the record.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2603_14110_b200 import bf16_to_f64
+from paper_2603_14110_b200 import _capi as capi
+from paper_2603_14110_b200.ffn_exec import Context, Pipeline, check
+from paper_2603_14110_b200.model import CONFIGS, build_host_layer, build_host_model, upload
+from parity_util import Y_RTOL, check_token, q_f32
+
+pytestmark = pytest.mark.gpu
+
+
+def _q(h):
+    return dict(gate=bf16_to_f64(h.gate), up=bf16_to_f64(h.up),
+                down=np.ascontiguousarray(bf16_to_f64(h.down_t).T), A=bf16_to_f64(h.A),
+                B=bf16_to_f64(h.B), bias=q_f32(h.bias))
+
+
+@pytest.fixture(scope="module")
+def stack7b():
+    cfg = CONFIGS["7b"]
+    cfg, host = build_host_model("7b", rank=256, sparsity=0.5, workers=8)
+    layers = [upload(h, cfg["d"], cfg["D"], cfg["act"], 256, hot_rows=16) for h in host]
+    return cfg, host, layers
+
+
+@pytest.mark.parametrize("chain", [0, 1])
+def test_bench_stack_7b_32_layers(stack7b, chain):
+    cfg, host, layers = stack7b
+    d, D, L = cfg["d"], cfg["D"], len(host)
+    assert L == 32
+    ctx = Context(0, d, D, 256)
+    check(capi.lib().sg_ctx_enable_stack_sets(ctx.handle, 1))
+    arr = (C.c_void_p * L)(*[l.handle.value for l in layers])
+    xs = np.ascontiguousarray(np.stack([h.x for h in host]), dtype=np.float32)
+    ys = np.zeros_like(xs)
+    st = (capi.sg_exec_stats * L)()
+    check(capi.lib().sg_ffn_forward_layers_host(ctx.handle, arr, L, int(Pipeline.Sequential),
+                                                xs.ctypes.data_as(C.c_void_p),
+                                                ys.ctypes.data_as(C.c_void_p), chain, st, None))
+    P = np.zeros(D, dtype=np.int32)
+    V = np.zeros(D, dtype=np.int32)
+    p, v = C.c_int64(0), C.c_int64(0)
+    flips = []
+    for l in range(L):
+        check(capi.lib().sg_ctx_read_stack_sets(ctx.handle, None, l, P.ctypes.data_as(C.c_void_p),
+                                                C.byref(p), V.ctypes.data_as(C.c_void_p), C.byref(v)))
+        assert (st[l].predicted_active, st[l].revalidated) == (p.value, v.value)
+        x = xs[l] if (chain == 0 or l == 0) else ys[l - 1]
+        try:
+            diag = check_token(_q(host[l]), x.astype(np.float64), ys[l], P[:p.value].copy(),
+                               V[:v.value].copy(), act=cfg["act"])
+        except AssertionError:
+            print(f"layer {l}: |x|={np.linalg.norm(x):.4g} |y|={np.linalg.norm(ys[l]):.4g} "
+                  f"p={p.value} v={v.value}")
+            raise
+        assert diag["rel"] <= Y_RTOL
+        if chain == 0:  # the calibrated operating point the bench quotes
+            assert 0.3 * D < diag["p"] < 0.7 * D and 0.03 * D < diag["v"] < 0.2 * D
+        flips.append((diag["dP"], diag["dV"], diag["near_p"], diag["near_v"]))
+    print(f"chain={chain}: per-layer (flips P, flips V, band P, band V): {flips}")
+
+
+def _global_map(layer):
+    return np.array([layer.global_index(k) for k in range(layer.local_inter)], dtype=np.int64)
+
+
+@pytest.mark.parametrize("config", ["7b", "13b"])
+def test_bench_batch_full_size(config):
+    cfg = CONFIGS[config]
+    d, D, act = cfg["d"], cfg["D"], cfg["act"]
+    h = build_host_layer(d, D, act, seed=1, rank=256, sparsity=0.5, eval_tokens=64)
+    layer = upload(h, d, D, act, 256, hot_rows=16)
+    q = _q(h)
+    gmap = _global_map(layer)
+    ctx = Context(0, d, D, 256)
+    for B in (17, 32, 64):
+        xs = np.ascontiguousarray(h.xs[:, :B].T, dtype=np.float32)
+        ys = np.zeros_like(xs)
+        st = (capi.sg_exec_stats * B)()
+        check(capi.lib().sg_ffn_forward_batch_host(ctx.handle, layer.handle,
+                                                   xs.ctypes.data_as(C.c_void_p), B,
+                                                   ys.ctypes.data_as(C.c_void_p), st, None))
+        pb = np.zeros(layer.local_inter, dtype=np.uint64)
+        vb = np.zeros_like(pb)
+        check(capi.lib().sg_ctx_read_batch(ctx.handle, None, B, None, pb.ctypes.data_as(C.c_void_p),
+                                           vb.ctypes.data_as(C.c_void_p)))
+        flips = []
+        for b in range(B):
+            bit = np.uint64(1) << np.uint64(b)
+            P = np.sort(gmap[(pb & bit) != 0])
+            V = np.sort(gmap[(vb & bit) != 0])
+            assert (st[b].predicted_active, st[b].revalidated) == (len(P), len(V))
+            diag = check_token(q, xs[b].astype(np.float64), ys[b], P, V, act=act)
+            assert diag["rel"] <= Y_RTOL
+            flips.append((diag["dP"], diag["dV"]))
+        print(f"{config} B={B}: flips per token {flips}")
