@@ -42,16 +42,6 @@ SHAPES = {
 }
 
 
-def batch_launches_per_layer(B):
-    """Kernels one sg_ffn_forward_batch call launches (sg_batch.cu launch_batch)."""
-    if B <= int(os.environ.get("SG_BATCH_STACK_MAX", "4")):
-        return 1
-    fuse = int(os.environ.get("SG_BATCH_FUSE", "0"))
-    n = 12 if B <= 16 else 13
-    n -= 1 if fuse & 1 else 0
-    n -= 1 if (fuse & 2) and B <= 16 else 0
-    return n
-
 def log(*a):
     print("[bench]", *a, file=sys.stderr, flush=True)
 
@@ -195,16 +185,20 @@ def run_reference(args, world, rank):
     w = 1
     t_build = time.time()
     per_layer = []
-    with cf.ThreadPoolExecutor(max(1, min(8, (os.cpu_count() or 8) // 2))) as ex:
-        futs = [ex.submit(_ref_layer_inputs, d, D, l, args.rank, args.sparsity) for l in range(L)]
-        for l, f in enumerate(futs):
-            gate, up, down, A, B, bias, ev = f.result()
-            ref = O.RefLayer(gate, up, down, A, B, bias, activation=cfg["act"])
-            xs = np.ascontiguousarray(ev[:ntok])
-            for _ in range(w):
-                ref.run(xs, pipeline=2)
-            per_layer.append(sum(ref.run(xs, pipeline=2)[2] for _ in range(k)) / k)
-            del ref, gate, up, down
+    chunk = max(1, min(8, (os.cpu_count() or 8) // 2))
+    with cf.ThreadPoolExecutor(chunk) as ex:
+        for l0 in range(0, L, chunk):
+            # build a chunk of layers in parallel, then time them with the host idle
+            built = list(ex.map(lambda l: _ref_layer_inputs(d, D, l, args.rank, args.sparsity),
+                                range(l0, min(L, l0 + chunk))))
+            for gate, up, down, A, B, bias, ev in built:
+                ref = O.RefLayer(gate, up, down, A, B, bias, activation=cfg["act"])
+                xs = np.ascontiguousarray(ev[:ntok])
+                for _ in range(w):
+                    ref.run(xs, pipeline=2)
+                per_layer.append(sum(ref.run(xs, pipeline=2)[2] for _ in range(k)) / k)
+                del ref
+            del built
     step_s = float(sum(per_layer))
     tok_s = ntok / step_s
     line = {
@@ -238,7 +232,7 @@ def bench_config(cfg, args, L, world):
                         f"sequential pipeline, {'chained' if chain else 'unchained'} decode",
             "layers": L, "hidden": d, "inter": D, "rank": args.rank,
             "predicted_sparsity_target": args.sparsity, "batch": max(1, args.batch),
-            "chained": bool(chain),
+            "chain": {0: "unchained", 1: "raw y_l -> x_{l+1}", 2: "residual h_{l+1} + y_l"}[chain],
             "parallelism": f"d_ff-shard{world}" if world > 1 else "none"}
 
 
@@ -285,8 +279,10 @@ def cpu_baseline_for(cfg, host_layer0, args):
 # our arm
 # ---------------------------------------------------------------------------
 def run_batch(args, cfg, host, layers, ctx, world, rank, local):
-    """Batched decode: B tokens per step through the L layers, one sg_ffn_forward_batch
-    per layer (≈10 kernels), the whole step captured in one CUDA graph."""
+    """Batched decode (configs[4]): B tokens per step through the L layers, one
+    sg_ffn_forward_batch per layer — for B >= 2 ONE persistent tcgen05 launch per layer
+    (csrc/sg_batch_tc.cu) — the whole step captured in one CUDA graph. The dense
+    comparator is the same kernel with every row (sg_ffn_forward_batch_dense)."""
     import ctypes as C
 
     import torch
@@ -299,15 +295,16 @@ def run_batch(args, cfg, host, layers, ctx, world, rank, local):
     Y = torch.zeros_like(X)
     stream = torch.cuda.Stream()
 
-    def step(sh):
+    def step(sh, fn=lib.sg_ffn_forward_batch):
         for l in range(L):
-            check(lib.sg_ffn_forward_batch(ctx.handle, layers[l].handle, C.c_void_p(X[l].data_ptr()),
-                                           B, C.c_void_p(Y[l].data_ptr()), C.c_void_p(sh)))
+            check(fn(ctx.handle, layers[l].handle, C.c_void_p(X[l].data_ptr()), B,
+                     C.c_void_p(Y[l].data_ptr()), C.c_void_p(sh)))
 
     with torch.cuda.stream(stream):
-        step(stream.cuda_stream)  # allocations / attributes before capture
+        step(stream.cuda_stream)  # workspaces / attributes / tensor maps before capture
+        step(stream.cuda_stream, lib.sg_ffn_forward_batch_dense)
     torch.cuda.synchronize()
-    # union sizes of the last layer (roofline bytes), per layer re-run un-captured
+    # union sizes per layer (roofline bytes), re-run un-captured
     pb = np.zeros(layers[0].local_inter, dtype=np.uint64)
     vb = np.zeros_like(pb)
     up, uv = [], []
@@ -319,24 +316,36 @@ def run_batch(args, cfg, host, layers, ctx, world, rank, local):
                                     pb.ctypes.data_as(C.c_void_p), vb.ctypes.data_as(C.c_void_p)))
         up.append(int((pb != 0).sum()))
         uv.append(int((vb != 0).sum()))
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=stream):
-        step(torch.cuda.current_stream().cuda_stream)
-    for _ in range(args.warmup):
-        graph.replay()
-    torch.cuda.synchronize()
-    sampler = ClockSampler(local)
-    time.sleep(0.15)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        graph.replay()
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
-    clocks = sampler.stop()
+
+    def graph_of(fn):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            step(torch.cuda.current_stream().cuda_stream, fn)
+        return g
+
+    graph = graph_of(lib.sg_ffn_forward_batch)
+    dgraph = graph_of(lib.sg_ffn_forward_batch_dense)
+
+    def timed(g, K, W, clocks=False):
+        for _ in range(W):
+            g.replay()
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local) if clocks else None
+        if sampler:
+            time.sleep(0.15)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(K):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / K, (sampler.stop() if sampler else None)
+
+    ms, clocks = timed(graph, args.steps, args.warmup, clocks=True)
+    ms_dense, _ = timed(dgraph, max(10, args.steps // 2), args.warmup)
     r = args.rank
     alg = sum(2 * r * d + 2 * D * r + 4 * D + 2 * d * p + 4 * d * v + 8 * d * B for p, v in zip(up, uv))
+    dense_alg = L * (3 * 2 * d * D + 8 * d * B)
     hbm, hbm_kind = peaks()
     # e2e: pinned host tokens in, outputs back, through the same graph
     xh = torch.empty_like(X, device="cpu").pin_memory()
@@ -360,30 +369,38 @@ def run_batch(args, cfg, host, layers, ctx, world, rank, local):
     t1.record()
     torch.cuda.synchronize()
     ms_e2e = t0.elapsed_time(t1) / ke
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_for(cfg, host[0], args)
+        except Exception as e:  # report, never fake
+            cpu = {"value": None, "error": str(e)[:200]}
+    conf = bench_config(cfg, args, L, world)
+    conf.update({"l2": "no flush: each step streams the union rows of %d distinct layers" % L,
+                 "path": "B = 1: persistent single-token executor; B >= 2: one tcgen05 launch per layer"})
     line = {
         "metric": "sparse-FFN decode tokens/s", "value": B * 1000.0 / ms, "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic",
-        "config": {"workload": f"{cfg['model']}: {L} layers d={d} d_ff={D} r={r} s={args.sparsity}, "
-                               f"batched decode B={B} (union mask, gathered rows)",
-                   "layers": L, "hidden": d, "inter": D, "rank": r, "batch": B,
-                   "l2": "no flush: each step streams the union rows of %d distinct layers" % L},
+        "data": "synthetic", "config": conf,
         "per_layer_us": ms * 1000.0 / L,
         "union_p_mean": float(np.mean(up)), "union_v_mean": float(np.mean(uv)),
         "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                      "frac": alg / (ms * 1e-3) / 1e9 / hbm, "peak_kind": hbm_kind, "traffic": None,
-                     "bytes_per_step": alg, "kernel": "sg_batch.cu (B <= 4: persistent stack executor; "
-                                               "B <= 16: CUDA-core row streaming; above: mma.sync gathered GEMMs)"},
+                     "bytes_per_step": alg,
+                     "kernel": "tc_kernel (csrc/sg_batch_tc.cu: tcgen05.mma + TMEM, TMA gather4)"
+                               if B > 1 else "ffn_kernel<2> (persistent single-token executor)"},
+        "dense": {"ms_per_step": ms_dense, "tokens_per_s": B * 1000.0 / ms_dense,
+                  "per_layer_us": ms_dense * 1000.0 / L,
+                  "achieved_gbs": dense_alg / (ms_dense * 1e-3) / 1e9,
+                  "frac": dense_alg / (ms_dense * 1e-3) / 1e9 / hbm,
+                  "sparse_speedup": ms_dense / ms,
+                  "kernel": "tc_kernel dense mode (sg_ffn_forward_batch_dense)"},
         "e2e": {"value": B * 1000.0 / ms_e2e, "unit": "tokens/s", "h2d_bytes_per_step": L * B * d * 4,
                 "d2h_bytes_per_step": L * B * d * 4, "ms_per_step": ms_e2e},
-        # per layer: B <= SG_BATCH_STACK_MAX (4): one persistent stack launch; nb <= 16:
-        # 12 kernels (CUDA-core gate / up / down row streaming) minus the fused ones
-        # (SG_BATCH_FUSE bit 0: survivor compaction in gate_epi's last block; bit 1,
-        # nb <= 16 only: T reduced in t_kernel's last split block); above: 13 (GEMM tiles)
-        "gpu_launches": args.steps * L * batch_launches_per_layer(B),
+        "gpu_launches": args.steps * L,
         "clocks": clocks,
-        "cpu_baseline": None,
+        "cpu_baseline": cpu,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -434,9 +451,12 @@ def main():
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--rank", type=int, default=256)
     ap.add_argument("--sparsity", type=float, default=0.5)
-    ap.add_argument("--chain", type=int, default=1,
-                    help="1 (default): layer l+1 reads layer l's output (a real decode chain); "
-                         "0: every layer reads its own token (the unchained line is reported too)")
+    ap.add_argument("--chain", type=int, default=2,
+                    help="2 (default): layer l+1 reads h_{l+1} + y_l (the residual-stream decode "
+                         "dependency: it cannot start before layer l's y exists); 1: reads y_l raw "
+                         "(this synthetic FFN shrinks y ~100x per layer, so the operating point "
+                         "drifts); 0: every layer reads its own token (the unchained line is "
+                         "reported too)")
     ap.add_argument("--mode", default="stack", choices=["stack", "per-layer"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
@@ -503,7 +523,12 @@ def main():
     ys = torch.zeros_like(xs)
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
-    chain = 0 if copies > 1 else args.chain  # rotated copies of one layer are independent
+    is_stack = args.mode == "stack" and world == 1
+    if copies > 1 or (not is_stack and args.chain == 2):
+        # rotated copies of one layer are independent; per-layer launches (N > 1) take
+        # one x pointer per layer, so no residual add between them
+        args.chain = 0
+    chain = args.chain
 
     def step_stack(pipe=Pipeline.Sequential, ch=None, s=None):
         check(lib.sg_ffn_forward_layers(ctx.handle, arr, Ls, int(pipe), C.c_void_p(xs.data_ptr()),
@@ -512,14 +537,13 @@ def main():
 
     def step_layers(pipe=Pipeline.Sequential, s=None):
         for l in range(Ls):
-            src = ys[l - 1] if (chain and l > 0) else xs[l]
+            src = ys[l - 1] if (chain == 1 and l > 0) else xs[l]
             check(lib.sg_ffn_forward_device(ctx.handle, layers[l].handle, int(pipe),
                                             C.c_void_p(src.data_ptr()),
                                             C.c_void_p(ys[l].data_ptr()), C.c_void_p(sh if s is None else s)))
             if world > 1:
                 torch.distributed.all_reduce(ys[l])
 
-    is_stack = args.mode == "stack" and world == 1
     launches_per_step = 1 if is_stack else Ls
 
     def capture(fn):
@@ -604,7 +628,7 @@ def main():
             check(lib.sg_ctx_enable_stack_sets(ctx.handle, 0))
     else:
         for l in range(Ls):
-            src = ys[l - 1] if (chain and l > 0) else xs[l]
+            src = ys[l - 1] if (chain == 1 and l > 0) else xs[l]
             layers[l].forward_device(src.data_ptr(), ys[l].data_ptr(), Pipeline.Sequential, ctx, sh)
             s1 = capi.sg_exec_stats()
             check(lib.sg_ctx_read_stats(ctx.handle, C.c_void_p(sh), C.byref(s1)))
@@ -618,7 +642,8 @@ def main():
     diag = None
     if sets is not None and world == 1 and Dl == D:
         xin = [xs[0].double().cpu().numpy()] + \
-              [(ys[l - 1] if chain else xs[l]).double().cpu().numpy() for l in range(1, Ls)]
+              [({0: xs[l], 1: ys[l - 1], 2: xs[l] + ys[l - 1]}[chain]).double().cpu().numpy()
+               for l in range(1, Ls)]
         diag = near_threshold(host_l, None, xin, sets, cfg["act"])
 
     # e2e through the C ABI host entry: pinned x in, y out, synchronised per step
@@ -640,7 +665,7 @@ def main():
 
     ke = max(10, min(args.steps, 500))
     ms_e2e, _ = timed(step_e2e if world == 1 else step_e2e_sharded, ke, 3)
-    h2d = (d if chain else Ls * d) * 4
+    h2d = (d if chain == 1 else Ls * d) * 4
     e2e = {"value": 1000.0 * copies / ms_e2e if copies > 1 else 1000.0 / ms_e2e, "unit": "tokens/s",
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": Ls * d * 4, "ms_per_step": ms_e2e,
            "steps": ke,

@@ -170,8 +170,12 @@ sg_status sg_ffn_forward(sg_ctx* ctx, const sg_layer* layer, sg_pipeline pipelin
                          sg_exec_stats* stats, void* stream);
 
 /* Multi-layer decode step on device: runs layers[0..n) in order on `stream`,
- * layer l reading xs + l*hidden and writing ys + l*hidden (fp32, device). With
- * chain != 0, layer l+1 reads layer l's output instead of xs (a real decode chain). */
+ * layer l reading xs + l*hidden and writing ys + l*hidden (fp32, device).
+ *   chain 0: layer l reads xs_l (independent layers);
+ *   chain 1: layer l+1 reads layer l's output y_l (a raw decode chain);
+ *   chain 2: layer l+1 reads xs_{l+1} + y_l (fp32 add: the residual-stream
+ *            dependency of a decoder block, h_{l+1} + FFN_l(x_l)).
+ * With chain 1 or 2, layer l+1 cannot start before every value of y_l exists. */
 sg_status sg_ffn_forward_layers(sg_ctx* ctx, const sg_layer* const* layers, int32_t n,
                                 sg_pipeline pipeline, const float* xs, float* ys, int32_t chain,
                                 void* stream);
@@ -203,6 +207,12 @@ sg_status sg_ctx_read_stack_sets(sg_ctx* ctx, void* stream, int32_t layer, int32
  * tensor cores. xs, ys: device fp32 [batch][hidden]. Asynchronous on `stream`. */
 sg_status sg_ffn_forward_batch(sg_ctx* ctx, const sg_layer* layer, const float* xs, int32_t batch,
                                float* ys, void* stream);
+/* Dense comparator of the batched path (no predictor: every gate, up and down row
+ * is read once and multiplied against all tokens) on the same tensor-core kernel:
+ * dense_ffn (ffn_exec.hpp:103-122) per token, batched. xs, ys: device fp32
+ * [batch][hidden], batch in [1, 64]. */
+sg_status sg_ffn_forward_batch_dense(sg_ctx* ctx, const sg_layer* layer, const float* xs,
+                                     int32_t batch, float* ys, void* stream);
 /* Synchronises, then per-token stats (batch entries) and, optionally, per-neuron
  * bit masks (local inter entries; bit b = token b): predicted active, survivor. */
 sg_status sg_ctx_read_batch(sg_ctx* ctx, void* stream, int32_t batch, sg_exec_stats* stats,

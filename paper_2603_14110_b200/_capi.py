@@ -82,6 +82,7 @@ SYMBOLS = [
     ("sg_ctx_enable_stack_sets", C.c_int, [_VP, _I32]),
     ("sg_ctx_read_stack_sets", C.c_int, [_VP, _VP, _I32, _VP, C.POINTER(_I64), _VP, C.POINTER(_I64)]),
     ("sg_ffn_forward_batch", C.c_int, [_VP, _VP, _VP, _I32, _VP, _VP]),
+    ("sg_ffn_forward_batch_dense", C.c_int, [_VP, _VP, _VP, _I32, _VP, _VP]),
     ("sg_ctx_read_batch", C.c_int, [_VP, _VP, _I32, C.POINTER(sg_exec_stats), _VP, _VP]),
     ("sg_ffn_forward_batch_host", C.c_int, [_VP, _VP, _VP, _I32, _VP, C.POINTER(sg_exec_stats), _VP]),
     ("sg_ctx_enable_phase_timing", C.c_int, [_VP, _I32]),

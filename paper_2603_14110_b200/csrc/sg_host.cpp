@@ -47,6 +47,8 @@ struct sg_layer {
     sg::LayerView view{};
     sg::LayerView* repdev = nullptr;  // [64] copies of view: small batches as one stack launch
     uint64_t id = 0;                  // unique per (layer, view contents): bumped by set_hot_rows
+    sg::TcMaps tcmaps{};              // weight tensor maps of the tensor-core batch path
+    bool has_tcmaps = false;
 };
 
 struct sg_ctx {
@@ -83,6 +85,11 @@ struct sg_ctx {
     const sg_layer* blast = nullptr;
     int blast_B = 0;
     bool blast_stack = false;  // the last batch ran as a stack launch (small B)
+    int blast_path = 0;        // 0 stack, 1 legacy mma.sync kernels, 2 tensor cores (tcgen05)
+    // tensor-core batch workspace (allocated on first use)
+    void* tmem_ws = nullptr;
+    sg::TcArgs tw{};
+    std::map<int, sg::TcMaps> tcmaps_ws;  // workspace maps per nb (box height N = 2 nb)
 };
 
 constexpr int kMaxStackLayers = 1024;
@@ -170,6 +177,36 @@ struct DeviceGuard {
     }
 };
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(f);
+    }();
+    return fn;
+}
+// 2-D bf16 map: `cols` x `rows`, row stride `row_elems`, box {64, box_rows}, 128-B swizzle.
+bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t row_elems,
+              int box_rows) {
+    EncodeTiledFn fn = encode_tiled();
+    if (fn == nullptr) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_elems) * 2};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int64_t local_to_global(const sg_layer* L, int64_t k) {
     return L->gidx.empty() ? L->gbase + k * L->gstride : L->gidx[static_cast<size_t>(k)];
 }
@@ -221,7 +258,7 @@ sg_exec_stats make_stats(const sg_layer* L, int pipeline, int64_t p, int64_t v) 
 int small_batch_limit() {
     static const int v = [] {
         const char* e = std::getenv("SG_BATCH_STACK_MAX");
-        return e ? std::atoi(e) : 4;
+        return e ? std::atoi(e) : 1;
     }();
     return v;
 }
@@ -264,7 +301,7 @@ sg_status stack_launch(sg_ctx* C, const sg_layer* const* layers, int32_t n,
                               sg_pipeline pipeline, const float* xs, float* ys, int32_t chain,
                               void* stream, unsigned long long* mbits, unsigned long long* vbits,
                               const sg::LayerView* views_dev = nullptr) {
-    if (C == nullptr || layers == nullptr || n < 1 || n > kMaxStackLayers)
+    if (C == nullptr || layers == nullptr || n < 1 || n > kMaxStackLayers || chain < 0 || chain > 2)
         return fail(SG_ERR_USAGE, "bad arguments");
     if (xs == nullptr || ys == nullptr) return fail(SG_ERR_USAGE, "null xs/ys");
     const sg_layer* L0 = layers[0];
@@ -531,6 +568,16 @@ sg_status sg_layer_create(const sg_layer_desc* desc, sg_layer** out) {
     V.gidx = L->gidx.empty() ? nullptr
                              : reinterpret_cast<const int*>(static_cast<char*>(L->dmem) + gidx_off);
     L->id = g_layer_ids.fetch_add(1);
+    if (has_w) {
+        // tensor maps of the batched tensor-core path (sg_batch_tc.cu)
+        sg::TcMaps& tm = L->tcmaps;
+        bool ok = make_map(&tm.gate, V.gate, pd, Dl, pd, 1) &&
+                  make_map(&tm.up, V.ud, pd, Dl, 2 * pd, 1) &&
+                  make_map(&tm.down, V.ud + pd, pd, Dl, 2 * pd, 1);
+        if (ok && has_pred)
+            ok = make_map(&tm.A, V.A, pr, Dl, pr, 128) && make_map(&tm.Bp, V.B, pd, r, pd, 128);
+        L->has_tcmaps = ok;
+    }
     if (has_w && has_pred) {
         // 64 copies of the view: small batches run as one stack launch (token b =
         // "layer" b); allocated here, never by a (possibly captured) forward call
@@ -663,6 +710,7 @@ sg_status sg_ctx_destroy(sg_ctx* C) {
     if (C->ysdev) cudaFree(C->ysdev);
     if (C->dbgdev) cudaFree(C->dbgdev);
     if (C->bmem) cudaFree(C->bmem);
+    if (C->tmem_ws) cudaFree(C->tmem_ws);
     delete C;
     return SG_OK;
 }
@@ -751,6 +799,138 @@ sg_status batch_workspace(sg_ctx* C) {
 }
 }  // namespace
 
+namespace {
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+constexpr int kTcKSMax = 8;   // K slices of the gate / up units (partial buffers sized for it)
+constexpr int kTcSMax = 16;   // block ranges of the down units
+
+sg_status tc_workspace(sg_ctx* C) {
+    if (C->tmem_ws) return SG_OK;
+    const size_t Dm = static_cast<size_t>(C->max_D), pd = static_cast<size_t>(C->pitch_dmax);
+    const size_t nblk = (Dm + 255) / 256, ndt = (pd + 255) / 256;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off += (bytes + 255) / 256 * 256;
+        return o;
+    };
+    const size_t o_x = take(128 * pd * 2), o_tp = take(((pd + 255) / 256) * 256 * 64 * 4),
+                 o_th = take(128 * 256 * 2), o_mb = take(Dm * 8), o_vb = take(Dm * 8),
+                 o_ul = take(nblk * 256 * 4), o_uc = take(nblk * 4), o_vl = take(nblk * 256 * 4),
+                 o_vc = take(nblk * 4), o_gp = take((kTcKSMax - 1) * nblk * 256 * 64 * 4),
+                 o_up = take((kTcKSMax - 1) * nblk * 256 * 64 * 4), o_G = take(Dm * 64 * 4),
+                 o_z = take(128 * nblk * 256 * 2), o_y = take(kTcSMax * ndt * 256 * 64 * 4),
+                 o_cnt = take((64 + 64 + 1) * 4),
+                 o_fl = take(static_cast<size_t>(sg::tc_flag_ints(static_cast<int>(nblk), static_cast<int>(ndt))) * 4);
+    DeviceGuard dg(C->device);
+    cudaError_t e = cudaMalloc(&C->tmem_ws, off);
+    if (e == cudaSuccess) e = cudaMemset(C->tmem_ws, 0, off);
+    if (e != cudaSuccess) {
+        C->tmem_ws = nullptr;
+        return fail(SG_ERR_CUDA, std::string("tensor-core batch workspace: ") + cudaGetErrorString(e));
+    }
+    char* b = static_cast<char*>(C->tmem_ws);
+    sg::TcArgs& a = C->tw;
+    a.xhl = reinterpret_cast<uint16_t*>(b + o_x);
+    a.tpart = reinterpret_cast<float*>(b + o_tp);
+    a.thl = reinterpret_cast<uint16_t*>(b + o_th);
+    a.mbits = reinterpret_cast<uint64_t*>(b + o_mb);
+    a.vbits = reinterpret_cast<uint64_t*>(b + o_vb);
+    a.ulist = reinterpret_cast<int*>(b + o_ul);
+    a.ucnt = reinterpret_cast<int*>(b + o_uc);
+    a.vlist = reinterpret_cast<int*>(b + o_vl);
+    a.vcnt = reinterpret_cast<int*>(b + o_vc);
+    a.gpart = reinterpret_cast<float*>(b + o_gp);
+    a.upart = reinterpret_cast<float*>(b + o_up);
+    a.G = reinterpret_cast<float*>(b + o_G);
+    a.zhl = reinterpret_cast<uint16_t*>(b + o_z);
+    a.ypart = reinterpret_cast<float*>(b + o_y);
+    a.pcount = reinterpret_cast<int*>(b + o_cnt);
+    a.vcount = a.pcount + 64;
+    a.bad = a.pcount + 128;
+    a.flags = reinterpret_cast<int*>(b + o_fl);
+    a.zpitch = static_cast<int>(nblk * 256);
+    a.xpitch = static_cast<int>(pd);
+    return SG_OK;
+}
+
+// Largest divisor k <= want of the 64-wide K chunks of pitch (so each slice is whole chunks).
+int k_slices(int pitch, int want) {
+    const int chunks = pitch / 64;
+    for (int k = std::min(want, chunks); k > 1; --k)
+        if (chunks % k == 0) return k;
+    return 1;
+}
+
+// One tensor-core launch: B tokens through one layer (dense != 0: every row, no predictor).
+sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float* ys, void* stream,
+                     int dense) {
+    if (sg_status s = tc_workspace(C); s != SG_OK) return s;
+    sg::TcArgs a = C->tw;
+    a.B = B;
+    a.nb = (B + 7) / 8 * 8;
+    a.N = 2 * a.nb;
+    a.d = static_cast<int>(L->d);
+    a.D = static_cast<int>(L->D_local);
+    a.r = static_cast<int>(L->r);
+    a.pitch_d = L->pitch_d;
+    a.pitch_r = L->pitch_r;
+    a.act = L->act;
+    a.nblk = (a.D + 255) / 256;
+    a.ndt = (a.pitch_d + 255) / 256;
+    a.dense = dense;
+    a.x = xs;
+    a.y = ys;
+    a.bias = L->view.bias;
+    // K slices of the gate / up units: enough units to spread the union rows over the
+    // SMs while the owner slice's fixed-order partial sum stays small (partials are
+    // 256 rows x nb fp32): SG_TC_KSG / SG_TC_KSU override
+    const int ksg_want = env_int("SG_TC_KSG", B <= 16 ? 4 : 2), ksu_want = env_int("SG_TC_KSU", B <= 16 ? 4 : 2);
+    a.KSg = k_slices(a.pitch_d, std::min(ksg_want, kTcKSMax));
+    a.KSu = k_slices(a.pitch_d, std::min(ksu_want, kTcKSMax));
+    a.ksg = a.pitch_d / a.KSg;
+    a.ksu = a.pitch_d / a.KSu;
+    a.S = std::max(1, std::min({env_int("SG_TC_S", 8), kTcSMax, a.nblk}));
+    a.kst = 256;
+    const int NX = 8, KT = dense ? 0 : (a.pitch_d + a.kst - 1) / a.kst, NTR = dense ? 0 : a.pitch_r / 16;
+    const int NPRE = dense ? 0 : a.nblk;
+    a.u_T = NX;
+    a.u_TR = a.u_T + KT;
+    a.u_PRE = a.u_TR + NTR;
+    a.u_GATE = a.u_PRE + NPRE;
+    a.u_UP = a.u_GATE + a.nblk * a.KSg;
+    a.u_DOWN = a.u_UP + a.nblk * a.KSu;
+    a.u_YR = a.u_DOWN + a.ndt * a.S;
+    a.u_end = a.u_YR + a.ndt * 4;
+    // workspace maps for this nb (box height N), cached per ctx
+    auto it = C->tcmaps_ws.find(a.nb);
+    if (it == C->tcmaps_ws.end()) {
+        sg::TcMaps m{};
+        if (!make_map(&m.xhl, a.xhl, C->pitch_dmax, a.N, C->pitch_dmax, a.N) ||
+            !make_map(&m.thl, a.thl, 256, a.N, 256, a.N) ||
+            !make_map(&m.zhl, a.zhl, a.zpitch, a.N, a.zpitch, a.N))
+            return fail(SG_ERR_CUDA, "cuTensorMapEncodeTiled failed (workspace maps)");
+        it = C->tcmaps_ws.emplace(a.nb, m).first;
+    }
+    // the workspace pitches are the ctx maxima: X^T / T^T rows use them
+    sg::TcMaps maps = L->tcmaps;
+    maps.xhl = it->second.xhl;
+    maps.thl = it->second.thl;
+    maps.zhl = it->second.zhl;
+    auto st = static_cast<cudaStream_t>(stream);
+    DeviceGuard dg(C->device);
+    SG_CUDA(cudaMemsetAsync(a.pcount, 0, (64 + 64 + 1) * sizeof(int), st));
+    const int e = sg::launch_batch_tc(maps, a, C->G, stream);
+    if (e != 0) return fail(SG_ERR_CUDA, std::string("tensor-core batch launch: ") +
+                                             cudaGetErrorString(static_cast<cudaError_t>(e)));
+    return SG_OK;
+}
+}  // namespace
+
 sg_status sg_ffn_forward_batch(sg_ctx* C, const sg_layer* L, const float* xs, int32_t batch,
                                float* ys, void* stream) {
     if (sg_status s = check_pair(C, L); s != SG_OK) return s;
@@ -776,6 +956,16 @@ sg_status sg_ffn_forward_batch(sg_ctx* C, const sg_layer* L, const float* xs, in
         C->blast = L;
         C->blast_B = batch;
         C->blast_stack = true;
+        C->blast_path = 0;
+        return SG_OK;
+    }
+    if (L->has_tcmaps && L->r <= 256 && L->d <= 8192 && !env_int("SG_BATCH_LEGACY", 0)) {
+        // tensor cores: one persistent tcgen05 launch (sg_batch_tc.cu)
+        if (sg_status s = tc_forward(C, L, xs, batch, ys, stream, 0); s != SG_OK) return s;
+        C->blast = L;
+        C->blast_B = batch;
+        C->blast_stack = false;
+        C->blast_path = 2;
         return SG_OK;
     }
     sg::BatchArgs a = C->bw;
@@ -818,6 +1008,22 @@ sg_status sg_ffn_forward_batch(sg_ctx* C, const sg_layer* L, const float* xs, in
     C->blast = L;
     C->blast_B = batch;
     C->blast_stack = false;
+    C->blast_path = 1;
+    return SG_OK;
+}
+
+sg_status sg_ffn_forward_batch_dense(sg_ctx* C, const sg_layer* L, const float* xs, int32_t batch,
+                                     float* ys, void* stream) {
+    if (sg_status s = check_pair(C, L); s != SG_OK) return s;
+    if (!L->has_w || !L->has_tcmaps) return fail(SG_ERR_USAGE, "dense batched decode needs weights");
+    if (batch < 1 || batch > 64) return fail(SG_ERR_USAGE, "batch must be in [1, 64]");
+    if (xs == nullptr || ys == nullptr) return fail(SG_ERR_USAGE, "null buffers");
+    if (L->d > 8192) return fail(SG_ERR_USAGE, "hidden too large for the tensor-core path");
+    if (sg_status s = tc_forward(C, L, xs, batch, ys, stream, 1); s != SG_OK) return s;
+    C->blast = L;
+    C->blast_B = batch;
+    C->blast_stack = false;
+    C->blast_path = 3;
     return SG_OK;
 }
 
@@ -839,17 +1045,22 @@ sg_status sg_ctx_read_batch(sg_ctx* C, void* stream, int32_t batch, sg_exec_stat
             bad |= st4[4 * b + 2] != 0;  // the device non-finite flag of token b
         }
     } else {
+        const bool tc = C->blast_path >= 2;
         int flag = 0;
-        SG_CUDA(cudaMemcpy(pc, C->bw.pcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
-        SG_CUDA(cudaMemcpy(vc, C->bw.vcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
-        SG_CUDA(cudaMemcpy(&flag, C->bw.bad, sizeof(int), cudaMemcpyDeviceToHost));
+        SG_CUDA(cudaMemcpy(pc, tc ? C->tw.pcount : C->bw.pcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
+        SG_CUDA(cudaMemcpy(vc, tc ? C->tw.vcount : C->bw.vcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
+        SG_CUDA(cudaMemcpy(&flag, tc ? C->tw.bad : C->bw.bad, sizeof(int), cudaMemcpyDeviceToHost));
         bad = flag != 0;
     }
-    for (int b = 0; stats && b < batch; ++b) stats[b] = make_stats(L, SG_PIPELINE_SEQUENTIAL, pc[b], vc[b]);
+    const int pipe = C->blast_path == 3 ? SG_PIPELINE_DENSE : SG_PIPELINE_SEQUENTIAL;
+    for (int b = 0; stats && b < batch; ++b) stats[b] = make_stats(L, pipe, pc[b], vc[b]);
+    const bool tc = C->blast_path >= 2;
     if (pred_bits)
-        SG_CUDA(cudaMemcpy(pred_bits, C->bw.mbits, sizeof(uint64_t) * L->D_local, cudaMemcpyDeviceToHost));
+        SG_CUDA(cudaMemcpy(pred_bits, tc ? C->tw.mbits : C->bw.mbits, sizeof(uint64_t) * L->D_local,
+                           cudaMemcpyDeviceToHost));
     if (surv_bits)
-        SG_CUDA(cudaMemcpy(surv_bits, C->bw.vbits, sizeof(uint64_t) * L->D_local, cudaMemcpyDeviceToHost));
+        SG_CUDA(cudaMemcpy(surv_bits, tc ? C->tw.vbits : C->bw.vbits, sizeof(uint64_t) * L->D_local,
+                           cudaMemcpyDeviceToHost));
     if (bad) return fail(SG_ERR_DATA, "ffn input has non-finite entries");  // ffn_exec.hpp:61-63
     return SG_OK;
 }
@@ -1107,7 +1318,7 @@ sg_status sg_ffn_forward_layers_host(sg_ctx* C, const sg_layer* const* layers, i
         C->xs_cap = need;
     }
     auto st = static_cast<cudaStream_t>(stream);
-    SG_CUDA(cudaMemcpyAsync(C->xsdev, xs_host, chain ? d * 4 : need, cudaMemcpyHostToDevice, st));
+    SG_CUDA(cudaMemcpyAsync(C->xsdev, xs_host, chain == 1 ? d * 4 : need, cudaMemcpyHostToDevice, st));
     if (sg_status s = sg_ffn_forward_layers(C, layers, n, pipeline, C->xsdev, C->ysdev, chain, stream);
         s != SG_OK)
         return s;

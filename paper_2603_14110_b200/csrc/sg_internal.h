@@ -2,6 +2,8 @@
 // code (sg_kernels.cu). Not part of the public ABI (include/sparsegate_c.h).
 #pragma once
 
+#include <cuda.h>
+
 #include <cstdint>
 
 namespace sg {
@@ -121,5 +123,54 @@ struct BatchArgs {
 };
 int batch_max();
 int launch_batch(const BatchArgs& a, const float* xs, float* ys, void* stream);
+
+// Batched decode on the tensor cores (sg_batch_tc.cu): one persistent launch per
+// layer, tcgen05.mma with TMEM accumulators, weight rows by TMA tile::gather4.
+struct TcMaps {            // TMA tensor maps (bf16, SWIZZLE_128B, 64-element inner box)
+    CUtensorMap xhl;       // X^T hi/lo   [N][pitch_d]        box {64, N}
+    CUtensorMap thl;       // T^T hi/lo   [N][pitch_r]        box {64, N}
+    CUtensorMap zhl;       // Z^T hi/lo   [N][zpitch]         box {64, N}
+    CUtensorMap Bp;        // predictor B [r][pitch_d]        box {64, 128}
+    CUtensorMap A;         // predictor A [D][pitch_r]        box {64, 128}
+    CUtensorMap gate;      // gate rows   [D][pitch_d]        box {64, 1} (gather4)
+    CUtensorMap up;        // up rows     [D][pitch_d], row stride 2*pitch_d (ud, first half)
+    CUtensorMap down;      // down rows   [D][pitch_d], row stride 2*pitch_d (ud + pitch_d)
+};
+struct TcArgs {
+    int B, nb, N;          // tokens, B rounded up to 8, MMA N = 2*nb (hi | lo columns)
+    int d, D, r, pitch_d, pitch_r, act;
+    int nblk;              // neuron blocks of 256
+    int kst;               // K of a T unit (the KT = u_TR - u_T slices)
+    int KSg, ksg, KSu, ksu;  // gate / up K slices and their width
+    int ndt, S;            // d tiles of 256 outputs, block ranges of the down GEMM
+    int dense;             // 1: dense comparator (no predictor; every row)
+    int u_T, u_TR, u_PRE, u_GATE, u_UP, u_DOWN, u_YR, u_end;  // unit index ranges
+    int zpitch;            // slots of Z^T per row (nblk * 256)
+    int xpitch;            // elements per X^T row (the ctx's max pitch; T^T rows are 256)
+    const float* x;        // [B][d] input tokens
+    float* y;              // [B][d] outputs
+    const float* bias;     // [D]
+    uint16_t* xhl;         // [N][pitch_d]
+    float* tpart;          // [KT][256][nb]
+    uint16_t* thl;         // [N][pitch_r]
+    uint64_t* mbits;       // [D] predicted bit per token
+    uint64_t* vbits;       // [D] survivor bit per token
+    int* ulist;            // [nblk][256] union rows of a block (local row in block), ascending
+    int* ucnt;             // [nblk]
+    int* vlist;            // [nblk][256] survivor rows of a block, ascending
+    int* vcnt;             // [nblk]
+    float* gpart;          // [KSg-1][nblk][256][nb]
+    float* upart;          // [KSu-1][nblk][256][nb]
+    float* G;              // [D][nb] gate pre-activations of the union rows
+    uint16_t* zhl;         // [N][zpitch]
+    float* ypart;          // [S][ndt*256][nb]
+    int* pcount;           // [64] |P_b|   (pcount, vcount, bad: zeroed by the host per call)
+    int* vcount;           // [64] |V_b|
+    int* bad;              // non-finite input flag
+    int* flags;            // dataflow counters, reset by the last CTA of every launch
+};
+int tc_smem_bytes();
+int tc_flag_ints(int nblk, int ndt);
+int launch_batch_tc(const TcMaps& maps, const TcArgs& a, int grid, void* stream);
 
 }  // namespace sg

@@ -484,26 +484,32 @@ __device__ __forceinline__ bool stage_x(const float* x, int d, int pitch_d, floa
 
 // Inside a stack, layer l+1 starts without a grid barrier: phase D of layer l
 // publishes y as tagged values and the next stage x polls them (chained: all
-// of y is the next x; unchained: one value per CTA slice, which orders the
-// layers — a CTA only reuses ypart once every CTA has finished reading it).
-__device__ __forceinline__ bool stage_x_poll(const float* x, const WorkView& W, int d, int pitch_d,
-                                             float* xs, uint32_t tag) {
+// of y is the next x — plus, for the residual chain, this layer's own token
+// xres: x_{l+1} = h_{l+1} + y_l, the residual-stream dependency of a decoder;
+// unchained: one value per CTA slice, which orders the layers — a CTA only
+// reuses ypart once every CTA has finished reading it).
+__device__ __forceinline__ bool stage_x_poll(const float* x, const float* xres, const WorkView& W,
+                                             int d, int pitch_d, float* xs, uint32_t tag) {
     bool bad = false;
     const int tid = threadIdx.x;
     if (x == nullptr) {
         constexpr int kIn = 8;
         for (int i0 = tid; i0 < pitch_d; i0 += kIn * kThreads) {
             uint32_t v[kIn], t[kIn];
+            float h[kIn];
 #pragma unroll
             for (int k = 0; k < kIn; ++k) {
                 const int i = i0 + k * kThreads;
                 v[k] = 0u;
                 t[k] = tag;
-                if (i < d)
+                h[k] = 0.f;
+                if (i < d) {
                     asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];"
                                  : "=r"(v[k]), "=r"(t[k])
                                  : "l"(W.ytag + 2 * i)
                                  : "memory");
+                    if (xres) h[k] = __ldcg(xres + i);
+                }
             }
 #pragma unroll
             for (int k = 0; k < kIn; ++k) {
@@ -511,6 +517,7 @@ __device__ __forceinline__ bool stage_x_poll(const float* x, const WorkView& W, 
                 if (i >= pitch_d) continue;
                 float f = __uint_as_float(v[k]);
                 if (t[k] != tag) f = ld_tagged(W.ytag + 2 * i, tag);
+                if (xres) f = h[k] + f;
                 xs[i] = f;
                 bad |= !isfinite(f);
             }
@@ -1323,7 +1330,7 @@ __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm
 template <int kPipe>
 __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
                           const SmemPlan& S, RunState& rs, const float* x, float* y,
-                          bool first_layer, bool chained, int lidx, bool want_sets,
+                          bool first_layer, int chain, int lidx, bool want_sets,
                           const LayerView* next, bool prestaged) {
     const int c = blockIdx.x, tid = threadIdx.x;
 #ifdef SG_PHASE_TIMING
@@ -1350,7 +1357,8 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
     // no grid barrier between the layers of a stack: the previous layer's y
     // arrives tagged (its tag: the partial barrier it followed)
     const bool bad = first_layer ? stage_x(x, L.d, L.pitch_d, sm.xs)
-                                 : stage_x_poll(chained ? nullptr : x, W, L.d, L.pitch_d, sm.xs,
+                                 : stage_x_poll(chain ? nullptr : x, chain == 2 ? x : nullptr, W,
+                                                L.d, L.pitch_d, sm.xs,
                                                 rs.tag0 + rs.bar_k);
     if (c == 0 && tid == 0) {
         // p and v (stats[0], [1]) are zeroed by the host before the launch
@@ -1443,13 +1451,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const LayerView L = sm.lv[l & 1];
         const LayerView* next = (layers && l + 1 < nlayers) ? layers + l + 1 : nullptr;
-        const float* x = (chain && l > 0) ? ys + static_cast<size_t>(l - 1) * xstride
-                                          : xs + static_cast<size_t>(l) * xstride;
+        // chain 1: x_l = y_{l-1}; chain 2 (residual): x_l = xs_l + y_{l-1}; 0: x_l = xs_l
+        const float* x = (chain == 1 && l > 0) ? ys + static_cast<size_t>(l - 1) * xstride
+                                               : xs + static_cast<size_t>(l) * xstride;
         float* y = ys + static_cast<size_t>(l) * xstride;
         WorkView Wl = W;
         Wl.stats = W.stats + 4 * l;  // per-layer {p, v, nonfinite, pipeline}
         Wl.bitpos = l;
-        prestaged = run_layer<kPipe>(L, Wl, sm, S, rs, x, y, l == 0, chain != 0, l, l == nlayers - 1,
+        prestaged = run_layer<kPipe>(L, Wl, sm, S, rs, x, y, l == 0, chain, l, l == nlayers - 1,
                                      next, prestaged);
         if (layers && l + 1 < nlayers) {
             if (threadIdx.x < kLvWords / 4) asm volatile("cp.async.wait_all;" ::: "memory");

@@ -357,6 +357,21 @@ class DeviceLayer:
         V = [np.sort(gidx[((vb >> np.uint64(b)) & np.uint64(1)).astype(bool)]) for b in range(B)]
         return Y.astype(np.float64), [ExecStats.from_c(s) for s in st], P, V
 
+    def forward_batch_dense(self, X, ctx: Optional[Context] = None) -> np.ndarray:
+        """Dense batched comparator (sg_ffn_forward_batch_dense): dense_ffn for every token
+        of X (B, hidden), every row read once on the tensor cores. Returns Y (B, hidden)."""
+        import torch
+        ctx = ctx or self.context()
+        X = np.ascontiguousarray(np.asarray(X, dtype=np.float32))
+        xt = torch.tensor(X, device=f"cuda:{self.device}")
+        yt = torch.zeros_like(xt)
+        sh = torch.cuda.current_stream(self.device).cuda_stream
+        check(capi.lib().sg_ffn_forward_batch_dense(ctx.handle, self.handle, C.c_void_p(xt.data_ptr()),
+                                                    X.shape[0], C.c_void_p(yt.data_ptr()),
+                                                    C.c_void_p(sh)))
+        check(capi.lib().sg_ctx_read_batch(ctx.handle, C.c_void_p(sh), X.shape[0], None, None, None))
+        return yt.double().cpu().numpy()
+
     def predict_mask(self, x, ctx: Optional[Context] = None, stream: int = 0) -> Mask:
         ctx = ctx or self.context()
         x = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1))

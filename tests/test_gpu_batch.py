@@ -1,5 +1,9 @@
 """GPU parity of batched decode (sg_ffn_forward_batch, BASELINE.json configs[4]).
 
+B >= 2 runs the tensor-core kernel (csrc/sg_batch_tc.cu: tcgen05.mma, TMEM
+accumulators, TMA tile::gather4 of the union rows); B = 1 the persistent
+single-token executor.
+
 Every token of a batch must get its own single-token result: its predicted and
 survivor sets (bit-exact up to the near-threshold band) and y (Y_RTOL), against
 the f64 oracle run on that token alone (tests/parity_util.py rules), and the
@@ -50,7 +54,7 @@ def test_batch_full_size_7b():
     layer = upload(h, d, D, 0, 256)
     q = _host_q(h)
     Y, stats, P, V = layer.forward_batch(h.xs.T)
-    for b in (0, 7, 15):
+    for b in range(16):
         diag = check_token(q, h.xs[:, b], Y[b], P[b], V[b])
         assert diag["rel"] <= Y_RTOL
 
@@ -64,3 +68,63 @@ def test_batch_rejects_bad_input():
     bad[1, 3] = np.nan
     with pytest.raises(DataError):
         layer.forward_batch(bad)
+
+
+@pytest.mark.parametrize("d,D,r,act", [(500, 1000, 64, 0), (512, 1408, 256, 1), (1024, 3000, 128, 0)])
+def test_batch_ragged_shapes_and_drelu(d, D, r, act):
+    """hidden not a multiple of 64, inter not a multiple of the 256-neuron block,
+    rank 64 / 128 / 256 (one or two M = 128 predictor sub-tiles), dReLU."""
+    from paper_2603_14110_b200 import Activation
+    fx, pred = _calibrated_layer(d, D, r, seed=21 + d, calib=1024, act=Activation(act))
+    q = quantize_layer(fx.weights.gate, fx.weights.up, fx.weights.down, pred.A, pred.B, pred.bias)
+    layer = DeviceLayer(fx.weights, pred)
+    rng = np.random.default_rng(d)
+    for B in (2, 9, 33):
+        X = fx.eval[:, rng.integers(0, fx.eval.shape[1], B)].T + 0.1 * rng.standard_normal((B, d))
+        Y, stats, P, V = layer.forward_batch(X)
+        for b in range(B):
+            diag = check_token(q, X[b], Y[b], P[b], V[b], act=act)
+            assert diag["rel"] <= Y_RTOL
+
+
+@pytest.mark.parametrize("B", [2, 8, 16, 40, 64])
+def test_dense_batch_matches_single_token_dense(B):
+    """sg_ffn_forward_batch_dense (every row on the tensor cores) against the dense
+    executor per token (ffn_exec.hpp:103-122), and against the f64 dense oracle."""
+    import oracle as O
+    d, D, r = 512, 2048, 64
+    fx, pred = _calibrated_layer(d, D, r, seed=4, calib=1024)
+    q = quantize_layer(fx.weights.gate, fx.weights.up, fx.weights.down, pred.A, pred.B, pred.bias)
+    layer = DeviceLayer(fx.weights, pred)
+    rng = np.random.default_rng(B)
+    X = fx.eval[:, rng.integers(0, fx.eval.shape[1], B)].T + 0.1 * rng.standard_normal((B, d))
+    X = X.astype(np.float32).astype(np.float64)
+    Y = layer.forward_batch_dense(X)
+    for b in range(B):
+        ref, _ = O.dense_ffn(q["gate"], q["up"], q["down"], X[b])
+        assert np.linalg.norm(Y[b] - ref) <= Y_RTOL * np.linalg.norm(ref)
+        one = layer.forward(X[b], Pipeline.Dense).y
+        assert np.linalg.norm(Y[b] - one) <= Y_RTOL * np.linalg.norm(one)
+
+
+def test_batch_device_entry_flags_nonfinite():
+    """The device entry has no host check: the kernel flags a non-finite token and
+    sg_ctx_read_batch raises DataError (ffn_exec.hpp:61-63)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2603_14110_b200 import _capi as capi
+    from paper_2603_14110_b200.ffn_exec import check
+    fx, pred = _calibrated_layer(256, 768, 32, seed=6)
+    layer = DeviceLayer(fx.weights, pred)
+    ctx = layer.context()
+    for B in (1, 5, 20):
+        X = torch.tensor(np.tile(fx.eval[:, :1].T, (B, 1)), dtype=torch.float32, device="cuda")
+        X[B - 1, 7] = float("inf")
+        Y = torch.zeros_like(X)
+        sh = torch.cuda.current_stream().cuda_stream
+        check(capi.lib().sg_ffn_forward_batch(ctx.handle, layer.handle, C.c_void_p(X.data_ptr()), B,
+                                              C.c_void_p(Y.data_ptr()), C.c_void_p(sh)))
+        with pytest.raises(DataError):
+            check(capi.lib().sg_ctx_read_batch(ctx.handle, C.c_void_p(sh), B, None, None, None))
