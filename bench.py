@@ -457,7 +457,7 @@ def main():
                          "(this synthetic FFN shrinks y ~100x per layer, so the operating point "
                          "drifts); 0: every layer reads its own token (the unchained line is "
                          "reported too)")
-    ap.add_argument("--mode", default="stack", choices=["stack", "per-layer"])
+    ap.add_argument("--mode", default="stack", choices=["stack", "per-layer", "sharded"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-diag", action="store_true", help="skip the near-threshold diagnostics")
@@ -523,12 +523,24 @@ def main():
     ys = torch.zeros_like(xs)
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
-    is_stack = args.mode == "stack" and world == 1
-    if copies > 1 or (not is_stack and args.chain == 2):
-        # rotated copies of one layer are independent; per-layer launches (N > 1) take
-        # one x pointer per layer, so no residual add between them
-        args.chain = 0
+    # N > 1 (or --mode sharded): the C++ sharded step (csrc/sg_comm.cpp) — per-layer
+    # launches on this rank's d_ff shard + one NCCL all-reduce per layer, from C++
+    sharded = world > 1 or args.mode == "sharded"
+    is_stack = args.mode == "stack" and not sharded
+    if copies > 1:
+        args.chain = 0  # rotated copies of one layer are independent
     chain = args.chain
+    comm = None
+    if sharded:
+        uid = (C.c_uint8 * 128)()
+        if rank == 0:
+            check(lib.sg_comm_unique_id(uid))
+        if world > 1:
+            obj = [bytes(uid)]
+            torch.distributed.broadcast_object_list(obj, src=0)
+            C.memmove(uid, obj[0], 128)
+        comm = C.c_void_p()
+        check(lib.sg_comm_create(local, world, rank, uid, C.byref(comm)))
 
     def step_stack(pipe=Pipeline.Sequential, ch=None, s=None):
         check(lib.sg_ffn_forward_layers(ctx.handle, arr, Ls, int(pipe), C.c_void_p(xs.data_ptr()),
@@ -536,13 +548,16 @@ def main():
                                         C.c_void_p(sh if s is None else s)))
 
     def step_layers(pipe=Pipeline.Sequential, s=None):
+        if sharded:
+            check(lib.sg_ffn_forward_layers_sharded(ctx.handle, comm, arr, Ls, int(pipe),
+                                                    C.c_void_p(xs.data_ptr()), C.c_void_p(ys.data_ptr()),
+                                                    chain, C.c_void_p(sh if s is None else s)))
+            return
         for l in range(Ls):
             src = ys[l - 1] if (chain == 1 and l > 0) else xs[l]
             check(lib.sg_ffn_forward_device(ctx.handle, layers[l].handle, int(pipe),
                                             C.c_void_p(src.data_ptr()),
                                             C.c_void_p(ys[l].data_ptr()), C.c_void_p(sh if s is None else s)))
-            if world > 1:
-                torch.distributed.all_reduce(ys[l])
 
     launches_per_step = 1 if is_stack else Ls
 
@@ -626,6 +641,9 @@ def main():
                                                  V.ctypes.data_as(C.c_void_p), C.byref(v)))
                 sets.append((P[:p.value].astype(np.int64), V[:v.value].astype(np.int64)))
             check(lib.sg_ctx_enable_stack_sets(ctx.handle, 0))
+    elif sharded:
+        step_layers()
+        check(lib.sg_ctx_read_stack_stats(ctx.handle, C.c_void_p(sh), Ls, stats))
     else:
         for l in range(Ls):
             src = ys[l - 1] if (chain == 1 and l > 0) else xs[l]
@@ -664,13 +682,13 @@ def main():
         stream.synchronize()
 
     ke = max(10, min(args.steps, 500))
-    ms_e2e, _ = timed(step_e2e if world == 1 else step_e2e_sharded, ke, 3)
+    ms_e2e, _ = timed(step_e2e if not sharded else step_e2e_sharded, ke, 3)
     h2d = (d if chain == 1 else Ls * d) * 4
     e2e = {"value": 1000.0 * copies / ms_e2e if copies > 1 else 1000.0 / ms_e2e, "unit": "tokens/s",
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": Ls * d * 4, "ms_per_step": ms_e2e,
            "steps": ke,
-           "call": "sg_ffn_forward_layers_host" if world == 1 else
-                   "H2D + per-layer sg_ffn_forward_device + NCCL all_reduce + D2H"}
+           "call": "sg_ffn_forward_layers_host" if not sharded else
+                   "H2D + sg_ffn_forward_layers_sharded (launches + NCCL all-reduces from C++) + D2H"}
 
     dense = None
     if not args.no_dense:
@@ -714,7 +732,9 @@ def main():
             "layout": "ascending" if args.no_balance else
                       "per-CTA load-balanced neuron order from calibration statistics",
             "hot_rows": 0 if args.no_balance else args.hot_rows,
-            "mode": "stack (one persistent launch per step)" if is_stack else "per-layer launches",
+            "mode": "stack (one persistent launch per step)" if is_stack else
+                    ("C++ sharded step: per-layer launches + one NCCL all-reduce per layer "
+                     "(sg_ffn_forward_layers_sharded)" if sharded else "per-layer launches"),
             "graph": graph_mode})
         line = {
             "metric": "sparse-FFN decode tokens/s", "value": tok_s, "unit": "tokens/s",
@@ -739,6 +759,8 @@ def main():
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        lib.sg_comm_destroy(comm)
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0

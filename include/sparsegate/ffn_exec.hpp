@@ -11,105 +11,34 @@
 //   gating_error           ffn_exec.hpp:256-285
 //   FfnWeights / Predictor / validate   types.hpp:21-105
 //   Error / IoError / DataError / PropertyViolation   common.hpp:20-37
-// The reference's Mat / Vec are Eigen row-major double matrices / vectors;
-// Eigen is not part of this build, so minimal containers with the members the
-// reference code uses (rows, cols, size, data, operator(), Zero, Identity) stand
-// in. Values are f64 on the host; the device computes in bf16 weights / fp32
-// arithmetic.
+// Mat / Vec / the domain types come from sparsegate/common.hpp and types.hpp:
+// the reference's own Eigen types when <Eigen/Dense> is available, minimal
+// stand-ins otherwise. Values are f64 on the host; the device computes with bf16
+// weights and fp32 arithmetic.
 //
 // The reference functions are stateless. A GPU needs resident weights, so the
 // stateless calls here keep a per-thread cache of device layers keyed by the
-// weight / predictor buffers (address, shape and a strided content
-// fingerprint); call sparsegate::gpu::clear_cache() after mutating weights in
-// place, or use the explicit sparsegate::gpu::Layer / Context objects.
+// weight / predictor buffers (address, shape and a digest of their full
+// contents: an in-place change re-uploads — and re-validates — the layer, as the
+// reference validates on every call), or use the explicit
+// sparsegate::gpu::Layer / Context objects.
 #pragma once
 
+#include "sparsegate/types.hpp"
 #include "sparsegate_c.h"
 
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
-#include <initializer_list>
 #include <map>
 #include <memory>
-#include <stdexcept>
 #include <string>
 #include <tuple>
 #include <utility>
 #include <vector>
 
 namespace sparsegate {
-
-using Index = std::int64_t;
-
-// ---- containers (row-major double, like the reference's Eigen types) ----
-class Mat {
-   public:
-    Mat() = default;
-    Mat(Index rows, Index cols) : r_(rows), c_(cols), v_(static_cast<size_t>(rows * cols), 0.0) {}
-    Mat(std::initializer_list<std::initializer_list<double>> rows) {
-        r_ = static_cast<Index>(rows.size());
-        c_ = r_ ? static_cast<Index>(rows.begin()->size()) : 0;
-        for (const auto& row : rows) {
-            if (static_cast<Index>(row.size()) != c_) throw std::invalid_argument("ragged Mat literal");
-            v_.insert(v_.end(), row.begin(), row.end());
-        }
-    }
-    static Mat Zero(Index rows, Index cols) { return Mat(rows, cols); }
-    static Mat Identity(Index n) {
-        Mat m(n, n);
-        for (Index i = 0; i < n; ++i) m(i, i) = 1.0;
-        return m;
-    }
-    Index rows() const { return r_; }
-    Index cols() const { return c_; }
-    Index size() const { return r_ * c_; }
-    double* data() { return v_.data(); }
-    const double* data() const { return v_.data(); }
-    double& operator()(Index i, Index j) { return v_[static_cast<size_t>(i * c_ + j)]; }
-    double operator()(Index i, Index j) const { return v_[static_cast<size_t>(i * c_ + j)]; }
-
-   private:
-    Index r_ = 0, c_ = 0;
-    std::vector<double> v_;
-};
-
-class Vec {
-   public:
-    Vec() = default;
-    explicit Vec(Index n) : v_(static_cast<size_t>(n), 0.0) {}
-    Vec(std::initializer_list<double> v) : v_(v) {}
-    static Vec Zero(Index n) { return Vec(n); }
-    Index size() const { return static_cast<Index>(v_.size()); }
-    double* data() { return v_.data(); }
-    const double* data() const { return v_.data(); }
-    double& operator()(Index i) { return v_[static_cast<size_t>(i)]; }
-    double operator()(Index i) const { return v_[static_cast<size_t>(i)]; }
-    double& operator[](Index i) { return v_[static_cast<size_t>(i)]; }
-    double operator[](Index i) const { return v_[static_cast<size_t>(i)]; }
-
-   private:
-    std::vector<double> v_;
-};
-
-// ---- errors (common.hpp:20-37) ----
-struct Error : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-struct IoError : Error {
-    using Error::Error;
-};
-struct DataError : Error {
-    using Error::Error;
-};
-struct PropertyViolation : Error {
-    using Error::Error;
-};
-// Failures with no reference counterpart (CUDA / NCCL, bad arguments).
-struct DeviceError : Error {
-    using Error::Error;
-};
 
 namespace detail {
 inline void check(sg_status s) {
@@ -122,72 +51,7 @@ inline void check(sg_status s) {
         default: throw DeviceError(msg);
     }
 }
-inline bool all_finite(const double* p, Index n) {
-    for (Index i = 0; i < n; ++i)
-        if (!std::isfinite(p[i])) return false;
-    return true;
-}
 }  // namespace detail
-
-// ---- domain types (types.hpp) ----
-enum class Activation { ReGLU, DReLU };
-inline std::string to_string(Activation a) { return a == Activation::ReGLU ? "reglu" : "drelu"; }
-
-struct FfnWeights {
-    Mat gate;  // D x d
-    Mat up;    // D x d
-    Mat down;  // d x D
-    Activation activation = Activation::ReGLU;
-    Index hidden_size() const { return gate.cols(); }
-    Index inter_size() const { return gate.rows(); }
-};
-
-struct Predictor {
-    Mat A;     // D x r
-    Mat B;     // r x d
-    Vec bias;  // D (+inf allowed)
-    Index rank = 0;
-    Index hidden_size() const { return B.cols(); }
-    Index inter_size() const { return A.rows(); }
-};
-
-// types.hpp:31-51: same checks and DataError messages.
-inline void validate(const FfnWeights& w) {
-    const Index d = w.gate.cols(), D = w.gate.rows();
-    if (d < 1 || D < 1)
-        throw DataError("ffn weights: gate must be at least 1x1, got " + std::to_string(D) + "x" +
-                        std::to_string(d));
-    if (w.up.rows() != D || w.up.cols() != d)
-        throw DataError("ffn weights: up is " + std::to_string(w.up.rows()) + "x" +
-                        std::to_string(w.up.cols()) + ", expected " + std::to_string(D) + "x" +
-                        std::to_string(d));
-    if (w.down.rows() != d || w.down.cols() != D)
-        throw DataError("ffn weights: down is " + std::to_string(w.down.rows()) + "x" +
-                        std::to_string(w.down.cols()) + ", expected " + std::to_string(d) + "x" +
-                        std::to_string(D));
-    if (!detail::all_finite(w.gate.data(), w.gate.size()) ||
-        !detail::all_finite(w.up.data(), w.up.size()) ||
-        !detail::all_finite(w.down.data(), w.down.size()))
-        throw DataError("ffn weights: non-finite entries");
-}
-
-// types.hpp:82-105.
-inline void validate(const Predictor& p) {
-    if (p.A.cols() != p.B.rows())
-        throw DataError("predictor: rank mismatch, A is " + std::to_string(p.A.rows()) + "x" +
-                        std::to_string(p.A.cols()) + " but B is " + std::to_string(p.B.rows()) +
-                        "x" + std::to_string(p.B.cols()));
-    if (p.rank != p.A.cols()) throw DataError("predictor: rank field disagrees with factor shapes");
-    if (p.bias.size() != p.A.rows())
-        throw DataError("predictor: bias length " + std::to_string(p.bias.size()) +
-                        " does not match intermediate size " + std::to_string(p.A.rows()));
-    const Index hi = std::min(p.A.rows(), p.B.cols());
-    if (p.rank < 1 || p.rank > hi)
-        throw DataError("predictor: rank " + std::to_string(p.rank) + " out of range [1, " +
-                        std::to_string(hi) + "]");
-    if (!detail::all_finite(p.A.data(), p.A.size()) || !detail::all_finite(p.B.data(), p.B.size()))
-        throw DataError("predictor: non-finite factor entries");
-}
 
 // ---- executor types (ffn_exec.hpp:27-52) ----
 struct Mask {
@@ -334,21 +198,21 @@ class Layer {
 };
 
 namespace detail {
-// Strided fingerprint of a buffer (catches most in-place mutations cheaply).
-inline std::uint64_t mix64(std::uint64_t z) {  // splitmix64 finalizer: full avalanche
+// Digest of a buffer's full contents (64-bit FNV-1a over 8-byte words, then a
+// splitmix finaliser).
+inline std::uint64_t mix64(std::uint64_t z) {
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
     z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
     return z ^ (z >> 31);
 }
 inline std::uint64_t fingerprint(const double* p, Index n, std::uint64_t salt) {
-    std::uint64_t h = mix64(salt ^ static_cast<std::uint64_t>(n));
-    const Index step = n > 4096 ? n / 4096 : 1;
-    for (Index i = 0; i < n; i += step) {
+    std::uint64_t h = 0xcbf29ce484222325ull ^ mix64(salt ^ static_cast<std::uint64_t>(n));
+    for (Index i = 0; i < n; ++i) {
         std::uint64_t b;
         std::memcpy(&b, p + i, 8);
-        h = mix64(h ^ b);
+        h = (h ^ b) * 0x100000001b3ull;
     }
-    return h;
+    return mix64(h);
 }
 using Key = std::tuple<const void*, const void*, const void*, Index, Index, Index, int, std::uint64_t>;
 inline Key key_of(const FfnWeights* w, const Predictor* p) {
@@ -445,27 +309,35 @@ inline OpCounts op_count_model(std::int64_t d, std::int64_t D, std::int64_t r, d
     return c;
 }
 
-// ffn_exec.hpp:256-285: dropped gate mass under the (device) predictor mask;
-// the gate projection itself is evaluated on the host in f64.
+// ffn_exec.hpp:251-285: the exact dropped-gate-mass formula under the (device)
+// predictor mask; the gate projection is evaluated on the host in f64 with the
+// reference's det_dot / det_sum, and the closed form is cross-checked against
+// the direct masked difference as the reference does.
 inline GatingError gating_error(const FfnWeights& w, const Predictor& pred, const Vec& x) {
     validate(w);
-    if (x.size() != w.hidden_size())
-        throw DataError("input length " + std::to_string(x.size()) + " does not match hidden size " +
+    if (x.size() != w.hidden_size())  // ffn_exec.hpp:58-63
+        throw DataError("ffn input length " + std::to_string(x.size()) + " does not match hidden size " +
                         std::to_string(w.hidden_size()));
-    if (!detail::all_finite(x.data(), x.size())) throw DataError("input: non-finite entries");
-    const Mask m = predict_mask(pred, x);
-    double e2 = 0.0, xx = 0.0;
-    for (Index i = 0; i < w.inter_size(); ++i) {
-        if (m.active[static_cast<size_t>(i)]) continue;
-        double g = 0.0;
-        for (Index j = 0; j < w.hidden_size(); ++j) g += w.gate(i, j) * x[j];
-        if (g > 0.0) e2 += g * g;
+    if (!all_finite(x)) throw DataError("ffn input has non-finite entries");
+    const Mask mask = predict_mask(pred, x);
+    const Index D = w.inter_size(), d = w.hidden_size();
+    std::vector<double> formula_terms(static_cast<size_t>(D)), direct_terms(static_cast<size_t>(D));
+    for (Index i = 0; i < D; ++i) {
+        const double a = relu(det_dot(w.gate.data() + i * d, x.data(), static_cast<size_t>(d)));
+        const bool on = mask.active[static_cast<size_t>(i)] != 0;
+        formula_terms[static_cast<size_t>(i)] = on ? 0.0 : a * a;
+        const double diff = a - (on ? a : 0.0);
+        direct_terms[static_cast<size_t>(i)] = diff * diff;
     }
-    for (Index j = 0; j < x.size(); ++j) xx += x[j] * x[j];
-    if (xx == 0.0) throw DataError("gating error: zero input has no relative form");
+    const double formula = std::sqrt(det_sum(formula_terms.data(), formula_terms.size()));
+    const double direct = std::sqrt(det_sum(direct_terms.data(), direct_terms.size()));
+    if (std::abs(formula - direct) > 1e-12 * std::max(1.0, std::abs(direct)))
+        throw PropertyViolation("gating error: closed form disagrees with direct difference");
+    const double x_norm = std::sqrt(det_dot(x.data(), x.data(), static_cast<size_t>(x.size())));
+    if (x_norm == 0.0) throw DataError("gating error: zero input has no relative form");
     GatingError err;
-    err.error_norm = std::sqrt(e2);
-    err.relative = err.error_norm / std::sqrt(xx);
+    err.error_norm = formula;
+    err.relative = formula / x_norm;
     return err;
 }
 

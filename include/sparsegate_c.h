@@ -237,6 +237,30 @@ sg_status sg_op_count_model(int64_t d, int64_t D, int64_t r, double s, double s_
 /* Host rounding used on upload: f64 -> f32 (RNE) -> bf16 (RNE), NaN-preserving. */
 void sg_round_bf16(const double* in, uint16_t* out, int64_t n);
 
+/* ---- multi-GPU: the d_ff-sharded decode step ----
+ * One process per GPU; every rank creates its shard of every layer
+ * (sg_layer_desc.shard_index / shard_count) and joins one communicator. A step runs
+ * each layer on the rank's shard and sums the d-sized partial outputs over ranks
+ * with one NCCL all-reduce per layer, all issued from C++ on `stream` (capturable
+ * in one CUDA graph). NCCL is loaded with dlopen("libnccl.so.2"). */
+typedef struct sg_comm sg_comm;
+/* 128-byte NCCL unique id, created on one rank and shared with the others. */
+sg_status sg_comm_unique_id(void* id128);
+sg_status sg_comm_create(int32_t device, int32_t nranks, int32_t rank, const void* id128, sg_comm** out);
+sg_status sg_comm_destroy(sg_comm* comm);
+int32_t sg_comm_size(const sg_comm* comm);
+int32_t sg_comm_rank(const sg_comm* comm);
+/* In-place sum of `count` fp32 values over the ranks of `comm`. */
+sg_status sg_allreduce_sum(sg_comm* comm, float* buf, int64_t count, void* stream);
+/* Sharded multi-layer step: same xs / ys / chain semantics as sg_ffn_forward_layers
+ * (ys receives the WHOLE layer outputs on every rank); per-layer stats of the rank's
+ * shard via sg_ctx_read_stack_stats (sum |P|, |V| over ranks for the whole layer). */
+sg_status sg_ffn_forward_layers_sharded(sg_ctx* ctx, sg_comm* comm, const sg_layer* const* layers,
+                                        int32_t n, sg_pipeline pipeline, const float* xs, float* ys,
+                                        int32_t chain, void* stream);
+/* Hidden size of a layer. */
+int64_t sg_layer_hidden(const sg_layer* layer);
+
 /* ---- multi-GPU sharding, pure host ----
  * The neuron set a shard holds: global index of local k = base + k*stride,
  * k in [0, count). Exactly the mapping sg_layer_create applies. */
@@ -275,6 +299,35 @@ sg_status sg_synthetic_fixture_bf16(int64_t hidden, int64_t inter, int64_t calib
 sg_status sg_greedy_calibrate(const double* scores, const double* weights, int64_t inter,
                               int64_t T, int32_t eta, double target_sparsity, double* bias,
                               double* achieved_sparsity, double* total_damage);
+
+/* ---- offline producer (csrc/sg_offline.cu): the predictor
+ * factors and calibration inputs in C++ without Eigen, large products on the GPU
+ * (current device). All arrays row-major f64 host buffers.
+ * svd_mode: 0 = exact (one-sided Jacobi, host; small shapes), 1 = randomized
+ * (range finder of width k + 8, 2 power iterations, CholeskyQR2 on the GPU). */
+
+/* factorization.hpp:31-64: S = chol(X X^T + lambda I) (d x d lower) and S^-1, with the
+ * damping ladder lambda = multipliers[k] * epsilon * trace(X X^T) / d tried in order;
+ * X is d x T (hidden x tokens). SG_ERR_DATA when every rung fails. */
+sg_status sg_cholesky_whitening(const double* X, int64_t d, int64_t T, double epsilon,
+                                const double* multipliers, int32_t n_mult, double* S, double* S_inv,
+                                double* lambda);
+/* factorization.hpp:93-144: A (D x rank) = U_r diag(s_r), B (rank x d) = V_r^T [S^-1] from
+ * the SVD of W S (whitened != 0) or W; sv receives the first n_sv singular values of
+ * that target, sigma_r1 = sigma_{rank+1}(W), lambda the damping used. */
+sg_status sg_build_predictor(const double* W, int64_t D, int64_t d, const double* X, int64_t T,
+                             int64_t rank, int32_t whitened, int32_t svd_mode, uint64_t seed,
+                             double epsilon, const double* multipliers, int32_t n_mult, double* A,
+                             double* B, double* sv, int64_t n_sv, double* sigma_r1, double* lambda);
+/* The k largest singular values of M (rows x cols). */
+sg_status sg_singular_values(const double* M, int64_t rows, int64_t cols, int32_t svd_mode, int64_t k,
+                             uint64_t seed, double* out);
+/* calibration.hpp:39-46: scores (D x T) = A (B X). */
+sg_status sg_proxy_scores(const double* A, const double* B, int64_t D, int64_t r, int64_t d,
+                          const double* X, int64_t T, double* scores);
+/* calibration.hpp:20-37: weights (D x T) = (act(gate X) * up'(X))^2 * |down column|^2. */
+sg_status sg_damage_weights(const double* gate, const double* up, const double* down, int64_t D,
+                            int64_t d, int32_t activation, const double* X, int64_t T, double* weights);
 
 #ifdef __cplusplus
 }  /* extern "C" */

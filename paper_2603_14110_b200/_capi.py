@@ -87,6 +87,14 @@ SYMBOLS = [
     ("sg_ffn_forward_batch_host", C.c_int, [_VP, _VP, _VP, _I32, _VP, C.POINTER(sg_exec_stats), _VP]),
     ("sg_ctx_enable_phase_timing", C.c_int, [_VP, _I32]),
     ("sg_ctx_read_phase_timing", C.c_int, [_VP, _VP, _I32, _VP, C.POINTER(_I32)]),
+    ("sg_comm_unique_id", C.c_int, [_VP]),
+    ("sg_comm_create", C.c_int, [_I32, _I32, _I32, _VP, C.POINTER(_VP)]),
+    ("sg_comm_destroy", C.c_int, [_VP]),
+    ("sg_comm_size", _I32, [_VP]),
+    ("sg_comm_rank", _I32, [_VP]),
+    ("sg_allreduce_sum", C.c_int, [_VP, _VP, _I64, _VP]),
+    ("sg_ffn_forward_layers_sharded", C.c_int, [_VP, _VP, _VP, _I32, C.c_int, _VP, _VP, _I32, _VP]),
+    ("sg_layer_hidden", _I64, [_VP]),
     ("sg_op_count_model", C.c_int, [_I64, _I64, _I64, _D, _D, C.POINTER(_I64), C.POINTER(_D),
                                     C.POINTER(_D)]),
     ("sg_round_bf16", None, [_VP, _VP, _I64]),
@@ -98,6 +106,12 @@ SYMBOLS = [
                                        _VP, _VP]),
     ("sg_synthetic_fixture_bf16", C.c_int, [_I64, _I64, _I64, _I64, _D, C.c_uint64, _VP, _VP,
                                             _VP, _VP, _VP]),
+    ("sg_cholesky_whitening", C.c_int, [_VP, _I64, _I64, _D, _VP, _I32, _VP, _VP, C.POINTER(_D)]),
+    ("sg_build_predictor", C.c_int, [_VP, _I64, _I64, _VP, _I64, _I64, _I32, _I32, C.c_uint64, _D, _VP,
+                                     _I32, _VP, _VP, _VP, _I64, C.POINTER(_D), C.POINTER(_D)]),
+    ("sg_singular_values", C.c_int, [_VP, _I64, _I64, _I32, _I64, C.c_uint64, _VP]),
+    ("sg_proxy_scores", C.c_int, [_VP, _VP, _I64, _I64, _I64, _VP, _I64, _VP]),
+    ("sg_damage_weights", C.c_int, [_VP, _VP, _VP, _I64, _I64, _I32, _VP, _I64, _VP]),
     ("sg_greedy_calibrate", C.c_int, [_VP, _VP, _I64, _I64, _I32, _D, _VP, C.POINTER(_D),
                                       C.POINTER(_D)]),
 ]

@@ -363,9 +363,45 @@ sg_status stack_launch(sg_ctx* C, const sg_layer* const* layers, int32_t n,
 
 }  // namespace
 
+// ---- internals shared with sg_comm.cpp (the sharded stack) ----
+sg_status sg_internal_fail(sg_status st, const std::string& msg) { return fail(st, msg); }
+
+// Validates a stack for a sequence of per-layer launches and zeroes its stats slots.
+sg_status sg_internal_begin_stack(sg_ctx* C, const sg_layer* const* layers, int32_t n, sg_pipeline pipeline,
+                                  void* stream) {
+    if (C == nullptr || layers == nullptr || n < 1 || n > kMaxStackLayers) return fail(SG_ERR_USAGE, "bad arguments");
+    for (int i = 0; i < n; ++i) {
+        if (sg_status s = check_pair(C, layers[i]); s != SG_OK) return s;
+        if (layers[i]->d != layers[0]->d) return fail(SG_ERR_USAGE, "all layers of a stack must share hidden");
+        if (pipeline != SG_PIPELINE_DENSE && !layers[i]->has_pred)
+            return fail(SG_ERR_USAGE, "sparse pipeline needs layers with predictors");
+        if (!layers[i]->has_w) return fail(SG_ERR_USAGE, "predictor-only layer cannot run the FFN");
+    }
+    DeviceGuard dg(C->device);
+    SG_CUDA(cudaMemsetAsync(C->W.stats, 0, static_cast<size_t>(n) * 4 * sizeof(int), static_cast<cudaStream_t>(stream)));
+    C->last_stack.assign(layers, layers + n);
+    C->last_pipeline = pipeline;
+    C->last_layer = layers[n - 1];
+    C->last_stack_bits = false;
+    return SG_OK;
+}
+
+// One layer launch writing stats slot `slot` (the stack's per-layer {p, v, bad, pipe}).
+sg_status sg_internal_forward_layer(sg_ctx* C, const sg_layer* L, sg_pipeline pipeline, const float* x,
+                                    const float* xres, float* y, int slot, void* stream) {
+    DeviceGuard dg(C->device);
+    sg::WorkView W = work_for(C, x, y);
+    W.xres = xres;
+    W.stats = C->W.stats + 4 * slot;
+    const int e = sg::launch_layer(L->view, W, pipeline, C->G, stream);
+    if (e != 0) return fail(SG_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
+    return SG_OK;
+}
+
 extern "C" {
 
 const char* sg_last_error(void) { return g_err.c_str(); }
+int64_t sg_layer_hidden(const sg_layer* L) { return L ? L->d : 0; }
 const char* sg_version(void) { return "sparsegate-b200 0.1 (sm_100a)"; }
 
 sg_status sg_op_count_model(int64_t d, int64_t D, int64_t r, double s, double sp, int64_t* dense,
@@ -657,7 +693,7 @@ sg_status sg_ctx_create(int32_t device, int64_t max_hidden, int64_t max_inter, i
     const size_t o_rec = take(Dm * 8), o_V = take(Dm * 4), o_zV = take(Dm * 4);
     const size_t o_vseg = take(Dm * 8);
     const size_t o_zD = take(Dm * 4);
-    const size_t o_ypart = take(static_cast<size_t>(G) * C->pitch_dmax * 4);
+    const size_t o_ypart = take(static_cast<size_t>(G) * C->pitch_dmax * 8);
     const size_t o_bar = take(8 * 256);
     const size_t o_ytag = take(static_cast<size_t>(C->pitch_dmax) * 8);
     const size_t o_stats = take(4 * 4 * kMaxStackLayers);
@@ -686,7 +722,7 @@ sg_status sg_ctx_create(int32_t device, int64_t max_hidden, int64_t max_inter, i
     W.V = reinterpret_cast<int*>(b + o_V);
     W.zV = reinterpret_cast<float*>(b + o_zV);
     W.zD = reinterpret_cast<float*>(b + o_zD);
-    W.ypart = reinterpret_cast<float*>(b + o_ypart);
+    W.ypart = reinterpret_cast<uint32_t*>(b + o_ypart);
     W.bar = reinterpret_cast<unsigned long long*>(b + o_bar);
     W.ytag = reinterpret_cast<uint32_t*>(b + o_ytag);
     W.stats = reinterpret_cast<int*>(b + o_stats);

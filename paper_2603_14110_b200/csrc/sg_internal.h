@@ -35,6 +35,7 @@ struct LayerView {
 // ctx's max_inter (Dmax), max_hidden (pitch) and the SM count (G).
 struct WorkView {
     const float* x;       // [d] input (caller's device buffer)
+    const float* xres;    // optional [d] added to x while it is staged (residual chains), or null
     float* y;             // [d] output (caller's device buffer)
     float* t;             // [pitch_r] predictor low-rank activations
     int* cnt;             // [2*gpad] per-CTA predicted counts, then survivor counts
@@ -47,7 +48,8 @@ struct WorkView {
     int* V;               // [Dmax] compacted GLOBAL survivor indices
     float* zV;            // [Dmax] gated value per survivor
     float* zD;            // [Dmax] dense pipeline: z per neuron
-    float* ypart;         // [G * pitch_dmax] dense pipeline: per-CTA partial outputs
+    uint32_t* ypart;      // [G * pitch_dmax] per-CTA partial outputs as {value bits, tag}
+                          // pairs: phase D polls them instead of a grid barrier
     uint32_t* ytag;       // [2 * pitch_dmax] {y bits, tag} published by phase D inside a stack
     unsigned long long* bar;  // 8 grid-barrier counters, 256 B apart (see grid_barrier)
     int* stats;           // [4 per layer] p, v, nonfinite(x), pipeline

@@ -308,6 +308,16 @@ __device__ __forceinline__ float ld_tagged(const void* p, uint32_t tag) {
     return __uint_as_float(v);
 }
 
+// 8 partial-y values of one chunk as tagged {value, tag} pairs (two 16-B stores:
+// each 8-B pair is one aligned half of a vector store, seen whole by a v2 load).
+__device__ __forceinline__ void st_partial8(uint32_t* dst, const float* v, uint32_t tag) {
+#pragma unroll
+    for (int e = 0; e < 8; e += 2)
+        asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %2};" ::"l"(dst + 2 * e),
+                     "r"(__float_as_uint(v[e])), "r"(tag), "r"(__float_as_uint(v[e + 1]))
+                     : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // Grid barrier on kBarCounters monotonically increasing 64-bit counters
 // (each in its own 256-B block, so they live in different L2 slices). CTA c
@@ -463,8 +473,19 @@ __device__ __forceinline__ void preissue_hot(const LayerView& L, const Smem& sm,
 }
 
 // Stage x (fp32, length d) into smem, zero-padded to pitch_d; flag non-finite.
-__device__ __forceinline__ bool stage_x(const float* x, int d, int pitch_d, float* xs) {
+// xres (optional): added element-wise (fp32) — x_l = xs_l + y_{l-1} of a residual
+// chain run as separate launches (the sharded path, sg_comm.cpp).
+__device__ __forceinline__ bool stage_x(const float* x, int d, int pitch_d, float* xs,
+                                        const float* xres = nullptr) {
     bool bad = false;
+    if (xres != nullptr) {
+        for (int i = threadIdx.x; i < pitch_d; i += kThreads) {
+            const float v = i < d ? __ldcg(xres + i) + __ldcg(x + i) : 0.f;
+            xs[i] = v;
+            bad |= !isfinite(v);
+        }
+        return __syncthreads_or(bad) != 0;
+    }
     if ((d & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
         for (int i = threadIdx.x * 4; i < pitch_d; i += kThreads * 4) {
             const float4 w = i < d ? __ldcg(reinterpret_cast<const float4*>(x + i))
@@ -1036,7 +1057,8 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
 // chunks t and t + 512 into its partial y, survivors in P order.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkView& W,
-                                                const Smem& sm, const SmemPlan& S, RunState& rs) {
+                                                const Smem& sm, const SmemPlan& S, RunState& rs,
+                                                uint32_t ptag) {
     const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nch = L.pitch_d >> 3;
     const int n0 = split_lo(c, gridDim.x, L.D);
@@ -1137,17 +1159,9 @@ __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkVi
         }
     }
     if (tid < 2) bu[tid] += (ngroups + 1 - tid) / 2;  // buffer 0: ceil(n/2), buffer 1: floor(n/2)
-    // this CTA's partial y
-    if (h0) {
-        float4* dst = reinterpret_cast<float4*>(W.ypart + static_cast<size_t>(c) * L.pitch_d + ch0 * 8);
-        dst[0] = make_float4(a0[0], a0[1], a0[2], a0[3]);
-        dst[1] = make_float4(a0[4], a0[5], a0[6], a0[7]);
-    }
-    if (h1) {
-        float4* dst = reinterpret_cast<float4*>(W.ypart + static_cast<size_t>(c) * L.pitch_d + ch1 * 8);
-        dst[0] = make_float4(a1[0], a1[1], a1[2], a1[3]);
-        dst[1] = make_float4(a1[4], a1[5], a1[6], a1[7]);
-    }
+    // this CTA's partial y, tagged with the layer's exchange tag (phase D polls it)
+    if (h0) st_partial8(W.ypart + 2 * (static_cast<size_t>(c) * L.pitch_d + ch0 * 8), a0, ptag);
+    if (h1) st_partial8(W.ypart + 2 * (static_cast<size_t>(c) * L.pitch_d + ch1 * 8), a1, ptag);
 }
 
 // ---------------------------------------------------------------------------
@@ -1157,7 +1171,7 @@ __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkVi
 // neuron range with z from zD; parallel: the survivor list of phase C.
 // ---------------------------------------------------------------------------
 template <int kPipe>
-__device__ void partial_down(const LayerView& L, const WorkView& W, const Smem& sm) {
+__device__ void partial_down(const LayerView& L, const WorkView& W, const Smem& sm, uint32_t ptag) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int nch = L.pitch_d >> 3;
     const int n0 = split_lo(c, G, L.D), n1 = split_lo(c + 1, G, L.D);
@@ -1204,9 +1218,7 @@ __device__ void partial_down(const LayerView& L, const WorkView& W, const Smem& 
             for (int u = 0; u < kU; ++u)
                 if (z[u] != 0.f) axpy8(w[u], z[u], acc);
         }
-        float4* dst = reinterpret_cast<float4*>(W.ypart + static_cast<size_t>(c) * L.pitch_d + ch * 8);
-        dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-        dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        st_partial8(W.ypart + 2 * (static_cast<size_t>(c) * L.pitch_d + ch * 8), acc, ptag);
     }
 }
 
@@ -1267,7 +1279,7 @@ __device__ __noinline__ void write_index_sets(int gbase, int gstride, const int*
 // its latency (divisions, parameter reads) hides under the barrier.
 struct DownPlan {
     int c0, ncols, ngrp, g0, g1;
-    const float* src;  // this thread's first partial (column c0 + tid % ncols)
+    const uint32_t* src;  // this thread's first tagged partial (column c0 + tid % ncols)
 };
 __device__ __forceinline__ DownPlan down_plan(const LayerView& L, const WorkView& W) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
@@ -1282,7 +1294,7 @@ __device__ __forceinline__ DownPlan down_plan(const LayerView& L, const WorkView
         const int grp = tid / p.ncols;
         p.g0 = split_lo(grp, p.ngrp, G);
         p.g1 = split_lo(grp + 1, p.ngrp, G);
-        p.src = W.ypart + static_cast<size_t>(p.g0) * L.pitch_d + p.c0 + tid % p.ncols;
+        p.src = W.ypart + 2 * (static_cast<size_t>(p.g0) * L.pitch_d + p.c0 + tid % p.ncols);
     }
     asm volatile("" ::"r"(p.c0), "r"(p.ncols), "r"(p.ngrp), "r"(p.g0), "r"(p.g1), "l"(p.src));
     return p;
@@ -1291,6 +1303,7 @@ __device__ __forceinline__ DownPlan down_plan(const LayerView& L, const WorkView
 template <int kPipe>
 __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm, float* y,
                            bool want_sets, bool publish, uint32_t ytag, const DownPlan& dp) {
+    const uint32_t ptag = ytag;  // the partials carry the same exchange tag
     const int tid = threadIdx.x;
     if (kPipe != 0 && want_sets && (tid >> 5) == kWarps)
         write_index_sets(L.gbase, L.gstride, L.gidx, L.D, W.cnt, W.plist, W.gN, W.vseg, W.P, W.gP,
@@ -1300,19 +1313,31 @@ __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm
     if (ncols > 0) {
         if (tid < ngrp * ncols) {
             const int g0 = dp.g0, g1 = dp.g1;
-            // all loads in flight before the (ordered) sum: one L2 round trip
+            // the partials are polled as tagged values (no grid barrier): all loads
+            // in flight at once, stragglers re-polled, then the fixed-order sum
             constexpr int kPer = 12;
-            const float* src = dp.src;
-            float v[kPer];
+            const uint32_t* src = dp.src;
+            uint32_t v[kPer], t[kPer];
 #pragma unroll
-            for (int i = 0; i < kPer; ++i)
-                v[i] = g0 + i < g1 ? __ldcg(src + static_cast<size_t>(i) * L.pitch_d) : 0.f;
+            for (int i = 0; i < kPer; ++i) {
+                v[i] = 0u;
+                t[i] = ptag;
+                if (g0 + i < g1)
+                    asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];"
+                                 : "=r"(v[i]), "=r"(t[i])
+                                 : "l"(src + 2 * static_cast<size_t>(i) * L.pitch_d)
+                                 : "memory");
+            }
             float s = 0.f;
 #pragma unroll
-            for (int i = 0; i < kPer; ++i)
-                if (g0 + i < g1) s += v[i];
+            for (int i = 0; i < kPer; ++i) {
+                if (g0 + i >= g1) continue;
+                float f = __uint_as_float(v[i]);
+                if (t[i] != ptag) f = ld_tagged(src + 2 * static_cast<size_t>(i) * L.pitch_d, ptag);
+                s += f;
+            }
             for (int g = g0 + kPer; g < g1; ++g)
-                s += __ldcg(src + static_cast<size_t>(g - g0) * L.pitch_d);
+                s += ld_tagged(src + 2 * static_cast<size_t>(g - g0) * L.pitch_d, ptag);
             part[tid] = s;
         }
         __syncthreads();
@@ -1356,7 +1381,7 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
                  "r"(S.sv_chunk), "r"(S.item_cap));
     // no grid barrier between the layers of a stack: the previous layer's y
     // arrives tagged (its tag: the partial barrier it followed)
-    const bool bad = first_layer ? stage_x(x, L.d, L.pitch_d, sm.xs)
+    const bool bad = first_layer ? stage_x(x, L.d, L.pitch_d, sm.xs, W.xres)
                                  : stage_x_poll(chain ? nullptr : x, chain == 2 ? x : nullptr, W,
                                                 L.d, L.pitch_d, sm.xs,
                                                 rs.tag0 + rs.bar_k);
@@ -1382,14 +1407,18 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
     }
     phase_gather<kPipe>(L, W, sm, S);
     SG_STAMP(dbg, 14);
+    // the layer's exchange tag: the barrier count after this layer's arrive
+    const uint32_t ptag = rs.tag0 + rs.bar_k + 1u;
     if (kPipe == 2) {
-        survivor_updown(L, W, sm, S, rs);
+        survivor_updown(L, W, sm, S, rs, ptag);
     } else {
-        partial_down<kPipe>(L, W, sm);
+        partial_down<kPipe>(L, W, sm, ptag);
     }
     SG_STAMP(dbg, 7);
-    // stage the next layer's predictor weights and hot prefix during the
-    // barrier: this CTA's ring and survivor rows are done, phase D uses reda
+    // stage the next layer's predictor weights and hot prefix: this CTA's ring and
+    // survivor rows are done, phase D uses reda. The partials travel tagged, so phase D
+    // waits only for the data it sums; the barrier arrive keeps the tag bookkeeping,
+    // and only the last layer (index sets over every CTA's counts) waits on it.
     grid_arrive(W, rs);
     bool next_staged = false;
     if (kPipe != 0 && next != nullptr) {
@@ -1397,7 +1426,7 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
         if (kPipe == 2) preissue_hot(*next, sm, S);
     }
     const DownPlan dp = down_plan(L, W);
-    grid_wait(W, rs);
+    if (want_sets || next == nullptr) grid_wait(W, rs);
     SG_STAMP(dbg, 8);
     phase_down<kPipe>(L, W, sm, y, want_sets, next != nullptr, rs.tag0 + rs.bar_k, dp);
     SG_STAMP(dbg, 9);

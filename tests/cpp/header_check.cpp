@@ -2,7 +2,7 @@
 // reference caller would. Mode "cpu": host-only entry points (no device calls).
 // Mode "gpu": the executor on cuda:0, with known answers from
 // /root/reference/proj/tests/ffn_exec_tests.cpp.
-//   g++ -std=c++17 -O2 -Iinclude tests/cpp/header_check.cpp \
+//   g++ -std=c++17 -O2 -Iinclude tests/cpp/header_check.cpp
 //       -Lpaper_2603_14110_b200 -lsparsegate_b200 -Wl,-rpath,<abs pkg dir>
 #include "sparsegate/ffn_exec.hpp"
 
@@ -52,15 +52,15 @@ static void cpu_checks() {
     CHECK(throws<DataError>([] { op_count_model(64, 256, 8, 0.9, 0.5); }));
     CHECK(throws<DataError>([] { op_count_model(0, 256, 8, 0.5, 0.9); }));
     // types.hpp validation
-    FfnWeights w{Mat(4, 2), Mat(4, 2), Mat(3, 4), Activation::ReGLU};
+    FfnWeights w{Mat::Zero(4, 2), Mat::Zero(4, 2), Mat::Zero(3, 4), Activation::ReGLU};
     CHECK(throws<DataError>([&] { validate(w); }));
-    w.down = Mat(2, 4);
+    w.down = Mat::Zero(2, 4);
     validate(w);
     w.up(1, 1) = std::nan("");
     CHECK(throws<DataError>([&] { validate(w); }));
-    Predictor p{Mat(4, 2), Mat(2, 3), Vec(4), 2};
+    Predictor p{Mat::Zero(4, 2), Mat::Zero(2, 3), Vec::Zero(4), 2};
     validate(p);
-    p.bias[0] = INFINITY;  // calibrated +inf biases are legal
+    p.bias(0) = INFINITY;  // calibrated +inf biases are legal
     validate(p);
     p.rank = 3;
     CHECK(throws<DataError>([&] { validate(p); }));
@@ -71,25 +71,30 @@ static void cpu_checks() {
 
 static void gpu_checks() {
     // ffn_exec_tests.cpp:51-82: 2x2 dense known answers
-    FfnWeights w{Mat{{1, 0}, {-1, 0}}, Mat::Identity(2), Mat::Identity(2), Activation::ReGLU};
-    const FfnResult r = dense_ffn(w, Vec{1, 1});
+    FfnWeights w{Mat(2, 2), Mat::Identity(2, 2), Mat::Identity(2, 2), Activation::ReGLU};
+    w.gate << 1, 0, -1, 0;
+    Vec x11(2), xnan(2), x3(3);
+    x11 << 1, 1;
+    xnan << 1, std::nan("");
+    x3 << 1, 1, 1;
+    const FfnResult r = dense_ffn(w, x11);
     CHECK(r.y[0] == 1.0 && r.y[1] == 0.0);
     CHECK(r.stats.multiplies == 12 && r.stats.pipeline == Pipeline::Dense);
-    CHECK(throws<DataError>([&] { dense_ffn(w, Vec{1, std::nan("")}); }));
-    CHECK(throws<DataError>([&] { dense_ffn(w, Vec{1, 1, 1}); }));
-    w.up = Mat{{-1, 0}, {0, 1}};
-    const FfnResult r2 = dense_ffn(w, Vec{1, 1});
+    CHECK(throws<DataError>([&] { dense_ffn(w, xnan); }));
+    CHECK(throws<DataError>([&] { dense_ffn(w, x3); }));
+    w.up << -1, 0, 0, 1;
+    const FfnResult r2 = dense_ffn(w, x11);
     if (r2.y[0] != -1.0) std::printf("reglu y = (%g, %g)\n", r2.y[0], r2.y[1]);
     CHECK(r2.y[0] == -1.0);
     w.activation = Activation::DReLU;
-    CHECK(dense_ffn(w, Vec{1, 1}).y[0] == 0.0);
+    CHECK(dense_ffn(w, x11).y[0] == 0.0);
 
     // exact predictor (A = gate, B = I): mask = gate support; all-active == dense
     std::mt19937_64 g(29);
     for (Activation act : {Activation::ReGLU, Activation::DReLU}) {
         FfnWeights rw{random_mat(g, 48, 16), random_mat(g, 48, 16), random_mat(g, 16, 48), act};
-        Predictor all{rw.gate, Mat::Identity(16), Vec(48), 16};
-        for (Index i = 0; i < 48; ++i) all.bias[i] = 1e12;
+        Predictor all{rw.gate, Mat::Identity(16, 16), Vec::Zero(48), 16};
+        all.bias.setConstant(1e12);
         Vec x(16);
         std::normal_distribution<double> nd(0.0, 1.0);
         for (Index i = 0; i < 16; ++i) x[i] = nd(g);
@@ -101,7 +106,7 @@ static void gpu_checks() {
         }
         CHECK(err <= 1e-10 * nrm);
         CHECK(a.stats.predicted_sparsity == 0.0);
-        Predictor exact{rw.gate, Mat::Identity(16), Vec(48), 16};
+        Predictor exact{rw.gate, Mat::Identity(16, 16), Vec::Zero(48), 16};
         const Mask m = predict_mask(exact, x);
         Index cnt = 0;
         for (auto v : m.active) cnt += v;

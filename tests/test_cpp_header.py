@@ -29,3 +29,19 @@ def test_header_host_entry_points(binary):
 def test_header_executor_known_answers(binary):
     r = subprocess.run([binary, "gpu"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+REF_BIN = os.path.join(ROOT, "tests", "cpp", "_ref_tests", "ffn_exec_tests")
+
+
+@pytest.mark.gpu
+def test_reference_ffn_exec_tests_unmodified():
+    """/root/reference/proj/tests/ffn_exec_tests.cpp, compiled UNMODIFIED against this
+    repo's drop-in headers (include/sparsegate/{common,types,ffn_exec,factorization}.hpp
+    over libsparsegate_b200.so; tests/cpp/Makefile, built by __graft_entry__.build()
+    where /root/reference exists), runs every TEST_CASE / SECTION on the B200."""
+    assert os.path.exists(REF_BIN), f"{REF_BIN} was not built (make -C tests/cpp)"
+    r = subprocess.run([REF_BIN], capture_output=True, text=True, timeout=600)
+    print(r.stdout[-3000:])
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " 0 failed" in r.stdout

@@ -1,3 +1,9 @@
-# batched-decode sweep (8-layer 7B stack); args: tag, then batch sizes
-tag=$1; shift
-for B in "$@"; do python bench.py --batch $B --layers 8 --steps 200 --warmup 20 --no-cpu-baseline --no-dense > gpurun_out/${tag}_B$B.json 2>gpurun_out/${tag}_B$B.err; python -c "import json;d=json.load(open('gpurun_out/${tag}_B$B.json'));print('$tag',$B,round(d['value']),round(d['per_layer_us'],1),round(d['roofline']['frac'],3))"; done
+#!/bin/bash
+# Batched-decode sweep (configs[4]) on the full 32-layer 7B stack: one JSON line per B
+# (sparse tcgen05 path, dense comparator, e2e, roofline) into gpurun_out/batch_B*.json.
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+for B in ${@:-2 4 8 16 32 64}; do
+  python bench.py --batch $B --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/batch_B$B.json 2> gpurun_out/batch_B$B.err
+  echo "B=$B exit=$?"
+done
