@@ -13,7 +13,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 # SG_LIB=timing selects the instrumented build (per-phase %globaltimer stamps,
 # tools/phase_profile.py); the default is the production library.
-LIB_PATH = os.path.join(HERE, "libsparsegate_b200_timing.so" if os.environ.get("SG_LIB") == "timing"
+LIB_PATH = os.path.join(HERE, f"libsparsegate_b200_{os.environ['SG_LIB']}.so" if os.environ.get("SG_LIB")
                         else "libsparsegate_b200.so")
 
 SG_OK, SG_ERR_USAGE, SG_ERR_DATA, SG_ERR_PROPERTY, SG_ERR_IO, SG_ERR_CUDA, SG_ERR_NCCL = range(7)
@@ -82,6 +82,9 @@ SYMBOLS = [
     ("sg_ctx_enable_stack_sets", C.c_int, [_VP, _I32]),
     ("sg_ctx_read_stack_sets", C.c_int, [_VP, _VP, _I32, _VP, C.POINTER(_I64), _VP, C.POINTER(_I64)]),
     ("sg_ffn_forward_batch", C.c_int, [_VP, _VP, _VP, _I32, _VP, _VP]),
+    ("sg_ctx_enable_tc_trace", C.c_int, [_VP, _I32]),
+    ("sg_ctx_read_tc_trace", C.c_int, [_VP, _VP, _I32, _VP, C.POINTER(_I32)]),
+    ("sg_tc_unit_codes", C.c_int, [_VP, _VP, _I32]),
     ("sg_ffn_forward_batch_dense", C.c_int, [_VP, _VP, _VP, _I32, _VP, _VP]),
     ("sg_ctx_read_batch", C.c_int, [_VP, _VP, _I32, C.POINTER(sg_exec_stats), _VP, _VP]),
     ("sg_ffn_forward_batch_host", C.c_int, [_VP, _VP, _VP, _I32, _VP, C.POINTER(sg_exec_stats), _VP]),

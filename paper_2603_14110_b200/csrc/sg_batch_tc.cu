@@ -46,14 +46,17 @@
 namespace sg {
 namespace {
 
-constexpr int kTcThreads = 192;
+constexpr int kProdThreads = 128;  // warps 0-3: producers (cp.async row gathers, TMA tiles)
+constexpr int kMmaWarp = 4;         // warp 4: MMA issuer; warps 5-8: epilogue
+constexpr int kEpiBase = 160;
+constexpr int kTcThreads = 288;
+constexpr int kLag = 3;             // stages a producer thread keeps in flight before arriving
 constexpr int kStages = 4;
 constexpr int kStageA = 32768;  // 256 rows x 64 K bf16 (two M = 128 sub-tiles)
 constexpr int kStageB = 16384;  // <= 128 rows (N) x 64 K bf16
 constexpr int kStageBytes = kStageA + kStageB;
 constexpr int kUQ = 4;          // unit queue depth (producer lead)
 constexpr int kBlk = 256;       // neurons per block / rows per unit
-constexpr int kTRRows = 16;     // T rows per TR unit
 constexpr int kYRRows = 64;     // y rows per YR unit
 
 enum UnitType : int { U_STOP = 0, U_X, U_T, U_TR, U_PRE, U_GATE, U_UP, U_DOWN, U_YR };
@@ -65,7 +68,8 @@ struct Unit {
     int nsub;    // M = 128 sub-tiles carrying rows (1 or 2)
     int cnt;     // rows of the unit (gather units)
     int acc;     // TMEM accumulator buffer
-    int pad;
+    int pad;     // gate / up: the block's rows are contiguous (dense comparator)
+    int u;       // index in the claim order
 };
 
 // ---- PTX wrappers -----------------------------------------------------------
@@ -147,6 +151,25 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 }
 __device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void prod_bar() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
+// 16-B global -> shared copy on the LSU path (row gathers: a TMA tile::gather4 moves
+// only 512 B per instruction, ~14 GB/s per SM on B200 — tools/bw_tma.cu)
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// this thread's copies of the stage have landed: make them visible to the tensor
+// cores (async proxy) and count the thread on the stage's full barrier
+__device__ __forceinline__ void stage_arrive(uint64_t* bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive(bar);
+}
+
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
@@ -159,6 +182,20 @@ __device__ __forceinline__ void wait_count(const int* p, int target) {
     while (ld_acquire(p) < target) __nanosleep(64);
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
+__device__ __forceinline__ bool flag_ready(const int* p, int target) { return ld_acquire(p) >= target; }
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// unit trace (diagnostics): [u][0] claim, [1] inputs ready, [2] loads issued,
+// [3] epilogue start, [4] epilogue end, [5] SM id
+#define TC_TRACE(a, u, k, v)                                                         \
+    do {                                                                             \
+        if ((a).trace != nullptr && (u) >= 0 && (u) < (a).n_units)                   \
+            (a).trace[static_cast<size_t>(u) * 6 + (k)] = (v);                      \
+    } while (0)
+
 // Publish this thread's (or, after a CTA-level barrier, the CTA's) global writes —
 // generic-proxy stores included, for later TMA reads — then count.
 __device__ __forceinline__ void signal(int* p) {
@@ -178,41 +215,34 @@ __device__ __forceinline__ float gated(float g, float u, int act) {
 }
 
 // ---- unit table ---------------------------------------------------------------
+// The host lays the units out in one claim order (TcArgs::order, built by
+// sg_host.cpp tc_schedule): the predictor chain first, then the GATE units block by
+// block (the K slices of a block KS-1 .. 0, the owner that sums the others'
+// partials last), with a block's UP units, a block range's DOWN units and a d
+// tile's YR units merged in about one wave of claims after the units they depend
+// on. Every unit's inputs come from units earlier in the order, so the dataflow
+// cannot deadlock, and no phase waits for a whole previous phase.
 __device__ __forceinline__ int unit_type(const TcArgs& a, int u, int& i, int& j) {
-    if (u < a.u_T) { i = u; j = 0; return U_X; }
-    if (u < a.u_TR) { i = u - a.u_T; j = 0; return U_T; }
-    if (u < a.u_PRE) { i = u - a.u_TR; j = 0; return U_TR; }
-    if (u < a.u_GATE) { i = u - a.u_PRE; j = 0; return U_PRE; }
-    if (u < a.u_UP) {  // slice KS-1 of every block first, slice 0 (the owner) last
-        const int k = u - a.u_GATE;
-        i = k % a.nblk;
-        j = a.KSg - 1 - k / a.nblk;
-        return U_GATE;
-    }
-    if (u < a.u_DOWN) {
-        const int k = u - a.u_UP;
-        i = k % a.nblk;
-        j = a.KSu - 1 - k / a.nblk;
-        return U_UP;
-    }
-    if (u < a.u_YR) {  // d tile i, block range j
-        const int k = u - a.u_DOWN;
-        i = k % a.ndt;
-        j = k / a.ndt;
-        return U_DOWN;
-    }
-    if (u < a.u_end) {
-        i = u - a.u_YR;
-        j = 0;
-        return U_YR;
-    }
-    return U_STOP;
+    if (u >= a.n_units) return U_STOP;
+    const int code = __ldg(a.order + u);
+    i = (code >> 8) & 0xffff;
+    j = code & 0xff;
+    return code >> 24;
 }
 __device__ __forceinline__ int blk_rows(const TcArgs& a, int blk) {
     const int r = a.D - blk * kBlk;
     return r < kBlk ? r : kBlk;
 }
 __device__ __forceinline__ int range_lo(const TcArgs& a, int s) { return s * a.nblk / a.S; }
+// A block whose listed rows are a large enough share of its rows is loaded whole by
+// TMA tiles (128 contiguous rows per instruction) instead of gathered row by row:
+// gathers stream ~26 GB/s per SM, tiles ~55 (tools/bw_tma.cu), so above ~45 %
+// density the tile is faster even though it also reads the unlisted rows. The
+// decision is a function of the block's count only, so every unit (and the UP
+// epilogue that lays out Z for DOWN) agrees on it.
+__device__ __forceinline__ bool blk_tiled(const TcArgs& a, int cnt, int blk, int thr) {
+    return a.dense || cnt * 1024 >= thr * blk_rows(a, blk);
+}
 
 // flags layout (ints), zeroed by the last CTA of every launch
 __device__ __forceinline__ int* fl_work(const TcArgs& a) { return a.flags; }
@@ -220,86 +250,161 @@ __device__ __forceinline__ int* fl_exit(const TcArgs& a) { return a.flags + 1; }
 __device__ __forceinline__ int* fl_x(const TcArgs& a) { return a.flags + 2; }
 __device__ __forceinline__ int* fl_t(const TcArgs& a) { return a.flags + 3; }
 __device__ __forceinline__ int* fl_tr(const TcArgs& a) { return a.flags + 4; }
-__device__ __forceinline__ int* fl_pre(const TcArgs& a, int b) { return a.flags + 8 + b; }
-__device__ __forceinline__ int* fl_gpart(const TcArgs& a, int b) { return a.flags + 8 + a.nblk + b; }
-__device__ __forceinline__ int* fl_gate(const TcArgs& a, int b) { return a.flags + 8 + 2 * a.nblk + b; }
-__device__ __forceinline__ int* fl_upart(const TcArgs& a, int b) { return a.flags + 8 + 3 * a.nblk + b; }
-__device__ __forceinline__ int* fl_up(const TcArgs& a, int b) { return a.flags + 8 + 4 * a.nblk + b; }
-__device__ __forceinline__ int* fl_down(const TcArgs& a, int t) { return a.flags + 8 + 5 * a.nblk + t; }
-__device__ __forceinline__ int flag_count(const TcArgs& a) { return 8 + 5 * a.nblk + a.ndt; }
+__device__ __forceinline__ int* fl_pre(const TcArgs& a, int b) { return a.flags + 32 + b; }
+__device__ __forceinline__ int* fl_gpart(const TcArgs& a, int b) { return a.flags + 32 + a.nblk + b; }
+__device__ __forceinline__ int* fl_gate(const TcArgs& a, int b) { return a.flags + 32 + 2 * a.nblk + b; }
+__device__ __forceinline__ int* fl_upart(const TcArgs& a, int b) { return a.flags + 32 + 3 * a.nblk + b; }
+__device__ __forceinline__ int* fl_up(const TcArgs& a, int b) { return a.flags + 32 + 4 * a.nblk + b; }
+__device__ __forceinline__ int* fl_down(const TcArgs& a, int t) { return a.flags + 32 + 5 * a.nblk + t; }
+__device__ __forceinline__ int flag_count(const TcArgs& a) { return 32 + 5 * a.nblk + a.ndt; }
 
 struct TcSmem {
     uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], uqf[kUQ], uqe[kUQ];
     Unit uq[kUQ];
     uint32_t tmem;
     int rows[kBlk];      // producer: gather rows of the current unit (global neuron index)
+    Unit pu;             // producer: the unit being loaded
+    int pready;          // producer: its inputs and queue slot are available now
     int flag[kBlk];      // epilogue: per-row flags / positions
     int cnt[64];         // epilogue: per-token counts
     int wsum[16];        // epilogue: per-(sub-tile, quarter) counts
 };
 
 // ---- producer: claim, wait, load ---------------------------------------------
+// 128 threads (warps 0-3). Thread 0 is the controller: it claims units, checks and
+// waits their inputs and publishes them. Contiguous rows (T, PRE, the dense
+// comparator) and the B operands come by TMA tiles from the controller; gathered
+// rows (the union / survivor rows of GATE, UP, DOWN) by 16-B cp.async from every
+// producer thread, written in the 128-B-swizzled UMMA layout. Each thread keeps kLag
+// stages of its copies in flight, then (wait_group, proxy fence) arrives on the
+// stage's full barrier (129 arrivals: 128 threads + the controller's expect_tx).
+// Before any blocking wait on another unit or on the epilogue every thread flushes
+// its pending arrivals, so no stage of an earlier unit is held back.
+__device__ __forceinline__ bool unit_inputs_ready(const TcArgs& a, int type, int i, int j) {
+    switch (type) {
+        case U_T: return flag_ready(fl_x(a), a.u_T);
+        case U_PRE: return flag_ready(fl_tr(a), a.u_PRE - a.u_TR);
+        case U_GATE: return a.dense ? flag_ready(fl_x(a), a.u_T) : flag_ready(fl_pre(a, i), 1);
+        case U_UP: return flag_ready(fl_gate(a, i), 1);
+        case U_DOWN:
+            for (int blk = range_lo(a, j); blk < range_lo(a, j + 1); ++blk)
+                if (!flag_ready(fl_up(a, blk), 1)) return false;
+            return true;
+        case U_TR: return flag_ready(fl_t(a), a.u_TR - a.u_T);
+        case U_YR: return flag_ready(fl_down(a, i / 4), a.S);
+        default: return true;  // U_X
+    }
+}
+__device__ __forceinline__ void unit_inputs_wait(const TcArgs& a, int type, int i, int j) {
+    switch (type) {
+        case U_T: wait_count(fl_x(a), a.u_T); break;
+        case U_PRE: wait_count(fl_tr(a), a.u_PRE - a.u_TR); break;
+        case U_GATE:
+            if (a.dense) wait_count(fl_x(a), a.u_T);
+            else wait_count(fl_pre(a, i), 1);
+            break;
+        case U_UP: wait_count(fl_gate(a, i), 1); break;
+        case U_TR: wait_count(fl_t(a), a.u_TR - a.u_T); break;
+        case U_YR: wait_count(fl_down(a, i / 4), a.S); break;
+        case U_DOWN:
+            for (int blk = range_lo(a, j); blk < range_lo(a, j + 1); ++blk) wait_count(fl_up(a, blk), 1);
+            break;
+        default: break;
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* stages) {
-    const int lane = threadIdx.x & 31;
+    const int pt = threadIdx.x;  // 0..127
     const uint64_t pol = policy_evict_first();
     const uint32_t bbytes = static_cast<uint32_t>(a.N) * 128u;
-    int seq = 0, stage = 0, accseq = 0;
-    uint32_t sphase = 0;  // bit s: phase of empty[s] to wait for
+    const uint32_t sbase = su32(stages);
+    int seq = 0, accseq = 0;
+    int n = 0;         // stages issued by this thread (all producer threads agree)
+    int pending = 0;   // of which not yet arrived
+    uint32_t ephase = 0;  // bit s: parity of empty[s] to wait for
+    auto flush = [&] {
+        cp_wait<0>();
+        for (; pending > 0; --pending) stage_arrive(&S.full[(n - pending) % kStages]);
+    };
     for (;;) {
-        int u = 0;
-        if (lane == 0) u = atomicAdd(fl_work(a), 1);
-        u = __shfl_sync(0xffffffffu, u, 0);
-        int i, j;
-        const int type = unit_type(a, u, i, j);
-        Unit un{type, i, j, 0, 0, 0, 0, 0};
-        // inputs of the unit (every producer lane observes them with acquire)
+        // ---- claim the next unit of the order (controller), then everyone sees it
+        if (pt == 0) {
+            const int u = atomicAdd(fl_work(a), 1);
+            int i = 0, j = 0;
+            const int type = unit_type(a, u, i, j);
+            S.pu = Unit{type, i, j, 0, 0, 0, 0, 0, u};
+            TC_TRACE(a, u, 0, gtimer());
+            bool ready = unit_inputs_ready(a, type, i, j);
+            if (ready && seq >= kUQ) {  // and its queue slot
+                uint32_t okw;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                    "selp.u32 %0, 1, 0, p;\n}"
+                    : "=r"(okw)
+                    : "r"(su32(&S.uqe[seq % kUQ])), "r"(((seq / kUQ) - 1) & 1)
+                    : "memory");
+                ready = okw != 0;
+            }
+            S.pready = ready && type != U_STOP;
+        }
+        prod_bar();
+        Unit un = S.pu;
+        if (!S.pready) {
+            // a blocking wait: no stage of this CTA's own earlier units may stay held
+            // back meanwhile (their epilogues may be what the others wait for)
+            flush();
+            if (pt == 0) {
+                unit_inputs_wait(a, un.type, un.a, un.b);
+                if (seq >= kUQ) mbar_wait(&S.uqe[seq % kUQ], ((seq / kUQ) - 1) & 1);
+            }
+        }
+        if (pt == 0) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            TC_TRACE(a, un.u, 1, gtimer());
+            unsigned smid;
+            asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+            TC_TRACE(a, un.u, 5, smid);
+        }
+        prod_bar();
+        const int type = un.type, i = un.a, j = un.b;
+        // ---- the unit's geometry and rows
         if (type == U_T) {
-            wait_count(fl_x(a), a.u_T);
             un.nst = a.kst / 64;
             un.nsub = a.r > 128 ? 2 : 1;
         } else if (type == U_PRE) {
-            wait_count(fl_tr(a), a.u_PRE - a.u_TR);
             un.nst = a.pitch_r / 64;
             un.nsub = blk_rows(a, i) > 128 ? 2 : 1;
         } else if (type == U_GATE || type == U_UP) {
-            int cnt;
-            const int* list;
-            if (type == U_GATE) {
-                if (a.dense) {
-                    wait_count(fl_x(a), a.u_T);
-                    cnt = blk_rows(a, i);
-                    list = nullptr;
-                } else {
-                    wait_count(fl_pre(a, i), 1);
-                    cnt = __ldcg(a.ucnt + i);
-                    list = a.ulist + i * kBlk;
-                }
-            } else {
-                wait_count(fl_gate(a, i), 1);
-                cnt = __ldcg(a.vcnt + i);
-                list = a.vlist + i * kBlk;
+            wait_count(type == U_UP ? fl_gate(a, i) : (a.dense ? fl_x(a) : fl_pre(a, i)),
+                       type == U_GATE && a.dense ? a.u_T : 1);  // (set: orders the reads below)
+            const int listed = type == U_GATE ? (a.dense ? blk_rows(a, i) : __ldcg(a.ucnt + i)) : __ldcg(a.vcnt + i);
+            const bool tiled = listed > 0 && blk_tiled(a, listed, i, type == U_GATE ? a.tile_g : a.tile_u);
+            // tiled: the unit's rows are the block's rows; else the listed rows, gathered
+            const int cnt = tiled ? blk_rows(a, i) : listed;
+            if (!tiled) {
+                const int* list = type == U_GATE ? a.ulist + i * kBlk : a.vlist + i * kBlk;
+                for (int k = pt; k < cnt; k += kProdThreads) S.rows[k] = i * kBlk + __ldcg(list + k);
             }
-            for (int k = lane; k < cnt; k += 32) S.rows[k] = i * kBlk + (list ? __ldcg(list + k) : k);
-            __syncwarp();
             un.cnt = cnt;
             un.nsub = cnt > 128 ? 2 : (cnt > 0 ? 1 : 0);
             un.nst = cnt > 0 ? (type == U_GATE ? a.ksg : a.ksu) / 64 : 0;
+            un.pad = tiled;
         } else if (type == U_DOWN) {
-            const int b0 = range_lo(a, j), b1 = range_lo(a, j + 1);
             int nst = 0;
-            for (int blk = b0; blk < b1; ++blk) {
+            for (int blk = range_lo(a, j); blk < range_lo(a, j + 1); ++blk) {
                 wait_count(fl_up(a, blk), 1);
-                nst += (__ldcg(a.vcnt + blk) + 63) / 64;
+                const int v = __ldcg(a.vcnt + blk);
+                nst += (v > 0 && blk_tiled(a, v, blk, a.tile_u) ? blk_rows(a, blk) + 63 : v + 63) / 64;
             }
             un.nst = nst;
             un.nsub = 2;
         }
         const bool mma_unit = type == U_T || type == U_PRE || type == U_GATE || type == U_UP || type == U_DOWN;
         if (mma_unit) un.acc = accseq++ & 1;
-        // publish the unit to the MMA warp and the epilogue
-        const int slot = seq % kUQ;
-        if (seq >= kUQ) mbar_wait(&S.uqe[slot], ((seq / kUQ) - 1) & 1);
-        if (lane == 0) {
+        prod_bar();  // S.rows complete
+        if (pt == 0) {
+            const int slot = seq % kUQ;
             S.uq[slot] = un;
             mbar_arrive(&S.uqf[slot]);
         }
@@ -307,81 +412,119 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
         if (type == U_STOP) break;
         if (!mma_unit || un.nst == 0) continue;
 
-        // ---- loads, one stage per 64-wide K chunk ----
-        auto next_stage = [&](uint8_t*& As, uint8_t*& Bs, uint64_t*& bar) {
-            mbar_wait(&S.empty[stage], (sphase >> stage) & 1u);
-            sphase ^= 1u << stage;
-            As = stages + stage * kStageBytes;
-            Bs = As + kStageA;
-            bar = &S.full[stage];
-            stage = (stage + 1) % kStages;
+        // ---- one stage per 64-wide K chunk
+        auto begin_stage = [&](uint8_t*& As, uint32_t& as, uint64_t*& bar) {
+            const int s = n % kStages;
+            mbar_wait(&S.empty[s], (ephase >> s) & 1u);
+            ephase ^= 1u << s;
+            As = stages + s * kStageBytes;
+            as = sbase + s * kStageBytes;
+            bar = &S.full[s];
         };
-        if (type == U_T || type == U_PRE) {
-            const CUtensorMap* am = type == U_T ? &M.Bp : &M.A;
-            const CUtensorMap* bm = type == U_T ? &M.xhl : &M.thl;
-            const int k0 = type == U_T ? i * a.kst : 0;
+        auto end_stage = [&] {
+            cp_commit();
+            ++n;
+            if (++pending > kLag) {
+                cp_wait<kLag>();
+                stage_arrive(&S.full[(n - pending) % kStages]);
+                --pending;
+            }
+        };
+        if (type == U_T || type == U_PRE || un.pad) {
+            // contiguous rows: TMA tiles (T: predictor B rows; PRE: A rows; dense: all rows)
+            const CUtensorMap* am = type == U_T ? &M.Bp : type == U_PRE ? &M.A : type == U_GATE ? &M.gate : &M.up;
+            const CUtensorMap* bm = type == U_PRE ? &M.thl : &M.xhl;
+            const int kw = type == U_GATE ? a.ksg : a.ksu;
+            const int k0 = type == U_T ? i * a.kst : type == U_PRE ? 0 : j * kw;
             const int r0 = type == U_T ? 0 : i * kBlk;
             for (int st = 0; st < un.nst; ++st) {
-                uint8_t *As, *Bs;
+                uint8_t* As;
+                uint32_t as;
                 uint64_t* bar;
-                next_stage(As, Bs, bar);
-                if (lane == 0) {
+                begin_stage(As, as, bar);
+                if (pt == 0) {
                     mbar_expect_tx(bar, un.nsub * 16384u + bbytes);
                     for (int t = 0; t < un.nsub; ++t) tma_tile(As + t * 16384, am, k0 + st * 64, r0 + t * 128, bar);
-                    tma_tile(Bs, bm, k0 + st * 64, 0, bar);
+                    tma_tile(As + kStageA, bm, k0 + st * 64, 0, bar);
                 }
-                __syncwarp();
+                end_stage();
             }
         } else if (type == U_GATE || type == U_UP) {
-            const CUtensorMap* am = type == U_GATE ? &M.gate : &M.up;
+            const uint16_t* base = type == U_GATE ? a.gate : a.ud;
+            const size_t rstride = type == U_GATE ? static_cast<size_t>(a.pitch_d) : 2 * static_cast<size_t>(a.pitch_d);
             const int kw = type == U_GATE ? a.ksg : a.ksu;
             const int k0 = j * kw;
-            const int ngrp = (un.cnt + 3) / 4;
+            const int jj = pt & 7;  // this thread's 16-B chunk of every row it copies
             for (int st = 0; st < un.nst; ++st) {
-                uint8_t *As, *Bs;
+                uint8_t* As;
+                uint32_t as;
                 uint64_t* bar;
-                next_stage(As, Bs, bar);
-                if (lane == 0) mbar_expect_tx(bar, static_cast<uint32_t>(ngrp) * 512u + bbytes);
-                __syncwarp();
+                begin_stage(As, as, bar);
                 const int kc = k0 + st * 64;
-                for (int g = lane; g < ngrp; g += 32) {
-                    int r[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) r[q] = S.rows[min(4 * g + q, un.cnt - 1)];
-                    // group g holds rows 4g..4g+3: sub-tile g / 32, 512 B per group
-                    tma_gather4(As + g * 512, am, kc, r[0], r[1], r[2], r[3], bar, pol);
+                if (pt == 0) {
+                    mbar_expect_tx(bar, bbytes);
+                    tma_tile(As + kStageA, &M.xhl, kc, 0, bar);
                 }
-                if (lane == 0) tma_tile(Bs, &M.xhl, kc, 0, bar);
-                __syncwarp();
+#pragma unroll 4
+                for (int r = pt >> 3; r < un.cnt; r += kProdThreads / 8) {
+                    const uint16_t* src = base + static_cast<size_t>(S.rows[r]) * rstride + kc + jj * 8;
+                    cp16(as + (r >> 3) * 1024 + (r & 7) * 128 + ((jj ^ (r & 7)) << 4), src, pol);
+                }
+                end_stage();
             }
         } else {  // U_DOWN: K = survivor slots of the block range, A = down rows (MN-major)
-            const int b0 = range_lo(a, j), b1 = range_lo(a, j + 1);
             const int m0 = i * 256;
-            for (int blk = b0; blk < b1; ++blk) {
-                const int cnt = __ldcg(a.vcnt + blk);
-                if (cnt == 0) continue;
-                for (int k = lane; k < cnt; k += 32) S.rows[k] = blk * kBlk + __ldcg(a.vlist + blk * kBlk + k);
-                __syncwarp();
-                for (int c0 = 0; c0 < cnt; c0 += 64) {
-                    uint8_t *As, *Bs;
-                    uint64_t* bar;
-                    next_stage(As, Bs, bar);
-                    if (lane == 0) mbar_expect_tx(bar, 4u * 16u * 512u + bbytes);
-                    __syncwarp();
-                    // 16 groups of 4 k-rows x 4 m-atoms of 64 outputs = 64 gathers
-                    for (int q = lane; q < 64; q += 32) {
-                        const int g = q & 15, atom = q >> 4;
-                        int r[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) r[e] = S.rows[min(c0 + 4 * g + e, cnt - 1)];
-                        tma_gather4(As + atom * 8192 + g * 512, &M.down, m0 + atom * 64, r[0], r[1], r[2],
-                                    r[3], bar, pol);
+            for (int blk = range_lo(a, j); blk < range_lo(a, j + 1); ++blk) {
+                const int v = __ldcg(a.vcnt + blk);
+                if (v == 0) continue;
+                if (blk_tiled(a, v, blk, a.tile_u)) {
+                    // the block's down rows by TMA tiles: 64 k-rows x 4 atoms of 64 outputs;
+                    // Z holds zeros for the rows that are not survivors (UP epilogue)
+                    for (int c0 = 0; c0 < blk_rows(a, blk); c0 += 64) {
+                        uint8_t* As;
+                        uint32_t as;
+                        uint64_t* bar;
+                        begin_stage(As, as, bar);
+                        if (pt == 0) {
+                            mbar_expect_tx(bar, 4u * 8192u + bbytes);
+                            for (int atom = 0; atom < 4; ++atom)
+                                tma_tile(As + atom * 8192, &M.down, m0 + atom * 64, blk * kBlk + c0, bar);
+                            tma_tile(As + kStageA, &M.zhl, blk * kBlk + c0, 0, bar);
+                        }
+                        end_stage();
                     }
-                    if (lane == 0) tma_tile(Bs, &M.zhl, blk * kBlk + c0, 0, bar);
-                    __syncwarp();
+                    continue;
+                }
+                const int cnt = v;
+                prod_bar();  // the previous block's rows are no longer read
+                for (int k = pt; k < cnt; k += kProdThreads)
+                    S.rows[k] = blk * kBlk + __ldcg(a.vlist + blk * kBlk + k);
+                prod_bar();
+                for (int c0 = 0; c0 < cnt; c0 += 64) {
+                    uint8_t* As;
+                    uint32_t as;
+                    uint64_t* bar;
+                    begin_stage(As, as, bar);
+                    if (pt == 0) {
+                        mbar_expect_tx(bar, bbytes);
+                        tma_tile(As + kStageA, &M.zhl, blk * kBlk + c0, 0, bar);
+                    }
+                    // 64 k-rows x 4 atoms of 64 outputs: 2048 chunks of 16 B, 16 per thread.
+                    // Slots past the block's survivors repeat its last row (finite data
+                    // against Z = 0: they add exact zeros).
+#pragma unroll 4
+                    for (int q = pt; q < 2048; q += kProdThreads) {
+                        const int r = q >> 5, atom = (q >> 3) & 3, jj = q & 7;
+                        const int row = S.rows[min(c0 + r, cnt - 1)];
+                        const uint16_t* src = a.ud + static_cast<size_t>(row) * 2 * a.pitch_d + a.pitch_d + m0 +
+                                              atom * 64 + jj * 8;
+                        cp16(as + atom * 8192 + (r >> 3) * 1024 + (r & 7) * 128 + ((jj ^ (r & 7)) << 4), src, pol);
+                    }
+                    end_stage();
                 }
             }
         }
+        if (pt == 0) TC_TRACE(a, un.u, 2, gtimer());
     }
 }
 
@@ -408,16 +551,19 @@ __device__ void mma_issuer(const TcArgs& a, TcSmem& S, uint8_t* stages) {
             const uint32_t id = idesc(a.N, mn ? 1 : 0);
             // down: K steps of 16 survivor slots; the last stage of a block may be partial
             int dblk = mn ? range_lo(a, un.b) : 0, dleft = 0;
+            bool dtiled = false;
             for (int st = 0; st < un.nst; ++st) {
                 int ksteps = 4;
                 if (mn) {
                     while (dleft <= 0) {
                         wait_count(fl_up(a, dblk), 1);  // (already set: orders the vcnt read)
-                        dleft = __ldcg(a.vcnt + dblk);
+                        const int v = __ldcg(a.vcnt + dblk);
+                        dtiled = v > 0 && blk_tiled(a, v, dblk, a.tile_u);
+                        dleft = dtiled ? blk_rows(a, dblk) : v;
                         ++dblk;
                     }
                     const int here = dleft < 64 ? dleft : 64;
-                    ksteps = (here + 15) / 16;
+                    ksteps = dtiled ? 4 : (here + 15) / 16;
                     dleft -= 64;
                 }
                 mbar_wait(&S.full[stage], (fphase >> stage) & 1u);
@@ -451,8 +597,22 @@ __device__ void mma_issuer(const TcArgs& a, TcSmem& S, uint8_t* stages) {
 }
 
 // ---- epilogue helpers ------------------------------------------------------------
-// hi + lo columns of the accumulator row (this thread's TMEM lane) for tokens
-// c0..c0+7 of sub-tile t
+// hi + lo accumulator columns of this thread's TMEM lane (row) for tokens c0..c0+15 of
+// sub-tile t: four tcgen05.ld issued back to back, one wait (tokens >= nb read stale
+// columns, ignored by the callers).
+__device__ __forceinline__ void acc16(const TcArgs& a, uint32_t tbase, int quarter, int accbuf, int t,
+                                      int c0, float* v) {
+    float h[16], l[16];
+    const uint32_t addr = tbase + (static_cast<uint32_t>(quarter * 32) << 16) +
+                          static_cast<uint32_t>(accbuf * 256 + t * a.N + c0);
+    tmem_ld8(addr, h);
+    tmem_ld8(addr + 8u, h + 8);
+    tmem_ld8(addr + static_cast<uint32_t>(a.nb), l);
+    tmem_ld8(addr + static_cast<uint32_t>(a.nb) + 8u, l + 8);
+    tmem_wait();
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = h[e] + l[e];
+}
 __device__ __forceinline__ void acc8(const TcArgs& a, uint32_t tbase, int quarter, int accbuf, int t,
                                      int c0, float* v) {
     float h[8], l[8];
@@ -464,12 +624,25 @@ __device__ __forceinline__ void acc8(const TcArgs& a, uint32_t tbase, int quarte
 #pragma unroll
     for (int e = 0; e < 8; ++e) v[e] = h[e] + l[e];
 }
+__device__ __forceinline__ void ld16(const float* p, float* v) {  // 16 floats, 16-B aligned
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const float4 f = __ldcg(reinterpret_cast<const float4*>(p) + q);
+        v[4 * q] = f.x;
+        v[4 * q + 1] = f.y;
+        v[4 * q + 2] = f.z;
+        v[4 * q + 3] = f.w;
+    }
+}
+__device__ __forceinline__ void st16(float* p, const float* v, int n) {  // n in {8, 16}
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (4 * q < n) reinterpret_cast<float4*>(p)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+}
 
-// ascending compaction of S.flag[0..n) (non-zero = keep) by the 128 epilogue
-// threads: returns the kept count; pos[k] = position of row k among the kept
-__device__ int epi_compact(TcSmem& S, int n, int et, int* out_list, int base_val_mode) {
-    // warp 0 of the epilogue scans 256 flags with ballots (8 rounds)
-    (void)base_val_mode;
+// ascending compaction of S.flag[0..n) (non-zero = keep) into out_list (the kept k),
+// by the first epilogue warp; returns the count to all epilogue threads
+__device__ int epi_compact(TcSmem& S, int n, int et, int* out_list) {
     __shared__ int total;
     if (et < 32) {
         int run = 0;
@@ -486,14 +659,23 @@ __device__ int epi_compact(TcSmem& S, int n, int et, int* out_list, int base_val
     return total;
 }
 
+// per-token counts of the set bits over the 128 epilogue rows (S.cnt, smem)
+__device__ __forceinline__ void count_bits(TcSmem& S, uint64_t bits, int B, int lane) {
+    for (int b = 0; b < B; ++b) {
+        const unsigned bal = __ballot_sync(0xffffffffu, (bits >> b) & 1ull);
+        if (lane == 0 && bal) atomicAdd(&S.cnt[b], __popc(bal));
+    }
+}
+
 // ---- epilogue -----------------------------------------------------------------
 __device__ void epilogue(const TcArgs& a, TcSmem& S) {
-    const int et = threadIdx.x - 64;          // 0..127
+    const int et = threadIdx.x - kEpiBase;     // 0..127
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int quarter = warp & 3;              // TMEM lane quarter of this warp
     int seq = 0;
     uint32_t tphase = 0;
     const uint64_t bmask = a.B >= 64 ? ~0ull : ((1ull << a.B) - 1ull);
+    const int nb = a.nb;
     for (;;) {
         const int slot = seq % kUQ;
         mbar_wait(&S.uqf[slot], (seq / kUQ) & 1);
@@ -510,35 +692,44 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
             tphase ^= 1u << un.acc;
             tc_fence_after();
         }
-        // rows of this thread: sub-tile t row = 32*quarter + lane
-        const int row0 = quarter * 32 + lane;
+        if (et == 0) TC_TRACE(a, un.u, 3, gtimer());
+        const int row0 = quarter * 32 + lane;  // this thread's row of each sub-tile
         const int acc = un.acc;
-        const int nb = a.nb;
 
         if (un.type == U_X) {
-            // x (fp32 [B][d]) -> X^T hi rows 0..nb-1, lo rows nb..2nb-1 (bf16 [N][pitch_d]),
-            // this unit's slice of 8-wide column chunks; unit 0 zeroes the counts
-            const int nch = a.pitch_d / 8;
-            const int per = (nch + (a.u_T - 1)) / a.u_T;
-            const int c0 = i * per, c1 = min(nch, c0 + per);
+            // x (fp32 [B][d]) -> X^T hi rows 0..nb-1, lo rows nb..2nb-1 (bf16 [N][xpitch]):
+            // this unit's share of the (token, 8-column chunk) items, float4 loads
+            const int nch = a.pitch_d / 8, items = nb * nch;
+            const int per = (items + a.u_T - 1) / a.u_T;
+            const int w0 = i * per, w1 = min(items, w0 + per);
             bool bad = false;
-            for (int w = et; w < (c1 - c0) * nb; w += 128) {
-                const int b = w / (c1 - c0), ch = c0 + w % (c1 - c0);
+            const bool vec = (a.d & 7) == 0;
+            for (int w = w0 + et; w < w1; w += 128) {
+                const int b = w / nch, ch = w % nch, k0 = ch * 8;
+                float v[8];
+                if (b < a.B && vec && k0 < a.d) {
+                    const float4 f0 = __ldg(reinterpret_cast<const float4*>(a.x + static_cast<size_t>(b) * a.d + k0));
+                    const float4 f1 = __ldg(reinterpret_cast<const float4*>(a.x + static_cast<size_t>(b) * a.d + k0) + 1);
+                    v[0] = f0.x; v[1] = f0.y; v[2] = f0.z; v[3] = f0.w;
+                    v[4] = f1.x; v[5] = f1.y; v[6] = f1.z; v[7] = f1.w;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        v[e] = (b < a.B && k0 + e < a.d) ? __ldg(a.x + static_cast<size_t>(b) * a.d + k0 + e) : 0.f;
+                }
                 uint16_t hi[8], lo[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    const int k = ch * 8 + e;
-                    const float v = (b < a.B && k < a.d) ? __ldg(a.x + static_cast<size_t>(b) * a.d + k) : 0.f;
-                    bad |= !isfinite(v);
-                    split_bf16(v, hi[e], lo[e]);
+                    bad |= !isfinite(v[e]);
+                    split_bf16(v[e], hi[e], lo[e]);
                 }
                 uint4 vh, vl;
                 vh.x = hi[0] | (uint32_t(hi[1]) << 16); vh.y = hi[2] | (uint32_t(hi[3]) << 16);
                 vh.z = hi[4] | (uint32_t(hi[5]) << 16); vh.w = hi[6] | (uint32_t(hi[7]) << 16);
                 vl.x = lo[0] | (uint32_t(lo[1]) << 16); vl.y = lo[2] | (uint32_t(lo[3]) << 16);
                 vl.z = lo[4] | (uint32_t(lo[5]) << 16); vl.w = lo[6] | (uint32_t(lo[7]) << 16);
-                *reinterpret_cast<uint4*>(a.xhl + static_cast<size_t>(b) * a.xpitch + ch * 8) = vh;
-                *reinterpret_cast<uint4*>(a.xhl + static_cast<size_t>(nb + b) * a.xpitch + ch * 8) = vl;
+                *reinterpret_cast<uint4*>(a.xhl + static_cast<size_t>(b) * a.xpitch + k0) = vh;
+                *reinterpret_cast<uint4*>(a.xhl + static_cast<size_t>(nb + b) * a.xpitch + k0) = vl;
             }
             if (bad) atomicOr(a.bad, 1);  // check_input, ffn_exec.hpp:61-63
             asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -548,12 +739,10 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
             // partial T^T over K slice i: tpart[i][row][b], hi + lo summed
             for (int t = 0; t < un.nsub; ++t) {
                 const int row = t * 128 + row0;
-                for (int c = 0; c < nb; c += 8) {
-                    float v[8];
-                    acc8(a, S.tmem, quarter, acc, t, c, v);
-                    float* dst = a.tpart + (static_cast<size_t>(i) * kBlk + row) * nb + c;
-                    *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
-                    *reinterpret_cast<float4*>(dst + 4) = make_float4(v[4], v[5], v[6], v[7]);
+                for (int c = 0; c < nb; c += 16) {
+                    float v[16];
+                    acc16(a, S.tmem, quarter, acc, t, c, v);
+                    st16(a.tpart + (static_cast<size_t>(i) * kBlk + row) * nb + c, v, min(16, nb - c));
                 }
             }
             tc_fence_before();
@@ -563,13 +752,22 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                 signal(fl_t(a));
             }
         } else if (un.type == U_TR) {
-            wait_count(fl_t(a), a.u_TR - a.u_T);
-            // rows [16i, 16i+16) x nb tokens: fixed-order sum of the KT slices
+            // rows [4i, 4i+4) x nb tokens: fixed-order sum of the KT slices, all loads first
             const int KT = a.u_TR - a.u_T;
-            for (int w = et; w < kTRRows * nb; w += 128) {
-                const int row = i * kTRRows + w / nb, b = w % nb;
+            wait_count(fl_t(a), KT);
+            for (int w = et; w < 4 * nb; w += 128) {
+                const int row = i * 4 + w / nb, b = w % nb;
+                const float* src = a.tpart + static_cast<size_t>(row) * nb + b;
                 float s = 0.f;
-                for (int k = 0; k < KT; ++k) s += __ldcg(a.tpart + (static_cast<size_t>(k) * kBlk + row) * nb + b);
+                for (int k0 = 0; k0 < KT; k0 += 16) {  // fixed order over the K slices
+                    float p[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k)
+                        p[k] = k0 + k < KT ? __ldcg(src + static_cast<size_t>(k0 + k) * kBlk * nb) : 0.f;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k)
+                        if (k0 + k < KT) s += p[k];
+                }
                 uint16_t hi, lo;
                 split_bf16(row < a.r ? s : 0.f, hi, lo);
                 a.thl[static_cast<size_t>(b) * 256 + row] = hi;
@@ -588,32 +786,27 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                 uint64_t bits = 0;
                 if (t < un.nsub) {  // warp-uniform: tcgen05.ld is warp-collective
                     const bool mine = k < rows;
-                    const int n = i * kBlk + (mine ? k : 0);
-                    const float bias = mine ? __ldg(a.bias + n) : 0.f;
-                    for (int c = 0; c < nb; c += 8) {
-                        float v[8];
-                        acc8(a, S.tmem, quarter, acc, t, c, v);
+                    const float bias = mine ? __ldg(a.bias + i * kBlk + k) : 0.f;
+                    for (int c = 0; c < nb; c += 16) {
+                        float v[16];
+                        acc16(a, S.tmem, quarter, acc, t, c, v);
 #pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            if (v[e] + bias > 0.f) bits |= 1ull << (c + e);  // strict, :141
+                        for (int e = 0; e < 16; ++e)
+                            if (c + e < nb && v[e] + bias > 0.f) bits |= 1ull << (c + e);
                     }
                     bits = mine ? (bits & bmask) : 0ull;
                     if (mine) {
-                        a.mbits[n] = bits;
-                        a.vbits[n] = 0ull;
+                        a.mbits[i * kBlk + k] = bits;
+                        a.vbits[i * kBlk + k] = 0ull;
                     }
                 }
                 S.flag[k] = bits != 0;
-                // per-token |P_b| of this block
-                for (int b = 0; b < a.B; ++b) {
-                    const unsigned bal = __ballot_sync(0xffffffffu, (bits >> b) & 1ull);
-                    if (lane == 0 && bal) atomicAdd(&S.cnt[b], __popc(bal));
-                }
+                count_bits(S, bits, a.B, lane);
             }
             tc_fence_before();
             epi_bar();
             if (et == 0) mbar_arrive(&S.tempty[acc]);
-            const int n = epi_compact(S, rows, et, a.ulist + i * kBlk, 0);
+            const int n = epi_compact(S, rows, et, a.ulist + i * kBlk);
             if (et < a.B && S.cnt[et]) atomicAdd(a.pcount + et, S.cnt[et]);
             if (et == 0) {
                 a.ucnt[i] = n;
@@ -630,13 +823,10 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                 for (int t = 0; t < un.nsub; ++t) {  // warp-uniform (have == nsub > 0)
                     const int k = t * 128 + row0;
                     float* dst = part + ((static_cast<size_t>(j - 1) * a.nblk + i) * kBlk + k) * nb;
-                    for (int c = 0; c < nb; c += 8) {
-                        float v[8];
-                        acc8(a, S.tmem, quarter, acc, t, c, v);
-                        if (k < cnt) {
-                            *reinterpret_cast<float4*>(dst + c) = make_float4(v[0], v[1], v[2], v[3]);
-                            *reinterpret_cast<float4*>(dst + c + 4) = make_float4(v[4], v[5], v[6], v[7]);
-                        }
+                    for (int c = 0; c < nb; c += 16) {
+                        float v[16];
+                        acc16(a, S.tmem, quarter, acc, t, c, v);
+                        if (k < cnt) st16(dst + c, v, min(16, nb - c));
                     }
                 }
                 tc_fence_before();
@@ -650,42 +840,63 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                 // inputs written by earlier units: the block's lists, mask / survivor bits, g
                 if (gate && !a.dense) wait_count(fl_pre(a, i), 1);
                 if (!gate) wait_count(fl_gate(a, i), 1);
-                epi_bar();
                 if (et < 64) S.cnt[et] = 0;
                 epi_bar();
-                const int* list = gate ? (a.dense ? nullptr : a.ulist + i * kBlk) : a.vlist + i * kBlk;
+                // tiled unit: position k IS local row k (and Z slot k), else the k-th listed row
+                const int* list = un.pad ? nullptr : gate ? a.ulist + i * kBlk : a.vlist + i * kBlk;
                 for (int t = 0; t < 2; ++t) {
                     const int k = t * 128 + row0;
                     const bool mine = have && k < cnt;
                     const int n = mine ? i * kBlk + (list ? __ldcg(list + k) : k) : 0;
+                    const uint64_t mb = gate ? (a.dense ? bmask : (mine ? __ldcg(a.mbits + n) : 0ull))
+                                             : (a.dense ? bmask : (mine ? __ldcg(a.vbits + n) : 0ull));
                     uint64_t sbits = 0;
                     for (int c = 0; c < nb && t < un.nsub; c += 8) {  // warp-uniform bound
+                        // every global load of the chunk first, then the TMEM loads
+                        float4 pp[3][2], gv[2];
+                        const int np = KS - 1 < 3 ? KS - 1 : 3;
+#pragma unroll
+                        for (int s = 0; s < 3; ++s)
+                            if (s < np && mine) {
+                                const float4* src = reinterpret_cast<const float4*>(
+                                    part + ((static_cast<size_t>(s) * a.nblk + i) * kBlk + k) * nb + c);
+                                pp[s][0] = __ldcg(src);
+                                pp[s][1] = __ldcg(src + 1);
+                            }
+                        if (!gate && mine) {
+                            const float4* src = reinterpret_cast<const float4*>(a.G + static_cast<size_t>(n) * nb + c);
+                            gv[0] = __ldcg(src);
+                            gv[1] = __ldcg(src + 1);
+                        }
                         float v[8];
                         acc8(a, S.tmem, quarter, acc, t, c, v);
                         if (!mine) continue;
-                        for (int s = 1; s < KS; ++s) {  // fixed order: own slice, then 1, 2, ...
-                            const float* src = part + ((static_cast<size_t>(s - 1) * a.nblk + i) * kBlk + k) * nb + c;
-                            const float4 p0 = __ldcg(reinterpret_cast<const float4*>(src));
-                            const float4 p1 = __ldcg(reinterpret_cast<const float4*>(src + 4));
-                            v[0] += p0.x; v[1] += p0.y; v[2] += p0.z; v[3] += p0.w;
-                            v[4] += p1.x; v[5] += p1.y; v[6] += p1.z; v[7] += p1.w;
+#pragma unroll
+                        for (int s = 0; s < 3; ++s)  // fixed order: own slice, then 1, 2, ...
+                            if (s < np) {
+                                v[0] += pp[s][0].x; v[1] += pp[s][0].y; v[2] += pp[s][0].z; v[3] += pp[s][0].w;
+                                v[4] += pp[s][1].x; v[5] += pp[s][1].y; v[6] += pp[s][1].z; v[7] += pp[s][1].w;
+                            }
+                        for (int s = 4; s < KS; ++s) {
+                            const float4* src = reinterpret_cast<const float4*>(
+                                part + ((static_cast<size_t>(s - 1) * a.nblk + i) * kBlk + k) * nb + c);
+                            const float4 q0 = __ldcg(src), q1 = __ldcg(src + 1);
+                            v[0] += q0.x; v[1] += q0.y; v[2] += q0.z; v[3] += q0.w;
+                            v[4] += q1.x; v[5] += q1.y; v[6] += q1.z; v[7] += q1.w;
                         }
                         if (gate) {
                             // g per token; survivor iff predicted and g > 0 (ffn_exec.hpp:200)
-                            float* gd = a.G + static_cast<size_t>(n) * nb + c;
-                            *reinterpret_cast<float4*>(gd) = make_float4(v[0], v[1], v[2], v[3]);
-                            *reinterpret_cast<float4*>(gd + 4) = make_float4(v[4], v[5], v[6], v[7]);
+                            st16(a.G + static_cast<size_t>(n) * nb + c, v, 8);
 #pragma unroll
                             for (int e = 0; e < 8; ++e)
                                 if (v[e] > 0.f) sbits |= 1ull << (c + e);
                         } else {
                             // z = gated(g, u) on the token's survivor bit, else +0 -> Z^T hi / lo
-                            const uint64_t sb = a.dense ? bmask : __ldcg(a.vbits + n);
-                            const float* gs = a.G + static_cast<size_t>(n) * nb + c;
+                            const float g8[8] = {gv[0].x, gv[0].y, gv[0].z, gv[0].w, gv[1].x, gv[1].y, gv[1].z, gv[1].w};
 #pragma unroll
                             for (int e = 0; e < 8; ++e) {
                                 const int b = c + e;
-                                const float z = ((sb >> b) & 1ull) ? gated(__ldcg(gs + e), v[e], a.act) : 0.f;
+                                const float z = ((mb >> b) & 1ull) ? gated(g8[e], v[e], a.act) : 0.f;
                                 uint16_t hi, lo;
                                 split_bf16(z, hi, lo);
                                 a.zhl[static_cast<size_t>(b) * a.zpitch + i * kBlk + k] = hi;
@@ -694,30 +905,23 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                         }
                     }
                     if (gate) {
-                        const uint64_t mb = a.dense ? bmask : (mine ? __ldcg(a.mbits + n) : 0ull);
                         sbits &= mb & bmask;
-                        if (mine && !a.dense) a.vbits[n] = sbits;
-                        // dense: every row is read for up / down, the survivor bits are the z mask
-                        if (mine && a.dense) a.vbits[n] = sbits;
+                        if (mine) a.vbits[n] = sbits;
+                        // dense: every row is read for up / down; the bits mask z
                         S.flag[k] = a.dense ? mine : (sbits != 0);
-                        for (int b = 0; b < a.B; ++b) {
-                            const unsigned bal = __ballot_sync(0xffffffffu, (sbits >> b) & 1ull);
-                            if (lane == 0 && bal) atomicAdd(&S.cnt[b], __popc(bal));
-                        }
+                        count_bits(S, sbits, a.B, lane);
                     } else if (!mine && k < ((cnt + 63) / 64) * 64) {
                         // padding slots of the block's last 64-slot stage: exact zeros
-                        for (int b = 0; b < 2 * nb; ++b)
-                            a.zhl[static_cast<size_t>(b) * a.zpitch + i * kBlk + k] = 0;
+                        for (int b = 0; b < 2 * nb; ++b) a.zhl[static_cast<size_t>(b) * a.zpitch + i * kBlk + k] = 0;
                     }
                 }
                 tc_fence_before();
                 epi_bar();
                 if (et == 0) mbar_arrive(&S.tempty[acc]);
                 if (gate) {
-                    // survivor list of the block (positions in the union list -> local rows)
+                    // survivor list of the block (union positions -> local rows)
                     int* vl = a.vlist + i * kBlk;
-                    const int nv = epi_compact(S, cnt, et, vl, 0);
-                    // epi_compact wrote union positions; map them to local neuron rows
+                    const int nv = epi_compact(S, cnt, et, vl);
                     for (int k = et; k < nv; k += 128) {
                         const int pos = vl[k];
                         vl[k] = list ? __ldcg(list + pos) : pos;
@@ -740,16 +944,15 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
             for (int t = 0; t < 2; ++t) {
                 const int m = i * 256 + t * 128 + row0;
                 float* dst = a.ypart + (static_cast<size_t>(j) * a.ndt * 256 + m) * nb;
-                for (int c = 0; c < nb; c += 8) {
-                    float v[8];
+                for (int c = 0; c < nb; c += 16) {
+                    float v[16];
                     if (have) {
-                        acc8(a, S.tmem, quarter, acc, t, c, v);
+                        acc16(a, S.tmem, quarter, acc, t, c, v);
                     } else {
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) v[e] = 0.f;
+                        for (int e = 0; e < 16; ++e) v[e] = 0.f;
                     }
-                    *reinterpret_cast<float4*>(dst + c) = make_float4(v[0], v[1], v[2], v[3]);
-                    *reinterpret_cast<float4*>(dst + c + 4) = make_float4(v[4], v[5], v[6], v[7]);
+                    st16(dst + c, v, min(16, nb - c));
                 }
             }
             tc_fence_before();
@@ -759,19 +962,42 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                 signal(fl_down(a, i));
             }
         } else if (un.type == U_YR) {
+            // y rows [dt*256 + 64q, +64) x tokens in groups of 8: fixed-order sum of the S
+            // block-range partials, all loads first
             const int dt = i / 4, q = i % 4;
             wait_count(fl_down(a, dt), a.S);
-            for (int w = et; w < kYRRows * a.B; w += 128) {
-                const int m = dt * 256 + q * kYRRows + w % kYRRows, b = w / kYRRows;
+            const int groups = nb / 8;
+            for (int w = et; w < kYRRows * groups; w += 128) {
+                const int m = dt * 256 + q * kYRRows + w % kYRRows, c = (w / kYRRows) * 8;
                 if (m >= a.d) continue;
-                float s = 0.f;
-                for (int r = 0; r < a.S; ++r)
-                    s += __ldcg(a.ypart + (static_cast<size_t>(r) * a.ndt * 256 + m) * nb + b);
-                a.y[static_cast<size_t>(b) * a.d + m] = s;
+                float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                for (int r0 = 0; r0 < a.S; r0 += 8) {  // fixed order: ranges 0, 1, ..., S-1
+                    float4 p[8][2];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+                        if (r0 + r < a.S) {
+                            const float4* src = reinterpret_cast<const float4*>(
+                                a.ypart + (static_cast<size_t>(r0 + r) * a.ndt * 256 + m) * nb + c);
+                            p[r][0] = __ldcg(src);
+                            p[r][1] = __ldcg(src + 1);
+                        }
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+                        if (r0 + r < a.S) {
+                            s[0] += p[r][0].x; s[1] += p[r][0].y; s[2] += p[r][0].z; s[3] += p[r][0].w;
+                            s[4] += p[r][1].x; s[5] += p[r][1].y; s[6] += p[r][1].z; s[7] += p[r][1].w;
+                        }
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    if (c + e < a.B) a.y[static_cast<size_t>(c + e) * a.d + m] = s[e];
             }
             epi_bar();
         }
-        if (et == 0) mbar_arrive(&S.uqe[slot]);
+        if (et == 0) {
+            TC_TRACE(a, un.u, 4, gtimer());
+            mbar_arrive(&S.uqe[slot]);
+        }
     }
 }
 
@@ -782,7 +1008,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     const int warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&S.full[s], 1);
+            mbar_init(&S.full[s], kProdThreads + 1);  // 128 producer threads + the expect_tx
             mbar_init(&S.empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
@@ -795,7 +1021,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 1) {
+    if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&S.tmem)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
@@ -806,9 +1032,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     if (threadIdx.x == 0)
         for (int s = 0; s < kStages; ++s) mbar_arrive(&S.empty[s]);
     __syncthreads();
-    if (warp == 0) {
+    if (warp < kMmaWarp) {
         producer(a, maps, S, stages);
-    } else if (warp == 1) {
+    } else if (warp == kMmaWarp) {
         mma_issuer(a, S, stages);
     } else {
         epilogue(a, S);
@@ -816,7 +1042,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(S.tmem));
+    if (warp == kMmaWarp) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(S.tmem));
     if (threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(fl_exit(a), 1) == static_cast<int>(gridDim.x) - 1) {
@@ -831,7 +1057,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
 }  // namespace
 
 int tc_smem_bytes() { return kStages * kStageBytes + static_cast<int>(sizeof(TcSmem)) + 1024; }
-int tc_flag_ints(int nblk, int ndt) { return 8 + 5 * nblk + ndt; }
+int tc_flag_ints(int nblk, int ndt) { return 32 + 5 * nblk + ndt; }
 
 int launch_batch_tc(const TcMaps& maps, const TcArgs& a, int grid, void* stream) {
     const int smem = tc_smem_bytes();

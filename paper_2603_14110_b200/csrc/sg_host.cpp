@@ -90,6 +90,12 @@ struct sg_ctx {
     void* tmem_ws = nullptr;
     sg::TcArgs tw{};
     std::map<int, sg::TcMaps> tcmaps_ws;  // workspace maps per nb (box height N = 2 nb)
+    std::map<std::vector<int>, int*> tc_orders;  // device claim orders per unit geometry
+    unsigned long long* tc_trace = nullptr;      // optional unit trace (sg_ctx_enable_tc_trace)
+    size_t tc_trace_cap = 0;
+    bool tc_trace_on = false;
+    int tc_last_units = 0;
+    const int* tc_last_order = nullptr;
 };
 
 constexpr int kMaxStackLayers = 1024;
@@ -607,9 +613,8 @@ sg_status sg_layer_create(const sg_layer_desc* desc, sg_layer** out) {
     if (has_w) {
         // tensor maps of the batched tensor-core path (sg_batch_tc.cu)
         sg::TcMaps& tm = L->tcmaps;
-        bool ok = make_map(&tm.gate, V.gate, pd, Dl, pd, 1) &&
-                  make_map(&tm.up, V.ud, pd, Dl, 2 * pd, 1) &&
-                  make_map(&tm.down, V.ud + pd, pd, Dl, 2 * pd, 1);
+        bool ok = make_map(&tm.gate, V.gate, pd, Dl, pd, 128) && make_map(&tm.up, V.ud, pd, Dl, 2 * pd, 128) &&
+                  make_map(&tm.down, V.ud + pd, pd, Dl, 2 * pd, 64);
         if (ok && has_pred)
             ok = make_map(&tm.A, V.A, pr, Dl, pr, 128) && make_map(&tm.Bp, V.B, pd, r, pd, 128);
         L->has_tcmaps = ok;
@@ -693,7 +698,7 @@ sg_status sg_ctx_create(int32_t device, int64_t max_hidden, int64_t max_inter, i
     const size_t o_rec = take(Dm * 8), o_V = take(Dm * 4), o_zV = take(Dm * 4);
     const size_t o_vseg = take(Dm * 8);
     const size_t o_zD = take(Dm * 4);
-    const size_t o_ypart = take(static_cast<size_t>(G) * C->pitch_dmax * 8);
+    const size_t o_ypart = take(static_cast<size_t>(G) * C->pitch_dmax * 4);
     const size_t o_bar = take(8 * 256);
     const size_t o_ytag = take(static_cast<size_t>(C->pitch_dmax) * 8);
     const size_t o_stats = take(4 * 4 * kMaxStackLayers);
@@ -722,7 +727,7 @@ sg_status sg_ctx_create(int32_t device, int64_t max_hidden, int64_t max_inter, i
     W.V = reinterpret_cast<int*>(b + o_V);
     W.zV = reinterpret_cast<float*>(b + o_zV);
     W.zD = reinterpret_cast<float*>(b + o_zD);
-    W.ypart = reinterpret_cast<uint32_t*>(b + o_ypart);
+    W.ypart = reinterpret_cast<float*>(b + o_ypart);
     W.bar = reinterpret_cast<unsigned long long*>(b + o_bar);
     W.ytag = reinterpret_cast<uint32_t*>(b + o_ytag);
     W.stats = reinterpret_cast<int*>(b + o_stats);
@@ -747,6 +752,8 @@ sg_status sg_ctx_destroy(sg_ctx* C) {
     if (C->dbgdev) cudaFree(C->dbgdev);
     if (C->bmem) cudaFree(C->bmem);
     if (C->tmem_ws) cudaFree(C->tmem_ws);
+    for (auto& kv : C->tc_orders) cudaFree(kv.second);
+    if (C->tc_trace) cudaFree(C->tc_trace);
     delete C;
     return SG_OK;
 }
@@ -902,6 +909,77 @@ int k_slices(int pitch, int want) {
     return 1;
 }
 
+// The claim order of the tensor-core kernel's units (sg_batch_tc.cu): the predictor
+// chain, then GATE units block by block, with each block's UP units, each block
+// range's DOWN units and each d tile's YR units merged in `lag` claims after the
+// units they depend on (about one wave of the grid: by then those have finished),
+// so no stage waits for a whole previous stage. Topological by construction.
+std::vector<int> tc_schedule(const sg::TcArgs& a, int NX, int KT, int NTR, int lag) {
+    auto code = [](int t, int i, int j) { return (t << 24) | (i << 8) | j; };
+    enum { X = 1, T, TR, PRE, GATE, UP, DOWN, YR };
+    std::vector<int> order;
+    for (int k = 0; k < NX; ++k) order.push_back(code(X, k, 0));
+    for (int k = 0; k < KT; ++k) order.push_back(code(T, k, 0));
+    for (int k = 0; k < NTR; ++k) order.push_back(code(TR, k, 0));
+    if (!a.dense)
+        for (int b = 0; b < a.nblk; ++b) order.push_back(code(PRE, b, 0));
+    struct Item {
+        int code, ready_at;
+    };
+    std::vector<Item> ups, downs, yrs;
+    std::vector<int> up_done_at(static_cast<size_t>(a.nblk), -1), down_cnt(static_cast<size_t>(a.ndt), 0);
+    std::vector<int> down_last(static_cast<size_t>(a.ndt), 0);
+    auto range_lo = [&](int sr) { return sr * a.nblk / a.S; };
+    size_t gi = 0;
+    std::vector<int> gates;
+    for (int b = 0; b < a.nblk; ++b)
+        for (int ks = a.KSg - 1; ks >= 0; --ks) gates.push_back(code(GATE, b, ks));
+    size_t ui = 0, di = 0, yi = 0;
+    auto emit = [&](int c) {
+        order.push_back(c);
+        const int pos = static_cast<int>(order.size());
+        const int t = c >> 24, i = (c >> 8) & 0xffff, j = c & 0xff;
+        if (t == GATE && j == 0)  // the block's owner: its UP units may follow `lag` later
+            for (int ks = a.KSu - 1; ks >= 0; --ks) ups.push_back({code(UP, i, ks), pos + lag});
+        if (t == UP && j == 0) {
+            up_done_at[static_cast<size_t>(i)] = pos;
+            for (int sr = 0; sr < a.S; ++sr) {
+                if (i != range_lo(sr + 1) - 1) continue;  // the range's last block
+                int ready = 0;
+                for (int b = range_lo(sr); b < range_lo(sr + 1); ++b)
+                    ready = std::max(ready, up_done_at[static_cast<size_t>(b)]);
+                for (int dt = 0; dt < a.ndt; ++dt) downs.push_back({code(DOWN, dt, sr), ready + lag});
+            }
+        }
+        if (t == DOWN) {
+            down_last[static_cast<size_t>(i)] = pos;
+            if (++down_cnt[static_cast<size_t>(i)] == a.S)
+                for (int q = 0; q < 4; ++q) yrs.push_back({code(YR, i * 4 + q, 0), pos + lag});
+        }
+    };
+    for (;;) {
+        const int pos = static_cast<int>(order.size());
+        if (yi < yrs.size() && yrs[yi].ready_at <= pos) {
+            emit(yrs[yi++].code);
+        } else if (di < downs.size() && downs[di].ready_at <= pos) {
+            emit(downs[di++].code);
+        } else if (ui < ups.size() && ups[ui].ready_at <= pos) {
+            emit(ups[ui++].code);
+        } else if (gi < gates.size()) {
+            emit(gates[gi++]);
+        } else if (ui < ups.size()) {
+            emit(ups[ui++].code);
+        } else if (di < downs.size()) {
+            emit(downs[di++].code);
+        } else if (yi < yrs.size()) {
+            emit(yrs[yi++].code);
+        } else {
+            break;
+        }
+    }
+    return order;
+}
+
 // One tensor-core launch: B tokens through one layer (dense != 0: every row, no predictor).
 sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float* ys, void* stream,
                      int dense) {
@@ -919,9 +997,15 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     a.nblk = (a.D + 255) / 256;
     a.ndt = (a.pitch_d + 255) / 256;
     a.dense = dense;
+    // blocks at least this dense (per 1024) stream whole by TMA tiles instead of row
+    // gathers: ~26 vs ~55 GB/s per SM (tools/bw_tma.cu) puts the break-even near 0.47
+    a.tile_g = env_int("SG_TC_TILE_G", 480);
+    a.tile_u = env_int("SG_TC_TILE_U", 480);
     a.x = xs;
     a.y = ys;
     a.bias = L->view.bias;
+    a.gate = L->view.gate;
+    a.ud = L->view.ud;
     // K slices of the gate / up units: enough units to spread the union rows over the
     // SMs while the owner slice's fixed-order partial sum stays small (partials are
     // 256 rows x nb fp32): SG_TC_KSG / SG_TC_KSU override
@@ -932,7 +1016,7 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     a.ksu = a.pitch_d / a.KSu;
     a.S = std::max(1, std::min({env_int("SG_TC_S", 8), kTcSMax, a.nblk}));
     a.kst = 256;
-    const int NX = 8, KT = dense ? 0 : (a.pitch_d + a.kst - 1) / a.kst, NTR = dense ? 0 : a.pitch_r / 16;
+    const int NX = 32, KT = dense ? 0 : (a.pitch_d + a.kst - 1) / a.kst, NTR = dense ? 0 : a.pitch_r / 4;
     const int NPRE = dense ? 0 : a.nblk;
     a.u_T = NX;
     a.u_TR = a.u_T + KT;
@@ -942,6 +1026,26 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     a.u_DOWN = a.u_UP + a.nblk * a.KSu;
     a.u_YR = a.u_DOWN + a.ndt * a.S;
     a.u_end = a.u_YR + a.ndt * 4;
+    {  // the claim order for this unit geometry, uploaded once per ctx (graph-capture safe after)
+        const int lag = env_int("SG_TC_LAG", C->G);
+        std::vector<int> key = {a.nblk, a.KSg, a.KSu, a.ndt, a.S, a.dense, NX, KT, NTR, lag};
+        auto oit = C->tc_orders.find(key);
+        if (oit == C->tc_orders.end()) {
+            const std::vector<int> order = tc_schedule(a, NX, KT, NTR, lag);
+            if (static_cast<int>(order.size()) != a.u_end)
+                return fail(SG_ERR_CUDA, "tensor-core schedule: unit count mismatch");
+            int* dev = nullptr;
+            DeviceGuard dg0(C->device);
+            SG_CUDA(cudaMalloc(&dev, order.size() * sizeof(int)));
+            SG_CUDA(cudaMemcpy(dev, order.data(), order.size() * sizeof(int), cudaMemcpyHostToDevice));
+            oit = C->tc_orders.emplace(key, dev).first;
+        }
+        a.order = oit->second;
+        a.n_units = a.u_end;
+    }
+    a.trace = C->tc_trace_on && C->tc_trace_cap >= static_cast<size_t>(a.n_units) ? C->tc_trace : nullptr;
+    C->tc_last_units = a.n_units;
+    C->tc_last_order = a.order;
     // workspace maps for this nb (box height N), cached per ctx
     auto it = C->tcmaps_ws.find(a.nb);
     if (it == C->tcmaps_ws.end()) {
@@ -1037,6 +1141,8 @@ sg_status sg_ffn_forward_batch(sg_ctx* C, const sg_layer* L, const float* xs, in
     a.bias = L->view.bias;
     a.gate = L->view.gate;
     a.ud = L->view.ud;
+    a.gate = L->view.gate;
+    a.ud = L->view.ud;
     SG_CUDA(cudaMemsetAsync(a.bad, 0, sizeof(int), static_cast<cudaStream_t>(stream)));
     const int e = sg::launch_batch(a, xs, ys, stream);
     if (e != 0) return fail(SG_ERR_CUDA, std::string("batch launch: ") +
@@ -1060,6 +1166,39 @@ sg_status sg_ffn_forward_batch_dense(sg_ctx* C, const sg_layer* L, const float* 
     C->blast_B = batch;
     C->blast_stack = false;
     C->blast_path = 3;
+    return SG_OK;
+}
+
+sg_status sg_ctx_enable_tc_trace(sg_ctx* C, int32_t max_units) {
+    if (C == nullptr || max_units < 0) return fail(SG_ERR_USAGE, "bad arguments");
+    DeviceGuard dg(C->device);
+    if (C->tc_trace) cudaFree(C->tc_trace);
+    C->tc_trace = nullptr;
+    C->tc_trace_cap = 0;
+    C->tc_trace_on = max_units > 0;
+    if (max_units > 0) {
+        SG_CUDA(cudaMalloc(&C->tc_trace, static_cast<size_t>(max_units) * 6 * 8));
+        SG_CUDA(cudaMemset(C->tc_trace, 0, static_cast<size_t>(max_units) * 6 * 8));
+        C->tc_trace_cap = static_cast<size_t>(max_units);
+    }
+    return SG_OK;
+}
+
+sg_status sg_ctx_read_tc_trace(sg_ctx* C, void* stream, int32_t max_units, uint64_t* out, int32_t* n_units) {
+    if (C == nullptr || out == nullptr || !C->tc_trace) return fail(SG_ERR_USAGE, "tc trace not enabled");
+    DeviceGuard dg(C->device);
+    SG_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    const int n = std::min<int>(max_units, C->tc_last_units);
+    SG_CUDA(cudaMemcpy(out, C->tc_trace, static_cast<size_t>(n) * 6 * 8, cudaMemcpyDeviceToHost));
+    if (n_units) *n_units = n;
+    return SG_OK;
+}
+
+sg_status sg_tc_unit_codes(sg_ctx* C, int32_t* out, int32_t max_units) {
+    if (C == nullptr || out == nullptr || C->tc_last_order == nullptr) return fail(SG_ERR_USAGE, "no tc call");
+    DeviceGuard dg(C->device);
+    const int n = std::min<int>(max_units, C->tc_last_units);
+    SG_CUDA(cudaMemcpy(out, C->tc_last_order, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost));
     return SG_OK;
 }
 

@@ -48,8 +48,7 @@ struct WorkView {
     int* V;               // [Dmax] compacted GLOBAL survivor indices
     float* zV;            // [Dmax] gated value per survivor
     float* zD;            // [Dmax] dense pipeline: z per neuron
-    uint32_t* ypart;      // [G * pitch_dmax] per-CTA partial outputs as {value bits, tag}
-                          // pairs: phase D polls them instead of a grid barrier
+    float* ypart;         // [G * pitch_dmax] per-CTA partial outputs
     uint32_t* ytag;       // [2 * pitch_dmax] {y bits, tag} published by phase D inside a stack
     unsigned long long* bar;  // 8 grid-barrier counters, 256 B apart (see grid_barrier)
     int* stats;           // [4 per layer] p, v, nonfinite(x), pipeline
@@ -134,9 +133,9 @@ struct TcMaps {            // TMA tensor maps (bf16, SWIZZLE_128B, 64-element in
     CUtensorMap zhl;       // Z^T hi/lo   [N][zpitch]         box {64, N}
     CUtensorMap Bp;        // predictor B [r][pitch_d]        box {64, 128}
     CUtensorMap A;         // predictor A [D][pitch_r]        box {64, 128}
-    CUtensorMap gate;      // gate rows   [D][pitch_d]        box {64, 1} (gather4)
+    CUtensorMap gate;      // gate rows   [D][pitch_d]        box {64, 128} (dense comparator)
     CUtensorMap up;        // up rows     [D][pitch_d], row stride 2*pitch_d (ud, first half)
-    CUtensorMap down;      // down rows   [D][pitch_d], row stride 2*pitch_d (ud + pitch_d)
+    CUtensorMap down;      // down rows   [D][pitch_d], row stride 2*pitch_d (ud + pitch_d) box {64, 64}
 };
 struct TcArgs {
     int B, nb, N;          // tokens, B rounded up to 8, MMA N = 2*nb (hi | lo columns)
@@ -146,12 +145,18 @@ struct TcArgs {
     int KSg, ksg, KSu, ksu;  // gate / up K slices and their width
     int ndt, S;            // d tiles of 256 outputs, block ranges of the down GEMM
     int dense;             // 1: dense comparator (no predictor; every row)
-    int u_T, u_TR, u_PRE, u_GATE, u_UP, u_DOWN, u_YR, u_end;  // unit index ranges
+    int tile_g, tile_u;    // per-1024 density at which a gate / up(+down) block is tiled, not gathered
+    int u_T, u_TR, u_PRE, u_GATE, u_UP, u_DOWN, u_YR, u_end;  // unit counts by type (prefix sums)
+    const int* order;      // [n_units] claim order: type << 24 | i << 8 | j (host-built)
+    int n_units;
+    unsigned long long* trace;  // optional [n_units][6] %globaltimer stamps (tools/tc_trace.py)
     int zpitch;            // slots of Z^T per row (nblk * 256)
     int xpitch;            // elements per X^T row (the ctx's max pitch; T^T rows are 256)
     const float* x;        // [B][d] input tokens
     float* y;              // [B][d] outputs
     const float* bias;     // [D]
+    const uint16_t* gate;  // [D][pitch_d]      gathered rows (cp.async)
+    const uint16_t* ud;    // [D][2*pitch_d]    [up | down] rows
     uint16_t* xhl;         // [N][pitch_d]
     float* tpart;          // [KT][256][nb]
     uint16_t* thl;         // [N][pitch_r]

@@ -308,16 +308,6 @@ __device__ __forceinline__ float ld_tagged(const void* p, uint32_t tag) {
     return __uint_as_float(v);
 }
 
-// 8 partial-y values of one chunk as tagged {value, tag} pairs (two 16-B stores:
-// each 8-B pair is one aligned half of a vector store, seen whole by a v2 load).
-__device__ __forceinline__ void st_partial8(uint32_t* dst, const float* v, uint32_t tag) {
-#pragma unroll
-    for (int e = 0; e < 8; e += 2)
-        asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %2};" ::"l"(dst + 2 * e),
-                     "r"(__float_as_uint(v[e])), "r"(tag), "r"(__float_as_uint(v[e + 1]))
-                     : "memory");
-}
-
 // ---------------------------------------------------------------------------
 // Grid barrier on kBarCounters monotonically increasing 64-bit counters
 // (each in its own 256-B block, so they live in different L2 slices). CTA c
@@ -1057,8 +1047,7 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
 // chunks t and t + 512 into its partial y, survivors in P order.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkView& W,
-                                                const Smem& sm, const SmemPlan& S, RunState& rs,
-                                                uint32_t ptag) {
+                                                const Smem& sm, const SmemPlan& S, RunState& rs) {
     const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nch = L.pitch_d >> 3;
     const int n0 = split_lo(c, gridDim.x, L.D);
@@ -1072,6 +1061,10 @@ __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkVi
     // gt + 128k in registers), so u — and therefore z and y — are bitwise the
     // same as in the dense / parallel pipelines (ffn_exec_tests.cpp:124-137, :171-192)
     const int grp = warp / kGroupWarps, gt = tid % kGroupThreads;
+#ifdef SG_SV_XREGS
+    XRegs X;
+    load_xregs(sm.xs, nch, gt, X);
+#endif
     float* gred = sm.reda + grp * (2 * kGroupWarps * 4);
     int gpar = 0;
     float* us = sm.reda + kGroups * 2 * kGroupWarps * 4;  // u of the group's rows
@@ -1122,13 +1115,21 @@ __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkVi
                 reinterpret_cast<const uint16_t*>(rows + static_cast<size_t>(j1) * ud_bytes)};
             float o[2];
             if (j1 < m) {
+#ifdef SG_SV_XREGS
+                group_dot<2>(rr, X, sm.xs, nch, gt, grp, gred, gpar, o);
+#else
                 group_dot_xs<2>(rr, sm.xs, nch, gt, grp, gred, gpar, o);
+#endif
                 if (gt == 0) {
                     us[j0] = o[0];
                     us[j1] = o[1];
                 }
             } else if (j0 < m) {
+#ifdef SG_SV_XREGS
+                group_dot<1>(rr, X, sm.xs, nch, gt, grp, gred, gpar, o);
+#else
                 group_dot_xs<1>(rr, sm.xs, nch, gt, grp, gred, gpar, o);
+#endif
                 if (gt == 0) us[j0] = o[0];
             }
         }
@@ -1159,9 +1160,17 @@ __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkVi
         }
     }
     if (tid < 2) bu[tid] += (ngroups + 1 - tid) / 2;  // buffer 0: ceil(n/2), buffer 1: floor(n/2)
-    // this CTA's partial y, tagged with the layer's exchange tag (phase D polls it)
-    if (h0) st_partial8(W.ypart + 2 * (static_cast<size_t>(c) * L.pitch_d + ch0 * 8), a0, ptag);
-    if (h1) st_partial8(W.ypart + 2 * (static_cast<size_t>(c) * L.pitch_d + ch1 * 8), a1, ptag);
+    // this CTA's partial y
+    if (h0) {
+        float4* dst = reinterpret_cast<float4*>(W.ypart + static_cast<size_t>(c) * L.pitch_d + ch0 * 8);
+        dst[0] = make_float4(a0[0], a0[1], a0[2], a0[3]);
+        dst[1] = make_float4(a0[4], a0[5], a0[6], a0[7]);
+    }
+    if (h1) {
+        float4* dst = reinterpret_cast<float4*>(W.ypart + static_cast<size_t>(c) * L.pitch_d + ch1 * 8);
+        dst[0] = make_float4(a1[0], a1[1], a1[2], a1[3]);
+        dst[1] = make_float4(a1[4], a1[5], a1[6], a1[7]);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1171,7 +1180,7 @@ __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkVi
 // neuron range with z from zD; parallel: the survivor list of phase C.
 // ---------------------------------------------------------------------------
 template <int kPipe>
-__device__ void partial_down(const LayerView& L, const WorkView& W, const Smem& sm, uint32_t ptag) {
+__device__ void partial_down(const LayerView& L, const WorkView& W, const Smem& sm) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
     const int nch = L.pitch_d >> 3;
     const int n0 = split_lo(c, G, L.D), n1 = split_lo(c + 1, G, L.D);
@@ -1218,7 +1227,9 @@ __device__ void partial_down(const LayerView& L, const WorkView& W, const Smem& 
             for (int u = 0; u < kU; ++u)
                 if (z[u] != 0.f) axpy8(w[u], z[u], acc);
         }
-        st_partial8(W.ypart + 2 * (static_cast<size_t>(c) * L.pitch_d + ch * 8), acc, ptag);
+        float4* dst = reinterpret_cast<float4*>(W.ypart + static_cast<size_t>(c) * L.pitch_d + ch * 8);
+        dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
     }
 }
 
@@ -1279,7 +1290,7 @@ __device__ __noinline__ void write_index_sets(int gbase, int gstride, const int*
 // its latency (divisions, parameter reads) hides under the barrier.
 struct DownPlan {
     int c0, ncols, ngrp, g0, g1;
-    const uint32_t* src;  // this thread's first tagged partial (column c0 + tid % ncols)
+    const float* src;  // this thread's first partial (column c0 + tid % ncols)
 };
 __device__ __forceinline__ DownPlan down_plan(const LayerView& L, const WorkView& W) {
     const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
@@ -1294,7 +1305,7 @@ __device__ __forceinline__ DownPlan down_plan(const LayerView& L, const WorkView
         const int grp = tid / p.ncols;
         p.g0 = split_lo(grp, p.ngrp, G);
         p.g1 = split_lo(grp + 1, p.ngrp, G);
-        p.src = W.ypart + 2 * (static_cast<size_t>(p.g0) * L.pitch_d + p.c0 + tid % p.ncols);
+        p.src = W.ypart + static_cast<size_t>(p.g0) * L.pitch_d + p.c0 + tid % p.ncols;
     }
     asm volatile("" ::"r"(p.c0), "r"(p.ncols), "r"(p.ngrp), "r"(p.g0), "r"(p.g1), "l"(p.src));
     return p;
@@ -1303,7 +1314,6 @@ __device__ __forceinline__ DownPlan down_plan(const LayerView& L, const WorkView
 template <int kPipe>
 __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm, float* y,
                            bool want_sets, bool publish, uint32_t ytag, const DownPlan& dp) {
-    const uint32_t ptag = ytag;  // the partials carry the same exchange tag
     const int tid = threadIdx.x;
     if (kPipe != 0 && want_sets && (tid >> 5) == kWarps)
         write_index_sets(L.gbase, L.gstride, L.gidx, L.D, W.cnt, W.plist, W.gN, W.vseg, W.P, W.gP,
@@ -1313,31 +1323,19 @@ __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm
     if (ncols > 0) {
         if (tid < ngrp * ncols) {
             const int g0 = dp.g0, g1 = dp.g1;
-            // the partials are polled as tagged values (no grid barrier): all loads
-            // in flight at once, stragglers re-polled, then the fixed-order sum
+            // all loads in flight before the (ordered) sum: one L2 round trip
             constexpr int kPer = 12;
-            const uint32_t* src = dp.src;
-            uint32_t v[kPer], t[kPer];
+            const float* src = dp.src;
+            float v[kPer];
 #pragma unroll
-            for (int i = 0; i < kPer; ++i) {
-                v[i] = 0u;
-                t[i] = ptag;
-                if (g0 + i < g1)
-                    asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];"
-                                 : "=r"(v[i]), "=r"(t[i])
-                                 : "l"(src + 2 * static_cast<size_t>(i) * L.pitch_d)
-                                 : "memory");
-            }
+            for (int i = 0; i < kPer; ++i)
+                v[i] = g0 + i < g1 ? __ldcg(src + static_cast<size_t>(i) * L.pitch_d) : 0.f;
             float s = 0.f;
 #pragma unroll
-            for (int i = 0; i < kPer; ++i) {
-                if (g0 + i >= g1) continue;
-                float f = __uint_as_float(v[i]);
-                if (t[i] != ptag) f = ld_tagged(src + 2 * static_cast<size_t>(i) * L.pitch_d, ptag);
-                s += f;
-            }
+            for (int i = 0; i < kPer; ++i)
+                if (g0 + i < g1) s += v[i];
             for (int g = g0 + kPer; g < g1; ++g)
-                s += ld_tagged(src + 2 * static_cast<size_t>(g - g0) * L.pitch_d, ptag);
+                s += __ldcg(src + static_cast<size_t>(g - g0) * L.pitch_d);
             part[tid] = s;
         }
         __syncthreads();
@@ -1407,18 +1405,14 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
     }
     phase_gather<kPipe>(L, W, sm, S);
     SG_STAMP(dbg, 14);
-    // the layer's exchange tag: the barrier count after this layer's arrive
-    const uint32_t ptag = rs.tag0 + rs.bar_k + 1u;
     if (kPipe == 2) {
-        survivor_updown(L, W, sm, S, rs, ptag);
+        survivor_updown(L, W, sm, S, rs);
     } else {
-        partial_down<kPipe>(L, W, sm, ptag);
+        partial_down<kPipe>(L, W, sm);
     }
     SG_STAMP(dbg, 7);
-    // stage the next layer's predictor weights and hot prefix: this CTA's ring and
-    // survivor rows are done, phase D uses reda. The partials travel tagged, so phase D
-    // waits only for the data it sums; the barrier arrive keeps the tag bookkeeping,
-    // and only the last layer (index sets over every CTA's counts) waits on it.
+    // stage the next layer's predictor weights and hot prefix during the
+    // barrier: this CTA's ring and survivor rows are done, phase D uses reda
     grid_arrive(W, rs);
     bool next_staged = false;
     if (kPipe != 0 && next != nullptr) {
@@ -1426,7 +1420,7 @@ __device__ bool run_layer(const LayerView& L, const WorkView& W, const Smem& sm,
         if (kPipe == 2) preissue_hot(*next, sm, S);
     }
     const DownPlan dp = down_plan(L, W);
-    if (want_sets || next == nullptr) grid_wait(W, rs);
+    grid_wait(W, rs);
     SG_STAMP(dbg, 8);
     phase_down<kPipe>(L, W, sm, y, want_sets, next != nullptr, rs.tag0 + rs.bar_k, dp);
     SG_STAMP(dbg, 9);

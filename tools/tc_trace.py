@@ -1,0 +1,81 @@
+#!/usr/bin/env python
+"""Timeline of one tensor-core batched-decode launch (csrc/sg_batch_tc.cu) from the
+per-unit %globaltimer trace (sg_ctx_enable_tc_trace).
+
+  python tools/tc_trace.py --batch 8 [--dense] [--config 7b]
+
+Per unit type: count, when the first / last unit was claimed and finished (us from
+the launch's first claim), mean wait for inputs, mean load (claim -> loads issued) and
+epilogue times, and the share of the launch the SMs spent busy per phase.
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+TYPES = {1: "X", 2: "T", 3: "TR", 4: "PRE", 5: "GATE", 6: "UP", 7: "DOWN", 8: "YR"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="7b")
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--dense", action="store_true")
+    args = ap.parse_args()
+    import torch
+
+    from paper_2603_14110_b200 import _capi as capi
+    from paper_2603_14110_b200.ffn_exec import Context, check
+    from paper_2603_14110_b200.model import CONFIGS, build_host_layer, upload
+    cfg = CONFIGS[args.config]
+    d, D, B = cfg["d"], cfg["D"], args.batch
+    h = build_host_layer(d, D, cfg["act"], seed=0, eval_tokens=max(16, B))
+    layer = upload(h, d, D, cfg["act"], 256)
+    ctx = Context(0, d, D, 256)
+    lib = capi.lib()
+    X = torch.tensor(h.xs[:, :B].T.copy(), dtype=torch.float32, device="cuda")
+    Y = torch.zeros_like(X)
+    fn = lib.sg_ffn_forward_batch_dense if args.dense else lib.sg_ffn_forward_batch
+    for _ in range(3):
+        check(fn(ctx.handle, layer.handle, C.c_void_p(X.data_ptr()), B, C.c_void_p(Y.data_ptr()), None))
+    torch.cuda.synchronize()
+    check(lib.sg_ctx_enable_tc_trace(ctx.handle, 8192))
+    check(fn(ctx.handle, layer.handle, C.c_void_p(X.data_ptr()), B, C.c_void_p(Y.data_ptr()), None))
+    out = np.zeros((8192, 6), dtype=np.uint64)
+    n = C.c_int32(0)
+    check(lib.sg_ctx_read_tc_trace(ctx.handle, None, 8192, out.ctypes.data_as(C.c_void_p), C.byref(n)))
+    tr = out[:n.value].astype(np.int64)
+    t0 = tr[:, 0][tr[:, 0] > 0].min()
+    rel = (tr[:, :5] - t0) / 1e3
+    codes = np.zeros(n.value, dtype=np.int32)
+    check(lib.sg_tc_unit_codes(ctx.handle, codes.ctypes.data_as(C.c_void_p), n.value))
+    order = codes >> 24
+    end = rel[:, 4].max()
+    print(f"{'dense' if args.dense else 'sparse'} B={B}: {n.value} units, launch span {end:.1f} us")
+    print(f"{'type':6s} {'n':>5s} {'claim0':>8s} {'claim1':>8s} {'done0':>8s} {'done1':>8s} "
+          f"{'wait':>7s} {'load':>7s} {'mma':>7s} {'epi':>7s}")
+    for t, name in TYPES.items():
+        sel = order == t
+        if not sel.any():
+            continue
+        r = rel[sel]
+        wait = r[:, 1] - r[:, 0]
+        load = r[:, 2] - r[:, 1]
+        mma = r[:, 3] - r[:, 2]
+        epi = r[:, 4] - r[:, 3]
+        print(f"{name:6s} {sel.sum():5d} {r[:, 0].min():8.1f} {r[:, 0].max():8.1f} {r[:, 4].min():8.1f} "
+              f"{r[:, 4].max():8.1f} {wait.mean():7.2f} {load.mean():7.2f} {mma.mean():7.2f} {epi.mean():7.2f}")
+    sms = tr[:, 5]
+    busy = np.zeros(int(sms.max()) + 1)
+    for k in range(n.value):
+        busy[sms[k]] += rel[k, 4] - rel[k, 1]
+    print(f"SM busy (inputs ready -> epilogue end) mean {busy.mean():.1f} us of {end:.1f}")
+
+
+if __name__ == "__main__":
+    main()
