@@ -5,7 +5,7 @@
 //
 // SVD: the reference's Eigen BDCSVD is exact. Here min(D, d) <= 1024 (and
 // D * d <= 4M) runs the exact one-sided Jacobi SVD on the host; larger shapes the
-// randomized rank-(r+8) range finder on the GPU, so spectral.singular_values then
+// randomized rank-(r+32) range finder (4 power iterations) on the GPU, so spectral.singular_values then
 // holds the leading rank + 1 values only.
 #pragma once
 

@@ -287,9 +287,20 @@ inline FfnResult dense_ffn(const FfnWeights& w, const Vec& x) {
     return l.forward(gpu::context_for(l), Pipeline::Dense, x);
 }
 
+// The standalone mask is exact: f64 on the GPU in det_dot order (sg_predict_mask_f64),
+// so it equals the reference bit for bit; the executors' internal masks use the
+// layer's bf16 predictor (gpu::Layer::predict is that one).
 inline Mask predict_mask(const Predictor& pred, const Vec& x) {
-    const auto& l = gpu::layer_for(nullptr, &pred);
-    return l.predict(gpu::context_for(l), x);
+    validate(pred);
+    if (x.size() != pred.hidden_size()) throw DataError("predictor input length does not match hidden size");
+    Mask m;
+    m.active.assign(static_cast<std::size_t>(pred.inter_size()), 0);
+    std::int64_t cnt = 0;
+    detail::check(sg_predict_mask_f64(0, pred.A.data(), pred.B.data(), pred.bias.data(),
+                                      pred.inter_size(), pred.rank, pred.hidden_size(), x.data(),
+                                      m.active.data(), &cnt));
+    m.predicted_active_count = cnt;
+    return m;
 }
 
 inline FfnResult sparse_ffn_parallel(const FfnWeights& w, const Predictor& pred, const Vec& x) {

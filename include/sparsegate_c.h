@@ -315,6 +315,15 @@ sg_status sg_greedy_calibrate(const double* scores, const double* weights, int64
  * svd_mode: 0 = exact (one-sided Jacobi, host; small shapes), 1 = randomized
  * (range finder of width k + 8, 2 power iterations, CholeskyQR2 on the GPU). */
 
+/* predict_mask (ffn_exec.hpp:125-146) in f64 on the GPU, bit-identical to the
+ * reference: t = B x and pre = A t + bias with common.hpp's det_dot reduction order
+ * (blocked 64, balanced tree, no FMA contraction); mask[i] = pre_i > 0 strictly.
+ * Host arrays (A inter x rank, B rank x hidden, bias inter, x hidden; row-major f64).
+ * The executors' own masks use the bf16 predictor of the layer. */
+sg_status sg_predict_mask_f64(int32_t device, const double* A, const double* B, const double* bias,
+                              int64_t inter, int64_t rank, int64_t hidden, const double* x,
+                              uint8_t* mask, int64_t* count);
+
 /* factorization.hpp:31-64: S = chol(X X^T + lambda I) (d x d lower) and S^-1, with the
  * damping ladder lambda = multipliers[k] * epsilon * trace(X X^T) / d tried in order;
  * X is d x T (hidden x tokens). SG_ERR_DATA when every rung fails. */

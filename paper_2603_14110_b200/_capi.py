@@ -109,6 +109,7 @@ SYMBOLS = [
                                        _VP, _VP]),
     ("sg_synthetic_fixture_bf16", C.c_int, [_I64, _I64, _I64, _I64, _D, C.c_uint64, _VP, _VP,
                                             _VP, _VP, _VP]),
+    ("sg_predict_mask_f64", C.c_int, [_I32, _VP, _VP, _VP, _I64, _I64, _I64, _VP, _VP, C.POINTER(_I64)]),
     ("sg_cholesky_whitening", C.c_int, [_VP, _I64, _I64, _D, _VP, _I32, _VP, _VP, C.POINTER(_D)]),
     ("sg_build_predictor", C.c_int, [_VP, _I64, _I64, _VP, _I64, _I64, _I32, _I32, C.c_uint64, _D, _VP,
                                      _I32, _VP, _VP, _VP, _I64, C.POINTER(_D), C.POINTER(_D)]),

@@ -100,6 +100,40 @@ __global__ void damage_kernel(const double* gp, const double* up,
     }
 }
 
+// common.hpp:52-90 det_dot on the device, bit for bit: products rounded one by one
+// (no FMA contraction), blocks of 64 reduced by the balanced binary tree (split at
+// n/2), block results accumulated left to right.
+__device__ double tree_sum_dev(const double* v, int n) {
+    if (n == 0) return 0.0;
+    if (n == 1) return v[0];
+    const int half = n / 2;
+    return __dadd_rn(tree_sum_dev(v, half), tree_sum_dev(v + half, n - half));
+}
+__device__ double det_dot_dev(const double* a, const double* b, int n) {
+    double buf[64];
+    double total = 0.0;
+    for (int base = 0; base < n; base += 64) {
+        const int m = n - base < 64 ? n - base : 64;
+        for (int j = 0; j < m; ++j) buf[j] = __dmul_rn(a[base + j], b[base + j]);
+        total = __dadd_rn(total, tree_sum_dev(buf, m));
+    }
+    return total;
+}
+// predict_mask (ffn_exec.hpp:125-146) in f64: t = B x (rows), then pre_i = A_i . t + b_i
+__global__ void predict_t_kernel(const double* B, const double* x, int r, int d, double* t) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < r) t[j] = det_dot_dev(B + static_cast<size_t>(j) * d, x, d);
+}
+__global__ void predict_pre_kernel(const double* A, const double* t, const double* bias, int D, int r,
+                                   uint8_t* mask, int* count) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= D) return;
+    const double pre = __dadd_rn(det_dot_dev(A + static_cast<size_t>(i) * r, t, r), bias[i]);
+    const bool on = pre > 0.0;
+    mask[i] = on ? 1 : 0;
+    if (on) atomicAdd(count, 1);
+}
+
 struct Dev {
     double* p = nullptr;
     Dev() = default;
@@ -383,7 +417,7 @@ sg_status randomized_svd(const double* M_host, int64_t m, int64_t n, int64_t k, 
 // Thin SVD of M (m x n row-major) truncated to k: exact (Jacobi) or randomized.
 sg_status svd_k(const double* M, int64_t m, int64_t n, int64_t k, int mode, uint64_t seed, std::vector<double>* U,
                 std::vector<double>& s, std::vector<double>* V) {
-    if (mode == 1) return randomized_svd(M, m, n, k, 8, 2, seed, U, s, V);
+    if (mode == 1) return randomized_svd(M, m, n, k, 32, 4, seed, U, s, V);
     const bool tr = m < n;  // Jacobi wants rows >= cols: work on M^T and swap U, V
     const int64_t rm = tr ? n : m, rn = tr ? m : n;
     std::vector<double> Mt;
@@ -572,6 +606,33 @@ sg_status sg_damage_weights(const double* gate, const double* up, const double* 
     damage_kernel<<<1024, 256>>>(GP.p, UP.p, N2.p, static_cast<int>(D), static_cast<int>(T), activation, GP.p);
     OFF_CUDA(cudaGetLastError());
     OFF_CUDA(cudaMemcpy(weights, GP.p, static_cast<size_t>(D * T) * 8, cudaMemcpyDeviceToHost));
+    return SG_OK;
+}
+
+sg_status sg_predict_mask_f64(int32_t device, const double* A, const double* B, const double* bias, int64_t D,
+                              int64_t r, int64_t d, const double* x, uint8_t* mask, int64_t* count) {
+    if (!A || !B || !bias || !x || !mask || D < 1 || r < 1 || d < 1)
+        return sg_internal_fail(SG_ERR_USAGE, "predict_mask_f64: bad arguments");
+    OFF_CUDA(cudaSetDevice(device));
+    Dev Ad(static_cast<size_t>(D * r)), Bd(static_cast<size_t>(r * d)), bd(static_cast<size_t>(D)),
+        xd(static_cast<size_t>(d)), td(static_cast<size_t>(r)), md(static_cast<size_t>(D + 15) / 8 + 1);
+    OFF_CUDA(cudaMemcpy(Ad.p, A, static_cast<size_t>(D * r) * 8, cudaMemcpyHostToDevice));
+    OFF_CUDA(cudaMemcpy(Bd.p, B, static_cast<size_t>(r * d) * 8, cudaMemcpyHostToDevice));
+    OFF_CUDA(cudaMemcpy(bd.p, bias, static_cast<size_t>(D) * 8, cudaMemcpyHostToDevice));
+    OFF_CUDA(cudaMemcpy(xd.p, x, static_cast<size_t>(d) * 8, cudaMemcpyHostToDevice));
+    auto* cnt = reinterpret_cast<int*>(md.p);
+    auto* m8 = reinterpret_cast<uint8_t*>(md.p) + 8;
+    OFF_CUDA(cudaMemset(cnt, 0, sizeof(int)));
+    predict_t_kernel<<<static_cast<int>((r + 127) / 128), 128>>>(Bd.p, xd.p, static_cast<int>(r), static_cast<int>(d),
+                                                                 td.p);
+    OFF_CUDA(cudaGetLastError());
+    predict_pre_kernel<<<static_cast<int>((D + 127) / 128), 128>>>(Ad.p, td.p, bd.p, static_cast<int>(D),
+                                                                   static_cast<int>(r), m8, cnt);
+    OFF_CUDA(cudaGetLastError());
+    int c = 0;
+    OFF_CUDA(cudaMemcpy(mask, m8, static_cast<size_t>(D), cudaMemcpyDeviceToHost));
+    OFF_CUDA(cudaMemcpy(&c, cnt, sizeof(int), cudaMemcpyDeviceToHost));
+    if (count) *count = c;
     return SG_OK;
 }
 
