@@ -214,9 +214,10 @@ sg_status sg_ffn_forward_batch(sg_ctx* ctx, const sg_layer* layer, const float* 
 sg_status sg_ffn_forward_batch_dense(sg_ctx* ctx, const sg_layer* layer, const float* xs,
                                      int32_t batch, float* ys, void* stream);
 /* Diagnostics of the tensor-core batch kernel: with max_units > 0, later batched calls
- * record per work unit 6 stamps (%globaltimer ns: claim, inputs ready, loads issued,
- * epilogue start / end; then the SM id); read_tc_trace copies the last call's
- * (min(max_units, its unit count)) records of 6 uint64 and the unit count. */
+ * record per work unit 8 values (%globaltimer ns: claim, inputs ready, loads issued,
+ * epilogue start / end; the SM id; two epilogue-internal stamps: partial written,
+ * group arrival counted); read_tc_trace copies the last call's
+ * (min(max_units, its unit count)) records of 8 uint64 and the unit count. */
 sg_status sg_ctx_enable_tc_trace(sg_ctx* ctx, int32_t max_units);
 sg_status sg_ctx_read_tc_trace(sg_ctx* ctx, void* stream, int32_t max_units, uint64_t* out,
                                int32_t* n_units);

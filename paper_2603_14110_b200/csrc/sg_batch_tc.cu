@@ -46,20 +46,22 @@
 namespace sg {
 namespace {
 
-constexpr int kProdThreads = 128;  // warps 0-3: producers (cp.async row gathers, TMA tiles)
-constexpr int kMmaWarp = 4;         // warp 4: MMA issuer; warps 5-8: epilogue
-constexpr int kEpiBase = 160;
-constexpr int kTcThreads = 288;
+// 8 warps = 2 per SM sub-partition, so a thread may hold up to 255 registers (a 9th
+// warp would put 3 on one sub-partition and cap them at 168)
+constexpr int kProdThreads = 96;   // warps 0-2: producers (cp.async row gathers, TMA tiles)
+constexpr int kMmaWarp = 3;         // warp 3: MMA issuer; warps 4-7: epilogue
+constexpr int kEpiBase = 128;
+constexpr int kTcThreads = 256;
 constexpr int kLag = 3;             // stages a producer thread keeps in flight before arriving
 constexpr int kStages = 4;
 constexpr int kStageA = 32768;  // 256 rows x 64 K bf16 (two M = 128 sub-tiles)
 constexpr int kStageB = 16384;  // <= 128 rows (N) x 64 K bf16
 constexpr int kStageBytes = kStageA + kStageB;
 constexpr int kUQ = 4;          // unit queue depth (producer lead)
-constexpr int kBlk = 256;       // neurons per block / rows per unit
-constexpr int kYRRows = 64;     // y rows per YR unit
+constexpr int kBlk = 128;       // neurons per block: one M = 128 tile of gate and of up rows
+constexpr int kTRows = 256;     // predictor rows of a T unit (rank <= 256: two M = 128 tiles)
 
-enum UnitType : int { U_STOP = 0, U_X, U_T, U_TR, U_PRE, U_GATE, U_UP, U_DOWN, U_YR };
+enum UnitType : int { U_STOP = 0, U_X, U_T, U_TR, U_PRE, U_GU, U_DOWN };
 
 struct Unit {
     int type;
@@ -68,7 +70,7 @@ struct Unit {
     int nsub;    // M = 128 sub-tiles carrying rows (1 or 2)
     int cnt;     // rows of the unit (gather units)
     int acc;     // TMEM accumulator buffer
-    int pad;     // gate / up: the block's rows are contiguous (dense comparator)
+    int pad;     // GU: the block's rows are contiguous (TMA tiles), not gathered
     int u;       // index in the claim order
 };
 
@@ -151,7 +153,16 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 }
 __device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-__device__ __forceinline__ void prod_bar() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
+__device__ __forceinline__ bool epi_bar_or(int v) {  // epi_bar + OR of v over the epilogue threads
+    uint32_t out;
+    asm volatile("{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\tbar.red.or.pred q, 1, 128, p;\n\t"
+                 "selp.u32 %0, 1, 0, q;\n}"
+                 : "=r"(out)
+                 : "r"(v)
+                 : "memory");
+    return out != 0;
+}
+__device__ __forceinline__ void prod_bar() { asm volatile("bar.sync 2, %0;" ::"n"(kProdThreads) : "memory"); }
 // 16-B global -> shared copy on the LSU path (row gathers: a TMA tile::gather4 moves
 // only 512 B per instruction, ~14 GB/s per SM on B200 — tools/bw_tma.cu)
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src, uint64_t pol) {
@@ -193,7 +204,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TC_TRACE(a, u, k, v)                                                         \
     do {                                                                             \
         if ((a).trace != nullptr && (u) >= 0 && (u) < (a).n_units)                   \
-            (a).trace[static_cast<size_t>(u) * 6 + (k)] = (v);                      \
+            (a).trace[static_cast<size_t>(u) * 8 + (k)] = (v);                      \
     } while (0)
 
 // Publish this thread's (or, after a CTA-level barrier, the CTA's) global writes —
@@ -243,6 +254,10 @@ __device__ __forceinline__ int range_lo(const TcArgs& a, int s) { return s * a.n
 __device__ __forceinline__ bool blk_tiled(const TcArgs& a, int cnt, int blk, int thr) {
     return a.dense || cnt * 1024 >= thr * blk_rows(a, blk);
 }
+// vcnt[blk] = survivor rows | kVTiled when DOWN streams the block whole (GU epilogue)
+constexpr int kVTiled = 1 << 16;
+__device__ __forceinline__ int vcnt_rows(int raw) { return raw & (kVTiled - 1); }
+__device__ __forceinline__ bool vcnt_tiled(int raw) { return (raw & kVTiled) != 0; }
 
 // flags layout (ints), zeroed by the last CTA of every launch
 __device__ __forceinline__ int* fl_work(const TcArgs& a) { return a.flags; }
@@ -252,11 +267,12 @@ __device__ __forceinline__ int* fl_t(const TcArgs& a) { return a.flags + 3; }
 __device__ __forceinline__ int* fl_tr(const TcArgs& a) { return a.flags + 4; }
 __device__ __forceinline__ int* fl_pre(const TcArgs& a, int b) { return a.flags + 32 + b; }
 __device__ __forceinline__ int* fl_gpart(const TcArgs& a, int b) { return a.flags + 32 + a.nblk + b; }
-__device__ __forceinline__ int* fl_gate(const TcArgs& a, int b) { return a.flags + 32 + 2 * a.nblk + b; }
-__device__ __forceinline__ int* fl_upart(const TcArgs& a, int b) { return a.flags + 32 + 3 * a.nblk + b; }
-__device__ __forceinline__ int* fl_up(const TcArgs& a, int b) { return a.flags + 32 + 4 * a.nblk + b; }
-__device__ __forceinline__ int* fl_down(const TcArgs& a, int t) { return a.flags + 32 + 5 * a.nblk + t; }
-__device__ __forceinline__ int flag_count(const TcArgs& a) { return 32 + 5 * a.nblk + a.ndt; }
+__device__ __forceinline__ int* fl_gu(const TcArgs& a, int b) { return a.flags + 32 + 2 * a.nblk + b; }
+__device__ __forceinline__ int* fl_down(const TcArgs& a, int t) { return a.flags + 32 + 3 * a.nblk + t; }
+__device__ __forceinline__ int flag_count(const TcArgs& a) { return 32 + 3 * a.nblk + a.ndt; }
+// GU units load without waiting for the block's mask: the dense comparator, and
+// batches wide enough that the union of the masks covers most rows anyway
+__device__ __forceinline__ bool gu_static(const TcArgs& a) { return a.dense || a.tile_all; }
 
 struct TcSmem {
     uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], uqf[kUQ], uqe[kUQ];
@@ -268,30 +284,27 @@ struct TcSmem {
     int flag[kBlk];      // epilogue: per-row flags / positions
     int cnt[64];         // epilogue: per-token counts
     int wsum[16];        // epilogue: per-(sub-tile, quarter) counts
+    int last;            // epilogue: this unit was the last of its group (it reduces)
+    alignas(16) uint16_t zst[2][8][kBlk];  // epilogue: Z hi / lo of 8 tokens x the block's slots
 };
 
 // ---- producer: claim, wait, load ---------------------------------------------
-// 128 threads (warps 0-3). Thread 0 is the controller: it claims units, checks and
+// 96 threads (warps 0-2). Thread 0 is the controller: it claims units, checks and
 // waits their inputs and publishes them. Contiguous rows (T, PRE, the dense
 // comparator) and the B operands come by TMA tiles from the controller; gathered
 // rows (the union / survivor rows of GATE, UP, DOWN) by 16-B cp.async from every
 // producer thread, written in the 128-B-swizzled UMMA layout. Each thread keeps kLag
 // stages of its copies in flight, then (wait_group, proxy fence) arrives on the
-// stage's full barrier (129 arrivals: 128 threads + the controller's expect_tx).
+// stage's full barrier (kProdThreads + 1 arrivals: the threads + the controller's expect_tx).
 // Before any blocking wait on another unit or on the epilogue every thread flushes
 // its pending arrivals, so no stage of an earlier unit is held back.
 __device__ __forceinline__ bool unit_inputs_ready(const TcArgs& a, int type, int i, int j) {
     switch (type) {
         case U_T: return flag_ready(fl_x(a), a.u_T);
         case U_PRE: return flag_ready(fl_tr(a), a.u_PRE - a.u_TR);
-        case U_GATE: return a.dense ? flag_ready(fl_x(a), a.u_T) : flag_ready(fl_pre(a, i), 1);
-        case U_UP: return flag_ready(fl_gate(a, i), 1);
-        case U_DOWN:
-            for (int blk = range_lo(a, j); blk < range_lo(a, j + 1); ++blk)
-                if (!flag_ready(fl_up(a, blk), 1)) return false;
-            return true;
+        case U_GU: return gu_static(a) ? flag_ready(fl_x(a), a.u_T) : flag_ready(fl_pre(a, i), 1);
+        case U_DOWN: return flag_ready(fl_gu(a, range_lo(a, j)), 1);  // later blocks: as they stream
         case U_TR: return flag_ready(fl_t(a), a.u_TR - a.u_T);
-        case U_YR: return flag_ready(fl_down(a, i / 4), a.S);
         default: return true;  // U_X
     }
 }
@@ -299,16 +312,12 @@ __device__ __forceinline__ void unit_inputs_wait(const TcArgs& a, int type, int 
     switch (type) {
         case U_T: wait_count(fl_x(a), a.u_T); break;
         case U_PRE: wait_count(fl_tr(a), a.u_PRE - a.u_TR); break;
-        case U_GATE:
-            if (a.dense) wait_count(fl_x(a), a.u_T);
+        case U_GU:
+            if (gu_static(a)) wait_count(fl_x(a), a.u_T);
             else wait_count(fl_pre(a, i), 1);
             break;
-        case U_UP: wait_count(fl_gate(a, i), 1); break;
         case U_TR: wait_count(fl_t(a), a.u_TR - a.u_T); break;
-        case U_YR: wait_count(fl_down(a, i / 4), a.S); break;
-        case U_DOWN:
-            for (int blk = range_lo(a, j); blk < range_lo(a, j + 1); ++blk) wait_count(fl_up(a, blk), 1);
-            break;
+        case U_DOWN: wait_count(fl_gu(a, range_lo(a, j)), 1); break;
         default: break;
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -375,32 +384,28 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
         } else if (type == U_PRE) {
             un.nst = a.pitch_r / 64;
             un.nsub = blk_rows(a, i) > 128 ? 2 : 1;
-        } else if (type == U_GATE || type == U_UP) {
-            wait_count(type == U_UP ? fl_gate(a, i) : (a.dense ? fl_x(a) : fl_pre(a, i)),
-                       type == U_GATE && a.dense ? a.u_T : 1);  // (set: orders the reads below)
-            const int listed = type == U_GATE ? (a.dense ? blk_rows(a, i) : __ldcg(a.ucnt + i)) : __ldcg(a.vcnt + i);
-            const bool tiled = listed > 0 && blk_tiled(a, listed, i, type == U_GATE ? a.tile_g : a.tile_u);
-            // tiled: the unit's rows are the block's rows; else the listed rows, gathered
-            const int cnt = tiled ? blk_rows(a, i) : listed;
-            if (!tiled) {
-                const int* list = type == U_GATE ? a.ulist + i * kBlk : a.vlist + i * kBlk;
-                for (int k = pt; k < cnt; k += kProdThreads) S.rows[k] = i * kBlk + __ldcg(list + k);
+        } else if (type == U_GU) {
+            // sub-tile 0 = gate rows, 1 = up rows (the same rows of both matrices)
+            bool tiled = true;
+            int cnt = blk_rows(a, i);
+            if (!gu_static(a)) {
+                wait_count(fl_pre(a, i), 1);  // (set: orders the list reads below)
+                const int listed = __ldcg(a.ucnt + i);
+                tiled = listed > 0 && blk_tiled(a, listed, i, a.tile_g);
+                if (!tiled) {
+                    cnt = listed;  // the block's union rows, gathered
+                    for (int k = pt; k < cnt; k += kProdThreads) S.rows[k] = i * kBlk + __ldcg(a.ulist + i * kBlk + k);
+                }
             }
             un.cnt = cnt;
-            un.nsub = cnt > 128 ? 2 : (cnt > 0 ? 1 : 0);
-            un.nst = cnt > 0 ? (type == U_GATE ? a.ksg : a.ksu) / 64 : 0;
+            un.nsub = cnt > 0 ? 2 : 0;
+            un.nst = cnt > 0 ? a.ksg / 64 : 0;
             un.pad = tiled;
         } else if (type == U_DOWN) {
-            int nst = 0;
-            for (int blk = range_lo(a, j); blk < range_lo(a, j + 1); ++blk) {
-                wait_count(fl_up(a, blk), 1);
-                const int v = __ldcg(a.vcnt + blk);
-                nst += (v > 0 && blk_tiled(a, v, blk, a.tile_u) ? blk_rows(a, blk) + 63 : v + 63) / 64;
-            }
-            un.nst = nst;
-            un.nsub = 2;
+            un.nst = 1;  // the stage count unfolds block by block (producer / MMA walk the range)
+            un.nsub = 1;
         }
-        const bool mma_unit = type == U_T || type == U_PRE || type == U_GATE || type == U_UP || type == U_DOWN;
+        const bool mma_unit = type == U_T || type == U_PRE || type == U_GU || type == U_DOWN;
         if (mma_unit) un.acc = accseq++ & 1;
         prod_bar();  // S.rows complete
         if (pt == 0) {
@@ -431,11 +436,12 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
             }
         };
         if (type == U_T || type == U_PRE || un.pad) {
-            // contiguous rows: TMA tiles (T: predictor B rows; PRE: A rows; dense: all rows)
-            const CUtensorMap* am = type == U_T ? &M.Bp : type == U_PRE ? &M.A : type == U_GATE ? &M.gate : &M.up;
+            // contiguous rows: TMA tiles (T: predictor B rows; PRE: A rows; GU: gate + up
+            // rows of the block). No thread copies: arrive at once, nothing held back.
+            flush();
+            const CUtensorMap* am = type == U_T ? &M.Bp : &M.A;
             const CUtensorMap* bm = type == U_PRE ? &M.thl : &M.xhl;
-            const int kw = type == U_GATE ? a.ksg : a.ksu;
-            const int k0 = type == U_T ? i * a.kst : type == U_PRE ? 0 : j * kw;
+            const int k0 = type == U_T ? i * a.kst : type == U_PRE ? 0 : j * a.ksg;
             const int r0 = type == U_T ? 0 : i * kBlk;
             for (int st = 0; st < un.nst; ++st) {
                 uint8_t* As;
@@ -444,16 +450,17 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                 begin_stage(As, as, bar);
                 if (pt == 0) {
                     mbar_expect_tx(bar, un.nsub * 16384u + bbytes);
-                    for (int t = 0; t < un.nsub; ++t) tma_tile(As + t * 16384, am, k0 + st * 64, r0 + t * 128, bar);
+                    for (int t = 0; t < un.nsub; ++t)
+                        tma_tile(As + t * 16384, type == U_GU ? (t ? &M.up : &M.gate) : am, k0 + st * 64,
+                                 type == U_GU ? r0 : r0 + t * 128, bar);
                     tma_tile(As + kStageA, bm, k0 + st * 64, 0, bar);
                 }
-                end_stage();
+                mbar_arrive(bar);
+                ++n;
             }
-        } else if (type == U_GATE || type == U_UP) {
-            const uint16_t* base = type == U_GATE ? a.gate : a.ud;
-            const size_t rstride = type == U_GATE ? static_cast<size_t>(a.pitch_d) : 2 * static_cast<size_t>(a.pitch_d);
-            const int kw = type == U_GATE ? a.ksg : a.ksu;
-            const int k0 = j * kw;
+        } else if (type == U_GU) {
+            // the block's union rows of gate (sub-tile 0) and up (sub-tile 1), gathered
+            const int k0 = j * a.ksg;
             const int jj = pt & 7;  // this thread's 16-B chunk of every row it copies
             for (int st = 0; st < un.nst; ++st) {
                 uint8_t* As;
@@ -467,35 +474,45 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                 }
 #pragma unroll 4
                 for (int r = pt >> 3; r < un.cnt; r += kProdThreads / 8) {
-                    const uint16_t* src = base + static_cast<size_t>(S.rows[r]) * rstride + kc + jj * 8;
-                    cp16(as + (r >> 3) * 1024 + (r & 7) * 128 + ((jj ^ (r & 7)) << 4), src, pol);
+                    const size_t row = static_cast<size_t>(S.rows[r]);
+                    const uint32_t dst = as + (r >> 3) * 1024 + (r & 7) * 128 + ((jj ^ (r & 7)) << 4);
+                    cp16(dst, a.gate + row * a.pitch_d + kc + jj * 8, pol);
+                    cp16(dst + 16384, a.ud + row * 2 * a.pitch_d + kc + jj * 8, pol);
                 }
                 end_stage();
             }
         } else {  // U_DOWN: K = survivor slots of the block range, A = down rows (MN-major)
-            const int m0 = i * 256;
+            const int m0 = i * 128;
             for (int blk = range_lo(a, j); blk < range_lo(a, j + 1); ++blk) {
+                // blocks become ready in order while the unit streams: a blocking wait
+                // first releases this thread's held-back stages
+                if (!flag_ready(fl_gu(a, blk), 1)) {
+                    flush();
+                    wait_count(fl_gu(a, blk), 1);
+                }
                 const int v = __ldcg(a.vcnt + blk);
-                if (v == 0) continue;
-                if (blk_tiled(a, v, blk, a.tile_u)) {
-                    // the block's down rows by TMA tiles: 64 k-rows x 4 atoms of 64 outputs;
-                    // Z holds zeros for the rows that are not survivors (UP epilogue)
+                if (vcnt_rows(v) == 0) continue;
+                if (vcnt_tiled(v)) {
+                    // the block's down rows by TMA tiles: 64 k-rows x 2 atoms of 64 outputs;
+                    // Z holds zeros for the rows that are not survivors (GU epilogue)
+                    flush();
                     for (int c0 = 0; c0 < blk_rows(a, blk); c0 += 64) {
                         uint8_t* As;
                         uint32_t as;
                         uint64_t* bar;
                         begin_stage(As, as, bar);
                         if (pt == 0) {
-                            mbar_expect_tx(bar, 4u * 8192u + bbytes);
-                            for (int atom = 0; atom < 4; ++atom)
+                            mbar_expect_tx(bar, 2u * 8192u + bbytes);
+                            for (int atom = 0; atom < 2; ++atom)
                                 tma_tile(As + atom * 8192, &M.down, m0 + atom * 64, blk * kBlk + c0, bar);
                             tma_tile(As + kStageA, &M.zhl, blk * kBlk + c0, 0, bar);
                         }
-                        end_stage();
+                        mbar_arrive(bar);
+                        ++n;
                     }
                     continue;
                 }
-                const int cnt = v;
+                const int cnt = vcnt_rows(v);
                 prod_bar();  // the previous block's rows are no longer read
                 for (int k = pt; k < cnt; k += kProdThreads)
                     S.rows[k] = blk * kBlk + __ldcg(a.vlist + blk * kBlk + k);
@@ -509,12 +526,12 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                         mbar_expect_tx(bar, bbytes);
                         tma_tile(As + kStageA, &M.zhl, blk * kBlk + c0, 0, bar);
                     }
-                    // 64 k-rows x 4 atoms of 64 outputs: 2048 chunks of 16 B, 16 per thread.
-                    // Slots past the block's survivors repeat its last row (finite data
-                    // against Z = 0: they add exact zeros).
+                    // 64 k-rows x 2 atoms of 64 outputs: 1024 chunks of 16 B. Slots past the
+                    // block's survivors repeat its last row (finite data against Z = 0: they
+                    // add exact zeros).
 #pragma unroll 4
-                    for (int q = pt; q < 2048; q += kProdThreads) {
-                        const int r = q >> 5, atom = (q >> 3) & 3, jj = q & 7;
+                    for (int q = pt; q < 1024; q += kProdThreads) {
+                        const int r = q >> 4, atom = (q >> 3) & 1, jj = q & 7;
                         const int row = S.rows[min(c0 + r, cnt - 1)];
                         const uint16_t* src = a.ud + static_cast<size_t>(row) * 2 * a.pitch_d + a.pitch_d + m0 +
                                               atom * 64 + jj * 8;
@@ -539,8 +556,7 @@ __device__ void mma_issuer(const TcArgs& a, TcSmem& S, uint8_t* stages) {
         mbar_wait(&S.uqf[slot], (seq / kUQ) & 1);
         const Unit un = S.uq[slot];
         ++seq;
-        const bool mma_unit = un.type == U_T || un.type == U_PRE || un.type == U_GATE ||
-                              un.type == U_UP || un.type == U_DOWN;
+        const bool mma_unit = un.type == U_T || un.type == U_PRE || un.type == U_GU || un.type == U_DOWN;
         if (mma_unit) {
             const int acc = un.acc;
             if (uses[acc] > 0) mbar_wait(&S.tempty[acc], (tphase >> acc) & 1u), tphase ^= 1u << acc;
@@ -551,20 +567,24 @@ __device__ void mma_issuer(const TcArgs& a, TcSmem& S, uint8_t* stages) {
             const uint32_t id = idesc(a.N, mn ? 1 : 0);
             // down: K steps of 16 survivor slots; the last stage of a block may be partial
             int dblk = mn ? range_lo(a, un.b) : 0, dleft = 0;
+            const int dend = mn ? range_lo(a, un.b + 1) : 0;
             bool dtiled = false;
-            for (int st = 0; st < un.nst; ++st) {
+            for (int st = 0;; ++st) {
                 int ksteps = 4;
                 if (mn) {
-                    while (dleft <= 0) {
-                        wait_count(fl_up(a, dblk), 1);  // (already set: orders the vcnt read)
+                    while (dleft <= 0 && dblk < dend) {
+                        wait_count(fl_gu(a, dblk), 1);  // orders the vcnt read
                         const int v = __ldcg(a.vcnt + dblk);
-                        dtiled = v > 0 && blk_tiled(a, v, dblk, a.tile_u);
-                        dleft = dtiled ? blk_rows(a, dblk) : v;
+                        dtiled = vcnt_tiled(v);
+                        dleft = dtiled ? blk_rows(a, dblk) : vcnt_rows(v);
                         ++dblk;
                     }
+                    if (dleft <= 0) break;
                     const int here = dleft < 64 ? dleft : 64;
                     ksteps = dtiled ? 4 : (here + 15) / 16;
                     dleft -= 64;
+                } else if (st >= un.nst) {
+                    break;
                 }
                 mbar_wait(&S.full[stage], (fphase >> stage) & 1u);
                 fphase ^= 1u << stage;
@@ -667,6 +687,160 @@ __device__ __forceinline__ void count_bits(TcSmem& S, uint64_t bits, int B, int 
     }
 }
 
+// Count this unit's (already CTA-synchronised) writes into a group of `total`; true
+// on every epilogue thread iff it was the last arrival, which then reads the others'
+// writes (release by their fence + add, acquire by this fence after the add).
+__device__ __forceinline__ bool arrive_last(int* p, int total, TcSmem& S, int et) {
+    if (et == 0) {
+        __threadfence();
+        const int last = atomicAdd(p, 1) == total - 1;
+        if (last) __threadfence();
+        S.last = last;
+    }
+    epi_bar();
+    return S.last != 0;
+}
+
+// g, u of this thread's row for every token: the KS slice partials summed in slice
+// order 0, 1, ..., KS-1 — this unit's own slice j straight from TMEM (sub-tiles 0 / 1),
+// the others from gpart — then z = gated(g, u) on the survivor bits (ffn_exec.hpp:200,
+// :68-76). GC chunks of 8 tokens per round of loads; partials held per slice index
+// (NS >= KS) so no register array is indexed at run time. With two slices the order is
+// moot (a + b == b + a exactly): NS = 1 holds just the other one.
+template <int GC, int NS>
+__device__ __forceinline__ void gu_reduce(const TcArgs& a, const TcSmem& S, int quarter, int acc, int j, int KS,
+                                          const float* rowpart, size_t sstride, bool mine, uint64_t mb,
+                                          float* z, uint64_t& sbits) {
+    const int nb = a.nb;
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 8 * GC) {
+        if (c0 >= nb) continue;  // warp-uniform
+        float4 q[NS][GC][4];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            const int sl = NS == 1 ? 1 - j : s;
+            if (sl >= KS || sl == j || !mine) continue;
+#pragma unroll
+            for (int gc = 0; gc < GC; ++gc) {
+                const int c = c0 + 8 * gc;
+                if (c >= nb) continue;
+                const float4* sg = reinterpret_cast<const float4*>(rowpart + sl * sstride + c);
+                const float4* su = reinterpret_cast<const float4*>(rowpart + sl * sstride + nb + c);
+                q[s][gc][0] = __ldcg(sg);
+                q[s][gc][1] = __ldcg(sg + 1);
+                q[s][gc][2] = __ldcg(su);
+                q[s][gc][3] = __ldcg(su + 1);
+            }
+        }
+#pragma unroll
+        for (int gc = 0; gc < GC; ++gc) {
+            const int c = c0 + 8 * gc;
+            if (c >= nb) continue;
+            float g[8], u[8];
+            acc8(a, S.tmem, quarter, acc, 0, c, g);
+            acc8(a, S.tmem, quarter, acc, 1, c, u);
+            if (!mine) continue;
+            if (NS == 1) {
+                if (KS == 2) {
+                    const float4 a0 = q[0][gc][0], a1 = q[0][gc][1], b0 = q[0][gc][2], b1 = q[0][gc][3];
+                    g[0] += a0.x; g[1] += a0.y; g[2] += a0.z; g[3] += a0.w;
+                    g[4] += a1.x; g[5] += a1.y; g[6] += a1.z; g[7] += a1.w;
+                    u[0] += b0.x; u[1] += b0.y; u[2] += b0.z; u[3] += b0.w;
+                    u[4] += b1.x; u[5] += b1.y; u[6] += b1.z; u[7] += b1.w;
+                }
+            } else {
+                float gs[8], us[8];
+#pragma unroll
+                for (int s = 0; s < NS; ++s) {  // slice order
+                    if (s >= KS) break;
+                    float gv[8], uv[8];
+                    if (s == j) {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) gv[e] = g[e], uv[e] = u[e];
+                    } else {
+                        const float4 a0 = q[s][gc][0], a1 = q[s][gc][1], b0 = q[s][gc][2], b1 = q[s][gc][3];
+                        gv[0] = a0.x; gv[1] = a0.y; gv[2] = a0.z; gv[3] = a0.w;
+                        gv[4] = a1.x; gv[5] = a1.y; gv[6] = a1.z; gv[7] = a1.w;
+                        uv[0] = b0.x; uv[1] = b0.y; uv[2] = b0.z; uv[3] = b0.w;
+                        uv[4] = b1.x; uv[5] = b1.y; uv[6] = b1.z; uv[7] = b1.w;
+                    }
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        gs[e] = s == 0 ? gv[e] : gs[e] + gv[e];
+                        us[e] = s == 0 ? uv[e] : us[e] + uv[e];
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) g[e] = gs[e], u[e] = us[e];
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const bool sv = ((mb >> (c + e)) & 1ull) && g[e] > 0.f;
+                if (sv) sbits |= 1ull << (c + e);
+                z[c + e] = sv ? gated(g[e], u[e], a.act) : 0.f;
+            }
+        }
+    }
+}
+
+// y rows of d tile i (this thread's row m): the S range partials in range order, this
+// unit's own range j from TMEM (zeros when it had no rows), the others from ypart.
+template <int GC, int NR>
+__device__ __forceinline__ void down_reduce(const TcArgs& a, const TcSmem& S, int quarter, int acc, int j,
+                                            bool have, int m) {
+    const int nb = a.nb, R = a.S;
+    const size_t rs = static_cast<size_t>(a.ndt) * 128 * nb;  // between ranges
+    const float* rowp = a.ypart + static_cast<size_t>(m) * nb;
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 8 * GC) {
+        if (c0 >= nb) continue;  // warp-uniform
+        float4 q[NR][GC][2];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            if (r >= R || r == j || m >= a.d) continue;
+#pragma unroll
+            for (int gc = 0; gc < GC; ++gc) {
+                const int c = c0 + 8 * gc;
+                if (c >= nb) continue;
+                const float4* src = reinterpret_cast<const float4*>(rowp + r * rs + c);
+                q[r][gc][0] = __ldcg(src);
+                q[r][gc][1] = __ldcg(src + 1);
+            }
+        }
+#pragma unroll
+        for (int gc = 0; gc < GC; ++gc) {
+            const int c = c0 + 8 * gc;
+            if (c >= nb) continue;
+            float own[8], y[8];
+            if (have) {
+                acc8(a, S.tmem, quarter, acc, 0, c, own);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) own[e] = 0.f;
+            }
+            if (m >= a.d) continue;
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {  // range order
+                if (r >= R) break;
+                float v[8];
+                if (r == j) {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) v[e] = own[e];
+                } else {
+                    const float4 a0 = q[r][gc][0], a1 = q[r][gc][1];
+                    v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w;
+                    v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) y[e] = r == 0 ? v[e] : y[e] + v[e];
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (c + e < a.B) a.y[static_cast<size_t>(c + e) * a.d + m] = y[e];
+        }
+    }
+}
+
 // ---- epilogue -----------------------------------------------------------------
 __device__ void epilogue(const TcArgs& a, TcSmem& S) {
     const int et = threadIdx.x - kEpiBase;     // 0..127
@@ -683,11 +857,10 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
         ++seq;
         if (un.type == U_STOP) break;
         const int i = un.a, j = un.b;
-        const bool mma_unit = un.type == U_T || un.type == U_PRE || un.type == U_GATE ||
-                              un.type == U_UP || un.type == U_DOWN;
+        const bool mma_unit = un.type == U_T || un.type == U_PRE || un.type == U_GU || un.type == U_DOWN;
         bool have = false;
         if (mma_unit) {
-            have = un.nst > 0;
+            have = un.nst > 0;  // DOWN: recomputed below from the range's survivor counts
             mbar_wait(&S.tfull[un.acc], (tphase >> un.acc) & 1u);
             tphase ^= 1u << un.acc;
             tc_fence_after();
@@ -704,32 +877,42 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
             const int w0 = i * per, w1 = min(items, w0 + per);
             bool bad = false;
             const bool vec = (a.d & 7) == 0;
-            for (int w = w0 + et; w < w1; w += 128) {
-                const int b = w / nch, ch = w % nch, k0 = ch * 8;
-                float v[8];
-                if (b < a.B && vec && k0 < a.d) {
-                    const float4 f0 = __ldg(reinterpret_cast<const float4*>(a.x + static_cast<size_t>(b) * a.d + k0));
-                    const float4 f1 = __ldg(reinterpret_cast<const float4*>(a.x + static_cast<size_t>(b) * a.d + k0) + 1);
-                    v[0] = f0.x; v[1] = f0.y; v[2] = f0.z; v[3] = f0.w;
-                    v[4] = f1.x; v[5] = f1.y; v[6] = f1.z; v[7] = f1.w;
-                } else {
+            for (int wb = w0 + et; wb < w1; wb += 4 * 128) {  // 4 items per thread: loads first
+                float v[4][8];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        v[e] = (b < a.B && k0 + e < a.d) ? __ldg(a.x + static_cast<size_t>(b) * a.d + k0 + e) : 0.f;
-                }
-                uint16_t hi[8], lo[8];
+                for (int h = 0; h < 4; ++h) {
+                    const int w = wb + h * 128;
+                    const int b = w / nch, k0 = (w % nch) * 8;
+                    if (w < w1 && b < a.B && vec && k0 < a.d) {
+                        const float4* src = reinterpret_cast<const float4*>(a.x + static_cast<size_t>(b) * a.d + k0);
+                        const float4 f0 = __ldg(src), f1 = __ldg(src + 1);
+                        v[h][0] = f0.x; v[h][1] = f0.y; v[h][2] = f0.z; v[h][3] = f0.w;
+                        v[h][4] = f1.x; v[h][5] = f1.y; v[h][6] = f1.z; v[h][7] = f1.w;
+                    } else {
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    bad |= !isfinite(v[e]);
-                    split_bf16(v[e], hi[e], lo[e]);
+                        for (int e = 0; e < 8; ++e)
+                            v[h][e] = (w < w1 && b < a.B && k0 + e < a.d) ? __ldg(a.x + static_cast<size_t>(b) * a.d + k0 + e) : 0.f;
+                    }
                 }
-                uint4 vh, vl;
-                vh.x = hi[0] | (uint32_t(hi[1]) << 16); vh.y = hi[2] | (uint32_t(hi[3]) << 16);
-                vh.z = hi[4] | (uint32_t(hi[5]) << 16); vh.w = hi[6] | (uint32_t(hi[7]) << 16);
-                vl.x = lo[0] | (uint32_t(lo[1]) << 16); vl.y = lo[2] | (uint32_t(lo[3]) << 16);
-                vl.z = lo[4] | (uint32_t(lo[5]) << 16); vl.w = lo[6] | (uint32_t(lo[7]) << 16);
-                *reinterpret_cast<uint4*>(a.xhl + static_cast<size_t>(b) * a.xpitch + k0) = vh;
-                *reinterpret_cast<uint4*>(a.xhl + static_cast<size_t>(nb + b) * a.xpitch + k0) = vl;
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int w = wb + h * 128;
+                    if (w >= w1) break;
+                    const int b = w / nch, k0 = (w % nch) * 8;
+                    uint16_t hi[8], lo[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        bad |= !isfinite(v[h][e]);
+                        split_bf16(v[h][e], hi[e], lo[e]);
+                    }
+                    uint4 vh, vl;
+                    vh.x = hi[0] | (uint32_t(hi[1]) << 16); vh.y = hi[2] | (uint32_t(hi[3]) << 16);
+                    vh.z = hi[4] | (uint32_t(hi[5]) << 16); vh.w = hi[6] | (uint32_t(hi[7]) << 16);
+                    vl.x = lo[0] | (uint32_t(lo[1]) << 16); vl.y = lo[2] | (uint32_t(lo[3]) << 16);
+                    vl.z = lo[4] | (uint32_t(lo[5]) << 16); vl.w = lo[6] | (uint32_t(lo[7]) << 16);
+                    *reinterpret_cast<uint4*>(a.xhl + static_cast<size_t>(b) * a.xpitch + k0) = vh;
+                    *reinterpret_cast<uint4*>(a.xhl + static_cast<size_t>(nb + b) * a.xpitch + k0) = vl;
+                }
             }
             if (bad) atomicOr(a.bad, 1);  // check_input, ffn_exec.hpp:61-63
             asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -742,7 +925,7 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                 for (int c = 0; c < nb; c += 16) {
                     float v[16];
                     acc16(a, S.tmem, quarter, acc, t, c, v);
-                    st16(a.tpart + (static_cast<size_t>(i) * kBlk + row) * nb + c, v, min(16, nb - c));
+                    st16(a.tpart + (static_cast<size_t>(i) * kTRows + row) * nb + c, v, min(16, nb - c));
                 }
             }
             tc_fence_before();
@@ -763,7 +946,7 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                     float p[16];
 #pragma unroll
                     for (int k = 0; k < 16; ++k)
-                        p[k] = k0 + k < KT ? __ldcg(src + static_cast<size_t>(k0 + k) * kBlk * nb) : 0.f;
+                        p[k] = k0 + k < KT ? __ldcg(src + static_cast<size_t>(k0 + k) * kTRows * nb) : 0.f;
 #pragma unroll
                     for (int k = 0; k < 16; ++k)
                         if (k0 + k < KT) s += p[k];
@@ -781,10 +964,10 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
             const int rows = blk_rows(a, i);
             if (et < 64) S.cnt[et] = 0;
             epi_bar();
-            for (int t = 0; t < 2; ++t) {
-                const int k = t * 128 + row0;
+            {
+                const int k = row0, t = 0;
                 uint64_t bits = 0;
-                if (t < un.nsub) {  // warp-uniform: tcgen05.ld is warp-collective
+                {
                     const bool mine = k < rows;
                     const float bias = mine ? __ldg(a.bias + i * kBlk + k) : 0.f;
                     for (int c = 0; c < nb; c += 16) {
@@ -813,186 +996,151 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                 signal(fl_pre(a, i));
             }
             epi_bar();
-        } else if (un.type == U_GATE || un.type == U_UP) {
-            const bool gate = un.type == U_GATE;
-            const int KS = gate ? a.KSg : a.KSu;
-            const int cnt = un.cnt;
-            float* part = gate ? a.gpart : a.upart;
-            if (j > 0) {
-                // partial over K slice j -> part[j-1][blk][row][b]
-                for (int t = 0; t < un.nsub; ++t) {  // warp-uniform (have == nsub > 0)
-                    const int k = t * 128 + row0;
-                    float* dst = part + ((static_cast<size_t>(j - 1) * a.nblk + i) * kBlk + k) * nb;
-                    for (int c = 0; c < nb; c += 16) {
-                        float v[16];
-                        acc16(a, S.tmem, quarter, acc, t, c, v);
-                        if (k < cnt) st16(dst + c, v, min(16, nb - c));
-                    }
-                }
-                tc_fence_before();
+        } else if (un.type == U_GU) {
+            // block i (128 neurons), K slice j: g (sub-tile 0) and u (sub-tile 1) partials;
+            // the last slice of the block to finish reduces them (no unit ever waits for
+            // another's epilogue)
+            const int KS = a.KSg, cnt = un.cnt, k = row0;
+            const size_t pw = 2 * static_cast<size_t>(nb);  // floats per partial row: g | u
+            const size_t sstride = static_cast<size_t>(a.nblk) * kBlk * pw;  // between slices
+            const float* rowpart = a.gpart + (static_cast<size_t>(i) * kBlk + k) * pw;
+            bool fin = true;
+            if (KS > 1) {
+                float* dst = a.gpart + static_cast<size_t>(j) * sstride + (static_cast<size_t>(i) * kBlk + k) * pw;
+                if (un.nsub > 0)  // warp-uniform
+                    for (int t = 0; t < 2; ++t)
+                        for (int c = 0; c < nb; c += 16) {
+                            float v[16];
+                            acc16(a, S.tmem, quarter, acc, t, c, v);
+                            if (k < cnt) st16(dst + t * nb + c, v, min(16, nb - c));
+                        }
                 epi_bar();
-                if (et == 0) {
-                    mbar_arrive(&S.tempty[acc]);
-                    signal(gate ? fl_gpart(a, i) : fl_upart(a, i));
-                }
-            } else {
-                if (et == 0) wait_count(gate ? fl_gpart(a, i) : fl_upart(a, i), KS - 1);
-                // inputs written by earlier units: the block's lists, mask / survivor bits, g
-                if (gate && !a.dense) wait_count(fl_pre(a, i), 1);
-                if (!gate) wait_count(fl_gate(a, i), 1);
-                if (et < 64) S.cnt[et] = 0;
-                epi_bar();
-                // tiled unit: position k IS local row k (and Z slot k), else the k-th listed row
-                const int* list = un.pad ? nullptr : gate ? a.ulist + i * kBlk : a.vlist + i * kBlk;
-                for (int t = 0; t < 2; ++t) {
-                    const int k = t * 128 + row0;
-                    const bool mine = have && k < cnt;
-                    const int n = mine ? i * kBlk + (list ? __ldcg(list + k) : k) : 0;
-                    const uint64_t mb = gate ? (a.dense ? bmask : (mine ? __ldcg(a.mbits + n) : 0ull))
-                                             : (a.dense ? bmask : (mine ? __ldcg(a.vbits + n) : 0ull));
-                    uint64_t sbits = 0;
-                    for (int c = 0; c < nb && t < un.nsub; c += 8) {  // warp-uniform bound
-                        // every global load of the chunk first, then the TMEM loads
-                        float4 pp[3][2], gv[2];
-                        const int np = KS - 1 < 3 ? KS - 1 : 3;
-#pragma unroll
-                        for (int s = 0; s < 3; ++s)
-                            if (s < np && mine) {
-                                const float4* src = reinterpret_cast<const float4*>(
-                                    part + ((static_cast<size_t>(s) * a.nblk + i) * kBlk + k) * nb + c);
-                                pp[s][0] = __ldcg(src);
-                                pp[s][1] = __ldcg(src + 1);
-                            }
-                        if (!gate && mine) {
-                            const float4* src = reinterpret_cast<const float4*>(a.G + static_cast<size_t>(n) * nb + c);
-                            gv[0] = __ldcg(src);
-                            gv[1] = __ldcg(src + 1);
-                        }
-                        float v[8];
-                        acc8(a, S.tmem, quarter, acc, t, c, v);
-                        if (!mine) continue;
-#pragma unroll
-                        for (int s = 0; s < 3; ++s)  // fixed order: own slice, then 1, 2, ...
-                            if (s < np) {
-                                v[0] += pp[s][0].x; v[1] += pp[s][0].y; v[2] += pp[s][0].z; v[3] += pp[s][0].w;
-                                v[4] += pp[s][1].x; v[5] += pp[s][1].y; v[6] += pp[s][1].z; v[7] += pp[s][1].w;
-                            }
-                        for (int s = 4; s < KS; ++s) {
-                            const float4* src = reinterpret_cast<const float4*>(
-                                part + ((static_cast<size_t>(s - 1) * a.nblk + i) * kBlk + k) * nb + c);
-                            const float4 q0 = __ldcg(src), q1 = __ldcg(src + 1);
-                            v[0] += q0.x; v[1] += q0.y; v[2] += q0.z; v[3] += q0.w;
-                            v[4] += q1.x; v[5] += q1.y; v[6] += q1.z; v[7] += q1.w;
-                        }
-                        if (gate) {
-                            // g per token; survivor iff predicted and g > 0 (ffn_exec.hpp:200)
-                            st16(a.G + static_cast<size_t>(n) * nb + c, v, 8);
-#pragma unroll
-                            for (int e = 0; e < 8; ++e)
-                                if (v[e] > 0.f) sbits |= 1ull << (c + e);
-                        } else {
-                            // z = gated(g, u) on the token's survivor bit, else +0 -> Z^T hi / lo
-                            const float g8[8] = {gv[0].x, gv[0].y, gv[0].z, gv[0].w, gv[1].x, gv[1].y, gv[1].z, gv[1].w};
-#pragma unroll
-                            for (int e = 0; e < 8; ++e) {
-                                const int b = c + e;
-                                const float z = ((mb >> b) & 1ull) ? gated(g8[e], v[e], a.act) : 0.f;
-                                uint16_t hi, lo;
-                                split_bf16(z, hi, lo);
-                                a.zhl[static_cast<size_t>(b) * a.zpitch + i * kBlk + k] = hi;
-                                a.zhl[static_cast<size_t>(nb + b) * a.zpitch + i * kBlk + k] = lo;
-                            }
-                        }
-                    }
-                    if (gate) {
-                        sbits &= mb & bmask;
-                        if (mine) a.vbits[n] = sbits;
-                        // dense: every row is read for up / down; the bits mask z
-                        S.flag[k] = a.dense ? mine : (sbits != 0);
-                        count_bits(S, sbits, a.B, lane);
-                    } else if (!mine && k < ((cnt + 63) / 64) * 64) {
-                        // padding slots of the block's last 64-slot stage: exact zeros
-                        for (int b = 0; b < 2 * nb; ++b) a.zhl[static_cast<size_t>(b) * a.zpitch + i * kBlk + k] = 0;
-                    }
-                }
+                if (et == 0) TC_TRACE(a, un.u, 6, gtimer());
+                fin = arrive_last(fl_gpart(a, i), KS, S, et);
+            }
+            if (et == 0) TC_TRACE(a, un.u, 7, gtimer());
+            if (!fin) {
                 tc_fence_before();
                 epi_bar();
                 if (et == 0) mbar_arrive(&S.tempty[acc]);
-                if (gate) {
-                    // survivor list of the block (union positions -> local rows)
-                    int* vl = a.vlist + i * kBlk;
-                    const int nv = epi_compact(S, cnt, et, vl);
-                    for (int k = et; k < nv; k += 128) {
-                        const int pos = vl[k];
-                        vl[k] = list ? __ldcg(list + pos) : pos;
-                    }
-                    if (et < a.B && S.cnt[et]) atomicAdd(a.vcount + et, S.cnt[et]);
-                    epi_bar();
-                    if (et == 0) {
-                        a.vcnt[i] = nv;
-                        signal(fl_gate(a, i));
-                    }
-                } else {
-                    asm volatile("fence.proxy.async.global;" ::: "memory");
-                    epi_bar();
-                    if (et == 0) signal(fl_up(a, i));
-                }
+            } else {
+                // survivors V_b = P_b & g > 0; z = gated(g, u) on V_b, else +0
+                if (!a.dense) wait_count(fl_pre(a, i), 1);  // mask bits (set long before, as a rule)
+                if (et < 64) S.cnt[et] = 0;
                 epi_bar();
+                const bool mine = un.nsub > 0 && k < cnt;
+                const int lrow = un.pad ? k : (mine ? __ldcg(a.ulist + i * kBlk + k) : 0);  // row in block
+                const int n = i * kBlk + lrow;
+                const uint64_t mb = a.dense ? bmask : (mine ? __ldcg(a.mbits + n) : 0ull);
+                float z[64];
+#pragma unroll
+                for (int e = 0; e < 64; ++e) z[e] = 0.f;
+                uint64_t sbits = 0;
+#ifdef SG_TC_FINTRACE
+                if (et == 0) TC_TRACE(a, un.u, 5, gtimer());
+#endif
+                if (un.nsub > 0) gu_reduce<4, 1>(a, S, quarter, acc, j, KS, rowpart, sstride, mine, mb, z, sbits);
+#ifdef SG_TC_FINTRACE
+                epi_bar();
+                if (et == 0) TC_TRACE(a, un.u, 6, gtimer());
+#endif
+                tc_fence_before();
+                sbits &= bmask;
+                if (mine) a.vbits[n] = sbits;
+                count_bits(S, sbits, a.B, lane);
+                // survivor slots: ascending rows (positions k ascend with the local row)
+                const bool keep = sbits != 0;
+                const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                if (lane == 0) S.wsum[quarter] = __popc(bal);
+                epi_bar();
+                if (et == 0) mbar_arrive(&S.tempty[acc]);
+                int before = 0;
+                for (int q = 0; q < quarter; ++q) before += S.wsum[q];
+                const int nv = S.wsum[0] + S.wsum[1] + S.wsum[2] + S.wsum[3];
+                const int slot_c = before + __popc(bal & ((1u << lane) - 1u));
+                // DOWN streams a tiled GU block whole (Z slot = row) when its survivors are
+                // dense enough, else gathers the survivor rows (Z slot = survivor position);
+                // the slots up to the next 64 are exact zeros either way
+                const bool dtile = un.pad && nv > 0 && blk_tiled(a, nv, i, a.tile_u);
+                const int pad_to = dtile ? (blk_rows(a, i) + 63) / 64 * 64 : (nv + 63) / 64 * 64;
+                // this thread's slots: its z (if any) and an exact-zero padding slot (if any)
+                int zslot = -1, pslot = -1;
+                if (dtile) {
+                    if (mine) zslot = lrow;
+                    else if (k < pad_to) pslot = k;
+                } else {
+                    if (keep) {
+                        zslot = slot_c;
+                        a.vlist[i * kBlk + slot_c] = lrow;
+                    }
+                    if (k >= nv && k < pad_to) pslot = k;
+                }
+                // Z^T rows are K-major (slots contiguous per token): stage 8 tokens at a time
+                // in smem, then store whole 16-B runs of 8 slots
+                const int chunks = pad_to / 8;
+#pragma unroll
+                for (int c = 0; c < 64; c += 8) {
+                    if (c >= nb) continue;  // uniform
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        uint16_t hi, lo;
+                        split_bf16(z[c + e], hi, lo);
+                        if (zslot >= 0) S.zst[0][e][zslot] = hi, S.zst[1][e][zslot] = lo;
+                        if (pslot >= 0) S.zst[0][e][pslot] = 0, S.zst[1][e][pslot] = 0;
+                    }
+                    epi_bar();
+                    for (int w = et; w < 16 * chunks; w += 128) {
+                        const int row = w / chunks, ch = w % chunks, hl = row >> 3, e = row & 7;
+                        const uint4 v = *reinterpret_cast<const uint4*>(&S.zst[hl][e][ch * 8]);
+                        *reinterpret_cast<uint4*>(a.zhl + static_cast<size_t>(hl * nb + c + e) * a.zpitch +
+                                                  static_cast<size_t>(i) * kBlk + ch * 8) = v;
+                    }
+                    epi_bar();
+                }
+                if (et < a.B && S.cnt[et]) atomicAdd(a.vcount + et, S.cnt[et]);
+#ifdef SG_TC_FINTRACE
+                epi_bar();
+                if (et == 0) TC_TRACE(a, un.u, 7, gtimer());
+#endif
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // Z is read by TMA
+                epi_bar();
+                if (et == 0) {
+                    a.vcnt[i] = nv | (dtile ? kVTiled : 0);
+                    signal(fl_gu(a, i));
+                }
             }
         } else if (un.type == U_DOWN) {
-            // partial y over block range j for d tile i: ypart[j][m][b]
-            for (int t = 0; t < 2; ++t) {
-                const int m = i * 256 + t * 128 + row0;
-                float* dst = a.ypart + (static_cast<size_t>(j) * a.ndt * 256 + m) * nb;
+            // partial y over block range j for d tile i (128 outputs): ypart[j][m][b]; the
+            // last range of the d tile to finish sums the S partials in range order into y
+            const int m = i * 128 + row0;
+            {  // did the range hold any survivor row (else the accumulator was never written)
+                int hv = 0;
+                for (int blk = range_lo(a, j) + et; blk < range_lo(a, j + 1); blk += 128)
+                    hv |= vcnt_rows(__ldcg(a.vcnt + blk)) > 0;
+                have = epi_bar_or(hv);
+            }
+            bool fin = true;
+            if (a.S > 1) {
+                float* dst = a.ypart + (static_cast<size_t>(j) * a.ndt * 128 + m) * nb;
                 for (int c = 0; c < nb; c += 16) {
                     float v[16];
                     if (have) {
-                        acc16(a, S.tmem, quarter, acc, t, c, v);
+                        acc16(a, S.tmem, quarter, acc, 0, c, v);
                     } else {
 #pragma unroll
                         for (int e = 0; e < 16; ++e) v[e] = 0.f;
                     }
                     st16(dst + c, v, min(16, nb - c));
                 }
+                epi_bar();
+                if (et == 0) TC_TRACE(a, un.u, 6, gtimer());
+                fin = arrive_last(fl_down(a, i), a.S, S, et);
             }
+            if (et == 0) TC_TRACE(a, un.u, 7, gtimer());
+            if (fin) down_reduce<2, 4>(a, S, quarter, acc, j, have, m);
             tc_fence_before();
             epi_bar();
-            if (et == 0) {
-                mbar_arrive(&S.tempty[acc]);
-                signal(fl_down(a, i));
-            }
-        } else if (un.type == U_YR) {
-            // y rows [dt*256 + 64q, +64) x tokens in groups of 8: fixed-order sum of the S
-            // block-range partials, all loads first
-            const int dt = i / 4, q = i % 4;
-            wait_count(fl_down(a, dt), a.S);
-            const int groups = nb / 8;
-            for (int w = et; w < kYRRows * groups; w += 128) {
-                const int m = dt * 256 + q * kYRRows + w % kYRRows, c = (w / kYRRows) * 8;
-                if (m >= a.d) continue;
-                float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                for (int r0 = 0; r0 < a.S; r0 += 8) {  // fixed order: ranges 0, 1, ..., S-1
-                    float4 p[8][2];
-#pragma unroll
-                    for (int r = 0; r < 8; ++r)
-                        if (r0 + r < a.S) {
-                            const float4* src = reinterpret_cast<const float4*>(
-                                a.ypart + (static_cast<size_t>(r0 + r) * a.ndt * 256 + m) * nb + c);
-                            p[r][0] = __ldcg(src);
-                            p[r][1] = __ldcg(src + 1);
-                        }
-#pragma unroll
-                    for (int r = 0; r < 8; ++r)
-                        if (r0 + r < a.S) {
-                            s[0] += p[r][0].x; s[1] += p[r][0].y; s[2] += p[r][0].z; s[3] += p[r][0].w;
-                            s[4] += p[r][1].x; s[5] += p[r][1].y; s[6] += p[r][1].z; s[7] += p[r][1].w;
-                        }
-                }
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    if (c + e < a.B) a.y[static_cast<size_t>(c + e) * a.d + m] = s[e];
-            }
-            epi_bar();
+            if (et == 0) mbar_arrive(&S.tempty[acc]);
         }
         if (et == 0) {
             TC_TRACE(a, un.u, 4, gtimer());
@@ -1008,7 +1156,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     const int warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&S.full[s], kProdThreads + 1);  // 128 producer threads + the expect_tx
+            mbar_init(&S.full[s], kProdThreads + 1);  // the producer threads + the expect_tx
             mbar_init(&S.empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
@@ -1057,7 +1205,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
 }  // namespace
 
 int tc_smem_bytes() { return kStages * kStageBytes + static_cast<int>(sizeof(TcSmem)) + 1024; }
-int tc_flag_ints(int nblk, int ndt) { return 32 + 5 * nblk + ndt; }
+int tc_flag_ints(int nblk, int ndt) { return 32 + 3 * nblk + ndt; }
 
 int launch_batch_tc(const TcMaps& maps, const TcArgs& a, int grid, void* stream) {
     const int smem = tc_smem_bytes();

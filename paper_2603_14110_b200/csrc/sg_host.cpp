@@ -848,13 +848,14 @@ int env_int(const char* name, int dflt) {
     return e ? std::atoi(e) : dflt;
 }
 
-constexpr int kTcKSMax = 8;   // K slices of the gate / up units (partial buffers sized for it)
-constexpr int kTcSMax = 16;   // block ranges of the down units
+constexpr int kTcKSMax = 2;   // K slices of the gate-up units (the finisher's register budget)
+constexpr int kTcBlk = 128;   // neurons per block of the tensor-core kernel
+constexpr int kTcSMax = 4;    // block ranges of the down units (the y finisher's register budget)
 
 sg_status tc_workspace(sg_ctx* C) {
     if (C->tmem_ws) return SG_OK;
     const size_t Dm = static_cast<size_t>(C->max_D), pd = static_cast<size_t>(C->pitch_dmax);
-    const size_t nblk = (Dm + 255) / 256, ndt = (pd + 255) / 256;
+    const size_t nblk = (Dm + kTcBlk - 1) / kTcBlk, ndt = (pd + 127) / 128;
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const size_t o = off;
@@ -863,10 +864,9 @@ sg_status tc_workspace(sg_ctx* C) {
     };
     const size_t o_x = take(128 * pd * 2), o_tp = take(((pd + 255) / 256) * 256 * 64 * 4),
                  o_th = take(128 * 256 * 2), o_mb = take(Dm * 8), o_vb = take(Dm * 8),
-                 o_ul = take(nblk * 256 * 4), o_uc = take(nblk * 4), o_vl = take(nblk * 256 * 4),
-                 o_vc = take(nblk * 4), o_gp = take((kTcKSMax - 1) * nblk * 256 * 64 * 4),
-                 o_up = take((kTcKSMax - 1) * nblk * 256 * 64 * 4), o_G = take(Dm * 64 * 4),
-                 o_z = take(128 * nblk * 256 * 2), o_y = take(kTcSMax * ndt * 256 * 64 * 4),
+                 o_ul = take(nblk * kTcBlk * 4), o_uc = take(nblk * 4), o_vl = take(nblk * kTcBlk * 4),
+                 o_vc = take(nblk * 4), o_gp = take(kTcKSMax * nblk * kTcBlk * 2 * 64 * 4),
+                 o_z = take(128 * nblk * kTcBlk * 2), o_y = take(kTcSMax * ndt * 128 * 64 * 4),
                  o_cnt = take((64 + 64 + 1) * 4),
                  o_fl = take(static_cast<size_t>(sg::tc_flag_ints(static_cast<int>(nblk), static_cast<int>(ndt))) * 4);
     DeviceGuard dg(C->device);
@@ -888,15 +888,13 @@ sg_status tc_workspace(sg_ctx* C) {
     a.vlist = reinterpret_cast<int*>(b + o_vl);
     a.vcnt = reinterpret_cast<int*>(b + o_vc);
     a.gpart = reinterpret_cast<float*>(b + o_gp);
-    a.upart = reinterpret_cast<float*>(b + o_up);
-    a.G = reinterpret_cast<float*>(b + o_G);
     a.zhl = reinterpret_cast<uint16_t*>(b + o_z);
     a.ypart = reinterpret_cast<float*>(b + o_y);
     a.pcount = reinterpret_cast<int*>(b + o_cnt);
     a.vcount = a.pcount + 64;
     a.bad = a.pcount + 128;
     a.flags = reinterpret_cast<int*>(b + o_fl);
-    a.zpitch = static_cast<int>(nblk * 256);
+    a.zpitch = static_cast<int>(nblk * kTcBlk);
     a.xpitch = static_cast<int>(pd);
     return SG_OK;
 }
@@ -916,7 +914,7 @@ int k_slices(int pitch, int want) {
 // so no stage waits for a whole previous stage. Topological by construction.
 std::vector<int> tc_schedule(const sg::TcArgs& a, int NX, int KT, int NTR, int lag) {
     auto code = [](int t, int i, int j) { return (t << 24) | (i << 8) | j; };
-    enum { X = 1, T, TR, PRE, GATE, UP, DOWN, YR };
+    enum { X = 1, T, TR, PRE, GU, DOWN };  // sg_batch_tc.cu UnitType
     std::vector<int> order;
     for (int k = 0; k < NX; ++k) order.push_back(code(X, k, 0));
     for (int k = 0; k < KT; ++k) order.push_back(code(T, k, 0));
@@ -926,53 +924,36 @@ std::vector<int> tc_schedule(const sg::TcArgs& a, int NX, int KT, int NTR, int l
     struct Item {
         int code, ready_at;
     };
-    std::vector<Item> ups, downs, yrs;
-    std::vector<int> up_done_at(static_cast<size_t>(a.nblk), -1), down_cnt(static_cast<size_t>(a.ndt), 0);
-    std::vector<int> down_last(static_cast<size_t>(a.ndt), 0);
+    std::vector<Item> downs;
+    std::vector<int> gu_done_at(static_cast<size_t>(a.nblk), -1);
     auto range_lo = [&](int sr) { return sr * a.nblk / a.S; };
-    size_t gi = 0;
-    std::vector<int> gates;
+    std::vector<int> gus;
     for (int b = 0; b < a.nblk; ++b)
-        for (int ks = a.KSg - 1; ks >= 0; --ks) gates.push_back(code(GATE, b, ks));
-    size_t ui = 0, di = 0, yi = 0;
+        for (int ks = a.KSg - 1; ks >= 0; --ks) gus.push_back(code(GU, b, ks));
+    size_t gi = 0, di = 0;
     auto emit = [&](int c) {
         order.push_back(c);
         const int pos = static_cast<int>(order.size());
-        const int t = c >> 24, i = (c >> 8) & 0xffff, j = c & 0xff;
-        if (t == GATE && j == 0)  // the block's owner: its UP units may follow `lag` later
-            for (int ks = a.KSu - 1; ks >= 0; --ks) ups.push_back({code(UP, i, ks), pos + lag});
-        if (t == UP && j == 0) {
-            up_done_at[static_cast<size_t>(i)] = pos;
+        const int t = c >> 24, i = (c >> 8) & 0xffff;
+        if (t == GU && (c & 0xff) == 0) {  // the block's owner
+            gu_done_at[static_cast<size_t>(i)] = pos;
             for (int sr = 0; sr < a.S; ++sr) {
                 if (i != range_lo(sr + 1) - 1) continue;  // the range's last block
                 int ready = 0;
                 for (int b = range_lo(sr); b < range_lo(sr + 1); ++b)
-                    ready = std::max(ready, up_done_at[static_cast<size_t>(b)]);
+                    ready = std::max(ready, gu_done_at[static_cast<size_t>(b)]);
                 for (int dt = 0; dt < a.ndt; ++dt) downs.push_back({code(DOWN, dt, sr), ready + lag});
             }
-        }
-        if (t == DOWN) {
-            down_last[static_cast<size_t>(i)] = pos;
-            if (++down_cnt[static_cast<size_t>(i)] == a.S)
-                for (int q = 0; q < 4; ++q) yrs.push_back({code(YR, i * 4 + q, 0), pos + lag});
         }
     };
     for (;;) {
         const int pos = static_cast<int>(order.size());
-        if (yi < yrs.size() && yrs[yi].ready_at <= pos) {
-            emit(yrs[yi++].code);
-        } else if (di < downs.size() && downs[di].ready_at <= pos) {
+        if (di < downs.size() && downs[di].ready_at <= pos) {
             emit(downs[di++].code);
-        } else if (ui < ups.size() && ups[ui].ready_at <= pos) {
-            emit(ups[ui++].code);
-        } else if (gi < gates.size()) {
-            emit(gates[gi++]);
-        } else if (ui < ups.size()) {
-            emit(ups[ui++].code);
+        } else if (gi < gus.size()) {
+            emit(gus[gi++]);
         } else if (di < downs.size()) {
             emit(downs[di++].code);
-        } else if (yi < yrs.size()) {
-            emit(yrs[yi++].code);
         } else {
             break;
         }
@@ -994,8 +975,8 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     a.pitch_d = L->pitch_d;
     a.pitch_r = L->pitch_r;
     a.act = L->act;
-    a.nblk = (a.D + 255) / 256;
-    a.ndt = (a.pitch_d + 255) / 256;
+    a.nblk = (a.D + kTcBlk - 1) / kTcBlk;
+    a.ndt = (a.pitch_d + 127) / 128;  // d tiles of 128 outputs (the down units' M)
     a.dense = dense;
     // blocks at least this dense (per 1024) stream whole by TMA tiles instead of row
     // gathers: ~26 vs ~55 GB/s per SM (tools/bw_tma.cu) puts the break-even near 0.47
@@ -1006,29 +987,26 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     a.bias = L->view.bias;
     a.gate = L->view.gate;
     a.ud = L->view.ud;
-    // K slices of the gate / up units: enough units to spread the union rows over the
-    // SMs while the owner slice's fixed-order partial sum stays small (partials are
-    // 256 rows x nb fp32): SG_TC_KSG / SG_TC_KSU override
-    const int ksg_want = env_int("SG_TC_KSG", B <= 16 ? 4 : 2), ksu_want = env_int("SG_TC_KSU", B <= 16 ? 4 : 2);
-    a.KSg = k_slices(a.pitch_d, std::min(ksg_want, kTcKSMax));
-    a.KSu = k_slices(a.pitch_d, std::min(ksu_want, kTcKSMax));
+    // from this batch size the union of the masks covers most rows: the GU units
+    // stream every block by TMA tiles without waiting for the predictor (SG_TC_TILE_ALL_B)
+    a.tile_all = !dense && B >= env_int("SG_TC_TILE_ALL_B", 8);
+    // K slices of the gate-up units: enough units to spread the rows over the SMs while
+    // the owner slice's fixed-order partial sum stays small (SG_TC_KSG overrides)
+    a.KSg = k_slices(a.pitch_d, std::min(env_int("SG_TC_KSG", 2), kTcKSMax));
     a.ksg = a.pitch_d / a.KSg;
-    a.ksu = a.pitch_d / a.KSu;
-    a.S = std::max(1, std::min({env_int("SG_TC_S", 8), kTcSMax, a.nblk}));
+    a.S = std::max(1, std::min({env_int("SG_TC_S", 4), kTcSMax, a.nblk}));
     a.kst = 256;
     const int NX = 32, KT = dense ? 0 : (a.pitch_d + a.kst - 1) / a.kst, NTR = dense ? 0 : a.pitch_r / 4;
     const int NPRE = dense ? 0 : a.nblk;
     a.u_T = NX;
     a.u_TR = a.u_T + KT;
     a.u_PRE = a.u_TR + NTR;
-    a.u_GATE = a.u_PRE + NPRE;
-    a.u_UP = a.u_GATE + a.nblk * a.KSg;
-    a.u_DOWN = a.u_UP + a.nblk * a.KSu;
-    a.u_YR = a.u_DOWN + a.ndt * a.S;
-    a.u_end = a.u_YR + a.ndt * 4;
+    a.u_GU = a.u_PRE + NPRE;
+    a.u_DOWN = a.u_GU + a.nblk * a.KSg;
+    a.u_end = a.u_DOWN + a.ndt * a.S;
     {  // the claim order for this unit geometry, uploaded once per ctx (graph-capture safe after)
         const int lag = env_int("SG_TC_LAG", C->G);
-        std::vector<int> key = {a.nblk, a.KSg, a.KSu, a.ndt, a.S, a.dense, NX, KT, NTR, lag};
+        std::vector<int> key = {a.nblk, a.KSg, a.ndt, a.S, a.dense, NX, KT, NTR, lag};
         auto oit = C->tc_orders.find(key);
         if (oit == C->tc_orders.end()) {
             const std::vector<int> order = tc_schedule(a, NX, KT, NTR, lag);
@@ -1177,8 +1155,8 @@ sg_status sg_ctx_enable_tc_trace(sg_ctx* C, int32_t max_units) {
     C->tc_trace_cap = 0;
     C->tc_trace_on = max_units > 0;
     if (max_units > 0) {
-        SG_CUDA(cudaMalloc(&C->tc_trace, static_cast<size_t>(max_units) * 6 * 8));
-        SG_CUDA(cudaMemset(C->tc_trace, 0, static_cast<size_t>(max_units) * 6 * 8));
+        SG_CUDA(cudaMalloc(&C->tc_trace, static_cast<size_t>(max_units) * 8 * 8));
+        SG_CUDA(cudaMemset(C->tc_trace, 0, static_cast<size_t>(max_units) * 8 * 8));
         C->tc_trace_cap = static_cast<size_t>(max_units);
     }
     return SG_OK;
@@ -1189,7 +1167,7 @@ sg_status sg_ctx_read_tc_trace(sg_ctx* C, void* stream, int32_t max_units, uint6
     DeviceGuard dg(C->device);
     SG_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
     const int n = std::min<int>(max_units, C->tc_last_units);
-    SG_CUDA(cudaMemcpy(out, C->tc_trace, static_cast<size_t>(n) * 6 * 8, cudaMemcpyDeviceToHost));
+    SG_CUDA(cudaMemcpy(out, C->tc_trace, static_cast<size_t>(n) * 8 * 8, cudaMemcpyDeviceToHost));
     if (n_units) *n_units = n;
     return SG_OK;
 }

@@ -140,17 +140,18 @@ struct TcMaps {            // TMA tensor maps (bf16, SWIZZLE_128B, 64-element in
 struct TcArgs {
     int B, nb, N;          // tokens, B rounded up to 8, MMA N = 2*nb (hi | lo columns)
     int d, D, r, pitch_d, pitch_r, act;
-    int nblk;              // neuron blocks of 256
+    int nblk;              // neuron blocks of 128 (one M = 128 tile of gate and of up rows)
     int kst;               // K of a T unit (the KT = u_TR - u_T slices)
-    int KSg, ksg, KSu, ksu;  // gate / up K slices and their width
+    int KSg, ksg;          // K slices of the gate-up (GU) units and their width
     int ndt, S;            // d tiles of 256 outputs, block ranges of the down GEMM
     int dense;             // 1: dense comparator (no predictor; every row)
-    int tile_g, tile_u;    // per-1024 density at which a gate / up(+down) block is tiled, not gathered
-    int u_T, u_TR, u_PRE, u_GATE, u_UP, u_DOWN, u_YR, u_end;  // unit counts by type (prefix sums)
+    int tile_g, tile_u;    // per-1024 density at which a GU / DOWN block is tiled, not gathered
+    int tile_all;          // 1: GU units tile every block without waiting for the mask (wide batches)
+    int u_T, u_TR, u_PRE, u_GU, u_DOWN, u_end;  // unit counts by type (prefix sums)
     const int* order;      // [n_units] claim order: type << 24 | i << 8 | j (host-built)
     int n_units;
     unsigned long long* trace;  // optional [n_units][6] %globaltimer stamps (tools/tc_trace.py)
-    int zpitch;            // slots of Z^T per row (nblk * 256)
+    int zpitch;            // slots of Z^T per row (nblk * 128)
     int xpitch;            // elements per X^T row (the ctx's max pitch; T^T rows are 256)
     const float* x;        // [B][d] input tokens
     float* y;              // [B][d] outputs
@@ -162,13 +163,11 @@ struct TcArgs {
     uint16_t* thl;         // [N][pitch_r]
     uint64_t* mbits;       // [D] predicted bit per token
     uint64_t* vbits;       // [D] survivor bit per token
-    int* ulist;            // [nblk][256] union rows of a block (local row in block), ascending
+    int* ulist;            // [nblk][128] union rows of a block (local row in block), ascending
     int* ucnt;             // [nblk]
-    int* vlist;            // [nblk][256] survivor rows of a block, ascending
-    int* vcnt;             // [nblk]
-    float* gpart;          // [KSg-1][nblk][256][nb]
-    float* upart;          // [KSu-1][nblk][256][nb]
-    float* G;              // [D][nb] gate pre-activations of the union rows
+    int* vlist;            // [nblk][128] survivor rows of a block, ascending
+    int* vcnt;             // [nblk] survivor rows | 1 << 16 when DOWN streams the block whole
+    float* gpart;          // [KSg-1][nblk][128][g nb | u nb]
     uint16_t* zhl;         // [N][zpitch]
     float* ypart;          // [S][ndt*256][nb]
     int* pcount;           // [64] |P_b|   (pcount, vcount, bad: zeroed by the host per call)
