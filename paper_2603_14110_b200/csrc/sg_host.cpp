@@ -49,6 +49,7 @@ struct sg_layer {
     uint64_t id = 0;                  // unique per (layer, view contents): bumped by set_hot_rows
     sg::TcMaps tcmaps{};              // weight tensor maps of the tensor-core batch path
     bool has_tcmaps = false;
+    int tc_brows = 0;                 // its neurons per block (sg::tc_block_rows)
 };
 
 struct sg_ctx {
@@ -613,10 +614,15 @@ sg_status sg_layer_create(const sg_layer_desc* desc, sg_layer** out) {
     if (has_w) {
         // tensor maps of the batched tensor-core path (sg_batch_tc.cu)
         sg::TcMaps& tm = L->tcmaps;
-        bool ok = make_map(&tm.gate, V.gate, pd, Dl, pd, 128) && make_map(&tm.up, V.ud, pd, Dl, 2 * pd, 128) &&
-                  make_map(&tm.down, V.ud + pd, pd, Dl, 2 * pd, 64);
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L->device);
+        const int br = sg::tc_block_rows(Dl, sms);
+        L->tc_brows = br;
+        bool ok = make_map(&tm.gate, V.gate, pd, Dl, pd, br) && make_map(&tm.up, V.ud, pd, Dl, 2 * pd, br) &&
+                  make_map(&tm.down, V.ud + pd, pd, Dl, 2 * pd, 16) &&
+                  make_map(&tm.down64, V.ud + pd, pd, Dl, 2 * pd, 64);
         if (ok && has_pred)
-            ok = make_map(&tm.A, V.A, pr, Dl, pr, 128) && make_map(&tm.Bp, V.B, pd, r, pd, 128);
+            ok = make_map(&tm.A, V.A, pr, Dl, pr, br) && make_map(&tm.Bp, V.B, pd, r, pd, 128);
         L->has_tcmaps = ok;
     }
     if (has_w && has_pred) {
@@ -848,24 +854,27 @@ int env_int(const char* name, int dflt) {
     return e ? std::atoi(e) : dflt;
 }
 
-constexpr int kTcKSMax = 2;   // K slices of the gate-up units (the finisher's register budget)
-constexpr int kTcBlk = 128;   // neurons per block of the tensor-core kernel
-constexpr int kTcSMax = 4;    // block ranges of the down units (the y finisher's register budget)
+constexpr int kTcBlk = 128;   // block capacity of the tensor-core kernel (rows of an M = 128 tile)
+constexpr int kTcSMax = 4;    // block ranges of the down units (the y finisher sums <= 4)
+constexpr int kTcKTMax = 4;   // K slices of the predictor's T units (the finisher sums <= 4)
+
+// blocks of a layer at most: one per SM, or D / 128 for very wide layers
+size_t tc_block_cap(const sg_ctx* C) {
+    return std::max<size_t>(static_cast<size_t>(C->G), (static_cast<size_t>(C->max_D) + kTcBlk - 1) / kTcBlk) + 8;
+}
 
 sg_status tc_workspace(sg_ctx* C) {
     if (C->tmem_ws) return SG_OK;
-    const size_t Dm = static_cast<size_t>(C->max_D), pd = static_cast<size_t>(C->pitch_dmax);
-    const size_t nblk = (Dm + kTcBlk - 1) / kTcBlk, ndt = (pd + 127) / 128;
+    const size_t pd = static_cast<size_t>(C->pitch_dmax);
+    const size_t nblk = tc_block_cap(C), ndt = (pd + 127) / 128, Dm = static_cast<size_t>(C->max_D);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const size_t o = off;
         off += (bytes + 255) / 256 * 256;
         return o;
     };
-    const size_t o_x = take(128 * pd * 2), o_tp = take(((pd + 255) / 256) * 256 * 64 * 4),
-                 o_th = take(128 * 256 * 2), o_mb = take(Dm * 8), o_vb = take(Dm * 8),
-                 o_ul = take(nblk * kTcBlk * 4), o_uc = take(nblk * 4), o_vl = take(nblk * kTcBlk * 4),
-                 o_vc = take(nblk * 4), o_gp = take(kTcKSMax * nblk * kTcBlk * 2 * 64 * 4),
+    const size_t o_x = take(128 * pd * 2), o_tp = take(kTcKTMax * 256 * 64 * 4), o_th = take(128 * 256 * 2),
+                 o_mb = take(Dm * 8), o_vb = take(Dm * 8), o_vl = take(nblk * kTcBlk * 4), o_vc = take(nblk * 4),
                  o_z = take(128 * nblk * kTcBlk * 2), o_y = take(kTcSMax * ndt * 128 * 64 * 4),
                  o_cnt = take((64 + 64 + 1) * 4),
                  o_fl = take(static_cast<size_t>(sg::tc_flag_ints(static_cast<int>(nblk), static_cast<int>(ndt))) * 4);
@@ -883,11 +892,8 @@ sg_status tc_workspace(sg_ctx* C) {
     a.thl = reinterpret_cast<uint16_t*>(b + o_th);
     a.mbits = reinterpret_cast<uint64_t*>(b + o_mb);
     a.vbits = reinterpret_cast<uint64_t*>(b + o_vb);
-    a.ulist = reinterpret_cast<int*>(b + o_ul);
-    a.ucnt = reinterpret_cast<int*>(b + o_uc);
     a.vlist = reinterpret_cast<int*>(b + o_vl);
     a.vcnt = reinterpret_cast<int*>(b + o_vc);
-    a.gpart = reinterpret_cast<float*>(b + o_gp);
     a.zhl = reinterpret_cast<uint16_t*>(b + o_z);
     a.ypart = reinterpret_cast<float*>(b + o_y);
     a.pcount = reinterpret_cast<int*>(b + o_cnt);
@@ -907,57 +913,33 @@ int k_slices(int pitch, int want) {
     return 1;
 }
 
-// The claim order of the tensor-core kernel's units (sg_batch_tc.cu): the predictor
-// chain, then GATE units block by block, with each block's UP units, each block
-// range's DOWN units and each d tile's YR units merged in `lag` claims after the
-// units they depend on (about one wave of the grid: by then those have finished),
-// so no stage waits for a whole previous stage. Topological by construction.
-std::vector<int> tc_schedule(const sg::TcArgs& a, int NX, int KT, int NTR, int lag) {
+// The claim order of the tensor-core kernel's units (sg_batch_tc.cu): X, the T
+// slices, the GU blocks, with each block range's DOWN units merged in `lag` claims
+// after the range's last GU block (about one wave of the grid: by then the range's
+// blocks are streaming in), so no unit waits for a whole previous phase.
+// Topological by construction.
+std::vector<int> tc_schedule(const sg::TcArgs& a, int NX, int KT, int lag) {
     auto code = [](int t, int i, int j) { return (t << 24) | (i << 8) | j; };
-    enum { X = 1, T, TR, PRE, GU, DOWN };  // sg_batch_tc.cu UnitType
+    enum { X = 1, T, GU, DOWN };  // sg_batch_tc.cu UnitType
     std::vector<int> order;
     for (int k = 0; k < NX; ++k) order.push_back(code(X, k, 0));
     for (int k = 0; k < KT; ++k) order.push_back(code(T, k, 0));
-    for (int k = 0; k < NTR; ++k) order.push_back(code(TR, k, 0));
-    if (!a.dense)
-        for (int b = 0; b < a.nblk; ++b) order.push_back(code(PRE, b, 0));
     struct Item {
         int code, ready_at;
     };
     std::vector<Item> downs;
-    std::vector<int> gu_done_at(static_cast<size_t>(a.nblk), -1);
     auto range_lo = [&](int sr) { return sr * a.nblk / a.S; };
-    std::vector<int> gus;
-    for (int b = 0; b < a.nblk; ++b)
-        for (int ks = a.KSg - 1; ks >= 0; --ks) gus.push_back(code(GU, b, ks));
-    size_t gi = 0, di = 0;
-    auto emit = [&](int c) {
-        order.push_back(c);
-        const int pos = static_cast<int>(order.size());
-        const int t = c >> 24, i = (c >> 8) & 0xffff;
-        if (t == GU && (c & 0xff) == 0) {  // the block's owner
-            gu_done_at[static_cast<size_t>(i)] = pos;
-            for (int sr = 0; sr < a.S; ++sr) {
-                if (i != range_lo(sr + 1) - 1) continue;  // the range's last block
-                int ready = 0;
-                for (int b = range_lo(sr); b < range_lo(sr + 1); ++b)
-                    ready = std::max(ready, gu_done_at[static_cast<size_t>(b)]);
-                for (int dt = 0; dt < a.ndt; ++dt) downs.push_back({code(DOWN, dt, sr), ready + lag});
-            }
-        }
-    };
-    for (;;) {
-        const int pos = static_cast<int>(order.size());
-        if (di < downs.size() && downs[di].ready_at <= pos) {
-            emit(downs[di++].code);
-        } else if (gi < gus.size()) {
-            emit(gus[gi++]);
-        } else if (di < downs.size()) {
-            emit(downs[di++].code);
-        } else {
-            break;
-        }
+    size_t di = 0;
+    for (int b = 0; b < a.nblk; ++b) {
+        while (di < downs.size() && downs[di].ready_at <= static_cast<int>(order.size()))
+            order.push_back(downs[di++].code);
+        order.push_back(code(GU, b, 0));
+        for (int sr = 0; sr < a.S; ++sr)
+            if (b == range_lo(sr + 1) - 1)  // the range's last block
+                for (int dt = 0; dt < a.ndt; ++dt)
+                    downs.push_back({code(DOWN, dt, sr), static_cast<int>(order.size()) + lag});
     }
+    for (; di < downs.size(); ++di) order.push_back(downs[di].code);
     return order;
 }
 
@@ -975,41 +957,35 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     a.pitch_d = L->pitch_d;
     a.pitch_r = L->pitch_r;
     a.act = L->act;
-    a.nblk = (a.D + kTcBlk - 1) / kTcBlk;
+    a.brows = L->tc_brows;
+    a.nblk = (a.D + a.brows - 1) / a.brows;
+    if (static_cast<size_t>(a.nblk) > tc_block_cap(C))
+        return fail(SG_ERR_USAGE, "tensor-core batch: layer has more blocks than the ctx workspace holds");
     a.ndt = (a.pitch_d + 127) / 128;  // d tiles of 128 outputs (the down units' M)
     a.dense = dense;
-    // blocks at least this dense (per 1024) stream whole by TMA tiles instead of row
-    // gathers: ~26 vs ~55 GB/s per SM (tools/bw_tma.cu) puts the break-even near 0.47
-    a.tile_g = env_int("SG_TC_TILE_G", 480);
-    a.tile_u = env_int("SG_TC_TILE_U", 480);
+    // a block's down rows stream whole once its survivors reach this density (per
+    // 1024; SG_TC_TILE_U): a row gather moves a fraction of the tile rate per SM
+    a.tile_u = env_int("SG_TC_TILE_U", 150);
     a.x = xs;
     a.y = ys;
     a.bias = L->view.bias;
-    a.gate = L->view.gate;
     a.ud = L->view.ud;
-    // from this batch size the union of the masks covers most rows: the GU units
-    // stream every block by TMA tiles without waiting for the predictor (SG_TC_TILE_ALL_B)
-    a.tile_all = !dense && B >= env_int("SG_TC_TILE_ALL_B", 8);
-    // K slices of the gate-up units: enough units to spread the rows over the SMs while
-    // the owner slice's fixed-order partial sum stays small (SG_TC_KSG overrides)
-    a.KSg = k_slices(a.pitch_d, std::min(env_int("SG_TC_KSG", 2), kTcKSMax));
-    a.ksg = a.pitch_d / a.KSg;
     a.S = std::max(1, std::min({env_int("SG_TC_S", 4), kTcSMax, a.nblk}));
-    a.kst = 256;
-    const int NX = 32, KT = dense ? 0 : (a.pitch_d + a.kst - 1) / a.kst, NTR = dense ? 0 : a.pitch_r / 4;
-    const int NPRE = dense ? 0 : a.nblk;
+    const int KT = dense ? 0 : k_slices(a.pitch_d, kTcKTMax);
+    a.kst = KT ? a.pitch_d / KT : 0;
+    // x -> X^T hi / lo: about 256 (token, 8-column) items per unit, so each epilogue
+    // thread issues its loads in one round
+    const int NX = std::max(8, std::min(128, a.nb * (a.pitch_d / 8) / 256));
     a.u_T = NX;
-    a.u_TR = a.u_T + KT;
-    a.u_PRE = a.u_TR + NTR;
-    a.u_GU = a.u_PRE + NPRE;
-    a.u_DOWN = a.u_GU + a.nblk * a.KSg;
+    a.u_GU = a.u_T + KT;
+    a.u_DOWN = a.u_GU + a.nblk;
     a.u_end = a.u_DOWN + a.ndt * a.S;
     {  // the claim order for this unit geometry, uploaded once per ctx (graph-capture safe after)
         const int lag = env_int("SG_TC_LAG", C->G);
-        std::vector<int> key = {a.nblk, a.KSg, a.ndt, a.S, a.dense, NX, KT, NTR, lag};
+        std::vector<int> key = {a.nblk, a.ndt, a.S, a.dense, NX, KT, lag};
         auto oit = C->tc_orders.find(key);
         if (oit == C->tc_orders.end()) {
-            const std::vector<int> order = tc_schedule(a, NX, KT, NTR, lag);
+            const std::vector<int> order = tc_schedule(a, NX, KT, lag);
             if (static_cast<int>(order.size()) != a.u_end)
                 return fail(SG_ERR_CUDA, "tensor-core schedule: unit count mismatch");
             int* dev = nullptr;
@@ -1197,12 +1173,27 @@ sg_status sg_ctx_read_batch(sg_ctx* C, void* stream, int32_t batch, sg_exec_stat
             vc[b] = st4[4 * b + 1];
             bad |= st4[4 * b + 2] != 0;  // the device non-finite flag of token b
         }
-    } else {
-        const bool tc = C->blast_path >= 2;
+    } else if (C->blast_path >= 2) {
+        // tensor-core path: the per-token counts are the bit columns' popcounts (the
+        // kernel keeps only the bits)
         int flag = 0;
-        SG_CUDA(cudaMemcpy(pc, tc ? C->tw.pcount : C->bw.pcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
-        SG_CUDA(cudaMemcpy(vc, tc ? C->tw.vcount : C->bw.vcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
-        SG_CUDA(cudaMemcpy(&flag, tc ? C->tw.bad : C->bw.bad, sizeof(int), cudaMemcpyDeviceToHost));
+        SG_CUDA(cudaMemcpy(&flag, C->tw.bad, sizeof(int), cudaMemcpyDeviceToHost));
+        bad = flag != 0;
+        std::vector<uint64_t> mb(static_cast<size_t>(L->D_local)), vb(static_cast<size_t>(L->D_local));
+        if (C->blast_path == 2)
+            SG_CUDA(cudaMemcpy(mb.data(), C->tw.mbits, sizeof(uint64_t) * mb.size(), cudaMemcpyDeviceToHost));
+        SG_CUDA(cudaMemcpy(vb.data(), C->tw.vbits, sizeof(uint64_t) * vb.size(), cudaMemcpyDeviceToHost));
+        for (int b = 0; b < batch; ++b) pc[b] = vc[b] = 0;
+        for (size_t n = 0; n < vb.size(); ++n)
+            for (int b = 0; b < batch; ++b) {
+                pc[b] += static_cast<int>((mb[n] >> b) & 1ull);
+                vc[b] += static_cast<int>((vb[n] >> b) & 1ull);
+            }
+    } else {
+        int flag = 0;
+        SG_CUDA(cudaMemcpy(pc, C->bw.pcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
+        SG_CUDA(cudaMemcpy(vc, C->bw.vcount, sizeof(int) * batch, cudaMemcpyDeviceToHost));
+        SG_CUDA(cudaMemcpy(&flag, C->bw.bad, sizeof(int), cudaMemcpyDeviceToHost));
         bad = flag != 0;
     }
     const int pipe = C->blast_path == 3 ? SG_PIPELINE_DENSE : SG_PIPELINE_SEQUENTIAL;

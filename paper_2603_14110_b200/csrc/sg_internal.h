@@ -126,50 +126,51 @@ int batch_max();
 int launch_batch(const BatchArgs& a, const float* xs, float* ys, void* stream);
 
 // Batched decode on the tensor cores (sg_batch_tc.cu): one persistent launch per
-// layer, tcgen05.mma with TMEM accumulators, weight rows by TMA tile::gather4.
+// layer, tcgen05.mma with TMEM accumulators, weight rows by TMA tiles (down rows of
+// sparse blocks by cp.async gathers).
 struct TcMaps {            // TMA tensor maps (bf16, SWIZZLE_128B, 64-element inner box)
-    CUtensorMap xhl;       // X^T hi/lo   [N][pitch_d]        box {64, N}
-    CUtensorMap thl;       // T^T hi/lo   [N][pitch_r]        box {64, N}
+    CUtensorMap xhl;       // X^T hi/lo   [N][xpitch]         box {64, N}
+    CUtensorMap thl;       // T^T hi/lo   [N][256]            box {64, N}
     CUtensorMap zhl;       // Z^T hi/lo   [N][zpitch]         box {64, N}
     CUtensorMap Bp;        // predictor B [r][pitch_d]        box {64, 128}
-    CUtensorMap A;         // predictor A [D][pitch_r]        box {64, 128}
-    CUtensorMap gate;      // gate rows   [D][pitch_d]        box {64, 128} (dense comparator)
-    CUtensorMap up;        // up rows     [D][pitch_d], row stride 2*pitch_d (ud, first half)
-    CUtensorMap down;      // down rows   [D][pitch_d], row stride 2*pitch_d (ud + pitch_d) box {64, 64}
+    CUtensorMap A;         // predictor A [D][pitch_r]        box {64, brows}
+    CUtensorMap gate;      // gate rows   [D][pitch_d]        box {64, brows}
+    CUtensorMap up;        // up rows     [D][pitch_d], row stride 2*pitch_d (ud, first half)   box {64, brows}
+    CUtensorMap down;      // down rows   [D][pitch_d], row stride 2*pitch_d (ud + pitch_d)     box {64, 16}
+    CUtensorMap down64;    // the same rows                                                     box {64, 64}
 };
+// Rows per neuron block of the tensor-core path for a layer of D (local) rows on a
+// device with `sms` SMs: about one block per SM beside the predictor's units, so the
+// gate / up streaming needs no split-K (sg_batch_tc.cu).
+int tc_block_rows(int64_t D, int sms);
 struct TcArgs {
     int B, nb, N;          // tokens, B rounded up to 8, MMA N = 2*nb (hi | lo columns)
     int d, D, r, pitch_d, pitch_r, act;
-    int nblk;              // neuron blocks of 128 (one M = 128 tile of gate and of up rows)
-    int kst;               // K of a T unit (the KT = u_TR - u_T slices)
-    int KSg, ksg;          // K slices of the gate-up (GU) units and their width
-    int ndt, S;            // d tiles of 256 outputs, block ranges of the down GEMM
+    int brows;             // neurons per block (<= 128: rows of one M = 128 tile)
+    int nblk;              // neuron blocks
+    int kst;               // K of a T unit (the KT = u_GU - u_T slices)
+    int ndt, S;            // d tiles of 128 outputs, block ranges of the down GEMM (S <= 4)
     int dense;             // 1: dense comparator (no predictor; every row)
-    int tile_g, tile_u;    // per-1024 density at which a GU / DOWN block is tiled, not gathered
-    int tile_all;          // 1: GU units tile every block without waiting for the mask (wide batches)
-    int u_T, u_TR, u_PRE, u_GU, u_DOWN, u_end;  // unit counts by type (prefix sums)
+    int tile_u;            // per-1024 survivor density at which DOWN tiles a block, not gathers
+    int u_T, u_GU, u_DOWN, u_end;  // unit counts by type (prefix sums: X, T, GU, DOWN)
     const int* order;      // [n_units] claim order: type << 24 | i << 8 | j (host-built)
     int n_units;
-    unsigned long long* trace;  // optional [n_units][6] %globaltimer stamps (tools/tc_trace.py)
-    int zpitch;            // slots of Z^T per row (nblk * 128)
-    int xpitch;            // elements per X^T row (the ctx's max pitch; T^T rows are 256)
+    unsigned long long* trace;  // optional [n_units][8] stamps (tools/tc_trace.py)
+    int zpitch;            // slots of Z^T per row (block capacity 128 x blocks)
+    int xpitch;            // elements per X^T row (the ctx's max pitch)
     const float* x;        // [B][d] input tokens
     float* y;              // [B][d] outputs
     const float* bias;     // [D]
-    const uint16_t* gate;  // [D][pitch_d]      gathered rows (cp.async)
-    const uint16_t* ud;    // [D][2*pitch_d]    [up | down] rows
-    uint16_t* xhl;         // [N][pitch_d]
+    const uint16_t* ud;    // [D][2*pitch_d]    [up | down] rows (down rows gathered by cp.async)
+    uint16_t* xhl;         // [N][xpitch]
     float* tpart;          // [KT][256][nb]
-    uint16_t* thl;         // [N][pitch_r]
+    uint16_t* thl;         // [N][256]
     uint64_t* mbits;       // [D] predicted bit per token
     uint64_t* vbits;       // [D] survivor bit per token
-    int* ulist;            // [nblk][128] union rows of a block (local row in block), ascending
-    int* ucnt;             // [nblk]
-    int* vlist;            // [nblk][128] survivor rows of a block, ascending
+    int* vlist;            // [nblk][128] survivor rows of a block (row in block), ascending
     int* vcnt;             // [nblk] survivor rows | 1 << 16 when DOWN streams the block whole
-    float* gpart;          // [KSg-1][nblk][128][g nb | u nb]
     uint16_t* zhl;         // [N][zpitch]
-    float* ypart;          // [S][ndt*256][nb]
+    float* ypart;          // [S][ndt*128][nb]
     int* pcount;           // [64] |P_b|   (pcount, vcount, bad: zeroed by the host per call)
     int* vcount;           // [64] |V_b|
     int* bad;              // non-finite input flag

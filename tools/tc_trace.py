@@ -18,7 +18,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-TYPES = {1: "X", 2: "T", 3: "TR", 4: "PRE", 5: "GU", 6: "DOWN"}
+TYPES = {1: "X", 2: "T", 3: "GU", 4: "DOWN"}
 
 
 def main():
@@ -74,7 +74,7 @@ def main():
         ep = np.nanmean(mm[:, 0] - r[:, 3]) if np.isfinite(mm[:, 0]).any() else float("nan")
         ea = np.nanmean(mm[:, 1] - mm[:, 0]) if np.isfinite(mm[:, 1]).any() else float("nan")
         ef = np.nanmean(r[:, 4] - mm[:, 1]) if np.isfinite(mm[:, 1]).any() else float("nan")
-        if t in (2, 3, 1, 4):  # units without a TMEM load stage: load / mma stamps unset
+        if t == 1:  # X: no loads, no MMA
             load = mma = np.full_like(load, np.nan)
         print(f"{name:6s} {sel.sum():5d} {r[:, 0].min():8.1f} {r[:, 0].max():8.1f} {r[:, 4].min():8.1f} "
               f"{r[:, 4].max():8.1f} {wait.mean():7.2f} {np.nanmean(load):7.2f} {np.nanmean(mma):7.2f} "
