@@ -508,8 +508,11 @@ def main():
     # configs[0] is ONE layer (~70 MB touched < 126 MB L2): the step rotates over 4
     # device copies of it so every step streams its bytes from HBM
     copies = 4 if L == 1 else 1
+    # batched decode: neurons by decreasing calibration activity (the batch's survivor
+    # rows concentrate in the leading blocks; trailing blocks skip their down rows)
+    balance = False if args.no_balance else ("sorted" if args.batch > 0 else True)
     layers = [upload(h, d, D, cfg["act"], args.rank, device=local, shard_index=rank,
-                     shard_count=world, balance=not args.no_balance,
+                     shard_count=world, balance=balance,
                      hot_rows=args.hot_rows) for h in host for _ in range(copies)]
     host_l = [h for h in host for _ in range(copies)]
     Ls = len(layers)  # layers per launch

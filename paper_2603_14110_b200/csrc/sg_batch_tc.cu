@@ -178,11 +178,15 @@ template <int N>
 __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
-// this thread's copies of the stage have landed: make them visible to the tensor
-// cores (async proxy) and count the thread on the stage's full barrier
+// the warp's copies of the stage have landed: make them visible to the tensor cores
+// (async proxy) and count the warp on the stage's full barrier (one arrival per
+// producer warp: a barrier word updated by 96 threads per stage costs more than the
+// stage's data takes to arrive)
+constexpr int kFullArrivals = kProdThreads / 32 + 1;  // the producer warps + the expect_tx
 __device__ __forceinline__ void stage_arrive(uint64_t* bar) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_arrive(bar);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
 }
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -245,7 +249,15 @@ __device__ __forceinline__ int blk_rows(const TcArgs& a, int blk) {
     const int r = a.D - blk * a.brows;
     return r < a.brows ? r : a.brows;
 }
-__device__ __forceinline__ int range_lo(const TcArgs& a, int s) { return s * a.nblk / a.S; }
+// The S block ranges of the DOWN units interleave chunks of kRangePair consecutive
+// blocks (range j: chunks j, j + S, j + 2S, ...), so every range mixes the layout's
+// leading (hot) and trailing (cold) blocks and the ranges carry about equal survivor
+// rows, while a chunk's tiled blocks still stream as one run of full stages; block k
+// of range j (>= nblk: past its end).
+constexpr int kRangePair = 8;
+__device__ __forceinline__ int range_block(const TcArgs& a, int j, int k) {
+    return (j + (k / kRangePair) * a.S) * kRangePair + k % kRangePair;
+}
 // DOWN streams a block whole by TMA tiles (reading its non-survivor rows too, against
 // Z = 0) once its survivors are a large enough share of its rows: a row gather moves
 // a fraction of the tile rate per SM.
@@ -264,47 +276,60 @@ __device__ __forceinline__ bool vcnt_tiled(int raw) { return (raw & kVTiled) != 
 // own. A stage covers `rows` K rows (its MMA runs ceil(rows / 16) K steps; the Z
 // slots up to the next 16 are exact zeros).
 struct DownWalk {
-    int blk, end;     // next block to visit, end of the range
+    int j, k, done;   // the range, its next block index, all blocks visited
     int run0, run1;   // tiled rows not yet staged
-    int pend, pnv;    // a gathered block behind the run, its survivor count
+    int pend, pv;     // a block that does not extend the run, its vcnt
     int gblk, g0, g1; // the gathered block being staged: survivor positions [g0, g1)
 };
 struct DownStage {
     int tiled;  // 1: rows [row0, row0 + rows); 0: block gblk's survivors [c0, c0 + rows)
     int row0, rows, gblk, c0;
+    int kd;     // K rows the stage's smem layout holds (128: tiled stages when Z fits twice)
 };
-__device__ __forceinline__ DownWalk down_walk(const TcArgs& a, int j) {
-    return DownWalk{range_lo(a, j), range_lo(a, j + 1), 0, 0, -1, 0, 0, 0, 0};
-}
+// tiled down stages take 128 K rows when the Z tile of 128 slots fits the B area
+__device__ __forceinline__ int down_kd(const TcArgs& a) { return a.N <= 64 ? 128 : 64; }
+__device__ __forceinline__ DownWalk down_walk(int j) { return DownWalk{j, 0, 0, 0, 0, -1, 0, 0, 0, 0}; }
 template <class Wait>
 __device__ __forceinline__ bool down_next(const TcArgs& a, DownWalk& w, DownStage& st, Wait&& wait) {
     for (;;) {
+        const int kd = down_kd(a);
         if (w.g0 < w.g1) {
-            st = DownStage{0, 0, min(64, w.g1 - w.g0), w.gblk, w.g0};
-            w.g0 += 64;
+            st = DownStage{0, 0, min(kd, w.g1 - w.g0), w.gblk, w.g0, kd};
+            w.g0 += kd;
             return true;
         }
-        if (w.run1 - w.run0 >= 64 || (w.run1 > w.run0 && (w.pend >= 0 || w.blk >= w.end))) {
-            st = DownStage{1, w.run0, min(64, w.run1 - w.run0), 0, 0};
+        if (w.run1 - w.run0 >= kd || (w.run1 > w.run0 && (w.pend >= 0 || w.done))) {
+            st = DownStage{1, w.run0, min(kd, w.run1 - w.run0), 0, 0, kd};
             w.run0 += st.rows;
             return true;
         }
-        if (w.pend >= 0) {  // the run is staged: now the gathered block
-            w.gblk = w.pend;
-            w.g0 = 0;
-            w.g1 = w.pnv;
+        if (w.pend >= 0) {  // the run is staged: now the block behind it
+            if (vcnt_tiled(w.pv)) {
+                w.run0 = w.run1 = w.pend * a.brows;
+                w.run1 += blk_rows(a, w.pend);
+            } else {  // (an empty block: nothing)
+                w.gblk = w.pend;
+                w.g0 = 0;
+                w.g1 = vcnt_rows(w.pv);
+            }
             w.pend = -1;
             continue;
         }
-        if (w.blk >= w.end) return false;
-        const int blk = w.blk++;
-        const int v = wait(blk);  // the block's vcnt once it is complete (in about claim order)
-        if (vcnt_tiled(v)) {
-            if (w.run1 == w.run0) w.run0 = w.run1 = blk * a.brows;
+        if (w.done) return false;
+        const int blk = range_block(a, w.j, w.k);
+        if (blk >= a.nblk) {
+            w.done = 1;
+            continue;
+        }
+        const int v = wait(w.k++, blk);  // the block's vcnt once it is complete
+        if (vcnt_tiled(v) && w.run1 > w.run0 && w.run1 == blk * a.brows) {
+            w.run1 += blk_rows(a, blk);  // contiguous with the run: extend it
+        } else if (vcnt_tiled(v) && w.run1 == w.run0) {
+            w.run0 = w.run1 = blk * a.brows;
             w.run1 += blk_rows(a, blk);
         } else {
-            w.pend = blk;  // (an empty block ends the run too)
-            w.pnv = vcnt_rows(v);
+            w.pend = blk;
+            w.pv = v;
         }
     }
 }
@@ -319,8 +344,16 @@ __device__ __forceinline__ int* fl_gu(const TcArgs& a, int b) { return a.flags +
 __device__ __forceinline__ int* fl_down(const TcArgs& a, int t) { return a.flags + 32 + a.nblk + t; }
 __device__ __forceinline__ int flag_count(const TcArgs& a) { return 32 + a.nblk + a.ndt; }
 
+// what the MMA issuer needs of a DOWN stage (written by the producer's controller
+// before it arrives on the stage's full barrier)
+struct StageInfo {
+    int ksteps;  // K steps of 16 (0: no data)
+    int kd;      // K rows of the stage's layout
+    int last;    // the unit's final (empty) stage
+};
 struct TcSmem {
     uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], uqf[kUQ], uqe[kUQ];
+    StageInfo sinfo[kStages];
     Unit uq[kUQ];
     uint32_t tmem;
     int rows[kBlk];      // producer: gather rows of the current block (global neuron index)
@@ -339,14 +372,14 @@ struct TcSmem {
 // TMA tiles from the controller; gathered down rows by 16-B cp.async from every
 // producer thread, written in the 128-B-swizzled UMMA layout. For gathered stages
 // each thread keeps kLag stages of its copies in flight, then (wait_group, proxy
-// fence) arrives on the stage's full barrier (kProdThreads + 1 arrivals: the threads
-// + the controller's expect_tx); tile stages arrive at once. Before any blocking
+// fence, warp sync) arrives on the stage's full barrier once per warp (kFullArrivals:
+// the warps + the controller's expect_tx); tile stages arrive at once. Before any blocking
 // wait every thread flushes its pending arrivals, so no stage is held back.
 __device__ __forceinline__ bool unit_inputs_ready(const TcArgs& a, int type, int j) {
     switch (type) {
         case U_T:
         case U_GU: return flag_ready(fl_x(a), a.u_T);
-        case U_DOWN: return flag_ready(fl_gu(a, range_lo(a, j)), 1);  // later blocks: as they stream
+        case U_DOWN: return flag_ready(fl_gu(a, range_block(a, j, 0)), 1);  // later blocks: as they stream
         default: return true;  // U_X
     }
 }
@@ -354,7 +387,7 @@ __device__ __forceinline__ void unit_inputs_wait(const TcArgs& a, int type, int 
     switch (type) {
         case U_T:
         case U_GU: wait_count(fl_x(a), a.u_T); break;
-        case U_DOWN: wait_count(fl_gu(a, range_lo(a, j)), 1); break;
+        case U_DOWN: wait_count(fl_gu(a, range_block(a, j, 0)), 1); break;
         default: break;
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -375,9 +408,18 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
         cp_wait<0>();
         for (; pending > 0; --pending) stage_arrive(&S.full[(n - pending) % kStages]);
     };
+#ifdef SG_TC_FINTRACE
+    unsigned long long ewait = 0;  // ns the controller spent waiting for free stages (this unit)
+#endif
     auto begin_stage = [&](uint8_t*& As, uint32_t& as, uint64_t*& bar) {
         const int s = n % kStages;
+#ifdef SG_TC_FINTRACE
+        const unsigned long long t0 = gtimer();
         mbar_wait(&S.empty[s], (ephase >> s) & 1u);
+        ewait += gtimer() - t0;
+#else
+        mbar_wait(&S.empty[s], (ephase >> s) & 1u);
+#endif
         ephase ^= 1u << s;
         As = stages + s * kStageBytes;
         as = sbase + s * kStageBytes;
@@ -392,8 +434,9 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
             --pending;
         }
     };
-    auto end_tile_stage = [&](uint64_t* bar) {  // (no copies of this thread: arrive now)
-        mbar_arrive(bar);
+    auto end_tile_stage = [&](uint64_t* bar) {  // (no copies of this warp: arrive now)
+        __syncwarp();
+        if ((pt & 31) == 0) mbar_arrive(bar);
         ++n;
     };
     // a cross-CTA wait inside a unit: release this thread's held-back stages first
@@ -509,42 +552,56 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
             }
         } else {  // U_DOWN: K = Z slots of the block range, A = down rows (MN-major)
             const int m0 = i * 128;
-            DownWalk w = down_walk(a, j);
+            DownWalk w = down_walk(j);
             DownStage ds;
-            {  // one round of loads for the range's completion flags and counts
-                const int blk = w.blk + pt;
-                int v = -1;
-                if (blk < w.end && flag_ready(fl_gu(a, blk), 1)) v = __ldcg(a.vcnt + blk);
-                S.dvc[pt] = v;
+            // the range's completion flags and counts, one round of loads for all blocks;
+            // a block found incomplete is waited for, then the rest are read again
+            auto fetch = [&] {
                 prod_bar();
-            }
-            auto wait_blk = [&](int blk) {
-                const int k = blk - range_lo(a, j);
-                int v = k < kProdThreads ? S.dvc[k] : -1;
-                if (v < 0) {
+                const int blk = range_block(a, j, pt);
+                S.dvc[pt] = (blk < a.nblk && flag_ready(fl_gu(a, blk), 1)) ? __ldcg(a.vcnt + blk) : -1;
+                prod_bar();
+            };
+            fetch();
+            auto wait_blk = [&](int k, int blk) {
+                if (k >= kProdThreads) {
                     wait_flag(fl_gu(a, blk), 1);
-                    v = __ldcg(a.vcnt + blk);
+                    return __ldcg(a.vcnt + blk);
                 }
-                return v;
+                if (S.dvc[k] < 0) {
+                    wait_flag(fl_gu(a, blk), 1);
+                    fetch();
+                }
+                return S.dvc[k];
             };
             int cnt = 0;
-            while (down_next(a, w, ds, wait_blk)) {
+#ifdef SG_TC_FINTRACE
+            int nstg = 0;
+#endif
+            auto next = [&] { return down_next(a, w, ds, wait_blk); };
+            while (next()) {
+#ifdef SG_TC_FINTRACE
+                if (pt == 0 && nstg++ == 0) TC_TRACE(a, un.u, 6, gtimer());
+#endif
                 if (ds.tiled) {
-                    // rows by TMA tiles: 16-row boxes x 2 atoms of 64 outputs
+                    // rows by TMA tiles into 2 atoms of 64 outputs x kd k-rows (64-row boxes,
+                    // 16-row boxes for the tail); Z: kd / 64 boxes of 64 slots
                     flush();
-                    const int nbox = (ds.rows + 15) / 16;
+                    const int full = ds.rows / 64, nbox = (ds.rows % 64 + 15) / 16, nz = ds.kd / 64;
                     begin_stage(As, as, bar);
                     if (pt == 0) {
-                        mbar_expect_tx(bar, static_cast<uint32_t>(nbox) * 2u * 2048u + bbytes);
+                        S.sinfo[(n) % kStages] = StageInfo{(ds.rows + 15) / 16, ds.kd, 0};
+                        mbar_expect_tx(bar, static_cast<uint32_t>(full * 8192 + nbox * 2048) * 2u + nz * bbytes);
                         for (int atom = 0; atom < 2; ++atom) {
-                            if (ds.rows == 64) {
-                                tma_tile(As + atom * 8192, &M.down64, m0 + atom * 64, ds.row0, bar);
-                            } else {
-                                for (int q = 0; q < nbox; ++q)
-                                    tma_tile(As + atom * 8192 + q * 2048, &M.down, m0 + atom * 64, ds.row0 + q * 16, bar);
-                            }
+                            uint8_t* dst = As + atom * ds.kd * 128;
+                            for (int f = 0; f < full; ++f)
+                                tma_tile(dst + f * 8192, &M.down64, m0 + atom * 64, ds.row0 + f * 64, bar);
+                            for (int q = 0; q < nbox; ++q)
+                                tma_tile(dst + full * 8192 + q * 2048, &M.down, m0 + atom * 64,
+                                         ds.row0 + full * 64 + q * 16, bar);
                         }
-                        tma_tile(As + kStageA, &M.zhl, ds.row0, 0, bar);
+                        for (int z = 0; z < nz; ++z)
+                            tma_tile(As + kStageA + z * a.N * 128, &M.zhl, ds.row0 + z * 64, 0, bar);
                     }
                     end_tile_stage(bar);
                     continue;
@@ -556,26 +613,42 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                         S.rows[k] = ds.gblk * a.brows + __ldcg(a.vlist + ds.gblk * kBlk + k);
                     prod_bar();
                 }
+                const int nz = ds.kd / 64, r16 = (ds.rows + 15) / 16 * 16;
                 begin_stage(As, as, bar);
                 if (pt == 0) {
-                    mbar_expect_tx(bar, bbytes);
-                    tma_tile(As + kStageA, &M.zhl, ds.gblk * a.brows + ds.c0, 0, bar);
+                    S.sinfo[n % kStages] = StageInfo{r16 / 16, ds.kd, 0};
+                    mbar_expect_tx(bar, nz * bbytes);
+                    for (int z = 0; z < nz; ++z)
+                        tma_tile(As + kStageA + z * a.N * 128, &M.zhl, ds.gblk * a.brows + ds.c0 + z * 64, 0, bar);
                 }
-                // 64 k-rows x 2 atoms of 64 outputs: 1024 chunks of 16 B. Slots past the
-                // block's survivors repeat its last row (finite data against Z = 0: they
-                // add exact zeros).
+                // the stage's k-rows (to the next 16) x 2 atoms of 64 outputs, 16-B chunks;
+                // rows past the block's survivors repeat its last row (finite data against
+                // Z = 0: they add exact zeros)
 #pragma unroll 4
-                for (int q = pt; q < 1024; q += kProdThreads) {
+                for (int q = pt; q < r16 * 16; q += kProdThreads) {
                     const int r = q >> 4, atom = (q >> 3) & 1, jj = q & 7;
                     const int row = S.rows[min(ds.c0 + r, cnt - 1)];
                     const uint16_t* src = a.ud + static_cast<size_t>(row) * 2 * a.pitch_d + a.pitch_d + m0 +
                                           atom * 64 + jj * 8;
-                    cp16(as + atom * 8192 + (r >> 3) * 1024 + (r & 7) * 128 + ((jj ^ (r & 7)) << 4), src, pol);
+                    cp16(as + atom * ds.kd * 128 + (r >> 3) * 1024 + (r & 7) * 128 + ((jj ^ (r & 7)) << 4), src, pol);
                 }
                 end_gather_stage();
             }
+            // the terminating stage (no data) tells the MMA issuer the unit is complete
+            flush();
+            begin_stage(As, as, bar);
+            if (pt == 0) {
+                S.sinfo[n % kStages] = StageInfo{0, 64, 1};
+                mbar_arrive(bar);  // (the expect_tx arrival, with no bytes)
+            }
+            end_tile_stage(bar);
         }
+#ifdef SG_TC_FINTRACE
+        if (pt == 0) TC_TRACE(a, un.u, 2, ewait);
+        ewait = 0;
+#else
         if (pt == 0) TC_TRACE(a, un.u, 2, gtimer());
+#endif
     }
     flush();
 }
@@ -590,8 +663,10 @@ __device__ void mma_issuer(const TcArgs& a, TcSmem& S, uint8_t* stages) {
         if (uses[b] > 0) mbar_wait(&S.tempty[b], (tphase >> b) & 1u), tphase ^= 1u << b;
         uses[b]++;
     };
-    // one smem stage: nsub A sub-tiles x ksteps K steps of 16 into columns dcol (+ t * N)
-    auto run_stage = [&](int nsub, int ksteps, bool mn, uint32_t dcol, uint32_t id, bool first) {
+    // one smem stage: nsub A sub-tiles x ksteps K steps of 16 into columns dcol (+ t * N);
+    // kd = K rows of the stage's layout (MN-major A atoms of 64 outputs x kd rows, K-major
+    // B in kd / 64 atoms of 64 K)
+    auto run_stage = [&](int nsub, int ksteps, bool mn, uint32_t dcol, uint32_t id, bool first, int kd = 64) {
         mbar_wait(&S.full[stage], (fphase >> stage) & 1u);
         fphase ^= 1u << stage;
         tc_fence_after();
@@ -601,9 +676,10 @@ __device__ void mma_issuer(const TcArgs& a, TcSmem& S, uint8_t* stages) {
                 for (int k = 0; k < ksteps; ++k) {
                     // MN-major SW128: atoms of 64 outputs x 64 k-rows (8 KB); K-major SW128:
                     // rows of 128 B, 8-row groups of 1 KB
-                    const uint64_t ad = mn ? sdesc(As + t * 16384 + k * 2048, 8192, 1024)
+                    const uint64_t ad = mn ? sdesc(As + t * 16384 + k * 2048, kd * 128, 1024)
                                            : sdesc(As + t * 16384 + k * 32, 16, 1024);
-                    umma(dcol + t * a.N, ad, sdesc(Bs + k * 32, 16, 1024), id, (first && k == 0) ? 0u : 1u);
+                    const uint32_t bk = Bs + (k >> 2) * a.N * 128 + (k & 3) * 32;
+                    umma(dcol + t * a.N, ad, sdesc(bk, 16, 1024), id, (first && k == 0) ? 0u : 1u);
                 }
             umma_commit(&S.empty[stage]);
         }
@@ -630,32 +706,20 @@ __device__ void mma_issuer(const TcArgs& a, TcSmem& S, uint8_t* stages) {
                 for (int st = ngu; st < un.nst; ++st)  // pre = A T into columns 2N..3N
                     run_stage(1, 4, false, dcol + 2 * a.N, idesc(a.N, 0), st == ngu);
             } else {
-                // down: K steps of 16 Z slots, the range's stages as its blocks complete
-                DownWalk w = down_walk(a, un.b);
-                DownStage ds;
-                // the range's counts, three blocks per lane, one round of loads
-                int dv[3];
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const int blk = w.blk + q * 32 + lane;
-                    dv[q] = (blk < w.end && flag_ready(fl_gu(a, blk), 1)) ? __ldcg(a.vcnt + blk) : -1;
+                // down: the producer's stages in order, each with its K steps (StageInfo),
+                // until the terminating one
+                for (int st = 0;; ++st) {
+                    mbar_wait(&S.full[stage], (fphase >> stage) & 1u);
+                    const StageInfo si = S.sinfo[stage];
+                    if (si.last) {
+                        fphase ^= 1u << stage;
+                        if (lane == 0) mbar_arrive(&S.empty[stage]);
+                        __syncwarp();
+                        stage = (stage + 1) % kStages;
+                        break;
+                    }
+                    run_stage(1, si.ksteps, true, dcol, idesc(a.N, 1), st == 0, si.kd);
                 }
-                auto wait_blk = [&](int blk) {
-                    const int k = blk - range_lo(a, un.b);
-                    int v = -1;
-                    if (k < 96) {
-                        const int v0 = __shfl_sync(0xffffffffu, dv[0], k & 31), v1 = __shfl_sync(0xffffffffu, dv[1], k & 31),
-                                  v2 = __shfl_sync(0xffffffffu, dv[2], k & 31);
-                        v = k < 32 ? v0 : (k < 64 ? v1 : v2);
-                    }
-                    if (v < 0) {
-                        wait_count(fl_gu(a, blk), 1);
-                        v = __ldcg(a.vcnt + blk);
-                    }
-                    return v;
-                };
-                for (int st = 0; down_next(a, w, ds, wait_blk); ++st)
-                    run_stage(1, (ds.rows + 15) / 16, true, dcol, idesc(a.N, 1), st == 0);
             }
             if (lane == 0) {
                 umma_commit(&S.tfull[acc]);
@@ -965,7 +1029,7 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
             bool have;
             {  // did the range hold any survivor row (else the accumulator was never written)
                 int hv = 0;
-                for (int blk = range_lo(a, j) + et; blk < range_lo(a, j + 1); blk += 128)
+                for (int k = et, blk; (blk = range_block(a, j, k)) < a.nblk; k += 128)
                     hv |= vcnt_rows(__ldcg(a.vcnt + blk)) > 0;
                 have = epi_bar_or(hv);
             }
@@ -981,7 +1045,11 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                 st16(dst + c, v, min(16, nb - c));
             }
             release();
+#ifndef SG_TC_FINTRACE
             if (et == 0) TC_TRACE(a, un.u, 6, gtimer());
+#else
+            if (et == 0) TC_TRACE(a, un.u, 7, gtimer());
+#endif
             if (arrive_last(fl_down(a, i), a.S, S, et)) {
                 // y rows of d tile i: the S range partials in range order, 2 chunks of 8
                 // tokens per round of loads
@@ -1030,7 +1098,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     const int warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&S.full[s], kProdThreads + 1);  // the producer threads + the expect_tx
+            mbar_init(&S.full[s], kFullArrivals);
             mbar_init(&S.empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
@@ -1042,6 +1110,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
             mbar_init(&S.uqe[s], 2);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (threadIdx.x == 32) {  // warm the TMA descriptor cache with every map this CTA may use
+        const CUtensorMap* ms[] = {&maps.xhl, &maps.thl, &maps.zhl, &maps.Bp, &maps.A,
+                                   &maps.gate, &maps.up, &maps.down, &maps.down64};
+        for (const CUtensorMap* m : ms)
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
     }
     if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&S.tmem)));

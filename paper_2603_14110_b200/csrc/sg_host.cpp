@@ -856,6 +856,7 @@ int env_int(const char* name, int dflt) {
 
 constexpr int kTcBlk = 128;   // block capacity of the tensor-core kernel (rows of an M = 128 tile)
 constexpr int kTcSMax = 4;    // block ranges of the down units (the y finisher sums <= 4)
+constexpr int kTcChunk = 8;   // consecutive blocks per range interleave step (sg_batch_tc.cu kRangePair)
 constexpr int kTcKTMax = 4;   // K slices of the predictor's T units (the finisher sums <= 4)
 
 // blocks of a layer at most: one per SM, or D / 128 for very wide layers
@@ -928,17 +929,24 @@ std::vector<int> tc_schedule(const sg::TcArgs& a, int NX, int KT, int lag) {
         int code, ready_at;
     };
     std::vector<Item> downs;
-    auto range_lo = [&](int sr) { return sr * a.nblk / a.S; };
+    // range sr: chunks of kTcChunk blocks sr, sr + S, ... (sg_batch_tc.cu range_block); its last block
+    const int chunks = (a.nblk + kTcChunk - 1) / kTcChunk;
+    auto range_last = [&](int sr) {
+        if (sr >= chunks) return -1;
+        const int p = sr + (chunks - 1 - sr) / a.S * a.S;
+        return std::min(a.nblk - 1, kTcChunk * p + kTcChunk - 1);
+    };
     size_t di = 0;
     for (int b = 0; b < a.nblk; ++b) {
         while (di < downs.size() && downs[di].ready_at <= static_cast<int>(order.size()))
             order.push_back(downs[di++].code);
         order.push_back(code(GU, b, 0));
         for (int sr = 0; sr < a.S; ++sr)
-            if (b == range_lo(sr + 1) - 1)  // the range's last block
+            if (b == range_last(sr))
                 for (int dt = 0; dt < a.ndt; ++dt)
                     downs.push_back({code(DOWN, dt, sr), static_cast<int>(order.size()) + lag});
     }
+
     for (; di < downs.size(); ++di) order.push_back(downs[di].code);
     return order;
 }
@@ -964,13 +972,15 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     a.ndt = (a.pitch_d + 127) / 128;  // d tiles of 128 outputs (the down units' M)
     a.dense = dense;
     // a block's down rows stream whole once its survivors reach this density (per
-    // 1024; SG_TC_TILE_U): a row gather moves a fraction of the tile rate per SM
-    a.tile_u = env_int("SG_TC_TILE_U", 150);
+    // 1024; SG_TC_TILE_U): a row gather moves a fraction of the tile rate per SM (on
+    // B200 even a block with a sixth of its rows surviving streams faster whole), so by
+    // default every block with a survivor is tiled and only empty blocks are skipped
+    a.tile_u = env_int("SG_TC_TILE_U", 1);
     a.x = xs;
     a.y = ys;
     a.bias = L->view.bias;
     a.ud = L->view.ud;
-    a.S = std::max(1, std::min({env_int("SG_TC_S", 4), kTcSMax, a.nblk}));
+    a.S = std::max(1, std::min({env_int("SG_TC_S", 4), kTcSMax, (a.nblk + kTcChunk - 1) / kTcChunk}));  // each range: >= 1 chunk
     const int KT = dense ? 0 : k_slices(a.pitch_d, kTcKTMax);
     a.kst = KT ? a.pitch_d / KT : 0;
     // x -> X^T hi / lo: about 256 (token, 8-column) items per unit, so each epilogue

@@ -135,8 +135,16 @@ def balanced_order(load: np.ndarray, neurons: np.ndarray, G: int) -> np.ndarray:
 
 def upload(host: HostLayer, d, D, act, rank=256, device=0, shard_index=0, shard_count=1,
            balance=True, hot_rows=16):
+    """Device layer of a host layer. balance=True: the single-token executor's
+    per-CTA load-balanced neuron layout (balanced_order); "sorted": neurons by
+    decreasing calibration activity, so a batch's survivor rows gather into the
+    leading blocks and the trailing blocks' down rows are skipped whole
+    (csrc/sg_batch_tc.cu); False: ascending."""
     raw = dict(hidden=d, inter=D, rank=rank, activation=act, gate=host.gate, up=host.up,
                down_t=host.down_t, A=host.A, B=host.B, bias=host.bias)
+    if balance == "sorted" and host.load is not None:
+        raw["order"] = np.argsort(-host.load, kind="stable").astype(np.int64)
+        balance = False
     if balance and host.load is not None:
         import torch
         from .sharded import shard_indices

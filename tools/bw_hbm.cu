@@ -8,6 +8,12 @@
 //   mode 2: DOWN pattern on the interleaved [D][2*4096] up|down rows: boxes of 64 rows
 //           x 64 outputs (128 B of each 16-KB row), four per stage
 //   mode 3: DOWN pre-packed d-tile-major ([tile][D][128 outputs]): one 32-KB bulk copy
+//   mode 4: the batch kernel's DOWN units: CTA c < 128 streams d tile c % 32 (128
+//           outputs) over row range c / 32 of 4, 128-row stages (2 atoms x 2 boxes of
+//           64 rows), as the tcgen05 kernel does
+//   mode 5: as 4 with d tiles of 256 outputs (64 units of 4 atoms)
+//   mode 6: as 4, but the 32 units of a range start their row walk at staggered rows
+//           (no two SMs read the same rows at the same time)
 // Prints GB/s per mode and ring depth.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++17 tools/bw_hbm.cu -o tools/bw_hbm
 #include <cuda.h>
@@ -69,9 +75,42 @@ __global__ void __launch_bounds__(64, 1) stream(const __grid_constant__ Maps M, 
     __syncthreads();
     // work: mode 0/1: (128-row block, 64-K chunk) stages, both matrices; 2/3: (64-row
     // group, 256-output half-tile) stages
-    const int total = (mode < 2) ? (D / 256) * (K / 64) : (D / 64) * (K / 256);
+    int total = (mode < 2) ? (D / 256) * (K / 64) : (D / 64) * (K / 256);
+    if (mode >= 4) total = 0;
     int n = 0;
-    if (warp == 0 && lane == 0) {
+    if (mode >= 4) {  // unit-major DOWN streaming: rows of one range, one column slab
+        const bool stag = mode == 6;
+        if (mode == 6) mode = 4;
+        const int tiles = mode == 4 ? 32 : 16, atoms = mode == 4 ? 2 : 4;
+        const int c = blockIdx.x;
+        if (c < tiles * 4) {
+            const int dt = c % tiles, rg = c / tiles, rows = D / 4, r0 = rg * rows;
+            const int nstage = rows / (mode == 4 ? 128 : 64);
+            if (warp == 0 && lane == 0) {
+                for (int st0 = 0; st0 < nstage; ++st0, ++n) {
+                    const int st = stag ? (st0 + dt * nstage / tiles) % nstage : st0;
+                    const int s = n % nst;
+                    if (n >= nst) mbar_wait(&empty[s], ((n / nst) - 1) & 1);
+                    uint8_t* dst = sm + s * kStage;
+                    mbar_expect_tx(&full[s], kStage);
+                    for (int a = 0; a < atoms; ++a)
+                        for (int f = 0; f < (mode == 4 ? 2 : 1); ++f)
+                            tile(dst + a * (mode == 4 ? 16384 : 8192) + f * 8192, &M.down, dt * atoms * 64 + a * 64,
+                                 r0 + st * (mode == 4 ? 128 : 64) + f * 64, &full[s]);
+                }
+            } else if (warp == 1) {
+                unsigned long long acc = 0;
+                for (int st = 0; st < nstage; ++st, ++n) {
+                    const int s = n % nst;
+                    mbar_wait(&full[s], (n / nst) & 1);
+                    acc += sm[s * kStage + lane * 64];
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[s]);
+                }
+                if (lane == 0) atomicAdd(sink, acc);
+            }
+        }
+    } else if (warp == 0 && lane == 0) {
         for (int u = blockIdx.x; u < total; u += gridDim.x, ++n) {
             const int s = n % nst;
             if (n >= nst) mbar_wait(&empty[s], ((n / nst) - 1) & 1);
@@ -139,8 +178,9 @@ int main() {
     const int smem = kMaxStages * kStage + 1024;
     cudaFuncSetAttribute(stream, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const char* names[] = {"GU row-major 2x box{64,128}", "GU packed 2x bulk 16KB", "DOWN interleaved 4x box{64,64}",
-                           "DOWN packed bulk 32KB"};
-    for (int mode = 0; mode < 4; ++mode) {
+                           "DOWN packed bulk 32KB", "DOWN units 32 tiles x 4 ranges", "DOWN units 16 tiles x 4 ranges",
+                           "DOWN units staggered rows"};
+    for (int mode = 0; mode < 7; ++mode) {
         for (int nst : {4, 6}) {
             // modes 0/1 read gate+up halves (D/2 rows each x K) = mat bytes; 2/3 the down half of ud = mat
             cudaEvent_t a, b;
@@ -155,6 +195,7 @@ int main() {
             float ms = 0;
             cudaEventElapsedTime(&ms, a, b);
             const double bytes = double(it) * (mode < 2 ? (size_t(D) / 256) * (K / 64) : (size_t(D) / 64) * (K / 256)) * kStage;
+            // (modes 4/5 move the same bytes: every down row once)
             std::printf("%-32s stages %d: %8.1f GB/s  (%s)\n", names[mode], nst, bytes / (ms * 1e-3) / 1e9,
                         cudaGetErrorString(e));
         }
