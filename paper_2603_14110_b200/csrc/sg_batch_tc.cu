@@ -156,6 +156,17 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
+// 16 fp32 columns of this warp's TMEM lane quarter (call tmem_wait before use)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
 __device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 __device__ __forceinline__ bool epi_bar_or(int v) {  // epi_bar + OR of v over the epilogue threads
@@ -363,7 +374,7 @@ struct TcSmem {
     int cnt[64];         // epilogue: per-token counts
     int wsum[8];         // epilogue: per-quarter counts
     int last;            // epilogue: this unit was the last of its group (it reduces)
-    alignas(16) uint16_t zst[2][8][kBlk];  // epilogue: hi / lo of 8 tokens x 128 rows, staged
+    alignas(16) uint16_t zst[2][16][kBlk];  // epilogue: hi / lo of 16 tokens x 128 rows, staged
 };
 
 // ---- producer: claim, wait, load ---------------------------------------------
@@ -769,14 +780,15 @@ __device__ __forceinline__ bool arrive_last(int* p, int total, TcSmem& S, int et
     return S.last != 0;
 }
 
-// Store 8 tokens' hi / lo values of this thread's row `slot` (v[e] for token c + e;
-// slot < 0: none) — or, for `zslot`, exact zeros — into the K-major bf16 rows
-// dst[(c + e) * pitch + slot] (hi) and dst[(nb + c + e) * pitch + slot] (lo), slots
-// [0, nslots), through smem so the global stores are whole 16-B runs of 8 slots.
-__device__ __forceinline__ void store_hilo8(TcSmem& S, int et, const float* v, int slot, int zslot, uint16_t* dst,
-                                            size_t pitch, int nb, int c, int nslots) {
+// Store E (8 or 16) tokens' hi / lo values of this thread's row `slot` (v[e] for
+// token c + e; slot < 0: none) — or, for `zslot`, exact zeros — into the K-major bf16
+// rows dst[(c + e) * pitch + slot] (hi) and dst[(nb + c + e) * pitch + slot] (lo),
+// slots [0, nslots), through smem so the global stores are whole 16-B runs of 8 slots.
+template <int E>
+__device__ __forceinline__ void store_hilo(TcSmem& S, int et, const float* v, int slot, int zslot, uint16_t* dst,
+                                           size_t pitch, int nb, int c, int nslots) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < E; ++e) {
         uint16_t hi, lo;
         split_bf16(v[e], hi, lo);
         if (slot >= 0) S.zst[0][e][slot] = hi, S.zst[1][e][slot] = lo;
@@ -784,8 +796,8 @@ __device__ __forceinline__ void store_hilo8(TcSmem& S, int et, const float* v, i
     }
     epi_bar();
     const int chunks = nslots / 8;
-    for (int w = et; w < 16 * chunks; w += 128) {
-        const int row = w / chunks, ch = w % chunks, hl = row >> 3, e = row & 7;
+    for (int w = et; w < 2 * E * chunks; w += 128) {
+        const int row = w / chunks, ch = w % chunks, hl = row / E, e = row % E;
         const uint4 q = *reinterpret_cast<const uint4*>(&S.zst[hl][e][ch * 8]);
         *reinterpret_cast<uint4*>(dst + static_cast<size_t>(hl * nb + c + e) * pitch + ch * 8) = q;
     }
@@ -813,6 +825,9 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
         if (un.type == U_STOP) break;
         const int i = un.a, j = un.b;
         const bool mma_unit = un.type == U_T || un.type == U_GU || un.type == U_DOWN;
+        // (GU: the row's predictor bias, loaded while the MMAs run)
+        const int grow = un.a * a.brows + quarter * 32 + lane;
+        const float gbias = (un.type == U_GU && !a.dense && quarter * 32 + lane < un.cnt) ? __ldg(a.bias + grow) : 0.f;
         if (mma_unit) {
             wait_acc(un.acc);
             if (un.both) wait_acc(1);
@@ -917,7 +932,7 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                                     s[4] += q[k][1].x; s[5] += q[k][1].y; s[6] += q[k][1].z; s[7] += q[k][1].w;
                                 }
                         }
-                        store_hilo8(S, et, s, row0, -1, a.thl + t * 128, 256, nb, c, 128);
+                        store_hilo<8>(S, et, s, row0, -1, a.thl + t * 128, 256, nb, c, 128);
                     }
                 }
                 asm volatile("fence.proxy.async.global;" ::: "memory");  // T^T is read by TMA
@@ -932,7 +947,7 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
             const int cnt = un.cnt, k = row0;
             const bool mine = k < cnt;
             const int n = i * a.brows + k;
-            const float bias = (!a.dense && mine) ? __ldg(a.bias + n) : 0.f;
+            const float bias = gbias;
             const uint32_t tl = S.tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * 256);
             float z[64];
             uint64_t mb = 0, sbits = 0;
@@ -943,19 +958,13 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                 if (c >= nb) continue;  // uniform
                 // this chunk's g, u (and pre) hi + lo columns: all loads, one wait
                 float gh[16], gl[16], uh[16], ul[16], ph[16], pl[16];
-                tmem_ld8(tl + c, gh);
-                tmem_ld8(tl + c + 8, gh + 8);
-                tmem_ld8(tl + nb + c, gl);
-                tmem_ld8(tl + nb + c + 8, gl + 8);
-                tmem_ld8(tl + a.N + c, uh);
-                tmem_ld8(tl + a.N + c + 8, uh + 8);
-                tmem_ld8(tl + a.N + nb + c, ul);
-                tmem_ld8(tl + a.N + nb + c + 8, ul + 8);
+                tmem_ld16(tl + c, gh);
+                tmem_ld16(tl + nb + c, gl);
+                tmem_ld16(tl + a.N + c, uh);
+                tmem_ld16(tl + a.N + nb + c, ul);
                 if (!a.dense) {
-                    tmem_ld8(tl + 2 * a.N + c, ph);
-                    tmem_ld8(tl + 2 * a.N + c + 8, ph + 8);
-                    tmem_ld8(tl + 2 * a.N + nb + c, pl);
-                    tmem_ld8(tl + 2 * a.N + nb + c + 8, pl + 8);
+                    tmem_ld16(tl + 2 * a.N + c, ph);
+                    tmem_ld16(tl + 2 * a.N + nb + c, pl);
                 }
                 tmem_wait();
 #pragma unroll
@@ -1007,10 +1016,14 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                 if (k >= nv && k < pad_to) pslot = k;
             }
 #pragma unroll
-            for (int c = 0; c < 64; c += 8) {
+            for (int c = 0; c < 64; c += 16) {
                 if (c >= nb) continue;  // uniform
-                store_hilo8(S, et, z + c, zslot, pslot, a.zhl + static_cast<size_t>(i) * a.brows, a.zpitch, nb, c,
-                            pad_to);
+                if (c + 16 <= nb)
+                    store_hilo<16>(S, et, z + c, zslot, pslot, a.zhl + static_cast<size_t>(i) * a.brows, a.zpitch, nb,
+                                   c, pad_to);
+                else
+                    store_hilo<8>(S, et, z + c, zslot, pslot, a.zhl + static_cast<size_t>(i) * a.brows, a.zpitch, nb,
+                                  c, pad_to);
             }
 #ifdef SG_TC_FINTRACE
             epi_bar();
