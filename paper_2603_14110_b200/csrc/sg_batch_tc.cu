@@ -620,6 +620,7 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                 if (ds.c0 == 0) {  // a new gathered block: its survivor rows
                     cnt = w.g1;
                     prod_bar();  // the previous block's rows are no longer read
+                    SG_CHECK(cnt <= kBlk && ds.gblk < a.nblk);
                     for (int k = pt; k < cnt; k += kProdThreads)
                         S.rows[k] = ds.gblk * a.brows + __ldcg(a.vlist + ds.gblk * kBlk + k);
                     prod_bar();
@@ -639,6 +640,7 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                 for (int q = pt; q < r16 * 16; q += kProdThreads) {
                     const int r = q >> 4, atom = (q >> 3) & 1, jj = q & 7;
                     const int row = S.rows[min(ds.c0 + r, cnt - 1)];
+                    SG_CHECK(row >= 0 && row < a.D);
                     const uint16_t* src = a.ud + static_cast<size_t>(row) * 2 * a.pitch_d + a.pitch_d + m0 +
                                           atom * 64 + jj * 8;
                     cp16(as + atom * ds.kd * 128 + (r >> 3) * 1024 + (r & 7) * 128 + ((jj ^ (r & 7)) << 4), src, pol);
@@ -799,6 +801,7 @@ __device__ __forceinline__ void store_hilo(TcSmem& S, int et, const float* v, in
     for (int w = et; w < 2 * E * chunks; w += 128) {
         const int row = w / chunks, ch = w % chunks, hl = row / E, e = row % E;
         const uint4 q = *reinterpret_cast<const uint4*>(&S.zst[hl][e][ch * 8]);
+        SG_CHECK(ch * 8 + 8 <= kBlk && hl * nb + c + e < 2 * nb);
         *reinterpret_cast<uint4*>(dst + static_cast<size_t>(hl * nb + c + e) * pitch + ch * 8) = q;
     }
     epi_bar();
@@ -983,6 +986,7 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
 #endif
             mb = mine ? (mb & bmask) : 0ull;
             sbits = mine ? (sbits & bmask) : 0ull;
+            SG_CHECK(!mine || n < a.D);
             if (mine) {
                 a.vbits[n] = sbits;
                 if (!a.dense) a.mbits[n] = mb;
@@ -1004,6 +1008,7 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
             // slots up to the next 16 are exact zeros either way
             const bool dtile = nv > 0 && down_tiled(a, nv, i);
             const int pad_to = dtile ? (cnt + 15) / 16 * 16 : (nv + 15) / 16 * 16;
+            SG_CHECK(static_cast<size_t>(i) * a.brows + pad_to <= static_cast<size_t>(a.zpitch));
             int zslot = -1, pslot = -1;
             if (dtile) {
                 if (mine) zslot = k;
@@ -1011,6 +1016,7 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
             } else {
                 if (keep) {
                     zslot = slot_c;
+                    SG_CHECK(slot_c < cnt && i < a.nblk);
                     a.vlist[i * kBlk + slot_c] = k;
                 }
                 if (k >= nv && k < pad_to) pslot = k;
@@ -1090,6 +1096,7 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                                 y[0] += q[r][h][0].x; y[1] += q[r][h][0].y; y[2] += q[r][h][0].z; y[3] += q[r][h][0].w;
                                 y[4] += q[r][h][1].x; y[5] += q[r][h][1].y; y[6] += q[r][h][1].z; y[7] += q[r][h][1].w;
                             }
+                        SG_CHECK(m < a.d);
 #pragma unroll
                         for (int e = 0; e < 8; ++e)
                             if (c + e < a.B) a.y[static_cast<size_t>(c + e) * a.d + m] = y[e];

@@ -2,6 +2,8 @@
 // code (sg_kernels.cu). Not part of the public ABI (include/sparsegate_c.h).
 #pragma once
 
+#include <cstdio>  // (device printf of the bounds-checked build)
+
 #include <cuda.h>
 
 #include <cstdint>
@@ -33,6 +35,25 @@ struct LayerView {
 
 // Per-context device workspace (one per stream). Sizes are bounded by the
 // ctx's max_inter (Dmax), max_hidden (pitch) and the SM count (G).
+// Bounds checks of the device paths' computed global indices (row gathers, list and
+// output writes): compiled in only for the checked variant (make checked ->
+// libsparsegate_b200_checked.so, SG_LIB=checked), where a violation prints its
+// site and traps — the stand-in for compute-sanitizer, which this GPU pool bars.
+#ifdef SG_BOUNDS_CHECK
+#define SG_CHECK(cond)                                                                   \
+    do {                                                                                 \
+        if (!(cond)) {                                                                   \
+            printf("SG_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, \
+                   __LINE__, static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x)); \
+            asm volatile("trap;");                                                       \
+        }                                                                                \
+    } while (0)
+#else
+#define SG_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
+
 struct WorkView {
     const float* x;       // [d] input (caller's device buffer)
     const float* xres;    // optional [d] added to x while it is staged (residual chains), or null

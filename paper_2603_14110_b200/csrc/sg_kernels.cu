@@ -766,6 +766,7 @@ __device__ void phase_mask(const LayerView& L, const WorkView& W, const Smem& sm
             const unsigned b = __ballot_sync(0xffffffffu, on);
             const unsigned bi = __ballot_sync(0xffffffffu, on && k >= hpre);
             const unsigned below = (1u << lane) - 1u;
+            SG_CHECK(!on || (n0 + run + __popc(b & below) < L.D && n0 + k < L.D));
             if (on) W.plist[n0 + run + __popc(b & below)] = n0 + k;
             if (k < hpre) sm.items[k] = n0 + k;
             if (on && k >= hpre) sm.items[irun + __popc(bi & below)] = n0 + k;
@@ -909,6 +910,7 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
             for (int j = slot; j < nitems; j += ns) {
                 if (j < hpre) continue;
                 const int n = kPipe == 0 ? n0 + j : sm.items[j];
+                SG_CHECK(n >= 0 && n < L.D);
                 const uint32_t use = u0 + static_cast<uint32_t>(j / ns);
                 if (use > 0) mbar_wait(sm.empty + slot, (use - 1) & 1u);
                 sm.slotn[slot] = n;
@@ -978,6 +980,7 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
                 const float u = res[2 * h + 1];
                 const int nn = n[h];
                 if (kPipe == 0) {
+                    SG_CHECK(gt != 0 || (nn >= 0 && nn < L.D));
                     if (gt == 0) W.zD[nn] = gated(g, u, L.act);
                     continue;
                 }
@@ -1020,6 +1023,7 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
                 const unsigned b = __ballot_sync(0xffffffffu, on);
                 if (on) {
                     const int dst = run + __popc(b & ((1u << lane) - 1u));
+                    SG_CHECK(n0 + dst < L.D);
                     list[dst] = rr;
                     reinterpret_cast<int2*>(W.vseg)[n0 + dst] = rr;
                 }
@@ -1088,6 +1092,7 @@ __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkVi
         uint64_t* bar = sm.full + kMaxSlots - 2 + (g & 1);
         if (lane == 0) mbar_expect_tx(bar, static_cast<uint32_t>(m) * ud_bytes);
         __syncwarp();
+        SG_CHECK(lane >= m || (sm.svl[r0 + lane].x >= 0 && sm.svl[r0 + lane].x < L.D));
         if (lane < m)
             bulk_g2s(sm.big + static_cast<size_t>((g & 1) * half + lane) * ud_bytes,
                      L.ud + static_cast<size_t>(sm.svl[r0 + lane].x) * 2 * L.pitch_d, ud_bytes, bar,
@@ -1140,6 +1145,7 @@ __device__ __forceinline__ void survivor_updown(const LayerView& L, const WorkVi
             const float z = gated(__int_as_float(e.y), u, L.act);
             zs[tid] = z;
             e.y = __float_as_int(z);
+            SG_CHECK(n0 + r0 + tid < L.D);
             reinterpret_cast<int2*>(W.vseg)[n0 + r0 + tid] = e;
         }
         __syncthreads();  // zs complete
@@ -1269,6 +1275,7 @@ __device__ __noinline__ void write_index_sets(int gbase, int gstride, const int*
     const int cntP = __ldcg(cnt + c * kSector);
     for (int k = lane; k < cntP; k += 32) {
         const int n = __ldcg(plist + n0 + k);
+        SG_CHECK(n >= 0 && n < D && mineP + k < D);
         P[mineP + k] = gidx ? __ldg(gidx + n) : gbase + n * gstride;
         gP[mineP + k] = __ldcg(gN + n);
     }
@@ -1276,6 +1283,7 @@ __device__ __noinline__ void write_index_sets(int gbase, int gstride, const int*
     const int2* seg = reinterpret_cast<const int2*>(vseg_raw) + n0;
     for (int k = lane; k < cntV; k += 32) {
         const int2 e = __ldcg(seg + k);
+        SG_CHECK(e.x >= 0 && e.x < D && mineV + k < D);
         V[mineV + k] = gidx ? __ldg(gidx + e.x) : gbase + e.x * gstride;
         zV[mineV + k] = __int_as_float(e.y);
     }
@@ -1342,6 +1350,7 @@ __device__ void phase_down(const LayerView& L, const WorkView& W, const Smem& sm
         if (tid < ncols) {
             float s = 0.f;
             for (int grp = 0; grp < ngrp; ++grp) s += part[grp * ncols + tid];
+            SG_CHECK(c0 + tid < L.d);
             y[c0 + tid] = s;
             if (publish) st_tagged(W.ytag + 2 * (c0 + tid), s, ytag);
         }
