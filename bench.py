@@ -295,14 +295,30 @@ def run_batch(args, cfg, host, layers, ctx, world, rank, local):
     Y = torch.zeros_like(X)
     stream = torch.cuda.Stream()
 
-    def step(sh, fn=lib.sg_ffn_forward_batch):
+    chain = args.chain
+
+    def layer_io(l):
+        """(x, residual) device pointers of layer l under the bench's chain mode:
+        0 independent batches, 1 x_{l+1} = y_l, 2 x_{l+1} = h_{l+1} + y_l."""
+        if l == 0 or chain == 0:
+            return X[l].data_ptr(), None
+        if chain == 1:
+            return Y[l - 1].data_ptr(), None
+        return X[l].data_ptr(), Y[l - 1].data_ptr()
+
+    def call(l, sh, dense=0):
+        x, res = layer_io(l)
+        check(lib.sg_ffn_forward_batch_res(ctx.handle, layers[l].handle, C.c_void_p(x),
+                                           C.c_void_p(res) if res else None, B,
+                                           C.c_void_p(Y[l].data_ptr()), dense, C.c_void_p(sh)))
+
+    def step(sh, dense=0):
         for l in range(L):
-            check(fn(ctx.handle, layers[l].handle, C.c_void_p(X[l].data_ptr()), B,
-                     C.c_void_p(Y[l].data_ptr()), C.c_void_p(sh)))
+            call(l, sh, dense)
 
     with torch.cuda.stream(stream):
         step(stream.cuda_stream)  # workspaces / attributes / tensor maps before capture
-        step(stream.cuda_stream, lib.sg_ffn_forward_batch_dense)
+        step(stream.cuda_stream, 1)
     torch.cuda.synchronize()
     # union sizes per layer (roofline bytes), re-run un-captured
     pb = np.zeros(layers[0].local_inter, dtype=np.uint64)
@@ -310,21 +326,20 @@ def run_batch(args, cfg, host, layers, ctx, world, rank, local):
     up, uv = [], []
     stats = (capi.sg_exec_stats * B)()
     for l in range(L):
-        check(lib.sg_ffn_forward_batch(ctx.handle, layers[l].handle, C.c_void_p(X[l].data_ptr()), B,
-                                       C.c_void_p(Y[l].data_ptr()), C.c_void_p(stream.cuda_stream)))
+        call(l, stream.cuda_stream)
         check(lib.sg_ctx_read_batch(ctx.handle, C.c_void_p(stream.cuda_stream), B, stats,
                                     pb.ctypes.data_as(C.c_void_p), vb.ctypes.data_as(C.c_void_p)))
         up.append(int((pb != 0).sum()))
         uv.append(int((vb != 0).sum()))
 
-    def graph_of(fn):
+    def graph_of(dense):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
-            step(torch.cuda.current_stream().cuda_stream, fn)
+            step(torch.cuda.current_stream().cuda_stream, dense)
         return g
 
-    graph = graph_of(lib.sg_ffn_forward_batch)
-    dgraph = graph_of(lib.sg_ffn_forward_batch_dense)
+    graph = graph_of(0)
+    dgraph = graph_of(1)
 
     def timed(g, K, W, clocks=False):
         for _ in range(W):
@@ -388,7 +403,7 @@ def run_batch(args, cfg, host, layers, ctx, world, rank, local):
         "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                      "frac": alg / (ms * 1e-3) / 1e9 / hbm, "peak_kind": hbm_kind, "traffic": None,
                      "bytes_per_step": alg,
-                     "kernel": "tc_kernel (csrc/sg_batch_tc.cu: tcgen05.mma + TMEM, TMA gather4)"
+                     "kernel": "tc_kernel (csrc/sg_batch_tc.cu: tcgen05.mma + TMEM, TMA tiles)"
                                if B > 1 else "ffn_kernel<2> (persistent single-token executor)"},
         "dense": {"ms_per_step": ms_dense, "tokens_per_s": B * 1000.0 / ms_dense,
                   "per_layer_us": ms_dense * 1000.0 / L,

@@ -865,14 +865,22 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                     const int b = w / nch, k0 = (w % nch) * 8;
                     if (w < w1 && b < a.B && vec && k0 < a.d) {
                         const float4* src = reinterpret_cast<const float4*>(a.x + static_cast<size_t>(b) * a.d + k0);
-                        const float4 f0 = __ldg(src), f1 = __ldg(src + 1);
+                        float4 f0 = __ldg(src), f1 = __ldg(src + 1);
+                        if (a.xres) {  // residual input: x = h + r, summed in fp32 before the split
+                            const float4* rs = reinterpret_cast<const float4*>(a.xres + static_cast<size_t>(b) * a.d + k0);
+                            const float4 r0 = __ldcg(rs), r1 = __ldcg(rs + 1);
+                            f0.x += r0.x; f0.y += r0.y; f0.z += r0.z; f0.w += r0.w;
+                            f1.x += r1.x; f1.y += r1.y; f1.z += r1.z; f1.w += r1.w;
+                        }
                         v[h][0] = f0.x; v[h][1] = f0.y; v[h][2] = f0.z; v[h][3] = f0.w;
                         v[h][4] = f1.x; v[h][5] = f1.y; v[h][6] = f1.z; v[h][7] = f1.w;
                     } else {
 #pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            v[h][e] = (w < w1 && b < a.B && k0 + e < a.d) ? __ldg(a.x + static_cast<size_t>(b) * a.d + k0 + e)
-                                                                        : 0.f;
+                        for (int e = 0; e < 8; ++e) {
+                            const bool in = w < w1 && b < a.B && k0 + e < a.d;
+                            const size_t o = static_cast<size_t>(b) * a.d + k0 + e;
+                            v[h][e] = in ? __ldg(a.x + o) + (a.xres ? __ldcg(a.xres + o) : 0.f) : 0.f;
+                        }
                     }
                 }
 #pragma unroll

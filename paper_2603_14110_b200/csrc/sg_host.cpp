@@ -953,7 +953,7 @@ std::vector<int> tc_schedule(const sg::TcArgs& a, int NX, int KT, int lag) {
 
 // One tensor-core launch: B tokens through one layer (dense != 0: every row, no predictor).
 sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float* ys, void* stream,
-                     int dense) {
+                     int dense, const float* xres = nullptr) {
     if (sg_status s = tc_workspace(C); s != SG_OK) return s;
     sg::TcArgs a = C->tw;
     a.B = B;
@@ -977,6 +977,7 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     // default every block with a survivor is tiled and only empty blocks are skipped
     a.tile_u = env_int("SG_TC_TILE_U", 1);
     a.x = xs;
+    a.xres = xres;
     a.y = ys;
     a.bias = L->view.bias;
     a.ud = L->view.ud;
@@ -1130,6 +1131,26 @@ sg_status sg_ffn_forward_batch_dense(sg_ctx* C, const sg_layer* L, const float* 
     C->blast_B = batch;
     C->blast_stack = false;
     C->blast_path = 3;
+    return SG_OK;
+}
+
+sg_status sg_ffn_forward_batch_res(sg_ctx* C, const sg_layer* L, const float* xs, const float* xres,
+                                   int32_t batch, float* ys, int32_t dense, void* stream) {
+    if (xres == nullptr)
+        return dense ? sg_ffn_forward_batch_dense(C, L, xs, batch, ys, stream)
+                     : sg_ffn_forward_batch(C, L, xs, batch, ys, stream);
+    if (sg_status s = check_pair(C, L); s != SG_OK) return s;
+    if (!L->has_w || !L->has_tcmaps || (!dense && !L->has_pred) || L->r > 256 || L->d > 8192)
+        return fail(SG_ERR_USAGE, "residual batched decode runs on the tensor-core path only");
+    if (batch < 1 || batch > 64) return fail(SG_ERR_USAGE, "batch must be in [1, 64]");
+    if (xs == nullptr || ys == nullptr) return fail(SG_ERR_USAGE, "null buffers");
+    if (sg_status s = batch_workspace(C); s != SG_OK) return s;
+    DeviceGuard dg(C->device);
+    if (sg_status s = tc_forward(C, L, xs, batch, ys, stream, dense ? 1 : 0, xres); s != SG_OK) return s;
+    C->blast = L;
+    C->blast_B = batch;
+    C->blast_stack = false;
+    C->blast_path = dense ? 3 : 2;
     return SG_OK;
 }
 

@@ -180,6 +180,7 @@ struct TcArgs {
     int zpitch;            // slots of Z^T per row (block capacity 128 x blocks)
     int xpitch;            // elements per X^T row (the ctx's max pitch)
     const float* x;        // [B][d] input tokens
+    const float* xres;     // optional [B][d] added to x while it is split (residual chains)
     float* y;              // [B][d] outputs
     const float* bias;     // [D]
     const uint16_t* ud;    // [D][2*pitch_d]    [up | down] rows (down rows gathered by cp.async)

@@ -128,3 +128,34 @@ def test_batch_device_entry_flags_nonfinite():
                                               C.c_void_p(Y.data_ptr()), C.c_void_p(sh)))
         with pytest.raises(DataError):
             check(capi.lib().sg_ctx_read_batch(ctx.handle, C.c_void_p(sh), B, None, None, None))
+
+
+@pytest.mark.parametrize("dense", [0, 1])
+def test_batch_residual_input_equals_summed_input(dense):
+    """sg_ffn_forward_batch_res (x_b = h_b + r_b formed inside the launch, the residual
+    chain of the batched bench) gives exactly the result of the same call on the
+    fp32 sums."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2603_14110_b200 import _capi as capi
+    from paper_2603_14110_b200.ffn_exec import Context, check
+
+    d, D, r, B = 512, 2048, 64, 12
+    fx, pred = _calibrated_layer(d, D, r, seed=5, calib=1024)
+    layer = DeviceLayer(fx.weights, pred)
+    rng = np.random.default_rng(3)
+    H = torch.tensor(fx.eval[:, rng.integers(0, fx.eval.shape[1], B)].T.copy(), dtype=torch.float32, device="cuda")
+    R = torch.tensor(0.1 * rng.standard_normal((B, d)), dtype=torch.float32, device="cuda")
+    S = (H + R).contiguous()
+    ctx = Context(0, d, D, r)
+    lib = capi.lib()
+    Y1, Y2 = torch.zeros_like(H), torch.zeros_like(H)
+    check(lib.sg_ffn_forward_batch_res(ctx.handle, layer.handle, C.c_void_p(H.data_ptr()),
+                                       C.c_void_p(R.data_ptr()), B, C.c_void_p(Y1.data_ptr()), dense, None))
+    check(lib.sg_ffn_forward_batch_res(ctx.handle, layer.handle, C.c_void_p(S.data_ptr()), None, B,
+                                       C.c_void_p(Y2.data_ptr()), dense, None))
+    torch.cuda.synchronize()
+    assert torch.equal(Y1, Y2)
+    assert float(Y1.abs().sum()) > 0
