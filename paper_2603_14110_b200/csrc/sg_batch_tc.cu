@@ -47,6 +47,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 namespace sg {
 namespace {
@@ -1155,6 +1156,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     // the producer waits on empty[] before every stage: pre-arrive the first round
     if (threadIdx.x == 0)
         for (int s = 0; s < kStages; ++s) mbar_arrive(&S.empty[s]);
+    // (programmatic dependent launch: everything above overlapped the previous launch's
+    // tail; from here on the previous launch's outputs and counters are read)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     if (warp < kMmaWarp) {
         producer(a, maps, S, stages);
@@ -1166,13 +1170,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" :::);
     if (warp == kMmaWarp) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(S.tmem));
     if (threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(fl_exit(a), 1) == static_cast<int>(gridDim.x) - 1) {
-            // last CTA out: every other CTA has finished; reset the dataflow counters
+            // last CTA out: every other CTA has finished; reset the dataflow counters and
+            // publish the non-finite flag (read by sg_ctx_read_batch), zero for the next
             __threadfence();
             for (int k = 0; k < flag_count(a); ++k) a.flags[k] = 0;
+            a.bad[1] = __ldcg(a.bad);
+            a.bad[0] = 0;
             __threadfence();
         }
     }
@@ -1194,7 +1202,23 @@ int launch_batch_tc(const TcMaps& maps, const TcArgs& a, int grid, void* stream)
     const int smem = tc_smem_bytes();
     const int e = ensure_smem_attr(reinterpret_cast<const void*>(tc_kernel), smem);
     if (e) return e;
-    tc_kernel<<<grid, kTcThreads, smem, static_cast<cudaStream_t>(stream)>>>(maps, a);
+    // programmatic dependent launch (SG_TC_PDL=0 disables): the next launch on the
+    // stream sets up its CTAs while this one drains
+    static const bool pdl = [] {
+        const char* e = std::getenv("SG_TC_PDL");
+        return e == nullptr || std::atoi(e) != 0;
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, tc_kernel, maps, a);
     return static_cast<int>(cudaGetLastError());
 }
 

@@ -877,7 +877,7 @@ sg_status tc_workspace(sg_ctx* C) {
     const size_t o_x = take(128 * pd * 2), o_tp = take(kTcKTMax * 256 * 64 * 4), o_th = take(128 * 256 * 2),
                  o_mb = take(Dm * 8), o_vb = take(Dm * 8), o_vl = take(nblk * kTcBlk * 4), o_vc = take(nblk * 4),
                  o_z = take(128 * nblk * kTcBlk * 2), o_y = take(kTcSMax * ndt * 128 * 64 * 4),
-                 o_cnt = take((64 + 64 + 1) * 4),
+                 o_cnt = take((64 + 64 + 2) * 4),
                  o_fl = take(static_cast<size_t>(sg::tc_flag_ints(static_cast<int>(nblk), static_cast<int>(ndt))) * 4);
     DeviceGuard dg(C->device);
     cudaError_t e = cudaMalloc(&C->tmem_ws, off);
@@ -1026,9 +1026,10 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     maps.xhl = it->second.xhl;
     maps.thl = it->second.thl;
     maps.zhl = it->second.zhl;
-    auto st = static_cast<cudaStream_t>(stream);
     DeviceGuard dg(C->device);
-    SG_CUDA(cudaMemsetAsync(a.pcount, 0, (64 + 64 + 1) * sizeof(int), st));
+    // (no memset between launches: a graph node between two launches would cut their
+    // programmatic dependent launch; the kernel's last CTA publishes and re-zeroes the
+    // non-finite flag itself)
     const int e = sg::launch_batch_tc(maps, a, C->G, stream);
     if (e != 0) return fail(SG_ERR_CUDA, std::string("tensor-core batch launch: ") +
                                              cudaGetErrorString(static_cast<cudaError_t>(e)));
@@ -1208,7 +1209,7 @@ sg_status sg_ctx_read_batch(sg_ctx* C, void* stream, int32_t batch, sg_exec_stat
         // tensor-core path: the per-token counts are the bit columns' popcounts (the
         // kernel keeps only the bits)
         int flag = 0;
-        SG_CUDA(cudaMemcpy(&flag, C->tw.bad, sizeof(int), cudaMemcpyDeviceToHost));
+        SG_CUDA(cudaMemcpy(&flag, C->tw.bad + 1, sizeof(int), cudaMemcpyDeviceToHost));  // published copy
         bad = flag != 0;
         std::vector<uint64_t> mb(static_cast<size_t>(L->D_local)), vb(static_cast<size_t>(L->D_local));
         if (C->blast_path == 2)

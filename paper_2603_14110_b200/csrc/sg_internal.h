@@ -195,7 +195,8 @@ struct TcArgs {
     float* ypart;          // [S][ndt*128][nb]
     int* pcount;           // [64] |P_b|   (pcount, vcount, bad: zeroed by the host per call)
     int* vcount;           // [64] |V_b|
-    int* bad;              // non-finite input flag
+    int* bad;              // [2] non-finite input flag of the running launch; [1] = that of the
+                           //   last completed launch (copied and re-zeroed by its last CTA)
     int* flags;            // dataflow counters, reset by the last CTA of every launch
 };
 int tc_smem_bytes();
