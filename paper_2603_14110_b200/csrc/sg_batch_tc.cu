@@ -65,7 +65,7 @@ constexpr int kUQ = 4;            // unit queue depth (producer lead)
 constexpr int kBlk = 128;         // neurons per block at most (one M = 128 tile)
 constexpr int kTRows = 256;       // predictor rows (rank <= 256: two M = 128 tiles)
 
-enum UnitType : int { U_STOP = 0, U_X, U_T, U_GU, U_DOWN };
+enum UnitType : int { U_STOP = 0, U_X, U_T, U_GU, U_DOWN, U_PF };
 
 struct Unit {
     int type;
@@ -111,12 +111,20 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t par) {
         : "memory");
     return ok != 0;
 }
-__device__ __forceinline__ void tma_tile(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* bar) {
+// TMA tile with an L2 policy: weight tiles are read once per launch (evict-first), the
+// X^T / T^T / Z^T operand tiles are re-read by every block / d tile (evict-last)
+__device__ __forceinline__ void tma_tile_ef(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* bar,
+                                            uint64_t pol) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            su32(dst)),
-        "l"(m), "r"(c0), "r"(c1), "r"(su32(bar))
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(su32(dst)),
+        "l"(m), "r"(c0), "r"(c1), "r"(su32(bar)), "l"(pol)
         : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
@@ -407,7 +415,7 @@ __device__ __forceinline__ void unit_inputs_wait(const TcArgs& a, int type, int 
 
 __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* stages) {
     const int pt = threadIdx.x;  // 0..95
-    const uint64_t pol = policy_evict_first();
+    const uint64_t pol = policy_evict_first(), pol_last = policy_evict_last();
     const uint32_t bbytes = static_cast<uint32_t>(a.N) * 128u;
     const uint32_t abytes = static_cast<uint32_t>(a.brows) * 128u;  // one block's rows x 64 K
     const uint32_t sbase = su32(stages);
@@ -518,6 +526,22 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
         }
         ++seq;
         if (type == U_STOP) break;
+        if (type == U_PF) {
+            // the NEXT layer's gate and up rows, the leading pf_bytes of each, into L2
+            // while this layer's down units stream (HBM has headroom then): its GU units
+            // find that share of their weights in L2. Slice i of the next layer's rows.
+            const int nrows = a.pf_D, n0 = static_cast<int>(static_cast<int64_t>(i) * nrows / a.pf_units),
+                      n1 = static_cast<int>(static_cast<int64_t>(i + 1) * nrows / a.pf_units);
+            for (int q = n0 * 2 + pt; q < n1 * 2; q += kProdThreads) {
+                const int n = q >> 1;
+                const uint16_t* src = (q & 1) ? a.pf_ud + static_cast<size_t>(n) * 2 * a.pf_pitch
+                                              : a.pf_gate + static_cast<size_t>(n) * a.pf_pitch;
+                asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src),
+                             "r"(a.pf_bytes), "l"(pol_last)
+                             : "memory");
+            }
+            continue;
+        }
         if (!mma_unit) continue;
 
         uint8_t* As;
@@ -530,8 +554,8 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                 begin_stage(As, as, bar);
                 if (pt == 0) {
                     mbar_expect_tx(bar, un.nsub * 16384u + bbytes);
-                    for (int t = 0; t < un.nsub; ++t) tma_tile(As + t * 16384, &M.Bp, k0 + st * 64, t * 128, bar);
-                    tma_tile(As + kStageA, &M.xhl, k0 + st * 64, 0, bar);
+                    for (int t = 0; t < un.nsub; ++t) tma_tile_ef(As + t * 16384, &M.Bp, k0 + st * 64, t * 128, bar, pol);
+                    tma_tile_ef(As + kStageA, &M.xhl, k0 + st * 64, 0, bar, pol_last);
                 }
                 end_tile_stage(bar);
             }
@@ -544,9 +568,9 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                 begin_stage(As, as, bar);
                 if (pt == 0) {
                     mbar_expect_tx(bar, 2u * abytes + bbytes);
-                    tma_tile(As, &M.gate, st * 64, r0, bar);
-                    tma_tile(As + 16384, &M.up, st * 64, r0, bar);
-                    tma_tile(As + kStageA, &M.xhl, st * 64, 0, bar);
+                    tma_tile_ef(As, &M.gate, st * 64, r0, bar, pol);
+                    tma_tile_ef(As + 16384, &M.up, st * 64, r0, bar, pol);
+                    tma_tile_ef(As + kStageA, &M.xhl, st * 64, 0, bar, pol_last);
                 }
                 end_tile_stage(bar);
             }
@@ -556,8 +580,8 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                     begin_stage(As, as, bar);
                     if (pt == 0) {
                         mbar_expect_tx(bar, abytes + bbytes);
-                        tma_tile(As, &M.A, st * 64, r0, bar);
-                        tma_tile(As + kStageA, &M.thl, st * 64, 0, bar);
+                        tma_tile_ef(As, &M.A, st * 64, r0, bar, pol);
+                        tma_tile_ef(As + kStageA, &M.thl, st * 64, 0, bar, pol_last);
                     }
                     end_tile_stage(bar);
                 }
@@ -607,13 +631,13 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                         for (int atom = 0; atom < 2; ++atom) {
                             uint8_t* dst = As + atom * ds.kd * 128;
                             for (int f = 0; f < full; ++f)
-                                tma_tile(dst + f * 8192, &M.down64, m0 + atom * 64, ds.row0 + f * 64, bar);
+                                tma_tile_ef(dst + f * 8192, &M.down64, m0 + atom * 64, ds.row0 + f * 64, bar, pol);
                             for (int q = 0; q < nbox; ++q)
-                                tma_tile(dst + full * 8192 + q * 2048, &M.down, m0 + atom * 64,
-                                         ds.row0 + full * 64 + q * 16, bar);
+                                tma_tile_ef(dst + full * 8192 + q * 2048, &M.down, m0 + atom * 64,
+                                            ds.row0 + full * 64 + q * 16, bar, pol);
                         }
                         for (int z = 0; z < nz; ++z)
-                            tma_tile(As + kStageA + z * a.N * 128, &M.zhl, ds.row0 + z * 64, 0, bar);
+                            tma_tile_ef(As + kStageA + z * a.N * 128, &M.zhl, ds.row0 + z * 64, 0, bar, pol_last);
                     }
                     end_tile_stage(bar);
                     continue;
@@ -632,7 +656,8 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                     S.sinfo[n % kStages] = StageInfo{r16 / 16, ds.kd, 0};
                     mbar_expect_tx(bar, nz * bbytes);
                     for (int z = 0; z < nz; ++z)
-                        tma_tile(As + kStageA + z * a.N * 128, &M.zhl, ds.gblk * a.brows + ds.c0 + z * 64, 0, bar);
+                        tma_tile_ef(As + kStageA + z * a.N * 128, &M.zhl, ds.gblk * a.brows + ds.c0 + z * 64, 0, bar,
+                                    pol_last);
                 }
                 // the stage's k-rows (to the next 16) x 2 atoms of 64 outputs, 16-B chunks;
                 // rows past the block's survivors repeat its last row (finite data against

@@ -919,9 +919,9 @@ int k_slices(int pitch, int want) {
 // after the range's last GU block (about one wave of the grid: by then the range's
 // blocks are streaming in), so no unit waits for a whole previous phase.
 // Topological by construction.
-std::vector<int> tc_schedule(const sg::TcArgs& a, int NX, int KT, int lag) {
+std::vector<int> tc_schedule(const sg::TcArgs& a, int NX, int KT, int lag, int NPF) {
     auto code = [](int t, int i, int j) { return (t << 24) | (i << 8) | j; };
-    enum { X = 1, T, GU, DOWN };  // sg_batch_tc.cu UnitType
+    enum { X = 1, T, GU, DOWN, PF };  // sg_batch_tc.cu UnitType
     std::vector<int> order;
     for (int k = 0; k < NX; ++k) order.push_back(code(X, k, 0));
     for (int k = 0; k < KT; ++k) order.push_back(code(T, k, 0));
@@ -948,12 +948,13 @@ std::vector<int> tc_schedule(const sg::TcArgs& a, int NX, int KT, int lag) {
     }
 
     for (; di < downs.size(); ++di) order.push_back(downs[di].code);
+    for (int k = 0; k < NPF; ++k) order.push_back(code(PF, k, 0));  // claimed by SMs without down work
     return order;
 }
 
 // One tensor-core launch: B tokens through one layer (dense != 0: every row, no predictor).
 sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float* ys, void* stream,
-                     int dense, const float* xres = nullptr) {
+                     int dense, const float* xres = nullptr, const sg_layer* next = nullptr) {
     if (sg_status s = tc_workspace(C); s != SG_OK) return s;
     sg::TcArgs a = C->tw;
     a.B = B;
@@ -990,13 +991,22 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     a.u_T = NX;
     a.u_GU = a.u_T + KT;
     a.u_DOWN = a.u_GU + a.nblk;
-    a.u_end = a.u_DOWN + a.ndt * a.S;
+    // L2 prefetch of the next layer's gate / up rows (their leading SG_TC_PF eighths)
+    const int pf8 = env_int("SG_TC_PF", 0);  // measured neutral to slower with evict-first weights: off
+    const int NPF = (next != nullptr && next->has_w && pf8 > 0) ? 32 : 0;
+    a.pf_gate = NPF ? next->view.gate : nullptr;
+    a.pf_ud = NPF ? next->view.ud : nullptr;
+    a.pf_D = NPF ? static_cast<int>(next->D_local) : 0;
+    a.pf_pitch = NPF ? next->pitch_d : 0;
+    a.pf_units = NPF;
+    a.pf_bytes = NPF ? static_cast<uint32_t>(next->pitch_d * 2 * std::min(pf8, 8) / 8 / 16 * 16) : 0;
+    a.u_end = a.u_DOWN + a.ndt * a.S + NPF;
     {  // the claim order for this unit geometry, uploaded once per ctx (graph-capture safe after)
         const int lag = env_int("SG_TC_LAG", C->G);
-        std::vector<int> key = {a.nblk, a.ndt, a.S, a.dense, NX, KT, lag};
+        std::vector<int> key = {a.nblk, a.ndt, a.S, a.dense, NX, KT, lag, NPF};
         auto oit = C->tc_orders.find(key);
         if (oit == C->tc_orders.end()) {
-            const std::vector<int> order = tc_schedule(a, NX, KT, lag);
+            const std::vector<int> order = tc_schedule(a, NX, KT, lag, NPF);
             if (static_cast<int>(order.size()) != a.u_end)
                 return fail(SG_ERR_CUDA, "tensor-core schedule: unit count mismatch");
             int* dev = nullptr;
@@ -1136,8 +1146,9 @@ sg_status sg_ffn_forward_batch_dense(sg_ctx* C, const sg_layer* L, const float* 
 }
 
 sg_status sg_ffn_forward_batch_res(sg_ctx* C, const sg_layer* L, const float* xs, const float* xres,
-                                   int32_t batch, float* ys, int32_t dense, void* stream) {
-    if (xres == nullptr)
+                                   int32_t batch, float* ys, int32_t dense, const sg_layer* next,
+                                   void* stream) {
+    if (xres == nullptr && next == nullptr)
         return dense ? sg_ffn_forward_batch_dense(C, L, xs, batch, ys, stream)
                      : sg_ffn_forward_batch(C, L, xs, batch, ys, stream);
     if (sg_status s = check_pair(C, L); s != SG_OK) return s;
@@ -1147,7 +1158,8 @@ sg_status sg_ffn_forward_batch_res(sg_ctx* C, const sg_layer* L, const float* xs
     if (xs == nullptr || ys == nullptr) return fail(SG_ERR_USAGE, "null buffers");
     if (sg_status s = batch_workspace(C); s != SG_OK) return s;
     DeviceGuard dg(C->device);
-    if (sg_status s = tc_forward(C, L, xs, batch, ys, stream, dense ? 1 : 0, xres); s != SG_OK) return s;
+    if (next != nullptr && next->device != L->device) return fail(SG_ERR_USAGE, "next layer on another device");
+    if (sg_status s = tc_forward(C, L, xs, batch, ys, stream, dense ? 1 : 0, xres, next); s != SG_OK) return s;
     C->blast = L;
     C->blast_B = batch;
     C->blast_stack = false;

@@ -173,7 +173,11 @@ struct TcArgs {
     int ndt, S;            // d tiles of 128 outputs, block ranges of the down GEMM (S <= 4)
     int dense;             // 1: dense comparator (no predictor; every row)
     int tile_u;            // per-1024 survivor density at which DOWN tiles a block, not gathers
-    int u_T, u_GU, u_DOWN, u_end;  // unit counts by type (prefix sums: X, T, GU, DOWN)
+    int u_T, u_GU, u_DOWN, u_end;  // unit counts by type (prefix sums: X, T, GU, DOWN; PF last)
+    const uint16_t* pf_gate;  // optional: the next layer's gate rows [pf_D][pf_pitch] to prefetch
+    const uint16_t* pf_ud;    //   and its [up | down] rows (up halves prefetched)
+    int pf_D, pf_pitch, pf_units;
+    uint32_t pf_bytes;        //   leading bytes of each row into L2
     const int* order;      // [n_units] claim order: type << 24 | i << 8 | j (host-built)
     int n_units;
     unsigned long long* trace;  // optional [n_units][8] stamps (tools/tc_trace.py)

@@ -153,9 +153,10 @@ def test_batch_residual_input_equals_summed_input(dense):
     lib = capi.lib()
     Y1, Y2 = torch.zeros_like(H), torch.zeros_like(H)
     check(lib.sg_ffn_forward_batch_res(ctx.handle, layer.handle, C.c_void_p(H.data_ptr()),
-                                       C.c_void_p(R.data_ptr()), B, C.c_void_p(Y1.data_ptr()), dense, None))
+                                       C.c_void_p(R.data_ptr()), B, C.c_void_p(Y1.data_ptr()), dense,
+                                       layer.handle, None))
     check(lib.sg_ffn_forward_batch_res(ctx.handle, layer.handle, C.c_void_p(S.data_ptr()), None, B,
-                                       C.c_void_p(Y2.data_ptr()), dense, None))
+                                       C.c_void_p(Y2.data_ptr()), dense, None, None))
     torch.cuda.synchronize()
     assert torch.equal(Y1, Y2)
     assert float(Y1.abs().sum()) > 0

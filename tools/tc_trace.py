@@ -36,7 +36,7 @@ def main():
     cfg = CONFIGS[args.config]
     d, D, B = cfg["d"], cfg["D"], args.batch
     h = build_host_layer(d, D, cfg["act"], seed=0, eval_tokens=max(16, B))
-    layer = upload(h, d, D, cfg["act"], 256)
+    layer = upload(h, d, D, cfg["act"], 256, balance="sorted")  # the batch bench layout
     ctx = Context(0, d, D, 256)
     lib = capi.lib()
     X = torch.tensor(h.xs[:, :B].T.copy(), dtype=torch.float32, device="cuda")
