@@ -988,13 +988,22 @@ __device__ void phase_gather(const LayerView& L, const WorkView& W, const Smem& 
                 const int jj = j + h * kc;
                 const bool inP = kPipe != 2 || jj >= sm.misc[4] || sm.mask[jj];
                 const bool sv = inP && g > 0.f;  // revalidation, ffn_exec.hpp:200 (strict)
-                // a survivor's [up | down] rows (16 KB, contiguous) go to L2 now,
-                // one 128-B line per thread of the group, for stages 4 and 5a
+                // a survivor's [up | down] rows (16 KB, contiguous) go to L2 now for
+                // stages 4 and 5a: one bulk prefetch, kept in L2 ahead of the
+                // evict-first gate stream (SG_FLAGS bit 2: per-line LSU prefetches)
                 if (sv && !(W.flags & 2)) {
                     const char* a = reinterpret_cast<const char*>(
                         L.ud + static_cast<size_t>(nn) * 2 * L.pitch_d);
-                    for (int off = gt * 128; off < 4 * L.pitch_d; off += kGroupThreads * 128)
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(a + off));
+                    if (W.flags & 4) {
+                        for (int off = gt * 128; off < 4 * L.pitch_d; off += kGroupThreads * 128)
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(a + off));
+                    } else if (gt == 0) {
+                        uint64_t keep;
+                        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+                        asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a),
+                                     "r"(static_cast<uint32_t>(4 * L.pitch_d)), "l"(keep)
+                                     : "memory");
+                    }
                 }
                 if (gt == 0) {
                     if (kPipe == 2 && sv && W.vbits) atomicOr(W.vbits + nn, 1ull << W.bitpos);
