@@ -74,7 +74,6 @@ struct Unit {
     int nsub;    // A sub-tiles per stage (T: 128-row halves; GU: gate, up)
     int cnt;     // rows of the unit
     int acc;     // TMEM accumulator buffer
-    int both;    // the unit's accumulators span both buffers
     int u;       // index in the claim order
 };
 
@@ -306,6 +305,14 @@ struct DownStage {
     int row0, rows, gblk, c0;
     int kd;     // K rows the stage's smem layout holds (128: tiled stages when Z fits twice)
 };
+// TMEM accumulator regions (512 columns). Normally two buffers of 256; a sparse GU
+// unit past 85 tokens needs g | u | pre = 3N columns, so then region 0 = [0, 3N) holds
+// the GU and T units and region 1 = [3N, 512) (>= N) the DOWN units: a down unit's
+// MMAs still overlap the GU epilogue on the same SM.
+__device__ __forceinline__ bool tmem_split(const TcArgs& a) { return !a.dense && 3 * a.N > 256; }
+__device__ __forceinline__ uint32_t acc_base(const TcArgs& a, int acc) {
+    return acc == 0 ? 0u : static_cast<uint32_t>(tmem_split(a) ? 3 * a.N : 256);
+}
 // tiled down stages take 128 K rows when the Z tile of 128 slots fits the B area
 __device__ __forceinline__ int down_kd(const TcArgs& a) { return a.N <= 64 ? 128 : 64; }
 __device__ __forceinline__ DownWalk down_walk(int j) { return DownWalk{j, 0, 0, 0, 0, -1, 0, 0, 0, 0}; }
@@ -419,7 +426,6 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
     const uint32_t bbytes = static_cast<uint32_t>(a.N) * 128u;
     const uint32_t abytes = static_cast<uint32_t>(a.brows) * 128u;  // one block's rows x 64 K
     const uint32_t sbase = su32(stages);
-    const bool both = !a.dense && 3 * a.N > 256;  // g | u | pre do not fit one buffer
     int seq = 0, accseq = 0;
     int n = 0;         // stages issued by this thread (all producer threads agree)
     int pending = 0;   // of which not yet arrived
@@ -473,7 +479,7 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
             const int u = atomicAdd(fl_work(a), 1);
             int i = 0, j = 0;
             const int type = unit_type(a, u, i, j);
-            S.pu = Unit{type, i, j, 0, 0, 0, 0, 0, u};
+            S.pu = Unit{type, i, j, 0, 0, 0, 0, u};
             TC_TRACE(a, u, 0, gtimer());
             bool ready = unit_inputs_ready(a, type, j);
             if (ready && seq >= kUQ) ready = mbar_test(&S.uqe[seq % kUQ], ((seq / kUQ) - 1) & 1);
@@ -505,20 +511,12 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
             un.cnt = blk_rows(a, i);
             un.nsub = 2;
             un.nst = a.pitch_d / 64 + (a.dense ? 0 : a.pitch_r / 64);
-            un.both = both;
         } else if (type == U_DOWN) {
             un.nst = 1;  // the stage count unfolds block by block
             un.nsub = 1;
         }
         const bool mma_unit = type == U_T || type == U_GU || type == U_DOWN;
-        if (mma_unit) {
-            if (un.both) {
-                un.acc = 0;
-                accseq = 1;
-            } else {
-                un.acc = accseq++ & 1;
-            }
-        }
+        if (mma_unit) un.acc = tmem_split(a) ? (type == U_DOWN ? 1 : 0) : (accseq++ & 1);
         if (pt == 0) {
             const int slot = seq % kUQ;
             S.uq[slot] = un;
@@ -734,9 +732,8 @@ __device__ void mma_issuer(const TcArgs& a, TcSmem& S, uint8_t* stages) {
         if (mma_unit) {
             const int acc = un.acc;
             take_buffer(acc);
-            if (un.both) take_buffer(1);
             tc_fence_after();
-            const uint32_t dcol = S.tmem + static_cast<uint32_t>(acc * 256);
+            const uint32_t dcol = S.tmem + acc_base(a, acc);
             if (un.type == U_T) {
                 for (int st = 0; st < un.nst; ++st) run_stage(un.nsub, 4, false, dcol, idesc(a.N, 0), st == 0);
             } else if (un.type == U_GU) {
@@ -762,7 +759,6 @@ __device__ void mma_issuer(const TcArgs& a, TcSmem& S, uint8_t* stages) {
             }
             if (lane == 0) {
                 umma_commit(&S.tfull[acc]);
-                if (un.both) umma_commit(&S.tfull[1]);
             }
             __syncwarp();
         }
@@ -779,7 +775,7 @@ __device__ __forceinline__ void acc16(const TcArgs& a, uint32_t tbase, int quart
                                       float* v) {
     float h[16], l[16];
     const uint32_t addr = tbase + (static_cast<uint32_t>(quarter * 32) << 16) +
-                          static_cast<uint32_t>(accbuf * 256 + t * a.N + c0);
+                          acc_base(a, accbuf) + static_cast<uint32_t>(t * a.N + c0);
     tmem_ld8(addr, h);
     tmem_ld8(addr + 8u, h + 8);
     tmem_ld8(addr + static_cast<uint32_t>(a.nb), l);
@@ -859,7 +855,6 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
         const float gbias = (un.type == U_GU && !a.dense && quarter * 32 + lane < un.cnt) ? __ldg(a.bias + grow) : 0.f;
         if (mma_unit) {
             wait_acc(un.acc);
-            if (un.both) wait_acc(1);
             tc_fence_after();
         }
         if (et == 0) TC_TRACE(a, un.u, 3, gtimer());
@@ -870,7 +865,6 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
             epi_bar();
             if (et == 0) {
                 mbar_arrive(&S.tempty[acc]);
-                if (un.both) mbar_arrive(&S.tempty[1]);
             }
         };
 
@@ -985,7 +979,7 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
             const bool mine = k < cnt;
             const int n = i * a.brows + k;
             const float bias = gbias;
-            const uint32_t tl = S.tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * 256);
+            const uint32_t tl = S.tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc_base(a, acc);
             float z[64];
             uint64_t mb = 0, sbits = 0;
 #pragma unroll
