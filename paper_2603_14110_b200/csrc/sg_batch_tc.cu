@@ -365,8 +365,10 @@ __device__ __forceinline__ bool down_next(const TcArgs& a, DownWalk& w, DownStag
 __device__ __forceinline__ int* fl_work(const TcArgs& a) { return a.flags; }
 __device__ __forceinline__ int* fl_exit(const TcArgs& a) { return a.flags + 1; }
 __device__ __forceinline__ int* fl_x(const TcArgs& a) { return a.flags + 2; }
-__device__ __forceinline__ int* fl_t(const TcArgs& a) { return a.flags + 3; }   // T partials counted
-__device__ __forceinline__ int* fl_tr(const TcArgs& a) { return a.flags + 4; }  // T^T hi / lo ready
+__device__ __forceinline__ int* fl_t(const TcArgs& a, int h) { return a.flags + 3 + 2 * h; }  // T partials of half h
+__device__ __forceinline__ int* fl_tr(const TcArgs& a) { return a.flags + 4; }  // T^T halves ready
+// predictor row halves (M = 128 tiles) of the T units
+__device__ __forceinline__ int t_halves(const TcArgs& a) { return a.r > 128 ? 2 : 1; }
 __device__ __forceinline__ int* fl_gu(const TcArgs& a, int b) { return a.flags + 32 + b; }
 __device__ __forceinline__ int* fl_down(const TcArgs& a, int t) { return a.flags + 32 + a.nblk + t; }
 __device__ __forceinline__ int flag_count(const TcArgs& a) { return 32 + a.nblk + a.ndt; }
@@ -506,7 +508,7 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
         // ---- the unit's geometry
         if (type == U_T) {
             un.nst = a.kst / 64;
-            un.nsub = a.r > 128 ? 2 : 1;
+            un.nsub = 1;  // predictor rows [128 j, 128 j + 128)
         } else if (type == U_GU) {
             un.cnt = blk_rows(a, i);
             un.nsub = 2;
@@ -552,7 +554,7 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                 begin_stage(As, as, bar);
                 if (pt == 0) {
                     mbar_expect_tx(bar, un.nsub * 16384u + bbytes);
-                    for (int t = 0; t < un.nsub; ++t) tma_tile_ef(As + t * 16384, &M.Bp, k0 + st * 64, t * 128, bar, pol);
+                    tma_tile_ef(As, &M.Bp, k0 + st * 64, j * 128, bar, pol);
                     tma_tile_ef(As + kStageA, &M.xhl, k0 + st * 64, 0, bar, pol_last);
                 }
                 end_tile_stage(bar);
@@ -573,7 +575,7 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                 end_tile_stage(bar);
             }
             if (!a.dense) {
-                wait_flag(fl_tr(a), 1);
+                wait_flag(fl_tr(a), t_halves(a));
                 for (int st = 0; st < a.pitch_r / 64; ++st) {
                     begin_stage(As, as, bar);
                     if (pt == 0) {
@@ -928,48 +930,55 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
             epi_bar();
             if (et == 0) signal(fl_x(a));
         } else if (un.type == U_T) {
-            // partial T^T over K slice i: tpart[i][row][b]; the last slice to finish sums
-            // the KT partials in slice order -> T^T hi / lo rows (B operand of the GU
-            // units' predictor MMA), zero past the rank
-            const int KT = a.u_GU - a.u_T;
-            for (int t = 0; t < un.nsub; ++t) {
-                const int row = t * 128 + row0;
-                for (int c = 0; c < nb; c += 16) {
-                    float v[16];
-                    acc16(a, S.tmem, quarter, acc, t, c, v);
-                    st16(a.tpart + (static_cast<size_t>(i) * kTRows + row) * nb + c, v, min(16, nb - c));
-                }
+            // partial T^T of predictor rows [128 j, 128 j + 128) over K slice i ->
+            // tpart[i][row][b]; the last slice of the half to finish sums its KT partials in
+            // slice order (its own straight from TMEM) -> T^T hi / lo (the B operand of the
+            // GU units' predictor MMA), zero past the rank
+            const int KT = a.kt, row = j * 128 + row0;
+            for (int c = 0; c < nb; c += 16) {
+                float v[16];
+                acc16(a, S.tmem, quarter, acc, 0, c, v);
+                st16(a.tpart + (static_cast<size_t>(i) * kTRows + row) * nb + c, v, min(16, nb - c));
             }
-            release();
-            if (arrive_last(fl_t(a), KT, S, et)) {
-                for (int t = 0; t < 2; ++t) {
-                    const int row = t * 128 + row0;
-                    const float* src = a.tpart + static_cast<size_t>(row) * nb;
-                    for (int c = 0; c < nb; c += 8) {
-                        float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                        if (row < a.r) {
-                            float4 q[4][2];
+            epi_bar();
+            if (arrive_last(fl_t(a, j), KT, S, et)) {
+                const float* src = a.tpart + static_cast<size_t>(row) * nb;
+                const uint32_t tl = S.tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc_base(a, acc);
+                for (int c = 0; c < nb; c += 8) {
+                    // the other slices' loads first, then this slice's TMEM columns
+                    float4 q[4][2];
 #pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                if (k < KT) {
-                                    const float4* p = reinterpret_cast<const float4*>(src + static_cast<size_t>(k) * kTRows * nb + c);
-                                    q[k][0] = __ldcg(p);
-                                    q[k][1] = __ldcg(p + 1);
-                                }
-#pragma unroll
-                            for (int k = 0; k < 4; ++k)  // fixed order: slices 0, 1, ...
-                                if (k < KT) {
-                                    s[0] += q[k][0].x; s[1] += q[k][0].y; s[2] += q[k][0].z; s[3] += q[k][0].w;
-                                    s[4] += q[k][1].x; s[5] += q[k][1].y; s[6] += q[k][1].z; s[7] += q[k][1].w;
-                                }
+                    for (int k = 0; k < 4; ++k)
+                        if (k < KT && k != i && row < a.r) {
+                            const float4* p = reinterpret_cast<const float4*>(src + static_cast<size_t>(k) * kTRows * nb + c);
+                            q[k][0] = __ldcg(p);
+                            q[k][1] = __ldcg(p + 1);
                         }
-                        store_hilo<8>(S, et, s, row0, -1, a.thl + t * 128, 256, nb, c, 128);
+                    float h[8], l[8], s[8];
+                    tmem_ld8(tl + c, h);
+                    tmem_ld8(tl + nb + c, l);
+                    tmem_wait();
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {  // fixed order: slices 0, 1, ... (own at i)
+                        if (k >= KT) break;
+                        const float v[8] = {q[k][0].x, q[k][0].y, q[k][0].z, q[k][0].w,
+                                            q[k][1].x, q[k][1].y, q[k][1].z, q[k][1].w};
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const float t = k == i ? h[e] + l[e] : v[e];
+                            s[e] = k == 0 ? t : s[e] + t;
+                        }
                     }
+                    if (row >= a.r)
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) s[e] = 0.f;
+                    store_hilo<8>(S, et, s, row0, -1, a.thl + j * 128, 256, nb, c, 128);
                 }
                 asm volatile("fence.proxy.async.global;" ::: "memory");  // T^T is read by TMA
                 epi_bar();
                 if (et == 0) signal(fl_tr(a));
             }
+            release();
         } else if (un.type == U_GU) {
             // block i: g (columns 0..N), u (N..2N), pre (2N..3N, sparse) of this thread's
             // row; mask P_b = pre + bias > 0 (ffn_exec.hpp:141), survivors V_b = P_b &

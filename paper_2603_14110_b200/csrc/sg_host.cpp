@@ -924,7 +924,8 @@ std::vector<int> tc_schedule(const sg::TcArgs& a, int NX, int KT, int lag, int N
     enum { X = 1, T, GU, DOWN, PF };  // sg_batch_tc.cu UnitType
     std::vector<int> order;
     for (int k = 0; k < NX; ++k) order.push_back(code(X, k, 0));
-    for (int k = 0; k < KT; ++k) order.push_back(code(T, k, 0));
+    for (int h = 0; h < (a.r > 128 ? 2 : 1); ++h)
+        for (int k = 0; k < KT; ++k) order.push_back(code(T, k, h));
     struct Item {
         int code, ready_at;
     };
@@ -985,11 +986,12 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     a.S = std::max(1, std::min({env_int("SG_TC_S", 4), kTcSMax, (a.nblk + kTcChunk - 1) / kTcChunk}));  // each range: >= 1 chunk
     const int KT = dense ? 0 : k_slices(a.pitch_d, kTcKTMax);
     a.kst = KT ? a.pitch_d / KT : 0;
+    a.kt = KT;
     // x -> X^T hi / lo: about 256 (token, 8-column) items per unit, so each epilogue
     // thread issues its loads in one round
     const int NX = std::max(8, std::min(128, a.nb * (a.pitch_d / 8) / 256));
     a.u_T = NX;
-    a.u_GU = a.u_T + KT;
+    a.u_GU = a.u_T + KT * (a.r > 128 ? 2 : 1);
     a.u_DOWN = a.u_GU + a.nblk;
     // L2 prefetch of the next layer's gate / up rows (their leading SG_TC_PF eighths)
     const int pf8 = env_int("SG_TC_PF", 0);  // measured neutral to slower with evict-first weights: off

@@ -169,7 +169,7 @@ struct TcArgs {
     int d, D, r, pitch_d, pitch_r, act;
     int brows;             // neurons per block (<= 128: rows of one M = 128 tile)
     int nblk;              // neuron blocks
-    int kst;               // K of a T unit (the KT = u_GU - u_T slices)
+    int kst, kt;           // K of a T unit, K slices of T (T units: kt per 128-row half of rank)
     int ndt, S;            // d tiles of 128 outputs, block ranges of the down GEMM (S <= 4)
     int dense;             // 1: dense comparator (no predictor; every row)
     int tile_u;            // per-1024 survivor density at which DOWN tiles a block, not gathers
