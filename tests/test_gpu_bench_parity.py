@@ -8,9 +8,11 @@
   (layer l+1 reads h_{l+1} + y_l, the decoder's residual-stream dependency and the
   bench headline). Every layer's P, V (sg_ctx_read_stack_sets) and y are
   checked against the f64 oracle (ffn_exec.hpp:183-218) under tests/parity_util.py.
-* configs[4] batched decode at full 7B and 13B size, B in {17, 32, 64}, through
-  sg_ffn_forward_batch_host (the e2e entry of the batch bench): every token's P_b,
-  V_b and y_b against the single-token oracle.
+* configs[4] batched decode at full 7B, 13B and Mistral (dReLU) size in the batch
+  bench's activity-sorted layout, B in {17, 32, 64}, through sg_ffn_forward_batch_host
+  (the e2e entry of the batch bench): every token's P_b, V_b and y_b against the
+  single-token oracle; and the bench's residual chain (sg_ffn_forward_batch_res, h_{l+1}
+  + y_l formed in the launch) over three full-size 7B layers.
 Near-threshold flips are bounded per token (parity_util.MAX_FLIPS) and their
 counts are printed (-s) for the record.
 """
@@ -93,12 +95,12 @@ def _global_map(layer):
     return np.array([layer.global_index(k) for k in range(layer.local_inter)], dtype=np.int64)
 
 
-@pytest.mark.parametrize("config", ["7b", "13b"])
+@pytest.mark.parametrize("config", ["7b", "13b", "mistral"])
 def test_bench_batch_full_size(config):
     cfg = CONFIGS[config]
     d, D, act = cfg["d"], cfg["D"], cfg["act"]
     h = build_host_layer(d, D, act, seed=1, rank=256, sparsity=0.5, eval_tokens=64)
-    layer = upload(h, d, D, act, 256, hot_rows=16)
+    layer = upload(h, d, D, act, 256, balance="sorted")  # the batch bench's layout
     q = _q(h)
     gmap = _global_map(layer)
     ctx = Context(0, d, D, 256)
@@ -123,3 +125,39 @@ def test_bench_batch_full_size(config):
             assert diag["rel"] <= Y_RTOL
             flips.append((diag["dP"], diag["dV"]))
         print(f"{config} B={B}: flips per token {flips}")
+
+
+def test_bench_batch_residual_chain_7b():
+    """The batch bench's exact step shape: full-size 7B layers in the bench's layout,
+    B = 17 tokens, layer l+1 fed h_{l+1} + y_l through sg_ffn_forward_batch_res (x formed
+    inside the launch). Every layer's tokens against the oracle on the input that layer
+    actually saw."""
+    import torch
+
+    cfg = CONFIGS["7b"]
+    d, D, act, L, B = cfg["d"], cfg["D"], cfg["act"], 3, 17
+    hosts = [build_host_layer(d, D, act, seed=20 + l, rank=256, sparsity=0.5, eval_tokens=B) for l in range(L)]
+    layers = [upload(h, d, D, act, 256, balance="sorted") for h in hosts]
+    ctx = Context(0, d, D, 256)
+    lib = capi.lib()
+    H = [torch.tensor(np.ascontiguousarray(h.xs[:, :B].T), dtype=torch.float32, device="cuda") for h in hosts]
+    Y = [torch.zeros_like(H[0]) for _ in range(L)]
+    for l in range(L):
+        res = C.c_void_p(Y[l - 1].data_ptr()) if l else None
+        nxt = layers[l + 1].handle if l + 1 < L else None
+        check(lib.sg_ffn_forward_batch_res(ctx.handle, layers[l].handle, C.c_void_p(H[l].data_ptr()), res, B,
+                                           C.c_void_p(Y[l].data_ptr()), 0, nxt, None))
+        pb = np.zeros(layers[l].local_inter, dtype=np.uint64)
+        vb = np.zeros_like(pb)
+        check(lib.sg_ctx_read_batch(ctx.handle, None, B, None, pb.ctypes.data_as(C.c_void_p),
+                                    vb.ctypes.data_as(C.c_void_p)))
+        gmap = _global_map(layers[l])
+        xin = (H[l] + Y[l - 1]).cpu().numpy() if l else H[l].cpu().numpy()
+        ys = Y[l].cpu().numpy()
+        q = _q(hosts[l])
+        for b in range(B):
+            bit = np.uint64(1) << np.uint64(b)
+            P = np.sort(gmap[(pb & bit) != 0])
+            V = np.sort(gmap[(vb & bit) != 0])
+            diag = check_token(q, xin[b].astype(np.float64), ys[b], P, V, act=act)
+            assert diag["rel"] <= Y_RTOL
