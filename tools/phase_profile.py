@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--steps", type=int, default=0, help="plain repeated stack calls (ncu target)")
     ap.add_argument("--json", default=None)
     ap.add_argument("--hot-rows", type=int, default=16)
+    ap.add_argument("--chain", type=int, default=2, help="0 unchained, 1 y->x, 2 residual (bench default)")
     args = ap.parse_args()
     import torch
     from paper_2603_14110_b200 import _capi as capi
@@ -52,7 +53,7 @@ def main():
 
     def call():
         check(lib.sg_ffn_forward_layers(ctx.handle, arr, L, pipe, C.c_void_p(xs.data_ptr()),
-                                        C.c_void_p(ys.data_ptr()), 0, C.c_void_p(sh)))
+                                        C.c_void_p(ys.data_ptr()), args.chain, C.c_void_p(sh)))
 
     for _ in range(5):
         call()
@@ -87,7 +88,7 @@ def main():
         rows.append((NAMES[k], crit, busy, worst))
         prev = k
     layer_us = np.median(rel[:, :, used[-1]].max(axis=1) - rel[:, :, 0].min(axis=1))
-    print(f"config={args.config} layers={L} pipeline={args.pipeline} G={G}")
+    print(f"config={args.config} layers={L} pipeline={args.pipeline} chain={args.chain} G={G}")
     print(f"{'phase':20s} {'critical_us':>12s} {'mean_cta_us':>12s} {'max_cta_us':>12s}")
     for n, c, b, w in rows:
         print(f"{n:20s} {c:12.2f} {b:12.2f} {w:12.2f}")
