@@ -308,10 +308,15 @@ def run_batch(args, cfg, host, layers, ctx, world, rank, local):
 
     def call(l, sh, dense=0):
         x, res = layer_io(l)
-        nxt = layers[l + 1].handle if l + 1 < L else layers[0].handle  # (the next step's first)
+        # the next call's input (h_{l+1} + y_l or y_l) is known: this launch's y finishers
+        # write its bf16 X^T too
+        nxt, nxs = None, None
+        if l + 1 < L and chain:
+            nxt = layers[l + 1].handle
+            nxs = C.c_void_p(X[l + 1].data_ptr()) if chain == 2 else None
         check(lib.sg_ffn_forward_batch_res(ctx.handle, layers[l].handle, C.c_void_p(x),
                                            C.c_void_p(res) if res else None, B,
-                                           C.c_void_p(Y[l].data_ptr()), dense, nxt, C.c_void_p(sh)))
+                                           C.c_void_p(Y[l].data_ptr()), dense, nxt, nxs, C.c_void_p(sh)))
 
     def step(sh, dense=0):
         for l in range(L):

@@ -215,13 +215,14 @@ sg_status sg_ffn_forward_batch_dense(sg_ctx* ctx, const sg_layer* layer, const f
                                      int32_t batch, float* ys, void* stream);
 /* Batched decode of a residual stream: token b's input is xs_b + xres_b (summed in
  * fp32 inside the launch, e.g. h_{l+1} + y_l between two FFN layers); xres may be
- * NULL. dense != 0 runs the dense comparator. `next` (optional): the layer the
- * caller runs next — SMs without down work prefetch the leading part of its gate /
- * up rows into L2 (timing only; results unchanged). Tensor-core path only (hidden <=
- * 8192, rank <= 256). */
+ * NULL. dense != 0 runs the dense comparator. `next` / `next_xs` (optional): the call
+ * that follows on this ctx will be on layer `next` with input next_xs + ys (next_xs
+ * may be NULL: input ys) — this launch's y finishers then also write that launch's
+ * bf16 hi/lo X^T, so it starts with no x split (results unchanged; a different next
+ * call simply splits its x itself). Tensor-core path only (hidden <= 8192, rank <= 256). */
 sg_status sg_ffn_forward_batch_res(sg_ctx* ctx, const sg_layer* layer, const float* xs, const float* xres,
                                    int32_t batch, float* ys, int32_t dense, const sg_layer* next,
-                                   void* stream);
+                                   const float* next_xs, void* stream);
 /* Diagnostics of the tensor-core batch kernel: with max_units > 0, later batched calls
  * record per work unit 8 values (%globaltimer ns: claim, inputs ready, loads issued,
  * epilogue start / end; the SM id; two epilogue-internal stamps: partial written,

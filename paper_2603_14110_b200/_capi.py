@@ -86,7 +86,7 @@ SYMBOLS = [
     ("sg_ctx_read_tc_trace", C.c_int, [_VP, _VP, _I32, _VP, C.POINTER(_I32)]),
     ("sg_tc_unit_codes", C.c_int, [_VP, _VP, _I32]),
     ("sg_ffn_forward_batch_dense", C.c_int, [_VP, _VP, _VP, _I32, _VP, _VP]),
-    ("sg_ffn_forward_batch_res", C.c_int, [_VP, _VP, _VP, _VP, _I32, _VP, _I32, _VP, _VP]),
+    ("sg_ffn_forward_batch_res", C.c_int, [_VP, _VP, _VP, _VP, _I32, _VP, _I32, _VP, _VP, _VP]),
     ("sg_ctx_read_batch", C.c_int, [_VP, _VP, _I32, C.POINTER(sg_exec_stats), _VP, _VP]),
     ("sg_ffn_forward_batch_host", C.c_int, [_VP, _VP, _VP, _I32, _VP, C.POINTER(sg_exec_stats), _VP]),
     ("sg_ctx_enable_phase_timing", C.c_int, [_VP, _I32]),

@@ -1109,10 +1109,12 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
             if (arrive_last(fl_down(a, i), a.S, S, et)) {
                 // y rows of d tile i: the S range partials in range order, 2 chunks of 8
                 // tokens per round of loads
+                bool xbad = false;
                 const size_t rs = static_cast<size_t>(a.ndt) * 128 * nb;
                 const float* rowp = a.ypart + static_cast<size_t>(m) * nb;
                 for (int c0 = 0; c0 < nb; c0 += 16) {
                     float4 q[4][2][2];
+                    float nv[16];  // (prep) the next launch's residual input, same round of loads
 #pragma unroll
                     for (int r = 0; r < 4; ++r)
 #pragma unroll
@@ -1123,22 +1125,45 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
                                 q[r][h][1] = __ldcg(src + 1);
                             }
 #pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        nv[e] = (a.prep && a.nh && c0 + e < a.B && m < a.d)
+                                    ? __ldcg(a.nh + static_cast<size_t>(c0 + e) * a.d + m)
+                                    : 0.f;
+#pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int c = c0 + 8 * h;
-                        if (c >= nb || m >= a.d) continue;
+                        if (c >= nb) continue;
                         float y[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                        if (m < a.d) {
 #pragma unroll
-                        for (int r = 0; r < 4; ++r)  // fixed order: ranges 0, 1, ..., S-1
-                            if (r < a.S) {
-                                y[0] += q[r][h][0].x; y[1] += q[r][h][0].y; y[2] += q[r][h][0].z; y[3] += q[r][h][0].w;
-                                y[4] += q[r][h][1].x; y[5] += q[r][h][1].y; y[6] += q[r][h][1].z; y[7] += q[r][h][1].w;
+                            for (int r = 0; r < 4; ++r)  // fixed order: ranges 0, 1, ..., S-1
+                                if (r < a.S) {
+                                    y[0] += q[r][h][0].x; y[1] += q[r][h][0].y; y[2] += q[r][h][0].z; y[3] += q[r][h][0].w;
+                                    y[4] += q[r][h][1].x; y[5] += q[r][h][1].y; y[6] += q[r][h][1].z; y[7] += q[r][h][1].w;
+                                }
+#pragma unroll
+                            for (int e = 0; e < 8; ++e)
+                                if (c + e < a.B) a.y[static_cast<size_t>(c + e) * a.d + m] = y[e];
+                        }
+                        if (a.prep) {
+                            // the NEXT launch's X^T column m: x = h_next + y (h_next may be
+                            // absent: x = y), split into bf16 hi / lo through smem staging —
+                            // the next launch then runs no X units (every GU unit of this
+                            // launch has finished)
+                            float xv[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                const int b = c + e;
+                                xv[e] = 0.f;
+                                if (b < a.B && m < a.d) xv[e] = y[e] + nv[8 * h + e];
+                                xbad |= !isfinite(xv[e]);
                             }
-                        SG_CHECK(m < a.d);
-#pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            if (c + e < a.B) a.y[static_cast<size_t>(c + e) * a.d + m] = y[e];
+                            store_hilo<8>(S, et, xv, row0, -1, a.xhl + static_cast<size_t>(i) * 128, a.xpitch, nb, c,
+                                          min(128, a.pitch_d - i * 128));
+                        }
                     }
                 }
+                if (xbad) atomicOr(a.bad + 2, 1);  // the next launch's check_input
             }
         }
         if (et == 0) {
@@ -1207,8 +1232,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
             // publish the non-finite flag (read by sg_ctx_read_batch), zero for the next
             __threadfence();
             for (int k = 0; k < flag_count(a); ++k) a.flags[k] = 0;
-            a.bad[1] = __ldcg(a.bad);
+            // bad: [0] this launch's x, [1] published, [2] the x this launch prepared for
+            // the next one, [3] that flag carried into the next launch
+            a.bad[1] = __ldcg(a.bad) | (a.x_ready ? __ldcg(a.bad + 3) : 0);
             a.bad[0] = 0;
+            a.bad[3] = __ldcg(a.bad + 2);
+            a.bad[2] = 0;
             __threadfence();
         }
     }

@@ -91,6 +91,15 @@ struct sg_ctx {
     void* tmem_ws = nullptr;
     sg::TcArgs tw{};
     std::map<int, sg::TcMaps> tcmaps_ws;  // workspace maps per nb (box height N = 2 nb)
+    // X^T prepared by the last tensor-core launch for the next one: valid for a call on
+    // `layer` with `batch` tokens whose input is hs + res == prep_h + prep_y
+    struct {
+        bool valid = false;
+        const sg_layer* layer = nullptr;
+        const float* h = nullptr;
+        const float* y = nullptr;
+        int batch = 0;
+    } tc_prep;
     std::map<std::vector<int>, int*> tc_orders;  // device claim orders per unit geometry
     unsigned long long* tc_trace = nullptr;      // optional unit trace (sg_ctx_enable_tc_trace)
     size_t tc_trace_cap = 0;
@@ -877,7 +886,7 @@ sg_status tc_workspace(sg_ctx* C) {
     const size_t o_x = take(128 * pd * 2), o_tp = take(kTcKTMax * 256 * 64 * 4), o_th = take(128 * 256 * 2),
                  o_mb = take(Dm * 8), o_vb = take(Dm * 8), o_vl = take(nblk * kTcBlk * 4), o_vc = take(nblk * 4),
                  o_z = take(128 * nblk * kTcBlk * 2), o_y = take(kTcSMax * ndt * 128 * 64 * 4),
-                 o_cnt = take((64 + 64 + 2) * 4),
+                 o_cnt = take((64 + 64 + 4) * 4),
                  o_fl = take(static_cast<size_t>(sg::tc_flag_ints(static_cast<int>(nblk), static_cast<int>(ndt))) * 4);
     DeviceGuard dg(C->device);
     cudaError_t e = cudaMalloc(&C->tmem_ws, off);
@@ -955,7 +964,8 @@ std::vector<int> tc_schedule(const sg::TcArgs& a, int NX, int KT, int lag, int N
 
 // One tensor-core launch: B tokens through one layer (dense != 0: every row, no predictor).
 sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float* ys, void* stream,
-                     int dense, const float* xres = nullptr, const sg_layer* next = nullptr) {
+                     int dense, const float* xres = nullptr, const sg_layer* next = nullptr,
+                     const float* next_xs = nullptr) {
     if (sg_status s = tc_workspace(C); s != SG_OK) return s;
     sg::TcArgs a = C->tw;
     a.B = B;
@@ -989,7 +999,21 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     a.kt = KT;
     // x -> X^T hi / lo: about 256 (token, 8-column) items per unit, so each epilogue
     // thread issues its loads in one round
-    const int NX = std::max(8, std::min(128, a.nb * (a.pitch_d / 8) / 256));
+    // the previous launch may have written this call's X^T already (x = h + y formed in its
+    // y finishers): then no X units
+    const auto& pp = C->tc_prep;
+    a.x_ready = pp.valid && pp.layer == L && pp.batch == B &&
+                ((xs == pp.h && xres == pp.y) || (pp.h == nullptr && xres == nullptr && xs == pp.y));
+    // (up to 32 tokens: past that the finishers' extra X^T stores cost more than the X
+    // split they save, measured B = 64 106 -> 111 µs/layer)
+    a.prep = next != nullptr && next != L && next->d == L->d && next->pitch_d == L->pitch_d && a.nb <= 32 ? 1 : 0;
+    a.nh = next_xs;
+    C->tc_prep.valid = a.prep != 0;
+    C->tc_prep.layer = next;
+    C->tc_prep.h = next_xs;
+    C->tc_prep.y = ys;
+    C->tc_prep.batch = B;
+    const int NX = a.x_ready ? 0 : std::max(8, std::min(128, a.nb * (a.pitch_d / 8) / 256));
     a.u_T = NX;
     a.u_GU = a.u_T + KT * (a.r > 128 ? 2 : 1);
     a.u_DOWN = a.u_GU + a.nblk;
@@ -1005,7 +1029,7 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     a.u_end = a.u_DOWN + a.ndt * a.S + NPF;
     {  // the claim order for this unit geometry, uploaded once per ctx (graph-capture safe after)
         const int lag = env_int("SG_TC_LAG", C->G);
-        std::vector<int> key = {a.nblk, a.ndt, a.S, a.dense, NX, KT, lag, NPF};
+        std::vector<int> key = {a.nblk, a.ndt, a.S, a.dense, NX, KT, lag, NPF};  // (NX = 0: X^T prepared)
         auto oit = C->tc_orders.find(key);
         if (oit == C->tc_orders.end()) {
             const std::vector<int> order = tc_schedule(a, NX, KT, lag, NPF);
@@ -1059,6 +1083,7 @@ sg_status sg_ffn_forward_batch(sg_ctx* C, const sg_layer* L, const float* xs, in
     if (sg_status s = batch_workspace(C); s != SG_OK) return s;
     DeviceGuard dg(C->device);
     if (batch <= small_batch_limit() && batch <= kMaxStackLayers) {
+        C->tc_prep.valid = false;  // (a prepared X^T is for the tensor-core call that follows it)
         // few tokens: one persistent launch with token b as "layer" b of a stack
         // (unchained; same per-token results), predicted / survivor bits per token
         auto st = static_cast<cudaStream_t>(stream);
@@ -1086,6 +1111,7 @@ sg_status sg_ffn_forward_batch(sg_ctx* C, const sg_layer* L, const float* xs, in
         C->blast_path = 2;
         return SG_OK;
     }
+    C->tc_prep.valid = false;
     sg::BatchArgs a = C->bw;
     a.B = batch;
     // split-K of the gate / up GEMMs: enough CTAs for ~2 full waves of the union
@@ -1149,8 +1175,8 @@ sg_status sg_ffn_forward_batch_dense(sg_ctx* C, const sg_layer* L, const float* 
 
 sg_status sg_ffn_forward_batch_res(sg_ctx* C, const sg_layer* L, const float* xs, const float* xres,
                                    int32_t batch, float* ys, int32_t dense, const sg_layer* next,
-                                   void* stream) {
-    if (xres == nullptr && next == nullptr)
+                                   const float* next_xs, void* stream) {
+    if (xres == nullptr && next == nullptr && !(C && C->tc_prep.valid))
         return dense ? sg_ffn_forward_batch_dense(C, L, xs, batch, ys, stream)
                      : sg_ffn_forward_batch(C, L, xs, batch, ys, stream);
     if (sg_status s = check_pair(C, L); s != SG_OK) return s;
@@ -1161,7 +1187,8 @@ sg_status sg_ffn_forward_batch_res(sg_ctx* C, const sg_layer* L, const float* xs
     if (sg_status s = batch_workspace(C); s != SG_OK) return s;
     DeviceGuard dg(C->device);
     if (next != nullptr && next->device != L->device) return fail(SG_ERR_USAGE, "next layer on another device");
-    if (sg_status s = tc_forward(C, L, xs, batch, ys, stream, dense ? 1 : 0, xres, next); s != SG_OK) return s;
+    if (sg_status s = tc_forward(C, L, xs, batch, ys, stream, dense ? 1 : 0, xres, next, next_xs); s != SG_OK)
+        return s;
     C->blast = L;
     C->blast_B = batch;
     C->blast_stack = false;

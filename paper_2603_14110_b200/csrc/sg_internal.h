@@ -199,8 +199,11 @@ struct TcArgs {
     float* ypart;          // [S][ndt*128][nb]
     int* pcount;           // [64] |P_b|   (pcount, vcount, bad: zeroed by the host per call)
     int* vcount;           // [64] |V_b|
-    int* bad;              // [2] non-finite input flag of the running launch; [1] = that of the
-                           //   last completed launch (copied and re-zeroed by its last CTA)
+    int* bad;              // [4] non-finite flags: [0] this launch's x, [1] published for the
+                           //   last completed launch, [2] / [3] the next launch's x (prep)
+    int prep;              // 1: the y finishers also write the NEXT launch's X^T (x = nh + y)
+    const float* nh;       //   its residual input h_{l+1} [B][d] (or null: x = y)
+    int x_ready;           // 1: X^T was prepared by the previous launch (no X units)
     int* flags;            // dataflow counters, reset by the last CTA of every launch
 };
 int tc_smem_bytes();

@@ -154,9 +154,53 @@ def test_batch_residual_input_equals_summed_input(dense):
     Y1, Y2 = torch.zeros_like(H), torch.zeros_like(H)
     check(lib.sg_ffn_forward_batch_res(ctx.handle, layer.handle, C.c_void_p(H.data_ptr()),
                                        C.c_void_p(R.data_ptr()), B, C.c_void_p(Y1.data_ptr()), dense,
-                                       layer.handle, None))
+                                       None, None, None))
     check(lib.sg_ffn_forward_batch_res(ctx.handle, layer.handle, C.c_void_p(S.data_ptr()), None, B,
-                                       C.c_void_p(Y2.data_ptr()), dense, None, None))
+                                       C.c_void_p(Y2.data_ptr()), dense, None, None, None))
     torch.cuda.synchronize()
     assert torch.equal(Y1, Y2)
     assert float(Y1.abs().sum()) > 0
+
+
+@pytest.mark.parametrize("chain", [1, 2])
+def test_batch_prepared_next_input_equals_plain_chain(chain):
+    """A chain of batched calls where each launch's y finishers also write the next
+    call's X^T (`next` / `next_xs`) gives exactly the results of the same chain run
+    without that, call by call (the next call then runs no x split)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2603_14110_b200 import _capi as capi
+    from paper_2603_14110_b200.ffn_exec import Context, check
+
+    d, D, r, B, L = 512, 2048, 64, 9, 3
+    layers = []
+    for l in range(L):
+        fx, pred = _calibrated_layer(d, D, r, seed=30 + l, calib=1024)
+        layers.append(DeviceLayer(fx.weights, pred))
+    rng = np.random.default_rng(7)
+    H = [torch.tensor(0.5 * rng.standard_normal((B, d)), dtype=torch.float32, device="cuda") for _ in range(L)]
+    lib = capi.lib()
+
+    def run(prep):
+        ctx = Context(0, d, D, r)
+        Y = [torch.zeros_like(H[0]) for _ in range(L)]
+        for l in range(L):
+            if l == 0:
+                x, res = H[0], None
+            elif chain == 1:
+                x, res = Y[l - 1], None
+            else:
+                x, res = H[l], Y[l - 1]
+            nxt = layers[l + 1].handle if prep and l + 1 < L else None
+            nxs = C.c_void_p(H[l + 1].data_ptr()) if prep and l + 1 < L and chain == 2 else None
+            check(lib.sg_ffn_forward_batch_res(ctx.handle, layers[l].handle, C.c_void_p(x.data_ptr()),
+                                               C.c_void_p(res.data_ptr()) if res is not None else None, B,
+                                               C.c_void_p(Y[l].data_ptr()), 0, nxt, nxs, None))
+        torch.cuda.synchronize()
+        return Y
+
+    Ya, Yb = run(False), run(True)
+    for l in range(L):
+        assert torch.equal(Ya[l], Yb[l]), l

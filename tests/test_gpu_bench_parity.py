@@ -144,9 +144,10 @@ def test_bench_batch_residual_chain_7b():
     Y = [torch.zeros_like(H[0]) for _ in range(L)]
     for l in range(L):
         res = C.c_void_p(Y[l - 1].data_ptr()) if l else None
-        nxt = layers[l + 1].handle if l + 1 < L else None
+        nxt = layers[l + 1].handle if l + 1 < L else None  # (as the bench: next X^T prepared)
+        nxs = C.c_void_p(H[l + 1].data_ptr()) if l + 1 < L else None
         check(lib.sg_ffn_forward_batch_res(ctx.handle, layers[l].handle, C.c_void_p(H[l].data_ptr()), res, B,
-                                           C.c_void_p(Y[l].data_ptr()), 0, nxt, None))
+                                           C.c_void_p(Y[l].data_ptr()), 0, nxt, nxs, None))
         pb = np.zeros(layers[l].local_inter, dtype=np.uint64)
         vb = np.zeros_like(pb)
         check(lib.sg_ctx_read_batch(ctx.handle, None, B, None, pb.ctypes.data_as(C.c_void_p),
