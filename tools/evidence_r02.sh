@@ -11,7 +11,7 @@ for c in 7b mistral 13b; do
   python -c "import json; d=json.loads(open('gpurun_out/bench_r02_$c.json').read().strip().splitlines()[-1]); print('$c', round(d['value'],1), d['unit'], 'e2e', round(d['e2e']['value'],1), 'frac', round(d['roofline']['frac'],3), 'us/layer', round(d.get('per_layer_us', 0),1))" || tail -3 gpurun_out/bench_r02_$c.err
 done
 timeout 900 python bench.py --impl reference > gpurun_out/bench_r02_reference.json 2> gpurun_out/bench_r02_reference.err; tail -c 400 gpurun_out/bench_r02_reference.json
-for B in 2 4 8 16 32 64; do
+for B in 2 4 8 16 32 48 64; do
   timeout 600 python bench.py --batch $B --layers 32 --steps 50 --warmup 5 > gpurun_out/batch_r02_B$B.json 2> gpurun_out/batch_r02_B$B.err
   python -c "import json; d=json.loads(open('gpurun_out/batch_r02_B$B.json').read().strip().splitlines()[-1]); print('B=$B', 'tok/s %.0f us/layer %.1f frac %.3f | dense us/layer %.1f | sparse/dense %.2f | e2e %.0f' % (d['value'], d['per_layer_us'], d['roofline']['frac'], d['dense']['per_layer_us'], d['dense']['sparse_speedup'], d['e2e']['value']))" || tail -3 gpurun_out/batch_r02_B$B.err
 done
