@@ -268,14 +268,13 @@ __device__ __forceinline__ int blk_rows(const TcArgs& a, int blk) {
     const int r = a.D - blk * a.brows;
     return r < a.brows ? r : a.brows;
 }
-// The S block ranges of the DOWN units interleave chunks of kRangePair consecutive
+// The S block ranges of the DOWN units interleave chunks of a.rchunk consecutive
 // blocks (range j: chunks j, j + S, j + 2S, ...), so every range mixes the layout's
 // leading (hot) and trailing (cold) blocks and the ranges carry about equal survivor
 // rows, while a chunk's tiled blocks still stream as one run of full stages; block k
 // of range j (>= nblk: past its end).
-constexpr int kRangePair = 8;
 __device__ __forceinline__ int range_block(const TcArgs& a, int j, int k) {
-    return (j + (k / kRangePair) * a.S) * kRangePair + k % kRangePair;
+    return (j + (k / a.rchunk) * a.S) * a.rchunk + k % a.rchunk;
 }
 // DOWN streams a block whole by TMA tiles (reading its non-survivor rows too, against
 // Z = 0) once its survivors are a large enough share of its rows: a row gather moves

@@ -865,7 +865,6 @@ int env_int(const char* name, int dflt) {
 
 constexpr int kTcBlk = 128;   // block capacity of the tensor-core kernel (rows of an M = 128 tile)
 constexpr int kTcSMax = 4;    // block ranges of the down units (the y finisher sums <= 4)
-constexpr int kTcChunk = 8;   // consecutive blocks per range interleave step (sg_batch_tc.cu kRangePair)
 constexpr int kTcKTMax = 4;   // K slices of the predictor's T units (the finisher sums <= 4)
 
 // blocks of a layer at most: one per SM, or D / 128 for very wide layers
@@ -939,7 +938,8 @@ std::vector<int> tc_schedule(const sg::TcArgs& a, int NX, int KT, int lag, int N
         int code, ready_at;
     };
     std::vector<Item> downs;
-    // range sr: chunks of kTcChunk blocks sr, sr + S, ... (sg_batch_tc.cu range_block); its last block
+    // range sr: chunks of rchunk blocks sr, sr + S, ... (sg_batch_tc.cu range_block); its last block
+    const int kTcChunk = a.rchunk;
     const int chunks = (a.nblk + kTcChunk - 1) / kTcChunk;
     auto range_last = [&](int sr) {
         if (sr >= chunks) return -1;
@@ -993,7 +993,11 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     a.y = ys;
     a.bias = L->view.bias;
     a.ud = L->view.ud;
-    a.S = std::max(1, std::min({env_int("SG_TC_S", 4), kTcSMax, (a.nblk + kTcChunk - 1) / kTcChunk}));  // each range: >= 1 chunk
+    // ranges interleave chunks of 8 blocks (SG_TC_RCHUNK; 0 = contiguous ranges)
+    a.rchunk = env_int("SG_TC_RCHUNK", 8);
+    a.S = std::max(1, std::min({env_int("SG_TC_S", 4), kTcSMax, a.nblk}));
+    if (a.rchunk <= 0) a.rchunk = (a.nblk + a.S - 1) / a.S;
+    a.S = std::max(1, std::min(a.S, (a.nblk + a.rchunk - 1) / a.rchunk));  // each range: >= 1 chunk
     const int KT = dense ? 0 : k_slices(a.pitch_d, kTcKTMax);
     a.kst = KT ? a.pitch_d / KT : 0;
     a.kt = KT;
@@ -1029,7 +1033,7 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     a.u_end = a.u_DOWN + a.ndt * a.S + NPF;
     {  // the claim order for this unit geometry, uploaded once per ctx (graph-capture safe after)
         const int lag = env_int("SG_TC_LAG", C->G);
-        std::vector<int> key = {a.nblk, a.ndt, a.S, a.dense, NX, KT, lag, NPF};  // (NX = 0: X^T prepared)
+        std::vector<int> key = {a.nblk, a.ndt, a.S, a.dense, NX, KT, lag, NPF, a.rchunk};  // (NX = 0: X^T prepared)
         auto oit = C->tc_orders.find(key);
         if (oit == C->tc_orders.end()) {
             const std::vector<int> order = tc_schedule(a, NX, KT, lag, NPF);

@@ -171,6 +171,7 @@ struct TcArgs {
     int nblk;              // neuron blocks
     int kst, kt;           // K of a T unit, K slices of T (T units: kt per 128-row half of rank)
     int ndt, S;            // d tiles of 128 outputs, block ranges of the down GEMM (S <= 4)
+    int rchunk;            // consecutive blocks per interleave step of the ranges
     int dense;             // 1: dense comparator (no predictor; every row)
     int tile_u;            // per-1024 survivor density at which DOWN tiles a block, not gathers
     int u_T, u_GU, u_DOWN, u_end;  // unit counts by type (prefix sums: X, T, GU, DOWN; PF last)
