@@ -318,7 +318,16 @@ def run_batch(args, cfg, host, layers, ctx, world, rank, local):
                                            C.c_void_p(res) if res else None, B,
                                            C.c_void_p(Y[l].data_ptr()), dense, nxt, nxs, C.c_void_p(sh)))
 
+    arr = (C.c_void_p * L)(*[ly.handle.value for ly in layers])
+
     def step(sh, dense=0):
+        if B == 1:
+            # one token: the persistent single-token executor over the whole stack in one
+            # launch (the headline path), dense comparator = its dense pipeline
+            check(lib.sg_ffn_forward_layers(ctx.handle, arr, L, 0 if dense else 2,
+                                            C.c_void_p(X.data_ptr()), C.c_void_p(Y.data_ptr()), chain,
+                                            C.c_void_p(sh)))
+            return
         for l in range(L):
             call(l, sh, dense)
 
@@ -398,7 +407,8 @@ def run_batch(args, cfg, host, layers, ctx, world, rank, local):
             cpu = {"value": None, "error": str(e)[:200]}
     conf = bench_config(cfg, args, L, world)
     conf.update({"l2": "no flush: each step streams the union rows of %d distinct layers" % L,
-                 "path": "B = 1: persistent single-token executor; B >= 2: one tcgen05 launch per layer"})
+                 "path": "B = 1: persistent single-token executor, one launch for the stack; "
+                         "B >= 2: one tcgen05 launch per layer"})
     line = {
         "metric": "sparse-FFN decode tokens/s", "value": B * 1000.0 / ms, "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -419,7 +429,7 @@ def run_batch(args, cfg, host, layers, ctx, world, rank, local):
                   "kernel": "tc_kernel dense mode (sg_ffn_forward_batch_dense)"},
         "e2e": {"value": B * 1000.0 / ms_e2e, "unit": "tokens/s", "h2d_bytes_per_step": L * B * d * 4,
                 "d2h_bytes_per_step": L * B * d * 4, "ms_per_step": ms_e2e},
-        "gpu_launches": args.steps * L,
+        "gpu_launches": args.steps * (1 if B == 1 else L),
         "clocks": clocks,
         "cpu_baseline": cpu,
     }
@@ -529,9 +539,10 @@ def main():
     # configs[0] is ONE layer (~70 MB touched < 126 MB L2): the step rotates over 4
     # device copies of it so every step streams its bytes from HBM
     copies = 4 if L == 1 else 1
-    # batched decode: neurons by decreasing calibration activity (the batch's survivor
-    # rows concentrate in the leading blocks; trailing blocks skip their down rows)
-    balance = False if args.no_balance else ("sorted" if args.batch > 0 else True)
+    # batched decode (B >= 2): neurons by decreasing calibration activity (the batch's
+    # survivor rows concentrate in the leading blocks; trailing blocks skip their down
+    # rows); one token keeps the single-token executor's per-CTA balanced layout
+    balance = False if args.no_balance else ("sorted" if args.batch > 1 else True)
     layers = [upload(h, d, D, cfg["act"], args.rank, device=local, shard_index=rank,
                      shard_count=world, balance=balance,
                      hot_rows=args.hot_rows) for h in host for _ in range(copies)]

@@ -1184,6 +1184,31 @@ sg_status sg_ffn_forward_batch_res(sg_ctx* C, const sg_layer* L, const float* xs
         return dense ? sg_ffn_forward_batch_dense(C, L, xs, batch, ys, stream)
                      : sg_ffn_forward_batch(C, L, xs, batch, ys, stream);
     if (sg_status s = check_pair(C, L); s != SG_OK) return s;
+    if (batch == 1 && !dense && L->has_pred && L->has_w) {
+        // one token: the persistent single-token executor with the residual formed while
+        // x is staged (the tensor-core launch would stream every gate / up row for it)
+        if (xs == nullptr || ys == nullptr) return fail(SG_ERR_USAGE, "null buffers");
+        if (sg_status s = batch_workspace(C); s != SG_OK) return s;
+        C->tc_prep.valid = false;
+        DeviceGuard dg(C->device);
+        auto st = static_cast<cudaStream_t>(stream);
+        const size_t bits = static_cast<size_t>(L->D_local) * sizeof(uint64_t);
+        SG_CUDA(cudaMemsetAsync(C->bw.mbits, 0, bits, st));
+        SG_CUDA(cudaMemsetAsync(C->bw.vbits, 0, bits, st));
+        SG_CUDA(cudaMemsetAsync(C->W.stats, 0, 4 * sizeof(int), st));
+        sg::WorkView W = work_for(C, xs, ys);
+        W.xres = xres;
+        W.mbits = reinterpret_cast<unsigned long long*>(C->bw.mbits);
+        W.vbits = reinterpret_cast<unsigned long long*>(C->bw.vbits);
+        W.bitpos = 0;
+        const int e = sg::launch_layer(L->view, W, SG_PIPELINE_SEQUENTIAL, C->G, stream);
+        if (e != 0) return fail(SG_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
+        C->blast = L;
+        C->blast_B = 1;
+        C->blast_stack = true;
+        C->blast_path = 0;
+        return SG_OK;
+    }
     if (!L->has_w || !L->has_tcmaps || (!dense && !L->has_pred) || L->r > 256 || L->d > 8192)
         return fail(SG_ERR_USAGE, "residual batched decode runs on the tensor-core path only");
     if (batch < 1 || batch > 64) return fail(SG_ERR_USAGE, "batch must be in [1, 64]");

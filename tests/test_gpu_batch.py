@@ -130,8 +130,8 @@ def test_batch_device_entry_flags_nonfinite():
             check(capi.lib().sg_ctx_read_batch(ctx.handle, C.c_void_p(sh), B, None, None, None))
 
 
-@pytest.mark.parametrize("dense", [0, 1])
-def test_batch_residual_input_equals_summed_input(dense):
+@pytest.mark.parametrize("dense,B", [(0, 12), (1, 12), (0, 1)])
+def test_batch_residual_input_equals_summed_input(dense, B):
     """sg_ffn_forward_batch_res (x_b = h_b + r_b formed inside the launch, the residual
     chain of the batched bench) gives exactly the result of the same call on the
     fp32 sums."""
@@ -142,7 +142,7 @@ def test_batch_residual_input_equals_summed_input(dense):
     from paper_2603_14110_b200 import _capi as capi
     from paper_2603_14110_b200.ffn_exec import Context, check
 
-    d, D, r, B = 512, 2048, 64, 12
+    d, D, r = 512, 2048, 64
     fx, pred = _calibrated_layer(d, D, r, seed=5, calib=1024)
     layer = DeviceLayer(fx.weights, pred)
     rng = np.random.default_rng(3)
