@@ -381,6 +381,7 @@ struct StageInfo {
 };
 struct TcSmem {
     uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], uqf[kUQ], uqe[kUQ];
+    uint64_t bbar[kUQ];  // a queued GU unit's predictor bias landed in bias[slot]
     StageInfo sinfo[kStages];
     Unit uq[kUQ];
     uint32_t tmem;
@@ -392,6 +393,7 @@ struct TcSmem {
     int wsum[8];         // epilogue: per-quarter counts
     int last;            // epilogue: this unit was the last of its group (it reduces)
     alignas(16) uint16_t zst[2][16][kBlk];  // epilogue: hi / lo of 16 tokens x 128 rows, staged
+    alignas(16) float bias[kUQ][kBlk];      // a queued GU unit's predictor bias (bulk-copied at claim)
 };
 
 // ---- producer: claim, wait, load ---------------------------------------------
@@ -521,6 +523,16 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
         if (pt == 0) {
             const int slot = seq % kUQ;
             S.uq[slot] = un;
+            if (type == U_GU && !a.dense) {
+                // the block's predictor bias, for the epilogue, long before it is needed
+                const uint32_t bytes = static_cast<uint32_t>((un.cnt * 4 + 15) / 16 * 16);
+                mbar_expect_tx(&S.bbar[slot], bytes);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        su32(&S.bias[slot][0])),
+                    "l"(a.bias + static_cast<size_t>(i) * a.brows), "r"(bytes), "r"(su32(&S.bbar[slot]))
+                    : "memory");
+            }
             mbar_arrive(&S.uqf[slot]);
         }
         ++seq;
@@ -836,7 +848,7 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int quarter = warp & 3;              // TMEM lane quarter of this warp
     int seq = 0;
-    uint32_t tphase = 0;
+    uint32_t tphase = 0, bphase = 0;  // tfull[] / bbar[] phases
     const uint64_t bmask = a.B >= 64 ? ~0ull : ((1ull << a.B) - 1ull);
     const int nb = a.nb;
     auto wait_acc = [&](int b) {
@@ -851,9 +863,6 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
         if (un.type == U_STOP) break;
         const int i = un.a, j = un.b;
         const bool mma_unit = un.type == U_T || un.type == U_GU || un.type == U_DOWN;
-        // (GU: the row's predictor bias, loaded while the MMAs run)
-        const int grow = un.a * a.brows + quarter * 32 + lane;
-        const float gbias = (un.type == U_GU && !a.dense && quarter * 32 + lane < un.cnt) ? __ldg(a.bias + grow) : 0.f;
         if (mma_unit) {
             wait_acc(un.acc);
             tc_fence_after();
@@ -986,7 +995,12 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
             const int cnt = un.cnt, k = row0;
             const bool mine = k < cnt;
             const int n = i * a.brows + k;
-            const float bias = gbias;
+            float bias = 0.f;
+            if (!a.dense) {  // (bulk-copied to smem when the unit was queued)
+                mbar_wait(&S.bbar[slot], (bphase >> slot) & 1u);
+                bphase ^= 1u << slot;
+                if (mine) bias = S.bias[slot][k];
+            }
             const uint32_t tl = S.tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc_base(a, acc);
             float z[64];
             uint64_t mb = 0, sbits = 0;
@@ -1189,6 +1203,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
         for (int s = 0; s < kUQ; ++s) {
             mbar_init(&S.uqf[s], 1);
             mbar_init(&S.uqe[s], 2);
+            mbar_init(&S.bbar[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
