@@ -204,3 +204,23 @@ def test_batch_prepared_next_input_equals_plain_chain(chain):
     Ya, Yb = run(False), run(True)
     for l in range(L):
         assert torch.equal(Ya[l], Yb[l]), l
+
+
+@pytest.mark.parametrize("tile_u", [2000, 300])
+def test_batch_gathered_down_rows(tile_u, monkeypatch):
+    """The down stage's row-gather path (survivor rows of a block gathered by cp.async
+    instead of the block tiled; the default tiles every block with a survivor):
+    SG_TC_TILE_U above 1024 gathers every block, 300 mixes gathered and tiled blocks
+    inside one range (runs broken by gathered blocks)."""
+    monkeypatch.setenv("SG_TC_TILE_U", str(tile_u))
+    d, D, r = 512, 2048, 64
+    fx, pred = _calibrated_layer(d, D, r, seed=11, calib=1024)
+    q = quantize_layer(fx.weights.gate, fx.weights.up, fx.weights.down, pred.A, pred.B, pred.bias)
+    layer = DeviceLayer(fx.weights, pred)
+    rng = np.random.default_rng(tile_u)
+    for B in (3, 16, 40):
+        X = fx.eval[:, rng.integers(0, fx.eval.shape[1], B)].T + 0.1 * rng.standard_normal((B, d))
+        Y, stats, P, V = layer.forward_batch(X)
+        for b in range(B):
+            diag = check_token(q, X[b], Y[b], P[b], V[b])
+            assert diag["rel"] <= Y_RTOL
