@@ -993,10 +993,22 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     a.y = ys;
     a.bias = L->view.bias;
     a.ud = L->view.ud;
-    // ranges interleave chunks of 8 blocks (SG_TC_RCHUNK; 0 = contiguous ranges)
-    a.rchunk = env_int("SG_TC_RCHUNK", 8);
+    // ranges interleave chunks of ~8 blocks, the chunk count a multiple of S so every
+    // range holds as many chunks (138 blocks: 16 chunks of 9, not 5/4/4/4 chunks of 8);
+    // SG_TC_RCHUNK forces a chunk size (0 = contiguous ranges)
     a.S = std::max(1, std::min({env_int("SG_TC_S", 4), kTcSMax, a.nblk}));
-    if (a.rchunk <= 0) a.rchunk = (a.nblk + a.S - 1) / a.S;
+    a.rchunk = env_int("SG_TC_RCHUNK", -1);
+    if (a.rchunk < 0) {
+        a.rchunk = 8;
+        for (int k = std::max(1, (a.nblk + 4 * a.S) / (8 * a.S)); k >= 1; --k) {
+            const int c = (a.nblk + a.S * k - 1) / (a.S * k);
+            if ((a.nblk + c - 1) / c == a.S * k) {
+                a.rchunk = c;
+                break;
+            }
+        }
+    }
+    if (a.rchunk == 0) a.rchunk = (a.nblk + a.S - 1) / a.S;
     a.S = std::max(1, std::min(a.S, (a.nblk + a.rchunk - 1) / a.rchunk));  // each range: >= 1 chunk
     const int KT = dense ? 0 : k_slices(a.pitch_d, kTcKTMax);
     a.kst = KT ? a.pitch_d / KT : 0;
