@@ -357,6 +357,27 @@ class DeviceLayer:
         V = [np.sort(gidx[((vb >> np.uint64(b)) & np.uint64(1)).astype(bool)]) for b in range(B)]
         return Y.astype(np.float64), [ExecStats.from_c(s) for s in st], P, V
 
+    def forward_batch_residual(self, H, R, ctx: Optional[Context] = None, dense: bool = False):
+        """Batched decode of a residual stream (sg_ffn_forward_batch_res): token b's input is
+        H[b] + R[b] (e.g. h_{l+1} + y_l), summed in fp32 inside the launch. H, R: torch CUDA
+        fp32 (B, hidden) tensors on this layer's device. Returns (Y torch tensor (B, hidden),
+        per-token ExecStats)."""
+        import torch
+        ctx = ctx or self.context()
+        if H.shape != R.shape or H.dim() != 2 or H.shape[1] != self.hidden:
+            raise DataError("batch input must be (B, hidden) and match the residual")
+        H = H.contiguous().float()
+        R = R.contiguous().float()
+        Y = torch.zeros_like(H)
+        B = H.shape[0]
+        sh = torch.cuda.current_stream(self.device).cuda_stream
+        check(capi.lib().sg_ffn_forward_batch_res(ctx.handle, self.handle, C.c_void_p(H.data_ptr()),
+                                                  C.c_void_p(R.data_ptr()), B, C.c_void_p(Y.data_ptr()),
+                                                  1 if dense else 0, None, None, C.c_void_p(sh)))
+        st = (capi.sg_exec_stats * B)()
+        check(capi.lib().sg_ctx_read_batch(ctx.handle, C.c_void_p(sh), B, st, None, None))
+        return Y, [ExecStats.from_c(x) for x in st]
+
     def forward_batch_dense(self, X, ctx: Optional[Context] = None) -> np.ndarray:
         """Dense batched comparator (sg_ffn_forward_batch_dense): dense_ffn for every token
         of X (B, hidden), every row read once on the tensor cores. Returns Y (B, hidden)."""

@@ -224,3 +224,19 @@ def test_batch_gathered_down_rows(tile_u, monkeypatch):
         for b in range(B):
             diag = check_token(q, X[b], Y[b], P[b], V[b])
             assert diag["rel"] <= Y_RTOL
+
+
+def test_forward_batch_residual_python_api():
+    """DeviceLayer.forward_batch_residual (Python mirror of sg_ffn_forward_batch_res)
+    equals forward_batch on the fp32 sums, stats included."""
+    import torch
+    d, D, r, B = 512, 2048, 64, 6
+    fx, pred = _calibrated_layer(d, D, r, seed=6, calib=1024)
+    layer = DeviceLayer(fx.weights, pred)
+    rng = np.random.default_rng(9)
+    H = torch.tensor(fx.eval[:, :B].T.copy(), dtype=torch.float32, device="cuda")
+    R = torch.tensor(0.1 * rng.standard_normal((B, d)), dtype=torch.float32, device="cuda")
+    Y, st = layer.forward_batch_residual(H, R)
+    Y2, st2, _, _ = layer.forward_batch((H + R).cpu().numpy())
+    assert np.array_equal(Y.double().cpu().numpy(), Y2)
+    assert [(s.predicted_active, s.revalidated) for s in st] == [(s.predicted_active, s.revalidated) for s in st2]
