@@ -47,6 +47,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdlib>
 
 namespace sg {
@@ -57,10 +58,9 @@ constexpr int kMmaWarp = 3;       // warp 3: MMA issuer; warps 4-7: epilogue
 constexpr int kEpiBase = 128;
 constexpr int kTcThreads = 256;
 constexpr int kLag = 3;           // stages a producer thread keeps in flight before arriving
-constexpr int kStages = 4;
+constexpr int kStagesMax = 6;     // smem ring depth at most (a.nstages: as many as fit)
 constexpr int kStageA = 32768;    // two M = 128 A tiles of 64 K (bf16)
-constexpr int kStageB = 16384;    // <= 128 rows (N) x 64 K bf16
-constexpr int kStageBytes = kStageA + kStageB;
+constexpr int kStageB = 16384;    // <= 128 rows (N) x 64 K bf16 (B area: a.stage_bytes - kStageA)
 constexpr int kUQ = 4;            // unit queue depth (producer lead)
 constexpr int kBlk = 128;         // neurons per block at most (one M = 128 tile)
 constexpr int kTRows = 256;       // predictor rows (rank <= 256: two M = 128 tiles)
@@ -380,9 +380,9 @@ struct StageInfo {
     int last;    // the unit's final (empty) stage
 };
 struct TcSmem {
-    uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], uqf[kUQ], uqe[kUQ];
+    uint64_t full[kStagesMax], empty[kStagesMax], tfull[2], tempty[2], uqf[kUQ], uqe[kUQ];
     uint64_t bbar[kUQ];  // a queued GU unit's predictor bias landed in bias[slot]
-    StageInfo sinfo[kStages];
+    StageInfo sinfo[kStagesMax];
     Unit uq[kUQ];
     uint32_t tmem;
     int rows[kBlk];      // producer: gather rows of the current block (global neuron index)
@@ -395,6 +395,7 @@ struct TcSmem {
     alignas(16) uint16_t zst[2][16][kBlk];  // epilogue: hi / lo of 16 tokens x 128 rows, staged
     alignas(16) float bias[kUQ][kBlk];      // a queued GU unit's predictor bias (bulk-copied at claim)
 };
+constexpr int kTcSmemPad = (static_cast<int>(sizeof(TcSmem)) + 1023) / 1024 * 1024;
 
 // ---- producer: claim, wait, load ---------------------------------------------
 // 96 threads (warps 0-2). Thread 0 is the controller: it claims units, checks and
@@ -432,16 +433,23 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
     int seq = 0, accseq = 0;
     int n = 0;         // stages issued by this thread (all producer threads agree)
     int pending = 0;   // of which not yet arrived
+    int spos = 0;      // n % a.nstages (the ring slot of stage n)
+    const int nst = a.nstages;
+    auto back = [&](int k) { return spos - k < 0 ? spos - k + nst : spos - k; };  // slot of stage n - k
+    auto advance = [&] {
+        ++n;
+        spos = spos + 1 == nst ? 0 : spos + 1;
+    };
     uint32_t ephase = 0;  // bit s: parity of empty[s] to wait for
     auto flush = [&] {
         cp_wait<0>();
-        for (; pending > 0; --pending) stage_arrive(&S.full[(n - pending) % kStages]);
+        for (; pending > 0; --pending) stage_arrive(&S.full[back(pending)]);
     };
 #ifdef SG_TC_FINTRACE
     unsigned long long ewait = 0;  // ns the controller spent waiting for free stages (this unit)
 #endif
     auto begin_stage = [&](uint8_t*& As, uint32_t& as, uint64_t*& bar) {
-        const int s = n % kStages;
+        const int s = spos;
 #ifdef SG_TC_FINTRACE
         const unsigned long long t0 = gtimer();
         mbar_wait(&S.empty[s], (ephase >> s) & 1u);
@@ -450,23 +458,23 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
         mbar_wait(&S.empty[s], (ephase >> s) & 1u);
 #endif
         ephase ^= 1u << s;
-        As = stages + s * kStageBytes;
-        as = sbase + s * kStageBytes;
+        As = stages + s * a.stage_bytes;
+        as = sbase + s * a.stage_bytes;
         bar = &S.full[s];
     };
     auto end_gather_stage = [&] {
         cp_commit();
-        ++n;
+        advance();
         if (++pending > kLag) {
             cp_wait<kLag>();
-            stage_arrive(&S.full[(n - pending) % kStages]);
+            stage_arrive(&S.full[back(pending)]);
             --pending;
         }
     };
     auto end_tile_stage = [&](uint64_t* bar) {  // (no copies of this warp: arrive now)
         __syncwarp();
         if ((pt & 31) == 0) mbar_arrive(bar);
-        ++n;
+        advance();
     };
     // a cross-CTA wait inside a unit: release this thread's held-back stages first
     auto wait_flag = [&](const int* p, int target) {
@@ -637,7 +645,7 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                     const int full = ds.rows / 64, nbox = (ds.rows % 64 + 15) / 16, nz = ds.kd / 64;
                     begin_stage(As, as, bar);
                     if (pt == 0) {
-                        S.sinfo[(n) % kStages] = StageInfo{(ds.rows + 15) / 16, ds.kd, 0};
+                        S.sinfo[spos] = StageInfo{(ds.rows + 15) / 16, ds.kd, 0};
                         mbar_expect_tx(bar, static_cast<uint32_t>(full * 8192 + nbox * 2048) * 2u + nz * bbytes);
                         for (int atom = 0; atom < 2; ++atom) {
                             uint8_t* dst = As + atom * ds.kd * 128;
@@ -664,7 +672,7 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                 const int nz = ds.kd / 64, r16 = (ds.rows + 15) / 16 * 16;
                 begin_stage(As, as, bar);
                 if (pt == 0) {
-                    S.sinfo[n % kStages] = StageInfo{r16 / 16, ds.kd, 0};
+                    S.sinfo[spos] = StageInfo{r16 / 16, ds.kd, 0};
                     mbar_expect_tx(bar, nz * bbytes);
                     for (int z = 0; z < nz; ++z)
                         tma_tile_ef(As + kStageA + z * a.N * 128, &M.zhl, ds.gblk * a.brows + ds.c0 + z * 64, 0, bar,
@@ -688,7 +696,7 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
             flush();
             begin_stage(As, as, bar);
             if (pt == 0) {
-                S.sinfo[n % kStages] = StageInfo{0, 64, 1};
+                S.sinfo[spos] = StageInfo{0, 64, 1};
                 mbar_arrive(bar);  // (the expect_tx arrival, with no bytes)
             }
             end_tile_stage(bar);
@@ -721,7 +729,7 @@ __device__ void mma_issuer(const TcArgs& a, TcSmem& S, uint8_t* stages) {
         fphase ^= 1u << stage;
         tc_fence_after();
         if (lane == 0) {
-            const uint32_t As = su32(stages + stage * kStageBytes), Bs = As + kStageA;
+            const uint32_t As = su32(stages + stage * a.stage_bytes), Bs = As + kStageA;
             for (int t = 0; t < nsub; ++t)
                 for (int k = 0; k < ksteps; ++k) {
                     // MN-major SW128: atoms of 64 outputs x 64 k-rows (8 KB); K-major SW128:
@@ -734,7 +742,7 @@ __device__ void mma_issuer(const TcArgs& a, TcSmem& S, uint8_t* stages) {
             umma_commit(&S.empty[stage]);
         }
         __syncwarp();
-        stage = (stage + 1) % kStages;
+        stage = stage + 1 == a.nstages ? 0 : stage + 1;
     };
     for (;;) {
         const int slot = seq % kUQ;
@@ -764,7 +772,7 @@ __device__ void mma_issuer(const TcArgs& a, TcSmem& S, uint8_t* stages) {
                         fphase ^= 1u << stage;
                         if (lane == 0) mbar_arrive(&S.empty[stage]);
                         __syncwarp();
-                        stage = (stage + 1) % kStages;
+                        stage = stage + 1 == a.nstages ? 0 : stage + 1;
                         break;
                     }
                     run_stage(1, si.ksteps, true, dcol, idesc(a.N, 1), st == 0, si.kd);
@@ -1188,11 +1196,13 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
 
 __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant__ TcMaps maps, const TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    TcSmem& S = *reinterpret_cast<TcSmem*>(stages + kStages * kStageBytes);
+    // [TcSmem | ring of a.nstages x a.stage_bytes], the ring 1024-B aligned (SW128 atoms)
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    TcSmem& S = *reinterpret_cast<TcSmem*>(base);
+    uint8_t* stages = base + kTcSmemPad;
     const int warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < a.nstages; ++s) {
             mbar_init(&S.full[s], kFullArrivals);
             mbar_init(&S.empty[s], 1);
         }
@@ -1222,7 +1232,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     tc_fence_after();
     // the producer waits on empty[] before every stage: pre-arrive the first round
     if (threadIdx.x == 0)
-        for (int s = 0; s < kStages; ++s) mbar_arrive(&S.empty[s]);
+        for (int s = 0; s < a.nstages; ++s) mbar_arrive(&S.empty[s]);
     // (programmatic dependent launch: everything above overlapped the previous launch's
     // tail; from here on the previous launch's outputs and counters are read)
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1266,11 +1276,28 @@ int tc_block_rows(int64_t D, int sms) {
     return static_cast<int>(per > kBlk ? kBlk : per);
 }
 
-int tc_smem_bytes() { return kStages * kStageBytes + static_cast<int>(sizeof(TcSmem)) + 1024; }
+int tc_smem_bytes(int nstages, int stage_bytes) { return 1024 + kTcSmemPad + nstages * stage_bytes; }
+
+// the smem ring for MMA N: stages of the two A tiles + the larger B operand of a stage
+// (the GU / T token tile of N rows x 64 K, or a down stage's Z tile of kd = 128 slots x N
+// when N <= 64), as many as the opt-in shared memory holds (SG_TC_STAGES caps it)
+void tc_ring(TcArgs& a) {
+    const int bneed = (a.N <= 64 ? 2 : 1) * a.N * 128;
+    a.stage_bytes = kStageA + (bneed + 1023) / 1024 * 1024;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const char* cap = std::getenv("SG_TC_STAGES");
+    int ns = (optin - 1024 - kTcSmemPad) / a.stage_bytes;
+    ns = std::min({ns, kStagesMax, cap ? std::atoi(cap) : kStagesMax});
+    a.nstages = std::max(kLag + 1, ns);  // (a producer thread holds kLag stages back)
+}
 int tc_flag_ints(int nblk, int ndt) { return 32 + nblk + ndt; }
 
-int launch_batch_tc(const TcMaps& maps, const TcArgs& a, int grid, void* stream) {
-    const int smem = tc_smem_bytes();
+int launch_batch_tc(const TcMaps& maps, const TcArgs& a_in, int grid, void* stream) {
+    TcArgs a = a_in;
+    tc_ring(a);
+    const int smem = tc_smem_bytes(a.nstages, a.stage_bytes);
     const int e = ensure_smem_attr(reinterpret_cast<const void*>(tc_kernel), smem);
     if (e) return e;
     // programmatic dependent launch (SG_TC_PDL=0 disables): the next launch on the

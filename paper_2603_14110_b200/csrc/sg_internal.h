@@ -174,6 +174,7 @@ struct TcArgs {
     int rchunk;            // consecutive blocks per interleave step of the ranges
     int dense;             // 1: dense comparator (no predictor; every row)
     int tile_u;            // per-1024 survivor density at which DOWN tiles a block, not gathers
+    int nstages, stage_bytes;  // smem ring: stages x bytes (set by launch_batch_tc from N)
     int u_T, u_GU, u_DOWN, u_end;  // unit counts by type (prefix sums: X, T, GU, DOWN; PF last)
     const uint16_t* pf_gate;  // optional: the next layer's gate rows [pf_D][pf_pitch] to prefetch
     const uint16_t* pf_ud;    //   and its [up | down] rows (up halves prefetched)
@@ -207,7 +208,7 @@ struct TcArgs {
     int x_ready;           // 1: X^T was prepared by the previous launch (no X units)
     int* flags;            // dataflow counters, reset by the last CTA of every launch
 };
-int tc_smem_bytes();
+int tc_smem_bytes(int nstages, int stage_bytes);
 int tc_flag_ints(int nblk, int ndt);
 int launch_batch_tc(const TcMaps& maps, const TcArgs& a, int grid, void* stream);
 
