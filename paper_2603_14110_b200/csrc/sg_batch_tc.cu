@@ -571,11 +571,9 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
             const int k0 = i * a.kst;
             for (int st = 0; st < un.nst; ++st) {
                 begin_stage(As, as, bar);
-                if (pt == 0) {
-                    mbar_expect_tx(bar, un.nsub * 16384u + bbytes);
-                    tma_tile_ef(As, &M.Bp, k0 + st * 64, j * 128, bar, pol);
-                    tma_tile_ef(As + kStageA, &M.xhl, k0 + st * 64, 0, bar, pol_last);
-                }
+                if (pt == 0) mbar_expect_tx(bar, un.nsub * 16384u + bbytes);
+                if (pt == 0) tma_tile_ef(As, &M.Bp, k0 + st * 64, j * 128, bar, pol);
+                else if (pt == 1) tma_tile_ef(As + kStageA, &M.xhl, k0 + st * 64, 0, bar, pol_last);
                 end_tile_stage(bar);
             }
         } else if (type == U_GU) {
@@ -585,11 +583,12 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
             const int r0 = i * a.brows;
             for (int st = 0; st < a.pitch_d / 64; ++st) {
                 begin_stage(As, as, bar);
-                if (pt == 0) {
-                    mbar_expect_tx(bar, 2u * abytes + bbytes);
-                    tma_tile_ef(As, &M.gate, st * 64, r0, bar, pol);
-                    tma_tile_ef(As + 16384, &M.up, st * 64, r0, bar, pol);
-                    tma_tile_ef(As + kStageA, &M.xhl, st * 64, 0, bar, pol_last);
+                // (the three copies issued by three lanes of warp 0 side by side)
+                if (pt == 0) mbar_expect_tx(bar, 2u * abytes + bbytes);
+                if (pt < 3) {
+                    if (pt == 0) tma_tile_ef(As, &M.gate, st * 64, r0, bar, pol);
+                    else if (pt == 1) tma_tile_ef(As + 16384, &M.up, st * 64, r0, bar, pol);
+                    else tma_tile_ef(As + kStageA, &M.xhl, st * 64, 0, bar, pol_last);
                 }
                 end_tile_stage(bar);
             }
@@ -597,11 +596,9 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                 wait_flag(fl_tr(a), t_halves(a));
                 for (int st = 0; st < a.pitch_r / 64; ++st) {
                     begin_stage(As, as, bar);
-                    if (pt == 0) {
-                        mbar_expect_tx(bar, abytes + bbytes);
-                        tma_tile_ef(As, &M.A, st * 64, r0, bar, pol);
-                        tma_tile_ef(As + kStageA, &M.thl, st * 64, 0, bar, pol_last);
-                    }
+                    if (pt == 0) mbar_expect_tx(bar, abytes + bbytes);
+                    if (pt == 0) tma_tile_ef(As, &M.A, st * 64, r0, bar, pol);
+                    else if (pt == 1) tma_tile_ef(As + kStageA, &M.thl, st * 64, 0, bar, pol_last);
                     end_tile_stage(bar);
                 }
             }
@@ -647,16 +644,21 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                     if (pt == 0) {
                         S.sinfo[spos] = StageInfo{(ds.rows + 15) / 16, ds.kd, 0};
                         mbar_expect_tx(bar, static_cast<uint32_t>(full * 8192 + nbox * 2048) * 2u + nz * bbytes);
-                        for (int atom = 0; atom < 2; ++atom) {
-                            uint8_t* dst = As + atom * ds.kd * 128;
-                            for (int f = 0; f < full; ++f)
-                                tma_tile_ef(dst + f * 8192, &M.down64, m0 + atom * 64, ds.row0 + f * 64, bar, pol);
-                            for (int q = 0; q < nbox; ++q)
-                                tma_tile_ef(dst + full * 8192 + q * 2048, &M.down, m0 + atom * 64,
-                                            ds.row0 + full * 64 + q * 16, bar, pol);
-                        }
-                        for (int z = 0; z < nz; ++z)
-                            tma_tile_ef(As + kStageA + z * a.N * 128, &M.zhl, ds.row0 + z * 64, 0, bar, pol_last);
+                    }
+                    // one copy per lane of warp 0: lane q < 2 * per issues A box q % per of
+                    // atom q / per, the next nz lanes the Z boxes
+                    const int per = full + nbox;
+                    if (pt < 2 * per) {
+                        const int atom = pt >= per, q = pt - atom * per;
+                        uint8_t* dst = As + atom * ds.kd * 128;
+                        if (q < full)
+                            tma_tile_ef(dst + q * 8192, &M.down64, m0 + atom * 64, ds.row0 + q * 64, bar, pol);
+                        else
+                            tma_tile_ef(dst + full * 8192 + (q - full) * 2048, &M.down, m0 + atom * 64,
+                                        ds.row0 + full * 64 + (q - full) * 16, bar, pol);
+                    } else if (pt < 2 * per + nz) {
+                        const int z = pt - 2 * per;
+                        tma_tile_ef(As + kStageA + z * a.N * 128, &M.zhl, ds.row0 + z * 64, 0, bar, pol_last);
                     }
                     end_tile_stage(bar);
                     continue;
