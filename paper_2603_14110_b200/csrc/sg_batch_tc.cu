@@ -646,12 +646,16 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                         mbar_expect_tx(bar, static_cast<uint32_t>(full * 8192 + nbox * 2048) * 2u + nz * bbytes);
                     }
                     // one copy per lane of warp 0: lane q < 2 * per issues A box q % per of
-                    // atom q / per, the next nz lanes the Z boxes
-                    const int per = full + nbox;
+                    // atom q / per (a full 128-row stage: one box per atom), the next nz
+                    // lanes the Z boxes
+                    const bool b128 = full == 2 && nbox == 0;
+                    const int per = b128 ? 1 : full + nbox;
                     if (pt < 2 * per) {
                         const int atom = pt >= per, q = pt - atom * per;
                         uint8_t* dst = As + atom * ds.kd * 128;
-                        if (q < full)
+                        if (b128)
+                            tma_tile_ef(dst, &M.down128, m0 + atom * 64, ds.row0, bar, pol);
+                        else if (q < full)
                             tma_tile_ef(dst + q * 8192, &M.down64, m0 + atom * 64, ds.row0 + q * 64, bar, pol);
                         else
                             tma_tile_ef(dst + full * 8192 + (q - full) * 2048, &M.down, m0 + atom * 64,
@@ -1221,7 +1225,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     }
     if (threadIdx.x == 32) {  // warm the TMA descriptor cache with every map this CTA may use
         const CUtensorMap* ms[] = {&maps.xhl, &maps.thl, &maps.zhl, &maps.Bp, &maps.A,
-                                   &maps.gate, &maps.up, &maps.down, &maps.down64};
+                                   &maps.gate, &maps.up, &maps.down, &maps.down64, &maps.down128};
         for (const CUtensorMap* m : ms)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
     }

@@ -629,7 +629,8 @@ sg_status sg_layer_create(const sg_layer_desc* desc, sg_layer** out) {
         L->tc_brows = br;
         bool ok = make_map(&tm.gate, V.gate, pd, Dl, pd, br) && make_map(&tm.up, V.ud, pd, Dl, 2 * pd, br) &&
                   make_map(&tm.down, V.ud + pd, pd, Dl, 2 * pd, 16) &&
-                  make_map(&tm.down64, V.ud + pd, pd, Dl, 2 * pd, 64);
+                  make_map(&tm.down64, V.ud + pd, pd, Dl, 2 * pd, 64) &&
+                  make_map(&tm.down128, V.ud + pd, pd, Dl, 2 * pd, 128);
         if (ok && has_pred)
             ok = make_map(&tm.A, V.A, pr, Dl, pr, br) && make_map(&tm.Bp, V.B, pd, r, pd, 128);
         L->has_tcmaps = ok;

@@ -159,6 +159,7 @@ struct TcMaps {            // TMA tensor maps (bf16, SWIZZLE_128B, 64-element in
     CUtensorMap up;        // up rows     [D][pitch_d], row stride 2*pitch_d (ud, first half)   box {64, brows}
     CUtensorMap down;      // down rows   [D][pitch_d], row stride 2*pitch_d (ud + pitch_d)     box {64, 16}
     CUtensorMap down64;    // the same rows                                                     box {64, 64}
+    CUtensorMap down128;   // the same rows                                                     box {64, 128}
 };
 // Rows per neuron block of the tensor-core path for a layer of D (local) rows on a
 // device with `sms` SMs: about one block per SM beside the predictor's units, so the
