@@ -15,3 +15,9 @@ for B in 2 4 8 16 32 48 64; do
   timeout 600 python bench.py --batch $B --layers 32 --steps 50 --warmup 5 > gpurun_out/batch_r02_B$B.json 2> gpurun_out/batch_r02_B$B.err
   python -c "import json; d=json.loads(open('gpurun_out/batch_r02_B$B.json').read().strip().splitlines()[-1]); print('B=$B', 'tok/s %.0f us/layer %.1f frac %.3f | dense us/layer %.1f | sparse/dense %.2f | e2e %.0f' % (d['value'], d['per_layer_us'], d['roofline']['frac'], d['dense']['per_layer_us'], d['dense']['sparse_speedup'], d['e2e']['value']))" || tail -3 gpurun_out/batch_r02_B$B.err
 done
+for c in 13b mistral; do
+  for B in 8 32; do
+    timeout 600 python bench.py --config $c --batch $B --steps 30 --warmup 5 > gpurun_out/batch_r02_${c}_$B.json 2> gpurun_out/batch_r02_${c}_$B.err
+    python -c "import json; d=json.loads(open('gpurun_out/batch_r02_${c}_$B.json').read().strip().splitlines()[-1]); print('$c B=$B', 'us/layer %.1f | dense %.1f | sparse/dense %.2f' % (d['per_layer_us'], d['dense']['per_layer_us'], d['dense']['sparse_speedup']))" || tail -3 gpurun_out/batch_r02_${c}_$B.err
+  done
+done
