@@ -141,11 +141,19 @@ __device__ __forceinline__ uint32_t idesc(int N, int a_mn) {
     return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
            (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
 }
-__device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+// D (+)= A B, issued by the whole (converged) warp: one elected lane executes it and
+// the operands stay warp-uniform (no per-lane operand broadcast loop around the MMA)
+__device__ __forceinline__ void umma_warp(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
         "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(su32(bar))
+        : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -734,7 +742,7 @@ __device__ void mma_issuer(const TcArgs& a, TcSmem& S, uint8_t* stages) {
         mbar_wait(&S.full[stage], (fphase >> stage) & 1u);
         fphase ^= 1u << stage;
         tc_fence_after();
-        if (lane == 0) {
+        {
             const uint32_t As = su32(stages + stage * a.stage_bytes), Bs = As + kStageA;
             for (int t = 0; t < nsub; ++t)
                 for (int k = 0; k < ksteps; ++k) {
@@ -743,9 +751,9 @@ __device__ void mma_issuer(const TcArgs& a, TcSmem& S, uint8_t* stages) {
                     const uint64_t ad = mn ? sdesc(As + t * 16384 + k * 2048, kd * 128, 1024)
                                            : sdesc(As + t * 16384 + k * 32, 16, 1024);
                     const uint32_t bk = Bs + (k >> 2) * a.N * 128 + (k & 3) * 32;
-                    umma(dcol + t * a.N, ad, sdesc(bk, 16, 1024), id, (first && k == 0) ? 0u : 1u);
+                    umma_warp(dcol + t * a.N, ad, sdesc(bk, 16, 1024), id, (first && k == 0) ? 0u : 1u);
                 }
-            umma_commit(&S.empty[stage]);
+            umma_commit_warp(&S.empty[stage]);
         }
         __syncwarp();
         stage = stage + 1 == a.nstages ? 0 : stage + 1;
