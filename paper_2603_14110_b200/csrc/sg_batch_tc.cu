@@ -306,6 +306,7 @@ struct DownWalk {
     int run0, run1;   // tiled rows not yet staged
     int pend, pv;     // a block that does not extend the run, its vcnt
     int gblk, g0, g1; // the gathered block being staged: survivor positions [g0, g1)
+    int cb, cp;       // block k = range_block(j, k), incrementally: chunk base, position in it
 };
 struct DownStage {
     int tiled;  // 1: rows [row0, row0 + rows); 0: block gblk's survivors [c0, c0 + rows)
@@ -322,7 +323,9 @@ __device__ __forceinline__ uint32_t acc_base(const TcArgs& a, int acc) {
 }
 // tiled down stages take 128 K rows when the Z tile of 128 slots fits the B area
 __device__ __forceinline__ int down_kd(const TcArgs& a) { return a.N <= 64 ? 128 : 64; }
-__device__ __forceinline__ DownWalk down_walk(int j) { return DownWalk{j, 0, 0, 0, 0, -1, 0, 0, 0, 0}; }
+__device__ __forceinline__ DownWalk down_walk(const TcArgs& a, int j) {
+    return DownWalk{j, 0, 0, 0, 0, -1, 0, 0, 0, 0, j * a.rchunk, 0};
+}
 template <class Wait>
 __device__ __forceinline__ bool down_next(const TcArgs& a, DownWalk& w, DownStage& st, Wait&& wait) {
     for (;;) {
@@ -350,10 +353,14 @@ __device__ __forceinline__ bool down_next(const TcArgs& a, DownWalk& w, DownStag
             continue;
         }
         if (w.done) return false;
-        const int blk = range_block(a, w.j, w.k);
+        const int blk = w.cb + w.cp;  // range_block(a, w.j, w.k)
         if (blk >= a.nblk) {
             w.done = 1;
             continue;
+        }
+        if (++w.cp == a.rchunk) {
+            w.cp = 0;
+            w.cb += a.S * a.rchunk;
         }
         const int v = wait(w.k++, blk);  // the block's vcnt once it is complete
         if (vcnt_tiled(v) && w.run1 > w.run0 && w.run1 == blk * a.brows) {
@@ -612,10 +619,13 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
             }
         } else {  // U_DOWN: K = Z slots of the block range, A = down rows (MN-major)
             const int m0 = i * 128;
-            DownWalk w = down_walk(j);
+            DownWalk w = down_walk(a, j);
             DownStage ds;
             // the range's completion flags and counts, one round of loads for all blocks;
             // a block found incomplete is waited for, then the rest are read again
+#ifdef SG_TC_FINTRACE
+            unsigned long long nfetch = 0, fetch_ns = 0;
+#endif
             auto fetch = [&] {
                 prod_bar();
                 const int blk = range_block(a, j, pt);
@@ -629,8 +639,15 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                     return __ldcg(a.vcnt + blk);
                 }
                 if (S.dvc[k] < 0) {
+#ifdef SG_TC_FINTRACE
+                    const unsigned long long f0 = gtimer();
+#endif
                     wait_flag(fl_gu(a, blk), 1);
                     fetch();
+#ifdef SG_TC_FINTRACE
+                    ++nfetch;
+                    fetch_ns += gtimer() - f0;
+#endif
                 }
                 return S.dvc[k];
             };
@@ -638,7 +655,17 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
 #ifdef SG_TC_FINTRACE
             int nstg = 0;
 #endif
+#ifdef SG_TC_FINTRACE
+            unsigned long long walk_ns = 0;
+            auto next = [&] {
+                const unsigned long long w0 = gtimer();
+                const bool r = down_next(a, w, ds, wait_blk);
+                walk_ns += gtimer() - w0;
+                return r;
+            };
+#else
             auto next = [&] { return down_next(a, w, ds, wait_blk); };
+#endif
             while (next()) {
 #ifdef SG_TC_FINTRACE
                 if (pt == 0 && nstg++ == 0) TC_TRACE(a, un.u, 6, gtimer());
@@ -651,14 +678,15 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                     begin_stage(As, as, bar);
                     if (pt == 0) {
                         S.sinfo[spos] = StageInfo{(ds.rows + 15) / 16, ds.kd, 0};
-                        mbar_expect_tx(bar, static_cast<uint32_t>(full * 8192 + nbox * 2048) * 2u + nz * bbytes);
+                        mbar_expect_tx(bar, (a.dbg & 1 ? 0u : static_cast<uint32_t>(full * 8192 + nbox * 2048) * 2u) +
+                                                (a.dbg & 2 ? 0u : nz * bbytes));
                     }
                     // one copy per lane of warp 0: lane q < 2 * per issues A box q % per of
                     // atom q / per (a full 128-row stage: one box per atom), the next nz
                     // lanes the Z boxes
                     const bool b128 = full == 2 && nbox == 0;
                     const int per = b128 ? 1 : full + nbox;
-                    if (pt < 2 * per) {
+                    if (pt < 2 * per && !(a.dbg & 1)) {
                         const int atom = pt >= per, q = pt - atom * per;
                         uint8_t* dst = As + atom * ds.kd * 128;
                         if (b128)
@@ -668,7 +696,7 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                         else
                             tma_tile_ef(dst + full * 8192 + (q - full) * 2048, &M.down, m0 + atom * 64,
                                         ds.row0 + full * 64 + (q - full) * 16, bar, pol);
-                    } else if (pt < 2 * per + nz) {
+                    } else if (pt >= 2 * per && pt < 2 * per + nz && !(a.dbg & 2)) {
                         const int z = pt - 2 * per;
                         tma_tile_ef(As + kStageA + z * a.N * 128, &M.zhl, ds.row0 + z * 64, 0, bar, pol_last);
                     }
@@ -706,6 +734,10 @@ __device__ void producer(const TcArgs& a, const TcMaps& M, TcSmem& S, uint8_t* s
                 }
                 end_gather_stage();
             }
+#ifdef SG_TC_FINTRACE
+            if (pt == 0) TC_TRACE(a, un.u, 5, (static_cast<unsigned long long>(nstg) << 40) | (nfetch << 32) | fetch_ns);
+            if (pt == 0) TC_TRACE(a, un.u, 7, walk_ns);
+#endif
             // the terminating stage (no data) tells the MMA issuer the unit is complete
             flush();
             begin_stage(As, as, bar);
@@ -789,7 +821,7 @@ __device__ void mma_issuer(const TcArgs& a, TcSmem& S, uint8_t* stages) {
                         stage = stage + 1 == a.nstages ? 0 : stage + 1;
                         break;
                     }
-                    run_stage(1, si.ksteps, true, dcol, idesc(a.N, 1), st == 0, si.kd);
+                    run_stage(1, a.dbg & 4 ? 0 : si.ksteps, true, dcol, idesc(a.N, 1), st == 0, si.kd);
                 }
             }
             if (lane == 0) {
@@ -1138,8 +1170,6 @@ __device__ void epilogue(const TcArgs& a, TcSmem& S) {
             release();
 #ifndef SG_TC_FINTRACE
             if (et == 0) TC_TRACE(a, un.u, 6, gtimer());
-#else
-            if (et == 0) TC_TRACE(a, un.u, 7, gtimer());
 #endif
             if (arrive_last(fl_down(a, i), a.S, S, et)) {
                 // y rows of d tile i: the S range partials in range order, 2 chunks of 8

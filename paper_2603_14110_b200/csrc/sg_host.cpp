@@ -989,6 +989,7 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     // B200 even a block with a sixth of its rows surviving streams faster whole), so by
     // default every block with a survivor is tiled and only empty blocks are skipped
     a.tile_u = env_int("SG_TC_TILE_U", 1);
+    a.dbg = env_int("SG_TC_DBG", 0);
     a.x = xs;
     a.xres = xres;
     a.y = ys;

@@ -175,6 +175,7 @@ struct TcArgs {
     int rchunk;            // consecutive blocks per interleave step of the ranges
     int dense;             // 1: dense comparator (no predictor; every row)
     int tile_u;            // per-1024 survivor density at which DOWN tiles a block, not gathers
+    int dbg;               // experiment switches (SG_TC_DBG; 1: down stages skip their weight copies)
     int nstages, stage_bytes;  // smem ring: stages x bytes (set by launch_batch_tc from N)
     int u_T, u_GU, u_DOWN, u_end;  // unit counts by type (prefix sums: X, T, GU, DOWN; PF last)
     const uint16_t* pf_gate;  // optional: the next layer's gate rows [pf_D][pf_pitch] to prefetch

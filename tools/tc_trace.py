@@ -27,7 +27,12 @@ def main():
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--dense", action="store_true")
     ap.add_argument("--sms", type=int, default=0, help="also print the unit timeline of this many SMs")
+    ap.add_argument("--fin", action="store_true",
+                    help="load the SG_TC_FINTRACE build: per DOWN unit, inputs ready -> first stage -> "
+                         "loads done, and the time the producer waited for free ring stages")
     args = ap.parse_args()
+    if args.fin:
+        os.environ["SG_LIB"] = "fintrace"
     import torch
 
     from paper_2603_14110_b200 import _capi as capi
@@ -79,6 +84,19 @@ def main():
         print(f"{name:6s} {sel.sum():5d} {r[:, 0].min():8.1f} {r[:, 0].max():8.1f} {r[:, 4].min():8.1f} "
               f"{r[:, 4].max():8.1f} {wait.mean():7.2f} {np.nanmean(load):7.2f} {np.nanmean(mma):7.2f} "
               f"{epi.mean():7.2f} {ep:7.2f} {ea:7.2f} {ef:7.2f}")
+    if args.fin:
+        sel = order == 4
+        r = tr[sel]
+        ready, first, ewait = (r[:, 1] - t0) / 1e3, (r[:, 6] - t0) / 1e3, r[:, 2] / 1e3
+        done = (r[:, 3] - t0) / 1e3
+        print(f"DOWN (fintrace): ready {ready.mean():.1f} first stage {first.mean():.1f} "
+              f"(+{(first - ready).mean():.2f}) accumulator done {done.mean():.1f} "
+              f"(first stage -> done {(done - first).mean():.2f} us, of which waiting for free stages "
+              f"{ewait.mean():.2f})")
+        nstg, nf, fns = r[:, 5] >> 40, (r[:, 5] >> 32) & 0xff, (r[:, 5] & 0xffffffff) / 1e3
+        print(f"  stages per unit {nstg.mean():.1f} (max {nstg.max()}), block-flag refetches {nf.mean():.1f}, "
+              f"time in them {fns.mean():.2f} us; in the block walker {r[:, 7].mean() / 1e3:.2f} us")
+        return
     sms = tr[:, 5]
     busy = np.zeros(int(sms.max()) + 1)
     for k in range(n.value):
