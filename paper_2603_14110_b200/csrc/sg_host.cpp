@@ -995,11 +995,11 @@ sg_status tc_forward(sg_ctx* C, const sg_layer* L, const float* xs, int B, float
     a.y = ys;
     a.bias = L->view.bias;
     a.ud = L->view.ud;
-    // ranges interleave chunks of ~8 blocks, the chunk count a multiple of S so every
-    // range holds as many chunks (138 blocks: 16 chunks of 9, not 5/4/4/4 chunks of 8);
-    // SG_TC_RCHUNK forces a chunk size (0 = contiguous ranges)
+    // default: S contiguous block ranges (longest runs of tiled blocks, fewest walker
+    // steps); SG_TC_RCHUNK = c > 0 interleaves chunks of c blocks, -1 picks ~8-block
+    // chunks with the chunk count a multiple of S (138 blocks: 16 chunks of 9)
     a.S = std::max(1, std::min({env_int("SG_TC_S", 4), kTcSMax, a.nblk}));
-    a.rchunk = env_int("SG_TC_RCHUNK", -1);
+    a.rchunk = env_int("SG_TC_RCHUNK", 0);  // default: contiguous ranges (measured best once the walk was cheap)
     if (a.rchunk < 0) {
         a.rchunk = 8;
         for (int k = std::max(1, (a.nblk + 4 * a.S) / (8 * a.S)); k >= 1; --k) {
